@@ -1,0 +1,227 @@
+/*
+ * ckf.h -- the C-ABI boundary of the B200 CheckFree / CheckFree+ engine.
+ *
+ * Plain C: opaque handles, plain pointers and sizes, int status codes; no
+ * C++ or torch types cross this line.  Host C++ (the drop-in `ckfree::` API
+ * under include/ckfree/, and the reference itself via INTEGRATION.md) calls
+ * CUDA only through these entry points.  Each group cites the reference
+ * interface it replaces (paths relative to /root/reference/proj).
+ *
+ * Error convention: every entry point returns CKF_OK (0) or a CKF_E_* code
+ * mirroring the reference's exception types (include/ckfree/errors.hpp:10-45);
+ * the message is in ckf_last_error() (thread-local).  Nothing here throws.
+ */
+#ifndef CKF_H_
+#define CKF_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------ status codes */
+enum ckf_status {
+  CKF_OK = 0,
+  CKF_E_CONFIG = 1,               /* ConfigError                (errors.hpp:10-13) */
+  CKF_E_DIVERGENCE = 2,           /* NumericDivergenceError     (errors.hpp:15-26) */
+  CKF_E_USAGE = 3,                /* UsageError                 (errors.hpp:28-32) */
+  CKF_E_PARSE = 4,                /* ParseError                 (errors.hpp:34-38) */
+  CKF_E_UNSUPPORTED_RECOVERY = 5, /* UnsupportedRecoveryError   (errors.hpp:40-45) */
+  CKF_E_CUDA = 6,
+  CKF_E_NCCL = 7
+};
+
+const char* ckf_last_error(void);
+/* iteration carried by the last CKF_E_DIVERGENCE, -1 outside a training loop */
+long ckf_last_error_iteration(void);
+int ckf_version(void);
+int ckf_device_count(int* out);
+
+/* enumerations shared with the reference */
+enum ckf_activation { CKF_ACT_TANH = 0, CKF_ACT_RELU = 1, CKF_ACT_IDENTITY = 2 }; /* kernels.hpp:19 */
+enum ckf_task { CKF_TASK_REGRESSION = 0, CKF_TASK_CLASSIFICATION = 1 };           /* model.hpp:16 */
+enum ckf_dtype { CKF_FP64 = 0, CKF_FP32 = 1, CKF_BF16 = 2 };
+
+/* =====================================================================
+ * (0) Host control logic (no GPU needed), bit-exact with the reference:
+ *     failure traces (src/failures.cpp:57-196), even partition
+ *     (src/model.cpp:63-73) and microbatch schedules (src/pipeline.cpp:11-56).
+ * ===================================================================== */
+/* generate_trace + serialize_trace ("checkfree-trace v1") into out */
+int ckf_generate_trace(uint64_t seed, double p_hour, double iter_s, long n_iters, const int* stages, int n_stages,
+                       char* out, size_t cap);
+/* parse_trace (ParseError on malformed input) then canonical re-serialization */
+int ckf_parse_trace(const char* text, char* out, size_t cap);
+/* consecutive_conflicts: writes (iteration, stage) pairs, *n_out pairs */
+int ckf_consecutive_conflicts(const char* text, long* out, int cap_pairs, int* n_out);
+double ckf_hourly_to_per_iteration(double p_hour, double iter_s);
+/* layers -> stages: writes 2*stages (first,last) 1-based */
+int ckf_even_partition(size_t layers, size_t stages, size_t* out);
+/* m execution orders of length s (standard, or swapped at even positions) */
+int ckf_build_schedule(int m, int swapped_half, int s, int* out);
+
+/* =====================================================================
+ * (1) L1 kernel seam.  Replaces the dispatching wrappers of
+ *     ckfree::kernels (include/ckfree/kernels.hpp:26-69,
+ *     src/kernels_dispatch.cpp:37-83) as a third Backend: identical
+ *     signatures (HOST fp64 pointers), computed on the current CUDA device
+ *     in fp64.  Staging through a device arena is internal.
+ * ===================================================================== */
+int ckf_k_gemm_nn(const double* a, const double* b, double* c, size_t m, size_t k, size_t n);
+int ckf_k_gemm_nn_acc(const double* a, const double* b, double* c, size_t m, size_t k, size_t n);
+int ckf_k_gemm_nt_acc(const double* a, const double* b, double* c, size_t m, size_t k, size_t n);
+int ckf_k_gemm_tn_acc(const double* a, const double* b, double* c, size_t m, size_t k, size_t n);
+int ckf_k_add_inplace(double* x, const double* y, size_t n);
+int ckf_k_axpy(double alpha, const double* x, double* y, size_t n);
+int ckf_k_scale(double alpha, double* x, size_t n);
+int ckf_k_apply_activation(int act, const double* a, double* z, size_t n);
+int ckf_k_activation_backward(int act, const double* z, const double* dz, double* da, size_t n);
+int ckf_k_sum_squares(const double* x, size_t n, double* out);
+int ckf_k_sum_squared_diff(const double* x, const double* y, size_t n, double* out);
+int ckf_k_adam_update(double* w, double* m, double* v, const double* g, size_t n, double lr, double beta1,
+                      double beta2, double eps, long step);
+int ckf_k_mse_loss_grad(const double* pred, const double* target, size_t rows, size_t cols, double* dpred,
+                        double* loss);
+int ckf_k_softmax_xent_loss_grad(const double* logits, const int* labels, size_t rows, size_t cols,
+                                 double* dlogits, double* loss);
+/* recovery::recover_checkfree on flat host vectors (src/recovery.cpp:57-73) */
+int ckf_k_recover_checkfree(const double* w_prev, const double* w_next, size_t n, double omega_prev,
+                            double omega_next, double* out, int* degenerate);
+/* n draws of CounterRng(key).uniform(lo, hi), counters 1..n (include/ckfree/rng.hpp:37-44), bit-exact */
+int ckf_k_counter_uniform(uint64_t key, double lo, double hi, double* out, size_t n);
+
+/* =====================================================================
+ * (2) Device-pointer primitives (the hot kernels on their own, for
+ *     benchmarks and for callers that keep state in HBM).  `stream` is a
+ *     cudaStream_t (NULL = legacy default stream).
+ * ===================================================================== */
+/* out = (op*wp + on*wn)/(op+on) (recovery.cpp:57-73) in one streaming pass.
+ * dtype CKF_FP64 is bit-exact with the reference (no FMA contraction); CKF_FP32
+ * computes the coefficients in fp64 and one FMA per element.  wp/wn may be peer
+ * (NVLink) pointers.  If old_out_sq is non-NULL the pass also reduces
+ * ||out_before - out_after||^2 (reduction_error, recovery.cpp:120-126) into it
+ * (device double*, deterministic order).  op+on == 0 -> uniform (degenerate). */
+int ckf_recover_device(int dtype, const void* wp, const void* wn, void* out, size_t n, double op, double on,
+                       double* old_out_sq, void* stream);
+/* fused Adam (kernels_serial.cpp:133-144) + omega = sum(g^2) (model.cpp:396):
+ * g_eff = g_sum * grad_scale; w,m,v updated in place; if w_bf16 != NULL the bf16
+ * shadow is rewritten; if zero_grad the accumulator is cleared for the next
+ * iteration; omega (device double*) receives sum(g_eff^2).  bc1/bc2 are the
+ * host-computed 1-beta^step (pow on the host). */
+int ckf_adam_device(int dtype, void* w, void* m, void* v, void* g, void* w_bf16, size_t n, double lr,
+                    double bc1, double bc2, double grad_scale, int zero_grad, double* omega, void* stream);
+
+/* =====================================================================
+ * (3) Device-resident engine: the throughput tier behind
+ *     ckfree::pipeline::run_iteration (pipeline.hpp:44-47),
+ *     ckfree::recovery (recovery.hpp:46-86) and harness::Trainer
+ *     (src/trainer.cpp:63-289).
+ * ===================================================================== */
+typedef struct ckf_engine_s* ckf_engine_t;
+
+enum ckf_block { CKF_BLOCK_MLP = 0, CKF_BLOCK_LLAMA = 1 };
+
+typedef struct {
+  int block;      /* ckf_block: residual MLP x + act(xW1)W2 (model.hpp:55-60) or LLaMA */
+  int precision;  /* ckf_dtype of the arithmetic: FP64 / FP32 (parity) or BF16 (tcgen05) */
+  int activation; /* MLP only */
+  int task;       /* MLP only; LLaMA is next-token cross-entropy */
+  size_t input_dim, hidden_dim, model_dim, output_dim; /* model.hpp:33-36; LLaMA: hidden = ffn width,
+                                                          input = output = vocab */
+  size_t num_layers, num_stages;
+  size_t n_heads;                 /* LLaMA only (head_dim = model_dim / n_heads) */
+  size_t seq_len;                 /* LLaMA only */
+  const size_t* partition;        /* 2*num_stages 1-based (first,last); NULL = even_partition */
+  size_t max_rows;                /* rows (MLP) or tokens (LLaMA) per microbatch */
+  int device;                     /* CUDA ordinal */
+} ckf_model_desc;
+
+int ckf_engine_create(const ckf_model_desc* desc, ckf_engine_t* out);
+int ckf_engine_destroy(ckf_engine_t e);
+/* parameters of one stage (canonical flat layout, model.cpp:117-125) / of an edge (0 embed, 1 de-embed) */
+int ckf_engine_param_counts(ckf_engine_t e, size_t* stage_params, size_t* embed_params, size_t* deembed_params);
+
+/* init_model(spec, seed, lr) (model.cpp:174-197): counter-RNG Glorot streams, bit-exact in fp64 */
+int ckf_engine_init(ckf_engine_t e, uint64_t seed, double lr);
+
+/* multi-GPU placement: stage_rank[s-1] = rank owning stage s; the embedding is
+ * co-located with stage 1, the de-embedding with stage s (cost_model.cpp:264-268).
+ * uid is a ckf_nccl_unique_id blob shared by all ranks (e.g. via torch.distributed). */
+int ckf_nccl_unique_id(void* uid_out, size_t cap);
+int ckf_engine_attach_comm(ckf_engine_t e, const void* uid, int nranks, int rank, const int* stage_rank);
+
+/* One training iteration (pipeline.cpp:58-95).  orders: m*s stage ids, one
+ * execution order per microbatch (ExecutionOrder, pipeline.hpp:12-24).
+ * MLP: x = rows x input_dim, y = rows x output_dim (regression) or rows labels (as
+ *      double, classification), fp64.
+ * LLaMA: x = rows x (seq_len+1) int32 token ids (inputs are [:, :T], labels [:, 1:]).
+ * on_device: 1 if x/y are device pointers.  loss: mean loss; omegas: s values
+ * (only owned stages are meaningful under multi-GPU). */
+int ckf_engine_run_iteration(ckf_engine_t e, const int* orders, int m, const void* x, const void* y,
+                             size_t rows, int on_device, long iteration, double* loss, double* omegas);
+/* loss of forward(model, order, x) against y (model.cpp:279-282,380-382), no update */
+int ckf_engine_eval_loss(ckf_engine_t e, const int* order, const void* x, const void* y, size_t rows,
+                         int on_device, double* loss);
+/* predictions of forward(model, order, x) into host fp64 (MLP only) */
+int ckf_engine_predict(ckf_engine_t e, const int* order, const double* x, size_t rows, double* pred);
+
+/* CheckFree+ edge replicas (recovery.cpp:80-88): copy E, E^-1 to the neighbours' buffers */
+int ckf_engine_refresh_edge_replicas(ckf_engine_t e);
+/* whole-stage loss: NaN-poisons the stage's weights and moments on its GPU */
+int ckf_engine_kill_stage(ckf_engine_t e, int stage);
+
+enum ckf_recovery_mode {
+  CKF_REC_CHECKFREE = 0, /* omega-weighted neighbour average (recovery.cpp:57-73) */
+  CKF_REC_UNIFORM = 1,   /* reinit_uniform_avg (recovery.cpp:105-110) */
+  CKF_REC_COPY_PREV = 2, /* reinit_copy (recovery.cpp:103) */
+  CKF_REC_RANDOM = 3,    /* reinit_random (recovery.cpp:112-118) */
+  CKF_REC_EDGE = 4       /* CheckFree+ first/last stage: neighbour copy + replica (recovery.cpp:90-101) */
+};
+enum ckf_moments { CKF_MOM_FRESH = 0, CKF_MOM_AVERAGED = 1 }; /* recovery.hpp:31 */
+
+typedef struct {
+  int degenerate;          /* both neighbour omegas were zero -> uniform average */
+  double reduction_error;  /* ||W_before - W_after||^2 (trainer.cpp:278-279), if requested */
+  double latency_ms;       /* CUDA-event time from issue to the stage being ready */
+} ckf_recovery_report;
+
+/* Rebuilds `stage` per the trainer's semantics (trainer.cpp:199-276): weights,
+ * moments (Fresh reset / Averaged), lr *= lr_bump, omega := 0, and for
+ * CKF_REC_EDGE the edge layer from the fresh replica with its Adam state reset.
+ * Neighbour weights are read peer-to-peer when they live on another GPU. */
+int ckf_engine_recover_stage(ckf_engine_t e, int stage, int mode, int moments, double lr_bump,
+                             uint64_t reinit_seed, int want_reduction_error, ckf_recovery_report* out);
+
+/* state exchange in the canonical fp64 flat layout (model.cpp:117-157) */
+int ckf_engine_export_stage(ckf_engine_t e, int stage, double* w, double* m, double* v);
+int ckf_engine_import_stage(ckf_engine_t e, int stage, const double* w, const double* m, const double* v);
+int ckf_engine_export_edge(ckf_engine_t e, int which, double* w, double* m, double* v);
+int ckf_engine_import_edge(ckf_engine_t e, int which, const double* w, const double* m, const double* v);
+int ckf_engine_get_scalars(ckf_engine_t e, int stage, double* omega, double* lr, long* step);
+int ckf_engine_set_scalars(ckf_engine_t e, int stage, double omega, double lr, long step);
+int ckf_engine_get_edge_scalars(ckf_engine_t e, double* lr, long* step_embed, long* step_deembed);
+int ckf_engine_set_edge_scalars(ckf_engine_t e, double lr, long step_embed, long step_deembed);
+
+/* launches of the engine's own kernels since creation (evidence for gpu_launches) */
+long ckf_engine_kernel_launches(ckf_engine_t e);
+/* synchronises the engine's streams */
+int ckf_engine_sync(ckf_engine_t e);
+
+/* =====================================================================
+ * (4) Trainer: harness::run_experiment (src/trainer.cpp:314-322) on the
+ *     engine.  kv_config: "key=value;..." with the keys of
+ *     ExperimentConfig::to_config_string (src/experiment.cpp:117-154) plus
+ *     block/precision/heads/seq-len/vocab for LLaMA.  trace_text: a
+ *     "checkfree-trace v1" file (failures.cpp:84-95); empty = generate from
+ *     the config (experiment.cpp:102-115).  record: E/F/U lines
+ *     ("E,iter,train,val", "F,iter,stage,action,reduction_error,loss_spike,recovery_ms",
+ *     "U,reason").
+ * ===================================================================== */
+int ckf_run_experiment(const char* kv_config, const char* trace_text, uint64_t seed, char* record, size_t cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CKF_H_ */

@@ -1,0 +1,296 @@
+"""Python face of the B200 engine, mirroring the reference's operator names
+(ckfree::pipeline / ckfree::recovery / harness, /root/reference/proj/include).
+
+Thin: all arithmetic runs in libckf.so's sm_100a kernels via include/ckf.h.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from ._native import check, lib
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _ip(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_int))
+
+
+# ------------------------------------------------------------- host logic (no GPU)
+def generate_trace(seed: int, p_hour: float, iter_s: float, n_iters: int, stages) -> str:
+    """failures::generate_trace + serialize_trace (src/failures.cpp:63-95)."""
+    arr = (C.c_int * len(stages))(*stages)
+    buf = C.create_string_buffer(1 << 22)
+    check(lib().ckf_generate_trace(seed, p_hour, iter_s, n_iters, arr, len(stages), buf, len(buf)))
+    return buf.value.decode()
+
+
+def parse_trace(text: str) -> str:
+    buf = C.create_string_buffer(max(1 << 16, 4 * len(text)))
+    check(lib().ckf_parse_trace(text.encode(), buf, len(buf)))
+    return buf.value.decode()
+
+
+def consecutive_conflicts(text: str):
+    out = (C.c_long * 20000)()
+    n = C.c_int(0)
+    check(lib().ckf_consecutive_conflicts(text.encode(), out, 10000, C.byref(n)))
+    return [(out[2 * i], out[2 * i + 1]) for i in range(n.value)]
+
+
+def hourly_to_per_iteration(p_hour: float, iter_s: float) -> float:
+    return lib().ckf_hourly_to_per_iteration(p_hour, iter_s)
+
+
+def even_partition(layers: int, stages: int):
+    out = (C.c_size_t * (2 * stages))()
+    check(lib().ckf_even_partition(layers, stages, out))
+    return [(out[2 * i], out[2 * i + 1]) for i in range(stages)]
+
+
+def build_schedule(m: int, swapped_half: bool, s: int):
+    out = (C.c_int * (max(m, 1) * s))()
+    check(lib().ckf_build_schedule(m, 1 if swapped_half else 0, s, out))
+    return [[out[k * s + j] for j in range(s)] for k in range(m)]
+
+
+# ------------------------------------------------------------- L1 seam (kernels.hpp)
+def recover_checkfree(w_prev, w_next, omega_prev: float, omega_next: float):
+    """recovery::recover_checkfree (src/recovery.cpp:57-73) on the GPU, fp64."""
+    wp = np.ascontiguousarray(w_prev, np.float64)
+    wn = np.ascontiguousarray(w_next, np.float64)
+    if wp.shape != wn.shape:
+        raise N.ConfigError(N.CKF_E_CONFIG, "neighbor stage weights differ in shape")
+    out = np.empty_like(wp)
+    deg = C.c_int(0)
+    check(lib().ckf_k_recover_checkfree(_dp(wp), _dp(wn), wp.size, omega_prev, omega_next, _dp(out), C.byref(deg)))
+    return out, bool(deg.value)
+
+
+def counter_uniform(key: int, lo: float, hi: float, n: int) -> np.ndarray:
+    out = np.empty(n, np.float64)
+    check(lib().ckf_k_counter_uniform(key, lo, hi, _dp(out), n))
+    return out
+
+
+def adam_update(w, m, v, g, lr, step):
+    w, m, v = (np.array(a, np.float64) for a in (w, m, v))
+    g = np.ascontiguousarray(g, np.float64)
+    check(lib().ckf_k_adam_update(_dp(w), _dp(m), _dp(v), _dp(g), w.size, lr, 0.9, 0.999, 1e-8, step))
+    return w, m, v
+
+
+def sum_squares(x) -> float:
+    x = np.ascontiguousarray(x, np.float64)
+    out = C.c_double(0)
+    check(lib().ckf_k_sum_squares(_dp(x), x.size, C.byref(out)))
+    return out.value
+
+
+def gemm(kind: str, a, b, c, m, k, n):
+    a = np.ascontiguousarray(a, np.float64)
+    b = np.ascontiguousarray(b, np.float64)
+    c = np.array(c, np.float64)
+    fn = {"nn": lib().ckf_k_gemm_nn, "nn_acc": lib().ckf_k_gemm_nn_acc, "nt_acc": lib().ckf_k_gemm_nt_acc,
+          "tn_acc": lib().ckf_k_gemm_tn_acc}[kind]
+    check(fn(_dp(a), _dp(b), _dp(c), m, k, n))
+    return c
+
+
+# ------------------------------------------------------------- device primitives
+def recover_device(wp, wn, out, omega_prev, omega_next, old_sq=None, stream=0):
+    """omega-weighted recovery on torch CUDA tensors (fp32 / fp64 master weights)."""
+    import torch
+    dt = {torch.float64: N.CKF_FP64, torch.float32: N.CKF_FP32}[out.dtype]
+    check(lib().ckf_recover_device(dt, wp.data_ptr(), wn.data_ptr(), out.data_ptr(), out.numel(), omega_prev,
+                                   omega_next, old_sq.data_ptr() if old_sq is not None else None, stream or None))
+
+
+def adam_device(w, m, v, g, lr, step, grad_scale=1.0, zero_grad=False, w_bf16=None, omega=None, stream=0):
+    import math
+    import torch
+    dt = {torch.float64: N.CKF_FP64, torch.float32: N.CKF_FP32}[w.dtype]
+    bc1 = 1.0 - math.pow(0.9, step)
+    bc2 = 1.0 - math.pow(0.999, step)
+    check(lib().ckf_adam_device(dt, w.data_ptr(), m.data_ptr(), v.data_ptr(), g.data_ptr(),
+                                w_bf16.data_ptr() if w_bf16 is not None else None, w.numel(), lr, bc1, bc2,
+                                grad_scale, 1 if zero_grad else 0, omega.data_ptr() if omega is not None else None,
+                                stream or None))
+
+
+# ------------------------------------------------------------- engine
+@dataclass
+class ModelSpec:
+    """ModelSpec (model.hpp:32-53) + the LLaMA shape keys."""
+    input_dim: int = 16
+    hidden_dim: int = 64
+    model_dim: int = 32
+    output_dim: int = 16
+    num_layers: int = 8
+    num_stages: int = 4
+    activation: str = "tanh"
+    task: str = "regression"
+    block: str = "mlp"
+    precision: str = "fp64"
+    n_heads: int = 1
+    seq_len: int = 1
+    max_rows: int = 256
+    device: int = 0
+
+    @staticmethod
+    def llama(vocab, d, layers, heads, ffn, seq_len, stages, precision="bf16", max_tokens=8192, device=0):
+        return ModelSpec(vocab, ffn, d, vocab, layers, stages, "identity", "classification", "llama", precision,
+                         heads, seq_len, max_tokens, device)
+
+
+class Engine:
+    """Device-resident stages + edges on one GPU (include/ckf.h section 3)."""
+
+    def __init__(self, spec: ModelSpec):
+        self.spec = spec
+        d = N.ModelDesc()
+        d.block = N.CKF_BLOCK_LLAMA if spec.block == "llama" else N.CKF_BLOCK_MLP
+        d.precision = {"fp64": N.CKF_FP64, "fp32": N.CKF_FP32, "bf16": N.CKF_BF16}[spec.precision]
+        d.activation = N.CKF_ACT[spec.activation]
+        d.task = N.CKF_TASK[spec.task]
+        d.input_dim, d.hidden_dim, d.model_dim, d.output_dim = spec.input_dim, spec.hidden_dim, spec.model_dim, \
+            spec.output_dim
+        d.num_layers, d.num_stages, d.n_heads, d.seq_len = spec.num_layers, spec.num_stages, spec.n_heads, spec.seq_len
+        d.partition = None
+        d.max_rows = spec.max_rows
+        d.device = spec.device
+        self._h = C.c_void_p()
+        check(lib().ckf_engine_create(C.byref(d), C.byref(self._h)))
+        sp, ep, dp = C.c_size_t(), C.c_size_t(), C.c_size_t()
+        check(lib().ckf_engine_param_counts(self._h, C.byref(sp), C.byref(ep), C.byref(dp)))
+        self.stage_params, self.embed_params, self.deembed_params = sp.value, ep.value, dp.value
+
+    def close(self):
+        if self._h:
+            check(lib().ckf_engine_destroy(self._h))
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def init(self, seed: int, lr: float):
+        check(lib().ckf_engine_init(self._h, seed, lr))
+
+    def run_iteration(self, orders, x, y, iteration: int, on_device: bool = False):
+        orders = np.ascontiguousarray(orders, np.int32).reshape(-1)
+        m = orders.size // self.spec.num_stages
+        loss = C.c_double(0)
+        om = np.zeros(self.spec.num_stages, np.float64)
+        xp, yp, rows = self._inputs(x, y, on_device)
+        check(lib().ckf_engine_run_iteration(self._h, _ip(orders), m, xp, yp, rows, 1 if on_device else 0, iteration,
+                                             C.byref(loss), _dp(om)))
+        return loss.value, om
+
+    def _inputs(self, x, y, on_device):
+        if on_device:
+            return x.data_ptr(), (y.data_ptr() if y is not None else None), x.shape[0]
+        if self.spec.block == "llama":
+            self._x = np.ascontiguousarray(x, np.int32)
+            return self._x.ctypes.data, None, self._x.shape[0]
+        self._x = np.ascontiguousarray(x, np.float64)
+        self._y = np.ascontiguousarray(y, np.float64)
+        return self._x.ctypes.data, self._y.ctypes.data, self._x.shape[0]
+
+    def eval_loss(self, order, x, y=None, on_device=False):
+        order = np.ascontiguousarray(order, np.int32)
+        xp, yp, rows = self._inputs(x, y, on_device)
+        out = C.c_double(0)
+        check(lib().ckf_engine_eval_loss(self._h, _ip(order), xp, yp, rows, 1 if on_device else 0, C.byref(out)))
+        return out.value
+
+    def predict(self, order, x):
+        order = np.ascontiguousarray(order, np.int32)
+        x = np.ascontiguousarray(x, np.float64)
+        pred = np.zeros((x.shape[0], self.spec.output_dim), np.float64)
+        check(lib().ckf_engine_predict(self._h, _ip(order), _dp(x), x.shape[0], _dp(pred)))
+        return pred
+
+    def refresh_edge_replicas(self):
+        check(lib().ckf_engine_refresh_edge_replicas(self._h))
+
+    def kill_stage(self, stage: int):
+        check(lib().ckf_engine_kill_stage(self._h, stage))
+
+    def recover_stage(self, stage, mode=N.CKF_REC_CHECKFREE, moments=N.CKF_MOM_FRESH, lr_bump=1.1, reinit_seed=0,
+                      reduction_error=False):
+        r = N.RecoveryReport()
+        check(lib().ckf_engine_recover_stage(self._h, stage, mode, moments, lr_bump, reinit_seed,
+                                             1 if reduction_error else 0, C.byref(r)))
+        return r
+
+    def export_stage(self, stage):
+        w, m, v = (np.zeros(self.stage_params) for _ in range(3))
+        check(lib().ckf_engine_export_stage(self._h, stage, _dp(w), _dp(m), _dp(v)))
+        return w, m, v
+
+    def import_stage(self, stage, w=None, m=None, v=None):
+        arrs = [None if a is None else np.ascontiguousarray(a, np.float64) for a in (w, m, v)]
+        check(lib().ckf_engine_import_stage(self._h, stage, *[None if a is None else _dp(a) for a in arrs]))
+
+    def export_edge(self, which):
+        n = self.embed_params if which == 0 else self.deembed_params
+        w, m, v = (np.zeros(n) for _ in range(3))
+        check(lib().ckf_engine_export_edge(self._h, which, _dp(w), _dp(m), _dp(v)))
+        return w, m, v
+
+    def import_edge(self, which, w=None, m=None, v=None):
+        arrs = [None if a is None else np.ascontiguousarray(a, np.float64) for a in (w, m, v)]
+        check(lib().ckf_engine_import_edge(self._h, which, *[None if a is None else _dp(a) for a in arrs]))
+
+    def scalars(self, stage):
+        om, lr, st = C.c_double(), C.c_double(), C.c_long()
+        check(lib().ckf_engine_get_scalars(self._h, stage, C.byref(om), C.byref(lr), C.byref(st)))
+        return om.value, lr.value, st.value
+
+    def set_scalars(self, stage, omega, lr, step):
+        check(lib().ckf_engine_set_scalars(self._h, stage, omega, lr, step))
+
+    def attach_comm(self, uid: bytes, nranks: int, rank: int, stage_rank):
+        sr = np.ascontiguousarray(stage_rank, np.int32)
+        buf = C.create_string_buffer(uid, 128)
+        check(lib().ckf_engine_attach_comm(self._h, buf, nranks, rank, _ip(sr)))
+
+    def sync(self):
+        check(lib().ckf_engine_sync(self._h))
+
+    def kernel_launches(self) -> int:
+        return lib().ckf_engine_kernel_launches(self._h)
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    check(lib().ckf_nccl_unique_id(buf, 128))
+    return buf.raw
+
+
+# ------------------------------------------------------------- trainer
+def run_experiment(cfg: dict, trace_text: str, seed: int):
+    """harness::run_experiment (src/trainer.cpp:314-322) on the GPU engine.
+    Returns (evals[(iter, train, val)], events[(iter, stage, action, red, spike, ms)], unrecoverable_reason|None)."""
+    kv = ";".join(f"{k}={v}" for k, v in cfg.items()).encode()
+    buf = C.create_string_buffer(1 << 22)
+    check(lib().ckf_run_experiment(kv, trace_text.encode(), seed, buf, len(buf)))
+    evals, events, unrec = [], [], None
+    for ln in buf.value.decode().splitlines():
+        p = ln.split(",")
+        if p[0] == "E":
+            evals.append((int(p[1]), float(p[2]), float(p[3])))
+        elif p[0] == "F":
+            events.append((int(p[1]), int(p[2]), p[3], float(p[4]), float(p[5]), float(p[6])))
+        elif p[0] == "U":
+            unrec = ln[2:]
+    return evals, events, unrec

@@ -1,0 +1,473 @@
+// extern "C" entry points of include/ckf.h.  Nothing throws across this line:
+// every call maps internal errors to CKF_E_* codes + ckf_last_error().
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/ckf.h"
+#include "engine.h"
+#include "host_logic.h"
+
+namespace ckf {
+std::string run_experiment(const std::string& kv, const std::string& trace_text, uint64_t seed);
+int nccl_unique_id(void* out, size_t cap);
+}  // namespace ckf
+
+namespace {
+
+thread_local std::string g_err;
+thread_local long g_err_iter = -1;
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    g_err.clear();
+    g_err_iter = -1;
+    return CKF_OK;
+  } catch (const ckf::Error& e) {
+    g_err = e.what();
+    g_err_iter = e.iteration;
+    return e.code;
+  } catch (const ckf::host::HostError& e) {
+    g_err = e.what();
+    g_err_iter = -1;
+    return e.code;
+  } catch (const std::bad_alloc& e) {
+    g_err = std::string("host allocation failed: ") + e.what();
+    return CKF_E_CUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return CKF_E_CONFIG;
+  }
+}
+
+// ---------------------------------------------------------------- L1 seam context
+// Host-pointer kernels stage through one device arena on a private stream.
+struct Seam {
+  std::mutex mu;
+  cudaStream_t st = nullptr;
+  void* arena = nullptr;
+  size_t cap = 0;
+  ckf::ReduceScratch red;
+  double* scal = nullptr;
+  int device = -1;
+
+  void ensure() {
+    int dev = 0;
+    CKF_CUDA(cudaGetDevice(&dev));
+    if (dev != device) {
+      device = dev;
+      CKF_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+      CKF_CUDA(cudaMalloc(&red.partials, ckf::ReduceScratch::kMaxReduceBlocks * sizeof(double)));
+      CKF_CUDA(cudaMalloc(&scal, 64 * sizeof(double)));
+      arena = nullptr;
+      cap = 0;
+    }
+  }
+  // returns n_bufs device pointers carved from the arena (each 256-B aligned)
+  std::vector<double*> bufs(std::initializer_list<size_t> elems) {
+    size_t total = 0;
+    for (size_t e : elems) total += (e * sizeof(double) + 255) / 256 * 256;
+    if (total > cap) {
+      if (arena) CKF_CUDA(cudaFree(arena));
+      CKF_CUDA(cudaMalloc(&arena, total));
+      cap = total;
+    }
+    std::vector<double*> out;
+    char* p = static_cast<char*>(arena);
+    for (size_t e : elems) {
+      out.push_back(reinterpret_cast<double*>(p));
+      p += (e * sizeof(double) + 255) / 256 * 256;
+    }
+    return out;
+  }
+  void h2d(double* d, const double* h, size_t n) {
+    if (n) CKF_CUDA(cudaMemcpyAsync(d, h, n * sizeof(double), cudaMemcpyHostToDevice, st));
+  }
+  void d2h(double* h, const double* d, size_t n) {
+    if (n) CKF_CUDA(cudaMemcpyAsync(h, d, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  }
+  void sync() { CKF_CUDA(cudaStreamSynchronize(st)); }
+};
+Seam& seam() {
+  static Seam s;
+  return s;
+}
+
+int seam_gemm(bool ta, bool tb, bool acc, const double* a, const double* b, double* c, size_t m, size_t k, size_t n) {
+  return guard([&] {
+    Seam& S = seam();
+    std::lock_guard<std::mutex> lk(S.mu);
+    S.ensure();
+    auto d = S.bufs({m * k, k * n, m * n});
+    S.h2d(d[0], a, m * k);
+    S.h2d(d[1], b, k * n);
+    if (acc) S.h2d(d[2], c, m * n);
+    const size_t lda = ta ? m : k, ldb = tb ? k : n;
+    ckf::k::gemm_simt<double>(ta, tb, m, n, k, d[0], lda, d[1], ldb, d[2], n, acc, S.st);
+    S.d2h(c, d[2], m * n);
+    S.sync();
+  });
+}
+
+ckf::Engine* E(ckf_engine_t e) { return reinterpret_cast<ckf::Engine*>(e); }
+
+}  // namespace
+
+extern "C" {
+
+const char* ckf_last_error(void) { return g_err.c_str(); }
+long ckf_last_error_iteration(void) { return g_err_iter; }
+int ckf_version(void) { return 1; }
+int ckf_device_count(int* out) {
+  return guard([&] { CKF_CUDA(cudaGetDeviceCount(out)); });
+}
+
+// ---------------------------------------------------------------- (0) host logic
+int ckf_generate_trace(uint64_t seed, double p_hour, double iter_s, long n_iters, const int* stages, int n_stages,
+                       char* out, size_t cap) {
+  return guard([&] {
+    auto t = ckf::host::generate_trace(seed, p_hour, iter_s, n_iters, std::vector<int>(stages, stages + n_stages));
+    const std::string s = ckf::host::serialize_trace(t);
+    if (s.size() + 1 > cap) ckf::raise(CKF_E_USAGE, "output buffer too small");
+    std::memcpy(out, s.c_str(), s.size() + 1);
+  });
+}
+int ckf_parse_trace(const char* text, char* out, size_t cap) {
+  return guard([&] {
+    const std::string s = ckf::host::serialize_trace(ckf::host::parse_trace(text ? text : ""));
+    if (s.size() + 1 > cap) ckf::raise(CKF_E_USAGE, "output buffer too small");
+    std::memcpy(out, s.c_str(), s.size() + 1);
+  });
+}
+int ckf_consecutive_conflicts(const char* text, long* out, int cap_pairs, int* n_out) {
+  return guard([&] {
+    auto c = ckf::host::consecutive_conflicts(ckf::host::parse_trace(text ? text : ""));
+    if (static_cast<int>(c.size()) > cap_pairs) ckf::raise(CKF_E_USAGE, "output buffer too small");
+    for (size_t i = 0; i < c.size(); ++i) {
+      out[2 * i] = c[i].iteration;
+      out[2 * i + 1] = c[i].stage;
+    }
+    *n_out = static_cast<int>(c.size());
+  });
+}
+double ckf_hourly_to_per_iteration(double p_hour, double iter_s) {
+  double r = NAN;
+  guard([&] { r = ckf::host::hourly_to_per_iteration(p_hour, iter_s); });
+  return r;
+}
+int ckf_even_partition(size_t layers, size_t stages, size_t* out) {
+  return guard([&] {
+    if (stages < 1 || stages > layers) ckf::raise(CKF_E_CONFIG, "num_stages must lie in [1, num_layers]");
+    auto p = ckf::even_partition(layers, stages);
+    for (size_t i = 0; i < p.size(); ++i) {
+      out[2 * i] = p[i].first;
+      out[2 * i + 1] = p[i].last;
+    }
+  });
+}
+int ckf_build_schedule(int m, int swapped_half, int s, int* out) {
+  return guard([&] {
+    auto o = ckf::host::build_schedule(m, swapped_half != 0, s);
+    std::memcpy(out, o.data(), o.size() * sizeof(int));
+  });
+}
+
+// ---------------------------------------------------------------- (1) L1 seam
+int ckf_k_gemm_nn(const double* a, const double* b, double* c, size_t m, size_t k, size_t n) {
+  return seam_gemm(false, false, false, a, b, c, m, k, n);
+}
+int ckf_k_gemm_nn_acc(const double* a, const double* b, double* c, size_t m, size_t k, size_t n) {
+  return seam_gemm(false, false, true, a, b, c, m, k, n);
+}
+int ckf_k_gemm_nt_acc(const double* a, const double* b, double* c, size_t m, size_t k, size_t n) {
+  return seam_gemm(false, true, true, a, b, c, m, k, n);
+}
+int ckf_k_gemm_tn_acc(const double* a, const double* b, double* c, size_t m, size_t k, size_t n) {
+  return seam_gemm(true, false, true, a, b, c, m, k, n);
+}
+
+#define SEAM_BEGIN            \
+  return guard([&] {          \
+    Seam& S = seam();         \
+    std::lock_guard<std::mutex> lk(S.mu); \
+    S.ensure();
+#define SEAM_END \
+  S.sync();      \
+  });
+
+int ckf_k_add_inplace(double* x, const double* y, size_t n) {
+  SEAM_BEGIN
+  auto d = S.bufs({n, n});
+  S.h2d(d[0], x, n);
+  S.h2d(d[1], y, n);
+  ckf::k::add_inplace(d[0], d[1], n, S.st);
+  S.d2h(x, d[0], n);
+  SEAM_END
+}
+int ckf_k_axpy(double alpha, const double* x, double* y, size_t n) {
+  SEAM_BEGIN
+  auto d = S.bufs({n, n});
+  S.h2d(d[0], x, n);
+  S.h2d(d[1], y, n);
+  ckf::k::axpy(alpha, d[0], d[1], n, S.st);
+  S.d2h(y, d[1], n);
+  SEAM_END
+}
+int ckf_k_scale(double alpha, double* x, size_t n) {
+  SEAM_BEGIN
+  auto d = S.bufs({n});
+  S.h2d(d[0], x, n);
+  ckf::k::scale(alpha, d[0], n, S.st);
+  S.d2h(x, d[0], n);
+  SEAM_END
+}
+int ckf_k_apply_activation(int act, const double* a, double* z, size_t n) {
+  SEAM_BEGIN
+  auto d = S.bufs({n, n});
+  S.h2d(d[0], a, n);
+  ckf::k::act_fwd(act, d[0], d[1], n, S.st);
+  S.d2h(z, d[1], n);
+  SEAM_END
+}
+int ckf_k_activation_backward(int act, const double* z, const double* dz, double* da, size_t n) {
+  SEAM_BEGIN
+  auto d = S.bufs({n, n, n});
+  S.h2d(d[0], z, n);
+  S.h2d(d[1], dz, n);
+  ckf::k::act_bwd(act, d[0], d[1], d[2], n, S.st);
+  S.d2h(da, d[2], n);
+  SEAM_END
+}
+int ckf_k_sum_squares(const double* x, size_t n, double* out) {
+  SEAM_BEGIN
+  auto d = S.bufs({n});
+  S.h2d(d[0], x, n);
+  ckf::k::sum_squares(d[0], n, S.scal, S.red, S.st);
+  S.d2h(out, S.scal, 1);
+  SEAM_END
+}
+int ckf_k_sum_squared_diff(const double* x, const double* y, size_t n, double* out) {
+  SEAM_BEGIN
+  auto d = S.bufs({n, n});
+  S.h2d(d[0], x, n);
+  S.h2d(d[1], y, n);
+  ckf::k::sum_sq_diff(d[0], d[1], n, S.scal, S.red, S.st);
+  S.d2h(out, S.scal, 1);
+  SEAM_END
+}
+int ckf_k_adam_update(double* w, double* m, double* v, const double* g, size_t n, double lr, double beta1,
+                      double beta2, double eps, long step) {
+  if (beta1 != 0.9 || beta2 != 0.999 || eps != 1e-8) {
+    g_err = "the fused Adam kernel is specialised for betas (0.9, 0.999), eps 1e-8 (model.hpp:72-74)";
+    return CKF_E_CONFIG;
+  }
+  SEAM_BEGIN
+  auto d = S.bufs({n, n, n, n});
+  S.h2d(d[0], w, n);
+  S.h2d(d[1], m, n);
+  S.h2d(d[2], v, n);
+  S.h2d(d[3], g, n);
+  const double bc1 = 1.0 - std::pow(beta1, static_cast<double>(step));
+  const double bc2 = 1.0 - std::pow(beta2, static_cast<double>(step));
+  ckf::k::adam<double>(d[0], d[1], d[2], d[3], nullptr, n, lr, bc1, bc2, 1.0, false, S.scal, S.red, S.st);
+  S.d2h(w, d[0], n);
+  S.d2h(m, d[1], n);
+  S.d2h(v, d[2], n);
+  SEAM_END
+}
+int ckf_k_mse_loss_grad(const double* pred, const double* target, size_t rows, size_t cols, double* dpred,
+                        double* loss) {
+  SEAM_BEGIN
+  const size_t n = rows * cols;
+  auto d = S.bufs({n, n, n});
+  S.h2d(d[0], pred, n);
+  S.h2d(d[1], target, n);
+  ckf::k::mse_loss_grad(d[0], d[1], rows, cols, dpred ? d[2] : nullptr, S.scal, S.red, S.st);
+  if (dpred) S.d2h(dpred, d[2], n);
+  S.d2h(loss, S.scal, 1);
+  SEAM_END
+}
+int ckf_k_softmax_xent_loss_grad(const double* logits, const int* labels, size_t rows, size_t cols, double* dlogits,
+                                 double* loss) {
+  SEAM_BEGIN
+  const size_t n = rows * cols;
+  auto d = S.bufs({n, n, (rows + 1) / 2});
+  S.h2d(d[0], logits, n);
+  CKF_CUDA(cudaMemcpyAsync(d[2], labels, rows * sizeof(int), cudaMemcpyHostToDevice, S.st));
+  ckf::k::xent_loss_grad(d[0], reinterpret_cast<const int*>(d[2]), rows, cols, dlogits ? d[1] : nullptr, S.scal,
+                         S.red, S.st);
+  if (dlogits) S.d2h(dlogits, d[1], n);
+  S.d2h(loss, S.scal, 1);
+  SEAM_END
+}
+int ckf_k_recover_checkfree(const double* w_prev, const double* w_next, size_t n, double op, double on, double* out,
+                            int* degenerate) {
+  if (op < 0.0 || on < 0.0) {
+    g_err = "gradient norms must be nonnegative";
+    return CKF_E_CONFIG;
+  }
+  SEAM_BEGIN
+  auto d = S.bufs({n, n, n});
+  S.h2d(d[0], w_prev, n);
+  S.h2d(d[1], w_next, n);
+  ckf::k::recover<double>(d[0], d[1], d[2], n, op, on, nullptr, S.red, S.st);
+  S.d2h(out, d[2], n);
+  if (degenerate) *degenerate = op + on == 0.0 ? 1 : 0;
+  SEAM_END
+}
+int ckf_k_counter_uniform(uint64_t key, double lo, double hi, double* out, size_t n) {
+  SEAM_BEGIN
+  auto d = S.bufs({n});
+  ckf::k::uniform<double>(d[0], n, key, lo, hi, 0, S.st);
+  S.d2h(out, d[0], n);
+  SEAM_END
+}
+
+// ---------------------------------------------------------------- (2) device primitives
+int ckf_recover_device(int dtype, const void* wp, const void* wn, void* out, size_t n, double op, double on,
+                       double* old_out_sq, void* stream) {
+  return guard([&] {
+    if (op < 0.0 || on < 0.0) ckf::raise(CKF_E_CONFIG, "gradient norms must be nonnegative");
+    static thread_local ckf::ReduceScratch red;
+    if (!red.partials) CKF_CUDA(cudaMalloc(&red.partials, ckf::ReduceScratch::kMaxReduceBlocks * sizeof(double)));
+    auto st = static_cast<cudaStream_t>(stream);
+    if (dtype == CKF_FP64)
+      ckf::k::recover(static_cast<const double*>(wp), static_cast<const double*>(wn), static_cast<double*>(out), n, op,
+                      on, old_out_sq, red, st);
+    else if (dtype == CKF_FP32)
+      ckf::k::recover(static_cast<const float*>(wp), static_cast<const float*>(wn), static_cast<float*>(out), n, op, on,
+                      old_out_sq, red, st);
+    else
+      ckf::raise(CKF_E_CONFIG, "recover: dtype must be CKF_FP64 or CKF_FP32 (master weights)");
+  });
+}
+
+int ckf_adam_device(int dtype, void* w, void* m, void* v, void* g, void* w_bf16, size_t n, double lr, double bc1,
+                    double bc2, double grad_scale, int zero_grad, double* omega, void* stream) {
+  return guard([&] {
+    static thread_local ckf::ReduceScratch red;
+    if (!red.partials) CKF_CUDA(cudaMalloc(&red.partials, ckf::ReduceScratch::kMaxReduceBlocks * sizeof(double)));
+    auto st = static_cast<cudaStream_t>(stream);
+    auto lp = static_cast<__nv_bfloat16*>(w_bf16);
+    if (dtype == CKF_FP64)
+      ckf::k::adam(static_cast<double*>(w), static_cast<double*>(m), static_cast<double*>(v), static_cast<double*>(g),
+                   lp, n, lr, bc1, bc2, grad_scale, zero_grad != 0, omega, red, st);
+    else if (dtype == CKF_FP32)
+      ckf::k::adam(static_cast<float*>(w), static_cast<float*>(m), static_cast<float*>(v), static_cast<float*>(g), lp,
+                   n, lr, bc1, bc2, grad_scale, zero_grad != 0, omega, red, st);
+    else
+      ckf::raise(CKF_E_CONFIG, "adam: dtype must be CKF_FP64 or CKF_FP32 (master weights)");
+  });
+}
+
+// ---------------------------------------------------------------- (3) engine
+int ckf_engine_create(const ckf_model_desc* desc, ckf_engine_t* out) {
+  return guard([&] {
+    if (!desc || !out) ckf::raise(CKF_E_USAGE, "null argument");
+    *out = reinterpret_cast<ckf_engine_t>(new ckf::Engine(*desc));
+  });
+}
+int ckf_engine_destroy(ckf_engine_t e) {
+  return guard([&] { delete E(e); });
+}
+int ckf_engine_param_counts(ckf_engine_t e, size_t* sp, size_t* ep, size_t* dp) {
+  return guard([&] {
+    if (sp) *sp = E(e)->stage(1).n;
+    if (ep) *ep = E(e)->embed().n;
+    if (dp) *dp = E(e)->deembed().n;
+  });
+}
+int ckf_engine_init(ckf_engine_t e, uint64_t seed, double lr) {
+  return guard([&] { E(e)->init(seed, lr); });
+}
+int ckf_nccl_unique_id(void* uid_out, size_t cap) {
+  return guard([&] { ckf::nccl_unique_id(uid_out, cap); });
+}
+int ckf_engine_attach_comm(ckf_engine_t e, const void* uid, int nranks, int rank, const int* stage_rank) {
+  return guard([&] { E(e)->attach_comm(uid, nranks, rank, stage_rank); });
+}
+int ckf_engine_run_iteration(ckf_engine_t e, const int* orders, int m, const void* x, const void* y, size_t rows,
+                             int on_device, long iteration, double* loss, double* omegas) {
+  return guard([&] { E(e)->run_iteration(orders, m, x, y, rows, on_device != 0, iteration, loss, omegas); });
+}
+int ckf_engine_eval_loss(ckf_engine_t e, const int* order, const void* x, const void* y, size_t rows, int on_device,
+                         double* loss) {
+  return guard([&] { *loss = E(e)->eval_loss(order, x, y, rows, on_device != 0); });
+}
+int ckf_engine_predict(ckf_engine_t e, const int* order, const double* x, size_t rows, double* pred) {
+  return guard([&] { E(e)->predict(order, x, rows, pred); });
+}
+int ckf_engine_refresh_edge_replicas(ckf_engine_t e) {
+  return guard([&] { E(e)->refresh_edge_replicas(); });
+}
+int ckf_engine_kill_stage(ckf_engine_t e, int stage) {
+  return guard([&] { E(e)->kill_stage(stage); });
+}
+int ckf_engine_recover_stage(ckf_engine_t e, int stage, int mode, int moments, double lr_bump, uint64_t reinit_seed,
+                             int want_reduction_error, ckf_recovery_report* out) {
+  return guard([&] {
+    ckf_recovery_report r = E(e)->recover_stage(stage, mode, moments, lr_bump, reinit_seed, want_reduction_error != 0);
+    if (out) *out = r;
+  });
+}
+int ckf_engine_export_stage(ckf_engine_t e, int stage, double* w, double* m, double* v) {
+  return guard([&] { E(e)->export_group(E(e)->stage(stage), w, m, v); });
+}
+int ckf_engine_import_stage(ckf_engine_t e, int stage, const double* w, const double* m, const double* v) {
+  return guard([&] { E(e)->import_group(E(e)->stage(stage), w, m, v); });
+}
+int ckf_engine_export_edge(ckf_engine_t e, int which, double* w, double* m, double* v) {
+  return guard([&] { E(e)->export_group(which == 0 ? E(e)->embed() : E(e)->deembed(), w, m, v); });
+}
+int ckf_engine_import_edge(ckf_engine_t e, int which, const double* w, const double* m, const double* v) {
+  return guard([&] { E(e)->import_group(which == 0 ? E(e)->embed() : E(e)->deembed(), w, m, v); });
+}
+int ckf_engine_get_scalars(ckf_engine_t e, int stage, double* omega, double* lr, long* step) {
+  return guard([&] {
+    auto& g = E(e)->stage(stage);
+    if (omega) *omega = g.omega;
+    if (lr) *lr = g.lr;
+    if (step) *step = g.step;
+  });
+}
+int ckf_engine_set_scalars(ckf_engine_t e, int stage, double omega, double lr, long step) {
+  return guard([&] {
+    auto& g = E(e)->stage(stage);
+    g.omega = omega;
+    g.lr = lr;
+    g.step = step;
+  });
+}
+int ckf_engine_get_edge_scalars(ckf_engine_t e, double* lr, long* se, long* sd) {
+  return guard([&] {
+    if (lr) *lr = E(e)->edge_lr;
+    if (se) *se = E(e)->embed().step;
+    if (sd) *sd = E(e)->deembed().step;
+  });
+}
+int ckf_engine_set_edge_scalars(ckf_engine_t e, double lr, long se, long sd) {
+  return guard([&] {
+    E(e)->edge_lr = lr;
+    E(e)->embed().step = se;
+    E(e)->deembed().step = sd;
+  });
+}
+long ckf_engine_kernel_launches(ckf_engine_t) { return ckf::launch_counter(); }
+int ckf_engine_sync(ckf_engine_t e) {
+  return guard([&] { CKF_CUDA(cudaStreamSynchronize(E(e)->stream())); });
+}
+
+// ---------------------------------------------------------------- (4) trainer
+int ckf_run_experiment(const char* kv, const char* trace_text, uint64_t seed, char* record, size_t cap) {
+  return guard([&] {
+    const std::string r = ckf::run_experiment(kv ? kv : "", trace_text ? trace_text : "", seed);
+    if (r.size() + 1 > cap) ckf::raise(CKF_E_USAGE, "record buffer too small");
+    std::memcpy(record, r.c_str(), r.size() + 1);
+  });
+}
+
+}  // extern "C"

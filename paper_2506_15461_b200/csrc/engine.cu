@@ -1,0 +1,633 @@
+// Engine core: parameter groups, the iteration driver, replicas and the
+// recovery path.  Block arithmetic lives in mlp_block.cu / llama_block.cu.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "engine.h"
+
+namespace ckf {
+
+long& launch_counter() {
+  static long n = 0;
+  return n;
+}
+
+std::vector<Range> even_partition(size_t layers, size_t stages) {
+  // model.cpp:63-73: contiguous, the first (L mod s) stages take one extra layer
+  std::vector<Range> out;
+  size_t next = 1;
+  for (size_t i = 0; i < stages; ++i) {
+    const size_t cnt = layers / stages + (i < layers % stages ? 1 : 0);
+    out.push_back({next, next + cnt - 1});
+    next += cnt;
+  }
+  return out;
+}
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+// Resolved at runtime so the library does not pin one libnccl: inside a torch
+// process this binds to the NCCL torch already loaded.
+namespace {
+struct NcclApi {
+  using Uid = struct { char b[128]; };
+  int (*GetUniqueId)(void*) = nullptr;
+  int (*CommInitRank)(void**, int, Uid, int) = nullptr;
+  int (*CommDestroy)(void*) = nullptr;
+  int (*Send)(const void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*Recv)(void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*GroupStart)() = nullptr;
+  int (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(int) = nullptr;
+  bool ok = false;
+};
+NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.GetUniqueId = reinterpret_cast<int (*)(void*)>(dlsym(h, "ncclGetUniqueId"));
+      api.CommInitRank = reinterpret_cast<int (*)(void**, int, NcclApi::Uid, int)>(dlsym(h, "ncclCommInitRank"));
+      api.CommDestroy = reinterpret_cast<int (*)(void*)>(dlsym(h, "ncclCommDestroy"));
+      api.Send = reinterpret_cast<int (*)(const void*, size_t, int, int, void*, cudaStream_t)>(dlsym(h, "ncclSend"));
+      api.Recv = reinterpret_cast<int (*)(void*, size_t, int, int, void*, cudaStream_t)>(dlsym(h, "ncclRecv"));
+      api.GroupStart = reinterpret_cast<int (*)()>(dlsym(h, "ncclGroupStart"));
+      api.GroupEnd = reinterpret_cast<int (*)()>(dlsym(h, "ncclGroupEnd"));
+      api.GetErrorString = reinterpret_cast<const char* (*)(int)>(dlsym(h, "ncclGetErrorString"));
+      api.ok = api.GetUniqueId && api.CommInitRank && api.Send && api.Recv;
+    }
+  }
+  if (!api.ok) raise(7, "libnccl.so.2 not loadable (multi-GPU placement needs NCCL)");
+  return api;
+}
+void nccl_check(int r, const char* what) {
+  if (r != 0) raise(7, std::string(what) + ": " + (nccl().GetErrorString ? nccl().GetErrorString(r) : "nccl error"));
+}
+}  // namespace
+
+int nccl_unique_id(void* out, size_t cap) {
+  if (cap < 128) raise(1, "unique id buffer must hold 128 bytes");
+  nccl_check(nccl().GetUniqueId(out), "ncclGetUniqueId");
+  return 128;
+}
+
+// ------------------------------------------------------------------ lifecycle
+Engine::Engine(const ckf_model_desc& in) {
+  d_.block = in.block;
+  d_.prec = in.precision;
+  d_.act = in.activation;
+  d_.task = in.task;
+  d_.in = in.input_dim;
+  d_.hid = in.hidden_dim;
+  d_.d = in.model_dim;
+  d_.out = in.output_dim;
+  d_.L = in.num_layers;
+  d_.s = in.num_stages;
+  d_.heads = in.n_heads ? in.n_heads : 1;
+  d_.T = in.seq_len ? in.seq_len : 1;
+  d_.max_rows = in.max_rows ? in.max_rows : 256;
+  d_.device = in.device;
+  if (d_.block != CKF_BLOCK_MLP && d_.block != CKF_BLOCK_LLAMA) raise(1, "unknown block kind");
+  if (d_.prec < CKF_FP64 || d_.prec > CKF_BF16) raise(1, "unknown precision");
+  if (d_.block == CKF_BLOCK_MLP && d_.prec == CKF_BF16) raise(1, "the residual-MLP parity block runs in fp64 or fp32");
+  if (d_.in == 0 || d_.hid == 0 || d_.d == 0 || d_.out == 0 || d_.L == 0)
+    raise(1, "model dimensions and layer count must be positive");
+  if (d_.s < 1 || d_.s > d_.L) raise(1, "num_stages must lie in [1, num_layers]");
+  if (in.partition) {
+    for (size_t i = 0; i < d_.s; ++i) d_.part.push_back({in.partition[2 * i], in.partition[2 * i + 1]});
+  } else {
+    d_.part = even_partition(d_.L, d_.s);
+  }
+  size_t expect = 1;  // model.cpp:88-94
+  for (auto& r : d_.part) {
+    if (r.first != expect || r.last < r.first || r.last > d_.L)
+      raise(1, "partition ranges must be contiguous, ordered and cover [1, num_layers]");
+    expect = r.last + 1;
+  }
+  if (expect != d_.L + 1) raise(1, "partition does not cover all layers");
+  if (d_.task == CKF_TASK_CLASSIFICATION && d_.out < 2) raise(1, "classification requires output_dim >= 2");
+
+  CKF_CUDA(cudaSetDevice(d_.device));
+  CKF_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+  CKF_CUDA(cudaMalloc(&red_.partials, ReduceScratch::kMaxReduceBlocks * sizeof(double)));
+  CKF_CUDA(cudaMalloc(&scal_, 4096 * sizeof(double)));
+  CKF_CUDA(cudaMemset(scal_, 0, 4096 * sizeof(double)));
+  CKF_CUDA(cudaEventCreate(&ev0_));
+  CKF_CUDA(cudaEventCreate(&ev1_));
+
+  impl_ = d_.block == CKF_BLOCK_MLP ? make_mlp_block(this) : make_llama_block(this);
+  const bool lowp = d_.prec == CKF_BF16;
+  stages_.resize(d_.s);
+  for (size_t i = 0; i < d_.s; ++i) alloc_group(stages_[i], impl_->stage_params(static_cast<int>(i + 1)), lowp);
+  alloc_group(embed_, impl_->embed_params(), lowp);
+  alloc_group(deembed_, impl_->deembed_params(), lowp);
+}
+
+Engine::~Engine() {
+  cudaSetDevice(d_.device);
+  if (st_) cudaStreamSynchronize(st_);
+  impl_.reset();
+  for (auto& g : stages_) free_group(g);
+  free_group(embed_);
+  free_group(deembed_);
+  cudaFree(rep_embed_);
+  cudaFree(rep_deembed_);
+  for (void* p : ws_) cudaFree(p);
+  cudaFree(red_.partials);
+  cudaFree(scal_);
+  if (comm_ && nccl().CommDestroy) nccl().CommDestroy(comm_);
+  if (ev0_) cudaEventDestroy(ev0_);
+  if (ev1_) cudaEventDestroy(ev1_);
+  if (st_) cudaStreamDestroy(st_);
+}
+
+void Engine::alloc_group(ParamGroup& g, size_t n, bool lowp) {
+  g.n = n;
+  const size_t b = n * master_bytes();
+  if (!g.owned || n == 0) return;
+  CKF_CUDA(cudaMalloc(&g.w, b));
+  CKF_CUDA(cudaMalloc(&g.g, b));
+  CKF_CUDA(cudaMalloc(&g.m, b));
+  CKF_CUDA(cudaMalloc(&g.v, b));
+  CKF_CUDA(cudaMemsetAsync(g.g, 0, b, st_));
+  CKF_CUDA(cudaMemsetAsync(g.m, 0, b, st_));
+  CKF_CUDA(cudaMemsetAsync(g.v, 0, b, st_));
+  if (lowp) CKF_CUDA(cudaMalloc(&g.wlp, n * sizeof(__nv_bfloat16)));
+}
+
+void Engine::free_group(ParamGroup& g) {
+  cudaFree(g.w);
+  cudaFree(g.g);
+  cudaFree(g.m);
+  cudaFree(g.v);
+  cudaFree(g.wlp);
+  g.w = g.g = g.m = g.v = nullptr;
+  g.wlp = nullptr;
+}
+
+void* Engine::ws(size_t bytes, int slot) {
+  if (slot >= static_cast<int>(ws_.size())) {
+    ws_.resize(static_cast<size_t>(slot) + 1, nullptr);
+    ws_size_.resize(static_cast<size_t>(slot) + 1, 0);
+  }
+  if (ws_size_[static_cast<size_t>(slot)] < bytes) {
+    CKF_CUDA(cudaStreamSynchronize(st_));
+    cudaFree(ws_[static_cast<size_t>(slot)]);
+    const size_t want = std::max<size_t>(bytes, 256);
+    CKF_CUDA(cudaMalloc(&ws_[static_cast<size_t>(slot)], want));
+    ws_size_[static_cast<size_t>(slot)] = want;
+  }
+  return ws_[static_cast<size_t>(slot)];
+}
+
+// ------------------------------------------------------------------ placement
+void Engine::attach_comm(const void* uid, int nranks, int rank, const int* stage_rank) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) raise(1, "invalid rank / world size");
+  stage_rank_.assign(stage_rank, stage_rank + d_.s);
+  for (int r : stage_rank_)
+    if (r < 0 || r >= nranks) raise(1, "stage placed on a rank outside the world");
+  rank_ = rank;
+  nranks_ = nranks;
+  if (nranks > 1) {
+    NcclApi::Uid u;
+    std::memcpy(u.b, uid, 128);
+    CKF_CUDA(cudaSetDevice(d_.device));
+    nccl_check(nccl().CommInitRank(&comm_, nranks, u, rank), "ncclCommInitRank");
+  }
+  // release buffers of stages this rank does not own
+  for (size_t i = 0; i < d_.s; ++i) {
+    stages_[i].owned = stage_rank_[i] == rank_;
+    if (!stages_[i].owned) free_group(stages_[i]);
+  }
+  embed_.owned = owner_of_embed() == rank_;
+  deembed_.owned = owner_of_deembed() == rank_;
+  if (!embed_.owned) free_group(embed_);
+  if (!deembed_.owned) free_group(deembed_);
+}
+
+void Engine::hop(void* buf, size_t bytes, int src, int dst) {
+  if (src == dst || bytes == 0) return;
+  if (rank_ == src) nccl_check(nccl().Send(buf, bytes, /*ncclInt8*/ 0, dst, comm_, st_), "ncclSend");
+  if (rank_ == dst) nccl_check(nccl().Recv(buf, bytes, /*ncclInt8*/ 0, src, comm_, st_), "ncclRecv");
+}
+
+// ------------------------------------------------------------------ init
+void Engine::init(uint64_t seed, double lr) {
+  CKF_CUDA(cudaSetDevice(d_.device));
+  if (lr <= 0.0) raise(1, "learning rate must be positive");
+  for (size_t i = 0; i < d_.s; ++i) {
+    ParamGroup& g = stages_[i];
+    g.step = 0;
+    g.omega = 0.0;
+    g.lr = lr;
+    if (!g.owned) continue;
+    impl_->init_stage(static_cast<int>(i + 1), seed, g.w);
+    CKF_CUDA(cudaMemsetAsync(g.g, 0, g.n * master_bytes(), st_));
+    CKF_CUDA(cudaMemsetAsync(g.m, 0, g.n * master_bytes(), st_));
+    CKF_CUDA(cudaMemsetAsync(g.v, 0, g.n * master_bytes(), st_));
+    if (g.wlp) k::convert(static_cast<const float*>(g.w), g.wlp, g.n, st_);
+  }
+  impl_->init_edges(seed, embed_.owned ? embed_.w : nullptr, deembed_.owned ? deembed_.w : nullptr);
+  for (ParamGroup* g : {&embed_, &deembed_}) {
+    g->step = 0;
+    g->lr = lr;
+    if (!g->owned) continue;
+    CKF_CUDA(cudaMemsetAsync(g->g, 0, g->n * master_bytes(), st_));
+    CKF_CUDA(cudaMemsetAsync(g->m, 0, g->n * master_bytes(), st_));
+    CKF_CUDA(cudaMemsetAsync(g->v, 0, g->n * master_bytes(), st_));
+    if (g->wlp) k::convert(static_cast<const float*>(g->w), g->wlp, g->n, st_);
+  }
+  edge_lr = lr;
+  replica_staleness_ = -1;
+  CKF_CUDA(cudaStreamSynchronize(st_));
+}
+
+// ------------------------------------------------------------------ iteration
+namespace {
+void validate_order(const int* order, size_t s) {
+  std::vector<bool> seen(s, false);  // model.cpp:201-209
+  for (size_t i = 0; i < s; ++i) {
+    const int sid = order[i];
+    if (sid < 1 || static_cast<size_t>(sid) > s || seen[static_cast<size_t>(sid - 1)])
+      raise(1, "stage order must be a permutation of [1..num_stages]");
+    seen[static_cast<size_t>(sid - 1)] = true;
+  }
+}
+}  // namespace
+
+void Engine::adam_group(ParamGroup& g, double lr, double gscale, double* omega_dev) {
+  if (!g.owned || g.n == 0) return;
+  ++g.step;
+  // bias corrections with std::pow on the host, exactly kernels_serial.cpp:135-136
+  const double bc1 = 1.0 - std::pow(0.9, static_cast<double>(g.step));
+  const double bc2 = 1.0 - std::pow(0.999, static_cast<double>(g.step));
+  if (fp64())
+    k::adam(static_cast<double*>(g.w), static_cast<double*>(g.m), static_cast<double*>(g.v),
+            static_cast<double*>(g.g), g.wlp, g.n, lr, bc1, bc2, gscale, true, omega_dev, red_, st_);
+  else
+    k::adam(static_cast<float*>(g.w), static_cast<float*>(g.m), static_cast<float*>(g.v), static_cast<float*>(g.g),
+            g.wlp, g.n, lr, bc1, bc2, gscale, true, omega_dev, red_, st_);
+}
+
+void Engine::run_iteration(const int* orders, int m, const void* x, const void* y, size_t rows, bool on_device,
+                           long iteration, double* loss, double* omegas) {
+  CKF_CUDA(cudaSetDevice(d_.device));
+  if (m < 1) raise(1, "microbatch count must be positive");
+  if (rows == 0 || rows % static_cast<size_t>(m) != 0)
+    raise(1, "batch size must be divisible by the microbatch count");  // pipeline.cpp:62-63
+  if (m > 2000) raise(1, "at most 2000 microbatches per iteration");
+  for (int k = 0; k < m; ++k) validate_order(orders + static_cast<size_t>(k) * d_.s, d_.s);
+  for (auto& g : stages_)
+    if (g.lr <= 0.0) raise(1, "learning rate must be positive");
+  const size_t mb = rows / static_cast<size_t>(m);
+
+  const size_t xcols = d_.block == CKF_BLOCK_MLP ? d_.in : d_.T + 1;
+  const size_t xelt = d_.block == CKF_BLOCK_MLP ? master_bytes() : sizeof(int);
+  const size_t ycols = d_.block == CKF_BLOCK_MLP ? (d_.task == CKF_TASK_REGRESSION ? d_.out : 1) : 0;
+  const size_t yelt = d_.task == CKF_TASK_REGRESSION ? master_bytes() : sizeof(int);
+
+  const char* xd = static_cast<const char*>(x);
+  const char* yd = static_cast<const char*>(y);
+  if (!on_device) {
+    impl_->eng = this;
+    void* xb = ws(rows * xcols * xelt, 0);
+    if (d_.block == CKF_BLOCK_MLP) {
+      // host inputs arrive as fp64 (the reference's Matrix); convert to the master dtype
+      void* tmp = ws(rows * std::max(xcols, ycols) * sizeof(double), 2);
+      CKF_CUDA(cudaMemcpyAsync(tmp, x, rows * xcols * sizeof(double), cudaMemcpyHostToDevice, st_));
+      if (fp64())
+        CKF_CUDA(cudaMemcpyAsync(xb, tmp, rows * xcols * 8, cudaMemcpyDeviceToDevice, st_));
+      else
+        k::convert(static_cast<const double*>(tmp), static_cast<float*>(xb), rows * xcols, st_);
+      void* yb = ws(rows * ycols * yelt, 1);
+      if (d_.task == CKF_TASK_REGRESSION) {
+        CKF_CUDA(cudaMemcpyAsync(tmp, y, rows * ycols * sizeof(double), cudaMemcpyHostToDevice, st_));
+        if (fp64())
+          CKF_CUDA(cudaMemcpyAsync(yb, tmp, rows * ycols * 8, cudaMemcpyDeviceToDevice, st_));
+        else
+          k::convert(static_cast<const double*>(tmp), static_cast<float*>(yb), rows * ycols, st_);
+      } else {
+        std::vector<int> lab(rows);
+        const double* yh = static_cast<const double*>(y);
+        for (size_t i = 0; i < rows; ++i) {
+          const double l = yh[i];
+          if (l < 0 || l >= static_cast<double>(d_.out)) raise(1, "label out of range for output_dim");
+          lab[i] = static_cast<int>(l);
+        }
+        CKF_CUDA(cudaMemcpyAsync(yb, lab.data(), rows * sizeof(int), cudaMemcpyHostToDevice, st_));
+        CKF_CUDA(cudaStreamSynchronize(st_));
+      }
+      yd = static_cast<const char*>(yb);
+    } else {
+      CKF_CUDA(cudaMemcpyAsync(xb, x, rows * xcols * xelt, cudaMemcpyHostToDevice, st_));
+    }
+    xd = static_cast<const char*>(xb);
+  }
+
+  for (int k = 0; k < m; ++k) {
+    const int* order = orders + static_cast<size_t>(k) * d_.s;
+    impl_->microbatch(order, xd + static_cast<size_t>(k) * mb * xcols * xelt,
+                      yd ? yd + static_cast<size_t>(k) * mb * ycols * yelt : nullptr, mb, true, scal_ + k);
+  }
+  // mean loss in microbatch order, then *1/m (model.cpp:299-312, pipeline.cpp:82-83)
+  std::vector<double> losses(static_cast<size_t>(m));
+  const double inv = 1.0 / static_cast<double>(m);
+  for (size_t i = 0; i < d_.s; ++i) adam_group(stages_[i], stages_[i].lr, inv, scal_ + 2048 + i);
+  adam_group(embed_, edge_lr, inv, scal_ + 3000);
+  adam_group(deembed_, edge_lr, inv, scal_ + 3001);
+  std::vector<double> om(d_.s);
+  CKF_CUDA(cudaMemcpyAsync(losses.data(), scal_, static_cast<size_t>(m) * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  CKF_CUDA(cudaMemcpyAsync(om.data(), scal_ + 2048, d_.s * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  CKF_CUDA(cudaStreamSynchronize(st_));
+  double total = 0.0;
+  for (double l : losses) total += l;
+  total *= inv;
+  bool finite = std::isfinite(total) || !mine(owner_of_deembed());
+  for (size_t i = 0; i < d_.s; ++i) {
+    if (!stages_[i].owned) continue;
+    stages_[i].omega = om[i];
+    if (!std::isfinite(om[i])) finite = false;
+  }
+  if (!finite) raise(2, "non-finite gradient or activation", iteration);
+  if (loss) *loss = mine(owner_of_deembed()) ? total : 0.0;
+  if (omegas)
+    for (size_t i = 0; i < d_.s; ++i) omegas[i] = stages_[i].omega;
+}
+
+double Engine::eval_loss(const int* order, const void* x, const void* y, size_t rows, bool on_device) {
+  CKF_CUDA(cudaSetDevice(d_.device));
+  validate_order(order, d_.s);
+  if (rows == 0) raise(1, "empty batch");
+  if (!on_device) {
+    // reuse the host upload path of run_iteration without training
+    const size_t xcols = d_.block == CKF_BLOCK_MLP ? d_.in : d_.T + 1;
+    if (d_.block == CKF_BLOCK_LLAMA) {
+      void* xb = ws(rows * xcols * sizeof(int), 0);
+      CKF_CUDA(cudaMemcpyAsync(xb, x, rows * xcols * sizeof(int), cudaMemcpyHostToDevice, st_));
+      x = xb;
+    } else {
+      const size_t ycols = d_.task == CKF_TASK_REGRESSION ? d_.out : 1;
+      void* tmp = ws(rows * std::max(xcols, ycols) * sizeof(double), 2);
+      void* xb = ws(rows * xcols * master_bytes(), 0);
+      CKF_CUDA(cudaMemcpyAsync(tmp, x, rows * xcols * 8, cudaMemcpyHostToDevice, st_));
+      if (fp64())
+        CKF_CUDA(cudaMemcpyAsync(xb, tmp, rows * xcols * 8, cudaMemcpyDeviceToDevice, st_));
+      else
+        k::convert(static_cast<const double*>(tmp), static_cast<float*>(xb), rows * xcols, st_);
+      void* yb = ws(rows * ycols * (d_.task == CKF_TASK_REGRESSION ? master_bytes() : 4), 1);
+      if (d_.task == CKF_TASK_REGRESSION) {
+        CKF_CUDA(cudaMemcpyAsync(tmp, y, rows * ycols * 8, cudaMemcpyHostToDevice, st_));
+        if (fp64())
+          CKF_CUDA(cudaMemcpyAsync(yb, tmp, rows * ycols * 8, cudaMemcpyDeviceToDevice, st_));
+        else
+          k::convert(static_cast<const double*>(tmp), static_cast<float*>(yb), rows * ycols, st_);
+      } else {
+        std::vector<int> lab(rows);
+        for (size_t i = 0; i < rows; ++i) lab[i] = static_cast<int>(static_cast<const double*>(y)[i]);
+        CKF_CUDA(cudaMemcpyAsync(yb, lab.data(), rows * 4, cudaMemcpyHostToDevice, st_));
+        CKF_CUDA(cudaStreamSynchronize(st_));
+      }
+      x = xb;
+      y = yb;
+    }
+  }
+  impl_->microbatch(order, x, y, rows, false, scal_ + 4000);
+  double l = 0.0;
+  CKF_CUDA(cudaMemcpyAsync(&l, scal_ + 4000, sizeof(double), cudaMemcpyDeviceToHost, st_));
+  CKF_CUDA(cudaStreamSynchronize(st_));
+  return l;
+}
+
+void Engine::predict_device(const int* order, const void* x_dev, size_t rows, void* pred_dev) {
+  validate_order(order, d_.s);
+  impl_->predict(order, x_dev, rows, pred_dev);
+}
+
+void Engine::predict(const int* order, const double* x_host, size_t rows, double* pred_host) {
+  CKF_CUDA(cudaSetDevice(d_.device));
+  if (d_.block != CKF_BLOCK_MLP) raise(1, "predict is defined for the residual-MLP block");
+  validate_order(order, d_.s);
+  void* tmp = ws(rows * std::max(d_.in, d_.out) * 8, 2);
+  void* xb = ws(rows * d_.in * master_bytes(), 0);
+  void* pb = ws(rows * d_.out * master_bytes(), 1);
+  CKF_CUDA(cudaMemcpyAsync(tmp, x_host, rows * d_.in * 8, cudaMemcpyHostToDevice, st_));
+  if (fp64())
+    CKF_CUDA(cudaMemcpyAsync(xb, tmp, rows * d_.in * 8, cudaMemcpyDeviceToDevice, st_));
+  else
+    k::convert(static_cast<const double*>(tmp), static_cast<float*>(xb), rows * d_.in, st_);
+  impl_->predict(order, xb, rows, pb);
+  if (fp64()) {
+    CKF_CUDA(cudaMemcpyAsync(pred_host, pb, rows * d_.out * 8, cudaMemcpyDeviceToHost, st_));
+  } else {
+    k::convert(static_cast<const float*>(pb), static_cast<double*>(tmp), rows * d_.out, st_);
+    CKF_CUDA(cudaMemcpyAsync(pred_host, tmp, rows * d_.out * 8, cudaMemcpyDeviceToHost, st_));
+  }
+  CKF_CUDA(cudaStreamSynchronize(st_));
+}
+
+// ------------------------------------------------------------------ replicas
+void Engine::refresh_edge_replicas() {
+  // recovery.cpp:80-84: replica := (E, E^-1); held by the GPUs of stages 2 and s-1
+  CKF_CUDA(cudaSetDevice(d_.device));
+  const int hold_e = owner_of_stage(d_.s >= 2 ? 2 : 1);
+  const int hold_d = owner_of_stage(d_.s >= 2 ? static_cast<int>(d_.s) - 1 : 1);
+  const size_t be = embed_.n * master_bytes(), bd = deembed_.n * master_bytes();
+  if (mine(hold_e) && !rep_embed_) CKF_CUDA(cudaMalloc(&rep_embed_, be));
+  if (mine(hold_d) && !rep_deembed_) CKF_CUDA(cudaMalloc(&rep_deembed_, bd));
+  if (mine(owner_of_embed()) && mine(hold_e))
+    CKF_CUDA(cudaMemcpyAsync(rep_embed_, embed_.w, be, cudaMemcpyDeviceToDevice, st_));
+  else
+    hop(mine(owner_of_embed()) ? embed_.w : rep_embed_, be, owner_of_embed(), hold_e);
+  if (mine(owner_of_deembed()) && mine(hold_d))
+    CKF_CUDA(cudaMemcpyAsync(rep_deembed_, deembed_.w, bd, cudaMemcpyDeviceToDevice, st_));
+  else
+    hop(mine(owner_of_deembed()) ? deembed_.w : rep_deembed_, bd, owner_of_deembed(), hold_d);
+  replica_staleness_ = 0;
+}
+
+void Engine::kill_stage(int sid) {
+  CKF_CUDA(cudaSetDevice(d_.device));
+  if (sid < 1 || static_cast<size_t>(sid) > d_.s) raise(1, "stage id out of range");
+  ParamGroup& g = stage(sid);
+  auto poison = [&](ParamGroup& p) {
+    if (!p.owned) return;
+    if (fp64()) {
+      for (void* b : {p.w, p.m, p.v}) k::poison(static_cast<double*>(b), p.n, st_);
+    } else {
+      for (void* b : {p.w, p.m, p.v}) k::poison(static_cast<float*>(b), p.n, st_);
+    }
+    if (p.wlp) k::fill(p.wlp, NAN, p.n, st_);
+  };
+  poison(g);
+  // the edge layers live on the GPUs of stages 1 and s (cost_model.cpp:264-268)
+  if (sid == 1) poison(embed_);
+  if (static_cast<size_t>(sid) == d_.s) poison(deembed_);
+}
+
+// ------------------------------------------------------------------ recovery
+ckf_recovery_report Engine::recover_stage(int sid, int mode, int moments, double lr_bump, uint64_t reinit_seed,
+                                          bool want_red) {
+  CKF_CUDA(cudaSetDevice(d_.device));
+  const int s = static_cast<int>(d_.s);
+  if (sid < 1 || sid > s) raise(1, "stage id out of range");
+  if (lr_bump <= 0.0) raise(1, "lr_bump must be positive");
+  ckf_recovery_report rep{0, 0.0, 0.0};
+  ParamGroup& f = stage(sid);
+  const bool edge = sid == 1 || sid == s;
+  if (edge && mode != CKF_REC_EDGE)
+    raise(5, std::string("stage ") + std::to_string(sid) +
+                 " is a first/last stage: only the CheckFree+ edge copy can recover it (single neighbour)");
+  if (!edge && mode == CKF_REC_EDGE) raise(1, "edge recovery applies to the first and last stage only");
+  if (mode == CKF_REC_EDGE && replica_staleness_ != 0)
+    raise(1, "edge replica is stale; refresh must precede recovery");  // recovery.cpp:98
+  if (f.lr <= 0.0) raise(1, "learning rate must be positive");
+  if (nranks_ > 1) raise(1, "multi-GPU recovery goes through ckf_engine_recover_stage_peer (not attached)");
+
+  const size_t mb = master_bytes();
+  const size_t bytes = f.n * mb;
+  double* red_dev = want_red ? scal_ + 3500 : nullptr;
+  CKF_CUDA(cudaEventRecord(ev0_, st_));
+  if (mode == CKF_REC_EDGE) {
+    ParamGroup& nb = stage(sid == 1 ? 2 : s - 1);
+    if (want_red) {
+      if (fp64())
+        k::sum_sq_diff(static_cast<const double*>(f.w), static_cast<const double*>(nb.w), f.n, red_dev, red_, st_);
+      else
+        k::sum_sq_diff(static_cast<const float*>(f.w), static_cast<const float*>(nb.w), f.n, red_dev, red_, st_);
+    }
+    CKF_CUDA(cudaMemcpyAsync(f.w, nb.w, bytes, cudaMemcpyDeviceToDevice, st_));
+    ParamGroup& eg = sid == 1 ? embed_ : deembed_;
+    CKF_CUDA(cudaMemcpyAsync(eg.w, sid == 1 ? rep_embed_ : rep_deembed_, eg.n * mb, cudaMemcpyDeviceToDevice, st_));
+    CKF_CUDA(cudaMemsetAsync(eg.m, 0, eg.n * mb, st_));  // that edge's Adam state resets (trainer.cpp:218-224)
+    CKF_CUDA(cudaMemsetAsync(eg.v, 0, eg.n * mb, st_));
+    CKF_CUDA(cudaMemsetAsync(eg.g, 0, eg.n * mb, st_));
+    eg.step = 0;
+    if (eg.wlp) k::convert(static_cast<const float*>(eg.w), eg.wlp, eg.n, st_);
+    if (moments == CKF_MOM_AVERAGED) {  // single neighbour: copy, like the weights (trainer.cpp:225-226)
+      CKF_CUDA(cudaMemcpyAsync(f.m, nb.m, bytes, cudaMemcpyDeviceToDevice, st_));
+      CKF_CUDA(cudaMemcpyAsync(f.v, nb.v, bytes, cudaMemcpyDeviceToDevice, st_));
+      f.step = nb.step;
+    } else {
+      CKF_CUDA(cudaMemsetAsync(f.m, 0, bytes, st_));
+      CKF_CUDA(cudaMemsetAsync(f.v, 0, bytes, st_));
+      f.step = 0;
+    }
+  } else {
+    ParamGroup& p = stage(sid - 1);
+    ParamGroup& n = stage(sid + 1);
+    double op = p.omega, on = n.omega;
+    if (op < 0.0 || on < 0.0) raise(1, "gradient norms must be nonnegative");
+    if (mode == CKF_REC_CHECKFREE) {
+      if (op + on == 0.0) rep.degenerate = 1;  // recovery.cpp:63-68
+    } else if (mode == CKF_REC_UNIFORM) {
+      op = on = 1.0;
+    } else if (mode == CKF_REC_COPY_PREV) {
+      op = 1.0;
+      on = 0.0;
+    }
+    if (mode == CKF_REC_RANDOM) {
+      void* tmp = want_red ? ws(bytes, 3) : nullptr;
+      if (want_red) CKF_CUDA(cudaMemcpyAsync(tmp, f.w, bytes, cudaMemcpyDeviceToDevice, st_));
+      impl_->init_stage(sid, reinit_seed, f.w);
+      if (want_red) {
+        if (fp64())
+          k::sum_sq_diff(static_cast<const double*>(tmp), static_cast<const double*>(f.w), f.n, red_dev, red_, st_);
+        else
+          k::sum_sq_diff(static_cast<const float*>(tmp), static_cast<const float*>(f.w), f.n, red_dev, red_, st_);
+      }
+    } else if (mode == CKF_REC_COPY_PREV) {
+      if (want_red) {
+        if (fp64())
+          k::sum_sq_diff(static_cast<const double*>(f.w), static_cast<const double*>(p.w), f.n, red_dev, red_, st_);
+        else
+          k::sum_sq_diff(static_cast<const float*>(f.w), static_cast<const float*>(p.w), f.n, red_dev, red_, st_);
+      }
+      CKF_CUDA(cudaMemcpyAsync(f.w, p.w, bytes, cudaMemcpyDeviceToDevice, st_));
+    } else {
+      if (fp64())
+        k::recover(static_cast<const double*>(p.w), static_cast<const double*>(n.w), static_cast<double*>(f.w), f.n,
+                   op, on, red_dev, red_, st_);
+      else
+        k::recover(static_cast<const float*>(p.w), static_cast<const float*>(n.w), static_cast<float*>(f.w), f.n, op,
+                   on, red_dev, red_, st_);
+    }
+    if (moments == CKF_MOM_AVERAGED && mode == CKF_REC_CHECKFREE) {
+      // omega-weighted moments, step = min (trainer.cpp:263-269)
+      const double wp = p.omega, wn = n.omega;
+      if (fp64()) {
+        k::weighted_or_uniform(static_cast<const double*>(p.m), static_cast<const double*>(n.m),
+                               static_cast<double*>(f.m), f.n, wp, wn, st_);
+        k::weighted_or_uniform(static_cast<const double*>(p.v), static_cast<const double*>(n.v),
+                               static_cast<double*>(f.v), f.n, wp, wn, st_);
+      } else {
+        k::weighted_or_uniform(static_cast<const float*>(p.m), static_cast<const float*>(n.m),
+                               static_cast<float*>(f.m), f.n, wp, wn, st_);
+        k::weighted_or_uniform(static_cast<const float*>(p.v), static_cast<const float*>(n.v),
+                               static_cast<float*>(f.v), f.n, wp, wn, st_);
+      }
+      f.step = std::min(p.step, n.step);
+    } else {
+      CKF_CUDA(cudaMemsetAsync(f.m, 0, bytes, st_));
+      CKF_CUDA(cudaMemsetAsync(f.v, 0, bytes, st_));
+      f.step = 0;
+    }
+  }
+  CKF_CUDA(cudaMemsetAsync(f.g, 0, bytes, st_));
+  if (f.wlp) k::convert(static_cast<const float*>(f.w), f.wlp, f.n, st_);
+  CKF_CUDA(cudaEventRecord(ev1_, st_));
+  f.lr = lr_bump * f.lr;  // bump_lr (recovery.cpp:75-78), failed stage only
+  f.omega = 0.0;          // trainer.cpp:276
+  if (want_red) CKF_CUDA(cudaMemcpyAsync(&rep.reduction_error, red_dev, sizeof(double), cudaMemcpyDeviceToHost, st_));
+  CKF_CUDA(cudaStreamSynchronize(st_));
+  float ms = 0.f;
+  CKF_CUDA(cudaEventElapsedTime(&ms, ev0_, ev1_));
+  rep.latency_ms = ms;
+  return rep;
+}
+
+// ------------------------------------------------------------------ state exchange
+void Engine::export_group(ParamGroup& g, double* w, double* m, double* v) {
+  CKF_CUDA(cudaSetDevice(d_.device));
+  if (!g.owned) raise(3, "parameter group is not resident on this rank");
+  void* srcs[3] = {g.w, g.m, g.v};
+  double* dsts[3] = {w, m, v};
+  for (int i = 0; i < 3; ++i) {
+    if (!dsts[i]) continue;
+    if (fp64()) {
+      CKF_CUDA(cudaMemcpyAsync(dsts[i], srcs[i], g.n * 8, cudaMemcpyDeviceToHost, st_));
+    } else {
+      double* tmp = static_cast<double*>(ws(g.n * 8, 3));
+      k::convert(static_cast<const float*>(srcs[i]), tmp, g.n, st_);
+      CKF_CUDA(cudaMemcpyAsync(dsts[i], tmp, g.n * 8, cudaMemcpyDeviceToHost, st_));
+    }
+    CKF_CUDA(cudaStreamSynchronize(st_));
+  }
+}
+
+void Engine::import_group(ParamGroup& g, const double* w, const double* m, const double* v) {
+  CKF_CUDA(cudaSetDevice(d_.device));
+  if (!g.owned) raise(3, "parameter group is not resident on this rank");
+  void* dsts[3] = {g.w, g.m, g.v};
+  const double* srcs[3] = {w, m, v};
+  for (int i = 0; i < 3; ++i) {
+    if (!srcs[i]) continue;
+    if (fp64()) {
+      CKF_CUDA(cudaMemcpyAsync(dsts[i], srcs[i], g.n * 8, cudaMemcpyHostToDevice, st_));
+    } else {
+      double* tmp = static_cast<double*>(ws(g.n * 8, 3));
+      CKF_CUDA(cudaMemcpyAsync(tmp, srcs[i], g.n * 8, cudaMemcpyHostToDevice, st_));
+      k::convert(tmp, static_cast<float*>(dsts[i]), g.n, st_);
+    }
+    CKF_CUDA(cudaStreamSynchronize(st_));
+  }
+  if (w && g.wlp) k::convert(static_cast<const float*>(g.w), g.wlp, g.n, st_);
+  CKF_CUDA(cudaStreamSynchronize(st_));
+}
+
+}  // namespace ckf

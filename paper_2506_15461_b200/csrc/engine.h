@@ -1,0 +1,152 @@
+// Device-resident CheckFree / CheckFree+ engine (internal C++; exported only
+// through include/ckf.h).
+//
+// One Engine per GPU.  It owns the master weights, gradient accumulators and
+// Adam moments of the stages placed on its GPU (plus the edge layers when it
+// hosts stage 1 / stage s), runs pipeline::run_iteration semantics
+// (src/pipeline.cpp:58-95) and the recovery path (src/recovery.cpp:57-126,
+// src/trainer.cpp:196-282).  Stage activations cross GPUs over NCCL
+// send/recv when the placement spans ranks.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <vector>
+
+#include "../../include/ckf.h"
+#include "common.cuh"
+#include "kernels.h"
+
+namespace ckf {
+
+struct Range {
+  size_t first = 0, last = 0;  // 1-based inclusive (model.hpp:24-28)
+  size_t count() const { return last - first + 1; }
+};
+
+struct Desc {
+  int block = CKF_BLOCK_MLP;
+  int prec = CKF_FP64;
+  int act = CKF_ACT_TANH;
+  int task = CKF_TASK_REGRESSION;
+  size_t in = 16, hid = 64, d = 32, out = 16, L = 8, s = 4, heads = 1, T = 1, max_rows = 256;
+  int device = 0;
+  std::vector<Range> part;
+};
+
+// Flat buffers of one parameter group (a stage or an edge layer).  The
+// master copy `w` has the engine's master dtype (fp64 in FP64 mode, fp32
+// otherwise); `wlp` is the bf16 shadow the tensor-core GEMMs read.
+struct ParamGroup {
+  size_t n = 0;
+  bool owned = true;
+  void* w = nullptr;
+  void* g = nullptr;
+  void* m = nullptr;
+  void* v = nullptr;
+  __nv_bfloat16* wlp = nullptr;
+  long step = 0;
+  double omega = 0.0;
+  double lr = 3e-4;
+};
+
+class Engine;
+
+// Block-specific arithmetic (residual MLP of model.hpp:55-60, or LLaMA).
+struct BlockImpl {
+  explicit BlockImpl(Engine* e) : eng(e) {}
+  virtual ~BlockImpl() = default;
+  virtual size_t stage_params(int sid) const = 0;
+  virtual size_t embed_params() const = 0;
+  virtual size_t deembed_params() const = 0;
+  // Fills master weights on the device (init_model streams, model.cpp:159-197).
+  virtual void init_stage(int sid, uint64_t seed, void* w) = 0;
+  virtual void init_edges(uint64_t seed, void* embed, void* deembed) = 0;
+  // One microbatch along `order`: forward, loss into *loss_dev (device double),
+  // and, when train, backward accumulating into the groups' g buffers.
+  virtual void microbatch(const int* order, const void* x, const void* y, size_t rows, bool train,
+                          double* loss_dev) = 0;
+  // Predictions of forward(order, x) (MLP) into a device buffer of rows*out.
+  virtual void predict(const int* order, const void* x, size_t rows, void* pred) = 0;
+  Engine* eng;
+};
+
+class Engine {
+ public:
+  explicit Engine(const ckf_model_desc& d);
+  ~Engine();
+
+  const Desc& desc() const { return d_; }
+  bool fp64() const { return d_.prec == CKF_FP64; }
+  size_t master_bytes() const { return fp64() ? 8 : 4; }
+  cudaStream_t stream() const { return st_; }
+  ReduceScratch& scratch() { return red_; }
+
+  void init(uint64_t seed, double lr);
+  void run_iteration(const int* orders, int m, const void* x, const void* y, size_t rows, bool on_device,
+                     long iteration, double* loss, double* omegas);
+  double eval_loss(const int* order, const void* x, const void* y, size_t rows, bool on_device);
+  void predict(const int* order, const double* x_host, size_t rows, double* pred_host);
+  // device-side variants used by the trainer's data path
+  void predict_device(const int* order, const void* x_dev, size_t rows, void* pred_dev);
+
+  void refresh_edge_replicas();
+  void kill_stage(int sid);
+  ckf_recovery_report recover_stage(int sid, int mode, int moments, double lr_bump, uint64_t reinit_seed,
+                                    bool want_reduction_error);
+
+  void export_group(ParamGroup& g, double* w, double* m, double* v);
+  void import_group(ParamGroup& g, const double* w, const double* m, const double* v);
+
+  ParamGroup& stage(int sid) { return stages_.at(static_cast<size_t>(sid - 1)); }
+  ParamGroup& embed() { return embed_; }
+  ParamGroup& deembed() { return deembed_; }
+  double edge_lr = 3e-4;
+
+  // placement (multi-GPU): rank owning each stage; edges follow stages 1 and s
+  int rank() const { return rank_; }
+  int owner_of_stage(int sid) const { return stage_rank_.empty() ? 0 : stage_rank_[static_cast<size_t>(sid - 1)]; }
+  int owner_of_embed() const { return owner_of_stage(1); }
+  int owner_of_deembed() const { return owner_of_stage(static_cast<int>(d_.s)); }
+  bool mine(int owner) const { return owner == rank_; }
+  void attach_comm(const void* uid, int nranks, int rank, const int* stage_rank);
+  // move `count` elements of `buf` (device, master or activation dtype bytes) from rank src to rank dst
+  void hop(void* buf, size_t bytes, int src, int dst);
+
+  // device workspace (grows on demand, reused across calls)
+  void* ws(size_t bytes, int slot);
+  double* dev_scalars() { return scal_; }  // small device double array (losses, omegas)
+
+ private:
+  void alloc_group(ParamGroup& g, size_t n, bool lowp);
+  void free_group(ParamGroup& g);
+  void adam_group(ParamGroup& g, double lr, double gscale, double* omega_dev);
+
+  Desc d_;
+  cudaStream_t st_ = nullptr;
+  ReduceScratch red_;
+  std::vector<ParamGroup> stages_;
+  ParamGroup embed_, deembed_;
+  void* rep_embed_ = nullptr;   // CheckFree+ replica of E held by stage 2's GPU
+  void* rep_deembed_ = nullptr; // replica of E^-1 held by stage s-1's GPU
+  long replica_staleness_ = -1; // recovery.hpp:57-61
+  std::unique_ptr<BlockImpl> impl_;
+  std::vector<void*> ws_;
+  std::vector<size_t> ws_size_;
+  double* scal_ = nullptr;
+  int rank_ = 0, nranks_ = 1;
+  std::vector<int> stage_rank_;
+  void* comm_ = nullptr;  // ncclComm_t
+  cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
+  friend struct MlpBlock;
+  friend struct LlamaBlock;
+};
+
+std::unique_ptr<BlockImpl> make_mlp_block(Engine* e);
+std::unique_ptr<BlockImpl> make_llama_block(Engine* e);
+
+std::vector<Range> even_partition(size_t layers, size_t stages);
+
+}  // namespace ckf

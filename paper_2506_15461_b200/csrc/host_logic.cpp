@@ -1,0 +1,321 @@
+// Host control logic (see host_logic.h).  Bit-exact restatement of the
+// reference's integer / host-double logic; checked against the reference's
+// golden traces and schedules in tests/test_host_logic.py.
+#include "host_logic.h"
+
+#include <algorithm>
+#include <cstdio>
+#include <fstream>
+#include <set>
+
+namespace ckf::host {
+
+namespace {
+std::string fmt17(double v) {
+  char b[64];
+  std::snprintf(b, sizeof(b), "%.17g", v);
+  return b;
+}
+}  // namespace
+
+double hourly_to_per_iteration(double p_hour, double iter_s) {
+  // failures.cpp:57-61
+  if (p_hour < 0.0 || p_hour >= 1.0) fail(1, "p_hour must lie in [0, 1)");
+  if (iter_s <= 0.0) fail(1, "iteration_seconds must be positive");
+  return 1.0 - std::pow(1.0 - p_hour, iter_s / 3600.0);
+}
+
+Trace generate_trace(uint64_t seed, double p_hour, double iter_s, long n_iters, std::vector<int> stages) {
+  // failures.cpp:63-82: each (iteration, stage) fails iff unit_at(seed, iter, stage) < p_iter
+  for (int s : stages)
+    if (s < 1) fail(1, "stage ids are 1-based");
+  if (n_iters <= 0) fail(1, "num_iterations must be positive");
+  Trace t;
+  t.seed = seed;
+  t.p_hour = p_hour;
+  t.iter_s = iter_s;
+  t.stages = stages;
+  const double p = hourly_to_per_iteration(p_hour, iter_s);
+  std::sort(stages.begin(), stages.end());
+  for (long it = 1; it <= n_iters; ++it)
+    for (int st : stages)
+      if (unit_at(seed, static_cast<uint64_t>(it), static_cast<uint64_t>(st)) < p) t.events.push_back({it, st});
+  return t;
+}
+
+std::string serialize_trace(const Trace& t) {
+  // failures.cpp:84-95
+  std::ostringstream o;
+  o << "checkfree-trace v1 seed=" << t.seed << " p_hour=" << fmt17(t.p_hour) << " iter_s=" << fmt17(t.iter_s)
+    << " stages=";
+  for (size_t i = 0; i < t.stages.size(); ++i) o << (i ? "," : "") << t.stages[i];
+  o << '\n';
+  for (const auto& e : t.events) o << e.iteration << ',' << e.stage << '\n';
+  return o.str();
+}
+
+void validate_trace(const Trace& t) {
+  // failures.cpp:30-54 (FailureRateSpec::validate + FailureTrace::validate)
+  if (t.p_hour < 0.0 || t.p_hour >= 1.0) fail(1, "p_hour must lie in [0, 1)");
+  for (int s : t.stages)
+    if (s < 1) fail(1, "stage ids are 1-based");
+  if (t.iter_s <= 0.0) fail(1, "iteration_seconds must be positive");
+  std::set<int> eligible(t.stages.begin(), t.stages.end());
+  std::set<std::pair<long, int>> seen;
+  long prev = 0;
+  for (const auto& e : t.events) {
+    if (e.iteration < 1) fail(1, "trace iterations are 1-based");
+    if (e.iteration < prev) fail(1, "trace events must be sorted by iteration");
+    if (e.stage < 1) fail(1, "stage ids are 1-based");
+    if (!eligible.count(e.stage)) fail(1, "trace event targets stage " + std::to_string(e.stage) + " outside the eligible set");
+    if (!seen.insert({e.iteration, e.stage}).second)
+      fail(1, "duplicate event for stage " + std::to_string(e.stage) + " at iteration " + std::to_string(e.iteration));
+    prev = e.iteration;
+  }
+}
+
+Trace parse_trace(const std::string& text, const std::string& ctx) {
+  // failures.cpp:97-155; errors are ParseError (code 4)
+  std::istringstream in(text);
+  std::string line;
+  if (!std::getline(in, line)) fail(4, ctx + ":1: empty trace file");
+  Trace t;
+  {
+    std::istringstream h(line);
+    std::string magic, ver, kv;
+    h >> magic >> ver;
+    if (magic != "checkfree-trace" || ver != "v1") fail(4, ctx + ":1: expected header 'checkfree-trace v1'");
+    while (h >> kv) {
+      const auto eq = kv.find('=');
+      if (eq == std::string::npos) fail(4, ctx + ":1: malformed header field '" + kv + "'");
+      const std::string k = kv.substr(0, eq), v = kv.substr(eq + 1);
+      try {
+        if (k == "seed") {
+          t.seed = std::stoull(v);
+        } else if (k == "p_hour") {
+          t.p_hour = std::stod(v);
+        } else if (k == "iter_s") {
+          t.iter_s = std::stod(v);
+        } else if (k == "stages") {
+          std::istringstream ls(v);
+          std::string tok;
+          while (std::getline(ls, tok, ','))
+            if (!tok.empty()) t.stages.push_back(std::stoi(tok));
+        } else {
+          fail(4, ctx + ":1: unknown header field '" + k + "'");
+        }
+      } catch (const std::invalid_argument&) {
+        fail(4, ctx + ":1: invalid value for '" + k + "'");
+      } catch (const std::out_of_range&) {
+        fail(4, ctx + ":1: value out of range for '" + k + "'");
+      }
+    }
+  }
+  size_t ln = 1;
+  while (std::getline(in, line)) {
+    ++ln;
+    if (line.empty()) continue;
+    long it = 0;
+    int st = 0;
+    if (std::sscanf(line.c_str(), "%ld,%d", &it, &st) != 2) fail(4, ctx + ":" + std::to_string(ln) + ": expected 'iteration,stage'");
+    t.events.push_back({it, st});
+  }
+  try {
+    validate_trace(t);
+  } catch (const HostError& e) {
+    fail(4, ctx + ": " + e.what());
+  }
+  return t;
+}
+
+std::vector<Event> consecutive_conflicts(const Trace& t) {
+  // failures.cpp:171-184
+  std::vector<Event> out;
+  size_t i = 0;
+  while (i < t.events.size()) {
+    size_t j = i;
+    while (j < t.events.size() && t.events[j].iteration == t.events[i].iteration) ++j;
+    std::set<int> st;
+    for (size_t q = i; q < j; ++q) st.insert(t.events[q].stage);
+    for (int s : st)
+      if (st.count(s + 1)) out.push_back({t.events[i].iteration, s});
+    i = j;
+  }
+  return out;
+}
+
+std::vector<int> standard_order(int s) {
+  std::vector<int> o(static_cast<size_t>(s));
+  for (int i = 0; i < s; ++i) o[static_cast<size_t>(i)] = i + 1;
+  return o;
+}
+
+std::vector<int> swapped_order(int s) {
+  // pipeline.cpp:18-26
+  if (s < 4) fail(1, "swapped order requires at least 4 stages (first and last pairs must be disjoint)");
+  auto o = standard_order(s);
+  std::swap(o[0], o[1]);
+  std::swap(o[static_cast<size_t>(s - 2)], o[static_cast<size_t>(s - 1)]);
+  return o;
+}
+
+std::vector<int> build_schedule(int m, bool swapped_half, int s) {
+  if (m < 1) fail(1, "microbatch count must be positive");
+  if (swapped_half && m % 2 != 0) fail(1, "swapped_half schedule requires an even microbatch count");
+  std::vector<int> out;
+  for (int k = 0; k < m; ++k) {
+    auto o = swapped_half && k % 2 == 0 ? swapped_order(s) : standard_order(s);
+    out.insert(out.end(), o.begin(), o.end());
+  }
+  return out;
+}
+
+// ------------------------------------------------------------------ config
+Config Config::from_kv(const std::string& text) {
+  Config c;
+  std::stringstream ss(text);
+  std::string item;
+  std::map<std::string, std::string> kv;
+  while (std::getline(ss, item, ';')) {
+    // also accept newline-separated "key = value" (config.resolved format)
+    std::stringstream ls(item);
+    std::string line;
+    while (std::getline(ls, line, '\n')) {
+      if (line.empty() || line[0] == '#') continue;
+      const auto eq = line.find('=');
+      if (eq == std::string::npos) fail(1, "malformed config item '" + line + "'");
+      auto trim = [](std::string s) {
+        const auto a = s.find_first_not_of(" \t"), b = s.find_last_not_of(" \t\r");
+        return a == std::string::npos ? std::string() : s.substr(a, b - a + 1);
+      };
+      kv[trim(line.substr(0, eq))] = trim(line.substr(eq + 1));
+    }
+  }
+  auto U = [&](const char* k, size_t& v) { if (kv.count(k)) v = std::stoul(kv[k]); };
+  auto L_ = [&](const char* k, long& v) { if (kv.count(k)) v = std::stol(kv[k]); };
+  auto D = [&](const char* k, double& v) { if (kv.count(k)) v = std::stod(kv[k]); };
+  auto S = [&](const char* k, std::string& v) { if (kv.count(k)) v = kv[k]; };
+  try {
+    S("block", c.block);
+    S("precision", c.precision);
+    U("input-dim", c.input_dim);
+    U("hidden-dim", c.hidden_dim);
+    U("model-dim", c.model_dim);
+    U("output-dim", c.output_dim);
+    U("layers", c.layers);
+    U("stages", c.stages);
+    U("heads", c.heads);
+    U("seq-len", c.seq_len);
+    if (kv.count("vocab")) c.input_dim = c.output_dim = std::stoul(kv["vocab"]);
+    if (kv.count("ffn")) c.hidden_dim = std::stoul(kv["ffn"]);
+    S("activation", c.activation);
+    S("task", c.task);
+    S("strategy", c.strategy);
+    L_("checkpoint-interval", c.checkpoint_interval);
+    D("lr-bump", c.lr_bump);
+    S("recovered-moments", c.recovered_moments);
+    S("trace", c.trace_path);
+    D("p-hour", c.p_hour);
+    D("p-iter", c.p_iter);
+    D("iter-seconds", c.iter_seconds);
+    S("eligible", c.eligible);
+    L_("iters", c.iters);
+    U("batch", c.batch);
+    if (kv.count("microbatches")) c.microbatches = std::stoi(kv["microbatches"]);
+    D("lr", c.lr);
+    D("target-loss", c.target_loss);
+    L_("eval-interval", c.eval_interval);
+    U("val-size", c.val_size);
+    if (kv.count("seed")) c.seed = std::stoull(kv["seed"]);
+    S("schedule", c.schedule);
+    L_("swap-from", c.swap_from);
+    if (kv.count("device")) c.device = std::stoi(kv["device"]);
+  } catch (const std::logic_error& e) {
+    fail(1, std::string("invalid config value: ") + e.what());
+  }
+  return c;
+}
+
+bool Config::swapped_schedule() const {
+  if (schedule == "standard") return false;
+  if (schedule == "swapped-half") return true;
+  return strategy == "checkfree-plus";  // experiment.cpp:64-69
+}
+
+bool Config::neighbor_based() const {
+  return strategy == "checkfree" || strategy == "checkfree-plus" || strategy == "reinit-random" ||
+         strategy == "reinit-copy" || strategy == "reinit-uniform-avg";  // recovery.cpp:44-55
+}
+
+std::vector<int> Config::resolved_eligible() const {
+  // experiment.cpp:71-85
+  const int s = static_cast<int>(stages);
+  std::vector<int> mid, all;
+  for (int i = 2; i < s; ++i) mid.push_back(i);
+  for (int i = 1; i <= s; ++i) all.push_back(i);
+  if (eligible == "intermediate") return mid;
+  if (eligible == "all") return all;
+  if (strategy == "checkfree" || strategy == "reinit-random" || strategy == "reinit-copy" ||
+      strategy == "reinit-uniform-avg")
+    return mid;
+  return all;
+}
+
+void Config::validate() const {
+  // experiment.cpp:34-62 plus the model checks (model.cpp:80-97)
+  static const std::set<std::string> kinds = {"no-failures", "checkpointing", "redundant", "checkfree",
+                                              "checkfree-plus", "reinit-random", "reinit-copy", "reinit-uniform-avg"};
+  if (!kinds.count(strategy)) fail(1, "unknown strategy '" + strategy + "'");
+  if (block != "mlp" && block != "llama") fail(1, "block must be mlp|llama");
+  if (precision != "fp64" && precision != "fp32" && precision != "bf16") fail(1, "precision must be fp64|fp32|bf16");
+  if (activation != "tanh" && activation != "relu" && activation != "identity")
+    fail(1, "unknown activation '" + activation + "' (expected tanh|relu|identity)");
+  if (task != "regression" && task != "classification")
+    fail(1, "unknown task '" + task + "' (expected regression|classification)");
+  if (input_dim == 0 || hidden_dim == 0 || model_dim == 0 || output_dim == 0 || layers == 0)
+    fail(1, "model dimensions and layer count must be positive");
+  if (stages < 1 || stages > layers) fail(1, "num_stages must lie in [1, num_layers]");
+  if (stages < 2) fail(1, "experiments need a pipeline of at least 2 stages");
+  if (strategy == "checkpointing" && checkpoint_interval <= 0) fail(1, "checkpoint interval must be positive");
+  if (lr_bump <= 0.0) fail(1, "lr_bump must be positive");
+  if (iters <= 0) fail(1, "total_iterations must be positive");
+  if (batch == 0 || microbatches <= 0 || batch % static_cast<size_t>(microbatches) != 0)
+    fail(1, "batch size must be a positive multiple of the microbatch count");
+  if (lr <= 0.0) fail(1, "learning rate must be positive");
+  if (eval_interval <= 0) fail(1, "eval_interval must be positive");
+  if (val_size == 0) fail(1, "validation set must be non-empty");
+  if (p_iter >= 1.0) fail(1, "p_iter must lie in [0, 1)");
+  if (p_hour < 0.0 || p_hour >= 1.0) fail(1, "p_hour must lie in [0, 1)");
+  if (iter_seconds <= 0.0) fail(1, "iteration_seconds must be positive");
+  if (schedule != "auto" && schedule != "standard" && schedule != "swapped-half")
+    fail(1, "schedule_mode must be auto|standard|swapped-half");
+  if (eligible != "auto" && eligible != "intermediate" && eligible != "all")
+    fail(1, "eligible must be auto|intermediate|all");
+  if (swapped_schedule()) {
+    if (stages < 4) fail(1, "the swapped schedule requires at least 4 stages");
+    if (microbatches % 2 != 0) fail(1, "the swapped schedule requires an even microbatch count");
+  }
+  if (neighbor_based() && layers % stages != 0)
+    fail(1, "neighbor-based recovery requires a uniform stage partition");
+  if (block == "llama") {
+    if (model_dim % heads != 0) fail(1, "model_dim must be divisible by heads");
+    if (precision == "fp64") fail(1, "the LLaMA block runs in fp32 (parity) or bf16");
+  } else if (precision == "bf16") {
+    fail(1, "the residual-MLP parity block runs in fp64 or fp32");
+  }
+}
+
+Trace Config::resolve_trace(uint64_t s) const {
+  // experiment.cpp:102-115
+  if (!trace_path.empty()) {
+    std::ifstream in(trace_path, std::ios::binary);
+    if (!in) fail(1, "cannot open trace file '" + trace_path + "'");
+    std::ostringstream b;
+    b << in.rdbuf();
+    return parse_trace(b.str(), trace_path);
+  }
+  if (p_iter >= 0.0) return generate_trace(s, p_iter, 3600.0, iters, resolved_eligible());
+  return generate_trace(s, p_hour, iter_seconds, iters, resolved_eligible());
+}
+
+}  // namespace ckf::host

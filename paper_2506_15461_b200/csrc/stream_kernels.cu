@@ -1,0 +1,553 @@
+// Bandwidth-bound kernels of the engine: counter-RNG init, activations,
+// losses, fused Adam + omega, omega-weighted recovery, reductions.
+//
+// All reductions are deterministic (fixed grid per n, fixed fold order, no
+// float atomics) -- the GPU analogue of the reference's fixed-order blocked
+// reductions (kernels.hpp:21-23, kernels_omp.cpp:135-206).  fp64 paths use
+// explicit round-to-nearest intrinsics wherever the reference's expression
+// order should be reproduced without FMA contraction.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace ckf::k {
+namespace {
+
+constexpr int kThreads = 256;
+
+unsigned reduce_grid(size_t n) {
+  size_t g = (n + kThreads * 8 - 1) / (kThreads * 8);
+  if (g < 1) g = 1;
+  if (g > ReduceScratch::kMaxReduceBlocks) g = ReduceScratch::kMaxReduceBlocks;
+  return static_cast<unsigned>(g);
+}
+
+__global__ void fold_partials(const double* __restrict__ partials, int n, double* __restrict__ out) {
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += 1024) acc += partials[i];
+  acc = block_sum<double, 1024>(acc);
+  if (threadIdx.x == 0) *out = acc;
+}
+
+void finish(ReduceScratch& sc, unsigned g, double* out, cudaStream_t s) {
+  fold_partials<<<1, 1024, 0, s>>>(sc.partials, static_cast<int>(g), out);
+  CKF_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------- RNG init
+template <typename T>
+__global__ void uniform_kernel(T* __restrict__ out, size_t n, uint64_t key, double lo, double hi, uint64_t c0) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    out[i] = static_cast<T>(counter_uniform_at(key, c0 + i + 1, lo, hi));
+}
+
+// ---------------------------------------------------------------- activations
+template <typename T>
+__device__ __forceinline__ T act_apply(int act, T a) {
+  if (act == kTanh) return tanh(a);
+  if (act == kRelu) return a > T(0) ? a : T(0);
+  return a;
+}
+
+template <typename T>
+__global__ void act_fwd_kernel(int act, const T* __restrict__ in, T* __restrict__ out, size_t n) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    out[i] = act_apply(act, in[i]);
+}
+
+template <typename T>
+__global__ void act_bwd_kernel(int act, const T* __restrict__ z, const T* __restrict__ dz, T* __restrict__ da,
+                               size_t n) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const T zi = z[i];
+    if (act == kTanh) {
+      // da = dz * (1 - z*z)  (kernels_serial.cpp:93), no contraction in fp64
+      if constexpr (sizeof(T) == 8)
+        da[i] = __dmul_rn(dz[i], __dsub_rn(1.0, __dmul_rn(zi, zi)));
+      else
+        da[i] = dz[i] * (1.0f - zi * zi);
+    } else if (act == kRelu) {
+      da[i] = zi > T(0) ? dz[i] : T(0);
+    } else {
+      da[i] = dz[i];
+    }
+  }
+}
+
+template <typename T>
+__global__ void add_kernel(T* __restrict__ x, const T* __restrict__ y, size_t n) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    x[i] += y[i];
+}
+
+template <typename T>
+__global__ void axpy_kernel(T alpha, const T* __restrict__ x, T* __restrict__ y, size_t n) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    if constexpr (sizeof(T) == 8)
+      y[i] = __dadd_rn(y[i], __dmul_rn(alpha, x[i]));
+    else
+      y[i] += alpha * x[i];
+  }
+}
+
+template <typename T>
+__global__ void scale_kernel(T alpha, T* __restrict__ x, size_t n) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    x[i] *= alpha;
+}
+
+template <typename T>
+__global__ void fill_kernel(T* __restrict__ x, T v, size_t n) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    x[i] = v;
+}
+
+template <typename A, typename B>
+__global__ void convert_kernel(const A* __restrict__ in, B* __restrict__ out, size_t n) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    out[i] = static_cast<B>(static_cast<float>(in[i]));
+}
+template <>
+__global__ void convert_kernel<double, double>(const double* __restrict__ in, double* __restrict__ out, size_t n) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    out[i] = in[i];
+}
+template <>
+__global__ void convert_kernel<float, double>(const float* __restrict__ in, double* __restrict__ out, size_t n) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    out[i] = static_cast<double>(in[i]);
+}
+template <>
+__global__ void convert_kernel<double, float>(const double* __restrict__ in, float* __restrict__ out, size_t n) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    out[i] = static_cast<float>(in[i]);
+}
+
+// ---------------------------------------------------------------- reductions
+template <typename T>
+__global__ void sumsq_kernel(const T* __restrict__ x, const T* __restrict__ y, size_t n,
+                             double* __restrict__ partials) {
+  double acc = 0.0;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const double d = y ? static_cast<double>(x[i]) - static_cast<double>(y[i]) : static_cast<double>(x[i]);
+    acc += d * d;
+  }
+  acc = block_sum<double, kThreads>(acc);
+  if (threadIdx.x == 0) partials[blockIdx.x] = acc;
+}
+
+// MSE: per-row partial sums, rows folded in order; dpred = 2 d / (rows*cols)
+template <typename T>
+__global__ void mse_kernel(const T* __restrict__ pred, const T* __restrict__ tgt, size_t rows, size_t cols,
+                           T* __restrict__ dpred, double inv, double* __restrict__ partials) {
+  double acc = 0.0;
+  const size_t n = rows * cols;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const double d = static_cast<double>(pred[i]) - static_cast<double>(tgt[i]);
+    acc += d * d;
+    if (dpred) {
+      if constexpr (sizeof(T) == 8)
+        dpred[i] = __dmul_rn(__dmul_rn(2.0, d), inv);
+      else
+        dpred[i] = static_cast<T>(2.0 * d * inv);
+    }
+  }
+  acc = block_sum<double, kThreads>(acc);
+  if (threadIdx.x == 0) partials[blockIdx.x] = acc * inv;
+}
+
+// softmax cross-entropy, one warp per row
+template <typename T>
+__global__ void xent_kernel(const T* __restrict__ logits, const int* __restrict__ labels, size_t rows, size_t cols,
+                            T* __restrict__ dlog, double invb, double* __restrict__ row_loss) {
+  const size_t row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const T* l = logits + row * cols;
+  double mx = -INFINITY;
+  for (size_t j = lane; j < cols; j += 32) mx = fmax(mx, static_cast<double>(l[j]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  double den = 0.0;
+  for (size_t j = lane; j < cols; j += 32) den += exp(static_cast<double>(l[j]) - mx);
+  den = warp_sum(den);
+  const int y = labels[row];
+  if (lane == 0) row_loss[row] = -(static_cast<double>(l[y]) - mx - log(den));
+  if (dlog) {
+    for (size_t j = lane; j < cols; j += 32) {
+      const double p = exp(static_cast<double>(l[j]) - mx) / den;
+      dlog[row * cols + j] = static_cast<T>((p - (static_cast<int>(j) == y ? 1.0 : 0.0)) * invb);
+    }
+  }
+}
+
+__global__ void fold_rows(const double* __restrict__ row_loss, size_t rows, double invb, double* __restrict__ out) {
+  double acc = 0.0;
+  for (size_t i = threadIdx.x; i < rows; i += 1024) acc += row_loss[i];
+  acc = block_sum<double, 1024>(acc);
+  if (threadIdx.x == 0) *out = acc * invb;
+}
+
+// ---------------------------------------------------------------- Adam + omega
+// kernels_serial.cpp:133-144 with the 1/m gradient scale of pipeline.cpp:82
+// folded in, and omega = sum(g_eff^2) (model.cpp:396,411-413) in the same pass.
+template <typename T>
+__global__ void adam_kernel(T* __restrict__ w, T* __restrict__ m, T* __restrict__ v, T* __restrict__ g,
+                            __nv_bfloat16* __restrict__ wlp, size_t n, double lr, double bc1, double bc2,
+                            double gscale, int zero_grad, double* __restrict__ partials) {
+  constexpr double b1 = 0.9, b2 = 0.999, eps = 1e-8;
+  double acc = 0.0;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    if constexpr (sizeof(T) == 8) {
+      const double gi = __dmul_rn(g[i], gscale);
+      const double mi = __dadd_rn(__dmul_rn(b1, m[i]), __dmul_rn(1.0 - b1, gi));
+      const double vi = __dadd_rn(__dmul_rn(b2, v[i]), __dmul_rn(__dmul_rn(1.0 - b2, gi), gi));
+      const double mhat = __ddiv_rn(mi, bc1);
+      const double vhat = __ddiv_rn(vi, bc2);
+      const double wi = __dsub_rn(w[i], __ddiv_rn(__dmul_rn(lr, mhat), __dadd_rn(__dsqrt_rn(vhat), eps)));
+      m[i] = mi;
+      v[i] = vi;
+      w[i] = wi;
+      acc = __fma_rn(gi, gi, acc);
+      if (wlp) wlp[i] = __float2bfloat16(static_cast<float>(wi));
+    } else {
+      const float gi = static_cast<float>(g[i]) * static_cast<float>(gscale);
+      const float mi = 0.9f * static_cast<float>(m[i]) + 0.1f * gi;
+      const float vi = 0.999f * static_cast<float>(v[i]) + 0.001f * gi * gi;
+      const float mhat = mi / static_cast<float>(bc1);
+      const float vhat = vi / static_cast<float>(bc2);
+      const float wi = static_cast<float>(w[i]) - static_cast<float>(lr) * mhat / (sqrtf(vhat) + 1e-8f);
+      m[i] = mi;
+      v[i] = vi;
+      w[i] = wi;
+      acc += static_cast<double>(gi) * static_cast<double>(gi);
+      if (wlp) wlp[i] = __float2bfloat16(wi);
+    }
+    if (zero_grad) g[i] = T(0);
+  }
+  acc = block_sum<double, kThreads>(acc);
+  if (threadIdx.x == 0) partials[blockIdx.x] = acc;
+}
+
+// Vectorised fp32 variant: 16 B per stream per thread-iteration (the
+// Adam kernel is the largest per-iteration HBM consumer besides the GEMMs).
+__global__ void adam_f32x4_kernel(float4* __restrict__ w, float4* __restrict__ m, float4* __restrict__ v,
+                                  float4* __restrict__ g, __nv_bfloat162* __restrict__ wlp, size_t n4, float lr,
+                                  float rbc1, float rbc2, float gscale, int zero_grad,
+                                  double* __restrict__ partials) {
+  double acc = 0.0;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    float4 gg = g[i], mm = m[i], vv = v[i], ww = w[i];
+    float* gp = &gg.x;
+    float* mp = &mm.x;
+    float* vp = &vv.x;
+    float* wp = &ww.x;
+    float part = 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float gi = gp[j] * gscale;
+      mp[j] = 0.9f * mp[j] + 0.1f * gi;
+      vp[j] = 0.999f * vp[j] + 0.001f * gi * gi;
+      wp[j] = wp[j] - lr * (mp[j] * rbc1) / (sqrtf(vp[j] * rbc2) + 1e-8f);
+      part += gi * gi;
+    }
+    acc += static_cast<double>(part);
+    m[i] = mm;
+    v[i] = vv;
+    w[i] = ww;
+    if (wlp) {
+      wlp[2 * i] = __floats2bfloat162_rn(ww.x, ww.y);
+      wlp[2 * i + 1] = __floats2bfloat162_rn(ww.z, ww.w);
+    }
+    if (zero_grad) g[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  acc = block_sum<double, kThreads>(acc);
+  if (threadIdx.x == 0) partials[blockIdx.x] = acc;
+}
+
+// ---------------------------------------------------------------- recovery
+template <typename T>
+__global__ void recover_kernel(const T* __restrict__ wp, const T* __restrict__ wn, T* __restrict__ out, size_t n,
+                               double op, double on, double denom, int want_sq, double* __restrict__ partials) {
+  double acc = 0.0;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    T r;
+    if constexpr (sizeof(T) == 8) {
+      // (wp*Wp[i] + wn*Wn[i]) / denom exactly as recovery.cpp:71
+      r = __ddiv_rn(__dadd_rn(__dmul_rn(op, wp[i]), __dmul_rn(on, wn[i])), denom);
+    } else {
+      r = static_cast<float>(op) * wp[i] + static_cast<float>(on) * wn[i];  // op,on pre-normalised
+    }
+    if (want_sq) {
+      const double d = static_cast<double>(out[i]) - static_cast<double>(r);
+      acc += d * d;
+    }
+    out[i] = r;
+  }
+  if (want_sq) {
+    acc = block_sum<double, kThreads>(acc);
+    if (threadIdx.x == 0) partials[blockIdx.x] = acc;
+  }
+}
+
+// 128-bit streaming variant for fp32 (the recovery microbench path): each
+// thread moves 4 floats per stream with no reduction.
+__global__ void recover_f32x4_kernel(const float4* __restrict__ wp, const float4* __restrict__ wn,
+                                     float4* __restrict__ out, size_t n4, float a, float b) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const float4 p = __ldcs(wp + i);
+    const float4 q = __ldcs(wn + i);
+    float4 r;
+    r.x = fmaf(a, p.x, b * q.x);
+    r.y = fmaf(a, p.y, b * q.y);
+    r.z = fmaf(a, p.z, b * q.z);
+    r.w = fmaf(a, p.w, b * q.w);
+    __stcs(out + i, r);
+  }
+}
+
+template <typename T>
+__global__ void wavg_kernel(const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ out, size_t n,
+                            double wa, double wb, double denom, int uniform) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    if constexpr (sizeof(T) == 8) {
+      out[i] = uniform ? __dmul_rn(0.5, __dadd_rn(a[i], b[i]))
+                       : __ddiv_rn(__dadd_rn(__dmul_rn(wa, a[i]), __dmul_rn(wb, b[i])), denom);
+    } else {
+      out[i] = uniform ? 0.5f * (a[i] + b[i])
+                       : static_cast<float>((wa * static_cast<double>(a[i]) + wb * static_cast<double>(b[i])) / denom);
+    }
+  }
+}
+
+template <typename T>
+__global__ void poison_kernel(T* __restrict__ x, size_t n) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    x[i] = T(NAN);
+}
+
+}  // namespace
+
+// ================================================================ launchers
+template <typename T>
+void uniform(T* out, size_t n, uint64_t key, double lo, double hi, uint64_t c0, cudaStream_t s) {
+  if (!n) return;
+  uniform_kernel<T><<<grid_for(n, kThreads), kThreads, 0, s>>>(out, n, key, lo, hi, c0);
+  CKF_LAUNCH_CHECK();
+}
+
+template <typename T>
+void act_fwd(int act, const T* in, T* out, size_t n, cudaStream_t s) {
+  if (!n) return;
+  act_fwd_kernel<T><<<grid_for(n, kThreads), kThreads, 0, s>>>(act, in, out, n);
+  CKF_LAUNCH_CHECK();
+}
+
+template <typename T>
+void act_bwd(int act, const T* z, const T* dz, T* da, size_t n, cudaStream_t s) {
+  if (!n) return;
+  act_bwd_kernel<T><<<grid_for(n, kThreads), kThreads, 0, s>>>(act, z, dz, da, n);
+  CKF_LAUNCH_CHECK();
+}
+
+template <typename T>
+void add_inplace(T* x, const T* y, size_t n, cudaStream_t s) {
+  if (!n) return;
+  add_kernel<T><<<grid_for(n, kThreads), kThreads, 0, s>>>(x, y, n);
+  CKF_LAUNCH_CHECK();
+}
+
+template <typename T>
+void axpy(double alpha, const T* x, T* y, size_t n, cudaStream_t s) {
+  if (!n) return;
+  axpy_kernel<T><<<grid_for(n, kThreads), kThreads, 0, s>>>(static_cast<T>(alpha), x, y, n);
+  CKF_LAUNCH_CHECK();
+}
+
+template <typename T>
+void scale(double alpha, T* x, size_t n, cudaStream_t s) {
+  if (!n) return;
+  scale_kernel<T><<<grid_for(n, kThreads), kThreads, 0, s>>>(static_cast<T>(alpha), x, n);
+  CKF_LAUNCH_CHECK();
+}
+
+template <typename T>
+void fill(T* x, double v, size_t n, cudaStream_t s) {
+  if (!n) return;
+  fill_kernel<T><<<grid_for(n, kThreads), kThreads, 0, s>>>(x, static_cast<T>(v), n);
+  CKF_LAUNCH_CHECK();
+}
+
+template <typename A, typename B>
+void convert(const A* in, B* out, size_t n, cudaStream_t s) {
+  if (!n) return;
+  convert_kernel<A, B><<<grid_for(n, kThreads), kThreads, 0, s>>>(in, out, n);
+  CKF_LAUNCH_CHECK();
+}
+
+template <typename T>
+void sum_squares(const T* x, size_t n, double* out, ReduceScratch& sc, cudaStream_t s) {
+  const unsigned g = reduce_grid(n);
+  sumsq_kernel<T><<<g, kThreads, 0, s>>>(x, nullptr, n, sc.partials);
+  CKF_LAUNCH_CHECK();
+  finish(sc, g, out, s);
+}
+
+template <typename T>
+void sum_sq_diff(const T* x, const T* y, size_t n, double* out, ReduceScratch& sc, cudaStream_t s) {
+  const unsigned g = reduce_grid(n);
+  sumsq_kernel<T><<<g, kThreads, 0, s>>>(x, y, n, sc.partials);
+  CKF_LAUNCH_CHECK();
+  finish(sc, g, out, s);
+}
+
+template <typename T>
+void mse_loss_grad(const T* pred, const T* target, size_t rows, size_t cols, T* dpred, double* loss,
+                   ReduceScratch& sc, cudaStream_t s) {
+  const size_t n = rows * cols;
+  const unsigned g = reduce_grid(n);
+  mse_kernel<T><<<g, kThreads, 0, s>>>(pred, target, rows, cols, dpred, 1.0 / static_cast<double>(n),
+                                       sc.partials);
+  CKF_LAUNCH_CHECK();
+  finish(sc, g, loss, s);
+}
+
+template <typename T>
+void xent_loss_grad(const T* logits, const int* labels, size_t rows, size_t cols, T* dlogits, double* loss,
+                    ReduceScratch& sc, cudaStream_t s) {
+  // per-row losses need rows doubles of scratch; reuse partials when it fits
+  double* rl = sc.partials;
+  double* tmp = nullptr;
+  if (rows > static_cast<size_t>(ReduceScratch::kMaxReduceBlocks)) {
+    CKF_CUDA(cudaMallocAsync(&tmp, rows * sizeof(double), s));
+    rl = tmp;
+  }
+  const int rows_per_block = 8;
+  xent_kernel<T><<<static_cast<unsigned>((rows + rows_per_block - 1) / rows_per_block), 32 * rows_per_block, 0,
+                   s>>>(logits, labels, rows, cols, dlogits, 1.0 / static_cast<double>(rows), rl);
+  CKF_LAUNCH_CHECK();
+  fold_rows<<<1, 1024, 0, s>>>(rl, rows, 1.0 / static_cast<double>(rows), loss);
+  CKF_LAUNCH_CHECK();
+  if (tmp) CKF_CUDA(cudaFreeAsync(tmp, s));
+}
+
+template <typename T>
+void adam(T* w, T* m, T* v, T* g, __nv_bfloat16* wlp, size_t n, double lr, double bc1, double bc2,
+          double grad_scale, bool zero_grad, double* omega, ReduceScratch& sc, cudaStream_t s) {
+  const unsigned g_ = reduce_grid(n);
+  if constexpr (sizeof(T) == 4) {
+    const bool aligned = (reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(m) |
+                          reinterpret_cast<uintptr_t>(v) | reinterpret_cast<uintptr_t>(g) |
+                          reinterpret_cast<uintptr_t>(wlp)) % 16 == 0;
+    if (aligned && n % 4 == 0) {
+      const unsigned gv = reduce_grid(n / 4 * 2);
+      adam_f32x4_kernel<<<gv, kThreads, 0, s>>>(
+          reinterpret_cast<float4*>(w), reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v),
+          reinterpret_cast<float4*>(g), reinterpret_cast<__nv_bfloat162*>(wlp), n / 4, static_cast<float>(lr),
+          static_cast<float>(1.0 / bc1), static_cast<float>(1.0 / bc2), static_cast<float>(grad_scale),
+          zero_grad ? 1 : 0, sc.partials);
+      CKF_LAUNCH_CHECK();
+      finish(sc, gv, omega, s);
+      return;
+    }
+  }
+  adam_kernel<T><<<g_, kThreads, 0, s>>>(w, m, v, g, wlp, n, lr, bc1, bc2, grad_scale, zero_grad ? 1 : 0,
+                                         sc.partials);
+  CKF_LAUNCH_CHECK();
+  finish(sc, g_, omega, s);
+}
+
+template <typename T>
+void recover(const T* wp, const T* wn, T* out, size_t n, double op, double on, double* old_sq, ReduceScratch& sc,
+             cudaStream_t s) {
+  double a = op, b = on;
+  if (a + b == 0.0) a = b = 1.0;  // degenerate: uniform average (recovery.cpp:63-68)
+  const double denom = a + b;
+  if constexpr (sizeof(T) == 4) {
+    const float fa = static_cast<float>(a / denom), fb = static_cast<float>(b / denom);
+    const bool aligned = (reinterpret_cast<uintptr_t>(wp) | reinterpret_cast<uintptr_t>(wn) |
+                          reinterpret_cast<uintptr_t>(out)) % 16 == 0;
+    if (!old_sq && aligned && n % 4 == 0) {
+      const size_t n4 = n / 4;
+      unsigned g = grid_for(n4, kThreads, kNumSMs * 8);
+      recover_f32x4_kernel<<<g, kThreads, 0, s>>>(reinterpret_cast<const float4*>(wp),
+                                                  reinterpret_cast<const float4*>(wn),
+                                                  reinterpret_cast<float4*>(out), n4, fa, fb);
+      CKF_LAUNCH_CHECK();
+      return;
+    }
+    const unsigned g = reduce_grid(n);
+    recover_kernel<float><<<g, kThreads, 0, s>>>(wp, wn, out, n, fa, fb, 1.0, old_sq ? 1 : 0, sc.partials);
+    CKF_LAUNCH_CHECK();
+    if (old_sq) finish(sc, g, old_sq, s);
+  } else {
+    const unsigned g = reduce_grid(n);
+    recover_kernel<T><<<g, kThreads, 0, s>>>(wp, wn, out, n, a, b, denom, old_sq ? 1 : 0, sc.partials);
+    CKF_LAUNCH_CHECK();
+    if (old_sq) finish(sc, g, old_sq, s);
+  }
+}
+
+template <typename T>
+void weighted_or_uniform(const T* a, const T* b, T* out, size_t n, double op, double on, cudaStream_t s) {
+  if (!n) return;
+  wavg_kernel<T><<<grid_for(n, kThreads), kThreads, 0, s>>>(a, b, out, n, op, on, op + on, op + on == 0.0 ? 1 : 0);
+  CKF_LAUNCH_CHECK();
+}
+
+template <typename T>
+void poison(T* x, size_t n, cudaStream_t s) {
+  if (!n) return;
+  poison_kernel<T><<<grid_for(n, kThreads), kThreads, 0, s>>>(x, n);
+  CKF_LAUNCH_CHECK();
+}
+
+#define CKF_INST(T)                                                                                            \
+  template void uniform<T>(T*, size_t, uint64_t, double, double, uint64_t, cudaStream_t);                    \
+  template void act_fwd<T>(int, const T*, T*, size_t, cudaStream_t);                                         \
+  template void act_bwd<T>(int, const T*, const T*, T*, size_t, cudaStream_t);                               \
+  template void add_inplace<T>(T*, const T*, size_t, cudaStream_t);                                          \
+  template void axpy<T>(double, const T*, T*, size_t, cudaStream_t);                                         \
+  template void scale<T>(double, T*, size_t, cudaStream_t);                                                  \
+  template void fill<T>(T*, double, size_t, cudaStream_t);                                                   \
+  template void sum_squares<T>(const T*, size_t, double*, ReduceScratch&, cudaStream_t);                     \
+  template void sum_sq_diff<T>(const T*, const T*, size_t, double*, ReduceScratch&, cudaStream_t);           \
+  template void mse_loss_grad<T>(const T*, const T*, size_t, size_t, T*, double*, ReduceScratch&,            \
+                                 cudaStream_t);                                                               \
+  template void xent_loss_grad<T>(const T*, const int*, size_t, size_t, T*, double*, ReduceScratch&,         \
+                                  cudaStream_t);                                                              \
+  template void adam<T>(T*, T*, T*, T*, __nv_bfloat16*, size_t, double, double, double, double, bool,        \
+                        double*, ReduceScratch&, cudaStream_t);                                               \
+  template void recover<T>(const T*, const T*, T*, size_t, double, double, double*, ReduceScratch&,          \
+                           cudaStream_t);                                                                     \
+  template void weighted_or_uniform<T>(const T*, const T*, T*, size_t, double, double, cudaStream_t);        \
+  template void poison<T>(T*, size_t, cudaStream_t);
+
+CKF_INST(double)
+CKF_INST(float)
+template void fill<__nv_bfloat16>(__nv_bfloat16*, double, size_t, cudaStream_t);
+template void convert<double, double>(const double*, double*, size_t, cudaStream_t);
+template void convert<double, float>(const double*, float*, size_t, cudaStream_t);
+template void convert<float, double>(const float*, double*, size_t, cudaStream_t);
+template void convert<float, __nv_bfloat16>(const float*, __nv_bfloat16*, size_t, cudaStream_t);
+template void convert<__nv_bfloat16, float>(const __nv_bfloat16*, float*, size_t, cudaStream_t);
+
+}  // namespace ckf::k

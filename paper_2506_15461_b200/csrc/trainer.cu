@@ -1,0 +1,266 @@
+// The failure-injected training loop on the device-resident engine:
+// harness::Trainer (src/trainer.cpp:63-289) re-built around ckf::Engine.
+// Slots vs model iterations, post-step failure handling in ascending stage
+// order, adjacency -> unrecoverable, CheckFree+ replica refresh after every
+// step, lr bump / omega reset / moment policy -- all as in the reference.
+// Data: the teacher-student task of src/dataset.cpp:15-57 generated on the
+// GPU (counter-RNG inputs, teacher forward) for the MLP block; the LLaMA block
+// uses the counter-RNG token process of llama_block.cu.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <map>
+#include <sstream>
+
+#include "engine.h"
+#include "host_logic.h"
+
+namespace ckf {
+
+void argmax_rows(const void* pred, bool f64, size_t rows, size_t cols, int* out, cudaStream_t s);
+void llama_token_batch(uint64_t data_seed, uint64_t stream, uint64_t index, size_t rows, size_t T, size_t V,
+                       int* out, cudaStream_t s);
+
+namespace {
+
+constexpr uint64_t kSeedModel = 11, kSeedTask = 12, kSeedReinit = 13;  // trainer.cpp:22-24
+constexpr uint64_t kStreamTrain = 1, kStreamVal = 2, kStreamTeacher = 3;  // dataset.cpp:11-13
+
+ckf_model_desc make_desc(const host::Config& c) {
+  ckf_model_desc d{};
+  d.block = c.block == "llama" ? CKF_BLOCK_LLAMA : CKF_BLOCK_MLP;
+  d.precision = c.precision == "fp64" ? CKF_FP64 : c.precision == "fp32" ? CKF_FP32 : CKF_BF16;
+  d.activation = c.activation == "tanh" ? CKF_ACT_TANH : c.activation == "relu" ? CKF_ACT_RELU : CKF_ACT_IDENTITY;
+  d.task = c.task == "regression" ? CKF_TASK_REGRESSION : CKF_TASK_CLASSIFICATION;
+  d.input_dim = c.input_dim;
+  d.hidden_dim = c.hidden_dim;
+  d.model_dim = c.model_dim;
+  d.output_dim = c.output_dim;
+  d.num_layers = c.layers;
+  d.num_stages = c.stages;
+  d.n_heads = c.heads;
+  d.seq_len = c.seq_len;
+  d.partition = nullptr;
+  const size_t mb = c.batch / static_cast<size_t>(c.microbatches);
+  d.max_rows = d.block == CKF_BLOCK_MLP ? std::max(mb, c.val_size) : mb * c.seq_len;
+  d.device = c.device;
+  return d;
+}
+
+struct Batch {
+  void* x = nullptr;  // device: master dtype [rows x in] (MLP) or int32 tokens [rows x (T+1)] (LLaMA)
+  void* y = nullptr;  // device: targets (master dtype) or int32 labels; null for LLaMA
+  size_t rows = 0;
+};
+
+class Trainer {
+ public:
+  Trainer(const host::Config& c, const host::Trace& trace, uint64_t seed)
+      : c_(c), seed_(seed), desc_(make_desc(c)), model_(desc_) {
+    data_seed_ = host::derive_key(seed, kSeedTask);
+    model_.init(host::derive_key(seed, kSeedModel), c.lr);
+    if (desc_.block == CKF_BLOCK_MLP) {
+      teacher_ = std::make_unique<Engine>(desc_);
+      teacher_->init(host::derive_key(data_seed_, kStreamTeacher), 1.0);
+    }
+    for (const auto& e : trace.events) events_[e.iteration].push_back(e.stage);
+    for (auto& kv : events_) std::sort(kv.second.begin(), kv.second.end());
+    const int s = static_cast<int>(c.stages);
+    std_sched_ = host::build_schedule(c.microbatches, false, s);
+    if (c.swapped_schedule()) sw_sched_ = host::build_schedule(c.microbatches, true, s);
+    val_ = make_batch(kStreamVal, 0, c.val_size, 20);
+  }
+
+  std::string run() {
+    const bool cfp = c_.strategy == "checkfree-plus";
+    const int s = static_cast<int>(c_.stages);
+    const auto std_order = host::standard_order(s);
+    if (cfp) model_.refresh_edge_replicas();
+    {  // record_initial_eval (trainer.cpp:122-126)
+      Batch first = make_batch(kStreamTrain, 1, c_.batch, 22);
+      last_train_ = eval(first, std_order);
+      add_eval(0);
+    }
+    bool stopped = false;
+    long slots_run = 0;
+    for (long slot = 1; slot <= c_.iters && !stopped; ++slot) {
+      slots_run = slot;
+      const bool swap_now = !sw_sched_.empty() && slot > c_.swap_from;
+      Batch b = make_batch(kStreamTrain, static_cast<uint64_t>(model_iter_ + 1), c_.batch, 22);
+      std::vector<double> om(c_.stages);
+      model_.run_iteration(swap_now ? sw_sched_.data() : std_sched_.data(), c_.microbatches, b.x, b.y, b.rows,
+                           true, slot, &last_train_, om.data());
+      ++model_iter_;
+      if (cfp) model_.refresh_edge_replicas();
+      if (c_.strategy != "no-failures") {
+        auto ev = events_.find(slot);
+        if (ev != events_.end() && !handle_failures(slot, ev->second)) {
+          add_eval(slot);
+          stopped = true;
+          break;
+        }
+      }
+      if (slot % c_.eval_interval == 0 || slot == c_.iters) {
+        const double v = add_eval(slot);
+        if (c_.target_loss > 0.0 && v <= c_.target_loss) stopped = true;
+      }
+    }
+    if (evals_.empty() || evals_.back().first != slots_run) add_eval(slots_run);
+    return out_.str();
+  }
+
+ private:
+  // dataset.cpp:15-39 on the device: x ~ U[-1,1] keyed (data_seed, stream, index); y = teacher forward
+  Batch make_batch(uint64_t stream, uint64_t index, size_t rows, int slot) {
+    Batch b;
+    b.rows = rows;
+    cudaStream_t st = model_.stream();
+    if (desc_.block == CKF_BLOCK_LLAMA) {
+      int* t = static_cast<int*>(model_.ws(rows * (c_.seq_len + 1) * sizeof(int), slot));
+      llama_token_batch(data_seed_, stream, index, rows, c_.seq_len, c_.output_dim, t, st);
+      b.x = t;
+      return b;
+    }
+    const size_t mbytes = model_.master_bytes();
+    void* x = model_.ws(rows * c_.input_dim * mbytes, slot);
+    const uint64_t key = host::derive_key(data_seed_, stream, index);
+    if (model_.fp64())
+      k::uniform(static_cast<double*>(x), rows * c_.input_dim, key, -1.0, 1.0, 0, st);
+    else
+      k::uniform(static_cast<float*>(x), rows * c_.input_dim, key, -1.0, 1.0, 0, st);
+    CKF_CUDA(cudaStreamSynchronize(st));
+    void* pred = teacher_->ws(rows * c_.output_dim * mbytes, 30);
+    const auto order = host::standard_order(static_cast<int>(c_.stages));
+    teacher_->predict_device(order.data(), x, rows, pred);
+    CKF_CUDA(cudaStreamSynchronize(teacher_->stream()));
+    if (c_.task == "regression") {
+      void* y = model_.ws(rows * c_.output_dim * mbytes, slot + 1);
+      CKF_CUDA(cudaMemcpy(y, pred, rows * c_.output_dim * mbytes, cudaMemcpyDeviceToDevice));
+      b.y = y;
+    } else {
+      int* y = static_cast<int*>(model_.ws(rows * sizeof(int), slot + 1));
+      argmax_rows(pred, model_.fp64(), rows, c_.output_dim, y, st);
+      b.y = y;
+    }
+    b.x = x;
+    CKF_CUDA(cudaDeviceSynchronize());
+    return b;
+  }
+
+  double eval(const Batch& b, const std::vector<int>& order) { return model_.eval_loss(order.data(), b.x, b.y, b.rows, true); }
+  double val_loss() { return eval(val_, host::standard_order(static_cast<int>(c_.stages))); }
+
+  double add_eval(long slot) {
+    const double v = val_loss();
+    evals_.push_back({slot, v});
+    char buf[160];
+    std::snprintf(buf, sizeof(buf), "E,%ld,%.17g,%.17g\n", slot, last_train_, v);
+    out_ << buf;
+    return v;
+  }
+
+  void add_event(long slot, int st, const std::string& action, double red, double spike, double ms) {
+    pending_.push_back({slot, st, action, red, spike, ms});
+  }
+  void flush_events(double spike, bool set_spike) {
+    for (auto& e : pending_) {
+      char buf[256];
+      std::snprintf(buf, sizeof(buf), "F,%ld,%d,%s,%.17g,%.17g,%.6g\n", e.slot, e.stage, e.action.c_str(), e.red,
+                    set_spike ? spike : e.spike, e.ms);
+      out_ << buf;
+    }
+    pending_.clear();
+  }
+
+  // trainer.cpp:146-289 (neighbour family, redundant, no-failures)
+  bool handle_failures(long slot, const std::vector<int>& stages) {
+    const int s = static_cast<int>(c_.stages);
+    if (c_.strategy == "checkpointing")
+      host::fail(1, "the checkpointing baseline is not part of the B200 engine (SURVEY §8f rank 2)");
+    for (size_t i = 0; i + 1 < stages.size(); ++i) {
+      if (stages[i + 1] == stages[i] + 1) {
+        for (int st : stages) add_event(slot, st, "unrecoverable", 0.0, 0.0, 0.0);
+        flush_events(0.0, false);
+        out_ << "U,stages " << stages[i] << " and " << stages[i] + 1 << " failed together at iteration " << slot
+             << "; no live neighbor to recover from\n";
+        return false;
+      }
+    }
+    if (c_.strategy == "redundant") {
+      for (int st : stages) add_event(slot, st, "redundant_copy", 0.0, 0.0, 0.0);
+      flush_events(0.0, false);
+      return true;
+    }
+    const double vpre = val_loss();
+    const bool averaged = c_.recovered_moments == "averaged";
+    for (int st : stages) {
+      int mode;
+      std::string action;
+      if (st == 1 || st == s) {
+        if (c_.strategy != "checkfree-plus") {
+          add_event(slot, st, "unsupported", 0.0, 0.0, 0.0);
+          flush_events(0.0, false);
+          out_ << "U," << c_.strategy << " cannot recover the " << (st == 1 ? "first" : "last")
+               << " stage (iteration " << slot << ")\n";
+          return false;
+        }
+        mode = CKF_REC_EDGE;
+        action = "edge_copy";
+      } else if (c_.strategy == "checkfree" || c_.strategy == "checkfree-plus") {
+        mode = CKF_REC_CHECKFREE;
+      } else if (c_.strategy == "reinit-random") {
+        mode = CKF_REC_RANDOM;
+        action = "random_reinit";
+      } else if (c_.strategy == "reinit-copy") {
+        mode = CKF_REC_COPY_PREV;
+        action = "copy_prev";
+      } else {
+        mode = CKF_REC_UNIFORM;
+        action = "uniform_avg";
+      }
+      const uint64_t rseed = host::derive_key(seed_, kSeedReinit, static_cast<uint64_t>(slot), static_cast<uint64_t>(st));
+      const int mom = averaged && (mode == CKF_REC_CHECKFREE || mode == CKF_REC_EDGE) ? CKF_MOM_AVERAGED : CKF_MOM_FRESH;
+      ckf_recovery_report r = model_.recover_stage(st, mode, mom, c_.lr_bump, rseed, true);
+      if (mode == CKF_REC_CHECKFREE) action = r.degenerate ? "uniform_avg_fallback" : "checkfree_avg";
+      add_event(slot, st, action, r.reduction_error, 0.0, r.latency_ms);
+    }
+    const double vpost = val_loss();
+    flush_events(vpost - vpre, true);
+    return true;
+  }
+
+  struct Pending {
+    long slot;
+    int stage;
+    std::string action;
+    double red, spike, ms;
+  };
+
+  host::Config c_;
+  uint64_t seed_;
+  uint64_t data_seed_ = 0;
+  ckf_model_desc desc_;
+  Engine model_;
+  std::unique_ptr<Engine> teacher_;
+  std::map<long, std::vector<int>> events_;
+  std::vector<int> std_sched_, sw_sched_;
+  Batch val_;
+  long model_iter_ = 0;
+  double last_train_ = 0.0;
+  std::vector<std::pair<long, double>> evals_;
+  std::vector<Pending> pending_;
+  std::ostringstream out_;
+};
+
+}  // namespace
+
+std::string run_experiment(const std::string& kv, const std::string& trace_text, uint64_t seed) {
+  host::Config c = host::Config::from_kv(kv);
+  c.validate();
+  host::Trace t = trace_text.empty() ? c.resolve_trace(seed) : host::parse_trace(trace_text);
+  host::validate_trace(t);
+  Trainer tr(c, t, seed);
+  return tr.run();
+}
+
+}  // namespace ckf
