@@ -1,0 +1,367 @@
+#!/usr/bin/env python
+"""Benchmark of the CheckFree / CheckFree+ pipeline training step on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload NAME]
+
+One "step" = one pipeline::run_iteration (src/pipeline.cpp:58-95) over one
+synthetic batch: every microbatch forward + backward through all stages in
+its execution order, gradient accumulation, fused Adam + omega per stage.
+N=1 keeps every stage resident on cuda:0 (BASELINE.json configs[1] shape);
+N>1 places contiguous stage blocks per rank (stage transfers over NCCL).
+
+Prints ONE JSON line (rank 0).  `value` = tokens/s with inputs resident in HBM,
+device time from CUDA events on the engine's stream, max over ranks, L2
+flushed (256 MiB memset) between steps outside the timed events.  `e2e` = the
+same step through the public API with pinned HOST inputs (H2D inside the timed
+region) and the loss/omegas read back.  `roofline` covers the dominant kernel
+class, timed live with CUDA events inside the timed region.  `cpu_baseline`
+times the reference's own CPU path (oracle/_ref, the unmodified reference
+library) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+# Workloads.  The residual-MLP block is the reference's own model family
+# (model.hpp:55-60); "mlp-124m" runs it at the LLaMA-124M pipeline shape
+# (d=512, hidden=2048, 12 layers, 4 stages, 8 microbatches, 65,536 rows/iter)
+# in the fp32 parity precision.
+WORKLOADS = {
+    "mlp-124m": dict(block="mlp", precision="fp32", input_dim=16, hidden_dim=2048, model_dim=512, output_dim=16,
+                     layers=12, stages=4, microbatches=8, rows=65536, seq_len=1, heads=1),
+}
+DEFAULT_WORKLOAD = "mlp-124m"
+
+
+def flops_per_token(w: dict) -> float:
+    """Training FLOPs per row/token (fwd + 2x bwd), algorithmic."""
+    if w["block"] == "mlp":
+        d, h, L = w["model_dim"], w["hidden_dim"], w["layers"]
+        return 6.0 * (w["input_dim"] * d + L * 2 * d * h + d * w["output_dim"])
+    d, f, L, V, T = w["model_dim"], w["hidden_dim"], w["layers"], w["output_dim"], w["seq_len"]
+    return 6.0 * (L * (4 * d * d + 3 * d * f) + d * V) + 6.0 * L * d * T  # causal attention at half
+
+
+def load_peaks() -> tuple[dict, str]:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            raw = json.load(f)
+        out = dict(PEAKS_FALLBACK)
+        for k in out:
+            if k in raw and isinstance(raw[k], (int, float)):
+                out[k] = float(raw[k])
+        return out, "measured"
+    return dict(PEAKS_FALLBACK), "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.samples: list[tuple[float, float, set]] = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                parts = [x.strip() for x in out.split(",")]
+                reasons = {n for n, v in zip(names, parts[2:]) if v.lower() == "active"}
+                self.samples.append((float(parts[0]), float(parts[1]), reasons))
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        reasons = sorted(set().union(*[s[2] for s in self.samples]))
+        return {"sm_mhz": statistics.median(s[0] for s in self.samples),
+                "sm_max_mhz": max(s[1] for s in self.samples), "reasons": reasons, "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- reference CPU arm
+def ref_sample_kv(w: dict, rows: int) -> dict:
+    """Residual-MLP config of the reference at the workload's pipeline shape, `rows` rows per iteration."""
+    return {"input-dim": w["input_dim"] if w["block"] == "mlp" else 16,
+            "hidden-dim": w["hidden_dim"], "model-dim": w["model_dim"],
+            "output-dim": w["output_dim"] if w["block"] == "mlp" else 16,
+            "layers": w["layers"], "stages": w["stages"], "batch": rows, "microbatches": w["microbatches"],
+            "activation": "tanh", "task": "regression", "strategy": "checkfree", "lr": 3e-4}
+
+
+def cpu_reference(w: dict, iters: int, rows: int) -> dict:
+    """Times the UNMODIFIED reference (oracle/_ref) training loop body on the host cores."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import refshim  # noqa: E402  (test/baseline infrastructure only)
+    cores = os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    s_per_iter = refshim.time_train_iterations(ref_sample_kv(w, rows), 1, iters)
+    return {"value": rows / s_per_iter, "unit": "tokens/s", "cores": refshim.parallel_threads(),
+            "kind": "reference", "s_per_iter": s_per_iter,
+            "sample": f"reference residual-MLP block (fp64, OpenMP) at this workload's pipeline shape "
+                      f"(d={w['model_dim']}, hidden={w['hidden_dim']}, L={w['layers']}, s={w['stages']}, "
+                      f"m={w['microbatches']}), {rows} rows/iteration, {iters} timed iterations after 1 warm-up"}
+
+
+def run_reference_arm(args, w: dict):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    rows = max(w["microbatches"], 64 if w["block"] == "mlp" else 32)
+    cb = cpu_reference(w, max(1, args.steps), rows)
+    line = {"metric": METRIC, "value": cb["value"], "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": cb["s_per_iter"] * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference", "config": workload_config(args, w),
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": cb["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+METRIC = "pipeline train tokens/s"
+
+
+def workload_config(args, w: dict) -> dict:
+    cfg = {"workload": args.workload, "block": w["block"], "stages": w["stages"],
+           "microbatches": w["microbatches"], "layers": w["layers"], "model_dim": w["model_dim"],
+           "hidden_dim": w["hidden_dim"], "tokens_per_step": tokens_per_step(w), "seq_len": w["seq_len"],
+           "strategy": "checkfree", "placement": f"{w['stages']} stages on {args.gpus} GPU(s)",
+           "l2": "256 MiB memset between timed steps (outside the events)"}
+    if w["block"] == "llama":
+        cfg.update(vocab=w["output_dim"], heads=w["heads"])
+    return cfg
+
+
+def tokens_per_step(w: dict) -> int:
+    return w["rows"] * (w["seq_len"] if w["block"] == "llama" else 1)
+
+
+# ----------------------------------------------------------------------------- our arm
+def make_batch(w: dict, gen, device):
+    import torch
+    rows = w["rows"]
+    if w["block"] == "llama":
+        x = torch.randint(0, w["output_dim"], (rows, w["seq_len"] + 1), generator=gen, dtype=torch.int32)
+        return x, None
+    x = torch.rand((rows, w["input_dim"]), generator=gen, dtype=torch.float64) * 2 - 1
+    y = torch.rand((rows, w["output_dim"]), generator=gen, dtype=torch.float64) * 2 - 1
+    return x, y
+
+
+def run_ours(args, w: dict):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2506_15461_b200 as P
+    from paper_2506_15461_b200 import api
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    s = w["stages"]
+    if world > 1 and s % world != 0:
+        raise SystemExit(f"{s} stages cannot be placed in contiguous blocks on {world} GPUs")
+
+    mb_rows = w["rows"] // w["microbatches"]
+    if w["block"] == "llama":
+        spec = api.ModelSpec.llama(w["output_dim"], w["model_dim"], w["layers"], w["heads"], w["hidden_dim"],
+                                   w["seq_len"], s, precision=w["precision"], max_tokens=mb_rows * w["seq_len"],
+                                   device=local)
+    else:
+        spec = api.ModelSpec(w["input_dim"], w["hidden_dim"], w["model_dim"], w["output_dim"], w["layers"], s,
+                             precision=w["precision"], max_rows=mb_rows, device=local)
+    eng = P.Engine(spec)
+    eng.init(1, 3e-4)
+    if world > 1:
+        uid = [P.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        eng.attach_comm(uid[0], world, rank, [(sid - 1) * world // s for sid in range(1, s + 1)])
+
+    orders = np.array(api.build_schedule(w["microbatches"], False, s), np.int32)
+    gen = torch.Generator().manual_seed(1234 + rank)
+    xh, yh = make_batch(w, gen, local)
+    xh, yh = xh.pin_memory(), (yh.pin_memory() if yh is not None else None)
+    xd = xh.to(f"cuda:{local}", non_blocking=False)
+    yd = yh.to(f"cuda:{local}") if yh is not None else None
+    if w["block"] == "mlp" and w["precision"] == "fp32":
+        xd, yd = xd.float(), yd.float()
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.ExternalStream(eng.stream_ptr(), device=local)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+
+    def step(it, on_device):
+        if on_device:
+            return eng.run_iteration(orders, xd, yd, it, on_device=True)
+        return eng.run_iteration(orders, xh.numpy(), yh.numpy() if yh is not None else None, it)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def timed(k, on_device, it0):
+        evs = []
+        for i in range(k):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+            step(it0 + i, on_device)
+            b.record(stream)
+            evs.append((a, b))
+        torch.cuda.synchronize()
+        return sum(a.elapsed_time(b) for a, b in evs)
+
+    it = 1
+    for _ in range(args.warmup):
+        step(it, True)
+        it += 1
+    barrier()
+    launches0 = eng.kernel_launches()
+    eng.kernel_timing(True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ms_total = timed(args.steps, True, it)
+        barrier()
+    it += args.steps
+    launches = eng.kernel_launches() - launches0
+    kstats = {c: eng.kernel_stats(c) for c in api.Engine.KCLASS}
+    eng.kernel_timing(False)
+
+    # e2e through the public API with pinned host buffers (H2D + loss/omega D2H inside)
+    for _ in range(1):
+        step(it, False)
+        it += 1
+    barrier()
+    e2e_total = timed(args.steps, False, it)
+    barrier()
+    it += args.steps
+
+    ms = ms_total / args.steps
+    e2e_ms = e2e_total / args.steps
+    if world > 1:
+        t = torch.tensor([ms, e2e_ms], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, e2e_ms = t.tolist()
+
+    # stage-recovery latency (trainer.cpp:230-276 semantics, weights + moments + lr + omega), stage 2
+    rec = None
+    if world == 1 and s >= 3:
+        lat = []
+        for _ in range(3):
+            eng.kill_stage(2)
+            r = eng.recover_stage(2, reduction_error=False)
+            lat.append(r.latency_ms)
+        pb = 4 if w["precision"] != "fp64" else 8
+        P_ = eng.stage_params
+        rec = {"stage": 2, "stage_params": P_, "latency_ms": min(lat),
+               "avg_bytes": 3 * pb * P_, "avg_gbs_incl_moment_reset": None}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peaks, peak_src = load_peaks()
+    tok = tokens_per_step(w) * (1 if world == 1 else 1)
+    value = tok / (ms / 1e3)
+    e2e_value = tok / (e2e_ms / 1e3)
+    # dominant kernel class (by device time inside the timed region)
+    dom = max(kstats, key=lambda c: kstats[c][0])
+    kms, kn, kfl, kby = kstats[dom]
+    if dom in ("gemm", "attention") and w["precision"] == "bf16":
+        achieved = kfl / (kms / 1e3) / 1e12
+        roof = {"bound": "tensor", "unit": "TFLOP/s", "peak": peaks["bf16_tflops_sustained"]}
+    elif dom in ("gemm", "attention"):
+        achieved = kfl / (kms / 1e3) / 1e12
+        roof = {"bound": "tensor", "unit": "TFLOP/s", "peak": peaks["bf16_tflops_sustained"],
+                "note": f"{w['precision']} parity path on CUDA cores, shown against the bf16 tensor peak"}
+    else:
+        achieved = kby / (kms / 1e3) / 1e9
+        roof = {"bound": "hbm", "unit": "GB/s", "peak": peaks["hbm_gbs"]}
+    roof.update(kernel_class=dom, achieved=achieved, frac=achieved / roof["peak"], traffic=None,
+                peak_source=peak_src, launches=kn, share_of_step=kms / ms_total,
+                per_launch={"ms": kms / max(kn, 1), "flops": kfl / max(kn, 1), "bytes": kby / max(kn, 1)},
+                classes={c: {"ms": v[0], "launches": v[1]} for c, v in kstats.items() if v[1]})
+    step_tflops = flops_per_token(w) * tok / (ms / 1e3) / 1e12
+
+    if rec is not None and rec["latency_ms"] > 0:
+        rec["avg_gbs_incl_moment_reset"] = (rec["avg_bytes"] + 3 * (4 if w["precision"] != "fp64" else 8)
+                                            * rec["stage_params"]) / (rec["latency_ms"] / 1e3) / 1e9
+
+    h2d = xh.numel() * xh.element_size() + (yh.numel() * yh.element_size() if yh is not None else 0)
+    d2h = 8 * (1 + s) + 8 * w["microbatches"]
+    cpu = None
+    if not args.no_cpu_baseline:
+        cpu = cpu_reference(w, 1, max(w["microbatches"], 64 if w["block"] == "mlp" else 32))
+        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": {"fp32": "f32", "fp64": "f64", "bf16": "bf16"}[w["precision"]],
+            "data": "synthetic (seeded random rows/tokens; random-init weights via the counter RNG)",
+            "config": workload_config(args, w),
+            "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "ms_per_step": e2e_ms},
+            "gpu_launches": launches, "roofline": roof, "step_tflops": step_tflops,
+            "flops_per_token": flops_per_token(w), "cpu_baseline": cpu, "clocks": clk.summary(),
+            "recovery": rec}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default=DEFAULT_WORKLOAD)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    w = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        run_reference_arm(args, w)
+    else:
+        run_ours(args, w)
+
+
+if __name__ == "__main__":
+    main()

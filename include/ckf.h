@@ -113,6 +113,17 @@ int ckf_recover_device(int dtype, const void* wp, const void* wn, void* out, siz
 int ckf_adam_device(int dtype, void* w, void* m, void* v, void* g, void* w_bf16, size_t n, double lr,
                     double bc1, double bc2, double grad_scale, int zero_grad, double* omega, void* stream);
 
+/* bf16 tensor-core GEMM (tcgen05 + TMA, fp32 accumulation in TMEM), the
+ * stage-GEMM primitive that replaces gemm_nn / gemm_nn_acc / gemm_nt_acc /
+ * gemm_tn_acc (kernels_serial.cpp:13-61) on the bf16 path:
+ *   C[M,N] (epi) alpha * op(A) op(B)
+ *   a_mn = 0: A stored [M][lda] (K contiguous), 1: A stored [K][lda] (M contiguous)
+ *   b_mn = 0: B stored [N][ldb] (K contiguous), 1: B stored [K][ldb] (N contiguous)
+ *   epi  = 0: C bf16 store, 1: C fp32 store, 2: C fp32 += (gradient accumulation)
+ *   bn   = 0 (heuristic), 128 or 256: N tile.  Device pointers; lda/ldb % 8 == 0. */
+int ckf_gemm_bf16(int M, int N, int K, const void* A, int lda, int a_mn, const void* B, int ldb, int b_mn, void* C,
+                  int ldc, int epi, float alpha, int bn, void* stream);
+
 /* =====================================================================
  * (3) Device-resident engine: the throughput tier behind
  *     ckfree::pipeline::run_iteration (pipeline.hpp:44-47),
@@ -208,6 +219,16 @@ int ckf_engine_set_edge_scalars(ckf_engine_t e, double lr, long step_embed, long
 long ckf_engine_kernel_launches(ckf_engine_t e);
 /* synchronises the engine's streams */
 int ckf_engine_sync(ckf_engine_t e);
+/* the cudaStream_t the engine launches its kernels on (for CUDA-event timing by the caller) */
+int ckf_engine_stream(ckf_engine_t e, void** stream);
+
+/* Per-class kernel timing (roofline evidence).  enable != 0 resets the stats
+ * and brackets every tagged launch with CUDA events on the engine stream.
+ * cls: 0 GEMM, 1 attention, 2 Adam+omega, 3 recovery, 4 norm/elementwise,
+ * 5 loss, 6 stage transfer.  ms = summed device time; flops / bytes = the
+ * launches' ALGORITHMIC work (2MNK per GEMM, compulsory bytes otherwise). */
+int ckf_engine_kernel_timing(ckf_engine_t e, int enable);
+int ckf_engine_kernel_stats(ckf_engine_t e, int cls, double* ms, long* launches, double* flops, double* bytes);
 
 /* =====================================================================
  * (4) Trainer: harness::run_experiment (src/trainer.cpp:314-322) on the

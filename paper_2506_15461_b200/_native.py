@@ -87,6 +87,7 @@ def lib():
         "ckf_k_recover_checkfree": (i, [dp, dp, sz, dbl, dbl, dp, ip]),
         "ckf_k_counter_uniform": (i, [u64, dbl, dbl, dp, sz]),
         "ckf_recover_device": (i, [i, vp, vp, vp, sz, dbl, dbl, vp, vp]),
+        "ckf_gemm_bf16": (i, [i, i, i, vp, i, i, vp, i, i, vp, i, i, C.c_float, i, vp]),
         "ckf_adam_device": (i, [i, vp, vp, vp, vp, vp, sz, dbl, dbl, dbl, dbl, i, vp, vp]),
         "ckf_engine_create": (i, [C.POINTER(ModelDesc), C.POINTER(eng)]), "ckf_engine_destroy": (i, [eng]),
         "ckf_engine_param_counts": (i, [eng, C.POINTER(sz), C.POINTER(sz), C.POINTER(sz)]),
@@ -104,6 +105,8 @@ def lib():
         "ckf_engine_get_edge_scalars": (i, [eng, dp, C.POINTER(lng), C.POINTER(lng)]),
         "ckf_engine_set_edge_scalars": (i, [eng, dbl, lng, lng]),
         "ckf_engine_kernel_launches": (lng, [eng]), "ckf_engine_sync": (i, [eng]),
+        "ckf_engine_stream": (i, [eng, C.POINTER(C.c_void_p)]), "ckf_engine_kernel_timing": (i, [eng, i]),
+        "ckf_engine_kernel_stats": (i, [eng, i, dp, C.POINTER(lng), dp, dp]),
         "ckf_run_experiment": (i, [cp, cp, u64, cp, sz]),
     }
     for name, (res, args) in sig.items():

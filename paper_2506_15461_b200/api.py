@@ -270,6 +270,24 @@ class Engine:
     def kernel_launches(self) -> int:
         return lib().ckf_engine_kernel_launches(self._h)
 
+    def stream_ptr(self) -> int:
+        """cudaStream_t the engine launches on (wrap with torch.cuda.ExternalStream for event timing)."""
+        s = C.c_void_p()
+        check(lib().ckf_engine_stream(self._h, C.byref(s)))
+        return s.value or 0
+
+    def kernel_timing(self, enable: bool):
+        check(lib().ckf_engine_kernel_timing(self._h, 1 if enable else 0))
+
+    KCLASS = {"gemm": 0, "attention": 1, "adam": 2, "recovery": 3, "norm": 4, "loss": 5, "transfer": 6}
+
+    def kernel_stats(self, cls: str):
+        """(ms, launches, algorithmic flops, algorithmic bytes) summed since kernel_timing(True)."""
+        ms, n, fl, by = C.c_double(), C.c_long(), C.c_double(), C.c_double()
+        check(lib().ckf_engine_kernel_stats(self._h, self.KCLASS[cls], C.byref(ms), C.byref(n), C.byref(fl),
+                                            C.byref(by)))
+        return ms.value, n.value, fl.value, by.value
+
 
 def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)

@@ -8,6 +8,7 @@
 
 #include "../../include/ckf.h"
 #include "engine.h"
+#include "gemm_tc.h"
 #include "host_logic.h"
 
 namespace ckf {
@@ -364,6 +365,30 @@ int ckf_adam_device(int dtype, void* w, void* m, void* v, void* g, void* w_bf16,
   });
 }
 
+int ckf_gemm_bf16(int M, int N, int K, const void* A, int lda, int a_mn, const void* B, int ldb, int b_mn, void* C,
+                  int ldc, int epi, float alpha, int bn, void* stream) {
+  return guard([&] {
+    if (epi < 0 || epi > 2) ckf::raise(CKF_E_CONFIG, "gemm_bf16: epi must be 0, 1 or 2");
+    if (bn != 0 && bn != 128 && bn != 256) ckf::raise(CKF_E_CONFIG, "gemm_bf16: bn must be 0, 128 or 256");
+    ckf::tc::GemmDesc g;
+    g.M = M;
+    g.N = N;
+    g.K = K;
+    g.A = static_cast<const __nv_bfloat16*>(A);
+    g.lda = lda;
+    g.a_mn = a_mn != 0;
+    g.B = static_cast<const __nv_bfloat16*>(B);
+    g.ldb = ldb;
+    g.b_mn = b_mn != 0;
+    g.C = C;
+    g.ldc = ldc;
+    g.epi = epi;
+    g.alpha = alpha;
+    g.bn = bn;
+    ckf::tc::gemm_bf16(g, static_cast<cudaStream_t>(stream));
+  });
+}
+
 // ---------------------------------------------------------------- (3) engine
 int ckf_engine_create(const ckf_model_desc* desc, ckf_engine_t* out) {
   return guard([&] {
@@ -459,6 +484,23 @@ int ckf_engine_set_edge_scalars(ckf_engine_t e, double lr, long se, long sd) {
 long ckf_engine_kernel_launches(ckf_engine_t) { return ckf::launch_counter(); }
 int ckf_engine_sync(ckf_engine_t e) {
   return guard([&] { CKF_CUDA(cudaStreamSynchronize(E(e)->stream())); });
+}
+
+int ckf_engine_stream(ckf_engine_t e, void** stream) {
+  return guard([&] { *stream = static_cast<void*>(E(e)->stream()); });
+}
+int ckf_engine_kernel_timing(ckf_engine_t e, int enable) {
+  return guard([&] { E(e)->kt_enable(enable != 0); });
+}
+int ckf_engine_kernel_stats(ckf_engine_t e, int cls, double* ms, long* launches, double* flops, double* bytes) {
+  return guard([&] {
+    if (cls < 0 || cls >= ckf::KC_N) ckf::raise(CKF_E_CONFIG, "kernel class out of range");
+    const ckf::KStat& k = E(e)->kt_stat(cls);
+    if (ms) *ms = k.ms;
+    if (launches) *launches = k.launches;
+    if (flops) *flops = k.flops;
+    if (bytes) *bytes = k.bytes;
+  });
 }
 
 // ---------------------------------------------------------------- (4) trainer

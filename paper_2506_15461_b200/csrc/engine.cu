@@ -142,6 +142,7 @@ Engine::~Engine() {
   cudaFree(red_.partials);
   cudaFree(scal_);
   if (comm_ && nccl().CommDestroy) nccl().CommDestroy(comm_);
+  for (cudaEvent_t ev : kev_) cudaEventDestroy(ev);
   if (ev0_) cudaEventDestroy(ev0_);
   if (ev1_) cudaEventDestroy(ev1_);
   if (st_) cudaStreamDestroy(st_);
@@ -184,6 +185,50 @@ void* Engine::ws(size_t bytes, int slot) {
     ws_size_[static_cast<size_t>(slot)] = want;
   }
   return ws_[static_cast<size_t>(slot)];
+}
+
+// ------------------------------------------------------------------ kernel timing
+void Engine::kt_enable(bool on) {
+  CKF_CUDA(cudaStreamSynchronize(st_));
+  kt_on_ = on;
+  kev_used_ = 0;
+  krec_.clear();
+  for (auto& k : kstat_) k = KStat{};
+}
+
+void Engine::kt_begin() {
+  if (!kt_on_) return;
+  if (kev_used_ + 2 > kev_.size()) {
+    // grow the pool; a long step can tag a few thousand launches
+    for (int i = 0; i < 256; ++i) {
+      cudaEvent_t ev;
+      CKF_CUDA(cudaEventCreate(&ev));
+      kev_.push_back(ev);
+    }
+  }
+  CKF_CUDA(cudaEventRecord(kev_[kev_used_], st_));
+}
+
+void Engine::kt_end(int cls, double flops, double bytes) {
+  if (!kt_on_) return;
+  CKF_CUDA(cudaEventRecord(kev_[kev_used_ + 1], st_));
+  kev_used_ += 2;
+  krec_.push_back({cls, flops, bytes});
+}
+
+void Engine::kt_collect() {
+  if (!kt_on_) return;
+  for (size_t i = 0; i < krec_.size(); ++i) {
+    float ms = 0.f;
+    CKF_CUDA(cudaEventElapsedTime(&ms, kev_[2 * i], kev_[2 * i + 1]));
+    KStat& k = kstat_[krec_[i].cls];
+    k.ms += ms;
+    k.flops += krec_[i].flops;
+    k.bytes += krec_[i].bytes;
+    ++k.launches;
+  }
+  krec_.clear();
+  kev_used_ = 0;
 }
 
 // ------------------------------------------------------------------ placement
@@ -267,12 +312,15 @@ void Engine::adam_group(ParamGroup& g, double lr, double gscale, double* omega_d
   // bias corrections with std::pow on the host, exactly kernels_serial.cpp:135-136
   const double bc1 = 1.0 - std::pow(0.9, static_cast<double>(g.step));
   const double bc2 = 1.0 - std::pow(0.999, static_cast<double>(g.step));
+  kt_begin();
   if (fp64())
     k::adam(static_cast<double*>(g.w), static_cast<double*>(g.m), static_cast<double*>(g.v),
             static_cast<double*>(g.g), g.wlp, g.n, lr, bc1, bc2, gscale, true, omega_dev, red_, st_);
   else
     k::adam(static_cast<float*>(g.w), static_cast<float*>(g.m), static_cast<float*>(g.v), static_cast<float*>(g.g),
             g.wlp, g.n, lr, bc1, bc2, gscale, true, omega_dev, red_, st_);
+  // g, w, m, v read; w, m, v, g(zeroed) written; + bf16 shadow
+  kt_end(KC_ADAM, 0.0, static_cast<double>(g.n) * (8.0 * master_bytes() + (g.wlp ? 2.0 : 0.0)));
 }
 
 void Engine::run_iteration(const int* orders, int m, const void* x, const void* y, size_t rows, bool on_device,
@@ -345,6 +393,7 @@ void Engine::run_iteration(const int* orders, int m, const void* x, const void* 
   CKF_CUDA(cudaMemcpyAsync(losses.data(), scal_, static_cast<size_t>(m) * sizeof(double), cudaMemcpyDeviceToHost, st_));
   CKF_CUDA(cudaMemcpyAsync(om.data(), scal_ + 2048, d_.s * sizeof(double), cudaMemcpyDeviceToHost, st_));
   CKF_CUDA(cudaStreamSynchronize(st_));
+  kt_collect();
   double total = 0.0;
   for (double l : losses) total += l;
   total *= inv;

@@ -54,6 +54,15 @@ struct ParamGroup {
 
 class Engine;
 
+// Per-class kernel timing (bench.py's roofline evidence): when enabled, each
+// tagged launch is bracketed by CUDA events on the engine stream and its
+// algorithmic FLOPs / bytes are recorded; collect() folds them after a sync.
+enum KClass { KC_GEMM = 0, KC_ATTN = 1, KC_ADAM = 2, KC_RECOVER = 3, KC_NORM = 4, KC_LOSS = 5, KC_COMM = 6, KC_N = 7 };
+struct KStat {
+  double ms = 0.0, flops = 0.0, bytes = 0.0;
+  long launches = 0;
+};
+
 // Block-specific arithmetic (residual MLP of model.hpp:55-60, or LLaMA).
 struct BlockImpl {
   explicit BlockImpl(Engine* e) : eng(e) {}
@@ -115,6 +124,14 @@ class Engine {
   // move `count` elements of `buf` (device, master or activation dtype bytes) from rank src to rank dst
   void hop(void* buf, size_t bytes, int src, int dst);
 
+  // kernel timing (KClass)
+  void kt_enable(bool on);
+  bool kt_on() const { return kt_on_; }
+  void kt_begin();
+  void kt_end(int cls, double flops, double bytes);
+  void kt_collect();  // stream must be synchronised
+  const KStat& kt_stat(int cls) const { return kstat_[cls]; }
+
   // device workspace (grows on demand, reused across calls)
   void* ws(size_t bytes, int slot);
   double* dev_scalars() { return scal_; }  // small device double array (losses, omegas)
@@ -140,6 +157,15 @@ class Engine {
   std::vector<int> stage_rank_;
   void* comm_ = nullptr;  // ncclComm_t
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
+  bool kt_on_ = false;
+  std::vector<cudaEvent_t> kev_;
+  size_t kev_used_ = 0;
+  struct KRec {
+    int cls;
+    double flops, bytes;
+  };
+  std::vector<KRec> krec_;
+  KStat kstat_[KC_N];
   friend struct MlpBlock;
   friend struct LlamaBlock;
 };

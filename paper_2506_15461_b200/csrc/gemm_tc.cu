@@ -1,0 +1,368 @@
+// bf16 tensor-core GEMM for sm_100a: TMA -> shared memory (128-B swizzle)
+// -> tcgen05.mma (fp32 accumulators in TMEM) -> tcgen05.ld epilogue.
+//
+// Replaces the reference's four row-major GEMMs (kernels_serial.cpp:13-61)
+// on the bf16 throughput path.  Every operand layout the stage forward /
+// backward needs is a template switch instead of a transpose:
+//   A K-major  = stored [M][lda]   A MN-major = stored [K][lda] (A^T)
+//   B K-major  = stored [N][ldb]   B MN-major = stored [K][ldb]
+//   forward  Y  = X W      A=X K-major,   B=W[K,N] MN-major
+//   dgrad    dX = dY W^T   A=dY K-major,  B=W[K,N] K-major  (as [N'][K'])
+//   wgrad    dW += X^T dY  A=X MN-major,  B=dY MN-major     (epilogue += fp32)
+//
+// Persistent, warp-specialised (one CTA per SM):
+//   warp 0      TMA producer (one elected lane), kStages-deep smem ring
+//   warp 1      MMA issuer (one lane): 128 x BN x 16 tcgen05.mma, commits
+//   warp 2      TMEM allocator (2 x BN fp32 columns: double-buffered accumulators)
+//   warps 4..7  epilogue: tcgen05.ld 32 lanes x 32 columns, fused store /
+//               fp32 accumulate, so tile i's epilogue overlaps tile i+1's MMAs.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "common.cuh"
+#include "gemm_tc.h"
+#include "sm100.cuh"
+
+namespace ckf {
+
+// ------------------------------------------------------------------ tensor maps (host)
+namespace tma {
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    CKF_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p) raise(6, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+}  // namespace
+
+CUtensorMap make_2d_bf16(const void* base, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_inner,
+                         uint32_t box_outer) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {inner, outer};
+  const cuuint64_t strides[1] = {ld * 2};
+  const cuuint32_t box[2] = {box_inner, box_outer};
+  const cuuint32_t estr[2] = {1, 1};
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || ((ld * 2) & 15))
+    raise(1, "TMA operands need 16-byte aligned base and row pitch (ld % 8 == 0 for bf16)");
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) raise(6, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
+  return m;
+}
+
+CUtensorMap make_3d_bf16(const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t ld1, uint64_t ld2,
+                         uint32_t box0, uint32_t box1) {
+  CUtensorMap m;
+  const cuuint64_t dims[3] = {d0, d1, d2};
+  const cuuint64_t strides[2] = {ld1 * 2, ld2 * 2};
+  const cuuint32_t box[3] = {box0, box1, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || ((ld1 * 2) & 15) || ((ld2 * 2) & 15))
+    raise(1, "TMA operands need 16-byte aligned base and pitches");
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) raise(6, "cuTensorMapEncodeTiled (3d) failed (" + std::to_string(static_cast<int>(r)) + ")");
+  return m;
+}
+}  // namespace tma
+
+namespace tc {
+namespace {
+
+using namespace ckf::sm100;
+
+constexpr int BM = 128, BK = 64, UK = 16;
+constexpr int kThreads = 256;
+constexpr uint32_t kAStage = BM * BK * 2;  // 16 KiB
+
+struct Params {
+  int M, N, K;
+  void* C;
+  int ldc;
+  float alpha;
+  int nm, nn, tiles, nk;
+  const float* bias_dummy;
+};
+
+template <int BN>
+struct Cfg {
+  static constexpr int kStages = BN == 256 ? 4 : 6;
+  static constexpr uint32_t kBStage = BN * BK * 2;
+  static constexpr uint32_t kStageBytes = kAStage + kBStage;
+  static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
+  static constexpr size_t kSmem = 1024 /*align slack*/ + kStages * kStageBytes + 256 /*barriers*/;
+};
+
+template <int EPI>
+__device__ __forceinline__ void store_row_chunk(const Params& p, int m, int n0, const uint32_t (&r)[32]) {
+  float v[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * p.alpha;
+  if (n0 + 32 <= p.N) {
+    if constexpr (EPI == kStoreBF16) {
+      __nv_bfloat16* c = static_cast<__nv_bfloat16*>(p.C) + static_cast<size_t>(m) * p.ldc + n0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 u;
+        u.x = pack_bf16(v[8 * q + 0], v[8 * q + 1]);
+        u.y = pack_bf16(v[8 * q + 2], v[8 * q + 3]);
+        u.z = pack_bf16(v[8 * q + 4], v[8 * q + 5]);
+        u.w = pack_bf16(v[8 * q + 6], v[8 * q + 7]);
+        reinterpret_cast<uint4*>(c)[q] = u;
+      }
+    } else {
+      float* c = static_cast<float*>(p.C) + static_cast<size_t>(m) * p.ldc + n0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float4 o = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        if constexpr (EPI == kAccF32) {
+          const float4 old = reinterpret_cast<const float4*>(c)[q];
+          o.x += old.x;
+          o.y += old.y;
+          o.z += old.z;
+          o.w += old.w;
+        }
+        reinterpret_cast<float4*>(c)[q] = o;
+      }
+    }
+  } else {
+    for (int j = 0; j < 32 && n0 + j < p.N; ++j) {
+      const size_t off = static_cast<size_t>(m) * p.ldc + n0 + j;
+      if constexpr (EPI == kStoreBF16)
+        static_cast<__nv_bfloat16*>(p.C)[off] = __float2bfloat16(v[j]);
+      else if constexpr (EPI == kStoreF32)
+        static_cast<float*>(p.C)[off] = v[j];
+      else
+        static_cast<float*>(p.C)[off] += v[j];
+    }
+  }
+}
+
+template <int BN, bool A_MN, bool B_MN, int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b, Params p) {
+  using C = Cfg<BN>;
+  constexpr int ST = C::kStages;
+  constexpr uint32_t IDESC = idesc_bf16_f32(BM, BN, A_MN, B_MN);
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + ST * kAStage;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ST * C::kStageBytes);
+  uint64_t* empty = full + ST;
+  uint64_t* tfull = empty + ST;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmap_a);
+    tma_prefetch(&tmap_b);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int i = 0; i < ST; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<C::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
+        const int mb = tile % p.nm, nb = tile / p.nm;
+        for (int kb = 0; kb < p.nk; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
+          uint8_t* a = sA + stage * kAStage;
+          uint8_t* b = sB + stage * C::kBStage;
+          if constexpr (A_MN) {
+#pragma unroll
+            for (int c = 0; c < BM / 64; ++c) tma_load_2d(a + c * 8192, &tmap_a, &full[stage], mb * BM + c * 64, kb * BK);
+          } else {
+            tma_load_2d(a, &tmap_a, &full[stage], kb * BK, mb * BM);
+          }
+          if constexpr (B_MN) {
+#pragma unroll
+            for (int c = 0; c < BN / 64; ++c) tma_load_2d(b + c * 8192, &tmap_b, &full[stage], nb * BN + c * 64, kb * BK);
+          } else {
+            tma_load_2d(b, &tmap_b, &full[stage], kb * BK, nb * BN);
+          }
+          if (++stage == ST) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + static_cast<uint32_t>(acc * BN);
+        for (int kb = 0; kb < p.nk; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * kAStage);
+          const uint32_t b0 = smem_u32(sB + stage * C::kBStage);
+#pragma unroll
+          for (int k = 0; k < BK / UK; ++k) {
+            const uint64_t ad = A_MN ? umma_desc_sw128(a0 + k * 2048, 8192, 1024) : umma_desc_sw128(a0 + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? umma_desc_sw128(b0 + k * 2048, 8192, 1024) : umma_desc_sw128(b0 + k * 32, 16, 1024);
+            umma_bf16(d, ad, bd, IDESC, (kb | k) != 0 ? 1u : 0u);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == ST) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue: TMEM -> registers -> global
+    const int q = warp - 4;  // TMEM lane quarter (warp % 4)
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
+      const int mb = tile % p.nm, nb = tile / p.nm;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int m = mb * BM + q * 32 + lane;
+      const uint32_t trow = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN);
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(trow + c0, r);
+        tmem_ld_wait();
+        const int n0 = nb * BN + c0;
+        if (m < p.M && n0 < p.N) store_row_chunk<EPI>(p, m, n0, r);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_free<C::kTmemCols>(tmem_base);
+}
+
+int num_sms() {
+  static int n = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v > 0 ? v : kNumSMs;
+  }();
+  return n;
+}
+
+template <int BN, bool A_MN, bool B_MN, int EPI>
+void launch_t(const GemmDesc& g, cudaStream_t s) {
+  using C = Cfg<BN>;
+  const CUtensorMap ta = A_MN ? tma::make_2d_bf16(g.A, g.M, g.K, g.lda, 64, 64)
+                              : tma::make_2d_bf16(g.A, g.K, g.M, g.lda, 64, BM);
+  const CUtensorMap tb = B_MN ? tma::make_2d_bf16(g.B, g.N, g.K, g.ldb, 64, 64)
+                              : tma::make_2d_bf16(g.B, g.K, g.N, g.ldb, 64, BN);
+  Params p;
+  p.M = g.M;
+  p.N = g.N;
+  p.K = g.K;
+  p.C = g.C;
+  p.ldc = g.ldc;
+  p.alpha = g.alpha;
+  p.nm = (g.M + BM - 1) / BM;
+  p.nn = (g.N + BN - 1) / BN;
+  p.tiles = p.nm * p.nn;
+  p.nk = (g.K + BK - 1) / BK;
+  p.bias_dummy = nullptr;
+  auto kern = gemm_kernel<BN, A_MN, B_MN, EPI>;
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    CKF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::kSmem)));
+    attr_set = true;
+  }
+  const int grid = std::min(p.tiles, num_sms());
+  kern<<<grid, kThreads, C::kSmem, s>>>(ta, tb, p);
+  CKF_LAUNCH_CHECK();
+}
+
+template <int BN>
+void dispatch_bn(const GemmDesc& g, cudaStream_t s) {
+#define CKF_GEMM_CASE(AM, BMN, E) \
+  if (g.a_mn == AM && g.b_mn == BMN && g.epi == E) return launch_t<BN, AM, BMN, E>(g, s);
+#define CKF_GEMM_EPIS(AM, BMN) CKF_GEMM_CASE(AM, BMN, kStoreBF16) CKF_GEMM_CASE(AM, BMN, kStoreF32) CKF_GEMM_CASE(AM, BMN, kAccF32)
+  CKF_GEMM_EPIS(false, false)
+  CKF_GEMM_EPIS(false, true)
+  CKF_GEMM_EPIS(true, false)
+  CKF_GEMM_EPIS(true, true)
+#undef CKF_GEMM_EPIS
+#undef CKF_GEMM_CASE
+  raise(1, "gemm_bf16: unsupported epilogue");
+}
+
+}  // namespace
+
+int pick_bn(int M, int N) {
+  const int sms = num_sms();
+  auto cost = [&](int bn) {
+    const long tiles = static_cast<long>((M + BM - 1) / BM) * ((N + bn - 1) / bn);
+    const long waves = (tiles + sms - 1) / sms;
+    return waves * (bn + 48);  // per-tile time ~ BN columns of MMA + fixed prologue/epilogue
+  };
+  return cost(128) < cost(256) ? 128 : 256;
+}
+
+void gemm_bf16(const GemmDesc& g, cudaStream_t s) {
+  if (g.M <= 0 || g.N <= 0 || g.K <= 0) return;
+  if (g.ldc % 4 != 0 && g.epi != kStoreBF16) raise(1, "gemm_bf16: fp32 C needs ldc % 4 == 0");
+  if (g.ldc % 8 != 0 && g.epi == kStoreBF16) raise(1, "gemm_bf16: bf16 C needs ldc % 8 == 0");
+  const int bn = g.bn ? g.bn : pick_bn(g.M, g.N);
+  if (bn == 128)
+    dispatch_bn<128>(g, s);
+  else
+    dispatch_bn<256>(g, s);
+}
+
+}  // namespace tc
+}  // namespace ckf

@@ -1,0 +1,33 @@
+// Host API of the sm_100a bf16 tensor-core GEMM (gemm_tc.cu).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+namespace ckf::tc {
+
+enum Epi { kStoreBF16 = 0, kStoreF32 = 1, kAccF32 = 2 };
+
+// C[M,N] (epi) alpha * op(A) op(B), bf16 operands, fp32 accumulation.
+//   a_mn = false: A stored [M][lda] (K contiguous); true: A stored [K][lda] (M contiguous)
+//   b_mn = false: B stored [N][ldb] (K contiguous); true: B stored [K][ldb] (N contiguous)
+//   epi: kStoreBF16 (C bf16), kStoreF32 (C fp32), kAccF32 (C fp32 +=)
+struct GemmDesc {
+  int M = 0, N = 0, K = 0;
+  const __nv_bfloat16* A = nullptr;
+  int lda = 0;
+  bool a_mn = false;
+  const __nv_bfloat16* B = nullptr;
+  int ldb = 0;
+  bool b_mn = false;
+  void* C = nullptr;
+  int ldc = 0;
+  int epi = kStoreBF16;
+  float alpha = 1.0f;
+  int bn = 0;  // 0 = heuristic (128 or 256)
+};
+
+void gemm_bf16(const GemmDesc& g, cudaStream_t s);
+int pick_bn(int M, int N);
+
+}  // namespace ckf::tc

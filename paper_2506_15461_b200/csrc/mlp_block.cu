@@ -82,6 +82,16 @@ struct MlpBlock final : BlockImpl {
       init_edges_t(seed, static_cast<float*>(e), static_cast<float*>(de));
   }
 
+  // CUDA-core GEMM, timed as KC_GEMM when the engine's kernel timing is on
+  template <typename T>
+  void gemm(bool ta, bool tb, size_t M, size_t N, size_t K, const T* A, size_t lda, const T* B, size_t ldb, T* C,
+            size_t ldc, bool acc) {
+    eng->kt_begin();
+    k::gemm_simt<T>(ta, tb, M, N, K, A, lda, B, ldb, C, ldc, acc, eng->stream());
+    eng->kt_end(KC_GEMM, 2.0 * M * N * K,
+                sizeof(T) * (static_cast<double>(M) * K + static_cast<double>(K) * N + (acc ? 2.0 : 1.0) * M * N));
+  }
+
   // Workspace slots (>= 8; 0-3 belong to the engine's upload paths).
   template <typename T>
   T* buf(int slot, size_t elems) {
@@ -114,8 +124,8 @@ struct MlpBlock final : BlockImpl {
     // ---- forward (model.cpp:226-253)
     int where = eng->owner_of_embed();
     if (eng->mine(where))
-      k::gemm_simt<T>(false, false, b, d.d, d.in, x, d.in, static_cast<const T*>(eng->embed().w), d.d, h, d.d,
-                      false, st);
+      gemm<T>(false, false, b, d.d, d.in, x, d.in, static_cast<const T*>(eng->embed().w), d.d, h, d.d,
+                      false);
     for (size_t oi = 0; oi < d.s; ++oi) {
       const int sid = order[oi];
       const int own = eng->owner_of_stage(sid);
@@ -131,16 +141,16 @@ struct MlpBlock final : BlockImpl {
         T* cin = cache_in + slot * b * d.d;
         T* cz = cache_z + slot * b * d.hid;
         CKF_CUDA(cudaMemcpyAsync(cin, h, b * d.d * sizeof(T), cudaMemcpyDeviceToDevice, st));
-        k::gemm_simt<T>(false, false, b, d.hid, d.d, h, d.d, w1, d.hid, pre, d.hid, false, st);
+        gemm<T>(false, false, b, d.hid, d.d, h, d.d, w1, d.hid, pre, d.hid, false);
         k::act_fwd<T>(d.act, pre, cz, b * d.hid, st);
-        k::gemm_simt<T>(false, false, b, d.d, d.hid, cz, d.hid, w2, d.d, h, d.d, true, st);
+        gemm<T>(false, false, b, d.d, d.hid, cz, d.hid, w2, d.d, h, d.d, true);
       }
     }
     const int dout = eng->owner_of_deembed();
     eng->hop(h, b * d.d * sizeof(T), where, dout);
     if (eng->mine(dout)) {
-      k::gemm_simt<T>(false, false, b, d.out, d.d, h, d.d, static_cast<const T*>(eng->deembed().w), d.out, pred,
-                      d.out, false, st);
+      gemm<T>(false, false, b, d.out, d.d, h, d.d, static_cast<const T*>(eng->deembed().w), d.out, pred,
+                      d.out, false);
       if (loss_dev) {
         if (d.task == CKF_TASK_REGRESSION)
           k::mse_loss_grad<T>(pred, static_cast<const T*>(y), b, d.out, train ? dpred : nullptr, loss_dev,
@@ -154,10 +164,10 @@ struct MlpBlock final : BlockImpl {
 
     // ---- backward (model.cpp:314-378); h still holds h_final on the de-embed GPU
     if (eng->mine(dout)) {
-      k::gemm_simt<T>(true, false, d.d, d.out, b, h, d.d, dpred, d.out, static_cast<T*>(eng->deembed().g), d.out,
-                      true, st);
-      k::gemm_simt<T>(false, true, b, d.d, d.out, dpred, d.out, static_cast<const T*>(eng->deembed().w), d.out, dh,
-                      d.d, false, st);
+      gemm<T>(true, false, d.d, d.out, b, h, d.d, dpred, d.out, static_cast<T*>(eng->deembed().g), d.out,
+                      true);
+      gemm<T>(false, true, b, d.d, d.out, dpred, d.out, static_cast<const T*>(eng->deembed().w), d.out, dh,
+                      d.d, false);
     }
     where = dout;
     for (size_t ai = applied.size(); ai-- > 0;) {
@@ -172,16 +182,16 @@ struct MlpBlock final : BlockImpl {
       T* gw2 = gw1 + d.d * d.hid;
       const T* cin = cache_in + ai * b * d.d;
       const T* cz = cache_z + ai * b * d.hid;
-      k::gemm_simt<T>(false, true, b, d.hid, d.d, dh, d.d, w2, d.d, dz, d.hid, false, st);   // dz = dh W2^T
+      gemm<T>(false, true, b, d.hid, d.d, dh, d.d, w2, d.d, dz, d.hid, false);   // dz = dh W2^T
       k::act_bwd<T>(d.act, cz, dz, da, b * d.hid, st);                                         // da = dz act'(z)
-      k::gemm_simt<T>(true, false, d.d, d.hid, b, cin, d.d, da, d.hid, gw1, d.hid, true, st);  // gW1 += in^T da
-      k::gemm_simt<T>(true, false, d.hid, d.d, b, cz, d.hid, dh, d.d, gw2, d.d, true, st);     // gW2 += z^T dh
-      k::gemm_simt<T>(false, true, b, d.d, d.hid, da, d.hid, w1, d.hid, dh, d.d, true, st);    // dh += da W1^T
+      gemm<T>(true, false, d.d, d.hid, b, cin, d.d, da, d.hid, gw1, d.hid, true);  // gW1 += in^T da
+      gemm<T>(true, false, d.hid, d.d, b, cz, d.hid, dh, d.d, gw2, d.d, true);     // gW2 += z^T dh
+      gemm<T>(false, true, b, d.d, d.hid, da, d.hid, w1, d.hid, dh, d.d, true);    // dh += da W1^T
     }
     const int ein = eng->owner_of_embed();
     eng->hop(dh, b * d.d * sizeof(T), where, ein);
     if (eng->mine(ein))
-      k::gemm_simt<T>(true, false, d.in, d.d, b, x, d.in, dh, d.d, static_cast<T*>(eng->embed().g), d.d, true, st);
+      gemm<T>(true, false, d.in, d.d, b, x, d.in, dh, d.d, static_cast<T*>(eng->embed().g), d.d, true);
   }
 
   void microbatch(const int* order, const void* x, const void* y, size_t rows, bool train, double* loss_dev) override {

@@ -1,0 +1,28 @@
+#!/usr/bin/env python
+"""Summarise an ncu launch list (--metrics gpu__time_duration.sum --csv) by kernel:
+launches, total device time, share.  Usage: ncu_summary.py launches.csv [--skip N]"""
+import csv
+import collections
+import re
+import sys
+
+
+def main():
+    path = sys.argv[1]
+    rows = [r for r in csv.reader(open(path)) if len(r) > 10 and r[0] != "ID"]
+    tot = collections.OrderedDict()
+    for r in rows:
+        name = re.sub(r"\(.*", "", r[4]).replace("void ", "")
+        ns = float(r[-1].replace(",", ""))
+        t = tot.setdefault(name, [0, 0.0])
+        t[0] += 1
+        t[1] += ns
+    all_ns = sum(v[1] for v in tot.values())
+    print(f"{len(rows)} launches, {all_ns / 1e6:.3f} ms total (cold-cache, serialised ncu replay)")
+    print(f"{'kernel':<90} {'n':>6} {'ms':>10} {'share':>7}")
+    for k, (n, ns) in sorted(tot.items(), key=lambda kv: -kv[1][1]):
+        print(f"{k[:90]:<90} {n:>6} {ns / 1e6:>10.3f} {ns / all_ns:>7.1%}")
+
+
+if __name__ == "__main__":
+    main()
