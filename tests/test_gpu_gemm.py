@@ -22,10 +22,11 @@ def _run(M, N, K, a_mn, b_mn, epi, bn=0, alpha=1.0, seed=0):
     import paper_2506_15461_b200 as P
     from paper_2506_15461_b200._native import check, lib
     g = torch.Generator(device="cuda").manual_seed(seed)
-    pad = 8
-    A = (torch.randn((K, M + pad) if a_mn else (M, K + pad), generator=g, device="cuda") * 0.5).bfloat16()
-    B = (torch.randn((K, N + pad) if b_mn else (N, K + pad), generator=g, device="cuda") * 0.5).bfloat16()
-    ldc = N + pad
+    def ld(x):  # padded row pitch, a multiple of 8 elements (16-byte TMA pitch)
+        return (x + 8 + 7) // 8 * 8
+    A = (torch.randn((K, ld(M)) if a_mn else (M, ld(K)), generator=g, device="cuda") * 0.5).bfloat16()
+    B = (torch.randn((K, ld(N)) if b_mn else (N, ld(K)), generator=g, device="cuda") * 0.5).bfloat16()
+    ldc = ld(N)
     if epi == 0:
         C = torch.zeros((M, ldc), dtype=torch.bfloat16, device="cuda")
     else:

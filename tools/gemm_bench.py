@@ -1,0 +1,45 @@
+#!/usr/bin/env python
+"""Times the tcgen05 bf16 GEMM (ckf_gemm_bf16) at the LLaMA stage shapes against
+torch.matmul (cuBLAS) on the same operands; CUDA events, L2-resident operands."""
+import sys, os, json
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2506_15461_b200  # noqa
+from paper_2506_15461_b200._native import check, lib
+
+SHAPES = [  # (name, M, N, K, a_mn, b_mn, epi)
+    ("qkv_fwd", 8192, 1536, 512, 0, 1, 0), ("o_fwd", 8192, 512, 512, 0, 1, 2), ("gu_fwd", 8192, 4096, 512, 0, 1, 0),
+    ("down_fwd", 8192, 512, 2048, 0, 1, 2), ("lmhead_fwd", 8192, 50304, 512, 0, 1, 0),
+    ("lmhead_dgrad", 8192, 512, 50304, 0, 0, 1), ("lmhead_wgrad", 512, 50304, 8192, 1, 1, 2),
+    ("gu_dgrad", 8192, 512, 4096, 0, 0, 1), ("gu_wgrad", 512, 4096, 8192, 1, 1, 2), ("qkv_wgrad", 512, 1536, 8192, 1, 1, 2),
+    ("sq4096", 4096, 4096, 4096, 0, 0, 0), ("sq8192", 8192, 8192, 8192, 0, 1, 0),
+]
+
+def run(name, M, N, K, a_mn, b_mn, epi, bn=0, iters=20):
+    A = torch.randn((K, M) if a_mn else (M, K), device="cuda").bfloat16()
+    B = torch.randn((K, N) if b_mn else (N, K), device="cuda").bfloat16()
+    C = torch.zeros((M, N), device="cuda", dtype=torch.bfloat16 if epi == 0 else torch.float32)
+    f = lambda: check(lib().ckf_gemm_bf16(M, N, K, A.data_ptr(), A.shape[1], a_mn, B.data_ptr(), B.shape[1], b_mn,
+                                          C.data_ptr(), N, epi, 1.0, bn, None))
+    a = A.t() if a_mn else A
+    b = B if b_mn else B.t()
+    g = lambda: torch.matmul(a, b)
+    res = {}
+    for tag, fn in (("ours", f), ("cublas", g)):
+        for _ in range(3): fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(iters): fn()
+        e1.record(); torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / iters
+        res[tag] = (ms, 2.0 * M * N * K / ms / 1e9)
+    print(json.dumps({"shape": name, "M": M, "N": N, "K": K, "bn": bn, "ours_ms": res["ours"][0],
+                      "ours_tflops": res["ours"][1], "cublas_ms": res["cublas"][0], "cublas_tflops": res["cublas"][1]}))
+
+if __name__ == "__main__":
+    for s in SHAPES:
+        run(*s)
+        if len(sys.argv) > 1:
+            for bn in (128, 256):
+                run(*s, bn=bn)
