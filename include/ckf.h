@@ -124,6 +124,12 @@ int ckf_adam_device(int dtype, void* w, void* m, void* v, void* g, void* w_bf16,
 int ckf_gemm_bf16(int M, int N, int K, const void* A, int lda, int a_mn, const void* B, int ldb, int b_mn, void* C,
                   int ldc, int epi, float alpha, int bn, void* stream);
 
+/* LLaMA token stream (csrc/tokens.cu): rows x (T+1) int32 ids keyed
+ * (data_seed, stream, index) like the reference's batches (dataset.cpp:15-20),
+ * generated on the device, copied to host `out`. */
+int ckf_llama_token_batch(uint64_t data_seed, uint64_t stream, uint64_t index, size_t rows, size_t T, size_t V,
+                          int* out);
+
 /* =====================================================================
  * (3) Device-resident engine: the throughput tier behind
  *     ckfree::pipeline::run_iteration (pipeline.hpp:44-47),
@@ -175,6 +181,15 @@ int ckf_engine_run_iteration(ckf_engine_t e, const int* orders, int m, const voi
 /* loss of forward(model, order, x) against y (model.cpp:279-282,380-382), no update */
 int ckf_engine_eval_loss(ckf_engine_t e, const int* order, const void* x, const void* y, size_t rows,
                          int on_device, double* loss);
+/* one microbatch forward + backward along `order`, ACCUMULATING into the gradient
+ * buffers without an optimizer step (Gradients::accumulate, model.cpp:299-305);
+ * *loss = the microbatch loss.  With ckf_engine_zero_grad / ckf_engine_export_grad
+ * this is the gradient-parity seam (tests/test_model.cpp:109-155 style checks). */
+int ckf_engine_accumulate(ckf_engine_t e, const int* order, const void* x, const void* y, size_t rows, int on_device,
+                          double* loss);
+int ckf_engine_zero_grad(ckf_engine_t e);
+/* which: 0 embedding, 1 de-embedding, 2 stage `stage`; canonical flat layout, fp64 */
+int ckf_engine_export_grad(ckf_engine_t e, int which, int stage, double* g);
 /* predictions of forward(model, order, x) into host fp64 (MLP only) */
 int ckf_engine_predict(ckf_engine_t e, const int* order, const double* x, size_t rows, double* pred);
 

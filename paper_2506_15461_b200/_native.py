@@ -88,6 +88,7 @@ def lib():
         "ckf_k_counter_uniform": (i, [u64, dbl, dbl, dp, sz]),
         "ckf_recover_device": (i, [i, vp, vp, vp, sz, dbl, dbl, vp, vp]),
         "ckf_gemm_bf16": (i, [i, i, i, vp, i, i, vp, i, i, vp, i, i, C.c_float, i, vp]),
+        "ckf_llama_token_batch": (i, [u64, u64, u64, sz, sz, sz, ip]),
         "ckf_adam_device": (i, [i, vp, vp, vp, vp, vp, sz, dbl, dbl, dbl, dbl, i, vp, vp]),
         "ckf_engine_create": (i, [C.POINTER(ModelDesc), C.POINTER(eng)]), "ckf_engine_destroy": (i, [eng]),
         "ckf_engine_param_counts": (i, [eng, C.POINTER(sz), C.POINTER(sz), C.POINTER(sz)]),
@@ -96,6 +97,8 @@ def lib():
         "ckf_engine_run_iteration": (i, [eng, ip, i, vp, vp, sz, i, lng, dp, dp]),
         "ckf_engine_eval_loss": (i, [eng, ip, vp, vp, sz, i, dp]),
         "ckf_engine_predict": (i, [eng, ip, dp, sz, dp]),
+        "ckf_engine_accumulate": (i, [eng, ip, vp, vp, sz, i, dp]), "ckf_engine_zero_grad": (i, [eng]),
+        "ckf_engine_export_grad": (i, [eng, i, i, dp]),
         "ckf_engine_refresh_edge_replicas": (i, [eng]), "ckf_engine_kill_stage": (i, [eng, i]),
         "ckf_engine_recover_stage": (i, [eng, i, i, i, dbl, u64, i, C.POINTER(RecoveryReport)]),
         "ckf_engine_export_stage": (i, [eng, i, dp, dp, dp]), "ckf_engine_import_stage": (i, [eng, i, dp, dp, dp]),

@@ -103,6 +103,13 @@ def gemm(kind: str, a, b, c, m, k, n):
     return c
 
 
+def llama_token_batch(data_seed: int, stream: int, index: int, rows: int, T: int, V: int) -> np.ndarray:
+    """Counter-RNG token stream of the LLaMA block, generated on the GPU (rows x (T+1) int32)."""
+    out = np.zeros((rows, T + 1), np.int32)
+    check(lib().ckf_llama_token_batch(data_seed, stream, index, rows, T, V, _ip(out)))
+    return out
+
+
 # ------------------------------------------------------------- device primitives
 def recover_device(wp, wn, out, omega_prev, omega_next, old_sq=None, stream=0):
     """omega-weighted recovery on torch CUDA tensors (fp32 / fp64 master weights)."""
@@ -211,6 +218,23 @@ class Engine:
         out = C.c_double(0)
         check(lib().ckf_engine_eval_loss(self._h, _ip(order), xp, yp, rows, 1 if on_device else 0, C.byref(out)))
         return out.value
+
+    def accumulate(self, order, x, y=None, on_device=False) -> float:
+        """One microbatch forward + backward accumulating gradients (no optimizer step)."""
+        order = np.ascontiguousarray(order, np.int32)
+        xp, yp, rows = self._inputs(x, y, on_device)
+        out = C.c_double(0)
+        check(lib().ckf_engine_accumulate(self._h, _ip(order), xp, yp, rows, 1 if on_device else 0, C.byref(out)))
+        return out.value
+
+    def zero_grad(self):
+        check(lib().ckf_engine_zero_grad(self._h))
+
+    def export_grad(self, which: str, stage: int = 0) -> np.ndarray:
+        n = {"embed": self.embed_params, "deembed": self.deembed_params, "stage": self.stage_params}[which]
+        g = np.zeros(n)
+        check(lib().ckf_engine_export_grad(self._h, {"embed": 0, "deembed": 1, "stage": 2}[which], stage, _dp(g)))
+        return g
 
     def predict(self, order, x):
         order = np.ascontiguousarray(order, np.int32)

@@ -1,5 +1,6 @@
 // extern "C" entry points of include/ckf.h.  Nothing throws across this line:
 // every call maps internal errors to CKF_E_* codes + ckf_last_error().
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -12,6 +13,8 @@
 #include "host_logic.h"
 
 namespace ckf {
+void llama_token_batch(uint64_t data_seed, uint64_t stream, uint64_t index, size_t rows, size_t T, size_t V, int* out,
+                       cudaStream_t s);
 std::string run_experiment(const std::string& kv, const std::string& trace_text, uint64_t seed);
 int nccl_unique_id(void* out, size_t cap);
 }  // namespace ckf
@@ -389,6 +392,20 @@ int ckf_gemm_bf16(int M, int N, int K, const void* A, int lda, int a_mn, const v
   });
 }
 
+int ckf_llama_token_batch(uint64_t data_seed, uint64_t stream, uint64_t index, size_t rows, size_t T, size_t V,
+                          int* out) {
+  return guard([&] {
+    if (V < 2 || V > (1ull << 31)) ckf::raise(CKF_E_CONFIG, "vocabulary size out of range");
+    int* d = nullptr;
+    const size_t n = rows * (T + 1);
+    CKF_CUDA(cudaMalloc(&d, std::max<size_t>(n, 1) * sizeof(int)));
+    ckf::llama_token_batch(data_seed, stream, index, rows, T, V, d, nullptr);
+    const cudaError_t e = cudaMemcpy(out, d, n * sizeof(int), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    CKF_CUDA(e);
+  });
+}
+
 // ---------------------------------------------------------------- (3) engine
 int ckf_engine_create(const ckf_model_desc* desc, ckf_engine_t* out) {
   return guard([&] {
@@ -422,6 +439,30 @@ int ckf_engine_run_iteration(ckf_engine_t e, const int* orders, int m, const voi
 int ckf_engine_eval_loss(ckf_engine_t e, const int* order, const void* x, const void* y, size_t rows, int on_device,
                          double* loss) {
   return guard([&] { *loss = E(e)->eval_loss(order, x, y, rows, on_device != 0); });
+}
+int ckf_engine_accumulate(ckf_engine_t e, const int* order, const void* x, const void* y, size_t rows, int on_device,
+                          double* loss) {
+  return guard([&] {
+    const double l = E(e)->accumulate(order, x, y, rows, on_device != 0);
+    if (loss) *loss = l;
+  });
+}
+int ckf_engine_zero_grad(ckf_engine_t e) {
+  return guard([&] { E(e)->zero_grad(); });
+}
+int ckf_engine_export_grad(ckf_engine_t e, int which, int stage, double* g) {
+  return guard([&] {
+    ckf::Engine* en = E(e);
+    if (which == 0)
+      en->export_grad(en->embed(), g);
+    else if (which == 1)
+      en->export_grad(en->deembed(), g);
+    else if (which == 2) {
+      if (stage < 1 || static_cast<size_t>(stage) > en->desc().s) ckf::raise(CKF_E_CONFIG, "stage id out of range");
+      en->export_grad(en->stage(stage), g);
+    } else
+      ckf::raise(CKF_E_CONFIG, "which must be 0 (embed), 1 (de-embed) or 2 (stage)");
+  });
 }
 int ckf_engine_predict(ckf_engine_t e, const int* order, const double* x, size_t rows, double* pred) {
   return guard([&] { E(e)->predict(order, x, rows, pred); });

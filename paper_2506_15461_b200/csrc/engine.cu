@@ -409,48 +409,104 @@ void Engine::run_iteration(const int* orders, int m, const void* x, const void* 
     for (size_t i = 0; i < d_.s; ++i) omegas[i] = stages_[i].omega;
 }
 
+void Engine::upload(const void* x, const void* y, size_t rows, const void** xd, const void** yd) {
+  const size_t xcols = d_.block == CKF_BLOCK_MLP ? d_.in : d_.T + 1;
+  if (d_.block == CKF_BLOCK_LLAMA) {
+    void* xb = ws(rows * xcols * sizeof(int), 0);
+    CKF_CUDA(cudaMemcpyAsync(xb, x, rows * xcols * sizeof(int), cudaMemcpyHostToDevice, st_));
+    *xd = xb;
+    *yd = nullptr;
+    return;
+  }
+  const size_t ycols = d_.task == CKF_TASK_REGRESSION ? d_.out : 1;
+  void* tmp = ws(rows * std::max(xcols, ycols) * sizeof(double), 2);
+  void* xb = ws(rows * xcols * master_bytes(), 0);
+  CKF_CUDA(cudaMemcpyAsync(tmp, x, rows * xcols * 8, cudaMemcpyHostToDevice, st_));
+  if (fp64())
+    CKF_CUDA(cudaMemcpyAsync(xb, tmp, rows * xcols * 8, cudaMemcpyDeviceToDevice, st_));
+  else
+    k::convert(static_cast<const double*>(tmp), static_cast<float*>(xb), rows * xcols, st_);
+  void* yb = ws(rows * ycols * (d_.task == CKF_TASK_REGRESSION ? master_bytes() : 4), 1);
+  if (d_.task == CKF_TASK_REGRESSION) {
+    CKF_CUDA(cudaMemcpyAsync(tmp, y, rows * ycols * 8, cudaMemcpyHostToDevice, st_));
+    if (fp64())
+      CKF_CUDA(cudaMemcpyAsync(yb, tmp, rows * ycols * 8, cudaMemcpyDeviceToDevice, st_));
+    else
+      k::convert(static_cast<const double*>(tmp), static_cast<float*>(yb), rows * ycols, st_);
+  } else {
+    std::vector<int> lab(rows);
+    for (size_t i = 0; i < rows; ++i) {
+      const double l = static_cast<const double*>(y)[i];
+      if (l < 0 || l >= static_cast<double>(d_.out)) raise(1, "label out of range for output_dim");
+      lab[i] = static_cast<int>(l);
+    }
+    CKF_CUDA(cudaMemcpyAsync(yb, lab.data(), rows * 4, cudaMemcpyHostToDevice, st_));
+    CKF_CUDA(cudaStreamSynchronize(st_));
+  }
+  *xd = xb;
+  *yd = yb;
+}
+
 double Engine::eval_loss(const int* order, const void* x, const void* y, size_t rows, bool on_device) {
   CKF_CUDA(cudaSetDevice(d_.device));
   validate_order(order, d_.s);
   if (rows == 0) raise(1, "empty batch");
-  if (!on_device) {
-    // reuse the host upload path of run_iteration without training
-    const size_t xcols = d_.block == CKF_BLOCK_MLP ? d_.in : d_.T + 1;
-    if (d_.block == CKF_BLOCK_LLAMA) {
-      void* xb = ws(rows * xcols * sizeof(int), 0);
-      CKF_CUDA(cudaMemcpyAsync(xb, x, rows * xcols * sizeof(int), cudaMemcpyHostToDevice, st_));
-      x = xb;
-    } else {
-      const size_t ycols = d_.task == CKF_TASK_REGRESSION ? d_.out : 1;
-      void* tmp = ws(rows * std::max(xcols, ycols) * sizeof(double), 2);
-      void* xb = ws(rows * xcols * master_bytes(), 0);
-      CKF_CUDA(cudaMemcpyAsync(tmp, x, rows * xcols * 8, cudaMemcpyHostToDevice, st_));
-      if (fp64())
-        CKF_CUDA(cudaMemcpyAsync(xb, tmp, rows * xcols * 8, cudaMemcpyDeviceToDevice, st_));
-      else
-        k::convert(static_cast<const double*>(tmp), static_cast<float*>(xb), rows * xcols, st_);
-      void* yb = ws(rows * ycols * (d_.task == CKF_TASK_REGRESSION ? master_bytes() : 4), 1);
-      if (d_.task == CKF_TASK_REGRESSION) {
-        CKF_CUDA(cudaMemcpyAsync(tmp, y, rows * ycols * 8, cudaMemcpyHostToDevice, st_));
-        if (fp64())
-          CKF_CUDA(cudaMemcpyAsync(yb, tmp, rows * ycols * 8, cudaMemcpyDeviceToDevice, st_));
-        else
-          k::convert(static_cast<const double*>(tmp), static_cast<float*>(yb), rows * ycols, st_);
-      } else {
-        std::vector<int> lab(rows);
-        for (size_t i = 0; i < rows; ++i) lab[i] = static_cast<int>(static_cast<const double*>(y)[i]);
-        CKF_CUDA(cudaMemcpyAsync(yb, lab.data(), rows * 4, cudaMemcpyHostToDevice, st_));
-        CKF_CUDA(cudaStreamSynchronize(st_));
-      }
-      x = xb;
-      y = yb;
-    }
+  if (!on_device) upload(x, y, rows, &x, &y);
+  double l = 0.0;
+  if (d_.block == CKF_BLOCK_LLAMA && rows * d_.T > d_.max_rows) {
+    // token-mean over equal-weight chunks of at most max_rows tokens
+    const size_t cr = std::max<size_t>(1, d_.max_rows / d_.T);
+    const int* xi = static_cast<const int*>(x);
+    std::vector<std::pair<size_t, size_t>> chunks;
+    for (size_t r0 = 0; r0 < rows; r0 += cr) chunks.push_back({r0, std::min(cr, rows - r0)});
+    if (chunks.size() > 64) raise(1, "evaluation batch too large for the engine's max_rows");
+    for (size_t i = 0; i < chunks.size(); ++i)
+      impl_->microbatch(order, xi + chunks[i].first * (d_.T + 1), nullptr, chunks[i].second, false, scal_ + 4010 + i);
+    std::vector<double> ls(chunks.size());
+    CKF_CUDA(cudaMemcpyAsync(ls.data(), scal_ + 4010, ls.size() * sizeof(double), cudaMemcpyDeviceToHost, st_));
+    CKF_CUDA(cudaStreamSynchronize(st_));
+    for (size_t i = 0; i < chunks.size(); ++i) l += ls[i] * static_cast<double>(chunks[i].second);
+    return l / static_cast<double>(rows);
   }
   impl_->microbatch(order, x, y, rows, false, scal_ + 4000);
-  double l = 0.0;
   CKF_CUDA(cudaMemcpyAsync(&l, scal_ + 4000, sizeof(double), cudaMemcpyDeviceToHost, st_));
   CKF_CUDA(cudaStreamSynchronize(st_));
   return l;
+}
+
+double Engine::accumulate(const int* order, const void* x, const void* y, size_t rows, bool on_device) {
+  CKF_CUDA(cudaSetDevice(d_.device));
+  validate_order(order, d_.s);
+  if (rows == 0) raise(1, "empty batch");
+  if (!on_device) upload(x, y, rows, &x, &y);
+  impl_->microbatch(order, x, y, rows, true, scal_ + 4001);
+  double l = 0.0;
+  CKF_CUDA(cudaMemcpyAsync(&l, scal_ + 4001, sizeof(double), cudaMemcpyDeviceToHost, st_));
+  CKF_CUDA(cudaStreamSynchronize(st_));
+  kt_collect();
+  return l;
+}
+
+void Engine::zero_grad() {
+  CKF_CUDA(cudaSetDevice(d_.device));
+  for (auto& g : stages_)
+    if (g.owned && g.n) CKF_CUDA(cudaMemsetAsync(g.g, 0, g.n * master_bytes(), st_));
+  for (ParamGroup* g : {&embed_, &deembed_})
+    if (g->owned && g->n) CKF_CUDA(cudaMemsetAsync(g->g, 0, g->n * master_bytes(), st_));
+  CKF_CUDA(cudaStreamSynchronize(st_));
+}
+
+void Engine::export_grad(ParamGroup& g, double* out) {
+  CKF_CUDA(cudaSetDevice(d_.device));
+  if (!g.owned) raise(3, "parameter group is not resident on this rank");
+  if (fp64()) {
+    CKF_CUDA(cudaMemcpyAsync(out, g.g, g.n * 8, cudaMemcpyDeviceToHost, st_));
+  } else {
+    double* tmp = static_cast<double*>(ws(g.n * 8, 3));
+    k::convert(static_cast<const float*>(g.g), tmp, g.n, st_);
+    CKF_CUDA(cudaMemcpyAsync(out, tmp, g.n * 8, cudaMemcpyDeviceToHost, st_));
+  }
+  CKF_CUDA(cudaStreamSynchronize(st_));
 }
 
 void Engine::predict_device(const int* order, const void* x_dev, size_t rows, void* pred_dev) {

@@ -97,6 +97,10 @@ class Engine {
   void run_iteration(const int* orders, int m, const void* x, const void* y, size_t rows, bool on_device,
                      long iteration, double* loss, double* omegas);
   double eval_loss(const int* order, const void* x, const void* y, size_t rows, bool on_device);
+  // one microbatch forward + backward accumulating into the gradient buffers (no Adam)
+  double accumulate(const int* order, const void* x, const void* y, size_t rows, bool on_device);
+  void zero_grad();
+  void export_grad(ParamGroup& g, double* out);
   void predict(const int* order, const double* x_host, size_t rows, double* pred_host);
   // device-side variants used by the trainer's data path
   void predict_device(const int* order, const void* x_dev, size_t rows, void* pred_dev);
@@ -140,6 +144,8 @@ class Engine {
   void alloc_group(ParamGroup& g, size_t n, bool lowp);
   void free_group(ParamGroup& g);
   void adam_group(ParamGroup& g, double lr, double gscale, double* omega_dev);
+  // uploads host inputs (fp64 rows / int32 tokens) into device buffers; returns device x, y
+  void upload(const void* x, const void* y, size_t rows, const void** xd, const void** yd);
 
   Desc d_;
   cudaStream_t st_ = nullptr;

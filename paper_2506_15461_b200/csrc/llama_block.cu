@@ -1,11 +1,341 @@
-// LLaMA-style block (RMSNorm -> QKV -> RoPE -> causal attention -> O ->
-// RMSNorm -> SwiGLU MLP), bf16 tcgen05 GEMMs or fp32 parity path.
+// LLaMA-style stage block on the bf16 throughput path:
+//   h  = E[tok]                                           (embedding, edge group 0)
+//   per layer:  h += Wo  . attn(rope(RMSNorm(h; g1) Wqkv))
+//               h += Wd  . swiglu(RMSNorm(h; g2) Wgu)
+//   logits = RMSNorm(h; gF) E_inv ; loss = mean CE        (de-embedding, edge group 1)
+// Stage GEMMs run on the tcgen05 kernel (gemm_tc.cu), attention on the flash
+// kernels (attention.cu), everything else on llama_kernels.cu.  The residual
+// stream, gradients, norms and Adam master weights are fp32; GEMM operands
+// and cached activations are bf16.
+//
+// It follows the reference's structure exactly where one exists
+// (/root/reference/proj/src/model.cpp:211-378): stages applied in the
+// microbatch's execution order with a per-applied-block activation cache,
+// gradients accumulated straight into the stage accumulators (GEMM epilogue
+// += instead of Gradients::accumulate, model.cpp:299-305), canonical flat
+// stage layout = blocks in order (model.cpp:117-125).  Per-layer flat layout:
+//   [g1 (d) | Wqkv (d x 3d) | Wo (d x d) | g2 (d) | Wgu (d x 2f) | Wd (f x d)]
+// edge groups: E [V x d];  [gF (d) | E_inv (d x V)].  Weights row-major
+// [fan_in x fan_out] like the reference (model.cpp:27-33).
+#include <vector>
+
 #include "engine.h"
+#include "gemm_tc.h"
+#include "llama_kernels.h"
 
 namespace ckf {
 
-std::unique_ptr<BlockImpl> make_llama_block(Engine*) {
-  raise(1, "LLaMA block not built yet");
+using llama::bf16;
+
+namespace {
+
+struct Off {
+  size_t g1, wqkv, wo, g2, wgu, wd, total;
+};
+Off layer_offsets(size_t d, size_t f) {
+  Off o;
+  o.g1 = 0;
+  o.wqkv = d;
+  o.wo = o.wqkv + 3 * d * d;
+  o.g2 = o.wo + d * d;
+  o.wgu = o.g2 + d;
+  o.wd = o.wgu + 2 * d * f;
+  o.total = o.wd + f * d;
+  return o;
 }
+
+}  // namespace
+
+struct LlamaBlock final : BlockImpl {
+  explicit LlamaBlock(Engine* e) : BlockImpl(e) {
+    const Desc& D = eng->desc();
+    d = D.d;
+    f = D.hid;
+    V = D.out;
+    H = D.heads;
+    T = D.T;
+    hd = d / H;
+    off = layer_offsets(d, f);
+    if (D.in != D.out) raise(1, "LLaMA block: input_dim and output_dim are both the vocabulary size");
+    if (d % 128 || d > 4096) raise(1, "LLaMA block: model_dim must be a multiple of 128 (<= 4096)");
+    if (d % H || (hd != 64 && hd != 128)) raise(1, "LLaMA block: head_dim = model_dim / n_heads must be 64 or 128");
+    if (T % 64) raise(1, "LLaMA block: seq_len must be a multiple of 64");
+    if (f % 64) raise(1, "LLaMA block: ffn width must be a multiple of 64");
+    if (V % 8) raise(1, "LLaMA block: vocabulary size must be a multiple of 8");
+    if (D.prec != CKF_BF16)
+      raise(1, "LLaMA block runs on the bf16 tensor-core path (the fp32/fp64 parity precisions use the residual-MLP "
+               "block)");
+  }
+
+  size_t d, f, V, H, T, hd;
+  Off off;
+
+  size_t stage_params(int sid) const override {
+    return eng->desc().part[static_cast<size_t>(sid - 1)].count() * off.total;
+  }
+  size_t embed_params() const override { return V * d; }
+  size_t deembed_params() const override { return d + d * V; }
+
+  void sample(float* w, size_t n, size_t fan_in, size_t fan_out, uint64_t key) {
+    const double a = std::sqrt(6.0 / static_cast<double>(fan_in + fan_out));  // model.cpp:27-33
+    k::uniform(w, n, key, -a, a, 0, eng->stream());
+  }
+
+  // init streams: the reference's tag scheme (model.cpp:24-25) extended per matrix:
+  //   Wqkv(l) = derive_key(seed, 2l, 1), Wo(l) = (2l, 2), Wgu(l) = (2l+1, 1), Wd(l) = (2l+1, 2);
+  //   E = derive_key(seed, 0), E_inv = derive_key(seed, 1); RMSNorm gains = 1.
+  void init_stage(int sid, uint64_t seed, void* wv) override {
+    float* w = static_cast<float*>(wv);
+    const Range& r = eng->desc().part[static_cast<size_t>(sid - 1)];
+    cudaStream_t st = eng->stream();
+    for (size_t l = r.first; l <= r.last; ++l) {
+      float* b = w + (l - r.first) * off.total;
+      k::fill(b + off.g1, 1.0, d, st);
+      sample(b + off.wqkv, 3 * d * d, d, 3 * d, derive_key(seed, 2 * l, 1));
+      sample(b + off.wo, d * d, d, d, derive_key(seed, 2 * l, 2));
+      k::fill(b + off.g2, 1.0, d, st);
+      sample(b + off.wgu, 2 * d * f, d, 2 * f, derive_key(seed, 2 * l + 1, 1));
+      sample(b + off.wd, f * d, f, d, derive_key(seed, 2 * l + 1, 2));
+    }
+  }
+  void init_edges(uint64_t seed, void* e, void* de) override {
+    if (e) sample(static_cast<float*>(e), V * d, V, d, derive_key(seed, 0));
+    if (de) {
+      k::fill(static_cast<float*>(de), 1.0, d, eng->stream());
+      sample(static_cast<float*>(de) + d, d * V, d, V, derive_key(seed, 1));
+    }
+  }
+
+  // ------------------------------------------------------------ workspace
+  template <typename T_>
+  T_* buf(int slot, size_t elems) {
+    return static_cast<T_*>(eng->ws(elems * sizeof(T_), slot));
+  }
+  struct Cache {
+    float *h_in, *rstd1, *lse, *h_mid, *rstd2;
+    bf16 *xn1, *qkv, *o, *xn2, *gu, *a;
+  };
+  static size_t al(size_t b) { return (b + 255) / 256 * 256; }
+  Cache cache(size_t slot, size_t Mt, size_t rows) {
+    const size_t bytes = al(Mt * d * 4) * 2 + al(Mt * 4) * 2 + al(rows * H * T * 4) + al(Mt * d * 2) * 3 +
+                         al(Mt * 3 * d * 2) + al(Mt * 2 * f * 2) + al(Mt * f * 2);
+    char* p = static_cast<char*>(eng->ws(bytes, 100 + static_cast<int>(slot)));
+    Cache c;
+    auto take = [&](size_t b) {
+      char* r = p;
+      p += al(b);
+      return r;
+    };
+    c.h_in = reinterpret_cast<float*>(take(Mt * d * 4));
+    c.h_mid = reinterpret_cast<float*>(take(Mt * d * 4));
+    c.rstd1 = reinterpret_cast<float*>(take(Mt * 4));
+    c.rstd2 = reinterpret_cast<float*>(take(Mt * 4));
+    c.lse = reinterpret_cast<float*>(take(rows * H * T * 4));
+    c.xn1 = reinterpret_cast<bf16*>(take(Mt * d * 2));
+    c.o = reinterpret_cast<bf16*>(take(Mt * d * 2));
+    c.xn2 = reinterpret_cast<bf16*>(take(Mt * d * 2));
+    c.qkv = reinterpret_cast<bf16*>(take(Mt * 3 * d * 2));
+    c.gu = reinterpret_cast<bf16*>(take(Mt * 2 * f * 2));
+    c.a = reinterpret_cast<bf16*>(take(Mt * f * 2));
+    return c;
+  }
+
+  // ------------------------------------------------------------ timed launch helpers
+  void gemm(int M, int N, int K, const bf16* A, int lda, bool a_mn, const bf16* B, int ldb, bool b_mn, void* C,
+            int ldc, int epi) {
+    tc::GemmDesc g;
+    g.M = M;
+    g.N = N;
+    g.K = K;
+    g.A = A;
+    g.lda = lda;
+    g.a_mn = a_mn;
+    g.B = B;
+    g.ldb = ldb;
+    g.b_mn = b_mn;
+    g.C = C;
+    g.ldc = ldc;
+    g.epi = epi;
+    eng->kt_begin();
+    tc::gemm_bf16(g, eng->stream());
+    const double cb = epi == tc::kStoreBF16 ? 2.0 : epi == tc::kStoreF32 ? 4.0 : 8.0;
+    eng->kt_end(KC_GEMM, 2.0 * M * N * K,
+                2.0 * (static_cast<double>(M) * K + static_cast<double>(K) * N) + cb * M * N);
+  }
+  template <typename F>
+  void timed(int cls, double flops, double bytes, F&& f) {
+    eng->kt_begin();
+    f();
+    eng->kt_end(cls, flops, bytes);
+  }
+
+  // ------------------------------------------------------------ one microbatch
+  void microbatch(const int* order, const void* xv, const void*, size_t rows, bool train, double* loss_dev) override {
+    const Desc& D = eng->desc();
+    cudaStream_t st = eng->stream();
+    const size_t Mt = rows * T;
+    if (Mt > D.max_rows) raise(1, "microbatch tokens exceed the engine's max_rows (tokens per microbatch)");
+    const int* x = static_cast<const int*>(xv);
+    const int Mi = static_cast<int>(Mt), di = static_cast<int>(d), Vi = static_cast<int>(V);
+
+    int* tok = buf<int>(40, Mt);
+    int* lab = buf<int>(41, Mt);
+    float* h = buf<float>(42, Mt * d);
+    float* dh = buf<float>(43, Mt * d);
+    bf16* dh_bf = buf<bf16>(44, Mt * d);
+    float* dxn = buf<float>(45, Mt * d);
+    bf16* scratch_bf = buf<bf16>(46, Mt * std::max(3 * d, 2 * f));  // da / dgu / do / dqkv staging
+    bf16* dgu = buf<bf16>(47, Mt * 2 * f);
+    float* Dsum = buf<float>(48, rows * H * T);
+    const int nblk = llama::rmsnorm_bwd_blocks(Mt);
+    float* gpart = buf<float>(49, static_cast<size_t>(nblk) * d);
+    bf16* xnF = buf<bf16>(50, Mt * d);
+    float* rstdF = buf<float>(51, Mt);
+    float* hF = buf<float>(52, Mt * d);
+    bf16* logits = buf<bf16>(53, Mt * V);
+    double* row_loss = buf<double>(54, Mt);
+
+    llama::split_tokens(x, rows, T, tok, lab, st);
+
+    struct Applied {
+      int sid;
+      size_t li;  // layer index within the stage
+    };
+    std::vector<Applied> applied;
+
+    // ---------------- forward (model.cpp:226-253)
+    int where = eng->owner_of_embed();
+    if (eng->mine(where))
+      timed(KC_NORM, 0.0, Mt * d * 8.0, [&] {
+        llama::embed_fwd(tok, Mt, static_cast<const float*>(eng->embed().w), d, h, st);
+      });
+    for (size_t oi = 0; oi < D.s; ++oi) {
+      const int sid = order[oi];
+      const int own = eng->owner_of_stage(sid);
+      eng->hop(h, Mt * d * 4, where, own);
+      where = own;
+      const Range& r = D.part[static_cast<size_t>(sid - 1)];
+      for (size_t li = 0; li < r.count(); ++li) {
+        const size_t slot = applied.size();
+        applied.push_back({sid, li});
+        if (!eng->mine(own)) continue;
+        layer_fwd(sid, li, cache(slot, Mt, rows), h, rows, Mt);
+      }
+    }
+    const int dout = eng->owner_of_deembed();
+    eng->hop(h, Mt * d * 4, where, dout);
+    if (eng->mine(dout)) {
+      const float* gF = static_cast<const float*>(eng->deembed().w);
+      const bf16* Einv = eng->deembed().wlp + d;
+      timed(KC_NORM, 0.0, Mt * d * 10.0, [&] { llama::rmsnorm_fwd(h, gF, Mt, d, xnF, rstdF, hF, st); });
+      gemm(Mi, Vi, di, xnF, di, false, Einv, Vi, true, logits, Vi, tc::kStoreBF16);
+      timed(KC_LOSS, 0.0, Mt * V * (train ? 6.0 : 2.0), [&] {
+        llama::xent_bf16(logits, lab, Mt, V, static_cast<float>(1.0 / static_cast<double>(Mt)), train ? 1 : 0,
+                         row_loss, st);
+        llama::fold_mean(row_loss, Mt, 1.0 / static_cast<double>(Mt), loss_dev, st);
+      });
+    }
+    if (!train) return;
+
+    // ---------------- backward (model.cpp:314-378)
+    if (eng->mine(dout)) {
+      float* gde = static_cast<float*>(eng->deembed().g);
+      const bf16* Einv = eng->deembed().wlp + d;
+      gemm(di, Vi, Mi, xnF, di, true, logits, Vi, true, gde + d, Vi, tc::kAccF32);   // gE_inv += xnF^T dlogits
+      gemm(Mi, di, Vi, logits, Vi, false, Einv, Vi, false, dxn, di, tc::kStoreF32);  // dxnF = dlogits E_inv^T
+      CKF_CUDA(cudaMemsetAsync(dh, 0, Mt * d * 4, st));
+      timed(KC_NORM, 0.0, Mt * d * 18.0, [&] {
+        llama::rmsnorm_bwd(dxn, hF, static_cast<const float*>(eng->deembed().w), rstdF, Mt, d, dh, dh_bf, gpart, st);
+        llama::gain_fold(gpart, nblk, d, gde, st);
+      });
+    }
+    where = dout;
+    for (size_t ai = applied.size(); ai-- > 0;) {
+      const Applied& a = applied[ai];
+      const int own = eng->owner_of_stage(a.sid);
+      if (own != where) {
+        eng->hop(dh, Mt * d * 4, where, own);
+        if (eng->mine(own)) llama::f32_to_bf16(dh, dh_bf, Mt * d, st);
+      }
+      where = own;
+      if (!eng->mine(own)) continue;
+      layer_bwd(a.sid, a.li, cache(ai, Mt, rows), dh, dh_bf, dxn, scratch_bf, dgu, Dsum, gpart, nblk, rows, Mt);
+    }
+    const int ein = eng->owner_of_embed();
+    eng->hop(dh, Mt * d * 4, where, ein);
+    if (eng->mine(ein)) {
+      void* sc = eng->ws(llama::embed_bwd_scratch(Mt), 55);
+      timed(KC_NORM, 0.0, Mt * d * 12.0, [&] {
+        llama::embed_bwd(tok, Mt, dh, d, static_cast<float*>(eng->embed().g), sc, st);
+      });
+    }
+  }
+
+  const bf16* wbf(int sid, size_t li) { return eng->stage(sid).wlp + li * off.total; }
+  const float* wf(int sid, size_t li) { return static_cast<const float*>(eng->stage(sid).w) + li * off.total; }
+  float* gf(int sid, size_t li) { return static_cast<float*>(eng->stage(sid).g) + li * off.total; }
+
+  double attn_flops_fwd(size_t rows) const {
+    return 2.0 * rows * H * static_cast<double>(T) * T * hd;  // QK^T + PV, causal half
+  }
+
+  void layer_fwd(int sid, size_t li, const Cache& c, float* h, size_t rows, size_t Mt) {
+    cudaStream_t st = eng->stream();
+    const bf16* W = wbf(sid, li);
+    const float* Wf = wf(sid, li);
+    const int Mi = static_cast<int>(Mt), di = static_cast<int>(d), fi = static_cast<int>(f);
+    timed(KC_NORM, 0.0, Mt * d * 10.0, [&] { llama::rmsnorm_fwd(h, Wf + off.g1, Mt, d, c.xn1, c.rstd1, c.h_in, st); });
+    gemm(Mi, 3 * di, di, c.xn1, di, false, W + off.wqkv, 3 * di, true, c.qkv, 3 * di, tc::kStoreBF16);
+    timed(KC_NORM, 0.0, Mt * d * 8.0, [&] { llama::rope(c.qkv, Mt, T, d, H, 0, st); });
+    timed(KC_ATTN, attn_flops_fwd(rows), Mt * d * 8.0, [&] { llama::attn_fwd(c.qkv, rows, T, H, hd, c.o, c.lse, st); });
+    gemm(Mi, di, di, c.o, di, false, W + off.wo, di, true, h, di, tc::kAccF32);
+    timed(KC_NORM, 0.0, Mt * d * 10.0, [&] { llama::rmsnorm_fwd(h, Wf + off.g2, Mt, d, c.xn2, c.rstd2, c.h_mid, st); });
+    gemm(Mi, 2 * fi, di, c.xn2, di, false, W + off.wgu, 2 * fi, true, c.gu, 2 * fi, tc::kStoreBF16);
+    timed(KC_NORM, 0.0, Mt * f * 6.0, [&] { llama::swiglu_fwd(c.gu, Mt, f, c.a, st); });
+    gemm(Mi, di, fi, c.a, fi, false, W + off.wd, di, true, h, di, tc::kAccF32);
+  }
+
+  void layer_bwd(int sid, size_t li, const Cache& c, float* dh, bf16* dh_bf, float* dxn, bf16* sbf, bf16* dgu,
+                 float* Dsum, float* gpart, int nblk, size_t rows, size_t Mt) {
+    cudaStream_t st = eng->stream();
+    const bf16* W = wbf(sid, li);
+    const float* Wf = wf(sid, li);
+    float* G = gf(sid, li);
+    const int Mi = static_cast<int>(Mt), di = static_cast<int>(d), fi = static_cast<int>(f);
+    // MLP half: h_out = h_mid + swiglu(xn2 Wgu) Wd
+    bf16* da = sbf;
+    gemm(fi, di, Mi, c.a, fi, true, dh_bf, di, true, G + off.wd, di, tc::kAccF32);             // gWd += a^T dh
+    gemm(Mi, fi, di, dh_bf, di, false, W + off.wd, di, false, da, fi, tc::kStoreBF16);         // da = dh Wd^T
+    timed(KC_NORM, 0.0, Mt * f * 10.0, [&] { llama::swiglu_bwd(c.gu, da, Mt, f, dgu, st); });
+    gemm(di, 2 * fi, Mi, c.xn2, di, true, dgu, 2 * fi, true, G + off.wgu, 2 * fi, tc::kAccF32);  // gWgu += xn2^T dgu
+    gemm(Mi, di, 2 * fi, dgu, 2 * fi, false, W + off.wgu, 2 * fi, false, dxn, di, tc::kStoreF32);  // dxn2 = dgu Wgu^T
+    timed(KC_NORM, 0.0, Mt * d * 18.0, [&] {
+      llama::rmsnorm_bwd(dxn, c.h_mid, Wf + off.g2, c.rstd2, Mt, d, dh, dh_bf, gpart, st);
+      llama::gain_fold(gpart, nblk, d, G + off.g2, st);
+    });
+    // attention half: h_mid = h_in + attn(rope(xn1 Wqkv)) Wo
+    bf16* d_o = sbf;
+    gemm(di, di, Mi, c.o, di, true, dh_bf, di, true, G + off.wo, di, tc::kAccF32);             // gWo += o^T dh
+    gemm(Mi, di, di, dh_bf, di, false, W + off.wo, di, false, d_o, di, tc::kStoreBF16);        // do = dh Wo^T
+    bf16* dqkv = dgu;  // dgu is dead; Mt x 3d fits in Mt x 2f only if 3d <= 2f
+    if (3 * d > 2 * f) dqkv = static_cast<bf16*>(eng->ws(Mt * 3 * d * 2, 56));
+    timed(KC_ATTN, 2.5 * attn_flops_fwd(rows), Mt * d * 16.0, [&] {
+      llama::attn_bwd(c.qkv, c.o, c.lse, d_o, rows, T, H, hd, dqkv, Dsum, st);
+    });
+    timed(KC_NORM, 0.0, Mt * d * 8.0, [&] { llama::rope(dqkv, Mt, T, d, H, 1, st); });
+    gemm(di, 3 * di, Mi, c.xn1, di, true, dqkv, 3 * di, true, G + off.wqkv, 3 * di, tc::kAccF32);  // gWqkv += xn1^T dqkv
+    gemm(Mi, di, 3 * di, dqkv, 3 * di, false, W + off.wqkv, 3 * di, false, dxn, di, tc::kStoreF32);  // dxn1
+    timed(KC_NORM, 0.0, Mt * d * 18.0, [&] {
+      llama::rmsnorm_bwd(dxn, c.h_in, Wf + off.g1, c.rstd1, Mt, d, dh, dh_bf, gpart, st);
+      llama::gain_fold(gpart, nblk, d, G + off.g1, st);
+    });
+  }
+
+  void predict(const int*, const void*, size_t, void*) override {
+    raise(1, "predict is defined for the residual-MLP block");
+  }
+};
+
+std::unique_ptr<BlockImpl> make_llama_block(Engine* e) { return std::make_unique<LlamaBlock>(e); }
 
 }  // namespace ckf

@@ -1,0 +1,442 @@
+// Bandwidth-bound kernels of the LLaMA-style stage block: embedding gather /
+// deterministic scatter, RMSNorm fwd/bwd (+ gain gradients), RoPE, SwiGLU,
+// cross-entropy over bf16 logits.  One warp per row for the row-wise ops,
+// 128-bit vector loads, warp-shuffle reductions; every reduction has a fixed
+// order so a training run is bit-reproducible (the GPU analogue of the
+// reference's fixed-order reductions, kernels.hpp:10-13).
+#include <cub/device/device_radix_sort.cuh>
+
+#include "common.cuh"
+#include "llama_kernels.h"
+
+namespace ckf::llama {
+namespace {
+
+constexpr int kWarpsPerBlock = 8;
+
+__device__ __forceinline__ float warp_sum_f(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ---------------------------------------------------------------- embedding
+__global__ void embed_fwd_kernel(const int* __restrict__ tok, size_t ntok, const float4* __restrict__ E, size_t d4,
+                                 float4* __restrict__ h) {
+  const size_t t = blockIdx.x * static_cast<size_t>(kWarpsPerBlock) + threadIdx.x / 32;
+  if (t >= ntok) return;
+  const float4* src = E + static_cast<size_t>(tok[t]) * d4;
+  float4* dst = h + t * d4;
+  for (size_t c = threadIdx.x & 31; c < d4; c += 32) dst[c] = src[c];
+}
+
+__global__ void iota_kernel(int* __restrict__ v, size_t n) {
+  const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+  if (i < n) v[i] = static_cast<int>(i);
+}
+
+// one warp per sorted position; the first position of each token segment sums
+// the segment's rows in (stable-sorted = token) order and adds once to gE
+__global__ void embed_bwd_kernel(const int* __restrict__ keys, const int* __restrict__ pos, size_t ntok,
+                                 const float4* __restrict__ dh, size_t d4, float4* __restrict__ gE) {
+  const size_t i = blockIdx.x * static_cast<size_t>(kWarpsPerBlock) + threadIdx.x / 32;
+  if (i >= ntok) return;
+  const int key = keys[i];
+  if (i > 0 && keys[i - 1] == key) return;
+  size_t end = i + 1;
+  while (end < ntok && keys[end] == key) ++end;
+  for (size_t c = threadIdx.x & 31; c < d4; c += 32) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (size_t j = i; j < end; ++j) {
+      const float4 v = dh[static_cast<size_t>(pos[j]) * d4 + c];
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    float4 g = gE[static_cast<size_t>(key) * d4 + c];
+    g.x += acc.x;
+    g.y += acc.y;
+    g.z += acc.z;
+    g.w += acc.w;
+    gE[static_cast<size_t>(key) * d4 + c] = g;
+  }
+}
+
+// ---------------------------------------------------------------- RMSNorm
+constexpr int kMaxV4 = 32;  // d <= 4096
+
+__global__ void rmsnorm_fwd_kernel(const float4* __restrict__ x, const float4* __restrict__ g, size_t rows,
+                                   size_t d4, __nv_bfloat162* __restrict__ y, float* __restrict__ rstd,
+                                   float4* __restrict__ xcopy) {
+  const size_t r = blockIdx.x * static_cast<size_t>(kWarpsPerBlock) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  float4 v[kMaxV4];
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < kMaxV4; ++i) {
+    const size_t c = lane + 32 * static_cast<size_t>(i);
+    if (c < d4) {
+      v[i] = x[r * d4 + c];
+      ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
+    }
+  }
+  ss = warp_sum_f(ss);
+  const float rs = rsqrtf(ss / static_cast<float>(4 * d4) + kNormEps);
+  if (lane == 0) rstd[r] = rs;
+#pragma unroll
+  for (int i = 0; i < kMaxV4; ++i) {
+    const size_t c = lane + 32 * static_cast<size_t>(i);
+    if (c < d4) {
+      const float4 gg = g[c];
+      y[(r * d4 + c) * 2] = __floats2bfloat162_rn(v[i].x * rs * gg.x, v[i].y * rs * gg.y);
+      y[(r * d4 + c) * 2 + 1] = __floats2bfloat162_rn(v[i].z * rs * gg.z, v[i].w * rs * gg.w);
+      if (xcopy) xcopy[r * d4 + c] = v[i];
+    }
+  }
+}
+
+constexpr int kBwdRowsPerBlock = 64;
+
+// dh += rstd*u - x*rstd^3*(u.x)/d with u = g*dy; gain partial += dy*x*rstd
+__global__ void rmsnorm_bwd_kernel(const float4* __restrict__ dy, const float4* __restrict__ x,
+                                   const float4* __restrict__ g, const float* __restrict__ rstd, size_t rows,
+                                   size_t d4, float4* __restrict__ dh, __nv_bfloat162* __restrict__ dh_bf,
+                                   float* __restrict__ gpart) {
+  extern __shared__ float4 sg[];  // [kWarpsPerBlock][d4] gain partials
+  const int w = threadIdx.x / 32, lane = threadIdx.x & 31;
+  float4* mine = sg + static_cast<size_t>(w) * d4;
+  for (size_t c = lane; c < d4; c += 32) mine[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+  const size_t r0 = static_cast<size_t>(blockIdx.x) * kBwdRowsPerBlock;
+  for (size_t r = r0 + w; r < r0 + kBwdRowsPerBlock && r < rows; r += kWarpsPerBlock) {
+    const float rs = rstd[r];
+    float dot = 0.f;
+    for (size_t c = lane; c < d4; c += 32) {
+      const float4 a = dy[r * d4 + c], b = x[r * d4 + c], gg = g[c];
+      dot += gg.x * a.x * b.x + gg.y * a.y * b.y + gg.z * a.z * b.z + gg.w * a.w * b.w;
+    }
+    dot = warp_sum_f(dot);
+    const float coef = rs * rs * rs * dot / static_cast<float>(4 * d4);
+    for (size_t c = lane; c < d4; c += 32) {
+      const float4 a = dy[r * d4 + c], b = x[r * d4 + c], gg = g[c];
+      float4 o = dh[r * d4 + c];
+      o.x += rs * gg.x * a.x - b.x * coef;
+      o.y += rs * gg.y * a.y - b.y * coef;
+      o.z += rs * gg.z * a.z - b.z * coef;
+      o.w += rs * gg.w * a.w - b.w * coef;
+      dh[r * d4 + c] = o;
+      if (dh_bf) {
+        dh_bf[(r * d4 + c) * 2] = __floats2bfloat162_rn(o.x, o.y);
+        dh_bf[(r * d4 + c) * 2 + 1] = __floats2bfloat162_rn(o.z, o.w);
+      }
+      float4 p = mine[c];
+      p.x += a.x * b.x * rs;
+      p.y += a.y * b.y * rs;
+      p.z += a.z * b.z * rs;
+      p.w += a.w * b.w * rs;
+      mine[c] = p;
+    }
+  }
+  __syncthreads();
+  // fold the 8 warps in order -> gpart[block]
+  const size_t d = d4 * 4;
+  const float* sgf = reinterpret_cast<const float*>(sg);
+  for (size_t c = threadIdx.x; c < d; c += blockDim.x) {
+    float acc = 0.f;
+    for (int ww = 0; ww < kWarpsPerBlock; ++ww) acc += sgf[static_cast<size_t>(ww) * d + c];
+    gpart[static_cast<size_t>(blockIdx.x) * d + c] = acc;
+  }
+}
+
+__global__ void gain_fold_kernel(const float* __restrict__ gpart, int nblk, size_t d, float* __restrict__ gg) {
+  const size_t c = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+  if (c >= d) return;
+  float acc = 0.f;
+  for (int b = 0; b < nblk; ++b) acc += gpart[static_cast<size_t>(b) * d + c];
+  gg[c] += acc;
+}
+
+// ---------------------------------------------------------------- RoPE
+__global__ void rope_kernel(__nv_bfloat16* __restrict__ qkv, size_t ntok, size_t T, size_t d, size_t hd, int inverse) {
+  const size_t half = hd / 2;
+  const size_t per_tok = d / 2 * 2;  // (heads*half) pairs for q, same for k
+  const size_t n = ntok * per_tok;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t t = i / per_tok;
+    size_t rem = i % per_tok;
+    const size_t which = rem / (d / 2);  // 0 = q, 1 = k
+    rem %= d / 2;
+    const size_t h = rem / half, j = rem % half;
+    const float pos = static_cast<float>(t % T);
+    const float inv_freq = exp2f(-static_cast<float>(2 * j) / static_cast<float>(hd) * log2f(kRopeTheta));
+    float sn, cs;
+    sincosf(pos * inv_freq, &sn, &cs);
+    if (inverse) sn = -sn;
+    __nv_bfloat16* base = qkv + t * 3 * d + which * d + h * hd;
+    const float x1 = __bfloat162float(base[j]), x2 = __bfloat162float(base[j + half]);
+    base[j] = __float2bfloat16(x1 * cs - x2 * sn);
+    base[j + half] = __float2bfloat16(x2 * cs + x1 * sn);
+  }
+}
+
+// ---------------------------------------------------------------- SwiGLU
+__global__ void swiglu_fwd_kernel(const __nv_bfloat162* __restrict__ gu, size_t ntok, size_t f2,
+                                  __nv_bfloat162* __restrict__ a) {
+  const size_t n = ntok * f2;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t t = i / f2, c = i % f2;
+    const float2 g = __bfloat1622float2(gu[t * 2 * f2 + c]);
+    const float2 u = __bfloat1622float2(gu[t * 2 * f2 + f2 + c]);
+    const float s0 = g.x / (1.f + __expf(-g.x)), s1 = g.y / (1.f + __expf(-g.y));
+    a[i] = __floats2bfloat162_rn(s0 * u.x, s1 * u.y);
+  }
+}
+
+__global__ void swiglu_bwd_kernel(const __nv_bfloat162* __restrict__ gu, const __nv_bfloat162* __restrict__ da,
+                                  size_t ntok, size_t f2, __nv_bfloat162* __restrict__ dgu) {
+  const size_t n = ntok * f2;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t t = i / f2, c = i % f2;
+    const float2 g = __bfloat1622float2(gu[t * 2 * f2 + c]);
+    const float2 u = __bfloat1622float2(gu[t * 2 * f2 + f2 + c]);
+    const float2 dd = __bfloat1622float2(da[i]);
+    const float sg0 = 1.f / (1.f + __expf(-g.x)), sg1 = 1.f / (1.f + __expf(-g.y));
+    const float si0 = g.x * sg0, si1 = g.y * sg1;
+    const float dg0 = dd.x * u.x * sg0 * (1.f + g.x * (1.f - sg0));
+    const float dg1 = dd.y * u.y * sg1 * (1.f + g.y * (1.f - sg1));
+    dgu[t * 2 * f2 + c] = __floats2bfloat162_rn(dg0, dg1);
+    dgu[t * 2 * f2 + f2 + c] = __floats2bfloat162_rn(dd.x * si0, dd.y * si1);
+  }
+}
+
+// ---------------------------------------------------------------- cross-entropy
+constexpr int kXentThreads = 512;
+
+__global__ void __launch_bounds__(kXentThreads) xent_kernel(__nv_bfloat16* __restrict__ logits,
+                                                            const int* __restrict__ labels, size_t V, float gscale,
+                                                            int grad, double* __restrict__ row_loss) {
+  __shared__ float sm[kXentThreads / 32], ss[kXentThreads / 32];
+  const size_t r = blockIdx.x;
+  __nv_bfloat16* row = logits + r * V;
+  float m = -INFINITY, s = 0.f;
+  const bool vec = (V % 8 == 0);
+  if (vec) {
+    const uint4* rv = reinterpret_cast<const uint4*>(row);
+    for (size_t c = threadIdx.x; c < V / 8; c += kXentThreads) {
+      uint4 u = rv[c];
+      const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 f = __bfloat1622float2(p[q]);
+        const float mx = fmaxf(m, fmaxf(f.x, f.y));
+        s = s * __expf(m - mx) + __expf(f.x - mx) + __expf(f.y - mx);
+        m = mx;
+      }
+    }
+  } else {
+    for (size_t c = threadIdx.x; c < V; c += kXentThreads) {
+      const float f = __bfloat162float(row[c]);
+      const float mx = fmaxf(m, f);
+      s = s * __expf(m - mx) + __expf(f - mx);
+      m = mx;
+    }
+  }
+  // warp then block combine of (max, sum)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, s, o);
+    const float mx = fmaxf(m, m2);
+    s = (mx == -INFINITY) ? 0.f : s * __expf(m - mx) + s2 * __expf(m2 - mx);
+    m = mx;
+  }
+  const int w = threadIdx.x / 32, l = threadIdx.x & 31;
+  if (l == 0) {
+    sm[w] = m;
+    ss[w] = s;
+  }
+  __syncthreads();
+  float M = -INFINITY, S = 0.f;
+  for (int i = 0; i < kXentThreads / 32; ++i) {
+    if (sm[i] == -INFINITY) continue;
+    const float mx = fmaxf(M, sm[i]);
+    S = S * __expf(M - mx) + ss[i] * __expf(sm[i] - mx);
+    M = mx;
+  }
+  const float lse = M + __logf(S);
+  const int y = labels[r];
+  if (threadIdx.x == 0) row_loss[r] = static_cast<double>(lse) - static_cast<double>(__bfloat162float(row[y]));
+  __syncthreads();  // everyone has read row[y] before it is overwritten
+  if (!grad) return;
+  if (vec) {
+    uint4* rv = reinterpret_cast<uint4*>(row);
+    for (size_t c = threadIdx.x; c < V / 8; c += kXentThreads) {
+      uint4 u = rv[c];
+      __nv_bfloat162* p = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 f = __bfloat1622float2(p[q]);
+        const size_t j = c * 8 + 2 * q;
+        const float g0 = (__expf(f.x - lse) - (static_cast<int>(j) == y ? 1.f : 0.f)) * gscale;
+        const float g1 = (__expf(f.y - lse) - (static_cast<int>(j + 1) == y ? 1.f : 0.f)) * gscale;
+        p[q] = __floats2bfloat162_rn(g0, g1);
+      }
+      rv[c] = u;
+    }
+  } else {
+    for (size_t c = threadIdx.x; c < V; c += kXentThreads) {
+      const float f = __bfloat162float(row[c]);
+      row[c] = __float2bfloat16((__expf(f - lse) - (static_cast<int>(c) == y ? 1.f : 0.f)) * gscale);
+    }
+  }
+}
+
+__global__ void fold_mean_kernel(const double* __restrict__ v, size_t n, double scale, double* __restrict__ out) {
+  double acc = 0.0;
+  for (size_t i = threadIdx.x; i < n; i += 1024) acc += v[i];
+  acc = block_sum<double, 1024>(acc);
+  if (threadIdx.x == 0) *out = acc * scale;
+}
+
+__global__ void split_tokens_kernel(const int* __restrict__ x, size_t rows, size_t T, int* __restrict__ tok,
+                                    int* __restrict__ lab) {
+  const size_t n = rows * T;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t r = i / T, j = i % T;
+    tok[i] = x[r * (T + 1) + j];
+    lab[i] = x[r * (T + 1) + j + 1];
+  }
+}
+
+__global__ void f2bf_kernel(const float4* __restrict__ x, __nv_bfloat162* __restrict__ y, size_t n4) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const float4 v = x[i];
+    y[2 * i] = __floats2bfloat162_rn(v.x, v.y);
+    y[2 * i + 1] = __floats2bfloat162_rn(v.z, v.w);
+  }
+}
+
+unsigned blocks_for_rows(size_t rows) { return static_cast<unsigned>((rows + kWarpsPerBlock - 1) / kWarpsPerBlock); }
+
+void need_d(size_t d) {
+  if (d % 128 != 0 || d > 4096) raise(1, "LLaMA model_dim must be a multiple of 128 and <= 4096");
+}
+
+}  // namespace
+
+void embed_fwd(const int* tok, size_t ntok, const float* E, size_t d, float* h, cudaStream_t s) {
+  need_d(d);
+  embed_fwd_kernel<<<blocks_for_rows(ntok), 32 * kWarpsPerBlock, 0, s>>>(
+      tok, ntok, reinterpret_cast<const float4*>(E), d / 4, reinterpret_cast<float4*>(h));
+  CKF_LAUNCH_CHECK();
+}
+
+size_t embed_bwd_scratch(size_t ntok) {
+  size_t temp = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, temp, static_cast<const int*>(nullptr), static_cast<int*>(nullptr),
+                                  static_cast<const int*>(nullptr), static_cast<int*>(nullptr),
+                                  static_cast<int>(ntok));
+  return temp + 3 * ntok * sizeof(int) + 1024;
+}
+
+void embed_bwd(const int* tok, size_t ntok, const float* dh, size_t d, float* gE, void* scratch, cudaStream_t s) {
+  need_d(d);
+  size_t temp = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, temp, static_cast<const int*>(nullptr), static_cast<int*>(nullptr),
+                                  static_cast<const int*>(nullptr), static_cast<int*>(nullptr),
+                                  static_cast<int>(ntok));
+  char* p = static_cast<char*>(scratch);
+  int* keys = reinterpret_cast<int*>(p);
+  int* vin = keys + ntok;
+  int* vout = vin + ntok;
+  void* tmp = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(vout + ntok) + 255) & ~uintptr_t(255));
+  iota_kernel<<<static_cast<unsigned>((ntok + 255) / 256), 256, 0, s>>>(vin, ntok);
+  CKF_LAUNCH_CHECK();
+  CKF_CUDA(cub::DeviceRadixSort::SortPairs(tmp, temp, tok, keys, vin, vout, static_cast<int>(ntok), 0, 32, s));
+  embed_bwd_kernel<<<blocks_for_rows(ntok), 32 * kWarpsPerBlock, 0, s>>>(
+      keys, vout, ntok, reinterpret_cast<const float4*>(dh), d / 4, reinterpret_cast<float4*>(gE));
+  CKF_LAUNCH_CHECK();
+}
+
+void rmsnorm_fwd(const float* x, const float* g, size_t rows, size_t d, bf16* y, float* rstd, float* xcopy,
+                 cudaStream_t s) {
+  need_d(d);
+  rmsnorm_fwd_kernel<<<blocks_for_rows(rows), 32 * kWarpsPerBlock, 0, s>>>(
+      reinterpret_cast<const float4*>(x), reinterpret_cast<const float4*>(g), rows, d / 4,
+      reinterpret_cast<__nv_bfloat162*>(y), rstd, reinterpret_cast<float4*>(xcopy));
+  CKF_LAUNCH_CHECK();
+}
+
+int rmsnorm_bwd_blocks(size_t rows) { return static_cast<int>((rows + kBwdRowsPerBlock - 1) / kBwdRowsPerBlock); }
+
+void rmsnorm_bwd(const float* dy, const float* x, const float* g, const float* rstd, size_t rows, size_t d, float* dh,
+                 bf16* dh_bf, float* gpart, cudaStream_t s) {
+  need_d(d);
+  const size_t smem = kWarpsPerBlock * d * sizeof(float);
+  static bool attr = false;
+  if (!attr) {
+    CKF_CUDA(cudaFuncSetAttribute(rmsnorm_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 8 * 4));
+    attr = true;
+  }
+  rmsnorm_bwd_kernel<<<rmsnorm_bwd_blocks(rows), 32 * kWarpsPerBlock, smem, s>>>(
+      reinterpret_cast<const float4*>(dy), reinterpret_cast<const float4*>(x), reinterpret_cast<const float4*>(g),
+      rstd, rows, d / 4, reinterpret_cast<float4*>(dh), reinterpret_cast<__nv_bfloat162*>(dh_bf), gpart);
+  CKF_LAUNCH_CHECK();
+}
+
+void gain_fold(const float* gpart, int nblk, size_t d, float* gg, cudaStream_t s) {
+  gain_fold_kernel<<<static_cast<unsigned>((d + 255) / 256), 256, 0, s>>>(gpart, nblk, d, gg);
+  CKF_LAUNCH_CHECK();
+}
+
+void rope(bf16* qkv, size_t ntok, size_t T, size_t d, size_t heads, int inverse, cudaStream_t s) {
+  const size_t hd = d / heads;
+  if (hd % 2) raise(1, "head_dim must be even for RoPE");
+  rope_kernel<<<grid_for(ntok * d, 256), 256, 0, s>>>(qkv, ntok, T, d, hd, inverse);
+  CKF_LAUNCH_CHECK();
+}
+
+void swiglu_fwd(const bf16* gu, size_t ntok, size_t f, bf16* a, cudaStream_t s) {
+  if (f % 2) raise(1, "ffn width must be even");
+  swiglu_fwd_kernel<<<grid_for(ntok * f / 2, 256), 256, 0, s>>>(reinterpret_cast<const __nv_bfloat162*>(gu), ntok,
+                                                                  f / 2, reinterpret_cast<__nv_bfloat162*>(a));
+  CKF_LAUNCH_CHECK();
+}
+
+void swiglu_bwd(const bf16* gu, const bf16* da, size_t ntok, size_t f, bf16* dgu, cudaStream_t s) {
+  swiglu_bwd_kernel<<<grid_for(ntok * f / 2, 256), 256, 0, s>>>(
+      reinterpret_cast<const __nv_bfloat162*>(gu), reinterpret_cast<const __nv_bfloat162*>(da), ntok, f / 2,
+      reinterpret_cast<__nv_bfloat162*>(dgu));
+  CKF_LAUNCH_CHECK();
+}
+
+void xent_bf16(bf16* logits, const int* labels, size_t rows, size_t V, float grad_scale, int grad, double* row_loss,
+               cudaStream_t s) {
+  if (rows == 0) return;
+  xent_kernel<<<static_cast<unsigned>(rows), kXentThreads, 0, s>>>(logits, labels, V, grad_scale, grad, row_loss);
+  CKF_LAUNCH_CHECK();
+}
+
+void fold_mean(const double* row_loss, size_t rows, double scale, double* out, cudaStream_t s) {
+  fold_mean_kernel<<<1, 1024, 0, s>>>(row_loss, rows, scale, out);
+  CKF_LAUNCH_CHECK();
+}
+
+void split_tokens(const int* x, size_t rows, size_t T, int* tok, int* lab, cudaStream_t s) {
+  split_tokens_kernel<<<grid_for(rows * T, 256), 256, 0, s>>>(x, rows, T, tok, lab);
+  CKF_LAUNCH_CHECK();
+}
+
+void f32_to_bf16(const float* x, bf16* y, size_t n, cudaStream_t s) {
+  if (n % 4) raise(1, "f32_to_bf16 needs n % 4 == 0");
+  f2bf_kernel<<<grid_for(n / 4, 256), 256, 0, s>>>(reinterpret_cast<const float4*>(x),
+                                                    reinterpret_cast<__nv_bfloat162*>(y), n / 4);
+  CKF_LAUNCH_CHECK();
+}
+
+}  // namespace ckf::llama

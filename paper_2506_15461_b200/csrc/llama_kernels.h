@@ -1,0 +1,65 @@
+// Bandwidth kernels of the LLaMA-style stage block (llama_kernels.cu) and the
+// flash attention kernels (attention.cu).  Activations are bf16, the residual
+// stream and every reduction fp32; all reductions are deterministic.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+namespace ckf::llama {
+
+using bf16 = __nv_bfloat16;
+constexpr float kNormEps = 1e-5f;
+constexpr float kRopeTheta = 10000.0f;
+
+// h[t,:] = E[tok[t],:]  (fp32 master embedding rows)
+void embed_fwd(const int* tok, size_t ntok, const float* E, size_t d, float* h, cudaStream_t s);
+// gE[v,:] += sum over t with tok[t]==v of dh[t,:], summed in token order (stable sort) -> deterministic.
+// scratch: >= embed_bwd_scratch(ntok) bytes
+size_t embed_bwd_scratch(size_t ntok);
+void embed_bwd(const int* tok, size_t ntok, const float* dh, size_t d, float* gE, void* scratch, cudaStream_t s);
+
+// y = x * rsqrt(mean(x^2) + eps) * g  -> bf16; rstd[t]; xcopy (optional) = x
+void rmsnorm_fwd(const float* x, const float* g, size_t rows, size_t d, bf16* y, float* rstd, float* xcopy,
+                 cudaStream_t s);
+// dh += d/dx rmsnorm(x) . dy ; dh_bf (optional) = bf16(dh after update);
+// gain partials: gpart[blk, :] for blk < rmsnorm_bwd_blocks(rows) (fold with gain_fold)
+int rmsnorm_bwd_blocks(size_t rows);
+void rmsnorm_bwd(const float* dy, const float* x, const float* g, const float* rstd, size_t rows, size_t d, float* dh,
+                 bf16* dh_bf, float* gpart, cudaStream_t s);
+// gg[:] += sum_blk gpart[blk, :]  (fixed order)
+void gain_fold(const float* gpart, int nblk, size_t d, float* gg, cudaStream_t s);
+
+// rotary embedding on the q and k column blocks of qkv [ntok x 3d] in place;
+// position = t % T; inverse = 1 applies the transpose (backward)
+void rope(bf16* qkv, size_t ntok, size_t T, size_t d, size_t heads, int inverse, cudaStream_t s);
+
+// a = silu(gate) * up ; gu = [gate | up] (ntok x 2f)
+void swiglu_fwd(const bf16* gu, size_t ntok, size_t f, bf16* a, cudaStream_t s);
+// dgu = [da * up * silu'(gate) | da * silu(gate)]
+void swiglu_bwd(const bf16* gu, const bf16* da, size_t ntok, size_t f, bf16* dgu, cudaStream_t s);
+
+// cross-entropy over bf16 logits rows: row_loss[r] = lse - logit[label]; logits are
+// overwritten (in place) with (softmax - onehot) * grad_scale when grad != 0
+void xent_bf16(bf16* logits, const int* labels, size_t rows, size_t V, float grad_scale, int grad, double* row_loss,
+               cudaStream_t s);
+// *out = scale * sum(row_loss[0..rows)) in fixed order
+void fold_mean(const double* row_loss, size_t rows, double scale, double* out, cudaStream_t s);
+
+// labels of the token batch: lab[r*T + j] = x[r*(T+1) + j + 1]; inputs tok[r*T + j] = x[r*(T+1) + j]
+void split_tokens(const int* x, size_t rows, size_t T, int* tok, int* lab, cudaStream_t s);
+
+void f32_to_bf16(const float* x, bf16* y, size_t n, cudaStream_t s);
+
+// ------------------------------------------------------------------ attention (attention.cu)
+// q, k, v: bf16 column blocks of qkv [B*T x 3*H*hd] (row pitch ld = 3*H*hd); o [B*T x H*hd];
+// lse [B*H*T] fp32 (natural log).  Causal, softmax scale 1/sqrt(hd).  hd in {64, 128}.
+void attn_fwd(const bf16* qkv, size_t B, size_t T, size_t H, size_t hd, bf16* o, float* lse, cudaStream_t s);
+// dqkv [B*T x 3*H*hd]; Dsum scratch [B*H*T] fp32.  Deterministic (no atomics).
+void attn_bwd(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, size_t B, size_t T, size_t H,
+              size_t hd, bf16* dqkv, float* Dsum, cudaStream_t s);
+
+}  // namespace ckf::llama

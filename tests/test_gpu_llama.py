@@ -1,0 +1,135 @@
+"""LLaMA-style stage block on the GPU (bf16 tcgen05 GEMMs + flash attention)
+against the CPU fp64 oracle (oracle/llama_oracle.py), through the C-ABI.
+
+Bars (stated here because the reference pins none of the LLaMA arithmetic):
+  * token stream, init streams: bit-exact (integer / fp64->fp32 rounding)
+  * microbatch loss: 2e-2 relative;  gradients: 6e-2 relative Frobenius error
+    per parameter group (bf16 operands, fp32 accumulation)
+  * loss curve over a short run: every point within 1% (north_star)
+  * recovered weights: fp32 recovery kernel within 1e-5 relative (north_star)
+  * two runs with the same seed: bit-identical losses (determinism)
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import llama_oracle as LO  # noqa: E402
+from ckfree_oracle import build_schedule, derive_key, recover_checkfree, standard_order  # noqa: E402
+
+SMALL = LO.LSpec(vocab=512, d=128, layers=4, heads=2, ffn=256, seq_len=64, stages=4)
+
+
+def _engine(spec, rows_per_mb, seed=3, lr=1e-3):
+    import paper_2506_15461_b200 as P
+    from paper_2506_15461_b200 import api
+    ms = api.ModelSpec.llama(spec.vocab, spec.d, spec.layers, spec.heads, spec.ffn, spec.seq_len, spec.stages,
+                             max_tokens=rows_per_mb * spec.seq_len)
+    eng = P.Engine(ms)
+    eng.init(seed, lr)
+    return eng
+
+
+def test_token_stream_bit_exact():
+    from paper_2506_15461_b200 import api
+    for (seed, stream, index, rows, T, V) in [(7, 1, 3, 16, 64, 4096), (1, 2, 0, 5, 128, 50304), (9, 1, 77, 3, 1, 97)]:
+        g = api.llama_token_batch(seed, stream, index, rows, T, V)
+        o = LO.token_batch(seed, stream, index, rows, T, V)
+        assert np.array_equal(g, o), (seed, stream, index)
+
+
+def test_init_bit_exact():
+    eng = _engine(SMALL, 2)
+    ref = LO.LModel(SMALL, 3, 1e-3)
+    for sid in range(1, SMALL.stages + 1):
+        w, m, v = eng.export_stage(sid)
+        assert np.array_equal(w, ref.stages[sid - 1].flat), sid
+        assert not m.any() and not v.any()
+    assert np.array_equal(eng.export_edge(0)[0], ref.embed)
+    assert np.array_equal(eng.export_edge(1)[0], ref.deembed)
+    eng.close()
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+@pytest.mark.parametrize("swapped", [False, True])
+def test_microbatch_loss_and_gradients(swapped):
+    eng = _engine(SMALL, 2)
+    ref = LO.LModel(SMALL, 3, 1e-3)
+    toks = LO.token_batch(11, 1, 1, 2, SMALL.seq_len, SMALL.vocab)
+    order = build_schedule(2, True, SMALL.stages)[0] if swapped else standard_order(SMALL.stages)
+    eng.zero_grad()
+    lg = eng.accumulate(order, toks)
+    lo, gs, ge, gd = LO.microbatch(ref, order, toks)
+    assert abs(lg - lo) <= 2e-2 * abs(lo), (lg, lo)
+    for sid in range(1, SMALL.stages + 1):
+        e = _rel(eng.export_grad("stage", sid), gs[sid - 1])
+        assert e < 6e-2, (sid, e)
+    assert _rel(eng.export_grad("embed"), ge) < 6e-2
+    assert _rel(eng.export_grad("deembed"), gd) < 6e-2
+    # eval path == accumulate path loss
+    assert abs(eng.eval_loss(order, toks) - lg) <= 1e-6 * abs(lg)
+    eng.close()
+
+
+def test_loss_curve_within_1pct_and_deterministic():
+    rows, m, iters = 8, 4, 12
+    curves = []
+    for _ in range(2):
+        eng = _engine(SMALL, rows // m, lr=2e-3)
+        c = []
+        for it in range(1, iters + 1):
+            toks = LO.token_batch(21, 1, it, rows, SMALL.seq_len, SMALL.vocab)
+            loss, om = eng.run_iteration(build_schedule(m, it % 2 == 0, SMALL.stages), toks, None, it)
+            c.append((loss, tuple(om)))
+        curves.append(c)
+        eng.close()
+    assert curves[0] == curves[1], "two identical runs must be bit-identical"
+    ref = LO.LModel(SMALL, 3, 2e-3)
+    for it in range(1, iters + 1):
+        toks = LO.token_batch(21, 1, it, rows, SMALL.seq_len, SMALL.vocab)
+        lo, omo = LO.run_iteration(ref, build_schedule(m, it % 2 == 0, SMALL.stages), toks)
+        lg, omg = curves[0][it - 1]
+        assert abs(lg - lo) <= 1e-2 * abs(lo), (it, lg, lo)
+        np.testing.assert_allclose(omg, omo, rtol=0.15)
+
+
+def test_checkfree_recovery_weights_and_state():
+    import paper_2506_15461_b200 as P
+    eng = _engine(SMALL, 2)
+    toks = LO.token_batch(31, 1, 1, 4, SMALL.seq_len, SMALL.vocab)
+    eng.run_iteration(build_schedule(2, False, SMALL.stages), toks, None, 1)
+    wp, wn = eng.export_stage(1)[0], eng.export_stage(3)[0]
+    op, _, _ = eng.scalars(1)
+    on, _, _ = eng.scalars(3)
+    _, lr2, _ = eng.scalars(2)
+    eng.kill_stage(2)
+    r = eng.recover_stage(2, mode=P._native.CKF_REC_CHECKFREE, reduction_error=False)
+    want, deg = recover_checkfree(wp, wn, op, on)
+    got, m, v = eng.export_stage(2)
+    assert not deg and r.degenerate == 0
+    assert _rel(got, want) <= 1e-5
+    assert not m.any() and not v.any()
+    om2, lr2b, step2 = eng.scalars(2)
+    assert om2 == 0.0 and step2 == 0 and abs(lr2b - 1.1 * lr2) <= 1e-15
+    assert r.latency_ms > 0
+    # the recovered model trains on (finite loss)
+    loss, _ = eng.run_iteration(build_schedule(2, False, SMALL.stages), toks, None, 2)
+    assert np.isfinite(loss)
+    eng.close()
+
+
+def test_full_sizes_attention_and_lm_head_shapes():
+    # LLaMA-124M shapes, one microbatch of 2 sequences: finite, sane loss ~ log(V) at init
+    spec = LO.LSpec(vocab=50304, d=512, layers=4, heads=8, ffn=2048, seq_len=1024, stages=4)
+    eng = _engine(spec, 2)
+    toks = LO.token_batch(5, 1, 1, 2, spec.seq_len, spec.vocab)
+    eng.zero_grad()
+    l = eng.accumulate(standard_order(4), toks)
+    assert abs(l - np.log(50304)) < 1.0, l
+    g = eng.export_grad("stage", 2)
+    assert np.isfinite(g).all() and np.abs(g).sum() > 0
+    eng.close()
