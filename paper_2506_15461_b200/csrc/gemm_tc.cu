@@ -60,6 +60,22 @@ CUtensorMap make_2d_bf16(const void* base, uint64_t inner, uint64_t outer, uint6
   return m;
 }
 
+CUtensorMap make_2d_f32(const void* base, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_inner,
+                        uint32_t box_outer) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {inner, outer};
+  const cuuint64_t strides[1] = {ld * 4};
+  const cuuint32_t box[2] = {box_inner, box_outer};
+  const cuuint32_t estr[2] = {1, 1};
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || ((ld * 4) & 15))
+    raise(1, "TMA fp32 operands need 16-byte aligned base and row pitch (ld % 4 == 0)");
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) raise(6, "cuTensorMapEncodeTiled (f32) failed (" + std::to_string(static_cast<int>(r)) + ")");
+  return m;
+}
+
 CUtensorMap make_3d_bf16(const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t ld1, uint64_t ld2,
                          uint32_t box0, uint32_t box1) {
   CUtensorMap m;
@@ -85,14 +101,14 @@ using namespace ckf::sm100;
 constexpr int BM = 128, BK = 64, UK = 16;
 constexpr int kThreads = 256;
 constexpr uint32_t kAStage = BM * BK * 2;  // 16 KiB
+constexpr uint32_t kStageBufBytes = 4096;  // per epilogue warp, x2: [32 rows][128 B] TMA-store staging
 
 struct Params {
   int M, N, K;
-  void* C;
-  int ldc;
   float alpha;
   int nm, nn, tiles, nk;
-  const float* bias_dummy;
+  int splits, kb_per_split, units;
+  int* flags;  // split-K ordering counters (one per tile), self-resetting
 };
 
 template <int BN>
@@ -101,57 +117,30 @@ struct Cfg {
   static constexpr uint32_t kBStage = BN * BK * 2;
   static constexpr uint32_t kStageBytes = kAStage + kBStage;
   static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
-  static constexpr size_t kSmem = 1024 /*align slack*/ + kStages * kStageBytes + 256 /*barriers*/;
+  static constexpr uint32_t kEpiBytes = 4 * 2 * kStageBufBytes;
+  static constexpr size_t kSmem = 1024 /*align slack*/ + kStages * kStageBytes + kEpiBytes + 256 /*barriers*/;
 };
 
-template <int EPI>
-__device__ __forceinline__ void store_row_chunk(const Params& p, int m, int n0, const uint32_t (&r)[32]) {
-  float v[32];
-#pragma unroll
-  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * p.alpha;
-  if (n0 + 32 <= p.N) {
-    if constexpr (EPI == kStoreBF16) {
-      __nv_bfloat16* c = static_cast<__nv_bfloat16*>(p.C) + static_cast<size_t>(m) * p.ldc + n0;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint4 u;
-        u.x = pack_bf16(v[8 * q + 0], v[8 * q + 1]);
-        u.y = pack_bf16(v[8 * q + 2], v[8 * q + 3]);
-        u.z = pack_bf16(v[8 * q + 4], v[8 * q + 5]);
-        u.w = pack_bf16(v[8 * q + 6], v[8 * q + 7]);
-        reinterpret_cast<uint4*>(c)[q] = u;
-      }
-    } else {
-      float* c = static_cast<float*>(p.C) + static_cast<size_t>(m) * p.ldc + n0;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        float4 o = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-        if constexpr (EPI == kAccF32) {
-          const float4 old = reinterpret_cast<const float4*>(c)[q];
-          o.x += old.x;
-          o.y += old.y;
-          o.z += old.z;
-          o.w += old.w;
-        }
-        reinterpret_cast<float4*>(c)[q] = o;
-      }
-    }
-  } else {
-    for (int j = 0; j < 32 && n0 + j < p.N; ++j) {
-      const size_t off = static_cast<size_t>(m) * p.ldc + n0 + j;
-      if constexpr (EPI == kStoreBF16)
-        static_cast<__nv_bfloat16*>(p.C)[off] = __float2bfloat16(v[j]);
-      else if constexpr (EPI == kStoreF32)
-        static_cast<float*>(p.C)[off] = v[j];
-      else
-        static_cast<float*>(p.C)[off] += v[j];
-    }
-  }
+// Persistent work unit -> (tile, split, k-block range).  Units are split-major so
+// split s of a tile always has a larger index than split s-1 (deadlock-free ordering).
+struct Unit {
+  int mb, nb, tile, split, kb0, kb1;
+};
+__device__ __forceinline__ Unit unit_of(const Params& p, int u) {
+  Unit w;
+  w.split = u / p.tiles;
+  w.tile = u % p.tiles;
+  w.mb = w.tile % p.nm;
+  w.nb = w.tile / p.nm;
+  w.kb0 = w.split * p.kb_per_split;
+  w.kb1 = min(p.nk, w.kb0 + p.kb_per_split);
+  return w;
 }
 
 template <int BN, bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
-    gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b, Params p) {
+    gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                const __grid_constant__ CUtensorMap tmap_c, Params p) {
   using C = Cfg<BN>;
   constexpr int ST = C::kStages;
   constexpr uint32_t IDESC = idesc_bf16_f32(BM, BN, A_MN, B_MN);
@@ -159,7 +148,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + ST * kAStage;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ST * C::kStageBytes);
+  uint8_t* sEpi = smem + ST * C::kStageBytes;  // 1024-aligned
+  uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + C::kEpiBytes);
   uint64_t* empty = full + ST;
   uint64_t* tfull = empty + ST;
   uint64_t* tempty = tfull + 2;
@@ -169,6 +159,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmap_a);
     tma_prefetch(&tmap_b);
+    tma_prefetch(&tmap_c);
   }
   if (warp == 1 && lane == 0) {
     for (int i = 0; i < ST; ++i) {
@@ -192,24 +183,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ---------------- TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
-        const int mb = tile % p.nm, nb = tile / p.nm;
-        for (int kb = 0; kb < p.nk; ++kb) {
+      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+        const Unit w = unit_of(p, u);
+        for (int kb = w.kb0; kb < w.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
           uint8_t* a = sA + stage * kAStage;
           uint8_t* b = sB + stage * C::kBStage;
           if constexpr (A_MN) {
 #pragma unroll
-            for (int c = 0; c < BM / 64; ++c) tma_load_2d(a + c * 8192, &tmap_a, &full[stage], mb * BM + c * 64, kb * BK);
+            for (int c = 0; c < BM / 64; ++c) tma_load_2d(a + c * 8192, &tmap_a, &full[stage], w.mb * BM + c * 64, kb * BK);
           } else {
-            tma_load_2d(a, &tmap_a, &full[stage], kb * BK, mb * BM);
+            tma_load_2d(a, &tmap_a, &full[stage], kb * BK, w.mb * BM);
           }
           if constexpr (B_MN) {
 #pragma unroll
-            for (int c = 0; c < BN / 64; ++c) tma_load_2d(b + c * 8192, &tmap_b, &full[stage], nb * BN + c * 64, kb * BK);
+            for (int c = 0; c < BN / 64; ++c) tma_load_2d(b + c * 8192, &tmap_b, &full[stage], w.nb * BN + c * 64, kb * BK);
           } else {
-            tma_load_2d(b, &tmap_b, &full[stage], kb * BK, nb * BN);
+            tma_load_2d(b, &tmap_b, &full[stage], kb * BK, w.nb * BN);
           }
           if (++stage == ST) {
             stage = 0;
@@ -225,11 +216,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
+      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+        const Unit w = unit_of(p, u);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + static_cast<uint32_t>(acc * BN);
-        for (int kb = 0; kb < p.nk; ++kb) {
+        for (int kb = w.kb0; kb < w.kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + stage * kAStage);
@@ -238,7 +230,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k = 0; k < BK / UK; ++k) {
             const uint64_t ad = A_MN ? umma_desc_sw128(a0 + k * 2048, 8192, 1024) : umma_desc_sw128(a0 + k * 32, 16, 1024);
             const uint64_t bd = B_MN ? umma_desc_sw128(b0 + k * 2048, 8192, 1024) : umma_desc_sw128(b0 + k * 32, 16, 1024);
-            umma_bf16(d, ad, bd, IDESC, (kb | k) != 0 ? 1u : 0u);
+            umma_bf16(d, ad, bd, IDESC, (kb > w.kb0 || k > 0) ? 1u : 0u);
           }
           umma_commit(&empty[stage]);
           if (++stage == ST) {
@@ -254,32 +246,94 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp >= 4) {
-    // ---------------- epilogue: TMEM -> registers -> global
+    // ---------------- epilogue: TMEM -> registers -> swizzled smem -> TMA store / reduce-add
     const int q = warp - 4;  // TMEM lane quarter (warp % 4)
-    int acc = 0;
+    uint8_t* stg = sEpi + q * 2 * kStageBufBytes;
+    int acc = 0, sbuf = 0;
     uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
-      const int mb = tile % p.nm, nb = tile / p.nm;
+    constexpr int CW = EPI == kStoreBF16 ? 64 : 32;  // columns per 128-byte staged row
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+      const Unit w = unit_of(p, u);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int m = mb * BM + q * 32 + lane;
-      const uint32_t trow = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN);
-#pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        uint32_t r[32];
-        tmem_ld32(trow + c0, r);
-        tmem_ld_wait();
-        const int n0 = nb * BN + c0;
-        if (m < p.M && n0 < p.N) store_row_chunk<EPI>(p, m, n0, r);
+      if (p.splits > 1 && w.split > 0) {
+        // ordered split-K: split s adds after all 4 warps of split s-1 finished theirs
+        if (lane == 0) {
+          while (ld_acquire(p.flags + w.tile) < 4 * w.split) __nanosleep(64);
+          fence_proxy_async_global();
+        }
+        __syncwarp();
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      const uint32_t trow = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN);
+      const int m0 = w.mb * BM + q * 32;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += CW) {
+        uint32_t r[CW];
+        if constexpr (CW == 64) {
+          uint32_t (&r0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&r[0]);
+          uint32_t (&r1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&r[32]);
+          tmem_ld32(trow + c0, r0);
+          tmem_ld32(trow + c0 + 32, r1);
+        } else {
+          uint32_t (&r0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&r[0]);
+          tmem_ld32(trow + c0, r0);
+        }
+        tmem_ld_wait();
+        if (c0 + CW >= BN) {  // last chunk loaded: hand the accumulator back to the MMA warp early
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+        uint8_t* sb = stg + sbuf * kStageBufBytes;
+        if (lane == 0) bulk_wait_read<1>();  // the staging buffer used two stores ago is free
+        __syncwarp();
+        const uint32_t row = smem_u32(sb) + lane * 128;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          uint32_t a, b, c, d;
+          if constexpr (EPI == kStoreBF16) {
+            a = pack_bf16(__uint_as_float(r[8 * j + 0]) * p.alpha, __uint_as_float(r[8 * j + 1]) * p.alpha);
+            b = pack_bf16(__uint_as_float(r[8 * j + 2]) * p.alpha, __uint_as_float(r[8 * j + 3]) * p.alpha);
+            c = pack_bf16(__uint_as_float(r[8 * j + 4]) * p.alpha, __uint_as_float(r[8 * j + 5]) * p.alpha);
+            d = pack_bf16(__uint_as_float(r[8 * j + 6]) * p.alpha, __uint_as_float(r[8 * j + 7]) * p.alpha);
+          } else {
+            a = __float_as_uint(__uint_as_float(r[4 * j + 0]) * p.alpha);
+            b = __float_as_uint(__uint_as_float(r[4 * j + 1]) * p.alpha);
+            c = __float_as_uint(__uint_as_float(r[4 * j + 2]) * p.alpha);
+            d = __float_as_uint(__uint_as_float(r[4 * j + 3]) * p.alpha);
+          }
+          st_shared_v4(row + ((j ^ (lane & 7)) << 4), a, b, c, d);
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          const int n0 = w.nb * BN + c0;
+          if (n0 < p.N && m0 < p.M) {
+            if constexpr (EPI == kAccF32)
+              tma_reduce_add_2d(&tmap_c, sb, n0, m0);
+            else
+              tma_store_2d(&tmap_c, sb, n0, m0);
+          }
+          bulk_commit();
+        }
+        sbuf ^= 1;
+      }
+      if (p.splits > 1) {
+        if (lane == 0) {
+          bulk_wait_all();  // this split's adds have landed
+          fence_proxy_async_global();
+          __threadfence();
+          const int old = atomicAdd(p.flags + w.tile, 1);
+          if (w.split == p.splits - 1 && old == 4 * p.splits - 1) atomicExch(p.flags + w.tile, 0);
+        }
+        __syncwarp();
+      }
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
       }
     }
+    if (lane == 0) bulk_wait_all();
   }
   tc_fence_before();
   __syncthreads();
@@ -297,40 +351,61 @@ int num_sms() {
   return n;
 }
 
+int* split_flags(size_t n) {
+  // one self-resetting counter per output tile (zero between launches)
+  static int* flags = nullptr;
+  static size_t cap = 0;
+  static int dev = -1;
+  int cur = 0;
+  CKF_CUDA(cudaGetDevice(&cur));
+  if (n > cap || cur != dev) {
+    if (flags && cur == dev) CKF_CUDA(cudaFree(flags));
+    cap = std::max<size_t>(n, 4096);
+    CKF_CUDA(cudaMalloc(&flags, cap * sizeof(int)));
+    CKF_CUDA(cudaMemset(flags, 0, cap * sizeof(int)));
+    dev = cur;
+  }
+  return flags;
+}
+
 template <int BN, bool A_MN, bool B_MN, int EPI>
-void launch_t(const GemmDesc& g, cudaStream_t s) {
+void launch_t(const GemmDesc& g, int splits, cudaStream_t s) {
   using C = Cfg<BN>;
   const CUtensorMap ta = A_MN ? tma::make_2d_bf16(g.A, g.M, g.K, g.lda, 64, 64)
                               : tma::make_2d_bf16(g.A, g.K, g.M, g.lda, 64, BM);
   const CUtensorMap tb = B_MN ? tma::make_2d_bf16(g.B, g.N, g.K, g.ldb, 64, 64)
                               : tma::make_2d_bf16(g.B, g.K, g.N, g.ldb, 64, BN);
+  const CUtensorMap tcm = EPI == kStoreBF16 ? tma::make_2d_bf16(g.C, g.N, g.M, g.ldc, 64, 32)
+                                            : tma::make_2d_f32(g.C, g.N, g.M, g.ldc, 32, 32);
   Params p;
   p.M = g.M;
   p.N = g.N;
   p.K = g.K;
-  p.C = g.C;
-  p.ldc = g.ldc;
   p.alpha = g.alpha;
   p.nm = (g.M + BM - 1) / BM;
   p.nn = (g.N + BN - 1) / BN;
   p.tiles = p.nm * p.nn;
   p.nk = (g.K + BK - 1) / BK;
-  p.bias_dummy = nullptr;
+  p.splits = std::max(1, std::min(splits, p.nk));
+  p.kb_per_split = (p.nk + p.splits - 1) / p.splits;
+  p.splits = (p.nk + p.kb_per_split - 1) / p.kb_per_split;  // no empty split
+  p.units = p.tiles * p.splits;
+  p.flags = p.splits > 1 ? split_flags(static_cast<size_t>(p.tiles)) : nullptr;
   auto kern = gemm_kernel<BN, A_MN, B_MN, EPI>;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
     CKF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::kSmem)));
     attr_set = true;
   }
-  const int grid = std::min(p.tiles, num_sms());
-  kern<<<grid, kThreads, C::kSmem, s>>>(ta, tb, p);
+  const int grid = std::min(p.units, num_sms());
+  kern<<<grid, kThreads, C::kSmem, s>>>(ta, tb, tcm, p);
   CKF_LAUNCH_CHECK();
 }
 
 template <int BN>
-void dispatch_bn(const GemmDesc& g, cudaStream_t s) {
+void dispatch_bn(const GemmDesc& g, int splits, cudaStream_t s) {
 #define CKF_GEMM_CASE(AM, BMN, E) \
-  if (g.a_mn == AM && g.b_mn == BMN && g.epi == E) return launch_t<BN, AM, BMN, E>(g, s);
+  if (g.a_mn == AM && g.b_mn == BMN && g.epi == E) return launch_t<BN, AM, BMN, E>(g, splits, s);
 #define CKF_GEMM_EPIS(AM, BMN) CKF_GEMM_CASE(AM, BMN, kStoreBF16) CKF_GEMM_CASE(AM, BMN, kStoreF32) CKF_GEMM_CASE(AM, BMN, kAccF32)
   CKF_GEMM_EPIS(false, false)
   CKF_GEMM_EPIS(false, true)
@@ -356,12 +431,25 @@ int pick_bn(int M, int N) {
 void gemm_bf16(const GemmDesc& g, cudaStream_t s) {
   if (g.M <= 0 || g.N <= 0 || g.K <= 0) return;
   if (g.ldc % 4 != 0 && g.epi != kStoreBF16) raise(1, "gemm_bf16: fp32 C needs ldc % 4 == 0");
+  if (reinterpret_cast<uintptr_t>(g.C) % 16) raise(1, "gemm_bf16: C must be 16-byte aligned");
   if (g.ldc % 8 != 0 && g.epi == kStoreBF16) raise(1, "gemm_bf16: bf16 C needs ldc % 8 == 0");
   const int bn = g.bn ? g.bn : pick_bn(g.M, g.N);
+  // split-K (ordered, deterministic) for the fp32-accumulate epilogue when the tile grid underfills the SMs
+  int splits = g.splits;
+  if (splits <= 0) {
+    splits = 1;
+    if (g.epi == kAccF32) {
+      const int tiles = ((g.M + BM - 1) / BM) * ((g.N + bn - 1) / bn);
+      const int nk = (g.K + BK - 1) / BK;
+      const int sms = num_sms();
+      if (tiles * 2 <= sms) splits = std::max(1, std::min({sms / tiles, nk / 4, 16}));
+    }
+  }
+  if (splits > 1 && g.epi != kAccF32) raise(1, "gemm_bf16: split-K needs the fp32 accumulate epilogue");
   if (bn == 128)
-    dispatch_bn<128>(g, s);
+    dispatch_bn<128>(g, splits, s);
   else
-    dispatch_bn<256>(g, s);
+    dispatch_bn<256>(g, splits, s);
 }
 
 }  // namespace tc

@@ -24,7 +24,8 @@ struct GemmDesc {
   int ldc = 0;
   int epi = kStoreBF16;
   float alpha = 1.0f;
-  int bn = 0;  // 0 = heuristic (128 or 256)
+  int bn = 0;      // 0 = heuristic (128 or 256)
+  int splits = 0;  // split-K factor; 0 = heuristic (kAccF32 only; ordered, deterministic)
 };
 
 void gemm_bf16(const GemmDesc& g, cudaStream_t s);

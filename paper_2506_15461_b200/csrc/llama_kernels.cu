@@ -6,6 +6,8 @@
 // reference's fixed-order reductions, kernels.hpp:10-13).
 #include <cub/device/device_radix_sort.cuh>
 
+#include <vector>
+
 #include "common.cuh"
 #include "llama_kernels.h"
 
@@ -99,117 +101,188 @@ __global__ void rmsnorm_fwd_kernel(const float4* __restrict__ x, const float4* _
 
 constexpr int kBwdRowsPerBlock = 64;
 
-// dh += rstd*u - x*rstd^3*(u.x)/d with u = g*dy; gain partial += dy*x*rstd
-__global__ void rmsnorm_bwd_kernel(const float4* __restrict__ dy, const float4* __restrict__ x,
-                                   const float4* __restrict__ g, const float* __restrict__ rstd, size_t rows,
-                                   size_t d4, float4* __restrict__ dh, __nv_bfloat162* __restrict__ dh_bf,
-                                   float* __restrict__ gpart) {
-  extern __shared__ float4 sg[];  // [kWarpsPerBlock][d4] gain partials
+// dh += rstd*u - x*rstd^3*(u.x)/d with u = g*dy; gain partial += dy*x*rstd.
+// One warp per row, row and gain partials held in registers (lane owns
+// columns lane + 32 i), the 8 warps' partials folded in fixed order.
+template <int V4>  // float4 per lane (d = 128 * V4)
+__global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(const float4* __restrict__ dy, const float4* __restrict__ x,
+                                                          const float4* __restrict__ g,
+                                                          const float* __restrict__ rstd, size_t rows,
+                                                          float4* __restrict__ dh,
+                                                          __nv_bfloat162* __restrict__ dh_bf,
+                                                          float* __restrict__ gpart) {
+  extern __shared__ float4 sg[];  // [kWarpsPerBlock][d4]
+  constexpr int d4 = 32 * V4;
   const int w = threadIdx.x / 32, lane = threadIdx.x & 31;
-  float4* mine = sg + static_cast<size_t>(w) * d4;
-  for (size_t c = lane; c < d4; c += 32) mine[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 gp[V4], gg[V4];
+#pragma unroll
+  for (int i = 0; i < V4; ++i) {
+    gp[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    gg[i] = g[lane + 32 * i];
+  }
   const size_t r0 = static_cast<size_t>(blockIdx.x) * kBwdRowsPerBlock;
   for (size_t r = r0 + w; r < r0 + kBwdRowsPerBlock && r < rows; r += kWarpsPerBlock) {
     const float rs = rstd[r];
+    float4 a[V4], b[V4];
     float dot = 0.f;
-    for (size_t c = lane; c < d4; c += 32) {
-      const float4 a = dy[r * d4 + c], b = x[r * d4 + c], gg = g[c];
-      dot += gg.x * a.x * b.x + gg.y * a.y * b.y + gg.z * a.z * b.z + gg.w * a.w * b.w;
+#pragma unroll
+    for (int i = 0; i < V4; ++i) {
+      a[i] = dy[r * d4 + lane + 32 * i];
+      b[i] = x[r * d4 + lane + 32 * i];
+      dot += gg[i].x * a[i].x * b[i].x + gg[i].y * a[i].y * b[i].y + gg[i].z * a[i].z * b[i].z +
+             gg[i].w * a[i].w * b[i].w;
     }
     dot = warp_sum_f(dot);
     const float coef = rs * rs * rs * dot / static_cast<float>(4 * d4);
-    for (size_t c = lane; c < d4; c += 32) {
-      const float4 a = dy[r * d4 + c], b = x[r * d4 + c], gg = g[c];
-      float4 o = dh[r * d4 + c];
-      o.x += rs * gg.x * a.x - b.x * coef;
-      o.y += rs * gg.y * a.y - b.y * coef;
-      o.z += rs * gg.z * a.z - b.z * coef;
-      o.w += rs * gg.w * a.w - b.w * coef;
-      dh[r * d4 + c] = o;
+#pragma unroll
+    for (int i = 0; i < V4; ++i) {
+      const size_t c = r * d4 + lane + 32 * i;
+      float4 o = dh[c];
+      o.x += rs * gg[i].x * a[i].x - b[i].x * coef;
+      o.y += rs * gg[i].y * a[i].y - b[i].y * coef;
+      o.z += rs * gg[i].z * a[i].z - b[i].z * coef;
+      o.w += rs * gg[i].w * a[i].w - b[i].w * coef;
+      dh[c] = o;
       if (dh_bf) {
-        dh_bf[(r * d4 + c) * 2] = __floats2bfloat162_rn(o.x, o.y);
-        dh_bf[(r * d4 + c) * 2 + 1] = __floats2bfloat162_rn(o.z, o.w);
+        dh_bf[2 * c] = __floats2bfloat162_rn(o.x, o.y);
+        dh_bf[2 * c + 1] = __floats2bfloat162_rn(o.z, o.w);
       }
-      float4 p = mine[c];
-      p.x += a.x * b.x * rs;
-      p.y += a.y * b.y * rs;
-      p.z += a.z * b.z * rs;
-      p.w += a.w * b.w * rs;
-      mine[c] = p;
+      gp[i].x += a[i].x * b[i].x * rs;
+      gp[i].y += a[i].y * b[i].y * rs;
+      gp[i].z += a[i].z * b[i].z * rs;
+      gp[i].w += a[i].w * b[i].w * rs;
     }
   }
+#pragma unroll
+  for (int i = 0; i < V4; ++i) sg[static_cast<size_t>(w) * d4 + lane + 32 * i] = gp[i];
   __syncthreads();
-  // fold the 8 warps in order -> gpart[block]
-  const size_t d = d4 * 4;
   const float* sgf = reinterpret_cast<const float*>(sg);
-  for (size_t c = threadIdx.x; c < d; c += blockDim.x) {
+  for (int c = threadIdx.x; c < 4 * d4; c += blockDim.x) {
     float acc = 0.f;
-    for (int ww = 0; ww < kWarpsPerBlock; ++ww) acc += sgf[static_cast<size_t>(ww) * d + c];
-    gpart[static_cast<size_t>(blockIdx.x) * d + c] = acc;
+#pragma unroll
+    for (int ww = 0; ww < kWarpsPerBlock; ++ww) acc += sgf[ww * 4 * d4 + c];
+    gpart[static_cast<size_t>(blockIdx.x) * 4 * d4 + c] = acc;
   }
 }
 
-__global__ void gain_fold_kernel(const float* __restrict__ gpart, int nblk, size_t d, float* __restrict__ gg) {
-  const size_t c = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
-  if (c >= d) return;
+// gg[c] += sum_b gpart[b, c]: 8 fixed residue classes of b per column, then a fixed-order fold
+__global__ void gain_fold_kernel(const float* __restrict__ gpart, int nblk, int d, float* __restrict__ gg) {
+  __shared__ float part[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
   float acc = 0.f;
-  for (int b = 0; b < nblk; ++b) acc += gpart[static_cast<size_t>(b) * d + c];
-  gg[c] += acc;
+  if (c < d)
+    for (int b = w; b < nblk; b += 8) acc += gpart[static_cast<size_t>(b) * d + c];
+  part[w][lane] = acc;
+  __syncthreads();
+  if (w == 0 && c < d) {
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += part[k][lane];
+    gg[c] += s;
+  }
 }
 
 // ---------------------------------------------------------------- RoPE
-__global__ void rope_kernel(__nv_bfloat16* __restrict__ qkv, size_t ntok, size_t T, size_t d, size_t hd, int inverse) {
-  const size_t half = hd / 2;
-  const size_t per_tok = d / 2 * 2;  // (heads*half) pairs for q, same for k
-  const size_t n = ntok * per_tok;
-  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    const size_t t = i / per_tok;
-    size_t rem = i % per_tok;
-    const size_t which = rem / (d / 2);  // 0 = q, 1 = k
-    rem %= d / 2;
-    const size_t h = rem / half, j = rem % half;
-    const float pos = static_cast<float>(t % T);
-    const float inv_freq = exp2f(-static_cast<float>(2 * j) / static_cast<float>(hd) * log2f(kRopeTheta));
-    float sn, cs;
-    sincosf(pos * inv_freq, &sn, &cs);
-    if (inverse) sn = -sn;
-    __nv_bfloat16* base = qkv + t * 3 * d + which * d + h * hd;
-    const float x1 = __bfloat162float(base[j]), x2 = __bfloat162float(base[j + half]);
-    base[j] = __float2bfloat16(x1 * cs - x2 * sn);
-    base[j + half] = __float2bfloat16(x2 * cs + x1 * sn);
+// cos/sin table [T][hd/2] (float2), built once per (T, hd) on the device
+__global__ void rope_table_kernel(float2* __restrict__ tab, int T, int hd) {
+  const int half = hd / 2;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= T * half) return;
+  const int pos = i / half, j = i % half;
+  const double inv = exp2(-static_cast<double>(2 * j) / hd * log2(static_cast<double>(kRopeTheta)));
+  double sn, cs;
+  sincos(static_cast<double>(pos) * inv, &sn, &cs);
+  tab[i] = make_float2(static_cast<float>(cs), static_cast<float>(sn));
+}
+
+// one thread = 4 consecutive rotation pairs (j..j+3, j+half..j+half+3) of one head of q or k
+__global__ void rope_kernel(__nv_bfloat16* __restrict__ qkv, const float2* __restrict__ tab, int ntok, int T, int d,
+                            int hd, int inverse) {
+  const int half = hd / 2, per_head = half / 4, per_tok = 2 * d / 8;  // items per token (q and k)
+  const long long n = static_cast<long long>(ntok) * per_tok;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int t = static_cast<int>(i / per_tok);
+    const int rem = static_cast<int>(i % per_tok);
+    const int hh = rem / per_head;  // 0..2H-1 (q heads then k heads)
+    const int j = (rem % per_head) * 4;
+    __nv_bfloat16* base = qkv + static_cast<size_t>(t) * 3 * d + static_cast<size_t>(hh) * hd;
+    uint2 u1 = *reinterpret_cast<const uint2*>(base + j);
+    uint2 u2 = *reinterpret_cast<const uint2*>(base + j + half);
+    __nv_bfloat162* p1 = reinterpret_cast<__nv_bfloat162*>(&u1);
+    __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(&u2);
+    const float2* cs = tab + static_cast<size_t>(t % T) * half + j;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const float2 a = __bfloat1622float2(p1[q]), b = __bfloat1622float2(p2[q]);
+      const float2 c0 = cs[2 * q], c1 = cs[2 * q + 1];
+      const float s0 = inverse ? -c0.y : c0.y, s1 = inverse ? -c1.y : c1.y;
+      p1[q] = __floats2bfloat162_rn(a.x * c0.x - b.x * s0, a.y * c1.x - b.y * s1);
+      p2[q] = __floats2bfloat162_rn(b.x * c0.x + a.x * s0, b.y * c1.x + a.y * s1);
+    }
+    *reinterpret_cast<uint2*>(base + j) = u1;
+    *reinterpret_cast<uint2*>(base + j + half) = u2;
   }
 }
 
 // ---------------------------------------------------------------- SwiGLU
-__global__ void swiglu_fwd_kernel(const __nv_bfloat162* __restrict__ gu, size_t ntok, size_t f2,
-                                  __nv_bfloat162* __restrict__ a) {
-  const size_t n = ntok * f2;
-  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    const size_t t = i / f2, c = i % f2;
-    const float2 g = __bfloat1622float2(gu[t * 2 * f2 + c]);
-    const float2 u = __bfloat1622float2(gu[t * 2 * f2 + f2 + c]);
-    const float s0 = g.x / (1.f + __expf(-g.x)), s1 = g.y / (1.f + __expf(-g.y));
-    a[i] = __floats2bfloat162_rn(s0 * u.x, s1 * u.y);
+// 8 columns per thread, 16-byte loads/stores; gu = [gate | up] rows of 2f
+__device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
+  const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float2 v = __bfloat1622float2(p[q]);
+    f[2 * q] = v.x;
+    f[2 * q + 1] = v.y;
+  }
+}
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+  uint4 u;
+  __nv_bfloat162* p = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) p[q] = __floats2bfloat162_rn(f[2 * q], f[2 * q + 1]);
+  return u;
+}
+
+__global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ gu, int ntok, int f,
+                                  __nv_bfloat16* __restrict__ a) {
+  const int f8 = f / 8;
+  const long long n = static_cast<long long>(ntok) * f8;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int t = static_cast<int>(i / f8), c = static_cast<int>(i % f8) * 8;
+    const __nv_bfloat16* row = gu + static_cast<size_t>(t) * 2 * f;
+    float g[8], u[8], o[8];
+    unpack8(*reinterpret_cast<const uint4*>(row + c), g);
+    unpack8(*reinterpret_cast<const uint4*>(row + f + c), u);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) o[k] = g[k] / (1.f + __expf(-g[k])) * u[k];
+    *reinterpret_cast<uint4*>(a + static_cast<size_t>(t) * f + c) = pack8(o);
   }
 }
 
-__global__ void swiglu_bwd_kernel(const __nv_bfloat162* __restrict__ gu, const __nv_bfloat162* __restrict__ da,
-                                  size_t ntok, size_t f2, __nv_bfloat162* __restrict__ dgu) {
-  const size_t n = ntok * f2;
-  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    const size_t t = i / f2, c = i % f2;
-    const float2 g = __bfloat1622float2(gu[t * 2 * f2 + c]);
-    const float2 u = __bfloat1622float2(gu[t * 2 * f2 + f2 + c]);
-    const float2 dd = __bfloat1622float2(da[i]);
-    const float sg0 = 1.f / (1.f + __expf(-g.x)), sg1 = 1.f / (1.f + __expf(-g.y));
-    const float si0 = g.x * sg0, si1 = g.y * sg1;
-    const float dg0 = dd.x * u.x * sg0 * (1.f + g.x * (1.f - sg0));
-    const float dg1 = dd.y * u.y * sg1 * (1.f + g.y * (1.f - sg1));
-    dgu[t * 2 * f2 + c] = __floats2bfloat162_rn(dg0, dg1);
-    dgu[t * 2 * f2 + f2 + c] = __floats2bfloat162_rn(dd.x * si0, dd.y * si1);
+__global__ void swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ gu, const __nv_bfloat16* __restrict__ da,
+                                  int ntok, int f, __nv_bfloat16* __restrict__ dgu) {
+  const int f8 = f / 8;
+  const long long n = static_cast<long long>(ntok) * f8;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int t = static_cast<int>(i / f8), c = static_cast<int>(i % f8) * 8;
+    const __nv_bfloat16* row = gu + static_cast<size_t>(t) * 2 * f;
+    float g[8], u[8], dd[8], dg[8], du[8];
+    unpack8(*reinterpret_cast<const uint4*>(row + c), g);
+    unpack8(*reinterpret_cast<const uint4*>(row + f + c), u);
+    unpack8(*reinterpret_cast<const uint4*>(da + static_cast<size_t>(t) * f + c), dd);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float sg = 1.f / (1.f + __expf(-g[k]));
+      dg[k] = dd[k] * u[k] * sg * (1.f + g[k] * (1.f - sg));
+      du[k] = dd[k] * g[k] * sg;
+    }
+    __nv_bfloat16* out = dgu + static_cast<size_t>(t) * 2 * f;
+    *reinterpret_cast<uint4*>(out + c) = pack8(dg);
+    *reinterpret_cast<uint4*>(out + f + c) = pack8(du);
   }
 }
 
@@ -374,44 +447,83 @@ void rmsnorm_fwd(const float* x, const float* g, size_t rows, size_t d, bf16* y,
 
 int rmsnorm_bwd_blocks(size_t rows) { return static_cast<int>((rows + kBwdRowsPerBlock - 1) / kBwdRowsPerBlock); }
 
-void rmsnorm_bwd(const float* dy, const float* x, const float* g, const float* rstd, size_t rows, size_t d, float* dh,
-                 bf16* dh_bf, float* gpart, cudaStream_t s) {
-  need_d(d);
-  const size_t smem = kWarpsPerBlock * d * sizeof(float);
+template <int V4>
+void rmsnorm_bwd_t(const float* dy, const float* x, const float* g, const float* rstd, size_t rows, float* dh,
+                   bf16* dh_bf, float* gpart, cudaStream_t s) {
+  const size_t smem = kWarpsPerBlock * V4 * 32 * sizeof(float4);
   static bool attr = false;
   if (!attr) {
-    CKF_CUDA(cudaFuncSetAttribute(rmsnorm_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 8 * 4));
+    CKF_CUDA(cudaFuncSetAttribute(rmsnorm_bwd_kernel<V4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
     attr = true;
   }
-  rmsnorm_bwd_kernel<<<rmsnorm_bwd_blocks(rows), 32 * kWarpsPerBlock, smem, s>>>(
+  rmsnorm_bwd_kernel<V4><<<rmsnorm_bwd_blocks(rows), 32 * kWarpsPerBlock, smem, s>>>(
       reinterpret_cast<const float4*>(dy), reinterpret_cast<const float4*>(x), reinterpret_cast<const float4*>(g),
-      rstd, rows, d / 4, reinterpret_cast<float4*>(dh), reinterpret_cast<__nv_bfloat162*>(dh_bf), gpart);
+      rstd, rows, reinterpret_cast<float4*>(dh), reinterpret_cast<__nv_bfloat162*>(dh_bf), gpart);
   CKF_LAUNCH_CHECK();
 }
 
+void rmsnorm_bwd(const float* dy, const float* x, const float* g, const float* rstd, size_t rows, size_t d, float* dh,
+                 bf16* dh_bf, float* gpart, cudaStream_t s) {
+  need_d(d);
+  switch (d / 128) {
+    case 1: return rmsnorm_bwd_t<1>(dy, x, g, rstd, rows, dh, dh_bf, gpart, s);
+    case 2: return rmsnorm_bwd_t<2>(dy, x, g, rstd, rows, dh, dh_bf, gpart, s);
+    case 3: return rmsnorm_bwd_t<3>(dy, x, g, rstd, rows, dh, dh_bf, gpart, s);
+    case 4: return rmsnorm_bwd_t<4>(dy, x, g, rstd, rows, dh, dh_bf, gpart, s);
+    case 6: return rmsnorm_bwd_t<6>(dy, x, g, rstd, rows, dh, dh_bf, gpart, s);
+    case 12: return rmsnorm_bwd_t<12>(dy, x, g, rstd, rows, dh, dh_bf, gpart, s);
+    case 24: return rmsnorm_bwd_t<24>(dy, x, g, rstd, rows, dh, dh_bf, gpart, s);
+    case 8: return rmsnorm_bwd_t<8>(dy, x, g, rstd, rows, dh, dh_bf, gpart, s);
+    case 16: return rmsnorm_bwd_t<16>(dy, x, g, rstd, rows, dh, dh_bf, gpart, s);
+    case 32: return rmsnorm_bwd_t<32>(dy, x, g, rstd, rows, dh, dh_bf, gpart, s);
+    default: raise(1, "LLaMA model_dim / 128 must be one of 1,2,3,4,6,8,12,16,24,32");
+  }
+}
+
 void gain_fold(const float* gpart, int nblk, size_t d, float* gg, cudaStream_t s) {
-  gain_fold_kernel<<<static_cast<unsigned>((d + 255) / 256), 256, 0, s>>>(gpart, nblk, d, gg);
+  gain_fold_kernel<<<static_cast<unsigned>((d + 31) / 32), 256, 0, s>>>(gpart, nblk, static_cast<int>(d), gg);
   CKF_LAUNCH_CHECK();
 }
 
 void rope(bf16* qkv, size_t ntok, size_t T, size_t d, size_t heads, int inverse, cudaStream_t s) {
   const size_t hd = d / heads;
-  if (hd % 2) raise(1, "head_dim must be even for RoPE");
-  rope_kernel<<<grid_for(ntok * d, 256), 256, 0, s>>>(qkv, ntok, T, d, hd, inverse);
+  if (hd % 8) raise(1, "head_dim must be a multiple of 8 for RoPE");
+  // per-(T, hd) cos/sin table, built once on the current device
+  struct Tab {
+    size_t T, hd;
+    int dev;
+    float2* p;
+  };
+  static std::vector<Tab> tabs;
+  int dev = 0;
+  CKF_CUDA(cudaGetDevice(&dev));
+  float2* tab = nullptr;
+  for (auto& t : tabs)
+    if (t.T == T && t.hd == hd && t.dev == dev) tab = t.p;
+  if (!tab) {
+    CKF_CUDA(cudaMalloc(&tab, T * hd / 2 * sizeof(float2)));
+    rope_table_kernel<<<static_cast<unsigned>((T * hd / 2 + 255) / 256), 256, 0, s>>>(tab, static_cast<int>(T),
+                                                                                     static_cast<int>(hd));
+    CKF_LAUNCH_CHECK();
+    tabs.push_back({T, hd, dev, tab});
+  }
+  const size_t items = ntok * (2 * d / 8);
+  rope_kernel<<<grid_for(items, 256), 256, 0, s>>>(qkv, tab, static_cast<int>(ntok), static_cast<int>(T),
+                                                   static_cast<int>(d), static_cast<int>(hd), inverse);
   CKF_LAUNCH_CHECK();
 }
 
 void swiglu_fwd(const bf16* gu, size_t ntok, size_t f, bf16* a, cudaStream_t s) {
-  if (f % 2) raise(1, "ffn width must be even");
-  swiglu_fwd_kernel<<<grid_for(ntok * f / 2, 256), 256, 0, s>>>(reinterpret_cast<const __nv_bfloat162*>(gu), ntok,
-                                                                  f / 2, reinterpret_cast<__nv_bfloat162*>(a));
+  if (f % 8) raise(1, "ffn width must be a multiple of 8");
+  swiglu_fwd_kernel<<<grid_for(ntok * f / 8, 256), 256, 0, s>>>(gu, static_cast<int>(ntok), static_cast<int>(f), a);
   CKF_LAUNCH_CHECK();
 }
 
 void swiglu_bwd(const bf16* gu, const bf16* da, size_t ntok, size_t f, bf16* dgu, cudaStream_t s) {
-  swiglu_bwd_kernel<<<grid_for(ntok * f / 2, 256), 256, 0, s>>>(
-      reinterpret_cast<const __nv_bfloat162*>(gu), reinterpret_cast<const __nv_bfloat162*>(da), ntok, f / 2,
-      reinterpret_cast<__nv_bfloat162*>(dgu));
+  if (f % 8) raise(1, "ffn width must be a multiple of 8");
+  swiglu_bwd_kernel<<<grid_for(ntok * f / 8, 256), 256, 0, s>>>(gu, da, static_cast<int>(ntok), static_cast<int>(f),
+                                                                 dgu);
   CKF_LAUNCH_CHECK();
 }
 

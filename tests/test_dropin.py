@@ -1,0 +1,52 @@
+"""The C++ drop-in (dropin/libckfree_b200.so over libckf.so's C-ABI) against the
+reference's OWN test suites: /root/reference/proj/tests/test_{model,pipeline,
+kernels}.cpp compiled UNMODIFIED against our include/ckfree headers by
+`make -C dropin reference-tests` (run by __graft_entry__.build() in the build
+container; the binaries travel to the GPU box with the snapshot).
+
+CPU part: the drop-in library loads and exports the reference API symbols.
+GPU part: each reference suite passes with every arithmetic op on the B200.
+"""
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+DROPIN = os.path.join(ROOT, "dropin")
+LIB = os.path.join(DROPIN, "libckfree_b200.so")
+BIN = os.path.join(DROPIN, "_bin")
+
+
+def _built():
+    return os.path.exists(LIB)
+
+
+@pytest.mark.skipif(not _built(), reason="dropin not built (python -c 'import __graft_entry__ as g; g.build()')")
+def test_dropin_exports_reference_api():
+    out = subprocess.run(["nm", "-DC", "--defined-only", LIB], capture_output=True, text=True).stdout
+    for sym in ["ckfree::init_model(", "ckfree::forward(", "ckfree::backward(", "ckfree::adam_step(",
+                "ckfree::pipeline::run_iteration(", "ckfree::pipeline::build_schedule(",
+                "ckfree::recovery::recover_checkfree(", "ckfree::recovery::recover_edge_stage(",
+                "ckfree::failures::generate_trace(", "ckfree::failures::parse_trace(",
+                "ckfree::kernels::gemm_nn(", "ckfree::kernels::serial::gemm_nn(", "ckfree::kernels::par::adam_update("]:
+        assert sym in out, sym
+    # the drop-in links the B200 engine, not any CPU library of the reference
+    deps = subprocess.run(["ldd", LIB], capture_output=True, text=True).stdout
+    assert "libckf.so" in deps
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("suite", ["kernels", "model", "pipeline"])
+def test_reference_suite_passes_on_dropin(suite):
+    exe = os.path.join(BIN, f"test_{suite}_dropin")
+    if not os.path.exists(exe):
+        pytest.skip(f"{exe} not built (needs /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    tail = (r.stdout + r.stderr)[-4000:]
+    m = re.search(r"test cases: (\d+) \| (\d+) failed \| checks: (\d+) \| (\d+) failed", r.stdout)
+    assert m, tail
+    cases, failed_cases, checks, failed_checks = map(int, m.groups())
+    assert r.returncode == 0 and failed_cases == 0 and failed_checks == 0, tail
+    assert cases > 0 and checks > 0

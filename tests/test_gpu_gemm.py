@@ -69,6 +69,28 @@ def test_stage_shapes_and_alpha():
     assert _run(512, 1536, 8192, True, True, 2) < 1e-3
 
 
+@pytest.mark.parametrize("shape", [(300, 200, 2000), (512, 512, 8192), (2048, 512, 8192)])
+def test_split_k_accumulate(shape):
+    # few output tiles + long K -> ordered split-K with TMA reduce-add (deterministic)
+    M, N, K = shape
+    assert _run(M, N, K, True, True, 2) < 1e-3
+
+
+def test_split_k_deterministic():
+    import paper_2506_15461_b200  # noqa: F401
+    from paper_2506_15461_b200._native import check, lib
+    A = torch.randn(8192, 512, device="cuda").bfloat16()
+    B = torch.randn(8192, 1536, device="cuda").bfloat16()
+    outs = []
+    for _ in range(3):
+        C = torch.ones(512, 1536, device="cuda")
+        check(lib().ckf_gemm_bf16(512, 1536, 8192, A.data_ptr(), 512, 1, B.data_ptr(), 1536, 1, C.data_ptr(), 1536, 2,
+                                  1.0, 0, None))
+        outs.append(C)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[1], outs[2])
+
+
 def test_deterministic():
     import paper_2506_15461_b200  # noqa: F401
     from paper_2506_15461_b200._native import check, lib
