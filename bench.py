@@ -318,6 +318,7 @@ def run_ours(args, w: dict):
         return
 
     peaks, peak_src = load_peaks()
+    sweep = recovery_sweep(P, local, peaks["hbm_gbs"]) if (world == 1 and not args.no_recovery_sweep) else None
     tok = tokens_per_step(w) * (1 if world == 1 else 1)
     value = tok / (ms / 1e3)
     e2e_value = tok / (e2e_ms / 1e3)
@@ -360,10 +361,40 @@ def run_ours(args, w: dict):
                     "ms_per_step": e2e_ms},
             "gpu_launches": launches, "roofline": roof, "step_tflops": step_tflops,
             "flops_per_token": flops_per_token(w), "cpu_baseline": cpu, "clocks": clk.summary(),
-            "recovery": rec}
+            "recovery": rec, "recovery_sweep": sweep}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def recovery_sweep(P, local, hbm_peak):
+    """BASELINE.json configs[4]: omega-weighted neighbour-average reinit over stage sizes
+    10M-400M params (fp32 masters, recovery.cpp:57-73), HBM GB/s of the streaming kernel
+    (12 B/param algorithmic: read W_prev, W_next; write W_stage).  L2 flushed before each rep."""
+    import torch
+    dev = f"cuda:{local}"
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    out = []
+    for n in (10_000_000, 25_000_000, 50_000_000, 100_000_000, 200_000_000, 400_000_000):
+        wp = torch.rand(n, device=dev)
+        wn = torch.rand(n, device=dev)
+        ws = torch.empty(n, device=dev)
+        P.recover_device(wp, wn, ws, 4.0, 1.0)
+        times = []
+        for _ in range(5):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            P.recover_device(wp, wn, ws, 4.0, 1.0)
+            b.record()
+            torch.cuda.synchronize()
+            times.append(a.elapsed_time(b))
+        ms = sorted(times)[len(times) // 2]
+        gbs = 12.0 * n / (ms / 1e3) / 1e9
+        out.append({"params": n, "ms": ms, "gbs": gbs, "frac_hbm": gbs / hbm_peak})
+        del wp, wn, ws
+    torch.cuda.empty_cache()
+    return out
 
 
 def main():
@@ -374,6 +405,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default=DEFAULT_WORKLOAD)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-recovery-sweep", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

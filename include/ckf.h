@@ -62,6 +62,17 @@ int ckf_even_partition(size_t layers, size_t stages, size_t* out);
 /* m execution orders of length s (standard, or swapped at even positions) */
 int ckf_build_schedule(int m, int swapped_half, int s, int* out);
 
+/* Multi-GPU pipeline plan: the global op sequence of one iteration for a
+ * stage -> rank placement (stage_rank[s]), exactly as every rank of the engine
+ * issues it.  6 ints per op: phase (0 fwd / 1 bwd), microbatch, kind
+ * (0 embed fwd, 1 stage fwd, 2 transfer, 3 head = loss + head backward,
+ * 4 stage bwd, 5 embed bwd), rank (transfer: source), arg (stage id, or the
+ * transfer's destination rank), aux (transfer: 0 activations, 1 gradients).
+ * schedule: 0 = forward+backward per microbatch (pipeline.cpp:66-81 order),
+ * 1 = GPipe (all forwards, then all backwards in microbatch order). */
+int ckf_pipeline_plan(int s, int m, const int* orders, const int* stage_rank, int schedule, int* out, int cap_ops,
+                      int* n_ops);
+
 /* =====================================================================
  * (1) L1 kernel seam.  Replaces the dispatching wrappers of
  *     ckfree::kernels (include/ckfree/kernels.hpp:26-69,
@@ -123,6 +134,16 @@ int ckf_adam_device(int dtype, void* w, void* m, void* v, void* g, void* w_bf16,
  *   bn   = 0 (heuristic), 128 or 256: N tile.  Device pointers; lda/ldb % 8 == 0. */
 int ckf_gemm_bf16(int M, int N, int K, const void* A, int lda, int a_mn, const void* B, int ldb, int b_mn, void* C,
                   int ldc, int epi, float alpha, int bn, void* stream);
+
+/* Causal attention of the LLaMA block on device bf16 buffers: qkv [B*T x 3*H*hd]
+ * (q | k | v column blocks), o [B*T x H*hd], lse [B*H*T] fp32 (natural log).
+ * impl: 0 = default for the shape, 1 = mma.sync flash kernel, 2 = tcgen05/TMEM
+ * kernel (head_dim 64, T % 128 == 0).  Backward: dout [B*T x H*hd] ->
+ * dqkv [B*T x 3*H*hd]; Dsum = [B*H*T] fp32 scratch. */
+int ckf_attention_fwd(const void* qkv, size_t B, size_t T, size_t H, size_t hd, void* o, float* lse, int impl,
+                      void* stream);
+int ckf_attention_bwd(const void* qkv, const void* o, const float* lse, const void* dout, size_t B, size_t T,
+                      size_t H, size_t hd, void* dqkv, float* Dsum, int impl, void* stream);
 
 /* LLaMA token stream (csrc/tokens.cu): rows x (T+1) int32 ids keyed
  * (data_seed, stream, index) like the reference's batches (dataset.cpp:15-20),
@@ -229,6 +250,14 @@ int ckf_engine_get_scalars(ckf_engine_t e, int stage, double* omega, double* lr,
 int ckf_engine_set_scalars(ckf_engine_t e, int stage, double omega, double lr, long step);
 int ckf_engine_get_edge_scalars(ckf_engine_t e, double* lr, long* step_embed, long* step_deembed);
 int ckf_engine_set_edge_scalars(ckf_engine_t e, double lr, long step_embed, long step_deembed);
+
+/* iteration schedule: 0 = sequential (default on one GPU), 1 = GPipe (default once attached to >1 rank) */
+int ckf_engine_set_schedule(ckf_engine_t e, int mode);
+/* Hop log for a VIRTUAL placement (stage -> rank), used to check on one GPU that
+ * the engine's stage transfers match ckf_pipeline_plan: when enabled, every
+ * cross-rank transfer the placement implies is recorded as (src, dst, bytes). */
+int ckf_engine_hop_log(ckf_engine_t e, int nranks, const int* stage_rank);
+int ckf_engine_get_hop_log(ckf_engine_t e, long* out, int cap_triples, int* n_triples);
 
 /* launches of the engine's own kernels since creation (evidence for gpu_launches) */
 long ckf_engine_kernel_launches(ckf_engine_t e);

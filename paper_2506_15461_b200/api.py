@@ -60,6 +60,22 @@ def build_schedule(m: int, swapped_half: bool, s: int):
     return [[out[k * s + j] for j in range(s)] for k in range(m)]
 
 
+PLAN_KINDS = ("embed_fwd", "stage_fwd", "xfer", "head", "stage_bwd", "embed_bwd")
+
+
+def pipeline_plan(orders, stage_rank, schedule: int = 1):
+    """Global op sequence of one iteration for a stage -> rank placement (ckf_pipeline_plan)."""
+    orders = np.ascontiguousarray(orders, np.int32)
+    m, s = orders.shape
+    sr = np.ascontiguousarray(stage_rank, np.int32)
+    cap = 8 * m * (s + 4) + 16
+    out = np.zeros(6 * cap, np.int32)
+    n = C.c_int(0)
+    check(lib().ckf_pipeline_plan(s, m, _ip(orders.reshape(-1)), _ip(sr), schedule, _ip(out), cap, C.byref(n)))
+    return [dict(phase=int(o[0]), mb=int(o[1]), kind=PLAN_KINDS[o[2]], rank=int(o[3]), arg=int(o[4]),
+                 aux=int(o[5])) for o in out[:6 * n.value].reshape(-1, 6)]
+
+
 # ------------------------------------------------------------- L1 seam (kernels.hpp)
 def recover_checkfree(w_prev, w_next, omega_prev: float, omega_next: float):
     """recovery::recover_checkfree (src/recovery.cpp:57-73) on the GPU, fp64."""
@@ -290,6 +306,21 @@ class Engine:
 
     def sync(self):
         check(lib().ckf_engine_sync(self._h))
+
+    def set_schedule(self, mode: int):
+        """0 = forward+backward per microbatch, 1 = GPipe (all forwards, then all backwards)."""
+        check(lib().ckf_engine_set_schedule(self._h, mode))
+
+    def hop_log(self, stage_rank=None):
+        """Enable (stage_rank given) or read back the virtual-placement transfer log [(src, dst, bytes)]."""
+        if stage_rank is not None:
+            self._vr = np.ascontiguousarray(stage_rank, np.int32)
+            check(lib().ckf_engine_hop_log(self._h, int(self._vr.max()) + 1, _ip(self._vr)))
+            return None
+        out = (C.c_long * (3 * 65536))()
+        n = C.c_int(0)
+        check(lib().ckf_engine_get_hop_log(self._h, out, 65536, C.byref(n)))
+        return [(out[3 * i], out[3 * i + 1], out[3 * i + 2]) for i in range(n.value)]
 
     def kernel_launches(self) -> int:
         return lib().ckf_engine_kernel_launches(self._h)

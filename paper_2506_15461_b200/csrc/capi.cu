@@ -11,6 +11,7 @@
 #include "engine.h"
 #include "gemm_tc.h"
 #include "host_logic.h"
+#include "llama_kernels.h"
 
 namespace ckf {
 void llama_token_batch(uint64_t data_seed, uint64_t stream, uint64_t index, size_t rows, size_t T, size_t V, int* out,
@@ -145,6 +146,26 @@ int ckf_parse_trace(const char* text, char* out, size_t cap) {
     const std::string s = ckf::host::serialize_trace(ckf::host::parse_trace(text ? text : ""));
     if (s.size() + 1 > cap) ckf::raise(CKF_E_USAGE, "output buffer too small");
     std::memcpy(out, s.c_str(), s.size() + 1);
+  });
+}
+int ckf_pipeline_plan(int s, int m, const int* orders, const int* stage_rank, int schedule, int* out, int cap_ops,
+                      int* n_ops) {
+  return guard([&] {
+    if (s < 1 || m < 1) ckf::raise(CKF_E_CONFIG, "pipeline plan needs s >= 1 and m >= 1");
+    const auto ops = ckf::host::pipeline_plan(
+        s, m, std::vector<int>(orders, orders + static_cast<size_t>(s) * static_cast<size_t>(m)),
+        std::vector<int>(stage_rank, stage_rank + s), schedule);
+    if (static_cast<int>(ops.size()) > cap_ops) ckf::raise(CKF_E_USAGE, "output buffer too small");
+    for (size_t i = 0; i < ops.size(); ++i) {
+      int* o = out + 6 * i;
+      o[0] = ops[i].phase;
+      o[1] = ops[i].mb;
+      o[2] = ops[i].kind;
+      o[3] = ops[i].rank;
+      o[4] = ops[i].arg;
+      o[5] = ops[i].aux;
+    }
+    *n_ops = static_cast<int>(ops.size());
   });
 }
 int ckf_consecutive_conflicts(const char* text, long* out, int cap_pairs, int* n_out) {
@@ -392,6 +413,28 @@ int ckf_gemm_bf16(int M, int N, int K, const void* A, int lda, int a_mn, const v
   });
 }
 
+int ckf_attention_fwd(const void* qkv, size_t B, size_t T, size_t H, size_t hd, void* o, float* lse, int impl,
+                      void* stream) {
+  return guard([&] {
+    auto st = static_cast<cudaStream_t>(stream);
+    const auto* q = static_cast<const __nv_bfloat16*>(qkv);
+    auto* out = static_cast<__nv_bfloat16*>(o);
+    const bool tc = impl == 2 || (impl == 0 && ckf::llama::attn_fwd_tc_supported(T, hd));
+    if (tc)
+      ckf::llama::attn_fwd_tc(q, B, T, H, hd, out, lse, st);
+    else
+      ckf::llama::attn_fwd(q, B, T, H, hd, out, lse, st);
+  });
+}
+int ckf_attention_bwd(const void* qkv, const void* o, const float* lse, const void* dout, size_t B, size_t T,
+                      size_t H, size_t hd, void* dqkv, float* Dsum, int impl, void* stream) {
+  return guard([&] {
+    if (impl == 2) ckf::raise(CKF_E_CONFIG, "tcgen05 attention backward: not built yet");
+    ckf::llama::attn_bwd(static_cast<const __nv_bfloat16*>(qkv), static_cast<const __nv_bfloat16*>(o), lse,
+                         static_cast<const __nv_bfloat16*>(dout), B, T, H, hd, static_cast<__nv_bfloat16*>(dqkv), Dsum,
+                         static_cast<cudaStream_t>(stream));
+  });
+}
 int ckf_llama_token_batch(uint64_t data_seed, uint64_t stream, uint64_t index, size_t rows, size_t T, size_t V,
                           int* out) {
   return guard([&] {
@@ -520,6 +563,21 @@ int ckf_engine_set_edge_scalars(ckf_engine_t e, double lr, long se, long sd) {
     E(e)->edge_lr = lr;
     E(e)->embed().step = se;
     E(e)->deembed().step = sd;
+  });
+}
+int ckf_engine_set_schedule(ckf_engine_t e, int mode) {
+  return guard([&] { E(e)->set_schedule(mode); });
+}
+int ckf_engine_hop_log(ckf_engine_t e, int nranks, const int* stage_rank) {
+  return guard([&] { E(e)->hop_log_enable(nranks, stage_rank); });
+}
+int ckf_engine_get_hop_log(ckf_engine_t e, long* out, int cap_triples, int* n_triples) {
+  return guard([&] {
+    const auto& l = E(e)->hop_log();
+    const int n = static_cast<int>(l.size() / 3);
+    if (n > cap_triples) ckf::raise(CKF_E_USAGE, "output buffer too small");
+    std::copy(l.begin(), l.end(), out);
+    *n_triples = n;
   });
 }
 long ckf_engine_kernel_launches(ckf_engine_t) { return ckf::launch_counter(); }

@@ -39,6 +39,7 @@ struct NcclApi {
   int (*CommDestroy)(void*) = nullptr;
   int (*Send)(const void*, size_t, int, int, void*, cudaStream_t) = nullptr;
   int (*Recv)(void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*AllReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
   int (*GroupStart)() = nullptr;
   int (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(int) = nullptr;
@@ -57,10 +58,12 @@ NcclApi& nccl() {
       api.CommDestroy = reinterpret_cast<int (*)(void*)>(dlsym(h, "ncclCommDestroy"));
       api.Send = reinterpret_cast<int (*)(const void*, size_t, int, int, void*, cudaStream_t)>(dlsym(h, "ncclSend"));
       api.Recv = reinterpret_cast<int (*)(void*, size_t, int, int, void*, cudaStream_t)>(dlsym(h, "ncclRecv"));
+      api.AllReduce = reinterpret_cast<int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t)>(
+          dlsym(h, "ncclAllReduce"));
       api.GroupStart = reinterpret_cast<int (*)()>(dlsym(h, "ncclGroupStart"));
       api.GroupEnd = reinterpret_cast<int (*)()>(dlsym(h, "ncclGroupEnd"));
       api.GetErrorString = reinterpret_cast<const char* (*)(int)>(dlsym(h, "ncclGetErrorString"));
-      api.ok = api.GetUniqueId && api.CommInitRank && api.Send && api.Recv;
+      api.ok = api.GetUniqueId && api.CommInitRank && api.Send && api.Recv && api.AllReduce;
     }
   }
   if (!api.ok) raise(7, "libnccl.so.2 not loadable (multi-GPU placement needs NCCL)");
@@ -239,6 +242,7 @@ void Engine::attach_comm(const void* uid, int nranks, int rank, const int* stage
     if (r < 0 || r >= nranks) raise(1, "stage placed on a rank outside the world");
   rank_ = rank;
   nranks_ = nranks;
+  if (nranks > 1) schedule_ = 1;
   if (nranks > 1) {
     NcclApi::Uid u;
     std::memcpy(u.b, uid, 128);
@@ -260,6 +264,33 @@ void Engine::hop(void* buf, size_t bytes, int src, int dst) {
   if (src == dst || bytes == 0) return;
   if (rank_ == src) nccl_check(nccl().Send(buf, bytes, /*ncclInt8*/ 0, dst, comm_, st_), "ncclSend");
   if (rank_ == dst) nccl_check(nccl().Recv(buf, bytes, /*ncclInt8*/ 0, src, comm_, st_), "ncclRecv");
+}
+
+bool Engine::move(void* buf, size_t bytes, int from_code, int to_code) {
+  if (log_hops_) {
+    auto vo = [&](int c) {
+      const int sid = c <= 0 ? 1 : c > static_cast<int>(d_.s) ? static_cast<int>(d_.s) : c;
+      return vrank_[static_cast<size_t>(sid - 1)];
+    };
+    if (vo(from_code) != vo(to_code)) {
+      hop_log_.push_back(vo(from_code));
+      hop_log_.push_back(vo(to_code));
+      hop_log_.push_back(static_cast<long>(bytes));
+    }
+  }
+  const int src = owner_of_code(from_code), dst = owner_of_code(to_code);
+  if (src == dst) return false;
+  hop(buf, bytes, src, dst);
+  return rank_ == dst;
+}
+
+void Engine::hop_log_enable(int nranks, const int* vrank) {
+  hop_log_.clear();
+  log_hops_ = vrank != nullptr && nranks > 0;
+  if (!log_hops_) return;
+  vrank_.assign(vrank, vrank + d_.s);
+  for (int r : vrank_)
+    if (r < 0 || r >= nranks) raise(1, "virtual placement names a rank outside the world");
 }
 
 // ------------------------------------------------------------------ init
@@ -307,8 +338,8 @@ void validate_order(const int* order, size_t s) {
 }  // namespace
 
 void Engine::adam_group(ParamGroup& g, double lr, double gscale, double* omega_dev) {
+  ++g.step;  // on every rank: optimizer scalars stay replicated
   if (!g.owned || g.n == 0) return;
-  ++g.step;
   // bias corrections with std::pow on the host, exactly kernels_serial.cpp:135-136
   const double bc1 = 1.0 - std::pow(0.9, static_cast<double>(g.step));
   const double bc2 = 1.0 - std::pow(0.999, static_cast<double>(g.step));
@@ -378,10 +409,17 @@ void Engine::run_iteration(const int* orders, int m, const void* x, const void* 
     xd = static_cast<const char*>(xb);
   }
 
-  for (int k = 0; k < m; ++k) {
-    const int* order = orders + static_cast<size_t>(k) * d_.s;
-    impl_->microbatch(order, xd + static_cast<size_t>(k) * mb * xcols * xelt,
-                      yd ? yd + static_cast<size_t>(k) * mb * ycols * yelt : nullptr, mb, true, scal_ + k);
+  auto xk = [&](int k) { return xd + static_cast<size_t>(k) * mb * xcols * xelt; };
+  auto yk = [&](int k) { return yd ? yd + static_cast<size_t>(k) * mb * ycols * yelt : nullptr; };
+  auto ok = [&](int k) { return orders + static_cast<size_t>(k) * d_.s; };
+  if (schedule_ == 0) {
+    for (int k = 0; k < m; ++k) impl_->microbatch(ok(k), xk(k), yk(k), mb, true, scal_ + k);
+  } else {
+    // GPipe: all forwards, then all backwards in microbatch order (per-stage accumulation
+    // order is the reference's, pipeline.cpp:66-81); hops are issued in one global order
+    // on every rank, so NCCL send/recv pair up without deadlock
+    for (int k = 0; k < m; ++k) impl_->mb_forward(k, ok(k), xk(k), yk(k), mb, true, scal_ + k);
+    for (int k = 0; k < m; ++k) impl_->mb_backward(k, ok(k), xk(k), mb);
   }
   // mean loss in microbatch order, then *1/m (model.cpp:299-312, pipeline.cpp:82-83)
   std::vector<double> losses(static_cast<size_t>(m));
@@ -397,14 +435,27 @@ void Engine::run_iteration(const int* orders, int m, const void* x, const void* 
   double total = 0.0;
   for (double l : losses) total += l;
   total *= inv;
-  bool finite = std::isfinite(total) || !mine(owner_of_deembed());
+  if (nranks_ > 1) {
+    // every rank learns every stage's omega (the recovery reads its neighbours') and the loss
+    std::vector<double> v(d_.s + 1, 0.0);
+    for (size_t i = 0; i < d_.s; ++i) v[i] = stages_[i].owned ? om[i] : 0.0;
+    v[d_.s] = mine(owner_of_deembed()) ? total : 0.0;
+    double* dv = scal_ + 3100;
+    CKF_CUDA(cudaMemcpyAsync(dv, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice, st_));
+    nccl_check(nccl().AllReduce(dv, dv, v.size(), /*ncclFloat64*/ 8, /*ncclSum*/ 0, comm_, st_), "ncclAllReduce");
+    CKF_CUDA(cudaMemcpyAsync(v.data(), dv, v.size() * sizeof(double), cudaMemcpyDeviceToHost, st_));
+    CKF_CUDA(cudaStreamSynchronize(st_));
+    for (size_t i = 0; i < d_.s; ++i) om[i] = v[i];
+    total = v[d_.s];
+  }
+  bool finite = std::isfinite(total);
   for (size_t i = 0; i < d_.s; ++i) {
-    if (!stages_[i].owned) continue;
+    if (!stages_[i].owned && nranks_ == 1) continue;
     stages_[i].omega = om[i];
     if (!std::isfinite(om[i])) finite = false;
   }
   if (!finite) raise(2, "non-finite gradient or activation", iteration);
-  if (loss) *loss = mine(owner_of_deembed()) ? total : 0.0;
+  if (loss) *loss = total;
   if (omegas)
     for (size_t i = 0; i < d_.s; ++i) omegas[i] = stages_[i].omega;
 }
@@ -592,40 +643,85 @@ ckf_recovery_report Engine::recover_stage(int sid, int mode, int moments, double
   if (mode == CKF_REC_EDGE && replica_staleness_ != 0)
     raise(1, "edge replica is stale; refresh must precede recovery");  // recovery.cpp:98
   if (f.lr <= 0.0) raise(1, "learning rate must be positive");
-  if (nranks_ > 1) raise(1, "multi-GPU recovery goes through ckf_engine_recover_stage_peer (not attached)");
+  if (mode < CKF_REC_CHECKFREE || mode > CKF_REC_EDGE) raise(1, "unknown recovery mode");
 
   const size_t mb = master_bytes();
   const size_t bytes = f.n * mb;
+  const int F = owner_of_stage(sid);  // the replacement GPU of the failed stage
+  const bool local = mine(F);
+  ParamGroup* nbp = mode == CKF_REC_EDGE ? &stage(sid == 1 ? 2 : s - 1) : (sid > 1 ? &stage(sid - 1) : nullptr);
+  ParamGroup* nxp = mode != CKF_REC_EDGE && sid < s ? &stage(sid + 1) : nullptr;
+  const bool avg = moments == CKF_MOM_AVERAGED && (mode == CKF_REC_CHECKFREE || mode == CKF_REC_EDGE);
+
+  // ---- bring the neighbour state this recovery reads onto F (peer pulls over NCCL;
+  //      a no-op when everything is resident, e.g. on one GPU)
+  std::vector<std::pair<void**, void*>> borrowed;  // (slot, temp) to undo
+  auto pull = [&](void** slot, int src, size_t nbytes, int ws_slot) {
+    if (src == F) return;
+    void* tmp = local ? ws(nbytes, ws_slot) : nullptr;
+    if (local) {
+      borrowed.push_back({slot, *slot});
+      *slot = tmp;
+    }
+    hop(local ? tmp : *slot, nbytes, src, F);
+  };
+  if (nranks_ > 1) {
+    const bool need_prev = mode != CKF_REC_RANDOM;
+    if (nbp && need_prev) {
+      const int src = owner_of_stage(mode == CKF_REC_EDGE ? (sid == 1 ? 2 : s - 1) : sid - 1);
+      pull(&nbp->w, src, bytes, 60);
+      if (avg) {
+        pull(&nbp->m, src, bytes, 61);
+        pull(&nbp->v, src, bytes, 62);
+      }
+    }
+    if (nxp && (mode == CKF_REC_CHECKFREE || mode == CKF_REC_UNIFORM)) {
+      const int src = owner_of_stage(sid + 1);
+      pull(&nxp->w, src, bytes, 63);
+      if (avg) {
+        pull(&nxp->m, src, bytes, 64);
+        pull(&nxp->v, src, bytes, 65);
+      }
+    }
+    if (mode == CKF_REC_EDGE) {  // the replica lives on the neighbour's GPU (recovery.cpp:80-84)
+      void** rep = sid == 1 ? &rep_embed_ : &rep_deembed_;
+      const size_t rb = (sid == 1 ? embed_.n : deembed_.n) * mb;
+      pull(rep, owner_of_stage(sid == 1 ? 2 : s - 1), rb, 66);
+    }
+  }
+
   double* red_dev = want_red ? scal_ + 3500 : nullptr;
-  CKF_CUDA(cudaEventRecord(ev0_, st_));
+  if (local) CKF_CUDA(cudaEventRecord(ev0_, st_));
+  long new_step = 0;
   if (mode == CKF_REC_EDGE) {
-    ParamGroup& nb = stage(sid == 1 ? 2 : s - 1);
-    if (want_red) {
-      if (fp64())
-        k::sum_sq_diff(static_cast<const double*>(f.w), static_cast<const double*>(nb.w), f.n, red_dev, red_, st_);
-      else
-        k::sum_sq_diff(static_cast<const float*>(f.w), static_cast<const float*>(nb.w), f.n, red_dev, red_, st_);
-    }
-    CKF_CUDA(cudaMemcpyAsync(f.w, nb.w, bytes, cudaMemcpyDeviceToDevice, st_));
+    ParamGroup& nb = *nbp;
     ParamGroup& eg = sid == 1 ? embed_ : deembed_;
-    CKF_CUDA(cudaMemcpyAsync(eg.w, sid == 1 ? rep_embed_ : rep_deembed_, eg.n * mb, cudaMemcpyDeviceToDevice, st_));
-    CKF_CUDA(cudaMemsetAsync(eg.m, 0, eg.n * mb, st_));  // that edge's Adam state resets (trainer.cpp:218-224)
-    CKF_CUDA(cudaMemsetAsync(eg.v, 0, eg.n * mb, st_));
-    CKF_CUDA(cudaMemsetAsync(eg.g, 0, eg.n * mb, st_));
-    eg.step = 0;
-    if (eg.wlp) k::convert(static_cast<const float*>(eg.w), eg.wlp, eg.n, st_);
-    if (moments == CKF_MOM_AVERAGED) {  // single neighbour: copy, like the weights (trainer.cpp:225-226)
-      CKF_CUDA(cudaMemcpyAsync(f.m, nb.m, bytes, cudaMemcpyDeviceToDevice, st_));
-      CKF_CUDA(cudaMemcpyAsync(f.v, nb.v, bytes, cudaMemcpyDeviceToDevice, st_));
-      f.step = nb.step;
-    } else {
-      CKF_CUDA(cudaMemsetAsync(f.m, 0, bytes, st_));
-      CKF_CUDA(cudaMemsetAsync(f.v, 0, bytes, st_));
-      f.step = 0;
+    if (local) {
+      if (want_red) {
+        if (fp64())
+          k::sum_sq_diff(static_cast<const double*>(f.w), static_cast<const double*>(nb.w), f.n, red_dev, red_, st_);
+        else
+          k::sum_sq_diff(static_cast<const float*>(f.w), static_cast<const float*>(nb.w), f.n, red_dev, red_, st_);
+      }
+      CKF_CUDA(cudaMemcpyAsync(f.w, nb.w, bytes, cudaMemcpyDeviceToDevice, st_));
+      CKF_CUDA(cudaMemcpyAsync(eg.w, sid == 1 ? rep_embed_ : rep_deembed_, eg.n * mb, cudaMemcpyDeviceToDevice, st_));
+      CKF_CUDA(cudaMemsetAsync(eg.m, 0, eg.n * mb, st_));  // that edge's Adam state resets (trainer.cpp:218-224)
+      CKF_CUDA(cudaMemsetAsync(eg.v, 0, eg.n * mb, st_));
+      CKF_CUDA(cudaMemsetAsync(eg.g, 0, eg.n * mb, st_));
+      if (eg.wlp) k::convert(static_cast<const float*>(eg.w), eg.wlp, eg.n, st_);
+      if (avg) {  // single neighbour: copy, like the weights (trainer.cpp:225-226)
+        CKF_CUDA(cudaMemcpyAsync(f.m, nb.m, bytes, cudaMemcpyDeviceToDevice, st_));
+        CKF_CUDA(cudaMemcpyAsync(f.v, nb.v, bytes, cudaMemcpyDeviceToDevice, st_));
+      } else {
+        CKF_CUDA(cudaMemsetAsync(f.m, 0, bytes, st_));
+        CKF_CUDA(cudaMemsetAsync(f.v, 0, bytes, st_));
+      }
     }
+    eg.step = 0;
+    new_step = avg ? nb.step : 0;
   } else {
-    ParamGroup& p = stage(sid - 1);
-    ParamGroup& n = stage(sid + 1);
+    ParamGroup& p = *nbp;
+    ParamGroup& n = *nxp;
     double op = p.omega, on = n.omega;
     if (op < 0.0 || on < 0.0) raise(1, "gradient norms must be nonnegative");
     if (mode == CKF_REC_CHECKFREE) {
@@ -636,63 +732,75 @@ ckf_recovery_report Engine::recover_stage(int sid, int mode, int moments, double
       op = 1.0;
       on = 0.0;
     }
-    if (mode == CKF_REC_RANDOM) {
-      void* tmp = want_red ? ws(bytes, 3) : nullptr;
-      if (want_red) CKF_CUDA(cudaMemcpyAsync(tmp, f.w, bytes, cudaMemcpyDeviceToDevice, st_));
-      impl_->init_stage(sid, reinit_seed, f.w);
-      if (want_red) {
-        if (fp64())
-          k::sum_sq_diff(static_cast<const double*>(tmp), static_cast<const double*>(f.w), f.n, red_dev, red_, st_);
-        else
-          k::sum_sq_diff(static_cast<const float*>(tmp), static_cast<const float*>(f.w), f.n, red_dev, red_, st_);
-      }
-    } else if (mode == CKF_REC_COPY_PREV) {
-      if (want_red) {
-        if (fp64())
-          k::sum_sq_diff(static_cast<const double*>(f.w), static_cast<const double*>(p.w), f.n, red_dev, red_, st_);
-        else
-          k::sum_sq_diff(static_cast<const float*>(f.w), static_cast<const float*>(p.w), f.n, red_dev, red_, st_);
-      }
-      CKF_CUDA(cudaMemcpyAsync(f.w, p.w, bytes, cudaMemcpyDeviceToDevice, st_));
-    } else {
-      if (fp64())
-        k::recover(static_cast<const double*>(p.w), static_cast<const double*>(n.w), static_cast<double*>(f.w), f.n,
-                   op, on, red_dev, red_, st_);
-      else
-        k::recover(static_cast<const float*>(p.w), static_cast<const float*>(n.w), static_cast<float*>(f.w), f.n, op,
-                   on, red_dev, red_, st_);
-    }
-    if (moments == CKF_MOM_AVERAGED && mode == CKF_REC_CHECKFREE) {
-      // omega-weighted moments, step = min (trainer.cpp:263-269)
-      const double wp = p.omega, wn = n.omega;
-      if (fp64()) {
-        k::weighted_or_uniform(static_cast<const double*>(p.m), static_cast<const double*>(n.m),
-                               static_cast<double*>(f.m), f.n, wp, wn, st_);
-        k::weighted_or_uniform(static_cast<const double*>(p.v), static_cast<const double*>(n.v),
-                               static_cast<double*>(f.v), f.n, wp, wn, st_);
+    if (local) {
+      if (mode == CKF_REC_RANDOM) {
+        void* tmp = want_red ? ws(bytes, 3) : nullptr;
+        if (want_red) CKF_CUDA(cudaMemcpyAsync(tmp, f.w, bytes, cudaMemcpyDeviceToDevice, st_));
+        impl_->init_stage(sid, reinit_seed, f.w);
+        if (want_red) {
+          if (fp64())
+            k::sum_sq_diff(static_cast<const double*>(tmp), static_cast<const double*>(f.w), f.n, red_dev, red_, st_);
+          else
+            k::sum_sq_diff(static_cast<const float*>(tmp), static_cast<const float*>(f.w), f.n, red_dev, red_, st_);
+        }
+      } else if (mode == CKF_REC_COPY_PREV) {
+        if (want_red) {
+          if (fp64())
+            k::sum_sq_diff(static_cast<const double*>(f.w), static_cast<const double*>(p.w), f.n, red_dev, red_, st_);
+          else
+            k::sum_sq_diff(static_cast<const float*>(f.w), static_cast<const float*>(p.w), f.n, red_dev, red_, st_);
+        }
+        CKF_CUDA(cudaMemcpyAsync(f.w, p.w, bytes, cudaMemcpyDeviceToDevice, st_));
       } else {
-        k::weighted_or_uniform(static_cast<const float*>(p.m), static_cast<const float*>(n.m),
-                               static_cast<float*>(f.m), f.n, wp, wn, st_);
-        k::weighted_or_uniform(static_cast<const float*>(p.v), static_cast<const float*>(n.v),
-                               static_cast<float*>(f.v), f.n, wp, wn, st_);
+        // the streaming omega-weighted average (recovery.cpp:57-73), optional ||old - new||^2 in the same pass
+        kt_begin();
+        if (fp64())
+          k::recover(static_cast<const double*>(p.w), static_cast<const double*>(n.w), static_cast<double*>(f.w), f.n,
+                     op, on, red_dev, red_, st_);
+        else
+          k::recover(static_cast<const float*>(p.w), static_cast<const float*>(n.w), static_cast<float*>(f.w), f.n, op,
+                     on, red_dev, red_, st_);
+        kt_end(KC_RECOVER, 0.0, 3.0 * static_cast<double>(bytes));
       }
-      f.step = std::min(p.step, n.step);
-    } else {
-      CKF_CUDA(cudaMemsetAsync(f.m, 0, bytes, st_));
-      CKF_CUDA(cudaMemsetAsync(f.v, 0, bytes, st_));
-      f.step = 0;
+      if (avg) {
+        // omega-weighted moments (trainer.cpp:263-269)
+        const double wp = p.omega, wn = n.omega;
+        if (fp64()) {
+          k::weighted_or_uniform(static_cast<const double*>(p.m), static_cast<const double*>(n.m),
+                                 static_cast<double*>(f.m), f.n, wp, wn, st_);
+          k::weighted_or_uniform(static_cast<const double*>(p.v), static_cast<const double*>(n.v),
+                                 static_cast<double*>(f.v), f.n, wp, wn, st_);
+        } else {
+          k::weighted_or_uniform(static_cast<const float*>(p.m), static_cast<const float*>(n.m),
+                                 static_cast<float*>(f.m), f.n, wp, wn, st_);
+          k::weighted_or_uniform(static_cast<const float*>(p.v), static_cast<const float*>(n.v),
+                                 static_cast<float*>(f.v), f.n, wp, wn, st_);
+        }
+      } else {
+        CKF_CUDA(cudaMemsetAsync(f.m, 0, bytes, st_));
+        CKF_CUDA(cudaMemsetAsync(f.v, 0, bytes, st_));
+      }
     }
+    new_step = avg ? std::min(p.step, n.step) : 0;
   }
-  CKF_CUDA(cudaMemsetAsync(f.g, 0, bytes, st_));
-  if (f.wlp) k::convert(static_cast<const float*>(f.w), f.wlp, f.n, st_);
-  CKF_CUDA(cudaEventRecord(ev1_, st_));
+  if (local) {
+    CKF_CUDA(cudaMemsetAsync(f.g, 0, bytes, st_));
+    if (f.wlp) k::convert(static_cast<const float*>(f.w), f.wlp, f.n, st_);
+    CKF_CUDA(cudaEventRecord(ev1_, st_));
+  }
+  f.step = new_step;
   f.lr = lr_bump * f.lr;  // bump_lr (recovery.cpp:75-78), failed stage only
   f.omega = 0.0;          // trainer.cpp:276
-  if (want_red) CKF_CUDA(cudaMemcpyAsync(&rep.reduction_error, red_dev, sizeof(double), cudaMemcpyDeviceToHost, st_));
+  if (local && want_red)
+    CKF_CUDA(cudaMemcpyAsync(&rep.reduction_error, red_dev, sizeof(double), cudaMemcpyDeviceToHost, st_));
   CKF_CUDA(cudaStreamSynchronize(st_));
-  float ms = 0.f;
-  CKF_CUDA(cudaEventElapsedTime(&ms, ev0_, ev1_));
-  rep.latency_ms = ms;
+  kt_collect();
+  for (auto it = borrowed.rbegin(); it != borrowed.rend(); ++it) *it->first = it->second;
+  if (local) {
+    float ms = 0.f;
+    CKF_CUDA(cudaEventElapsedTime(&ms, ev0_, ev1_));
+    rep.latency_ms = ms;
+  }
   return rep;
 }
 

@@ -73,10 +73,20 @@ struct BlockImpl {
   // Fills master weights on the device (init_model streams, model.cpp:159-197).
   virtual void init_stage(int sid, uint64_t seed, void* w) = 0;
   virtual void init_edges(uint64_t seed, void* embed, void* deembed) = 0;
-  // One microbatch along `order`: forward, loss into *loss_dev (device double),
-  // and, when train, backward accumulating into the groups' g buffers.
-  virtual void microbatch(const int* order, const void* x, const void* y, size_t rows, bool train,
+  // Forward of microbatch slot `mb` along `order`: embedding, the owned
+  // stages' layers, and on the de-embedding owner the head: loss into
+  // *loss_dev (device double) and, when train, the head backward leaving
+  // dL/dh_final in the slot.  Activations are cached per (slot, applied layer).
+  virtual void mb_forward(int mb, const int* order, const void* x, const void* y, size_t rows, bool train,
                           double* loss_dev) = 0;
+  // Backward of slot `mb`: owned layers in reverse applied order (gradients
+  // accumulate into the groups' g buffers), then the embedding.
+  virtual void mb_backward(int mb, const int* order, const void* x, size_t rows) = 0;
+  // the reference's per-microbatch order: forward then backward (model.cpp:211-378)
+  void microbatch(const int* order, const void* x, const void* y, size_t rows, bool train, double* loss_dev) {
+    mb_forward(0, order, x, y, rows, train, loss_dev);
+    if (train) mb_backward(0, order, x, rows);
+  }
   // Predictions of forward(order, x) (MLP) into a device buffer of rows*out.
   virtual void predict(const int* order, const void* x, size_t rows, void* pred) = 0;
   Engine* eng;
@@ -125,8 +135,27 @@ class Engine {
   int owner_of_deembed() const { return owner_of_stage(static_cast<int>(d_.s)); }
   bool mine(int owner) const { return owner == rank_; }
   void attach_comm(const void* uid, int nranks, int rank, const int* stage_rank);
-  // move `count` elements of `buf` (device, master or activation dtype bytes) from rank src to rank dst
+  // 0 = sequential (forward+backward per microbatch, one live activation cache);
+  // 1 = GPipe (all forwards, then all backwards in microbatch order: the ranks of
+  //     a multi-GPU pipeline overlap; per-stage accumulation order is unchanged)
+  void set_schedule(int mode) {
+    if (mode != 0 && mode != 1) raise(1, "schedule must be 0 (sequential) or 1 (gpipe)");
+    schedule_ = mode;
+  }
+  int schedule() const { return schedule_; }
+  // move `bytes` of `buf` from rank src to rank dst (NCCL send/recv on the engine stream)
   void hop(void* buf, size_t bytes, int src, int dst);
+  // Stage-boundary transfer between pipeline positions (codes: 0 = embedding,
+  // 1..s = stage, s+1 = de-embedding).  Returns true on the rank that received
+  // data from another rank.  Logged against the virtual placement when enabled.
+  bool move(void* buf, size_t bytes, int from_code, int to_code);
+  int owner_of_code(int code) const {
+    return code <= 0 ? owner_of_embed() : code > static_cast<int>(d_.s) ? owner_of_deembed() : owner_of_stage(code);
+  }
+  // hop log (multi-GPU placement check on one GPU): records (src, dst, bytes) of every
+  // transfer the virtual placement `vrank` (stage -> rank) would perform
+  void hop_log_enable(int nranks, const int* vrank);
+  const std::vector<long>& hop_log() const { return hop_log_; }
 
   // kernel timing (KClass)
   void kt_enable(bool on);
@@ -160,6 +189,10 @@ class Engine {
   std::vector<size_t> ws_size_;
   double* scal_ = nullptr;
   int rank_ = 0, nranks_ = 1;
+  int schedule_ = 0;
+  bool log_hops_ = false;
+  std::vector<int> vrank_;
+  std::vector<long> hop_log_;
   std::vector<int> stage_rank_;
   void* comm_ = nullptr;  // ncclComm_t
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;

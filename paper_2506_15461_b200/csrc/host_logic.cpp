@@ -318,4 +318,54 @@ Trace Config::resolve_trace(uint64_t s) const {
   return generate_trace(s, p_hour, iter_seconds, iters, resolved_eligible());
 }
 
+// ------------------------------------------------------------------ pipeline plan
+std::vector<PlanOp> pipeline_plan(int s, int m, const std::vector<int>& orders, const std::vector<int>& stage_rank,
+                                  int schedule) {
+  if (s < 1 || m < 1) fail(1, "pipeline plan needs s >= 1 and m >= 1");
+  if (orders.size() != static_cast<size_t>(s) * static_cast<size_t>(m)) fail(1, "orders must hold m*s stage ids");
+  if (stage_rank.size() != static_cast<size_t>(s)) fail(1, "placement must name one rank per stage");
+  if (schedule != 0 && schedule != 1) fail(1, "schedule must be 0 (sequential) or 1 (gpipe)");
+  auto owner = [&](int code) {  // 0 embedding, 1..s stages, s+1 de-embedding
+    const int sid = code <= 0 ? 1 : code > s ? s : code;
+    return stage_rank[static_cast<size_t>(sid - 1)];
+  };
+  std::vector<PlanOp> ops;
+  auto xfer = [&](int phase, int mb, int from, int to, int aux) {
+    if (owner(from) != owner(to)) ops.push_back({phase, mb, PlanOp::kXfer, owner(from), owner(to), aux});
+  };
+  auto fwd = [&](int k) {
+    const int* o = orders.data() + static_cast<size_t>(k) * static_cast<size_t>(s);
+    ops.push_back({0, k, PlanOp::kEmbedFwd, owner(0), 0, 0});
+    int at = 0;
+    for (int i = 0; i < s; ++i) {
+      xfer(0, k, at, o[i], 0);
+      ops.push_back({0, k, PlanOp::kStageFwd, owner(o[i]), o[i], 0});
+      at = o[i];
+    }
+    xfer(0, k, at, s + 1, 0);
+    ops.push_back({0, k, PlanOp::kHead, owner(s + 1), 0, 0});
+  };
+  auto bwd = [&](int k) {
+    const int* o = orders.data() + static_cast<size_t>(k) * static_cast<size_t>(s);
+    int at = s + 1;
+    for (int i = s - 1; i >= 0; --i) {
+      xfer(1, k, at, o[i], 1);
+      ops.push_back({1, k, PlanOp::kStageBwd, owner(o[i]), o[i], 0});
+      at = o[i];
+    }
+    xfer(1, k, at, 0, 1);
+    ops.push_back({1, k, PlanOp::kEmbedBwd, owner(0), 0, 0});
+  };
+  if (schedule == 0) {
+    for (int k = 0; k < m; ++k) {
+      fwd(k);
+      bwd(k);
+    }
+  } else {
+    for (int k = 0; k < m; ++k) fwd(k);
+    for (int k = 0; k < m; ++k) bwd(k);
+  }
+  return ops;
+}
+
 }  // namespace ckf::host

@@ -63,6 +63,26 @@ std::vector<int> swapped_order(int s);
 // m*s flattened orders; swapped at even positions (pipeline.cpp:41-56)
 std::vector<int> build_schedule(int m, bool swapped_half, int s);
 
+// ------------------------------------------------------------------ multi-GPU pipeline plan
+// The global op sequence of one iteration for a stage -> rank placement, in
+// the order every rank issues it (the engine's stage walk, engine.cu /
+// *_block.cu): each microbatch enters at the embedding (owned with stage 1),
+// visits the stages in its execution order, leaves through the de-embedding
+// (owned with stage s), and the backward walks the applied stages in reverse.
+// schedule 0 = forward+backward per microbatch, 1 = GPipe (all forwards, then
+// all backwards in microbatch order).
+struct PlanOp {
+  enum Kind { kEmbedFwd = 0, kStageFwd = 1, kXfer = 2, kHead = 3, kStageBwd = 4, kEmbedBwd = 5 };
+  int phase;  // 0 forward, 1 backward
+  int mb;
+  int kind;
+  int rank;   // executing rank (kXfer: source)
+  int arg;    // stage id (kStage*) or destination rank (kXfer)
+  int aux;    // kXfer: 0 activations, 1 activation gradients
+};
+std::vector<PlanOp> pipeline_plan(int s, int m, const std::vector<int>& orders, const std::vector<int>& stage_rank,
+                                  int schedule);
+
 // ------------------------------------------------------------------ config
 struct Config {
   // model (model.hpp:32-42) + LLaMA extension

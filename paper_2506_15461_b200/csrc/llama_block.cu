@@ -119,7 +119,7 @@ struct LlamaBlock final : BlockImpl {
   Cache cache(size_t slot, size_t Mt, size_t rows) {
     const size_t bytes = al(Mt * d * 4) * 2 + al(Mt * 4) * 2 + al(rows * H * T * 4) + al(Mt * d * 2) * 3 +
                          al(Mt * 3 * d * 2) + al(Mt * 2 * f * 2) + al(Mt * f * 2);
-    char* p = static_cast<char*>(eng->ws(bytes, 100 + static_cast<int>(slot)));
+    char* p = static_cast<char*>(eng->ws(bytes, 100 + static_cast<int>(slot)));  // slot = cache_id - 100
     Cache c;
     auto take = [&](size_t b) {
       char* r = p;
@@ -170,7 +170,29 @@ struct LlamaBlock final : BlockImpl {
   }
 
   // ------------------------------------------------------------ one microbatch
-  void microbatch(const int* order, const void* xv, const void*, size_t rows, bool train, double* loss_dev) override {
+  // Per-slot state (kept from mb_forward to mb_backward): tokens, labels, the
+  // gradient of the final residual stream, and one cache slab per applied layer.
+  static int slot_id(int mb, int k) { return 1000 + 8 * mb + k; }
+  static int cache_id(int mb, size_t applied) { return 100000 + 64 * mb + static_cast<int>(applied); }
+  struct Applied {
+    int sid;
+    size_t li;  // layer index within the stage
+  };
+  std::vector<Applied> applied_order(const int* order) const {
+    std::vector<Applied> v;
+    const Desc& D = eng->desc();
+    for (size_t oi = 0; oi < D.s; ++oi) {
+      const Range& r = D.part[static_cast<size_t>(order[oi] - 1)];
+      for (size_t li = 0; li < r.count(); ++li) v.push_back({order[oi], li});
+    }
+    return v;
+  }
+  Cache cache_for(int mb, size_t applied, size_t Mt, size_t rows) {
+    return cache(static_cast<size_t>(cache_id(mb, applied)) - 100, Mt, rows);
+  }
+
+  void mb_forward(int mb, const int* order, const void* xv, const void*, size_t rows, bool train,
+                  double* loss_dev) override {
     const Desc& D = eng->desc();
     cudaStream_t st = eng->stream();
     const size_t Mt = rows * T;
@@ -178,15 +200,12 @@ struct LlamaBlock final : BlockImpl {
     const int* x = static_cast<const int*>(xv);
     const int Mi = static_cast<int>(Mt), di = static_cast<int>(d), Vi = static_cast<int>(V);
 
-    int* tok = buf<int>(40, Mt);
-    int* lab = buf<int>(41, Mt);
+    int* tok = buf<int>(slot_id(mb, 0), Mt);
+    int* lab = buf<int>(slot_id(mb, 1), Mt);
+    float* dh = buf<float>(slot_id(mb, 2), Mt * d);
+    bf16* dh_bf = buf<bf16>(slot_id(mb, 3), Mt * d);
     float* h = buf<float>(42, Mt * d);
-    float* dh = buf<float>(43, Mt * d);
-    bf16* dh_bf = buf<bf16>(44, Mt * d);
     float* dxn = buf<float>(45, Mt * d);
-    bf16* scratch_bf = buf<bf16>(46, Mt * std::max(3 * d, 2 * f));  // da / dgu / do / dqkv staging
-    bf16* dgu = buf<bf16>(47, Mt * 2 * f);
-    float* Dsum = buf<float>(48, rows * H * T);
     const int nblk = llama::rmsnorm_bwd_blocks(Mt);
     float* gpart = buf<float>(49, static_cast<size_t>(nblk) * d);
     bf16* xnF = buf<bf16>(50, Mt * d);
@@ -197,73 +216,71 @@ struct LlamaBlock final : BlockImpl {
 
     llama::split_tokens(x, rows, T, tok, lab, st);
 
-    struct Applied {
-      int sid;
-      size_t li;  // layer index within the stage
-    };
-    std::vector<Applied> applied;
-
     // ---------------- forward (model.cpp:226-253)
-    int where = eng->owner_of_embed();
-    if (eng->mine(where))
+    int at = 0;  // pipeline position of h (0 = embedding)
+    if (eng->mine(eng->owner_of_embed()))
       timed(KC_NORM, 0.0, Mt * d * 8.0, [&] {
         llama::embed_fwd(tok, Mt, static_cast<const float*>(eng->embed().w), d, h, st);
       });
+    size_t slot = 0;
     for (size_t oi = 0; oi < D.s; ++oi) {
       const int sid = order[oi];
       const int own = eng->owner_of_stage(sid);
-      eng->hop(h, Mt * d * 4, where, own);
-      where = own;
+      eng->move(h, Mt * d * 4, at, sid);
+      at = sid;
       const Range& r = D.part[static_cast<size_t>(sid - 1)];
-      for (size_t li = 0; li < r.count(); ++li) {
-        const size_t slot = applied.size();
-        applied.push_back({sid, li});
+      for (size_t li = 0; li < r.count(); ++li, ++slot) {
         if (!eng->mine(own)) continue;
-        layer_fwd(sid, li, cache(slot, Mt, rows), h, rows, Mt);
+        layer_fwd(sid, li, cache_for(train ? mb : 0, slot, Mt, rows), h, rows, Mt);
       }
     }
-    const int dout = eng->owner_of_deembed();
-    eng->hop(h, Mt * d * 4, where, dout);
-    if (eng->mine(dout)) {
-      const float* gF = static_cast<const float*>(eng->deembed().w);
-      const bf16* Einv = eng->deembed().wlp + d;
-      timed(KC_NORM, 0.0, Mt * d * 10.0, [&] { llama::rmsnorm_fwd(h, gF, Mt, d, xnF, rstdF, hF, st); });
-      gemm(Mi, Vi, di, xnF, di, false, Einv, Vi, true, logits, Vi, tc::kStoreBF16);
-      timed(KC_LOSS, 0.0, Mt * V * (train ? 6.0 : 2.0), [&] {
-        llama::xent_bf16(logits, lab, Mt, V, static_cast<float>(1.0 / static_cast<double>(Mt)), train ? 1 : 0,
-                         row_loss, st);
-        llama::fold_mean(row_loss, Mt, 1.0 / static_cast<double>(Mt), loss_dev, st);
-      });
-    }
+    eng->move(h, Mt * d * 4, at, static_cast<int>(D.s) + 1);
+    if (!eng->mine(eng->owner_of_deembed())) return;
+    const float* gF = static_cast<const float*>(eng->deembed().w);
+    const bf16* Einv = eng->deembed().wlp + d;
+    timed(KC_NORM, 0.0, Mt * d * 10.0, [&] { llama::rmsnorm_fwd(h, gF, Mt, d, xnF, rstdF, hF, st); });
+    gemm(Mi, Vi, di, xnF, di, false, Einv, Vi, true, logits, Vi, tc::kStoreBF16);
+    timed(KC_LOSS, 0.0, Mt * V * (train ? 6.0 : 2.0), [&] {
+      llama::xent_bf16(logits, lab, Mt, V, static_cast<float>(1.0 / static_cast<double>(Mt)), train ? 1 : 0,
+                       row_loss, st);
+      llama::fold_mean(row_loss, Mt, 1.0 / static_cast<double>(Mt), loss_dev, st);
+    });
     if (!train) return;
+    // head backward (model.cpp:322-342): gE_inv += xnF^T dlogits, dh_final = rmsnorm'(dlogits E_inv^T)
+    float* gde = static_cast<float*>(eng->deembed().g);
+    gemm(di, Vi, Mi, xnF, di, true, logits, Vi, true, gde + d, Vi, tc::kAccF32);
+    gemm(Mi, di, Vi, logits, Vi, false, Einv, Vi, false, dxn, di, tc::kStoreF32);
+    CKF_CUDA(cudaMemsetAsync(dh, 0, Mt * d * 4, st));
+    timed(KC_NORM, 0.0, Mt * d * 18.0, [&] {
+      llama::rmsnorm_bwd(dxn, hF, gF, rstdF, Mt, d, dh, dh_bf, gpart, st);
+      llama::gain_fold(gpart, nblk, d, gde, st);
+    });
+  }
 
-    // ---------------- backward (model.cpp:314-378)
-    if (eng->mine(dout)) {
-      float* gde = static_cast<float*>(eng->deembed().g);
-      const bf16* Einv = eng->deembed().wlp + d;
-      gemm(di, Vi, Mi, xnF, di, true, logits, Vi, true, gde + d, Vi, tc::kAccF32);   // gE_inv += xnF^T dlogits
-      gemm(Mi, di, Vi, logits, Vi, false, Einv, Vi, false, dxn, di, tc::kStoreF32);  // dxnF = dlogits E_inv^T
-      CKF_CUDA(cudaMemsetAsync(dh, 0, Mt * d * 4, st));
-      timed(KC_NORM, 0.0, Mt * d * 18.0, [&] {
-        llama::rmsnorm_bwd(dxn, hF, static_cast<const float*>(eng->deembed().w), rstdF, Mt, d, dh, dh_bf, gpart, st);
-        llama::gain_fold(gpart, nblk, d, gde, st);
-      });
-    }
-    where = dout;
+  void mb_backward(int mb, const int* order, const void*, size_t rows) override {
+    cudaStream_t st = eng->stream();
+    const size_t Mt = rows * T;
+    int* tok = buf<int>(slot_id(mb, 0), Mt);
+    float* dh = buf<float>(slot_id(mb, 2), Mt * d);
+    bf16* dh_bf = buf<bf16>(slot_id(mb, 3), Mt * d);
+    float* dxn = buf<float>(45, Mt * d);
+    bf16* scratch_bf = buf<bf16>(46, Mt * std::max(3 * d, 2 * f));  // da / do staging
+    bf16* dgu = buf<bf16>(47, Mt * 2 * f);
+    float* Dsum = buf<float>(48, rows * H * T);
+    const int nblk = llama::rmsnorm_bwd_blocks(Mt);
+    float* gpart = buf<float>(49, static_cast<size_t>(nblk) * d);
+    const std::vector<Applied> applied = applied_order(order);
+    int at = static_cast<int>(eng->desc().s) + 1;  // dL/dh_final sits at the de-embedding
     for (size_t ai = applied.size(); ai-- > 0;) {
       const Applied& a = applied[ai];
       const int own = eng->owner_of_stage(a.sid);
-      if (own != where) {
-        eng->hop(dh, Mt * d * 4, where, own);
-        if (eng->mine(own)) llama::f32_to_bf16(dh, dh_bf, Mt * d, st);
-      }
-      where = own;
+      if (eng->move(dh, Mt * d * 4, at, a.sid)) llama::f32_to_bf16(dh, dh_bf, Mt * d, st);
+      at = a.sid;
       if (!eng->mine(own)) continue;
-      layer_bwd(a.sid, a.li, cache(ai, Mt, rows), dh, dh_bf, dxn, scratch_bf, dgu, Dsum, gpart, nblk, rows, Mt);
+      layer_bwd(a.sid, a.li, cache_for(mb, ai, Mt, rows), dh, dh_bf, dxn, scratch_bf, dgu, Dsum, gpart, nblk, rows, Mt);
     }
-    const int ein = eng->owner_of_embed();
-    eng->hop(dh, Mt * d * 4, where, ein);
-    if (eng->mine(ein)) {
+    eng->move(dh, Mt * d * 4, at, 0);
+    if (eng->mine(eng->owner_of_embed())) {
       void* sc = eng->ws(llama::embed_bwd_scratch(Mt), 55);
       timed(KC_NORM, 0.0, Mt * d * 12.0, [&] {
         llama::embed_bwd(tok, Mt, dh, d, static_cast<float*>(eng->embed().g), sc, st);
@@ -287,7 +304,12 @@ struct LlamaBlock final : BlockImpl {
     timed(KC_NORM, 0.0, Mt * d * 10.0, [&] { llama::rmsnorm_fwd(h, Wf + off.g1, Mt, d, c.xn1, c.rstd1, c.h_in, st); });
     gemm(Mi, 3 * di, di, c.xn1, di, false, W + off.wqkv, 3 * di, true, c.qkv, 3 * di, tc::kStoreBF16);
     timed(KC_NORM, 0.0, Mt * d * 8.0, [&] { llama::rope(c.qkv, Mt, T, d, H, 0, st); });
-    timed(KC_ATTN, attn_flops_fwd(rows), Mt * d * 8.0, [&] { llama::attn_fwd(c.qkv, rows, T, H, hd, c.o, c.lse, st); });
+    timed(KC_ATTN, attn_flops_fwd(rows), Mt * d * 8.0, [&] {
+      if (llama::attn_fwd_tc_supported(T, hd))
+        llama::attn_fwd_tc(c.qkv, rows, T, H, hd, c.o, c.lse, st);  // tcgen05 + TMEM
+      else
+        llama::attn_fwd(c.qkv, rows, T, H, hd, c.o, c.lse, st);
+    });
     gemm(Mi, di, di, c.o, di, false, W + off.wo, di, true, h, di, tc::kAccF32);
     timed(KC_NORM, 0.0, Mt * d * 10.0, [&] { llama::rmsnorm_fwd(h, Wf + off.g2, Mt, d, c.xn2, c.rstd2, c.h_mid, st); });
     gemm(Mi, 2 * fi, di, c.xn2, di, false, W + off.wgu, 2 * fi, true, c.gu, 2 * fi, tc::kStoreBF16);

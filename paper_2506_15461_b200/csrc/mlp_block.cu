@@ -98,43 +98,35 @@ struct MlpBlock final : BlockImpl {
     return static_cast<T*>(eng->ws(elems * sizeof(T), slot));
   }
 
+  // Per-slot state kept from forward to backward: the applied-block caches
+  // (block input, hidden activation) and dL/dh_final.
+  static int slot_id(int mb, int k) { return 1000 + 8 * mb + k; }
+
   template <typename T>
-  void run(const int* order, const T* x, const void* y, size_t b, bool train, double* loss_dev, T* pred_out) {
+  void fwd(int mb, const int* order, const T* x, const void* y, size_t b, bool train, double* loss_dev, T* pred_out) {
     const Desc& d = eng->desc();
     cudaStream_t st = eng->stream();
-    const int me = eng->rank();
     const size_t L = d.L;
-    // activations: h (current), cache of (input, hidden) per applied block
     T* h = buf<T>(8, b * d.d);
-    T* cache_in = buf<T>(9, L * b * d.d);
-    T* cache_z = buf<T>(10, L * b * d.hid);
+    T* cache_in = buf<T>(slot_id(mb, 0), L * b * d.d);
+    T* cache_z = buf<T>(slot_id(mb, 1), L * b * d.hid);
+    T* dh = buf<T>(slot_id(mb, 2), b * d.d);
     T* pre = buf<T>(11, b * d.hid);
     T* pred = pred_out ? pred_out : buf<T>(12, b * d.out);
     T* dpred = buf<T>(13, b * d.out);
-    T* dh = buf<T>(14, b * d.d);
-    T* dz = buf<T>(15, b * d.hid);
-    T* da = buf<T>(16, b * d.hid);
-    struct Applied {
-      int sid;
-      size_t bi;
-    };
-    std::vector<Applied> applied;
-    applied.reserve(L);
 
     // ---- forward (model.cpp:226-253)
-    int where = eng->owner_of_embed();
-    if (eng->mine(where))
-      gemm<T>(false, false, b, d.d, d.in, x, d.in, static_cast<const T*>(eng->embed().w), d.d, h, d.d,
-                      false);
+    int at = 0;  // pipeline position of h (0 = embedding)
+    if (eng->mine(eng->owner_of_embed()))
+      gemm<T>(false, false, b, d.d, d.in, x, d.in, static_cast<const T*>(eng->embed().w), d.d, h, d.d, false);
+    size_t slot = 0;
     for (size_t oi = 0; oi < d.s; ++oi) {
       const int sid = order[oi];
       const int own = eng->owner_of_stage(sid);
-      eng->hop(h, b * d.d * sizeof(T), where, own);
-      where = own;
+      eng->move(h, b * d.d * sizeof(T), at, sid);
+      at = sid;
       const Range& r = d.part[static_cast<size_t>(sid - 1)];
-      for (size_t bi = 0; bi < r.count(); ++bi) {
-        const size_t slot = applied.size();
-        applied.push_back({sid, bi});
+      for (size_t bi = 0; bi < r.count(); ++bi, ++slot) {
         if (!eng->mine(own)) continue;
         const T* w1 = static_cast<const T*>(eng->stage(sid).w) + bi * blk_params();
         const T* w2 = w1 + d.d * d.hid;
@@ -146,35 +138,50 @@ struct MlpBlock final : BlockImpl {
         gemm<T>(false, false, b, d.d, d.hid, cz, d.hid, w2, d.d, h, d.d, true);
       }
     }
-    const int dout = eng->owner_of_deembed();
-    eng->hop(h, b * d.d * sizeof(T), where, dout);
-    if (eng->mine(dout)) {
-      gemm<T>(false, false, b, d.out, d.d, h, d.d, static_cast<const T*>(eng->deembed().w), d.out, pred,
-                      d.out, false);
-      if (loss_dev) {
-        if (d.task == CKF_TASK_REGRESSION)
-          k::mse_loss_grad<T>(pred, static_cast<const T*>(y), b, d.out, train ? dpred : nullptr, loss_dev,
-                              eng->scratch(), st);
-        else
-          k::xent_loss_grad<T>(pred, static_cast<const int*>(y), b, d.out, train ? dpred : nullptr, loss_dev,
-                               eng->scratch(), st);
-      }
+    eng->move(h, b * d.d * sizeof(T), at, static_cast<int>(d.s) + 1);
+    if (!eng->mine(eng->owner_of_deembed())) return;
+    gemm<T>(false, false, b, d.out, d.d, h, d.d, static_cast<const T*>(eng->deembed().w), d.out, pred, d.out, false);
+    if (loss_dev) {
+      if (d.task == CKF_TASK_REGRESSION)
+        k::mse_loss_grad<T>(pred, static_cast<const T*>(y), b, d.out, train ? dpred : nullptr, loss_dev,
+                            eng->scratch(), st);
+      else
+        k::xent_loss_grad<T>(pred, static_cast<const int*>(y), b, d.out, train ? dpred : nullptr, loss_dev,
+                             eng->scratch(), st);
     }
     if (!train) return;
+    // head backward (model.cpp:322-342); h holds h_final on the de-embedding GPU
+    gemm<T>(true, false, d.d, d.out, b, h, d.d, dpred, d.out, static_cast<T*>(eng->deembed().g), d.out, true);
+    gemm<T>(false, true, b, d.d, d.out, dpred, d.out, static_cast<const T*>(eng->deembed().w), d.out, dh, d.d,
+            false);
+  }
 
-    // ---- backward (model.cpp:314-378); h still holds h_final on the de-embed GPU
-    if (eng->mine(dout)) {
-      gemm<T>(true, false, d.d, d.out, b, h, d.d, dpred, d.out, static_cast<T*>(eng->deembed().g), d.out,
-                      true);
-      gemm<T>(false, true, b, d.d, d.out, dpred, d.out, static_cast<const T*>(eng->deembed().w), d.out, dh,
-                      d.d, false);
+  template <typename T>
+  void bwd(int mb, const int* order, const T* x, size_t b) {
+    const Desc& d = eng->desc();
+    cudaStream_t st = eng->stream();
+    const size_t L = d.L;
+    const T* cache_in = buf<T>(slot_id(mb, 0), L * b * d.d);
+    const T* cache_z = buf<T>(slot_id(mb, 1), L * b * d.hid);
+    T* dh = buf<T>(slot_id(mb, 2), b * d.d);
+    T* dz = buf<T>(15, b * d.hid);
+    T* da = buf<T>(16, b * d.hid);
+    struct Applied {
+      int sid;
+      size_t bi;
+    };
+    std::vector<Applied> applied;
+    for (size_t oi = 0; oi < d.s; ++oi) {
+      const Range& r = d.part[static_cast<size_t>(order[oi] - 1)];
+      for (size_t bi = 0; bi < r.count(); ++bi) applied.push_back({order[oi], bi});
     }
-    where = dout;
+    // ---- backward (model.cpp:344-372), reverse application order
+    int at = static_cast<int>(d.s) + 1;  // dL/dh_final sits at the de-embedding
     for (size_t ai = applied.size(); ai-- > 0;) {
       const Applied& a = applied[ai];
       const int own = eng->owner_of_stage(a.sid);
-      eng->hop(dh, b * d.d * sizeof(T), where, own);
-      where = own;
+      eng->move(dh, b * d.d * sizeof(T), at, a.sid);
+      at = a.sid;
       if (!eng->mine(own)) continue;
       const T* w1 = static_cast<const T*>(eng->stage(a.sid).w) + a.bi * blk_params();
       const T* w2 = w1 + d.d * d.hid;
@@ -183,28 +190,35 @@ struct MlpBlock final : BlockImpl {
       const T* cin = cache_in + ai * b * d.d;
       const T* cz = cache_z + ai * b * d.hid;
       gemm<T>(false, true, b, d.hid, d.d, dh, d.d, w2, d.d, dz, d.hid, false);   // dz = dh W2^T
-      k::act_bwd<T>(d.act, cz, dz, da, b * d.hid, st);                                         // da = dz act'(z)
+      k::act_bwd<T>(d.act, cz, dz, da, b * d.hid, st);                         // da = dz act'(z)
       gemm<T>(true, false, d.d, d.hid, b, cin, d.d, da, d.hid, gw1, d.hid, true);  // gW1 += in^T da
       gemm<T>(true, false, d.hid, d.d, b, cz, d.hid, dh, d.d, gw2, d.d, true);     // gW2 += z^T dh
       gemm<T>(false, true, b, d.d, d.hid, da, d.hid, w1, d.hid, dh, d.d, true);    // dh += da W1^T
     }
-    const int ein = eng->owner_of_embed();
-    eng->hop(dh, b * d.d * sizeof(T), where, ein);
-    if (eng->mine(ein))
+    eng->move(dh, b * d.d * sizeof(T), at, 0);
+    if (eng->mine(eng->owner_of_embed()))
       gemm<T>(true, false, d.in, d.d, b, x, d.in, dh, d.d, static_cast<T*>(eng->embed().g), d.d, true);
   }
 
-  void microbatch(const int* order, const void* x, const void* y, size_t rows, bool train, double* loss_dev) override {
+  void mb_forward(int mb, const int* order, const void* x, const void* y, size_t rows, bool train,
+                  double* loss_dev) override {
+    const int slot = train ? mb : 0;
     if (eng->fp64())
-      run<double>(order, static_cast<const double*>(x), y, rows, train, loss_dev, nullptr);
+      fwd<double>(slot, order, static_cast<const double*>(x), y, rows, train, loss_dev, nullptr);
     else
-      run<float>(order, static_cast<const float*>(x), y, rows, train, loss_dev, nullptr);
+      fwd<float>(slot, order, static_cast<const float*>(x), y, rows, train, loss_dev, nullptr);
+  }
+  void mb_backward(int mb, const int* order, const void* x, size_t rows) override {
+    if (eng->fp64())
+      bwd<double>(mb, order, static_cast<const double*>(x), rows);
+    else
+      bwd<float>(mb, order, static_cast<const float*>(x), rows);
   }
   void predict(const int* order, const void* x, size_t rows, void* pred) override {
     if (eng->fp64())
-      run<double>(order, static_cast<const double*>(x), nullptr, rows, false, nullptr, static_cast<double*>(pred));
+      fwd<double>(0, order, static_cast<const double*>(x), nullptr, rows, false, nullptr, static_cast<double*>(pred));
     else
-      run<float>(order, static_cast<const float*>(x), nullptr, rows, false, nullptr, static_cast<float*>(pred));
+      fwd<float>(0, order, static_cast<const float*>(x), nullptr, rows, false, nullptr, static_cast<float*>(pred));
   }
 };
 
