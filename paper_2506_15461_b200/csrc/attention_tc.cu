@@ -31,21 +31,30 @@ constexpr uint32_t kPBuf = TQ * TK * 2;      // 32 KiB: P as [2 K-chunks][128 ro
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Forward: 96 KiB of shared memory and 256 TMEM columns per CTA so that two
+// CTAs share an SM (two softmax warpgroups per SM hide the exp / TMEM latency).
 struct Smem {
-  // 1024-aligned tiles first
   uint8_t q[kTile];
   uint8_t k[2][kTile];
-  uint8_t v[2][kTile];
-  uint8_t p[2][kPBuf];
+  uint8_t v[kTile];
+  uint8_t p[kPBuf];
   uint64_t q_full;
-  uint64_t kv_full[2], kv_empty[2];
-  uint64_t s_full[2], s_free[2];
-  uint64_t p_full[2], p_free[2];
+  uint64_t k_full[2], k_empty[2], v_full, v_empty;
+  uint64_t s_full, s_free, p_full, p_free;
   uint64_t o_full;
   uint32_t tmem;
 };
 
-__global__ void __launch_bounds__(kThreads, 1)
+// Pass 1 reduces each row of S to its maximum only; pass 2 accumulates
+// O = sum_j exp(S_j - max) V_j with the true row max (no rescaling ever
+// needed) and the row sum l; the epilogue divides by l.
+__global__ void __launch_bounds__(kThreads, 2)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, int T, int H, __nv_bfloat16* __restrict__ o,
                        float* __restrict__ lse, float scale_log2) {
   extern __shared__ uint8_t smem_raw[];
@@ -62,35 +71,41 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1 && lane == 0) {
     mbar_init(&sm.q_full, 1);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&sm.kv_full[i], 1);
-      mbar_init(&sm.kv_empty[i], 1);
-      mbar_init(&sm.s_full[i], 1);
-      mbar_init(&sm.s_free[i], 4);
-      mbar_init(&sm.p_full[i], 4);
-      mbar_init(&sm.p_free[i], 1);
+      mbar_init(&sm.k_full[i], 1);
+      mbar_init(&sm.k_empty[i], 1);
     }
+    mbar_init(&sm.v_full, 1);
+    mbar_init(&sm.v_empty, 1);
+    mbar_init(&sm.s_full, 1);
+    mbar_init(&sm.s_free, 4);
+    mbar_init(&sm.p_full, 4);
+    mbar_init(&sm.p_free, 1);
     mbar_init(&sm.o_full, 1);
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<512>(&sm.tmem);
+  if (warp == 2) tmem_alloc<256>(&sm.tmem);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = sm.tmem;  // S[0] cols 0-127, S[1] 128-255, O 256-319
+  const uint32_t tmem = sm.tmem;  // S cols 0-127, O 128-191
 
   if (warp == 0) {
     if (lane == 0) {
-      // ---------------- TMA producer: Q once; K (pass 1) then K+V (pass 2) per key tile
+      // ---------------- TMA producer: Q once; K per tile in both passes, V per tile in pass 2
       mbar_arrive_expect_tx(&sm.q_full, kTile);
       tma_load_2d(sm.q, &tm_qkv, &sm.q_full, qcol, row0 + qb * TQ);
       int c = 0;
       for (int pass = 0; pass < 2; ++pass) {
         for (int j = 0; j < nkb; ++j, ++c) {
           const int st = c & 1;
-          mbar_wait(&sm.kv_empty[st], ((c >> 1) & 1) ^ 1);
-          mbar_arrive_expect_tx(&sm.kv_full[st], pass ? 2 * kTile : kTile);
-          tma_load_2d(sm.k[st], &tm_qkv, &sm.kv_full[st], kcol, row0 + j * TK);
-          if (pass) tma_load_2d(sm.v[st], &tm_qkv, &sm.kv_full[st], vcol, row0 + j * TK);
+          mbar_wait(&sm.k_empty[st], ((c >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(&sm.k_full[st], kTile);
+          tma_load_2d(sm.k[st], &tm_qkv, &sm.k_full[st], kcol, row0 + j * TK);
+          if (pass) {
+            mbar_wait(&sm.v_empty, (j & 1) ^ 1);
+            mbar_arrive_expect_tx(&sm.v_full, kTile);
+            tma_load_2d(sm.v, &tm_qkv, &sm.v_full, vcol, row0 + j * TK);
+          }
         }
       }
     }
@@ -100,42 +115,33 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t kIdS = idesc_bf16_f32(TQ, TK, false, false);  // S = Q K^T
       constexpr uint32_t kIdO = idesc_bf16_f32(TQ, HD, false, true);   // O += P V (V MN-major)
       mbar_wait(&sm.q_full, 0);
-      const uint32_t qa = smem_u32(sm.q);
-      int c = 0;  // kv loads consumed == S tiles produced
-      auto issue_s = [&](int cc) {
-        const int st = cc & 1, sb = cc & 1;
-        mbar_wait(&sm.kv_full[st], (cc >> 1) & 1);
-        mbar_wait(&sm.s_free[sb], ((cc >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t ka = smem_u32(sm.k[st]);
+      const uint32_t qa = smem_u32(sm.q), va = smem_u32(sm.v), pa = smem_u32(sm.p);
+      int c = 0;
+      for (int pass = 0; pass < 2; ++pass) {
+        for (int j = 0; j < nkb; ++j, ++c) {
+          const int st = c & 1;
+          mbar_wait(&sm.k_full[st], (c >> 1) & 1);
+          mbar_wait(&sm.s_free, (c & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t ka = smem_u32(sm.k[st]);
 #pragma unroll
-        for (int k = 0; k < HD / 16; ++k)
-          umma_bf16(tmem + sb * TK, umma_desc_sw128(qa + k * 32, 16, 1024), umma_desc_sw128(ka + k * 32, 16, 1024),
-                    kIdS, k > 0 ? 1u : 0u);
-        umma_commit(&sm.s_full[sb]);
-      };
-      // pass 1: S tiles only (the softmax warps reduce them to the row log-sum-exp)
-      for (int j = 0; j < nkb; ++j, ++c) {
-        issue_s(c);
-        umma_commit(&sm.kv_empty[c & 1]);
-      }
-      // pass 2: S_{j+1} is issued before waiting for P_j so softmax and MMA overlap
-      const int c0 = c;
-      issue_s(c0);
-      for (int j = 0; j < nkb; ++j) {
-        const int cc = c0 + j;
-        if (j + 1 < nkb) issue_s(cc + 1);
-        const int pb = j & 1;
-        mbar_wait(&sm.p_full[pb], (j >> 1) & 1);
-        tc_fence_after();
-        const uint32_t pa = smem_u32(sm.p[pb]);
-        const uint32_t va = smem_u32(sm.v[cc & 1]);
+          for (int k = 0; k < HD / 16; ++k)
+            umma_bf16(tmem, umma_desc_sw128(qa + k * 32, 16, 1024), umma_desc_sw128(ka + k * 32, 16, 1024), kIdS,
+                      k > 0 ? 1u : 0u);
+          umma_commit(&sm.s_full);
+          umma_commit(&sm.k_empty[st]);
+          if (pass) {
+            mbar_wait(&sm.v_full, j & 1);
+            mbar_wait(&sm.p_full, j & 1);
+            tc_fence_after();
 #pragma unroll
-        for (int k = 0; k < TK / 16; ++k)
-          umma_bf16(tmem + 256, umma_desc_sw128(pa + (k >> 2) * (TQ * 128) + (k & 3) * 32, 16, 1024),
-                    umma_desc_sw128(va + k * 2048, 8192, 1024), kIdO, (j > 0 || k > 0) ? 1u : 0u);
-        umma_commit(&sm.p_free[pb]);
-        umma_commit(&sm.kv_empty[cc & 1]);
+            for (int k = 0; k < TK / 16; ++k)
+              umma_bf16(tmem + 128, umma_desc_sw128(pa + (k >> 2) * (TQ * 128) + (k & 3) * 32, 16, 1024),
+                        umma_desc_sw128(va + k * 2048, 8192, 1024), kIdO, (j > 0 || k > 0) ? 1u : 0u);
+            umma_commit(&sm.p_free);
+            umma_commit(&sm.v_empty);
+          }
+        }
       }
       umma_commit(&sm.o_full);
     }
@@ -144,75 +150,430 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int r = (warp - 4) * 32 + lane;
     const int q = qb * TQ + r;
     const uint32_t trow = tmem + (static_cast<uint32_t>((warp - 4) * 32) << 16);
-    float m = -INFINITY, l = 0.f;
     int c = 0;
-    auto load_s = [&](int cc, float (&s)[TK]) {
-      const int sb = cc & 1;
-      mbar_wait(&sm.s_full[sb], (cc >> 1) & 1);
+    float mraw = -INFINITY;
+    for (int j = 0; j < nkb; ++j, ++c) {  // pass 1: row max of the raw scores
+      mbar_wait(&sm.s_full, c & 1);
       tc_fence_after();
+      const bool diag = j == qb;
 #pragma unroll
       for (int k4 = 0; k4 < TK / 32; ++k4) {
         uint32_t u[32];
-        tmem_ld32(trow + sb * TK + k4 * 32, u);
+        tmem_ld32(trow + k4 * 32, u);
         tmem_ld_wait();
 #pragma unroll
-        for (int t = 0; t < 32; ++t) s[k4 * 32 + t] = __uint_as_float(u[t]);
+        for (int t = 0; t < 32; ++t) {
+          const float x = __uint_as_float(u[t]);
+          if (!diag || k4 * 32 + t <= r) mraw = fmaxf(mraw, x);
+        }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.s_free[sb]);
-    };
-    float s[TK];
-    for (int j = 0; j < nkb; ++j, ++c) {
-      load_s(c, s);
-      float mx = -INFINITY;
-#pragma unroll
-      for (int t = 0; t < TK; ++t) {
-        float x = s[t] * scale_log2;
-        if (j == qb && j * TK + t > q) x = -INFINITY;
-        s[t] = x;
-        mx = fmaxf(mx, x);
-      }
-      const float mn = fmaxf(m, mx);
-      float acc = 0.f;
-#pragma unroll
-      for (int t = 0; t < TK; ++t) acc += exp2f(s[t] - mn);
-      l = l * exp2f(m - mn) + acc;
-      m = mn;
+      if (lane == 0) mbar_arrive(&sm.s_free);
     }
-    const float lse2 = m + log2f(l);
-    for (int j = 0; j < nkb; ++j, ++c) {
-      load_s(c, s);
-      const int pb = j & 1;
-      mbar_wait(&sm.p_free[pb], ((j >> 1) & 1) ^ 1);
-      const uint32_t prow = smem_u32(sm.p[pb]) + r * 128;
+    const float m2 = mraw * scale_log2;
+    float l = 0.f;
+    const uint32_t pbase = smem_u32(sm.p) + r * 128;
+    for (int j = 0; j < nkb; ++j, ++c) {  // pass 2: P = exp(S - max), l += rowsum(P)
+      mbar_wait(&sm.s_full, c & 1);
+      tc_fence_after();
+      mbar_wait(&sm.p_free, (j & 1) ^ 1);
+      const bool diag = j == qb;
 #pragma unroll
-      for (int ch = 0; ch < TK / 64; ++ch) {
+      for (int k4 = 0; k4 < TK / 32; ++k4) {
+        uint32_t u[32];
+        tmem_ld32(trow + k4 * 32, u);
+        tmem_ld_wait();
+        uint32_t w[16];
 #pragma unroll
-        for (int piece = 0; piece < 8; ++piece) {
-          uint32_t w[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int t = ch * 64 + piece * 8 + 2 * e;
-            float p0 = exp2f(s[t] * scale_log2 - lse2), p1 = exp2f(s[t + 1] * scale_log2 - lse2);
-            if (j == qb) {
-              if (j * TK + t > q) p0 = 0.f;
-              if (j * TK + t + 1 > q) p1 = 0.f;
-            }
-            w[e] = pack_bf16(p0, p1);
+        for (int t = 0; t < 32; t += 2) {
+          float p0 = ex2(__uint_as_float(u[t]) * scale_log2 - m2);
+          float p1 = ex2(__uint_as_float(u[t + 1]) * scale_log2 - m2);
+          if (diag) {
+            if (k4 * 32 + t > r) p0 = 0.f;
+            if (k4 * 32 + t + 1 > r) p1 = 0.f;
           }
-          st_shared_v4(prow + ch * (TQ * 128) + ((piece ^ (r & 7)) << 4), w[0], w[1], w[2], w[3]);
+          l += p0 + p1;
+          w[t / 2] = pack_bf16(p0, p1);
         }
+        const int ch = k4 >> 1, piece0 = (k4 & 1) * 4;
+#pragma unroll
+        for (int pc = 0; pc < 4; ++pc)
+          st_shared_v4(pbase + ch * (TQ * 128) + (((piece0 + pc) ^ (r & 7)) << 4), w[4 * pc], w[4 * pc + 1],
+                       w[4 * pc + 2], w[4 * pc + 3]);
       }
+      tc_fence_before();
       fence_proxy_async();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.p_full[pb]);
+      if (lane == 0) {
+        mbar_arrive(&sm.s_free);
+        mbar_arrive(&sm.p_full);
+      }
     }
-    // ---------------- epilogue: O (already normalised) -> bf16, lse
+    // ---------------- epilogue: O / l -> bf16, lse
     mbar_wait(&sm.o_full, 0);
     tc_fence_after();
+    const float inv = 1.f / l;
     const size_t ldo = static_cast<size_t>(H) * HD;
     __nv_bfloat16* orow = o + (static_cast<size_t>(row0) + q) * ldo + static_cast<size_t>(h) * HD;
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      uint32_t u[32];
+      tmem_ld32(trow + 128 + half * 32, u);
+      tmem_ld_wait();
+#pragma unroll
+      for (int piece = 0; piece < 4; ++piece) {
+        uint4 v;
+        v.x = pack_bf16(__uint_as_float(u[8 * piece + 0]) * inv, __uint_as_float(u[8 * piece + 1]) * inv);
+        v.y = pack_bf16(__uint_as_float(u[8 * piece + 2]) * inv, __uint_as_float(u[8 * piece + 3]) * inv);
+        v.z = pack_bf16(__uint_as_float(u[8 * piece + 4]) * inv, __uint_as_float(u[8 * piece + 5]) * inv);
+        v.w = pack_bf16(__uint_as_float(u[8 * piece + 6]) * inv, __uint_as_float(u[8 * piece + 7]) * inv);
+        reinterpret_cast<uint4*>(orow + half * 32)[piece] = v;
+      }
+    }
+    lse[static_cast<size_t>(bh) * T + q] = (m2 + log2f(l)) * kLn2;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_free<256>(tmem);
+}
+
+// ---------------------------------------------------------------- backward
+// D[bh*T + q] = sum_c dO[q, c] O[q, c]   (one warp per (token, head))
+__global__ void dsum_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout, int B, int T,
+                            int H, float* __restrict__ D) {
+  const long long w = blockIdx.x * 8LL + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (w >= static_cast<long long>(B) * T * H) return;
+  const long long tok = w / H;
+  const int h = static_cast<int>(w % H);
+  const size_t off = static_cast<size_t>(tok) * H * HD + static_cast<size_t>(h) * HD + 2 * lane;
+  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(o + off));
+  const float2 d = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dout + off));
+  float acc = a.x * d.x + a.y * d.y;
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+  const int b = static_cast<int>(tok / T), q = static_cast<int>(tok % T);
+  if (lane == 0) D[(static_cast<size_t>(b) * H + h) * T + q] = acc;
+}
+
+// writes 32 bf16 values (one 64-byte half of a 128-byte swizzled row segment) of row r into
+// a K-major SW128 operand buffer laid out as [K/64 chunks][128 rows][128 B]
+__device__ __forceinline__ void put32(uint32_t base, int r, int col0, const float (&v)[32]) {
+  const int ch = col0 >> 6, piece0 = (col0 & 63) >> 3;
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const uint32_t w0 = pack_bf16(v[8 * p + 0], v[8 * p + 1]), w1 = pack_bf16(v[8 * p + 2], v[8 * p + 3]);
+    const uint32_t w2 = pack_bf16(v[8 * p + 4], v[8 * p + 5]), w3 = pack_bf16(v[8 * p + 6], v[8 * p + 7]);
+    st_shared_v4(base + ch * (128 * 128) + r * 128 + (((piece0 + p) ^ (r & 7)) << 4), w0, w1, w2, w3);
+  }
+}
+
+struct SmemKV {  // dK / dV kernel
+  uint8_t k[kTile], v[kTile];
+  uint8_t q[2][kTile], d_o[2][kTile];
+  uint8_t p[kPBuf], ds[kPBuf];
+  float lse2[2][TQ], dsum[2][TQ];
+  uint64_t kv_full, qd_full[2], qd_empty[2], s_full, s_free, pd_full, pd_free, acc_full;
+  uint32_t tmem;
+};
+
+// One CTA per (128-key tile, sequence x head); loops over query tiles i >= key tile.
+//   S^T = K Q^T, dP^T = V dO^T (TMEM)  ->  P^T = exp(S^T - lse), dS^T = P^T (dP^T - D)  (softmax warps,
+//   row = key)  ->  dV += P^T dO, dK += dS^T Q (TMEM accumulators, B operands MN-major from the tiles)
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+                        const float* __restrict__ lse, const float* __restrict__ D, int T, int H,
+                        __nv_bfloat16* __restrict__ dqkv, float scale, float scale_log2) {
+  extern __shared__ uint8_t smem_raw[];
+  SmemKV& sm = *reinterpret_cast<SmemKV*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nqb = T / TQ, kb = blockIdx.x;
+  const int bh = blockIdx.y, b = bh / H, h = bh % H;
+  const int row0 = b * T;
+  const int qcol = h * HD, kcol = (H + h) * HD, vcol = (2 * H + h) * HD, ocol = h * HD;
+  const int ntiles = nqb - kb;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tm_qkv);
+    tma_prefetch(&tm_do);
+  }
+  if (warp == 1 && lane == 0) {
+    mbar_init(&sm.kv_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm.qd_full[i], 1);
+      mbar_init(&sm.qd_empty[i], 1);
+    }
+    mbar_init(&sm.s_full, 1);
+    mbar_init(&sm.s_free, 4);
+    mbar_init(&sm.pd_full, 4);
+    mbar_init(&sm.pd_free, 1);
+    mbar_init(&sm.acc_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(&sm.tmem);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem;  // S^T cols 0-127, dP^T 128-255, dV 256-319, dK 320-383
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(&sm.kv_full, 2 * kTile);
+      tma_load_2d(sm.k, &tm_qkv, &sm.kv_full, kcol, row0 + kb * TK);
+      tma_load_2d(sm.v, &tm_qkv, &sm.kv_full, vcol, row0 + kb * TK);
+      for (int i = 0; i < ntiles; ++i) {
+        const int st = i & 1;
+        mbar_wait(&sm.qd_empty[st], ((i >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&sm.qd_full[st], 2 * kTile);
+        const int qrow = row0 + (kb + i) * TQ;
+        tma_load_2d(sm.q[st], &tm_qkv, &sm.qd_full[st], qcol, qrow);
+        tma_load_2d(sm.d_o[st], &tm_do, &sm.qd_full[st], ocol, qrow);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t kIdS = idesc_bf16_f32(TK, TQ, false, false);  // [keys x q], K = hd
+      constexpr uint32_t kIdA = idesc_bf16_f32(TK, HD, false, true);   // [keys x hd], K = q, B MN-major
+      mbar_wait(&sm.kv_full, 0);
+      const uint32_t ka = smem_u32(sm.k), va = smem_u32(sm.v);
+      const uint32_t pa = smem_u32(sm.p), da = smem_u32(sm.ds);
+      for (int i = 0; i < ntiles; ++i) {
+        const int st = i & 1;
+        mbar_wait(&sm.qd_full[st], (i >> 1) & 1);
+        mbar_wait(&sm.s_free, (i & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t qa = smem_u32(sm.q[st]), oa = smem_u32(sm.d_o[st]);
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k) {
+          umma_bf16(tmem, umma_desc_sw128(ka + k * 32, 16, 1024), umma_desc_sw128(qa + k * 32, 16, 1024), kIdS,
+                    k > 0 ? 1u : 0u);
+          umma_bf16(tmem + 128, umma_desc_sw128(va + k * 32, 16, 1024), umma_desc_sw128(oa + k * 32, 16, 1024), kIdS,
+                    k > 0 ? 1u : 0u);
+        }
+        umma_commit(&sm.s_full);
+        mbar_wait(&sm.pd_full, i & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < TQ / 16; ++k) {
+          const uint32_t aoff = (k >> 2) * (128 * 128) + (k & 3) * 32;
+          umma_bf16(tmem + 256, umma_desc_sw128(pa + aoff, 16, 1024), umma_desc_sw128(oa + k * 2048, 8192, 1024),
+                    kIdA, (i > 0 || k > 0) ? 1u : 0u);
+          umma_bf16(tmem + 320, umma_desc_sw128(da + aoff, 16, 1024), umma_desc_sw128(qa + k * 2048, 8192, 1024),
+                    kIdA, (i > 0 || k > 0) ? 1u : 0u);
+        }
+        umma_commit(&sm.pd_free);
+        umma_commit(&sm.qd_empty[st]);
+      }
+      umma_commit(&sm.acc_full);
+    }
+  } else if (warp >= 4) {
+    const int r = (warp - 4) * 32 + lane;  // key row within the tile
+    const int key = kb * TK + r;
+    const uint32_t trow = tmem + (static_cast<uint32_t>((warp - 4) * 32) << 16);
+    // stage the per-query lse / D of each query tile in shared memory (softmax warps only)
+    for (int i = 0; i < ntiles; ++i) {
+      const int st = i & 1;
+      const int q0 = (kb + i) * TQ;
+      // lse/D for this tile: every softmax thread loads one value (the tile has 128 queries)
+      sm.lse2[st][r] = lse[static_cast<size_t>(bh) * T + q0 + r] * kLog2e;
+      sm.dsum[st][r] = D[static_cast<size_t>(bh) * T + q0 + r];
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      mbar_wait(&sm.s_full, i & 1);
+      tc_fence_after();
+      mbar_wait(&sm.pd_free, (i & 1) ^ 1);  // the previous tile's dV/dK MMAs have read P / dS
+      const uint32_t pbase = smem_u32(sm.p), dbase = smem_u32(sm.ds);
+#pragma unroll 1
+      for (int c0 = 0; c0 < TQ; c0 += 32) {
+        uint32_t us[32], ud[32];
+        tmem_ld32(trow + c0, us);
+        tmem_ld32(trow + 128 + c0, ud);
+        tmem_ld_wait();
+        float pv[32], dv[32];
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+          const int qi = c0 + t;
+          float p = ex2(__uint_as_float(us[t]) * scale_log2 - sm.lse2[st][qi]);
+          if (i == 0 && qi < r) p = 0.f;  // diagonal tile: query before key
+          pv[t] = p;
+          dv[t] = p * (__uint_as_float(ud[t]) - sm.dsum[st][qi]);
+        }
+        put32(pbase, r, c0, pv);
+        put32(dbase, r, c0, dv);
+      }
+      tc_fence_before();
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&sm.s_free);
+        mbar_arrive(&sm.pd_full);
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // lse/D slots of this stage are reused two tiles later
+    }
+    (void)key;
+    // ---------------- epilogue: dV, dK (x scale) -> dqkv
+    mbar_wait(&sm.acc_full, 0);
+    tc_fence_after();
+    const size_t ld = static_cast<size_t>(3) * H * HD;
+    __nv_bfloat16* krow = dqkv + (static_cast<size_t>(row0) + kb * TK + r) * ld + static_cast<size_t>(kcol);
+    __nv_bfloat16* vrow = dqkv + (static_cast<size_t>(row0) + kb * TK + r) * ld + static_cast<size_t>(vcol);
+#pragma unroll
+    for (int which = 0; which < 2; ++which) {
+      __nv_bfloat16* dst = which ? krow : vrow;
+      const float mul = which ? scale : 1.f;
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        uint32_t u[32];
+        tmem_ld32(trow + 256 + which * 64 + half * 32, u);
+        tmem_ld_wait();
+#pragma unroll
+        for (int piece = 0; piece < 4; ++piece) {
+          uint4 w;
+          w.x = pack_bf16(__uint_as_float(u[8 * piece + 0]) * mul, __uint_as_float(u[8 * piece + 1]) * mul);
+          w.y = pack_bf16(__uint_as_float(u[8 * piece + 2]) * mul, __uint_as_float(u[8 * piece + 3]) * mul);
+          w.z = pack_bf16(__uint_as_float(u[8 * piece + 4]) * mul, __uint_as_float(u[8 * piece + 5]) * mul);
+          w.w = pack_bf16(__uint_as_float(u[8 * piece + 6]) * mul, __uint_as_float(u[8 * piece + 7]) * mul);
+          reinterpret_cast<uint4*>(dst + half * 32)[piece] = w;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_free<512>(tmem);
+}
+
+struct SmemQ {  // dQ kernel
+  uint8_t q[kTile], d_o[kTile];
+  uint8_t k[2][kTile], v[2][kTile];
+  uint8_t ds[kPBuf];
+  uint64_t qd_full, kv_full[2], kv_empty[2], s_full, s_free, ds_full, ds_free, acc_full;
+  uint32_t tmem;
+};
+
+// One CTA per (128-query tile, sequence x head); loops over key tiles j <= query tile.
+//   S = Q K^T, dP = dO V^T (TMEM) -> dS = P (dP - D) (softmax warps, row = query) -> dQ += dS K
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_dq_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+                      const float* __restrict__ lse, const float* __restrict__ D, int T, int H,
+                      __nv_bfloat16* __restrict__ dqkv, float scale, float scale_log2) {
+  extern __shared__ uint8_t smem_raw[];
+  SmemQ& sm = *reinterpret_cast<SmemQ*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nqb = T / TQ;
+  const int qb = nqb - 1 - static_cast<int>(blockIdx.x);
+  const int bh = blockIdx.y, b = bh / H, h = bh % H;
+  const int row0 = b * T;
+  const int qcol = h * HD, kcol = (H + h) * HD, vcol = (2 * H + h) * HD, ocol = h * HD;
+  const int nkb = qb + 1;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tm_qkv);
+    tma_prefetch(&tm_do);
+  }
+  if (warp == 1 && lane == 0) {
+    mbar_init(&sm.qd_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm.kv_full[i], 1);
+      mbar_init(&sm.kv_empty[i], 1);
+    }
+    mbar_init(&sm.s_full, 1);
+    mbar_init(&sm.s_free, 4);
+    mbar_init(&sm.ds_full, 4);
+    mbar_init(&sm.ds_free, 1);
+    mbar_init(&sm.acc_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(&sm.tmem);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem;  // S cols 0-127, dP 128-255, dQ 256-319
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(&sm.qd_full, 2 * kTile);
+      tma_load_2d(sm.q, &tm_qkv, &sm.qd_full, qcol, row0 + qb * TQ);
+      tma_load_2d(sm.d_o, &tm_do, &sm.qd_full, ocol, row0 + qb * TQ);
+      for (int j = 0; j < nkb; ++j) {
+        const int st = j & 1;
+        mbar_wait(&sm.kv_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&sm.kv_full[st], 2 * kTile);
+        tma_load_2d(sm.k[st], &tm_qkv, &sm.kv_full[st], kcol, row0 + j * TK);
+        tma_load_2d(sm.v[st], &tm_qkv, &sm.kv_full[st], vcol, row0 + j * TK);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t kIdS = idesc_bf16_f32(TQ, TK, false, false);  // [q x keys], K = hd
+      constexpr uint32_t kIdQ = idesc_bf16_f32(TQ, HD, false, true);   // [q x hd], K = keys, B MN-major
+      mbar_wait(&sm.qd_full, 0);
+      const uint32_t qa = smem_u32(sm.q), oa = smem_u32(sm.d_o), da = smem_u32(sm.ds);
+      for (int j = 0; j < nkb; ++j) {
+        const int st = j & 1;
+        mbar_wait(&sm.kv_full[st], (j >> 1) & 1);
+        mbar_wait(&sm.s_free, (j & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t ka = smem_u32(sm.k[st]), va = smem_u32(sm.v[st]);
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k) {
+          umma_bf16(tmem, umma_desc_sw128(qa + k * 32, 16, 1024), umma_desc_sw128(ka + k * 32, 16, 1024), kIdS,
+                    k > 0 ? 1u : 0u);
+          umma_bf16(tmem + 128, umma_desc_sw128(oa + k * 32, 16, 1024), umma_desc_sw128(va + k * 32, 16, 1024), kIdS,
+                    k > 0 ? 1u : 0u);
+        }
+        umma_commit(&sm.s_full);
+        mbar_wait(&sm.ds_full, j & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < TK / 16; ++k)
+          umma_bf16(tmem + 256, umma_desc_sw128(da + (k >> 2) * (128 * 128) + (k & 3) * 32, 16, 1024),
+                    umma_desc_sw128(ka + k * 2048, 8192, 1024), kIdQ, (j > 0 || k > 0) ? 1u : 0u);
+        umma_commit(&sm.ds_free);
+        umma_commit(&sm.kv_empty[st]);
+      }
+      umma_commit(&sm.acc_full);
+    }
+  } else if (warp >= 4) {
+    const int r = (warp - 4) * 32 + lane;
+    const int q = qb * TQ + r;
+    const uint32_t trow = tmem + (static_cast<uint32_t>((warp - 4) * 32) << 16);
+    const float l2 = lse[static_cast<size_t>(bh) * T + q] * kLog2e;
+    const float dq = D[static_cast<size_t>(bh) * T + q];
+    const uint32_t dbase = smem_u32(sm.ds);
+    for (int j = 0; j < nkb; ++j) {
+      mbar_wait(&sm.s_full, j & 1);
+      tc_fence_after();
+      mbar_wait(&sm.ds_free, (j & 1) ^ 1);
+#pragma unroll 1
+      for (int c0 = 0; c0 < TK; c0 += 32) {
+        uint32_t us[32], ud[32];
+        tmem_ld32(trow + c0, us);
+        tmem_ld32(trow + 128 + c0, ud);
+        tmem_ld_wait();
+        float dv[32];
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+          float p = ex2(__uint_as_float(us[t]) * scale_log2 - l2);
+          if (j == qb && c0 + t > r) p = 0.f;  // diagonal tile: key after query
+          dv[t] = p * (__uint_as_float(ud[t]) - dq);
+        }
+        put32(dbase, r, c0, dv);
+      }
+      tc_fence_before();
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&sm.s_free);
+        mbar_arrive(&sm.ds_full);
+      }
+    }
+    mbar_wait(&sm.acc_full, 0);
+    tc_fence_after();
+    const size_t ld = static_cast<size_t>(3) * H * HD;
+    __nv_bfloat16* qrow = dqkv + (static_cast<size_t>(row0) + q) * ld + static_cast<size_t>(qcol);
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
       uint32_t u[32];
@@ -220,15 +581,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_ld_wait();
 #pragma unroll
       for (int piece = 0; piece < 4; ++piece) {
-        uint4 v;
-        v.x = pack_bf16(__uint_as_float(u[8 * piece + 0]), __uint_as_float(u[8 * piece + 1]));
-        v.y = pack_bf16(__uint_as_float(u[8 * piece + 2]), __uint_as_float(u[8 * piece + 3]));
-        v.z = pack_bf16(__uint_as_float(u[8 * piece + 4]), __uint_as_float(u[8 * piece + 5]));
-        v.w = pack_bf16(__uint_as_float(u[8 * piece + 6]), __uint_as_float(u[8 * piece + 7]));
-        reinterpret_cast<uint4*>(orow + half * 32)[piece] = v;
+        uint4 w;
+        w.x = pack_bf16(__uint_as_float(u[8 * piece + 0]) * scale, __uint_as_float(u[8 * piece + 1]) * scale);
+        w.y = pack_bf16(__uint_as_float(u[8 * piece + 2]) * scale, __uint_as_float(u[8 * piece + 3]) * scale);
+        w.z = pack_bf16(__uint_as_float(u[8 * piece + 4]) * scale, __uint_as_float(u[8 * piece + 5]) * scale);
+        w.w = pack_bf16(__uint_as_float(u[8 * piece + 6]) * scale, __uint_as_float(u[8 * piece + 7]) * scale);
+        reinterpret_cast<uint4*>(qrow + half * 32)[piece] = w;
       }
     }
-    lse[static_cast<size_t>(bh) * T + q] = lse2 * kLn2;
   }
   tc_fence_before();
   __syncthreads();
@@ -253,6 +613,34 @@ void attn_fwd_tc(const bf16* qkv, size_t B, size_t T, size_t H, size_t hd, bf16*
   const float scale_log2 = kLog2e / sqrtf(static_cast<float>(hd));
   dim3 grid(static_cast<unsigned>(T / TQ), static_cast<unsigned>(B * H));
   attn_fwd_tc_kernel<<<grid, kThreads, smem, s>>>(tm, static_cast<int>(T), static_cast<int>(H), o, lse, scale_log2);
+  CKF_LAUNCH_CHECK();
+}
+
+void attn_bwd_tc(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, size_t B, size_t T, size_t H,
+                 size_t hd, bf16* dqkv, float* Dsum, cudaStream_t s) {
+  if (!attn_fwd_tc_supported(T, hd)) raise(1, "tcgen05 attention: head_dim 64 and seq_len % 128 == 0");
+  const size_t warps = B * T * H;
+  dsum_kernel<<<static_cast<unsigned>((warps + 7) / 8), 256, 0, s>>>(o, dout, static_cast<int>(B), static_cast<int>(T),
+                                                                     static_cast<int>(H), Dsum);
+  CKF_LAUNCH_CHECK();
+  const CUtensorMap tq = tma::make_2d_bf16(qkv, 3 * H * hd, B * T, 3 * H * hd, 64, 128);
+  const CUtensorMap td = tma::make_2d_bf16(dout, H * hd, B * T, H * hd, 64, 128);
+  const size_t smem_kv = sizeof(SmemKV) + 1024, smem_q = sizeof(SmemQ) + 1024;
+  static bool attr = false;
+  if (!attr) {
+    CKF_CUDA(cudaFuncSetAttribute(attn_dkdv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem_kv)));
+    CKF_CUDA(cudaFuncSetAttribute(attn_dq_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem_q)));
+    attr = true;
+  }
+  const float scale = 1.f / sqrtf(static_cast<float>(hd));
+  dim3 grid(static_cast<unsigned>(T / TQ), static_cast<unsigned>(B * H));
+  attn_dkdv_tc_kernel<<<grid, kThreads, smem_kv, s>>>(tq, td, lse, Dsum, static_cast<int>(T), static_cast<int>(H),
+                                                      dqkv, scale, scale * kLog2e);
+  CKF_LAUNCH_CHECK();
+  attn_dq_tc_kernel<<<grid, kThreads, smem_q, s>>>(tq, td, lse, Dsum, static_cast<int>(T), static_cast<int>(H), dqkv,
+                                                   scale, scale * kLog2e);
   CKF_LAUNCH_CHECK();
 }
 

@@ -342,7 +342,10 @@ struct LlamaBlock final : BlockImpl {
     bf16* dqkv = dgu;  // dgu is dead; Mt x 3d fits in Mt x 2f only if 3d <= 2f
     if (3 * d > 2 * f) dqkv = static_cast<bf16*>(eng->ws(Mt * 3 * d * 2, 56));
     timed(KC_ATTN, 2.5 * attn_flops_fwd(rows), Mt * d * 16.0, [&] {
-      llama::attn_bwd(c.qkv, c.o, c.lse, d_o, rows, T, H, hd, dqkv, Dsum, st);
+      if (llama::attn_fwd_tc_supported(T, hd))
+        llama::attn_bwd_tc(c.qkv, c.o, c.lse, d_o, rows, T, H, hd, dqkv, Dsum, st);  // tcgen05 + TMEM
+      else
+        llama::attn_bwd(c.qkv, c.o, c.lse, d_o, rows, T, H, hd, dqkv, Dsum, st);
     });
     timed(KC_NORM, 0.0, Mt * d * 8.0, [&] { llama::rope(dqkv, Mt, T, d, H, 1, st); });
     gemm(di, 3 * di, Mi, c.xn1, di, true, dqkv, 3 * di, true, G + off.wqkv, 3 * di, tc::kAccF32);  // gWqkv += xn1^T dqkv

@@ -66,36 +66,32 @@ __global__ void embed_bwd_kernel(const int* __restrict__ keys, const int* __rest
 }
 
 // ---------------------------------------------------------------- RMSNorm
-constexpr int kMaxV4 = 32;  // d <= 4096
-
-__global__ void rmsnorm_fwd_kernel(const float4* __restrict__ x, const float4* __restrict__ g, size_t rows,
-                                   size_t d4, __nv_bfloat162* __restrict__ y, float* __restrict__ rstd,
-                                   float4* __restrict__ xcopy) {
+// one warp per row; the row lives in registers (lane owns columns lane + 32 i)
+template <int V4>  // float4 per lane (d = 128 * V4)
+__global__ void __launch_bounds__(256) rmsnorm_fwd_kernel(const float4* __restrict__ x, const float4* __restrict__ g,
+                                                          size_t rows, __nv_bfloat162* __restrict__ y,
+                                                          float* __restrict__ rstd, float4* __restrict__ xcopy) {
+  constexpr int d4 = 32 * V4;
   const size_t r = blockIdx.x * static_cast<size_t>(kWarpsPerBlock) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (r >= rows) return;
-  float4 v[kMaxV4];
+  float4 v[V4];
   float ss = 0.f;
 #pragma unroll
-  for (int i = 0; i < kMaxV4; ++i) {
-    const size_t c = lane + 32 * static_cast<size_t>(i);
-    if (c < d4) {
-      v[i] = x[r * d4 + c];
-      ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
-    }
+  for (int i = 0; i < V4; ++i) {
+    v[i] = x[r * d4 + lane + 32 * i];
+    ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
   }
   ss = warp_sum_f(ss);
   const float rs = rsqrtf(ss / static_cast<float>(4 * d4) + kNormEps);
   if (lane == 0) rstd[r] = rs;
 #pragma unroll
-  for (int i = 0; i < kMaxV4; ++i) {
-    const size_t c = lane + 32 * static_cast<size_t>(i);
-    if (c < d4) {
-      const float4 gg = g[c];
-      y[(r * d4 + c) * 2] = __floats2bfloat162_rn(v[i].x * rs * gg.x, v[i].y * rs * gg.y);
-      y[(r * d4 + c) * 2 + 1] = __floats2bfloat162_rn(v[i].z * rs * gg.z, v[i].w * rs * gg.w);
-      if (xcopy) xcopy[r * d4 + c] = v[i];
-    }
+  for (int i = 0; i < V4; ++i) {
+    const size_t c = r * d4 + lane + 32 * i;
+    const float4 gg = g[lane + 32 * i];
+    y[2 * c] = __floats2bfloat162_rn(v[i].x * rs * gg.x, v[i].y * rs * gg.y);
+    y[2 * c + 1] = __floats2bfloat162_rn(v[i].z * rs * gg.z, v[i].w * rs * gg.w);
+    if (xcopy) xcopy[c] = v[i];
   }
 }
 
@@ -247,11 +243,10 @@ __device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
 
 __global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ gu, int ntok, int f,
                                   __nv_bfloat16* __restrict__ a) {
-  const int f8 = f / 8;
-  const long long n = static_cast<long long>(ntok) * f8;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int t = static_cast<int>(i / f8), c = static_cast<int>(i % f8) * 8;
+  const unsigned f8 = static_cast<unsigned>(f) / 8;
+  const unsigned n = static_cast<unsigned>(ntok) * f8;  // < 2^32 for any microbatch this engine runs
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const unsigned t = i / f8, c = (i - t * f8) * 8;
     const __nv_bfloat16* row = gu + static_cast<size_t>(t) * 2 * f;
     float g[8], u[8], o[8];
     unpack8(*reinterpret_cast<const uint4*>(row + c), g);
@@ -264,11 +259,10 @@ __global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ gu, int ntok
 
 __global__ void swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ gu, const __nv_bfloat16* __restrict__ da,
                                   int ntok, int f, __nv_bfloat16* __restrict__ dgu) {
-  const int f8 = f / 8;
-  const long long n = static_cast<long long>(ntok) * f8;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int t = static_cast<int>(i / f8), c = static_cast<int>(i % f8) * 8;
+  const unsigned f8 = static_cast<unsigned>(f) / 8;
+  const unsigned n = static_cast<unsigned>(ntok) * f8;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const unsigned t = i / f8, c = (i - t * f8) * 8;
     const __nv_bfloat16* row = gu + static_cast<size_t>(t) * 2 * f;
     float g[8], u[8], dd[8], dg[8], du[8];
     unpack8(*reinterpret_cast<const uint4*>(row + c), g);
@@ -436,13 +430,30 @@ void embed_bwd(const int* tok, size_t ntok, const float* dh, size_t d, float* gE
   CKF_LAUNCH_CHECK();
 }
 
+template <int V4>
+void rmsnorm_fwd_t(const float* x, const float* g, size_t rows, bf16* y, float* rstd, float* xcopy, cudaStream_t s) {
+  rmsnorm_fwd_kernel<V4><<<blocks_for_rows(rows), 32 * kWarpsPerBlock, 0, s>>>(
+      reinterpret_cast<const float4*>(x), reinterpret_cast<const float4*>(g), rows,
+      reinterpret_cast<__nv_bfloat162*>(y), rstd, reinterpret_cast<float4*>(xcopy));
+  CKF_LAUNCH_CHECK();
+}
+
 void rmsnorm_fwd(const float* x, const float* g, size_t rows, size_t d, bf16* y, float* rstd, float* xcopy,
                  cudaStream_t s) {
   need_d(d);
-  rmsnorm_fwd_kernel<<<blocks_for_rows(rows), 32 * kWarpsPerBlock, 0, s>>>(
-      reinterpret_cast<const float4*>(x), reinterpret_cast<const float4*>(g), rows, d / 4,
-      reinterpret_cast<__nv_bfloat162*>(y), rstd, reinterpret_cast<float4*>(xcopy));
-  CKF_LAUNCH_CHECK();
+  switch (d / 128) {
+    case 1: return rmsnorm_fwd_t<1>(x, g, rows, y, rstd, xcopy, s);
+    case 2: return rmsnorm_fwd_t<2>(x, g, rows, y, rstd, xcopy, s);
+    case 3: return rmsnorm_fwd_t<3>(x, g, rows, y, rstd, xcopy, s);
+    case 4: return rmsnorm_fwd_t<4>(x, g, rows, y, rstd, xcopy, s);
+    case 6: return rmsnorm_fwd_t<6>(x, g, rows, y, rstd, xcopy, s);
+    case 8: return rmsnorm_fwd_t<8>(x, g, rows, y, rstd, xcopy, s);
+    case 12: return rmsnorm_fwd_t<12>(x, g, rows, y, rstd, xcopy, s);
+    case 16: return rmsnorm_fwd_t<16>(x, g, rows, y, rstd, xcopy, s);
+    case 24: return rmsnorm_fwd_t<24>(x, g, rows, y, rstd, xcopy, s);
+    case 32: return rmsnorm_fwd_t<32>(x, g, rows, y, rstd, xcopy, s);
+    default: raise(1, "LLaMA model_dim / 128 must be one of 1,2,3,4,6,8,12,16,24,32");
+  }
 }
 
 int rmsnorm_bwd_blocks(size_t rows) { return static_cast<int>((rows + kBwdRowsPerBlock - 1) / kBwdRowsPerBlock); }
@@ -516,6 +527,7 @@ void rope(bf16* qkv, size_t ntok, size_t T, size_t d, size_t heads, int inverse,
 
 void swiglu_fwd(const bf16* gu, size_t ntok, size_t f, bf16* a, cudaStream_t s) {
   if (f % 8) raise(1, "ffn width must be a multiple of 8");
+  if (ntok * f / 8 >= (1ull << 32)) raise(1, "swiglu: microbatch too large");
   swiglu_fwd_kernel<<<grid_for(ntok * f / 8, 256), 256, 0, s>>>(gu, static_cast<int>(ntok), static_cast<int>(f), a);
   CKF_LAUNCH_CHECK();
 }

@@ -61,6 +61,8 @@ void attn_fwd(const bf16* qkv, size_t B, size_t T, size_t H, size_t hd, bf16* o,
 // tcgen05/TMEM/TMA forward (attention_tc.cu) for head_dim 64, seq_len % 128 == 0
 bool attn_fwd_tc_supported(size_t T, size_t hd);
 void attn_fwd_tc(const bf16* qkv, size_t B, size_t T, size_t H, size_t hd, bf16* o, float* lse, cudaStream_t s);
+void attn_bwd_tc(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, size_t B, size_t T, size_t H,
+                 size_t hd, bf16* dqkv, float* Dsum, cudaStream_t s);
 // dqkv [B*T x 3*H*hd]; Dsum scratch [B*H*T] fp32.  Deterministic (no atomics).
 void attn_bwd(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, size_t B, size_t T, size_t H,
               size_t hd, bf16* dqkv, float* Dsum, cudaStream_t s);
