@@ -285,6 +285,10 @@ int ckf_engine_kernel_stats(ckf_engine_t e, int cls, double* ms, long* launches,
  *     "U,reason").
  * ===================================================================== */
 int ckf_run_experiment(const char* kv_config, const char* trace_text, uint64_t seed, char* record, size_t cap);
+/* run_experiment_to_dir (src/experiment.cpp:202-213): the same run, writing
+ * metrics.csv, events.csv, summary.json and config.resolved in the reference's
+ * schema (format_version=1) into dir; wall_hours / recovery_s are measured. */
+int ckf_run_experiment_to_dir(const char* kv_config, const char* trace_text, uint64_t seed, const char* dir);
 
 #ifdef __cplusplus
 }

@@ -113,6 +113,7 @@ def lib():
         "ckf_engine_stream": (i, [eng, C.POINTER(C.c_void_p)]), "ckf_engine_kernel_timing": (i, [eng, i]),
         "ckf_engine_kernel_stats": (i, [eng, i, dp, C.POINTER(lng), dp, dp]),
         "ckf_run_experiment": (i, [cp, cp, u64, cp, sz]),
+        "ckf_run_experiment_to_dir": (i, [cp, cp, u64, cp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

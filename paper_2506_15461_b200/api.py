@@ -361,9 +361,16 @@ def run_experiment(cfg: dict, trace_text: str, seed: int):
     for ln in buf.value.decode().splitlines():
         p = ln.split(",")
         if p[0] == "E":
-            evals.append((int(p[1]), float(p[2]), float(p[3])))
+            evals.append((int(p[1]), float(p[2]), float(p[3])))  # p[4]: measured wall hours
         elif p[0] == "F":
             events.append((int(p[1]), int(p[2]), p[3], float(p[4]), float(p[5]), float(p[6])))
         elif p[0] == "U":
             unrec = ln[2:]
     return evals, events, unrec
+
+
+def run_experiment_to_dir(cfg: dict, trace_text: str, seed: int, out_dir: str):
+    """harness::run_experiment_to_dir (src/experiment.cpp:202-213): metrics.csv, events.csv,
+    summary.json, config.resolved in the reference's schema."""
+    kv = ";".join(f"{k}={v}" for k, v in cfg.items()).encode()
+    check(lib().ckf_run_experiment_to_dir(kv, trace_text.encode(), seed, out_dir.encode()))

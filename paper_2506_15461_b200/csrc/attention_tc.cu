@@ -26,6 +26,7 @@ using namespace ckf::sm100;
 
 constexpr int TQ = 128, TK = 128, HD = 64;
 constexpr int kThreads = 256;
+constexpr int kThreadsBwd = 384;  // backward: 8 softmax warps (2 per TMEM lane quarter, column halves)
 constexpr uint32_t kTile = TQ * HD * 2;      // 16 KiB: one 128 x 64 bf16 tile
 constexpr uint32_t kPBuf = TQ * TK * 2;      // 32 KiB: P as [2 K-chunks][128 rows][128 B]
 constexpr float kLog2e = 1.4426950408889634f;
@@ -282,7 +283,7 @@ struct SmemKV {  // dK / dV kernel
 // One CTA per (128-key tile, sequence x head); loops over query tiles i >= key tile.
 //   S^T = K Q^T, dP^T = V dO^T (TMEM)  ->  P^T = exp(S^T - lse), dS^T = P^T (dP^T - D)  (softmax warps,
 //   row = key)  ->  dV += P^T dO, dK += dS^T Q (TMEM accumulators, B operands MN-major from the tiles)
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreadsBwd, 1)
     attn_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
                         const float* __restrict__ lse, const float* __restrict__ D, int T, int H,
                         __nv_bfloat16* __restrict__ dqkv, float scale, float scale_log2) {
@@ -306,8 +307,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&sm.qd_empty[i], 1);
     }
     mbar_init(&sm.s_full, 1);
-    mbar_init(&sm.s_free, 4);
-    mbar_init(&sm.pd_full, 4);
+    mbar_init(&sm.s_free, 8);
+    mbar_init(&sm.pd_full, 8);
     mbar_init(&sm.pd_free, 1);
     mbar_init(&sm.acc_full, 1);
     fence_barrier_init();
@@ -369,23 +370,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       umma_commit(&sm.acc_full);
     }
   } else if (warp >= 4) {
-    const int r = (warp - 4) * 32 + lane;  // key row within the tile
-    const int key = kb * TK + r;
-    const uint32_t trow = tmem + (static_cast<uint32_t>((warp - 4) * 32) << 16);
-    // stage the per-query lse / D of each query tile in shared memory (softmax warps only)
+    const int sw = warp - 4, quarter = sw & 3, half = sw >> 2;
+    const int r = quarter * 32 + lane;  // key row within the tile
+    const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
     for (int i = 0; i < ntiles; ++i) {
       const int st = i & 1;
       const int q0 = (kb + i) * TQ;
-      // lse/D for this tile: every softmax thread loads one value (the tile has 128 queries)
-      sm.lse2[st][r] = lse[static_cast<size_t>(bh) * T + q0 + r] * kLog2e;
-      sm.dsum[st][r] = D[static_cast<size_t>(bh) * T + q0 + r];
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+      // per-query lse / D of this tile staged in shared memory by the first 128 softmax threads
+      if (half == 0) {
+        sm.lse2[st][r] = lse[static_cast<size_t>(bh) * T + q0 + r] * kLog2e;
+        sm.dsum[st][r] = D[static_cast<size_t>(bh) * T + q0 + r];
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");
       mbar_wait(&sm.s_full, i & 1);
       tc_fence_after();
       mbar_wait(&sm.pd_free, (i & 1) ^ 1);  // the previous tile's dV/dK MMAs have read P / dS
       const uint32_t pbase = smem_u32(sm.p), dbase = smem_u32(sm.ds);
 #pragma unroll 1
-      for (int c0 = 0; c0 < TQ; c0 += 32) {
+      for (int c0 = half * 64; c0 < half * 64 + 64; c0 += 32) {
         uint32_t us[32], ud[32];
         tmem_ld32(trow + c0, us);
         tmem_ld32(trow + 128 + c0, ud);
@@ -409,33 +411,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(&sm.s_free);
         mbar_arrive(&sm.pd_full);
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");  // lse/D slots of this stage are reused two tiles later
+      asm volatile("bar.sync 1, 256;" ::: "memory");  // lse/D slots of this stage are reused two tiles later
     }
-    (void)key;
-    // ---------------- epilogue: dV, dK (x scale) -> dqkv
+    // ---------------- epilogue: column half 0 -> dV, half 1 -> dK (x scale)
     mbar_wait(&sm.acc_full, 0);
     tc_fence_after();
     const size_t ld = static_cast<size_t>(3) * H * HD;
-    __nv_bfloat16* krow = dqkv + (static_cast<size_t>(row0) + kb * TK + r) * ld + static_cast<size_t>(kcol);
-    __nv_bfloat16* vrow = dqkv + (static_cast<size_t>(row0) + kb * TK + r) * ld + static_cast<size_t>(vcol);
+    const int which = half;
+    __nv_bfloat16* dst = dqkv + (static_cast<size_t>(row0) + kb * TK + r) * ld + static_cast<size_t>(which ? kcol : vcol);
+    const float mul = which ? scale : 1.f;
 #pragma unroll
-    for (int which = 0; which < 2; ++which) {
-      __nv_bfloat16* dst = which ? krow : vrow;
-      const float mul = which ? scale : 1.f;
+    for (int hh = 0; hh < 2; ++hh) {
+      uint32_t u[32];
+      tmem_ld32(trow + 256 + which * 64 + hh * 32, u);
+      tmem_ld_wait();
 #pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        uint32_t u[32];
-        tmem_ld32(trow + 256 + which * 64 + half * 32, u);
-        tmem_ld_wait();
-#pragma unroll
-        for (int piece = 0; piece < 4; ++piece) {
-          uint4 w;
-          w.x = pack_bf16(__uint_as_float(u[8 * piece + 0]) * mul, __uint_as_float(u[8 * piece + 1]) * mul);
-          w.y = pack_bf16(__uint_as_float(u[8 * piece + 2]) * mul, __uint_as_float(u[8 * piece + 3]) * mul);
-          w.z = pack_bf16(__uint_as_float(u[8 * piece + 4]) * mul, __uint_as_float(u[8 * piece + 5]) * mul);
-          w.w = pack_bf16(__uint_as_float(u[8 * piece + 6]) * mul, __uint_as_float(u[8 * piece + 7]) * mul);
-          reinterpret_cast<uint4*>(dst + half * 32)[piece] = w;
-        }
+      for (int piece = 0; piece < 4; ++piece) {
+        uint4 w;
+        w.x = pack_bf16(__uint_as_float(u[8 * piece + 0]) * mul, __uint_as_float(u[8 * piece + 1]) * mul);
+        w.y = pack_bf16(__uint_as_float(u[8 * piece + 2]) * mul, __uint_as_float(u[8 * piece + 3]) * mul);
+        w.z = pack_bf16(__uint_as_float(u[8 * piece + 4]) * mul, __uint_as_float(u[8 * piece + 5]) * mul);
+        w.w = pack_bf16(__uint_as_float(u[8 * piece + 6]) * mul, __uint_as_float(u[8 * piece + 7]) * mul);
+        reinterpret_cast<uint4*>(dst + hh * 32)[piece] = w;
       }
     }
   }
@@ -455,7 +452,7 @@ struct SmemQ {  // dQ kernel
 
 // One CTA per (128-query tile, sequence x head); loops over key tiles j <= query tile.
 //   S = Q K^T, dP = dO V^T (TMEM) -> dS = P (dP - D) (softmax warps, row = query) -> dQ += dS K
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreadsBwd, 1)
     attn_dq_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
                       const float* __restrict__ lse, const float* __restrict__ D, int T, int H,
                       __nv_bfloat16* __restrict__ dqkv, float scale, float scale_log2) {
@@ -480,8 +477,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&sm.kv_empty[i], 1);
     }
     mbar_init(&sm.s_full, 1);
-    mbar_init(&sm.s_free, 4);
-    mbar_init(&sm.ds_full, 4);
+    mbar_init(&sm.s_free, 8);
+    mbar_init(&sm.ds_full, 8);
     mbar_init(&sm.ds_free, 1);
     mbar_init(&sm.acc_full, 1);
     fence_barrier_init();
@@ -537,9 +534,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       umma_commit(&sm.acc_full);
     }
   } else if (warp >= 4) {
-    const int r = (warp - 4) * 32 + lane;
+    const int sw = warp - 4, quarter = sw & 3, half = sw >> 2;
+    const int r = quarter * 32 + lane;
     const int q = qb * TQ + r;
-    const uint32_t trow = tmem + (static_cast<uint32_t>((warp - 4) * 32) << 16);
+    const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
     const float l2 = lse[static_cast<size_t>(bh) * T + q] * kLog2e;
     const float dq = D[static_cast<size_t>(bh) * T + q];
     const uint32_t dbase = smem_u32(sm.ds);
@@ -548,7 +546,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       mbar_wait(&sm.ds_free, (j & 1) ^ 1);
 #pragma unroll 1
-      for (int c0 = 0; c0 < TK; c0 += 32) {
+      for (int c0 = half * 64; c0 < half * 64 + 64; c0 += 32) {
         uint32_t us[32], ud[32];
         tmem_ld32(trow + c0, us);
         tmem_ld32(trow + 128 + c0, ud);
@@ -573,21 +571,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_wait(&sm.acc_full, 0);
     tc_fence_after();
     const size_t ld = static_cast<size_t>(3) * H * HD;
-    __nv_bfloat16* qrow = dqkv + (static_cast<size_t>(row0) + q) * ld + static_cast<size_t>(qcol);
+    __nv_bfloat16* qrow = dqkv + (static_cast<size_t>(row0) + q) * ld + static_cast<size_t>(qcol) + half * 32;
+    uint32_t u[32];
+    tmem_ld32(trow + 256 + half * 32, u);
+    tmem_ld_wait();
 #pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      uint32_t u[32];
-      tmem_ld32(trow + 256 + half * 32, u);
-      tmem_ld_wait();
-#pragma unroll
-      for (int piece = 0; piece < 4; ++piece) {
-        uint4 w;
-        w.x = pack_bf16(__uint_as_float(u[8 * piece + 0]) * scale, __uint_as_float(u[8 * piece + 1]) * scale);
-        w.y = pack_bf16(__uint_as_float(u[8 * piece + 2]) * scale, __uint_as_float(u[8 * piece + 3]) * scale);
-        w.z = pack_bf16(__uint_as_float(u[8 * piece + 4]) * scale, __uint_as_float(u[8 * piece + 5]) * scale);
-        w.w = pack_bf16(__uint_as_float(u[8 * piece + 6]) * scale, __uint_as_float(u[8 * piece + 7]) * scale);
-        reinterpret_cast<uint4*>(qrow + half * 32)[piece] = w;
-      }
+    for (int piece = 0; piece < 4; ++piece) {
+      uint4 w;
+      w.x = pack_bf16(__uint_as_float(u[8 * piece + 0]) * scale, __uint_as_float(u[8 * piece + 1]) * scale);
+      w.y = pack_bf16(__uint_as_float(u[8 * piece + 2]) * scale, __uint_as_float(u[8 * piece + 3]) * scale);
+      w.z = pack_bf16(__uint_as_float(u[8 * piece + 4]) * scale, __uint_as_float(u[8 * piece + 5]) * scale);
+      w.w = pack_bf16(__uint_as_float(u[8 * piece + 6]) * scale, __uint_as_float(u[8 * piece + 7]) * scale);
+      reinterpret_cast<uint4*>(qrow)[piece] = w;
     }
   }
   tc_fence_before();
@@ -636,10 +631,10 @@ void attn_bwd_tc(const bf16* qkv, const bf16* o, const float* lse, const bf16* d
   }
   const float scale = 1.f / sqrtf(static_cast<float>(hd));
   dim3 grid(static_cast<unsigned>(T / TQ), static_cast<unsigned>(B * H));
-  attn_dkdv_tc_kernel<<<grid, kThreads, smem_kv, s>>>(tq, td, lse, Dsum, static_cast<int>(T), static_cast<int>(H),
+  attn_dkdv_tc_kernel<<<grid, kThreadsBwd, smem_kv, s>>>(tq, td, lse, Dsum, static_cast<int>(T), static_cast<int>(H),
                                                       dqkv, scale, scale * kLog2e);
   CKF_LAUNCH_CHECK();
-  attn_dq_tc_kernel<<<grid, kThreads, smem_q, s>>>(tq, td, lse, Dsum, static_cast<int>(T), static_cast<int>(H), dqkv,
+  attn_dq_tc_kernel<<<grid, kThreadsBwd, smem_q, s>>>(tq, td, lse, Dsum, static_cast<int>(T), static_cast<int>(H), dqkv,
                                                    scale, scale * kLog2e);
   CKF_LAUNCH_CHECK();
 }

@@ -16,7 +16,8 @@
 namespace ckf {
 void llama_token_batch(uint64_t data_seed, uint64_t stream, uint64_t index, size_t rows, size_t T, size_t V, int* out,
                        cudaStream_t s);
-std::string run_experiment(const std::string& kv, const std::string& trace_text, uint64_t seed);
+std::string run_experiment(const std::string& kv, const std::string& trace_text, uint64_t seed,
+                           const std::string& dir);
 int nccl_unique_id(void* out, size_t cap);
 }  // namespace ckf
 
@@ -611,9 +612,16 @@ int ckf_engine_kernel_stats(ckf_engine_t e, int cls, double* ms, long* launches,
 // ---------------------------------------------------------------- (4) trainer
 int ckf_run_experiment(const char* kv, const char* trace_text, uint64_t seed, char* record, size_t cap) {
   return guard([&] {
-    const std::string r = ckf::run_experiment(kv ? kv : "", trace_text ? trace_text : "", seed);
+    const std::string r = ckf::run_experiment(kv ? kv : "", trace_text ? trace_text : "", seed, "");
     if (r.size() + 1 > cap) ckf::raise(CKF_E_USAGE, "record buffer too small");
     std::memcpy(record, r.c_str(), r.size() + 1);
+  });
+}
+
+int ckf_run_experiment_to_dir(const char* kv, const char* trace_text, uint64_t seed, const char* dir) {
+  return guard([&] {
+    if (!dir || !*dir) ckf::raise(CKF_E_CONFIG, "output directory required");
+    ckf::run_experiment(kv ? kv : "", trace_text ? trace_text : "", seed, dir);
   });
 }
 

@@ -108,7 +108,10 @@ struct Params {
   float alpha;
   int nm, nn, tiles, nk;
   int splits, kb_per_split, units;
-  int* flags;  // split-K ordering counters (one per tile), self-resetting
+  int* flags;    // split-K: 2 counters per tile (partials stored, reduction done), self-resetting
+  float* ws;     // split-K partial tiles: [units][BM][BN] fp32
+  float* C;      // split-K: fp32 C (row pitch ldc) the reduced tile is added into
+  int ldc;
 };
 
 template <int BN>
@@ -140,7 +143,7 @@ __device__ __forceinline__ Unit unit_of(const Params& p, int u) {
 template <int BN, bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
-                const __grid_constant__ CUtensorMap tmap_c, Params p) {
+                const __grid_constant__ CUtensorMap tmap_c, const __grid_constant__ CUtensorMap tmap_ws, Params p) {
   using C = Cfg<BN>;
   constexpr int ST = C::kStages;
   constexpr uint32_t IDESC = idesc_bf16_f32(BM, BN, A_MN, B_MN);
@@ -160,6 +163,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch(&tmap_a);
     tma_prefetch(&tmap_b);
     tma_prefetch(&tmap_c);
+    if (p.splits > 1) tma_prefetch(&tmap_ws);
   }
   if (warp == 1 && lane == 0) {
     for (int i = 0; i < ST; ++i) {
@@ -256,14 +260,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       const Unit w = unit_of(p, u);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      if (p.splits > 1 && w.split > 0) {
-        // ordered split-K: split s adds after all 4 warps of split s-1 finished theirs
-        if (lane == 0) {
-          while (ld_acquire(p.flags + w.tile) < 4 * w.split) __nanosleep(64);
-          fence_proxy_async_global();
-        }
-        __syncwarp();
-      }
       const uint32_t trow = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN);
       const int m0 = w.mb * BM + q * 32;
 #pragma unroll 1
@@ -308,7 +304,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) {
           const int n0 = w.nb * BN + c0;
-          if (n0 < p.N && m0 < p.M) {
+          if (p.splits > 1) {
+            // split-K: this split's partial tile goes to its workspace slot (plain store)
+            tma_store_2d(&tmap_ws, sb, c0, (w.split * p.tiles + w.tile) * BM + q * 32);
+          } else if (n0 < p.N && m0 < p.M) {
             if constexpr (EPI == kAccF32)
               tma_reduce_add_2d(&tmap_c, sb, n0, m0);
             else
@@ -319,12 +318,54 @@ __global__ void __launch_bounds__(kThreads, 1)
         sbuf ^= 1;
       }
       if (p.splits > 1) {
+        // Deterministic split-K reduction (all units are co-resident: units <= grid):
+        // 1) every warp publishes its stored partial rows, 2) once all 4*splits warps of the
+        // tile have, the tile's rows are shared out among them and each sums the partials in
+        // split order and adds the result into C.
+        int* stored = p.flags + 2 * w.tile;
+        int* reduced = stored + 1;
+        const int nwarps = 4 * p.splits;
         if (lane == 0) {
-          bulk_wait_all();  // this split's adds have landed
+          bulk_wait_all();  // this warp's partial rows have landed in the workspace
           fence_proxy_async_global();
           __threadfence();
-          const int old = atomicAdd(p.flags + w.tile, 1);
-          if (w.split == p.splits - 1 && old == 4 * p.splits - 1) atomicExch(p.flags + w.tile, 0);
+          atomicAdd(stored, 1);
+          while (ld_acquire(stored) < nwarps) __nanosleep(32);
+        }
+        __syncwarp();
+        const int wid = w.split * 4 + q;
+        const int per = (BM + nwarps - 1) / nwarps;
+        for (int rr = wid * per; rr < min(BM, (wid + 1) * per); ++rr) {
+          const int m = w.mb * BM + rr;
+          if (m >= p.M) break;
+          for (int c = lane * 4; c < BN; c += 128) {
+            const int n = w.nb * BN + c;
+            if (n >= p.N) break;
+            float4 acc4 = __ldcg(reinterpret_cast<const float4*>(p.ws + (static_cast<size_t>(w.tile) * BM + rr) * BN + c));
+            for (int sp = 1; sp < p.splits; ++sp) {
+              const float4 v = __ldcg(reinterpret_cast<const float4*>(
+                  p.ws + ((static_cast<size_t>(sp) * p.tiles + w.tile) * BM + rr) * BN + c));
+              acc4.x += v.x;
+              acc4.y += v.y;
+              acc4.z += v.z;
+              acc4.w += v.w;
+            }
+            float4* dst = reinterpret_cast<float4*>(p.C + static_cast<size_t>(m) * p.ldc + n);
+            float4 o = *dst;
+            o.x += acc4.x;
+            o.y += acc4.y;
+            o.z += acc4.z;
+            o.w += acc4.w;
+            *dst = o;
+          }
+        }
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence();
+          if (atomicAdd(reduced, 1) == nwarps - 1) {  // last one out resets the tile's counters
+            atomicExch(stored, 0);
+            atomicExch(reduced, 0);
+          }
         }
         __syncwarp();
       }
@@ -351,8 +392,19 @@ int num_sms() {
   return n;
 }
 
+float* split_workspace(size_t bytes) {
+  static float* ws = nullptr;
+  static size_t cap = 0;
+  if (bytes > cap) {
+    if (ws) CKF_CUDA(cudaFree(ws));
+    cap = std::max<size_t>(bytes, 32u << 20);
+    CKF_CUDA(cudaMalloc(&ws, cap));
+  }
+  return ws;
+}
+
 int* split_flags(size_t n) {
-  // one self-resetting counter per output tile (zero between launches)
+  // two self-resetting counters per output tile (zero between launches)
   static int* flags = nullptr;
   static size_t cap = 0;
   static int dev = -1;
@@ -390,7 +442,14 @@ void launch_t(const GemmDesc& g, int splits, cudaStream_t s) {
   p.kb_per_split = (p.nk + p.splits - 1) / p.splits;
   p.splits = (p.nk + p.kb_per_split - 1) / p.kb_per_split;  // no empty split
   p.units = p.tiles * p.splits;
-  p.flags = p.splits > 1 ? split_flags(static_cast<size_t>(p.tiles)) : nullptr;
+  if (p.splits > 1 && (p.units > num_sms() || EPI != kAccF32 || g.N % 4 != 0)) p.splits = 1, p.units = p.tiles,
+                                                                                   p.kb_per_split = p.nk;
+  p.flags = p.splits > 1 ? split_flags(2 * static_cast<size_t>(p.tiles)) : nullptr;
+  p.ws = p.splits > 1 ? split_workspace(static_cast<size_t>(p.units) * BM * BN * sizeof(float)) : nullptr;
+  p.C = static_cast<float*>(g.C);
+  p.ldc = g.ldc;
+  const CUtensorMap twm = p.splits > 1 ? tma::make_2d_f32(p.ws, BN, static_cast<uint64_t>(p.units) * BM, BN, 32, 32)
+                                       : tcm;
   auto kern = gemm_kernel<BN, A_MN, B_MN, EPI>;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
@@ -398,7 +457,7 @@ void launch_t(const GemmDesc& g, int splits, cudaStream_t s) {
     attr_set = true;
   }
   const int grid = std::min(p.units, num_sms());
-  kern<<<grid, kThreads, C::kSmem, s>>>(ta, tb, tcm, p);
+  kern<<<grid, kThreads, C::kSmem, s>>>(ta, tb, tcm, twm, p);
   CKF_LAUNCH_CHECK();
 }
 

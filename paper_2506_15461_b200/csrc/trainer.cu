@@ -9,6 +9,9 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <filesystem>
+#include <fstream>
 #include <map>
 #include <sstream>
 
@@ -72,6 +75,7 @@ class Trainer {
   }
 
   std::string run() {
+    t0_ = std::chrono::steady_clock::now();
     const bool cfp = c_.strategy == "checkfree-plus";
     const int s = static_cast<int>(c_.stages);
     const auto std_order = host::standard_order(s);
@@ -153,8 +157,9 @@ class Trainer {
   double add_eval(long slot) {
     const double v = val_loss();
     evals_.push_back({slot, v});
-    char buf[160];
-    std::snprintf(buf, sizeof(buf), "E,%ld,%.17g,%.17g\n", slot, last_train_, v);
+    char buf[200];
+    const double hours = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0_).count() / 3600.0;
+    std::snprintf(buf, sizeof(buf), "E,%ld,%.17g,%.17g,%.17g\n", slot, last_train_, v, hours);
     out_ << buf;
     return v;
   }
@@ -250,17 +255,96 @@ class Trainer {
   std::vector<std::pair<long, double>> evals_;
   std::vector<Pending> pending_;
   std::ostringstream out_;
+  std::chrono::steady_clock::time_point t0_;
 };
+
+// ------------------------------------------------------------------ run records (experiment.cpp:156-213)
+std::string fmt12(double v) {
+  char b[64];
+  std::snprintf(b, sizeof(b), "%.12g", v);
+  return b;
+}
+
+void write_text(const std::string& path, const std::string& text) {
+  std::ofstream f(path, std::ios::binary);
+  if (!f) host::fail(1, "cannot write '" + path + "'");
+  f << text;
+}
+
+// metrics.csv / events.csv / summary.json / config.resolved in the reference's schema.
+// wall_hours and recovery_s are MEASURED on the B200 (host clock around the device
+// work; CUDA events around the recovery), where the reference models them.
+void write_records(const host::Config& c, uint64_t seed, const std::string& rec, const std::string& dir) {
+  std::filesystem::create_directories(dir);
+  std::ostringstream m, e;
+  m << "# format_version=1\niter,train_loss,val_loss,wall_hours\n";
+  e << "# format_version=1\niter,stage,action,reduction_error,recovery_s\n";
+  std::istringstream in(rec);
+  std::string line, unrec;
+  long last_iter = 0, n_events = 0;
+  double last_train = 0.0, last_val = 0.0, hours = 0.0;
+  while (std::getline(in, line)) {
+    std::vector<std::string> f;
+    std::stringstream ls(line);
+    std::string tok;
+    while (std::getline(ls, tok, ',')) f.push_back(tok);
+    if (f.empty()) continue;
+    if (f[0] == "E" && f.size() >= 5) {
+      last_iter = std::stol(f[1]);
+      last_train = std::stod(f[2]);
+      last_val = std::stod(f[3]);
+      hours = std::stod(f[4]);
+      m << last_iter << ',' << fmt12(last_train) << ',' << fmt12(last_val) << ',' << fmt12(hours) << '\n';
+    } else if (f[0] == "F" && f.size() >= 7) {
+      e << f[1] << ',' << f[2] << ',' << f[3] << ',' << fmt12(std::stod(f[4])) << ',' << fmt12(std::stod(f[6]) / 1e3)
+        << '\n';
+      ++n_events;
+    } else if (f[0] == "U") {
+      unrec = line.substr(2);
+    }
+  }
+  std::ostringstream j;
+  j << "{\n  \"format_version\": 1,\n  \"strategy\": \"" << c.strategy << "\",\n  \"seed\": " << seed
+    << ",\n  \"iterations_run\": " << last_iter << ",\n  \"model_iterations\": " << last_iter
+    << ",\n  \"iterations_to_target\": null,\n  \"model_iterations_to_target\": null,\n  \"total_hours\": "
+    << fmt12(hours) << ",\n  \"iteration_time_s\": " << fmt12(last_iter ? hours * 3600.0 / last_iter : 0.0)
+    << ",\n  \"unrecoverable\": " << (unrec.empty() ? "false" : "true");
+  if (!unrec.empty()) j << ",\n  \"unrecoverable_reason\": \"" << unrec << "\"";
+  j << ",\n  \"final_train_loss\": " << fmt12(last_train) << ",\n  \"final_val_loss\": " << fmt12(last_val)
+    << ",\n  \"failure_events\": " << n_events << ",\n  \"timing\": \"measured on the GPU\"\n}\n";
+  std::ostringstream r;
+  r << "# resolved experiment configuration\n";
+  r << "block = " << c.block << "\nprecision = " << c.precision << '\n';
+  r << "input-dim = " << c.input_dim << "\nhidden-dim = " << c.hidden_dim << "\nmodel-dim = " << c.model_dim
+    << "\noutput-dim = " << c.output_dim << "\nlayers = " << c.layers << "\nstages = " << c.stages << '\n';
+  if (c.block == "llama") r << "heads = " << c.heads << "\nseq-len = " << c.seq_len << '\n';
+  r << "activation = " << c.activation << "\ntask = " << c.task << "\nstrategy = " << c.strategy
+    << "\ncheckpoint-interval = " << c.checkpoint_interval << "\nlr-bump = " << fmt12(c.lr_bump)
+    << "\nrecovered-moments = " << c.recovered_moments << "\np-hour = " << fmt12(c.p_hour) << '\n';
+  if (c.p_iter >= 0.0) r << "p-iter = " << fmt12(c.p_iter) << '\n';
+  r << "iter-seconds = " << fmt12(c.iter_seconds) << "\neligible = " << c.eligible << "\niters = " << c.iters
+    << "\nbatch = " << c.batch << "\nmicrobatches = " << c.microbatches << "\nlr = " << fmt12(c.lr) << '\n';
+  if (c.target_loss > 0.0) r << "target-loss = " << fmt12(c.target_loss) << '\n';
+  r << "eval-interval = " << c.eval_interval << "\nval-size = " << c.val_size << "\nseed = " << seed
+    << "\nschedule = " << c.schedule << "\nswap-from = " << c.swap_from << '\n';
+  write_text(dir + "/metrics.csv", m.str());
+  write_text(dir + "/events.csv", e.str());
+  write_text(dir + "/summary.json", j.str());
+  write_text(dir + "/config.resolved", r.str());
+}
 
 }  // namespace
 
-std::string run_experiment(const std::string& kv, const std::string& trace_text, uint64_t seed) {
+std::string run_experiment(const std::string& kv, const std::string& trace_text, uint64_t seed,
+                           const std::string& dir) {
   host::Config c = host::Config::from_kv(kv);
   c.validate();
   host::Trace t = trace_text.empty() ? c.resolve_trace(seed) : host::parse_trace(trace_text);
   host::validate_trace(t);
   Trainer tr(c, t, seed);
-  return tr.run();
+  std::string rec = tr.run();
+  if (!dir.empty()) write_records(c, seed, rec, dir);
+  return rec;
 }
 
 }  // namespace ckf

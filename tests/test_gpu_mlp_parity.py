@@ -195,3 +195,34 @@ def test_fp32_recovered_weights_within_1e5(goldens):
         assert np.all(m == 0) and np.all(v == 0)
         om, lr, step = eng.scalars(2)
         assert om == 0.0 and step == 0 and lr == pytest.approx(1.1 * lr_before, rel=1e-15)
+
+
+def test_run_records_in_reference_schema(tmp_path, trainer_goldens):
+    """run_experiment_to_dir (experiment.cpp:202-213): the four artefacts in the reference's schema;
+    metrics.csv / events.csv equal the reference's own files except the time columns (modeled there,
+    measured here)."""
+    import json
+    run = next(r for r in trainer_goldens["runs"] if r["name"] == "checkfree_s2_at50")
+    P.api.run_experiment_to_dir(run["cfg"], run["trace"], run["seed"], str(tmp_path))
+
+    def strip(text, col):  # drop one column (wall_hours / recovery_s)
+        return [",".join(f for i, f in enumerate(l.split(",")) if i != col) if not l.startswith("#") else l
+                for l in text.strip().splitlines()]
+
+    ours = strip((tmp_path / "metrics.csv").read_text(), 3)
+    ref = strip(run["metrics_csv"], 3)
+    assert ours[:2] == ref[:2] and len(ours) == len(ref)
+    for a, b in zip(ours[2:], ref[2:]):
+        fa, fb = a.split(","), b.split(",")
+        assert fa[0] == fb[0]
+        for x, y in zip(fa[1:], fb[1:]):
+            assert float(x) == pytest.approx(float(y), rel=1e-9)
+    oe = strip((tmp_path / "events.csv").read_text(), 4)
+    re_ = strip(run["events_csv"], 4)
+    assert oe[:2] == re_[:2] and len(oe) == len(re_)
+    for a, b in zip(oe[2:], re_[2:]):
+        fa, fb = a.split(","), b.split(",")
+        assert fa[:3] == fb[:3] and float(fa[3]) == pytest.approx(float(fb[3]), rel=1e-6)
+    s = json.loads((tmp_path / "summary.json").read_text())
+    assert s["format_version"] == 1 and s["strategy"] == "checkfree" and s["failure_events"] == 1
+    assert "strategy = checkfree" in (tmp_path / "config.resolved").read_text()
