@@ -163,11 +163,22 @@ def run_reference_arm(args, w: dict):
 METRIC = "pipeline train tokens/s"
 
 
+def placement(world: int, s: int):
+    """(pipeline ranks P, replicas R) with P * R = world: contiguous stage blocks per rank,
+    data-parallel replicas once every stage has its own GPU."""
+    if world <= s and s % world == 0:
+        return world, 1
+    if world % s == 0:
+        return s, world // s
+    raise SystemExit(f"{s} stages cannot be placed on {world} GPUs (need world | s or s | world)")
+
+
 def workload_config(args, w: dict) -> dict:
-    cfg = {"workload": args.workload, "block": w["block"], "stages": w["stages"],
+    P, R = placement(args.gpus, w["stages"])
+    cfg = {"parallelism": f"pp{P}" + (f"xdp{R}" if R > 1 else ""),"workload": args.workload, "block": w["block"], "stages": w["stages"],
            "microbatches": w["microbatches"], "layers": w["layers"], "model_dim": w["model_dim"],
-           "hidden_dim": w["hidden_dim"], "tokens_per_step": tokens_per_step(w), "seq_len": w["seq_len"],
-           "strategy": "checkfree", "placement": f"{w['stages']} stages on {args.gpus} GPU(s)",
+           "hidden_dim": w["hidden_dim"], "tokens_per_step": tokens_per_step(w) * R, "seq_len": w["seq_len"],
+           "strategy": "checkfree", "placement": f"{w['stages']} stages on {P} pipeline rank(s) x {R} replica(s)",
            "l2": "256 MiB memset between timed steps (outside the events)"}
     if w["block"] == "llama":
         cfg.update(vocab=w["output_dim"], heads=w["heads"])
@@ -195,7 +206,7 @@ def run_ours(args, w: dict):
     import torch
     import torch.distributed as dist
 
-    import paper_2506_15461_b200 as P
+    import paper_2506_15461_b200 as P_
     from paper_2506_15461_b200 import api
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -205,8 +216,7 @@ def run_ours(args, w: dict):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     s = w["stages"]
-    if world > 1 and s % world != 0:
-        raise SystemExit(f"{s} stages cannot be placed in contiguous blocks on {world} GPUs")
+    P, R = placement(world, s)
 
     mb_rows = w["rows"] // w["microbatches"]
     if w["block"] == "llama":
@@ -216,15 +226,15 @@ def run_ours(args, w: dict):
     else:
         spec = api.ModelSpec(w["input_dim"], w["hidden_dim"], w["model_dim"], w["output_dim"], w["layers"], s,
                              precision=w["precision"], max_rows=mb_rows, device=local)
-    eng = P.Engine(spec)
+    eng = P_.Engine(spec)
     eng.init(1, 3e-4)
     if world > 1:
-        uid = [P.nccl_unique_id() if rank == 0 else None]
+        uid = [P_.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
-        eng.attach_comm(uid[0], world, rank, [(sid - 1) * world // s for sid in range(1, s + 1)])
+        eng.attach_comm(uid[0], world, rank, [(sid - 1) * P // s for sid in range(1, s + 1)], R)
 
     orders = np.array(api.build_schedule(w["microbatches"], False, s), np.int32)
-    gen = torch.Generator().manual_seed(1234 + rank)
+    gen = torch.Generator().manual_seed(1234 + rank // P)  # one batch per replica (weak scaling)
     xh, yh = make_batch(w, gen, local)
     xh, yh = xh.pin_memory(), (yh.pin_memory() if yh is not None else None)
     xd = xh.to(f"cuda:{local}", non_blocking=False)
@@ -318,8 +328,8 @@ def run_ours(args, w: dict):
         return
 
     peaks, peak_src = load_peaks()
-    sweep = recovery_sweep(P, local, peaks["hbm_gbs"]) if (world == 1 and not args.no_recovery_sweep) else None
-    tok = tokens_per_step(w) * (1 if world == 1 else 1)
+    sweep = recovery_sweep(P_, local, peaks["hbm_gbs"]) if (world == 1 and not args.no_recovery_sweep) else None
+    tok = tokens_per_step(w) * R  # every replica trains on its own batch
     value = tok / (ms / 1e3)
     e2e_value = tok / (e2e_ms / 1e3)
     # dominant kernel class (by device time inside the timed region)

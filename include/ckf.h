@@ -189,6 +189,12 @@ int ckf_engine_init(ckf_engine_t e, uint64_t seed, double lr);
  * uid is a ckf_nccl_unique_id blob shared by all ranks (e.g. via torch.distributed). */
 int ckf_nccl_unique_id(void* uid_out, size_t cap);
 int ckf_engine_attach_comm(ckf_engine_t e, const void* uid, int nranks, int rank, const int* stage_rank);
+/* pipeline x data parallel (config 4: 4 stages x DP2): nranks = replicas * P; rank r is
+ * pipeline rank r % P of replica r / P; stage_rank[] names PIPELINE ranks (0..P-1).  Each
+ * replica runs its own microbatches; owned gradients are summed over the replicas
+ * (ncclAllReduce on an ncclCommSplit group) before Adam, which divides by m * replicas. */
+int ckf_engine_attach_comm_dp(ckf_engine_t e, const void* uid, int nranks, int rank, const int* stage_rank,
+                              int replicas);
 
 /* One training iteration (pipeline.cpp:58-95).  orders: m*s stage ids, one
  * execution order per microbatch (ExecutionOrder, pipeline.hpp:12-24).

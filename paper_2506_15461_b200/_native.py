@@ -96,6 +96,7 @@ def lib():
         "ckf_engine_param_counts": (i, [eng, C.POINTER(sz), C.POINTER(sz), C.POINTER(sz)]),
         "ckf_engine_init": (i, [eng, u64, dbl]),
         "ckf_nccl_unique_id": (i, [vp, sz]), "ckf_engine_attach_comm": (i, [eng, vp, i, i, ip]),
+        "ckf_engine_attach_comm_dp": (i, [eng, vp, i, i, ip, i]),
         "ckf_engine_run_iteration": (i, [eng, ip, i, vp, vp, sz, i, lng, dp, dp]),
         "ckf_engine_eval_loss": (i, [eng, ip, vp, vp, sz, i, dp]),
         "ckf_engine_predict": (i, [eng, ip, dp, sz, dp]),

@@ -299,10 +299,11 @@ class Engine:
     def set_scalars(self, stage, omega, lr, step):
         check(lib().ckf_engine_set_scalars(self._h, stage, omega, lr, step))
 
-    def attach_comm(self, uid: bytes, nranks: int, rank: int, stage_rank):
+    def attach_comm(self, uid: bytes, nranks: int, rank: int, stage_rank, replicas: int = 1):
+        """Multi-GPU placement: stage_rank = pipeline rank per stage; nranks = replicas * pipeline ranks."""
         sr = np.ascontiguousarray(stage_rank, np.int32)
         buf = C.create_string_buffer(uid, 128)
-        check(lib().ckf_engine_attach_comm(self._h, buf, nranks, rank, _ip(sr)))
+        check(lib().ckf_engine_attach_comm_dp(self._h, buf, nranks, rank, _ip(sr), replicas))
 
     def sync(self):
         check(lib().ckf_engine_sync(self._h))

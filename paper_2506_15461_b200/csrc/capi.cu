@@ -480,7 +480,11 @@ int ckf_nccl_unique_id(void* uid_out, size_t cap) {
   return guard([&] { ckf::nccl_unique_id(uid_out, cap); });
 }
 int ckf_engine_attach_comm(ckf_engine_t e, const void* uid, int nranks, int rank, const int* stage_rank) {
-  return guard([&] { E(e)->attach_comm(uid, nranks, rank, stage_rank); });
+  return guard([&] { E(e)->attach_comm(uid, nranks, rank, stage_rank, 1); });
+}
+int ckf_engine_attach_comm_dp(ckf_engine_t e, const void* uid, int nranks, int rank, const int* stage_rank,
+                              int replicas) {
+  return guard([&] { E(e)->attach_comm(uid, nranks, rank, stage_rank, replicas); });
 }
 int ckf_engine_run_iteration(ckf_engine_t e, const int* orders, int m, const void* x, const void* y, size_t rows,
                              int on_device, long iteration, double* loss, double* omegas) {

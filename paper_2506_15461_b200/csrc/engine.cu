@@ -40,6 +40,7 @@ struct NcclApi {
   int (*Send)(const void*, size_t, int, int, void*, cudaStream_t) = nullptr;
   int (*Recv)(void*, size_t, int, int, void*, cudaStream_t) = nullptr;
   int (*AllReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*CommSplit)(void*, int, int, void**, void*) = nullptr;
   int (*GroupStart)() = nullptr;
   int (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(int) = nullptr;
@@ -60,6 +61,7 @@ NcclApi& nccl() {
       api.Recv = reinterpret_cast<int (*)(void*, size_t, int, int, void*, cudaStream_t)>(dlsym(h, "ncclRecv"));
       api.AllReduce = reinterpret_cast<int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t)>(
           dlsym(h, "ncclAllReduce"));
+      api.CommSplit = reinterpret_cast<int (*)(void*, int, int, void**, void*)>(dlsym(h, "ncclCommSplit"));
       api.GroupStart = reinterpret_cast<int (*)()>(dlsym(h, "ncclGroupStart"));
       api.GroupEnd = reinterpret_cast<int (*)()>(dlsym(h, "ncclGroupEnd"));
       api.GetErrorString = reinterpret_cast<const char* (*)(int)>(dlsym(h, "ncclGetErrorString"));
@@ -144,6 +146,7 @@ Engine::~Engine() {
   for (void* p : ws_) cudaFree(p);
   cudaFree(red_.partials);
   cudaFree(scal_);
+  if (dp_comm_ && nccl().CommDestroy) nccl().CommDestroy(dp_comm_);
   if (comm_ && nccl().CommDestroy) nccl().CommDestroy(comm_);
   for (cudaEvent_t ev : kev_) cudaEventDestroy(ev);
   if (ev0_) cudaEventDestroy(ev0_);
@@ -188,6 +191,15 @@ void* Engine::ws(size_t bytes, int slot) {
     ws_size_[static_cast<size_t>(slot)] = want;
   }
   return ws_[static_cast<size_t>(slot)];
+}
+
+std::vector<ParamGroup*> Engine::owned_groups() {
+  std::vector<ParamGroup*> v;
+  for (auto& g : stages_)
+    if (g.owned && g.n) v.push_back(&g);
+  for (ParamGroup* g : {&embed_, &deembed_})
+    if (g->owned && g->n) v.push_back(g);
+  return v;
 }
 
 // ------------------------------------------------------------------ kernel timing
@@ -235,11 +247,17 @@ void Engine::kt_collect() {
 }
 
 // ------------------------------------------------------------------ placement
-void Engine::attach_comm(const void* uid, int nranks, int rank, const int* stage_rank) {
+void Engine::attach_comm(const void* uid, int nranks, int rank, const int* stage_rank, int replicas) {
   if (nranks < 1 || rank < 0 || rank >= nranks) raise(1, "invalid rank / world size");
-  stage_rank_.assign(stage_rank, stage_rank + d_.s);
-  for (int r : stage_rank_)
-    if (r < 0 || r >= nranks) raise(1, "stage placed on a rank outside the world");
+  if (replicas < 1 || nranks % replicas) raise(1, "world size must be a multiple of the replica count");
+  const int P = nranks / replicas;  // pipeline ranks per replica
+  for (size_t i = 0; i < d_.s; ++i)
+    if (stage_rank[i] < 0 || stage_rank[i] >= P) raise(1, "stage placed on a pipeline rank outside the replica");
+  replicas_ = replicas;
+  replica_ = rank / P;
+  // global owner of each stage inside this rank's replica: ranks [replica * P, replica * P + P)
+  stage_rank_.resize(d_.s);
+  for (size_t i = 0; i < d_.s; ++i) stage_rank_[i] = replica_ * P + stage_rank[i];
   rank_ = rank;
   nranks_ = nranks;
   if (nranks > 1) schedule_ = 1;
@@ -248,6 +266,11 @@ void Engine::attach_comm(const void* uid, int nranks, int rank, const int* stage
     std::memcpy(u.b, uid, 128);
     CKF_CUDA(cudaSetDevice(d_.device));
     nccl_check(nccl().CommInitRank(&comm_, nranks, u, rank), "ncclCommInitRank");
+    if (replicas > 1) {
+      // data-parallel group: the same pipeline rank of every replica
+      if (!nccl().CommSplit) raise(7, "ncclCommSplit unavailable (NCCL >= 2.18 needed for replicas)");
+      nccl_check(nccl().CommSplit(comm_, rank % P, replica_, &dp_comm_, nullptr), "ncclCommSplit");
+    }
   }
   // release buffers of stages this rank does not own
   for (size_t i = 0; i < d_.s; ++i) {
@@ -421,9 +444,17 @@ void Engine::run_iteration(const int* orders, int m, const void* x, const void* 
     for (int k = 0; k < m; ++k) impl_->mb_forward(k, ok(k), xk(k), yk(k), mb, true, scal_ + k);
     for (int k = 0; k < m; ++k) impl_->mb_backward(k, ok(k), xk(k), mb);
   }
+  // data parallelism: sum every owned group's gradient over the replicas (each replica ran
+  // its own m microbatches of the global batch), then Adam with 1/(m*R)
+  if (replicas_ > 1) {
+    for (ParamGroup* g : owned_groups())
+      nccl_check(nccl().AllReduce(g->g, g->g, g->n, fp64() ? /*ncclFloat64*/ 8 : /*ncclFloat32*/ 7, /*ncclSum*/ 0,
+                                  dp_comm_, st_),
+                 "ncclAllReduce (data parallel)");
+  }
   // mean loss in microbatch order, then *1/m (model.cpp:299-312, pipeline.cpp:82-83)
   std::vector<double> losses(static_cast<size_t>(m));
-  const double inv = 1.0 / static_cast<double>(m);
+  const double inv = 1.0 / (static_cast<double>(m) * replicas_);
   for (size_t i = 0; i < d_.s; ++i) adam_group(stages_[i], stages_[i].lr, inv, scal_ + 2048 + i);
   adam_group(embed_, edge_lr, inv, scal_ + 3000);
   adam_group(deembed_, edge_lr, inv, scal_ + 3001);
@@ -434,11 +465,11 @@ void Engine::run_iteration(const int* orders, int m, const void* x, const void* 
   kt_collect();
   double total = 0.0;
   for (double l : losses) total += l;
-  total *= inv;
+  total *= inv;  // this replica's share of the global mean loss
   if (nranks_ > 1) {
     // every rank learns every stage's omega (the recovery reads its neighbours') and the loss
     std::vector<double> v(d_.s + 1, 0.0);
-    for (size_t i = 0; i < d_.s; ++i) v[i] = stages_[i].owned ? om[i] : 0.0;
+    for (size_t i = 0; i < d_.s; ++i) v[i] = stages_[i].owned && replica_ == 0 ? om[i] : 0.0;
     v[d_.s] = mine(owner_of_deembed()) ? total : 0.0;
     double* dv = scal_ + 3100;
     CKF_CUDA(cudaMemcpyAsync(dv, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice, st_));

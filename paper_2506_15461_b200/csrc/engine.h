@@ -134,7 +134,10 @@ class Engine {
   int owner_of_embed() const { return owner_of_stage(1); }
   int owner_of_deembed() const { return owner_of_stage(static_cast<int>(d_.s)); }
   bool mine(int owner) const { return owner == rank_; }
-  void attach_comm(const void* uid, int nranks, int rank, const int* stage_rank);
+  // nranks = replicas x P pipeline ranks; rank r is pipeline rank r % P of replica r / P;
+  // stage_rank[s-1] names the pipeline rank (0..P-1) holding stage s in every replica
+  void attach_comm(const void* uid, int nranks, int rank, const int* stage_rank, int replicas = 1);
+  std::vector<ParamGroup*> owned_groups();
   // 0 = sequential (forward+backward per microbatch, one live activation cache);
   // 1 = GPipe (all forwards, then all backwards in microbatch order: the ranks of
   //     a multi-GPU pipeline overlap; per-stage accumulation order is unchanged)
@@ -190,6 +193,8 @@ class Engine {
   double* scal_ = nullptr;
   int rank_ = 0, nranks_ = 1;
   int schedule_ = 0;
+  int replicas_ = 1, replica_ = 0;
+  void* dp_comm_ = nullptr;  // ncclComm_t over the same pipeline rank of every replica
   bool log_hops_ = false;
   std::vector<int> vrank_;
   std::vector<long> hop_log_;

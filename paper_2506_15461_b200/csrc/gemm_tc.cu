@@ -341,17 +341,25 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int c = lane * 4; c < BN; c += 128) {
             const int n = w.nb * BN + c;
             if (n >= p.N) break;
-            float4 acc4 = __ldcg(reinterpret_cast<const float4*>(p.ws + (static_cast<size_t>(w.tile) * BM + rr) * BN + c));
-            for (int sp = 1; sp < p.splits; ++sp) {
-              const float4 v = __ldcg(reinterpret_cast<const float4*>(
-                  p.ws + ((static_cast<size_t>(sp) * p.tiles + w.tile) * BM + rr) * BN + c));
-              acc4.x += v.x;
-              acc4.y += v.y;
-              acc4.z += v.z;
-              acc4.w += v.w;
-            }
+            // all partial loads in flight first (memory-level parallelism), then a fixed-order sum
+            constexpr int kMaxSplits = 16;
+            float4 part[kMaxSplits];
+#pragma unroll
+            for (int sp = 0; sp < kMaxSplits; ++sp)
+              if (sp < p.splits)
+                part[sp] = __ldcg(reinterpret_cast<const float4*>(
+                    p.ws + ((static_cast<size_t>(sp) * p.tiles + w.tile) * BM + rr) * BN + c));
             float4* dst = reinterpret_cast<float4*>(p.C + static_cast<size_t>(m) * p.ldc + n);
             float4 o = *dst;
+            float4 acc4 = part[0];
+#pragma unroll
+            for (int sp = 1; sp < kMaxSplits; ++sp)
+              if (sp < p.splits) {
+                acc4.x += part[sp].x;
+                acc4.y += part[sp].y;
+                acc4.z += part[sp].z;
+                acc4.w += part[sp].w;
+              }
             o.x += acc4.x;
             o.y += acc4.y;
             o.z += acc4.z;

@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(256) rmsnorm_fwd_kernel(const float4* __restri
   }
 }
 
-constexpr int kBwdRowsPerBlock = 64;
+constexpr int kBwdRowsPerBlock = 16;  // 512 CTAs for 8192 rows: enough warps in flight per SM
 
 // dh += rstd*u - x*rstd^3*(u.x)/d with u = g*dy; gain partial += dy*x*rstd.
 // One warp per row, row and gain partials held in registers (lane owns
