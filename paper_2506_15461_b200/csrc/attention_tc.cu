@@ -38,49 +38,63 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-// Forward: 96 KiB of shared memory and 256 TMEM columns per CTA so that two
-// CTAs share an SM (two softmax warpgroups per SM hide the exp / TMEM latency).
+// Forward.  128 queries x 64-key tiles: S double-buffered in TMEM (2 x 64
+// columns) + O (64 columns) = 256 columns and 88 KiB of shared memory per CTA,
+// so two CTAs share an SM; 8 softmax warps per CTA (two per TMEM lane quarter,
+// each owning 32 of the tile's 64 key columns), so 16 softmax warps per SM hide
+// the TMEM-load / exp latency while the MMA warp computes S_{j+1}.
+constexpr int FK = 64;                        // keys per forward tile
+constexpr uint32_t kKTile = FK * HD * 2;      // 8 KiB (64 keys x 64 hd)
+constexpr uint32_t kPTile = TQ * FK * 2;      // 16 KiB: P [128 rows][128 B]
+constexpr int kFwdThreads = 384;
+
 struct Smem {
   uint8_t q[kTile];
-  uint8_t k[2][kTile];
-  uint8_t v[kTile];
-  uint8_t p[kPBuf];
+  uint8_t k[3][kKTile];
+  uint8_t v[2][kKTile];
+  uint8_t p[2][kPTile];
+  float red[2][TQ];  // cross-warp row max / row sum exchange (column halves)
   uint64_t q_full;
-  uint64_t k_full[2], k_empty[2], v_full, v_empty;
-  uint64_t s_full, s_free, p_full, p_free;
+  uint64_t k_full[3], k_empty[3], v_full[2], v_empty[2];
+  uint64_t s_full[2], s_free[2], p_full[2], p_free[2];
   uint64_t o_full;
   uint32_t tmem;
 };
 
-// Pass 1 reduces each row of S to its maximum only; pass 2 accumulates
-// O = sum_j exp(S_j - max) V_j with the true row max (no rescaling ever
-// needed) and the row sum l; the epilogue divides by l.
-__global__ void __launch_bounds__(kThreads, 2)
-    attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, int T, int H, __nv_bfloat16* __restrict__ o,
-                       float* __restrict__ lse, float scale_log2) {
+// Pass 1 reduces each row of S to its maximum; pass 2 accumulates
+// O = sum_j exp(S_j - max) V_j with the true row max (never rescaled) and the
+// row sum l; the epilogue divides by l.
+__global__ void __launch_bounds__(kFwdThreads, 2)
+    attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_kv,
+                       int T, int H, __nv_bfloat16* __restrict__ o, float* __restrict__ lse, float scale_log2) {
   extern __shared__ uint8_t smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = T / TQ;
   const int qb = nqb - 1 - static_cast<int>(blockIdx.x);  // heavy (late) query tiles first
   const int bh = blockIdx.y, b = bh / H, h = bh % H;
-  const int nkb = qb + 1;  // causal: key tiles 0..qb
+  const int nkb = 2 * qb + 2;  // causal: 64-key tiles 0 .. 2qb+1
   const int row0 = b * T;
   const int qcol = h * HD, kcol = (H + h) * HD, vcol = (2 * H + h) * HD;
 
-  if (warp == 0 && lane == 0) tma_prefetch(&tm_qkv);
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tm_qkv);
+    tma_prefetch(&tm_kv);
+  }
   if (warp == 1 && lane == 0) {
     mbar_init(&sm.q_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 3; ++i) {
       mbar_init(&sm.k_full[i], 1);
       mbar_init(&sm.k_empty[i], 1);
     }
-    mbar_init(&sm.v_full, 1);
-    mbar_init(&sm.v_empty, 1);
-    mbar_init(&sm.s_full, 1);
-    mbar_init(&sm.s_free, 4);
-    mbar_init(&sm.p_full, 4);
-    mbar_init(&sm.p_free, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm.v_full[i], 1);
+      mbar_init(&sm.v_empty[i], 1);
+      mbar_init(&sm.s_full[i], 1);
+      mbar_init(&sm.s_free[i], 8);
+      mbar_init(&sm.p_full[i], 8);
+      mbar_init(&sm.p_free[i], 1);
+    }
     mbar_init(&sm.o_full, 1);
     fence_barrier_init();
   }
@@ -88,7 +102,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = sm.tmem;  // S cols 0-127, O 128-191
+  const uint32_t tmem = sm.tmem;  // S[0] cols 0-63, S[1] 64-127, O 128-191
 
   if (warp == 0) {
     if (lane == 0) {
@@ -98,14 +112,15 @@ __global__ void __launch_bounds__(kThreads, 2)
       int c = 0;
       for (int pass = 0; pass < 2; ++pass) {
         for (int j = 0; j < nkb; ++j, ++c) {
-          const int st = c & 1;
-          mbar_wait(&sm.k_empty[st], ((c >> 1) & 1) ^ 1);
-          mbar_arrive_expect_tx(&sm.k_full[st], kTile);
-          tma_load_2d(sm.k[st], &tm_qkv, &sm.k_full[st], kcol, row0 + j * TK);
+          const int st = c % 3;
+          mbar_wait(&sm.k_empty[st], ((c / 3) & 1) ^ 1);
+          mbar_arrive_expect_tx(&sm.k_full[st], kKTile);
+          tma_load_2d(sm.k[st], &tm_kv, &sm.k_full[st], kcol, row0 + j * FK);
           if (pass) {
-            mbar_wait(&sm.v_empty, (j & 1) ^ 1);
-            mbar_arrive_expect_tx(&sm.v_full, kTile);
-            tma_load_2d(sm.v, &tm_qkv, &sm.v_full, vcol, row0 + j * TK);
+            const int vs = j & 1;
+            mbar_wait(&sm.v_empty[vs], ((j >> 1) & 1) ^ 1);
+            mbar_arrive_expect_tx(&sm.v_full[vs], kKTile);
+            tma_load_2d(sm.v[vs], &tm_kv, &sm.v_full[vs], vcol, row0 + j * FK);
           }
         }
       }
@@ -113,126 +128,135 @@ __global__ void __launch_bounds__(kThreads, 2)
   } else if (warp == 1) {
     if (lane == 0) {
       // ---------------- MMA issuer
-      constexpr uint32_t kIdS = idesc_bf16_f32(TQ, TK, false, false);  // S = Q K^T
-      constexpr uint32_t kIdO = idesc_bf16_f32(TQ, HD, false, true);   // O += P V (V MN-major)
+      constexpr uint32_t kIdS = idesc_bf16_f32(TQ, FK, false, false);  // S = Q K^T  (128 x 64)
+      constexpr uint32_t kIdO = idesc_bf16_f32(TQ, HD, false, true);   // O += P V   (V MN-major)
       mbar_wait(&sm.q_full, 0);
-      const uint32_t qa = smem_u32(sm.q), va = smem_u32(sm.v), pa = smem_u32(sm.p);
+      const uint32_t qa = smem_u32(sm.q);
+      auto issue_s = [&](int cc, int j) {
+        const int st = cc % 3, sb = cc & 1;
+        mbar_wait(&sm.k_full[st], (cc / 3) & 1);
+        mbar_wait(&sm.s_free[sb], ((cc >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t ka = smem_u32(sm.k[st]);
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k)
+          umma_bf16(tmem + sb * FK, umma_desc_sw128(qa + k * 32, 16, 1024), umma_desc_sw128(ka + k * 32, 16, 1024),
+                    kIdS, k > 0 ? 1u : 0u);
+        umma_commit(&sm.s_full[sb]);
+        umma_commit(&sm.k_empty[st]);
+        (void)j;
+      };
       int c = 0;
-      for (int pass = 0; pass < 2; ++pass) {
-        for (int j = 0; j < nkb; ++j, ++c) {
-          const int st = c & 1;
-          mbar_wait(&sm.k_full[st], (c >> 1) & 1);
-          mbar_wait(&sm.s_free, (c & 1) ^ 1);
-          tc_fence_after();
-          const uint32_t ka = smem_u32(sm.k[st]);
+      for (int j = 0; j < nkb; ++j, ++c) issue_s(c, j);  // pass 1
+      const int c0 = c;
+      issue_s(c0, 0);
+      for (int j = 0; j < nkb; ++j) {  // pass 2: S_{j+1} overlaps softmax(j)
+        if (j + 1 < nkb) issue_s(c0 + j + 1, j + 1);
+        const int pb = j & 1;
+        mbar_wait(&sm.v_full[pb], (j >> 1) & 1);
+        mbar_wait(&sm.p_full[pb], (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t pa = smem_u32(sm.p[pb]), va = smem_u32(sm.v[pb]);
 #pragma unroll
-          for (int k = 0; k < HD / 16; ++k)
-            umma_bf16(tmem, umma_desc_sw128(qa + k * 32, 16, 1024), umma_desc_sw128(ka + k * 32, 16, 1024), kIdS,
-                      k > 0 ? 1u : 0u);
-          umma_commit(&sm.s_full);
-          umma_commit(&sm.k_empty[st]);
-          if (pass) {
-            mbar_wait(&sm.v_full, j & 1);
-            mbar_wait(&sm.p_full, j & 1);
-            tc_fence_after();
-#pragma unroll
-            for (int k = 0; k < TK / 16; ++k)
-              umma_bf16(tmem + 128, umma_desc_sw128(pa + (k >> 2) * (TQ * 128) + (k & 3) * 32, 16, 1024),
-                        umma_desc_sw128(va + k * 2048, 8192, 1024), kIdO, (j > 0 || k > 0) ? 1u : 0u);
-            umma_commit(&sm.p_free);
-            umma_commit(&sm.v_empty);
-          }
-        }
+        for (int k = 0; k < FK / 16; ++k)
+          umma_bf16(tmem + 128, umma_desc_sw128(pa + k * 32, 16, 1024), umma_desc_sw128(va + k * 2048, 8192, 1024),
+                    kIdO, (j > 0 || k > 0) ? 1u : 0u);
+        umma_commit(&sm.p_free[pb]);
+        umma_commit(&sm.v_empty[pb]);
       }
       umma_commit(&sm.o_full);
     }
   } else if (warp >= 4) {
-    // ---------------- softmax: one query row per thread
-    const int r = (warp - 4) * 32 + lane;
+    // ---------------- softmax: thread = (query row, 32-column half of the key tile)
+    const int sw = warp - 4, quarter = sw & 3, half = sw >> 2;
+    const int r = quarter * 32 + lane;
     const int q = qb * TQ + r;
-    const uint32_t trow = tmem + (static_cast<uint32_t>((warp - 4) * 32) << 16);
+    const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + half * 32;
     int c = 0;
     float mraw = -INFINITY;
     for (int j = 0; j < nkb; ++j, ++c) {  // pass 1: row max of the raw scores
-      mbar_wait(&sm.s_full, c & 1);
+      const int sb = c & 1;
+      mbar_wait(&sm.s_full[sb], (c >> 1) & 1);
       tc_fence_after();
-      const bool diag = j == qb;
-#pragma unroll
-      for (int k4 = 0; k4 < TK / 32; ++k4) {
-        uint32_t u[32];
-        tmem_ld32(trow + k4 * 32, u);
-        tmem_ld_wait();
-#pragma unroll
-        for (int t = 0; t < 32; ++t) {
-          const float x = __uint_as_float(u[t]);
-          if (!diag || k4 * 32 + t <= r) mraw = fmaxf(mraw, x);
-        }
-      }
+      uint32_t u[32];
+      tmem_ld32(trow + sb * FK, u);
+      tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.s_free);
+      if (lane == 0) mbar_arrive(&sm.s_free[sb]);
+      const int kbase = j * FK + half * 32;  // key index of u[0]
+      if (kbase + 31 <= q) {
+#pragma unroll
+        for (int t = 0; t < 32; ++t) mraw = fmaxf(mraw, __uint_as_float(u[t]));
+      } else {
+#pragma unroll
+        for (int t = 0; t < 32; ++t)
+          if (kbase + t <= q) mraw = fmaxf(mraw, __uint_as_float(u[t]));
+      }
     }
+    // combine the two column halves' maxima of each row
+    sm.red[half][r] = mraw;
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    mraw = fmaxf(sm.red[0][r], sm.red[1][r]);
+    asm volatile("bar.sync 1, 256;" ::: "memory");
     const float m2 = mraw * scale_log2;
     float l = 0.f;
-    const uint32_t pbase = smem_u32(sm.p) + r * 128;
     for (int j = 0; j < nkb; ++j, ++c) {  // pass 2: P = exp(S - max), l += rowsum(P)
-      mbar_wait(&sm.s_full, c & 1);
+      const int sb = c & 1, pb = j & 1;
+      mbar_wait(&sm.s_full[sb], (c >> 1) & 1);
       tc_fence_after();
-      mbar_wait(&sm.p_free, (j & 1) ^ 1);
-      const bool diag = j == qb;
-#pragma unroll
-      for (int k4 = 0; k4 < TK / 32; ++k4) {
-        uint32_t u[32];
-        tmem_ld32(trow + k4 * 32, u);
-        tmem_ld_wait();
-        uint32_t w[16];
-#pragma unroll
-        for (int t = 0; t < 32; t += 2) {
-          float p0 = ex2(__uint_as_float(u[t]) * scale_log2 - m2);
-          float p1 = ex2(__uint_as_float(u[t + 1]) * scale_log2 - m2);
-          if (diag) {
-            if (k4 * 32 + t > r) p0 = 0.f;
-            if (k4 * 32 + t + 1 > r) p1 = 0.f;
-          }
-          l += p0 + p1;
-          w[t / 2] = pack_bf16(p0, p1);
-        }
-        const int ch = k4 >> 1, piece0 = (k4 & 1) * 4;
-#pragma unroll
-        for (int pc = 0; pc < 4; ++pc)
-          st_shared_v4(pbase + ch * (TQ * 128) + (((piece0 + pc) ^ (r & 7)) << 4), w[4 * pc], w[4 * pc + 1],
-                       w[4 * pc + 2], w[4 * pc + 3]);
-      }
+      uint32_t u[32];
+      tmem_ld32(trow + sb * FK, u);
+      tmem_ld_wait();
       tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.s_free[sb]);
+      const int kbase = j * FK + half * 32;
+      const bool full = kbase + 31 <= q;
+      uint32_t w[16];
+#pragma unroll
+      for (int t = 0; t < 32; t += 2) {
+        float p0 = ex2(__uint_as_float(u[t]) * scale_log2 - m2);
+        float p1 = ex2(__uint_as_float(u[t + 1]) * scale_log2 - m2);
+        if (!full) {
+          if (kbase + t > q) p0 = 0.f;
+          if (kbase + t + 1 > q) p1 = 0.f;
+        }
+        l += p0 + p1;
+        w[t / 2] = pack_bf16(p0, p1);
+      }
+      mbar_wait(&sm.p_free[pb], ((j >> 1) & 1) ^ 1);
+      const uint32_t prow = smem_u32(sm.p[pb]) + r * 128;
+#pragma unroll
+      for (int pc = 0; pc < 4; ++pc)
+        st_shared_v4(prow + (((half * 4 + pc) ^ (r & 7)) << 4), w[4 * pc], w[4 * pc + 1], w[4 * pc + 2],
+                     w[4 * pc + 3]);
       fence_proxy_async();
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&sm.s_free);
-        mbar_arrive(&sm.p_full);
-      }
+      if (lane == 0) mbar_arrive(&sm.p_full[pb]);
     }
-    // ---------------- epilogue: O / l -> bf16, lse
+    sm.red[half][r] = l;
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    l = sm.red[0][r] + sm.red[1][r];
+    // ---------------- epilogue: O / l -> bf16 (each half writes 32 of the 64 head columns), lse
     mbar_wait(&sm.o_full, 0);
     tc_fence_after();
     const float inv = 1.f / l;
     const size_t ldo = static_cast<size_t>(H) * HD;
-    __nv_bfloat16* orow = o + (static_cast<size_t>(row0) + q) * ldo + static_cast<size_t>(h) * HD;
+    __nv_bfloat16* orow = o + (static_cast<size_t>(row0) + q) * ldo + static_cast<size_t>(h) * HD + half * 32;
+    uint32_t u[32];
+    tmem_ld32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + 128 + half * 32, u);
+    tmem_ld_wait();
 #pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      uint32_t u[32];
-      tmem_ld32(trow + 128 + half * 32, u);
-      tmem_ld_wait();
-#pragma unroll
-      for (int piece = 0; piece < 4; ++piece) {
-        uint4 v;
-        v.x = pack_bf16(__uint_as_float(u[8 * piece + 0]) * inv, __uint_as_float(u[8 * piece + 1]) * inv);
-        v.y = pack_bf16(__uint_as_float(u[8 * piece + 2]) * inv, __uint_as_float(u[8 * piece + 3]) * inv);
-        v.z = pack_bf16(__uint_as_float(u[8 * piece + 4]) * inv, __uint_as_float(u[8 * piece + 5]) * inv);
-        v.w = pack_bf16(__uint_as_float(u[8 * piece + 6]) * inv, __uint_as_float(u[8 * piece + 7]) * inv);
-        reinterpret_cast<uint4*>(orow + half * 32)[piece] = v;
-      }
+    for (int piece = 0; piece < 4; ++piece) {
+      uint4 v;
+      v.x = pack_bf16(__uint_as_float(u[8 * piece + 0]) * inv, __uint_as_float(u[8 * piece + 1]) * inv);
+      v.y = pack_bf16(__uint_as_float(u[8 * piece + 2]) * inv, __uint_as_float(u[8 * piece + 3]) * inv);
+      v.z = pack_bf16(__uint_as_float(u[8 * piece + 4]) * inv, __uint_as_float(u[8 * piece + 5]) * inv);
+      v.w = pack_bf16(__uint_as_float(u[8 * piece + 6]) * inv, __uint_as_float(u[8 * piece + 7]) * inv);
+      reinterpret_cast<uint4*>(orow)[piece] = v;
     }
-    lse[static_cast<size_t>(bh) * T + q] = (m2 + log2f(l)) * kLn2;
+    if (half == 0) lse[static_cast<size_t>(bh) * T + q] = (m2 + log2f(l)) * kLn2;
   }
   tc_fence_before();
   __syncthreads();
@@ -598,6 +622,7 @@ bool attn_fwd_tc_supported(size_t T, size_t hd) { return hd == HD && T % TQ == 0
 void attn_fwd_tc(const bf16* qkv, size_t B, size_t T, size_t H, size_t hd, bf16* o, float* lse, cudaStream_t s) {
   if (!attn_fwd_tc_supported(T, hd)) raise(1, "tcgen05 attention: head_dim 64 and seq_len % 128 == 0");
   const CUtensorMap tm = tma::make_2d_bf16(qkv, 3 * H * hd, B * T, 3 * H * hd, 64, 128);
+  const CUtensorMap tkv = tma::make_2d_bf16(qkv, 3 * H * hd, B * T, 3 * H * hd, 64, FK);
   const size_t smem = sizeof(Smem) + 1024;
   static bool attr = false;
   if (!attr) {
@@ -607,7 +632,8 @@ void attn_fwd_tc(const bf16* qkv, size_t B, size_t T, size_t H, size_t hd, bf16*
   }
   const float scale_log2 = kLog2e / sqrtf(static_cast<float>(hd));
   dim3 grid(static_cast<unsigned>(T / TQ), static_cast<unsigned>(B * H));
-  attn_fwd_tc_kernel<<<grid, kThreads, smem, s>>>(tm, static_cast<int>(T), static_cast<int>(H), o, lse, scale_log2);
+  attn_fwd_tc_kernel<<<grid, kFwdThreads, smem, s>>>(tm, tkv, static_cast<int>(T), static_cast<int>(H), o, lse,
+                                                     scale_log2);
   CKF_LAUNCH_CHECK();
 }
 

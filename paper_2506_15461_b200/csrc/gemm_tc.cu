@@ -19,6 +19,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -181,6 +182,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Programmatic dependent launch: the set-up above overlaps the previous kernel's tail;
+  // nothing global is read or written before the previous grid has fully completed.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp == 0) {
     if (lane == 0) {
@@ -465,7 +470,17 @@ void launch_t(const GemmDesc& g, int splits, cudaStream_t s) {
     attr_set = true;
   }
   const int grid = std::min(p.units, num_sms());
-  kern<<<grid, kThreads, C::kSmem, s>>>(ta, tb, tcm, twm, p);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = C::kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CKF_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, tcm, twm, p));
   CKF_LAUNCH_CHECK();
 }
 
@@ -500,16 +515,31 @@ void gemm_bf16(const GemmDesc& g, cudaStream_t s) {
   if (g.ldc % 4 != 0 && g.epi != kStoreBF16) raise(1, "gemm_bf16: fp32 C needs ldc % 4 == 0");
   if (reinterpret_cast<uintptr_t>(g.C) % 16) raise(1, "gemm_bf16: C must be 16-byte aligned");
   if (g.ldc % 8 != 0 && g.epi == kStoreBF16) raise(1, "gemm_bf16: bf16 C needs ldc % 8 == 0");
-  const int bn = g.bn ? g.bn : pick_bn(g.M, g.N);
-  // split-K (ordered, deterministic) for the fp32-accumulate epilogue when the tile grid underfills the SMs
+  int bn = g.bn ? g.bn : pick_bn(g.M, g.N);
+  // Split-K (deterministic workspace reduction) only for the fp32-accumulate (weight-gradient)
+  // epilogue, and only when no tile width fills the GPU: measured on B200
+  // (profiles/r01_gemm_splitk_sweep.jsonl), a >= ~100-tile grid beats any split.
   int splits = g.splits;
+  static const int env_splits = [] {  // tuning override (tools/gemm_splits.py), 0 = heuristic
+    const char* v = std::getenv("CKF_GEMM_SPLITS");
+    return v ? std::atoi(v) : 0;
+  }();
+  if (splits <= 0 && env_splits > 0) splits = env_splits;
   if (splits <= 0) {
     splits = 1;
     if (g.epi == kAccF32) {
-      const int tiles = ((g.M + BM - 1) / BM) * ((g.N + bn - 1) / bn);
-      const int nk = (g.K + BK - 1) / BK;
       const int sms = num_sms();
-      if (tiles * 2 <= sms) splits = std::max(1, std::min({sms / tiles, nk / 4, 16}));
+      const int nm = (g.M + BM - 1) / BM;
+      const int t256 = nm * ((g.N + 255) / 256), t128 = nm * ((g.N + 127) / 128);
+      const int nk = (g.K + BK - 1) / BK;
+      if (!g.bn && t256 * 3 >= sms * 2) {
+        bn = 256;
+      } else if (!g.bn && t128 * 3 >= sms * 2) {
+        bn = 128;
+      } else {
+        const int tiles = nm * ((g.N + bn - 1) / bn);
+        if (tiles * 2 <= sms) splits = std::max(1, std::min({sms / tiles, nk / 4, 16}));
+      }
     }
   }
   if (splits > 1 && g.epi != kAccF32) raise(1, "gemm_bf16: split-K needs the fp32 accumulate epilogue");
