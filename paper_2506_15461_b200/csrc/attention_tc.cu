@@ -15,6 +15,8 @@
 //
 // Warp roles (256 threads): 0 TMA producer, 1 MMA issuer (one lane),
 // 2 TMEM allocator, 4..7 softmax / epilogue (query row = 32 (w-4) + lane).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "llama_kernels.h"
 #include "sm100.cuh"
@@ -38,36 +40,40 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-// Forward.  128 queries x 64-key tiles: S double-buffered in TMEM (2 x 64
-// columns) + O (64 columns) = 256 columns and 88 KiB of shared memory per CTA,
-// so two CTAs share an SM; 8 softmax warps per CTA (two per TMEM lane quarter,
-// each owning 32 of the tile's 64 key columns), so 16 softmax warps per SM hide
-// the TMEM-load / exp latency while the MMA warp computes S_{j+1}.
+// Forward (single pass, FA4-style lazy rescaling).  128 queries x 64-key tiles:
+// S double-buffered in TMEM (2 x 64 columns) + O (64 columns) = 256 columns and
+// 104 KiB of shared memory per CTA -> two CTAs per SM.  Each softmax thread owns
+// one query row: running max m (log2 domain) and sum l; P = exp2(S*scale - m)
+// is written to swizzled smem for O += P V.  m is only raised when a tile's max
+// exceeds it by more than kRescale (P stays <= 2^kRescale, exact in bf16 range);
+// then the thread rescales its O row in TMEM (tcgen05.ld/st) after the previous
+// P V has completed.  K and V are each loaded once.
 constexpr int FK = 64;                        // keys per forward tile
 constexpr uint32_t kKTile = FK * HD * 2;      // 8 KiB (64 keys x 64 hd)
 constexpr uint32_t kPTile = TQ * FK * 2;      // 16 KiB: P [128 rows][128 B]
-constexpr int kFwdThreads = 384;
+constexpr int kKStages = 4, kVStages = 3;
+constexpr float kRescale = 8.f;
 
 struct Smem {
   uint8_t q[kTile];
-  uint8_t k[3][kKTile];
-  uint8_t v[2][kKTile];
+  uint8_t k[kKStages][kKTile];
+  uint8_t v[kVStages][kKTile];
   uint8_t p[2][kPTile];
-  float red[2][TQ];  // cross-warp row max / row sum exchange (column halves)
   uint64_t q_full;
-  uint64_t k_full[3], k_empty[3], v_full[2], v_empty[2];
+  uint64_t k_full[kKStages], k_empty[kKStages], v_full[kVStages], v_empty[kVStages];
   uint64_t s_full[2], s_free[2], p_full[2], p_free[2];
   uint64_t o_full;
   uint32_t tmem;
 };
 
-// Pass 1 reduces each row of S to its maximum; pass 2 accumulates
-// O = sum_j exp(S_j - max) V_j with the true row max (never rescaled) and the
-// row sum l; the epilogue divides by l.
-__global__ void __launch_bounds__(kFwdThreads, 2)
+__device__ __forceinline__ void tmem_st32_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+__global__ void __launch_bounds__(kThreads, 2)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_kv,
-                       int T, int H, __nv_bfloat16* __restrict__ o, float* __restrict__ lse, float scale_log2) {
+                       int T, int H, __nv_bfloat16* __restrict__ o, float* __restrict__ lse, float scale_log2,
+                       long long* __restrict__ dbg) {
   extern __shared__ uint8_t smem_raw[];
+  const long long t_start = clock64();
   Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = T / TQ;
@@ -83,16 +89,18 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
   }
   if (warp == 1 && lane == 0) {
     mbar_init(&sm.q_full, 1);
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < kKStages; ++i) {
       mbar_init(&sm.k_full[i], 1);
       mbar_init(&sm.k_empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kVStages; ++i) {
       mbar_init(&sm.v_full[i], 1);
       mbar_init(&sm.v_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&sm.s_full[i], 1);
-      mbar_init(&sm.s_free[i], 8);
-      mbar_init(&sm.p_full[i], 8);
+      mbar_init(&sm.s_free[i], 4);
+      mbar_init(&sm.p_full[i], 4);
       mbar_init(&sm.p_free[i], 1);
     }
     mbar_init(&sm.o_full, 1);
@@ -106,157 +114,180 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
 
   if (warp == 0) {
     if (lane == 0) {
-      // ---------------- TMA producer: Q once; K per tile in both passes, V per tile in pass 2
+      // ---------------- TMA producer: Q once, then K_j and V_j (each exactly once)
       mbar_arrive_expect_tx(&sm.q_full, kTile);
       tma_load_2d(sm.q, &tm_qkv, &sm.q_full, qcol, row0 + qb * TQ);
-      int c = 0;
-      for (int pass = 0; pass < 2; ++pass) {
-        for (int j = 0; j < nkb; ++j, ++c) {
-          const int st = c % 3;
-          mbar_wait(&sm.k_empty[st], ((c / 3) & 1) ^ 1);
-          mbar_arrive_expect_tx(&sm.k_full[st], kKTile);
-          tma_load_2d(sm.k[st], &tm_kv, &sm.k_full[st], kcol, row0 + j * FK);
-          if (pass) {
-            const int vs = j & 1;
-            mbar_wait(&sm.v_empty[vs], ((j >> 1) & 1) ^ 1);
-            mbar_arrive_expect_tx(&sm.v_full[vs], kKTile);
-            tma_load_2d(sm.v[vs], &tm_kv, &sm.v_full[vs], vcol, row0 + j * FK);
-          }
-        }
+      for (int j = 0; j < nkb; ++j) {
+        const int ks = j % kKStages, vs = j % kVStages;
+        mbar_wait(&sm.k_empty[ks], ((j / kKStages) & 1) ^ 1);
+        mbar_arrive_expect_tx(&sm.k_full[ks], kKTile);
+        tma_load_2d(sm.k[ks], &tm_kv, &sm.k_full[ks], kcol, row0 + j * FK);
+        mbar_wait(&sm.v_empty[vs], ((j / kVStages) & 1) ^ 1);
+        mbar_arrive_expect_tx(&sm.v_full[vs], kKTile);
+        tma_load_2d(sm.v[vs], &tm_kv, &sm.v_full[vs], vcol, row0 + j * FK);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      // ---------------- MMA issuer
+      // ---------------- MMA issuer: S_{j+1} is issued before P_j is awaited
       constexpr uint32_t kIdS = idesc_bf16_f32(TQ, FK, false, false);  // S = Q K^T  (128 x 64)
       constexpr uint32_t kIdO = idesc_bf16_f32(TQ, HD, false, true);   // O += P V   (V MN-major)
       mbar_wait(&sm.q_full, 0);
       const uint32_t qa = smem_u32(sm.q);
-      auto issue_s = [&](int cc, int j) {
-        const int st = cc % 3, sb = cc & 1;
-        mbar_wait(&sm.k_full[st], (cc / 3) & 1);
-        mbar_wait(&sm.s_free[sb], ((cc >> 1) & 1) ^ 1);
+      auto issue_s = [&](int j) {
+        const int ks = j % kKStages, sb = j & 1;
+        mbar_wait(&sm.k_full[ks], (j / kKStages) & 1);
+        mbar_wait(&sm.s_free[sb], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t ka = smem_u32(sm.k[st]);
+        const uint32_t ka = smem_u32(sm.k[ks]);
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k)
           umma_bf16(tmem + sb * FK, umma_desc_sw128(qa + k * 32, 16, 1024), umma_desc_sw128(ka + k * 32, 16, 1024),
                     kIdS, k > 0 ? 1u : 0u);
         umma_commit(&sm.s_full[sb]);
-        umma_commit(&sm.k_empty[st]);
-        (void)j;
+        umma_commit(&sm.k_empty[ks]);
       };
-      int c = 0;
-      for (int j = 0; j < nkb; ++j, ++c) issue_s(c, j);  // pass 1
-      const int c0 = c;
-      issue_s(c0, 0);
-      for (int j = 0; j < nkb; ++j) {  // pass 2: S_{j+1} overlaps softmax(j)
-        if (j + 1 < nkb) issue_s(c0 + j + 1, j + 1);
-        const int pb = j & 1;
-        mbar_wait(&sm.v_full[pb], (j >> 1) & 1);
+      issue_s(0);
+      for (int j = 0; j < nkb; ++j) {
+        if (j + 1 < nkb) issue_s(j + 1);
+        const int pb = j & 1, vs = j % kVStages;
+        mbar_wait(&sm.v_full[vs], (j / kVStages) & 1);
         mbar_wait(&sm.p_full[pb], (j >> 1) & 1);
         tc_fence_after();
-        const uint32_t pa = smem_u32(sm.p[pb]), va = smem_u32(sm.v[pb]);
+        const uint32_t pa = smem_u32(sm.p[pb]), va = smem_u32(sm.v[vs]);
 #pragma unroll
         for (int k = 0; k < FK / 16; ++k)
           umma_bf16(tmem + 128, umma_desc_sw128(pa + k * 32, 16, 1024), umma_desc_sw128(va + k * 2048, 8192, 1024),
                     kIdO, (j > 0 || k > 0) ? 1u : 0u);
         umma_commit(&sm.p_free[pb]);
-        umma_commit(&sm.v_empty[pb]);
+        umma_commit(&sm.v_empty[vs]);
       }
       umma_commit(&sm.o_full);
     }
   } else if (warp >= 4) {
-    // ---------------- softmax: thread = (query row, 32-column half of the key tile)
-    const int sw = warp - 4, quarter = sw & 3, half = sw >> 2;
-    const int r = quarter * 32 + lane;
+    // ---------------- softmax: one query row per thread, online with lazy rescaling
+    const int r = (warp - 4) * 32 + lane;
     const int q = qb * TQ + r;
-    const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + half * 32;
-    int c = 0;
-    float mraw = -INFINITY;
-    for (int j = 0; j < nkb; ++j, ++c) {  // pass 1: row max of the raw scores
-      const int sb = c & 1;
-      mbar_wait(&sm.s_full[sb], (c >> 1) & 1);
+    const uint32_t trow = tmem + (static_cast<uint32_t>((warp - 4) * 32) << 16);
+    float m = -INFINITY, l = 0.f;  // m: running max of S * scale_log2
+    long long w_s = 0, w_p = 0, t_first = 0;
+    for (int j = 0; j < nkb; ++j) {
+      const int sb = j & 1, pb = j & 1;
+      const long long t0 = clock64();
+      mbar_wait(&sm.s_full[sb], (j >> 1) & 1);
+      const long long t1 = clock64();
+      if (j == 0) t_first = t1 - t_start;
+      w_s += t1 - t0;
       tc_fence_after();
-      uint32_t u[32];
-      tmem_ld32(trow + sb * FK, u);
+      uint32_t u[64];
+      tmem_ld32(trow + sb * FK, *reinterpret_cast<uint32_t(*)[32]>(&u[0]));
+      tmem_ld32(trow + sb * FK + 32, *reinterpret_cast<uint32_t(*)[32]>(&u[32]));
       tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.s_free[sb]);
-      const int kbase = j * FK + half * 32;  // key index of u[0]
-      if (kbase + 31 <= q) {
+      const int kbase = j * FK;
+      const int nvalid = min(FK, q - kbase + 1);  // keys <= q are visible (causal)
+      // row max of the visible scores: 8 independent chains (no 64-deep FMNMX dependency)
+      float mx8[8];
 #pragma unroll
-        for (int t = 0; t < 32; ++t) mraw = fmaxf(mraw, __uint_as_float(u[t]));
+      for (int i = 0; i < 8; ++i) mx8[i] = -INFINITY;
+      if (nvalid >= FK) {
+#pragma unroll
+        for (int t = 0; t < FK; ++t) mx8[t & 7] = fmaxf(mx8[t & 7], __uint_as_float(u[t]));
       } else {
 #pragma unroll
-        for (int t = 0; t < 32; ++t)
-          if (kbase + t <= q) mraw = fmaxf(mraw, __uint_as_float(u[t]));
+        for (int t = 0; t < FK; ++t)
+          if (t < nvalid) mx8[t & 7] = fmaxf(mx8[t & 7], __uint_as_float(u[t]));
       }
-    }
-    // combine the two column halves' maxima of each row
-    sm.red[half][r] = mraw;
-    asm volatile("bar.sync 1, 256;" ::: "memory");
-    mraw = fmaxf(sm.red[0][r], sm.red[1][r]);
-    asm volatile("bar.sync 1, 256;" ::: "memory");
-    const float m2 = mraw * scale_log2;
-    float l = 0.f;
-    for (int j = 0; j < nkb; ++j, ++c) {  // pass 2: P = exp(S - max), l += rowsum(P)
-      const int sb = c & 1, pb = j & 1;
-      mbar_wait(&sm.s_full[sb], (c >> 1) & 1);
-      tc_fence_after();
-      uint32_t u[32];
-      tmem_ld32(trow + sb * FK, u);
-      tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.s_free[sb]);
-      const int kbase = j * FK + half * 32;
-      const bool full = kbase + 31 <= q;
-      uint32_t w[16];
+      const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * scale_log2;
+      // lazy rescale: only when this tile's max exceeds the running max by > kRescale
+      const bool need = mx > m + kRescale;
+      const float mn = need ? mx : m;
+      const float alpha = need ? ex2(m - mn) : 1.f;  // m = -inf on the first tile -> 0
+      if (__any_sync(0xffffffffu, need) && j > 0) {
+        // the previous P V must have landed before this warp rewrites its O rows
+        mbar_wait(&sm.p_free[(j - 1) & 1], ((j - 1) >> 1) & 1);
+        tc_fence_after();
 #pragma unroll
-      for (int t = 0; t < 32; t += 2) {
-        float p0 = ex2(__uint_as_float(u[t]) * scale_log2 - m2);
-        float p1 = ex2(__uint_as_float(u[t + 1]) * scale_log2 - m2);
-        if (!full) {
-          if (kbase + t > q) p0 = 0.f;
-          if (kbase + t + 1 > q) p1 = 0.f;
+        for (int hf = 0; hf < 2; ++hf) {
+          uint32_t ov[32];
+          tmem_ld32(trow + 128 + hf * 32, ov);
+          tmem_ld_wait();
+#pragma unroll
+          for (int t = 0; t < 32; ++t) ov[t] = __float_as_uint(__uint_as_float(ov[t]) * alpha);
+          tmem_st32(trow + 128 + hf * 32, ov);
         }
-        l += p0 + p1;
-        w[t / 2] = pack_bf16(p0, p1);
+        tmem_st32_wait();
       }
-      mbar_wait(&sm.p_free[pb], ((j >> 1) & 1) ^ 1);
+      l *= alpha;
+      m = mn;
+      const long long t2 = clock64();
+      mbar_wait(&sm.p_free[pb], ((j >> 1) & 1) ^ 1);  // P V_{j-2} has read this P buffer
+      w_p += clock64() - t2;
       const uint32_t prow = smem_u32(sm.p[pb]) + r * 128;
 #pragma unroll
-      for (int pc = 0; pc < 4; ++pc)
-        st_shared_v4(prow + (((half * 4 + pc) ^ (r & 7)) << 4), w[4 * pc], w[4 * pc + 1], w[4 * pc + 2],
-                     w[4 * pc + 3]);
+      for (int hf = 0; hf < 2; ++hf) {  // 32 keys at a time: P -> bf16 -> swizzled smem
+        uint32_t w[16];
+        float l4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int t = 0; t < 32; t += 2) {
+          const int tt = hf * 32 + t;
+          float p0 = ex2(fmaf(__uint_as_float(u[tt]), scale_log2, -m));
+          float p1 = ex2(fmaf(__uint_as_float(u[tt + 1]), scale_log2, -m));
+          if (nvalid < FK) {
+            p0 = tt < nvalid ? p0 : 0.f;
+            p1 = tt + 1 < nvalid ? p1 : 0.f;
+          }
+          l4[(t >> 1) & 3] += p0 + p1;
+          w[t / 2] = pack_bf16(p0, p1);
+        }
+        l += (l4[0] + l4[1]) + (l4[2] + l4[3]);
+#pragma unroll
+        for (int pc = 0; pc < 4; ++pc)
+          st_shared_v4(prow + (((hf * 4 + pc) ^ (r & 7)) << 4), w[4 * pc], w[4 * pc + 1], w[4 * pc + 2],
+                       w[4 * pc + 3]);
+      }
       fence_proxy_async();
+      tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.p_full[pb]);
     }
-    sm.red[half][r] = l;
-    asm volatile("bar.sync 1, 256;" ::: "memory");
-    l = sm.red[0][r] + sm.red[1][r];
-    // ---------------- epilogue: O / l -> bf16 (each half writes 32 of the 64 head columns), lse
+    // ---------------- epilogue: O / l -> bf16, lse
     mbar_wait(&sm.o_full, 0);
     tc_fence_after();
     const float inv = 1.f / l;
     const size_t ldo = static_cast<size_t>(H) * HD;
-    __nv_bfloat16* orow = o + (static_cast<size_t>(row0) + q) * ldo + static_cast<size_t>(h) * HD + half * 32;
-    uint32_t u[32];
-    tmem_ld32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + 128 + half * 32, u);
-    tmem_ld_wait();
+    __nv_bfloat16* orow = o + (static_cast<size_t>(row0) + q) * ldo + static_cast<size_t>(h) * HD;
 #pragma unroll
-    for (int piece = 0; piece < 4; ++piece) {
-      uint4 v;
-      v.x = pack_bf16(__uint_as_float(u[8 * piece + 0]) * inv, __uint_as_float(u[8 * piece + 1]) * inv);
-      v.y = pack_bf16(__uint_as_float(u[8 * piece + 2]) * inv, __uint_as_float(u[8 * piece + 3]) * inv);
-      v.z = pack_bf16(__uint_as_float(u[8 * piece + 4]) * inv, __uint_as_float(u[8 * piece + 5]) * inv);
-      v.w = pack_bf16(__uint_as_float(u[8 * piece + 6]) * inv, __uint_as_float(u[8 * piece + 7]) * inv);
-      reinterpret_cast<uint4*>(orow)[piece] = v;
+    for (int hf = 0; hf < 2; ++hf) {
+      uint32_t u[32];
+      tmem_ld32(trow + 128 + hf * 32, u);
+      tmem_ld_wait();
+#pragma unroll
+      for (int piece = 0; piece < 4; ++piece) {
+        uint4 v;
+        v.x = pack_bf16(__uint_as_float(u[8 * piece + 0]) * inv, __uint_as_float(u[8 * piece + 1]) * inv);
+        v.y = pack_bf16(__uint_as_float(u[8 * piece + 2]) * inv, __uint_as_float(u[8 * piece + 3]) * inv);
+        v.z = pack_bf16(__uint_as_float(u[8 * piece + 4]) * inv, __uint_as_float(u[8 * piece + 5]) * inv);
+        v.w = pack_bf16(__uint_as_float(u[8 * piece + 6]) * inv, __uint_as_float(u[8 * piece + 7]) * inv);
+        reinterpret_cast<uint4*>(orow + hf * 32)[piece] = v;
+      }
     }
-    if (half == 0) lse[static_cast<size_t>(bh) * T + q] = (m2 + log2f(l)) * kLn2;
+    lse[static_cast<size_t>(bh) * T + q] = (m + log2f(l)) * kLn2;
+    if (dbg && threadIdx.x == 128) {
+      long long* d = dbg + 8 * (blockIdx.y * gridDim.x + blockIdx.x);
+      d[0] = nkb;
+      d[1] = t_first;
+      d[2] = w_s;
+      d[3] = w_p;
+      d[4] = clock64() - t_start;
+      unsigned smid;
+      asm("mov.u32 %0, %%smid;" : "=r"(smid));
+      d[5] = smid;
+      d[6] = t_start;
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -417,13 +448,24 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
         tmem_ld32(trow + 128 + c0, ud);
         tmem_ld_wait();
         float pv[32], dv[32];
+        const float4* l4 = reinterpret_cast<const float4*>(&sm.lse2[st][c0]);
+        const float4* d4 = reinterpret_cast<const float4*>(&sm.dsum[st][c0]);
 #pragma unroll
-        for (int t = 0; t < 32; ++t) {
-          const int qi = c0 + t;
-          float p = ex2(__uint_as_float(us[t]) * scale_log2 - sm.lse2[st][qi]);
-          if (i == 0 && qi < r) p = 0.f;  // diagonal tile: query before key
-          pv[t] = p;
-          dv[t] = p * (__uint_as_float(ud[t]) - sm.dsum[st][qi]);
+        for (int t4 = 0; t4 < 8; ++t4) {  // 128-bit broadcast reads of the per-query lse / D
+          const float4 lv = l4[t4], dvv = d4[t4];
+          const float la[4] = {lv.x, lv.y, lv.z, lv.w}, da[4] = {dvv.x, dvv.y, dvv.z, dvv.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int t = 4 * t4 + e;
+            const float p = ex2(fmaf(__uint_as_float(us[t]), scale_log2, -la[e]));
+            pv[t] = p;
+            dv[t] = p * (__uint_as_float(ud[t]) - da[e]);
+          }
+        }
+        if (i == 0) {  // diagonal tile: a query before the key sees nothing
+#pragma unroll
+          for (int t = 0; t < 32; ++t)
+            if (c0 + t < r) pv[t] = dv[t] = 0.f;
         }
         put32(pbase, r, c0, pv);
         put32(dbase, r, c0, dv);
@@ -578,9 +620,13 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
         float dv[32];
 #pragma unroll
         for (int t = 0; t < 32; ++t) {
-          float p = ex2(__uint_as_float(us[t]) * scale_log2 - l2);
-          if (j == qb && c0 + t > r) p = 0.f;  // diagonal tile: key after query
+          const float p = ex2(fmaf(__uint_as_float(us[t]), scale_log2, -l2));
           dv[t] = p * (__uint_as_float(ud[t]) - dq);
+        }
+        if (j == qb) {  // diagonal tile: keys after the query are invisible
+#pragma unroll
+          for (int t = 0; t < 32; ++t)
+            if (c0 + t > r) dv[t] = 0.f;
         }
         put32(dbase, r, c0, dv);
       }
@@ -619,6 +665,16 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
 
 bool attn_fwd_tc_supported(size_t T, size_t hd) { return hd == HD && T % TQ == 0; }
 
+// CKF_ATTN_DEBUG=1: per-CTA phase timings of the forward kernel (tools/attn_debug.py)
+long long* attn_fwd_debug_buffer() {
+  static long long* p = [] {
+    long long* b = nullptr;
+    if (std::getenv("CKF_ATTN_DEBUG")) CKF_CUDA(cudaMalloc(&b, 8 * sizeof(long long) * 65536));
+    return b;
+  }();
+  return p;
+}
+
 void attn_fwd_tc(const bf16* qkv, size_t B, size_t T, size_t H, size_t hd, bf16* o, float* lse, cudaStream_t s) {
   if (!attn_fwd_tc_supported(T, hd)) raise(1, "tcgen05 attention: head_dim 64 and seq_len % 128 == 0");
   const CUtensorMap tm = tma::make_2d_bf16(qkv, 3 * H * hd, B * T, 3 * H * hd, 64, 128);
@@ -632,8 +688,9 @@ void attn_fwd_tc(const bf16* qkv, size_t B, size_t T, size_t H, size_t hd, bf16*
   }
   const float scale_log2 = kLog2e / sqrtf(static_cast<float>(hd));
   dim3 grid(static_cast<unsigned>(T / TQ), static_cast<unsigned>(B * H));
-  attn_fwd_tc_kernel<<<grid, kFwdThreads, smem, s>>>(tm, tkv, static_cast<int>(T), static_cast<int>(H), o, lse,
-                                                     scale_log2);
+  long long* dbg = attn_fwd_debug_buffer();
+  attn_fwd_tc_kernel<<<grid, kThreads, smem, s>>>(tm, tkv, static_cast<int>(T), static_cast<int>(H), o, lse,
+                                                  scale_log2, dbg);
   CKF_LAUNCH_CHECK();
 }
 

@@ -442,6 +442,14 @@ int ckf_attention_bwd(const void* qkv, const void* o, const float* lse, const vo
                          static_cast<cudaStream_t>(stream));
   });
 }
+// debug (not part of the ABI contract): per-CTA forward-attention timings, 8 longs per CTA
+int ckf_debug_attn_fwd_timings(long long* out, int n_ctas) {
+  return guard([&] {
+    long long* b = ckf::llama::attn_fwd_debug_buffer();
+    if (!b) ckf::raise(CKF_E_USAGE, "set CKF_ATTN_DEBUG=1");
+    CKF_CUDA(cudaMemcpy(out, b, 8 * sizeof(long long) * static_cast<size_t>(n_ctas), cudaMemcpyDeviceToHost));
+  });
+}
 int ckf_llama_token_batch(uint64_t data_seed, uint64_t stream, uint64_t index, size_t rows, size_t T, size_t V,
                           int* out) {
   return guard([&] {

@@ -113,6 +113,8 @@ struct Params {
   float* ws;     // split-K partial tiles: [units][BM][BN] fp32
   float* C;      // split-K: fp32 C (row pitch ldc) the reduced tile is added into
   int ldc;
+  const float2* rope_tab;  // fused RoPE (bf16 epilogue): heads of 64 columns below rope_cols
+  int rope_T, rope_cols;
 };
 
 template <int BN>
@@ -280,6 +282,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld32(trow + c0, r0);
         }
         tmem_ld_wait();
+        if constexpr (EPI == kStoreBF16) {
+          // fused RoPE: this 64-column chunk is one head of q or k; rotate (j, j+32) in fp32
+          if (p.rope_tab && w.nb * BN + c0 < p.rope_cols) {
+            const float2* cs = p.rope_tab + static_cast<size_t>((m0 + lane) % p.rope_T) * 32;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float2 t = cs[j];
+              const float x1 = __uint_as_float(r[j]), x2 = __uint_as_float(r[j + 32]);
+              r[j] = __float_as_uint(x1 * t.x - x2 * t.y);
+              r[j + 32] = __float_as_uint(x2 * t.x + x1 * t.y);
+            }
+          }
+        }
         if (c0 + CW >= BN) {  // last chunk loaded: hand the accumulator back to the MMA warp early
           tc_fence_before();
           __syncwarp();
@@ -461,6 +476,11 @@ void launch_t(const GemmDesc& g, int splits, cudaStream_t s) {
   p.ws = p.splits > 1 ? split_workspace(static_cast<size_t>(p.units) * BM * BN * sizeof(float)) : nullptr;
   p.C = static_cast<float*>(g.C);
   p.ldc = g.ldc;
+  p.rope_tab = g.rope_tab;
+  p.rope_T = g.rope_T;
+  p.rope_cols = g.rope_cols;
+  if (g.rope_tab && (EPI != kStoreBF16 || g.rope_T <= 0 || g.rope_cols % 64))
+    raise(1, "gemm_bf16: fused RoPE needs the bf16 epilogue and 64-column heads");
   const CUtensorMap twm = p.splits > 1 ? tma::make_2d_f32(p.ws, BN, static_cast<uint64_t>(p.units) * BM, BN, 32, 32)
                                        : tcm;
   auto kern = gemm_kernel<BN, A_MN, B_MN, EPI>;

@@ -26,6 +26,10 @@ struct GemmDesc {
   float alpha = 1.0f;
   int bn = 0;      // 0 = heuristic (128 or 256)
   int splits = 0;  // split-K factor; 0 = heuristic (kAccF32 only; ordered, deterministic)
+  // fused rotary embedding (kStoreBF16 only): columns [0, rope_cols) are 64-wide heads whose
+  // (j, j+32) pairs are rotated by rope_tab[(row % rope_T) * 32 + j] = (cos, sin)
+  const float2* rope_tab = nullptr;
+  int rope_T = 0, rope_cols = 0;
 };
 
 void gemm_bf16(const GemmDesc& g, cudaStream_t s);

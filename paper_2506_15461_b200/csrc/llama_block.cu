@@ -142,8 +142,11 @@ struct LlamaBlock final : BlockImpl {
 
   // ------------------------------------------------------------ timed launch helpers
   void gemm(int M, int N, int K, const bf16* A, int lda, bool a_mn, const bf16* B, int ldb, bool b_mn, void* C,
-            int ldc, int epi) {
+            int ldc, int epi, const float2* rope_tab = nullptr, int rope_cols = 0) {
     tc::GemmDesc g;
+    g.rope_tab = rope_tab;
+    g.rope_T = static_cast<int>(T);
+    g.rope_cols = rope_cols;
     g.M = M;
     g.N = N;
     g.K = K;
@@ -302,8 +305,13 @@ struct LlamaBlock final : BlockImpl {
     const float* Wf = wf(sid, li);
     const int Mi = static_cast<int>(Mt), di = static_cast<int>(d), fi = static_cast<int>(f);
     timed(KC_NORM, 0.0, Mt * d * 10.0, [&] { llama::rmsnorm_fwd(h, Wf + off.g1, Mt, d, c.xn1, c.rstd1, c.h_in, st); });
-    gemm(Mi, 3 * di, di, c.xn1, di, false, W + off.wqkv, 3 * di, true, c.qkv, 3 * di, tc::kStoreBF16);
-    timed(KC_NORM, 0.0, Mt * d * 8.0, [&] { llama::rope(c.qkv, Mt, T, d, H, 0, st); });
+    if (hd == 64) {  // RoPE fused into the QKV GEMM epilogue (q and k column blocks)
+      gemm(Mi, 3 * di, di, c.xn1, di, false, W + off.wqkv, 3 * di, true, c.qkv, 3 * di, tc::kStoreBF16,
+           llama::rope_table(T, hd, st), static_cast<int>(2 * d));
+    } else {
+      gemm(Mi, 3 * di, di, c.xn1, di, false, W + off.wqkv, 3 * di, true, c.qkv, 3 * di, tc::kStoreBF16);
+      timed(KC_NORM, 0.0, Mt * d * 8.0, [&] { llama::rope(c.qkv, Mt, T, d, H, 0, st); });
+    }
     timed(KC_ATTN, attn_flops_fwd(rows), Mt * d * 8.0, [&] {
       if (llama::attn_fwd_tc_supported(T, hd))
         llama::attn_fwd_tc(c.qkv, rows, T, H, hd, c.o, c.lse, st);  // tcgen05 + TMEM

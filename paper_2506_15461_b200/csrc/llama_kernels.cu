@@ -497,10 +497,8 @@ void gain_fold(const float* gpart, int nblk, size_t d, float* gg, cudaStream_t s
   CKF_LAUNCH_CHECK();
 }
 
-void rope(bf16* qkv, size_t ntok, size_t T, size_t d, size_t heads, int inverse, cudaStream_t s) {
-  const size_t hd = d / heads;
-  if (hd % 8) raise(1, "head_dim must be a multiple of 8 for RoPE");
-  // per-(T, hd) cos/sin table, built once on the current device
+const float2* rope_table(size_t T, size_t hd, cudaStream_t s) {
+  // per-(T, hd) cos/sin table, built once per device
   struct Tab {
     size_t T, hd;
     int dev;
@@ -509,16 +507,21 @@ void rope(bf16* qkv, size_t ntok, size_t T, size_t d, size_t heads, int inverse,
   static std::vector<Tab> tabs;
   int dev = 0;
   CKF_CUDA(cudaGetDevice(&dev));
-  float2* tab = nullptr;
   for (auto& t : tabs)
-    if (t.T == T && t.hd == hd && t.dev == dev) tab = t.p;
-  if (!tab) {
-    CKF_CUDA(cudaMalloc(&tab, T * hd / 2 * sizeof(float2)));
-    rope_table_kernel<<<static_cast<unsigned>((T * hd / 2 + 255) / 256), 256, 0, s>>>(tab, static_cast<int>(T),
-                                                                                     static_cast<int>(hd));
-    CKF_LAUNCH_CHECK();
-    tabs.push_back({T, hd, dev, tab});
-  }
+    if (t.T == T && t.hd == hd && t.dev == dev) return t.p;
+  float2* tab = nullptr;
+  CKF_CUDA(cudaMalloc(&tab, T * hd / 2 * sizeof(float2)));
+  rope_table_kernel<<<static_cast<unsigned>((T * hd / 2 + 255) / 256), 256, 0, s>>>(tab, static_cast<int>(T),
+                                                                                   static_cast<int>(hd));
+  CKF_LAUNCH_CHECK();
+  tabs.push_back({T, hd, dev, tab});
+  return tab;
+}
+
+void rope(bf16* qkv, size_t ntok, size_t T, size_t d, size_t heads, int inverse, cudaStream_t s) {
+  const size_t hd = d / heads;
+  if (hd % 8) raise(1, "head_dim must be a multiple of 8 for RoPE");
+  const float2* tab = rope_table(T, hd, s);
   const size_t items = ntok * (2 * d / 8);
   rope_kernel<<<grid_for(items, 256), 256, 0, s>>>(qkv, tab, static_cast<int>(ntok), static_cast<int>(T),
                                                    static_cast<int>(d), static_cast<int>(hd), inverse);

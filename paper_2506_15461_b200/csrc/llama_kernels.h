@@ -36,6 +36,8 @@ void gain_fold(const float* gpart, int nblk, size_t d, float* gg, cudaStream_t s
 // rotary embedding on the q and k column blocks of qkv [ntok x 3d] in place;
 // position = t % T; inverse = 1 applies the transpose (backward)
 void rope(bf16* qkv, size_t ntok, size_t T, size_t d, size_t heads, int inverse, cudaStream_t s);
+// device cos/sin table [T][hd/2] (float2), built on first use (the QKV GEMM epilogue reads it)
+const float2* rope_table(size_t T, size_t hd, cudaStream_t s);
 
 // a = silu(gate) * up ; gu = [gate | up] (ntok x 2f)
 void swiglu_fwd(const bf16* gu, size_t ntok, size_t f, bf16* a, cudaStream_t s);
@@ -60,6 +62,7 @@ void f32_to_bf16(const float* x, bf16* y, size_t n, cudaStream_t s);
 void attn_fwd(const bf16* qkv, size_t B, size_t T, size_t H, size_t hd, bf16* o, float* lse, cudaStream_t s);
 // tcgen05/TMEM/TMA forward (attention_tc.cu) for head_dim 64, seq_len % 128 == 0
 bool attn_fwd_tc_supported(size_t T, size_t hd);
+long long* attn_fwd_debug_buffer();  // non-null only with CKF_ATTN_DEBUG=1
 void attn_fwd_tc(const bf16* qkv, size_t B, size_t T, size_t H, size_t hd, bf16* o, float* lse, cudaStream_t s);
 void attn_bwd_tc(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, size_t B, size_t T, size_t H,
                  size_t hd, bf16* dqkv, float* Dsum, cudaStream_t s);

@@ -1,0 +1,27 @@
+#!/usr/bin/env python
+"""CKF_ATTN_DEBUG=1 python tools/attn_debug.py: per-CTA phase timings of the tcgen05 attention forward."""
+import ctypes as C, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+import paper_2506_15461_b200  # noqa
+from paper_2506_15461_b200._native import check, lib
+B, T, H, hd = 8, 1024, 8, 64
+qkv = torch.randn(B * T, 3 * H * hd, device="cuda").bfloat16()
+o = torch.empty(B * T, H * hd, dtype=torch.bfloat16, device="cuda")
+lse = torch.empty(B * H * T, device="cuda")
+for _ in range(3):
+    check(lib().ckf_attention_fwd(qkv.data_ptr(), B, T, H, hd, o.data_ptr(), lse.data_ptr(), 2, None))
+torch.cuda.synchronize()
+n = (T // 128) * B * H
+buf = (C.c_longlong * (8 * n))()
+L = lib()
+L.ckf_debug_attn_fwd_timings.argtypes = [C.POINTER(C.c_longlong), C.c_int]
+check(L.ckf_debug_attn_fwd_timings(buf, n))
+a = np.array(buf[:]).reshape(n, 8)
+t0 = a[:, 6].min()
+print("ctas", n, "cycles: total(max)", a[:, 4].max(), "mean", a[:, 4].mean())
+for nk in sorted(set(a[:, 0])):
+    s = a[a[:, 0] == nk]
+    print(f"nkb={nk:3d} n={len(s):4d} first_S={s[:,1].mean():8.0f} wait_S={s[:,2].mean():8.0f} wait_P={s[:,3].mean():8.0f} "
+          f"total={s[:,4].mean():8.0f} per_tile={(s[:,4]-s[:,1]).mean()/nk:7.0f} start={((s[:,6]-t0)/1e3).mean():8.1f}k")
