@@ -341,8 +341,9 @@ struct SmemKV {  // dK / dV kernel
 __global__ void __launch_bounds__(kThreadsBwd, 1)
     attn_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
                         const float* __restrict__ lse, const float* __restrict__ D, int T, int H,
-                        __nv_bfloat16* __restrict__ dqkv, float scale, float scale_log2) {
+                        __nv_bfloat16* __restrict__ dqkv, float scale, float scale_log2, long long* __restrict__ dbg) {
   extern __shared__ uint8_t smem_raw[];
+  const long long t_start = clock64();
   SmemKV& sm = *reinterpret_cast<SmemKV*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = T / TQ, kb = blockIdx.x;
@@ -395,7 +396,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
       mbar_wait(&sm.kv_full, 0);
       const uint32_t ka = smem_u32(sm.k), va = smem_u32(sm.v);
       const uint32_t pa = smem_u32(sm.p), da = smem_u32(sm.ds);
-      for (int i = 0; i < ntiles; ++i) {
+      auto issue_s = [&](int i) {  // S^T = K Q_i^T, dP^T = V dO_i^T
         const int st = i & 1;
         mbar_wait(&sm.qd_full[st], (i >> 1) & 1);
         mbar_wait(&sm.s_free, (i & 1) ^ 1);
@@ -409,8 +410,16 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
                     k > 0 ? 1u : 0u);
         }
         umma_commit(&sm.s_full);
+      };
+      issue_s(0);
+      for (int i = 0; i < ntiles; ++i) {
+        const int st = i & 1;
+        // the softmax warps release S^T/dP^T (s_free) as soon as they have loaded them, so the
+        // next tile's scores run on the tensor core while they still compute P / dS
+        if (i + 1 < ntiles) issue_s(i + 1);
         mbar_wait(&sm.pd_full, i & 1);
         tc_fence_after();
+        const uint32_t qa = smem_u32(sm.q[st]), oa = smem_u32(sm.d_o[st]);
 #pragma unroll
         for (int k = 0; k < TQ / 16; ++k) {
           const uint32_t aoff = (k >> 2) * (128 * 128) + (k & 3) * 32;
@@ -428,6 +437,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
     const int sw = warp - 4, quarter = sw & 3, half = sw >> 2;
     const int r = quarter * 32 + lane;  // key row within the tile
     const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+    long long w_bar = 0, w_s = 0, w_pd = 0, t_first = 0;
     for (int i = 0; i < ntiles; ++i) {
       const int st = i & 1;
       const int q0 = (kb + i) * TQ;
@@ -436,10 +446,18 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
         sm.lse2[st][r] = lse[static_cast<size_t>(bh) * T + q0 + r] * kLog2e;
         sm.dsum[st][r] = D[static_cast<size_t>(bh) * T + q0 + r];
       }
+      const long long t0 = clock64();
       asm volatile("bar.sync 1, 256;" ::: "memory");
+      const long long t1 = clock64();
       mbar_wait(&sm.s_full, i & 1);
+      const long long t2 = clock64();
+      if (i == 0) t_first = t2 - t_start;
       tc_fence_after();
       mbar_wait(&sm.pd_free, (i & 1) ^ 1);  // the previous tile's dV/dK MMAs have read P / dS
+      const long long t3 = clock64();
+      w_bar += t1 - t0;
+      w_s += t2 - t1;
+      w_pd += t3 - t2;
       const uint32_t pbase = smem_u32(sm.p), dbase = smem_u32(sm.ds);
 #pragma unroll 1
       for (int c0 = half * 64; c0 < half * 64 + 64; c0 += 32) {
@@ -447,6 +465,11 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
         tmem_ld32(trow + c0, us);
         tmem_ld32(trow + 128 + c0, ud);
         tmem_ld_wait();
+        if (c0 == half * 64 + 32) {  // last TMEM read of this tile: let the next S^T / dP^T start
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm.s_free);
+        }
         float pv[32], dv[32];
         const float4* l4 = reinterpret_cast<const float4*>(&sm.lse2[st][c0]);
         const float4* d4 = reinterpret_cast<const float4*>(&sm.dsum[st][c0]);
@@ -470,14 +493,20 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
         put32(pbase, r, c0, pv);
         put32(dbase, r, c0, dv);
       }
-      tc_fence_before();
       fence_proxy_async();
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&sm.s_free);
-        mbar_arrive(&sm.pd_full);
-      }
+      if (lane == 0) mbar_arrive(&sm.pd_full);
       asm volatile("bar.sync 1, 256;" ::: "memory");  // lse/D slots of this stage are reused two tiles later
+    }
+    if (dbg && threadIdx.x == 128) {
+      long long* d = dbg + 8 * (blockIdx.y * gridDim.x + blockIdx.x);
+      d[0] = ntiles;
+      d[1] = t_first;
+      d[2] = w_s;
+      d[3] = w_pd;
+      d[4] = clock64() - t_start;
+      d[5] = w_bar;
+      d[6] = t_start;
     }
     // ---------------- epilogue: column half 0 -> dV, half 1 -> dK (x scale)
     mbar_wait(&sm.acc_full, 0);
@@ -574,7 +603,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
       constexpr uint32_t kIdQ = idesc_bf16_f32(TQ, HD, false, true);   // [q x hd], K = keys, B MN-major
       mbar_wait(&sm.qd_full, 0);
       const uint32_t qa = smem_u32(sm.q), oa = smem_u32(sm.d_o), da = smem_u32(sm.ds);
-      for (int j = 0; j < nkb; ++j) {
+      auto issue_s = [&](int j) {  // S = Q K_j^T, dP = dO V_j^T
         const int st = j & 1;
         mbar_wait(&sm.kv_full[st], (j >> 1) & 1);
         mbar_wait(&sm.s_free, (j & 1) ^ 1);
@@ -588,8 +617,14 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
                     k > 0 ? 1u : 0u);
         }
         umma_commit(&sm.s_full);
+      };
+      issue_s(0);
+      for (int j = 0; j < nkb; ++j) {
+        const int st = j & 1;
+        if (j + 1 < nkb) issue_s(j + 1);  // overlaps the softmax warps' dS of tile j
         mbar_wait(&sm.ds_full, j & 1);
         tc_fence_after();
+        const uint32_t ka = smem_u32(sm.k[st]);
 #pragma unroll
         for (int k = 0; k < TK / 16; ++k)
           umma_bf16(tmem + 256, umma_desc_sw128(da + (k >> 2) * (128 * 128) + (k & 3) * 32, 16, 1024),
@@ -617,6 +652,11 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
         tmem_ld32(trow + c0, us);
         tmem_ld32(trow + 128 + c0, ud);
         tmem_ld_wait();
+        if (c0 == half * 64 + 32) {  // last TMEM read of this tile: let the next S / dP start
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm.s_free);
+        }
         float dv[32];
 #pragma unroll
         for (int t = 0; t < 32; ++t) {
@@ -630,13 +670,9 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
         }
         put32(dbase, r, c0, dv);
       }
-      tc_fence_before();
       fence_proxy_async();
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&sm.s_free);
-        mbar_arrive(&sm.ds_full);
-      }
+      if (lane == 0) mbar_arrive(&sm.ds_full);
     }
     mbar_wait(&sm.acc_full, 0);
     tc_fence_after();
@@ -714,8 +750,9 @@ void attn_bwd_tc(const bf16* qkv, const bf16* o, const float* lse, const bf16* d
   }
   const float scale = 1.f / sqrtf(static_cast<float>(hd));
   dim3 grid(static_cast<unsigned>(T / TQ), static_cast<unsigned>(B * H));
+  long long* dbg = attn_fwd_debug_buffer();
   attn_dkdv_tc_kernel<<<grid, kThreadsBwd, smem_kv, s>>>(tq, td, lse, Dsum, static_cast<int>(T), static_cast<int>(H),
-                                                      dqkv, scale, scale * kLog2e);
+                                                         dqkv, scale, scale * kLog2e, dbg ? dbg + 8 * 32768 : nullptr);
   CKF_LAUNCH_CHECK();
   attn_dq_tc_kernel<<<grid, kThreadsBwd, smem_q, s>>>(tq, td, lse, Dsum, static_cast<int>(T), static_cast<int>(H), dqkv,
                                                    scale, scale * kLog2e);

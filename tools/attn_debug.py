@@ -25,3 +25,20 @@ for nk in sorted(set(a[:, 0])):
     s = a[a[:, 0] == nk]
     print(f"nkb={nk:3d} n={len(s):4d} first_S={s[:,1].mean():8.0f} wait_S={s[:,2].mean():8.0f} wait_P={s[:,3].mean():8.0f} "
           f"total={s[:,4].mean():8.0f} per_tile={(s[:,4]-s[:,1]).mean()/nk:7.0f} start={((s[:,6]-t0)/1e3).mean():8.1f}k")
+
+# backward dK/dV kernel (timings at offset 32768 CTAs)
+dout = torch.randn(B * T, H * hd, device="cuda").bfloat16()
+dqkv = torch.empty_like(qkv)
+Dd = torch.empty(B * H * T, device="cuda")
+for _ in range(3):
+    check(lib().ckf_attention_bwd(qkv.data_ptr(), o.data_ptr(), lse.data_ptr(), dout.data_ptr(), B, T, H, hd,
+                                  dqkv.data_ptr(), Dd.data_ptr(), 2, None))
+torch.cuda.synchronize()
+buf2 = (C.c_longlong * (8 * (32768 + n)))()
+check(L.ckf_debug_attn_fwd_timings(buf2, 32768 + n))
+a = np.array(buf2[8 * 32768:]).reshape(n, 8)
+print("dkdv ctas", n, "cycles: total(max)", a[:, 4].max(), "mean", a[:, 4].mean())
+for nt in sorted(set(a[:, 0])):
+    s = a[a[:, 0] == nt]
+    print(f"ntiles={nt:3d} n={len(s):4d} first_S={s[:,1].mean():8.0f} wait_S={s[:,2].mean():8.0f} wait_PD={s[:,3].mean():8.0f} "
+          f"wait_bar={s[:,5].mean():8.0f} total={s[:,4].mean():8.0f} per_tile={(s[:,4]-s[:,1]).mean()/nt:7.0f}")
