@@ -318,9 +318,9 @@ def run_ours(args, w: dict):
             r = eng.recover_stage(2, reduction_error=False)
             lat.append(r.latency_ms)
         pb = 4 if w["precision"] != "fp64" else 8
-        P_ = eng.stage_params
-        rec = {"stage": 2, "stage_params": P_, "latency_ms": min(lat),
-               "avg_bytes": 3 * pb * P_, "avg_gbs_incl_moment_reset": None}
+        n_stage = eng.stage_params
+        rec = {"stage": 2, "stage_params": n_stage, "latency_ms": min(lat),
+               "avg_bytes": 3 * pb * n_stage, "avg_gbs_incl_moment_reset": None}
 
     if rank != 0:
         if world > 1:
