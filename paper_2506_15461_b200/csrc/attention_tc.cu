@@ -299,19 +299,32 @@ __global__ void __launch_bounds__(kThreads, 2)
 // D[bh*T + q] = sum_c dO[q, c] O[q, c]   (one warp per (token, head))
 __global__ void dsum_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout, int B, int T,
                             int H, float* __restrict__ D) {
-  const long long w = blockIdx.x * 8LL + threadIdx.x / 32;
-  const int lane = threadIdx.x & 31;
-  if (w >= static_cast<long long>(B) * T * H) return;
-  const long long tok = w / H;
-  const int h = static_cast<int>(w % H);
-  const size_t off = static_cast<size_t>(tok) * H * HD + static_cast<size_t>(h) * HD + 2 * lane;
-  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(o + off));
-  const float2 d = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dout + off));
-  float acc = a.x * d.x + a.y * d.y;
+  // 8 lanes per (token, head), 16-byte loads: a warp covers 4 (token, head) rows
+  const long long i = blockIdx.x * 256LL + threadIdx.x;
+  const long long row = i >> 3;
+  const int part = static_cast<int>(i & 7);
+  const bool live = row < static_cast<long long>(B) * T * H;
+  float acc = 0.f;
+  if (live) {
+    const size_t off = static_cast<size_t>(row) * HD + 8 * part;  // o / dout are [tok][H][HD]: row index = tok * H + h
+    const uint4 a = *reinterpret_cast<const uint4*>(o + off);
+    const uint4 d = *reinterpret_cast<const uint4*>(dout + off);
+    const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&a);
+    const __nv_bfloat162* pd = reinterpret_cast<const __nv_bfloat162*>(&d);
 #pragma unroll
-  for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
-  const int b = static_cast<int>(tok / T), q = static_cast<int>(tok % T);
-  if (lane == 0) D[(static_cast<size_t>(b) * H + h) * T + q] = acc;
+    for (int q = 0; q < 4; ++q) {
+      const float2 x = __bfloat1622float2(pa[q]), y = __bfloat1622float2(pd[q]);
+      acc += x.x * y.x + x.y * y.y;
+    }
+  }
+#pragma unroll
+  for (int s = 4; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+  if (live && part == 0) {
+    const long long tok = row / H;
+    const int h = static_cast<int>(row % H);
+    const int b = static_cast<int>(tok / T), q = static_cast<int>(tok % T);
+    D[(static_cast<size_t>(b) * H + h) * T + q] = acc;
+  }
 }
 
 // writes 32 bf16 values (one 64-byte half of a 128-byte swizzled row segment) of row r into
@@ -733,8 +746,8 @@ void attn_fwd_tc(const bf16* qkv, size_t B, size_t T, size_t H, size_t hd, bf16*
 void attn_bwd_tc(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, size_t B, size_t T, size_t H,
                  size_t hd, bf16* dqkv, float* Dsum, cudaStream_t s) {
   if (!attn_fwd_tc_supported(T, hd)) raise(1, "tcgen05 attention: head_dim 64 and seq_len % 128 == 0");
-  const size_t warps = B * T * H;
-  dsum_kernel<<<static_cast<unsigned>((warps + 7) / 8), 256, 0, s>>>(o, dout, static_cast<int>(B), static_cast<int>(T),
+  const size_t rows = B * T * H;
+  dsum_kernel<<<static_cast<unsigned>((rows + 31) / 32), 256, 0, s>>>(o, dout, static_cast<int>(B), static_cast<int>(T),
                                                                      static_cast<int>(H), Dsum);
   CKF_LAUNCH_CHECK();
   const CUtensorMap tq = tma::make_2d_bf16(qkv, 3 * H * hd, B * T, 3 * H * hd, 64, 128);

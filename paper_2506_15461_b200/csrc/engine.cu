@@ -435,15 +435,23 @@ void Engine::run_iteration(const int* orders, int m, const void* x, const void* 
   auto xk = [&](int k) { return xd + static_cast<size_t>(k) * mb * xcols * xelt; };
   auto yk = [&](int k) { return yd ? yd + static_cast<size_t>(k) * mb * ycols * yelt : nullptr; };
   auto ok = [&](int k) { return orders + static_cast<size_t>(k) * d_.s; };
+  impl_->begin_iteration(m, mb);
   if (schedule_ == 0) {
-    for (int k = 0; k < m; ++k) impl_->microbatch(ok(k), xk(k), yk(k), mb, true, scal_ + k);
+    for (int k = 0; k < m; ++k) impl_->microbatch(k, ok(k), xk(k), yk(k), mb, true, scal_ + k);
   } else {
     // GPipe: all forwards, then all backwards in microbatch order (per-stage accumulation
     // order is the reference's, pipeline.cpp:66-81); hops are issued in one global order
     // on every rank, so NCCL send/recv pair up without deadlock
-    for (int k = 0; k < m; ++k) impl_->mb_forward(k, ok(k), xk(k), yk(k), mb, true, scal_ + k);
-    for (int k = 0; k < m; ++k) impl_->mb_backward(k, ok(k), xk(k), mb);
+    for (int k = 0; k < m; ++k) {
+      impl_->wk = k;
+      impl_->mb_forward(k, ok(k), xk(k), yk(k), mb, true, scal_ + k);
+    }
+    for (int k = 0; k < m; ++k) {
+      impl_->wk = k;
+      impl_->mb_backward(k, ok(k), xk(k), mb);
+    }
   }
+  impl_->flush_grads();
   // data parallelism: sum every owned group's gradient over the replicas (each replica ran
   // its own m microbatches of the global batch), then Adam with 1/(m*R)
   if (replicas_ > 1) {
@@ -543,14 +551,14 @@ double Engine::eval_loss(const int* order, const void* x, const void* y, size_t 
     for (size_t r0 = 0; r0 < rows; r0 += cr) chunks.push_back({r0, std::min(cr, rows - r0)});
     if (chunks.size() > 64) raise(1, "evaluation batch too large for the engine's max_rows");
     for (size_t i = 0; i < chunks.size(); ++i)
-      impl_->microbatch(order, xi + chunks[i].first * (d_.T + 1), nullptr, chunks[i].second, false, scal_ + 4010 + i);
+      impl_->microbatch(0, order, xi + chunks[i].first * (d_.T + 1), nullptr, chunks[i].second, false, scal_ + 4010 + i);
     std::vector<double> ls(chunks.size());
     CKF_CUDA(cudaMemcpyAsync(ls.data(), scal_ + 4010, ls.size() * sizeof(double), cudaMemcpyDeviceToHost, st_));
     CKF_CUDA(cudaStreamSynchronize(st_));
     for (size_t i = 0; i < chunks.size(); ++i) l += ls[i] * static_cast<double>(chunks[i].second);
     return l / static_cast<double>(rows);
   }
-  impl_->microbatch(order, x, y, rows, false, scal_ + 4000);
+  impl_->microbatch(0, order, x, y, rows, false, scal_ + 4000);
   CKF_CUDA(cudaMemcpyAsync(&l, scal_ + 4000, sizeof(double), cudaMemcpyDeviceToHost, st_));
   CKF_CUDA(cudaStreamSynchronize(st_));
   return l;
@@ -561,7 +569,9 @@ double Engine::accumulate(const int* order, const void* x, const void* y, size_t
   validate_order(order, d_.s);
   if (rows == 0) raise(1, "empty batch");
   if (!on_device) upload(x, y, rows, &x, &y);
-  impl_->microbatch(order, x, y, rows, true, scal_ + 4001);
+  impl_->begin_iteration(1, rows);
+  impl_->microbatch(0, order, x, y, rows, true, scal_ + 4001);
+  impl_->flush_grads();
   double l = 0.0;
   CKF_CUDA(cudaMemcpyAsync(&l, scal_ + 4001, sizeof(double), cudaMemcpyDeviceToHost, st_));
   CKF_CUDA(cudaStreamSynchronize(st_));

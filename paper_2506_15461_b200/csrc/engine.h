@@ -82,11 +82,22 @@ struct BlockImpl {
   // Backward of slot `mb`: owned layers in reverse applied order (gradients
   // accumulate into the groups' g buffers), then the embedding.
   virtual void mb_backward(int mb, const int* order, const void* x, size_t rows) = 0;
-  // the reference's per-microbatch order: forward then backward (model.cpp:211-378)
-  void microbatch(const int* order, const void* x, const void* y, size_t rows, bool train, double* loss_dev) {
+  // the reference's per-microbatch order: forward then backward (model.cpp:211-378);
+  // k = the microbatch's position in the iteration (activation slot 0 is reused)
+  void microbatch(int k, const int* order, const void* x, const void* y, size_t rows, bool train, double* loss_dev) {
+    wk = k;
     mb_forward(0, order, x, y, rows, train, loss_dev);
     if (train) mb_backward(0, order, x, rows);
   }
+  // An iteration of m microbatches of `rows` each begins / its backward phase is
+  // over: blocks that defer work to the end of the backward phase (the LLaMA
+  // block's weight-gradient GEMMs) flush it here, before DP all-reduce and Adam.
+  virtual void begin_iteration(int m, size_t rows) {
+    (void)m;
+    (void)rows;
+  }
+  virtual void flush_grads() {}
+  int wk = 0;  // position of the current microbatch within the iteration
   // Predictions of forward(order, x) (MLP) into a device buffer of rows*out.
   virtual void predict(const int* order, const void* x, size_t rows, void* pred) = 0;
   Engine* eng;

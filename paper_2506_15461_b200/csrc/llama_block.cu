@@ -17,6 +17,9 @@
 //   [g1 (d) | Wqkv (d x 3d) | Wo (d x d) | g2 (d) | Wgu (d x 2f) | Wd (f x d)]
 // edge groups: E [V x d];  [gF (d) | E_inv (d x V)].  Weights row-major
 // [fan_in x fan_out] like the reference (model.cpp:27-33).
+#include <algorithm>
+#include <cstdlib>
+#include <utility>
 #include <vector>
 
 #include "engine.h"
@@ -116,11 +119,14 @@ struct LlamaBlock final : BlockImpl {
     bf16 *xn1, *qkv, *o, *xn2, *gu, *a;
   };
   static size_t al(size_t b) { return (b + 255) / 256 * 256; }
-  Cache cache(size_t slot, size_t Mt, size_t rows) {
-    const size_t bytes = al(Mt * d * 4) * 2 + al(Mt * 4) * 2 + al(rows * H * T * 4) + al(Mt * d * 2) * 3 +
-                         al(Mt * 3 * d * 2) + al(Mt * 2 * f * 2) + al(Mt * f * 2);
+  // with_x = false: the layer inputs X (xn1, o, xn2, a) live in the deferred
+  // weight-gradient buffers instead (WSet below)
+  Cache cache(size_t slot, size_t Mt, size_t rows, bool with_x) {
+    const size_t xb = with_x ? al(Mt * d * 2) * 3 + al(Mt * f * 2) : 0;
+    const size_t bytes = al(Mt * d * 4) * 2 + al(Mt * 4) * 2 + al(rows * H * T * 4) + al(Mt * 3 * d * 2) +
+                         al(Mt * 2 * f * 2) + xb;
     char* p = static_cast<char*>(eng->ws(bytes, 100 + static_cast<int>(slot)));  // slot = cache_id - 100
-    Cache c;
+    Cache c{};
     auto take = [&](size_t b) {
       char* r = p;
       p += al(b);
@@ -131,13 +137,105 @@ struct LlamaBlock final : BlockImpl {
     c.rstd1 = reinterpret_cast<float*>(take(Mt * 4));
     c.rstd2 = reinterpret_cast<float*>(take(Mt * 4));
     c.lse = reinterpret_cast<float*>(take(rows * H * T * 4));
-    c.xn1 = reinterpret_cast<bf16*>(take(Mt * d * 2));
-    c.o = reinterpret_cast<bf16*>(take(Mt * d * 2));
-    c.xn2 = reinterpret_cast<bf16*>(take(Mt * d * 2));
     c.qkv = reinterpret_cast<bf16*>(take(Mt * 3 * d * 2));
     c.gu = reinterpret_cast<bf16*>(take(Mt * 2 * f * 2));
-    c.a = reinterpret_cast<bf16*>(take(Mt * f * 2));
+    if (with_x) {
+      c.xn1 = reinterpret_cast<bf16*>(take(Mt * d * 2));
+      c.o = reinterpret_cast<bf16*>(take(Mt * d * 2));
+      c.xn2 = reinterpret_cast<bf16*>(take(Mt * d * 2));
+      c.a = reinterpret_cast<bf16*>(take(Mt * f * 2));
+    }
     return c;
+  }
+
+  // ------------------------------------------------------------ deferred weight gradients
+  // A layer's four weight gradients (gW += X^T dY for Wqkv, Wo, Wgu, Wd) feed
+  // nothing inside the iteration but Adam, so they are deferred to the end of
+  // the backward phase and computed ONCE over all m microbatches (GEMM depth
+  // K = m * Mt tokens instead of m GEMMs of depth Mt): with M = d small, a
+  // per-microbatch wgrad has too few output tiles for 148 SMs and pays a
+  // split-K reduction; the batched one fills the machine.  This is the
+  // "W pass" of zero-bubble pipeline schedules, and in a multi-GPU pipeline it
+  // runs in the drain bubble.  The layer inputs X and output gradients dY are
+  // written by the forward / backward straight into per-layer buffers
+  // [m * Mt x width] (microbatch k at rows k * Mt), so deferral costs no copies.
+  // Numerics: one fp32 GEMM over all tokens replaces the reference's
+  // per-microbatch Gradients::accumulate (model.cpp:299-305) -- a different
+  // fp32 association, still deterministic.  CKF_WGRAD_DEFER=0, or too little
+  // free HBM, selects the per-microbatch form.
+  struct WSet {
+    bf16 *xn1, *o, *xn2, *a;        // X: inputs of Wqkv, Wo, Wgu, Wd
+    bf16 *dqkv, *dho, *dgu, *dhd;   // dY: output gradients of Wqkv, Wo, Wgu, Wd
+  };
+  static constexpr int kWSlot = 300000;
+  bool defer_ = false;
+  int defer_m_ = 1;
+  size_t defer_Mt_ = 0;
+  std::vector<std::pair<int, size_t>> pending_;
+  size_t wrow_elems() const { return 8 * d + 3 * f; }  // X (3d + f) + dY (5d + 2f) bf16 per token
+  WSet wset(int sid, size_t li, int k) {
+    const size_t R = static_cast<size_t>(defer_m_) * defer_Mt_, o = static_cast<size_t>(k) * defer_Mt_;
+    bf16* p = static_cast<bf16*>(eng->ws(R * wrow_elems() * 2, kWSlot + 1024 * (sid - 1) + static_cast<int>(li)));
+    WSet w;
+    size_t at = 0;
+    auto take = [&](size_t width) {
+      bf16* r = p + at * R + o * width;
+      at += width;
+      return r;
+    };
+    w.xn1 = take(d);
+    w.o = take(d);
+    w.xn2 = take(d);
+    w.a = take(f);
+    w.dqkv = take(3 * d);
+    w.dho = take(d);
+    w.dgu = take(2 * f);
+    w.dhd = take(d);
+    return w;
+  }
+  // per-microbatch form: X in the activation cache, dY in scratch
+  WSet wset_local(const Cache& c, bf16* dh_bf, size_t Mt) {
+    WSet w{c.xn1, c.o, c.xn2, c.a, nullptr, dh_bf, nullptr, dh_bf};
+    w.dgu = buf<bf16>(47, Mt * 2 * f);
+    w.dqkv = 3 * d <= 2 * f ? w.dgu : static_cast<bf16*>(eng->ws(Mt * 3 * d * 2, 56));  // dgu is dead by then
+    return w;
+  }
+
+  void begin_iteration(int m, size_t rows) override {
+    pending_.clear();
+    const char* env = std::getenv("CKF_WGRAD_DEFER");
+    bool want = !(env && env[0] == '0') && m > 1;
+    const size_t Mt = rows * T;
+    if (want) {
+      size_t layers = 0;
+      const Desc& D = eng->desc();
+      for (size_t i = 0; i < D.s; ++i)
+        if (eng->mine(eng->owner_of_stage(static_cast<int>(i + 1)))) layers += D.part[i].count();
+      const size_t need = layers * static_cast<size_t>(m) * Mt * wrow_elems() * 2;
+      size_t fr = 0, tot = 0;
+      CKF_CUDA(cudaMemGetInfo(&fr, &tot));
+      const size_t have = (defer_m_ == m && defer_Mt_ == Mt && defer_) ? need : 0;  // already allocated
+      want = need <= have + fr / 2;
+    }
+    defer_ = want;
+    defer_m_ = want ? m : 1;
+    defer_Mt_ = Mt;
+  }
+
+  void flush_grads() override {
+    if (!defer_ || pending_.empty()) return;
+    std::sort(pending_.begin(), pending_.end());
+    const int R = static_cast<int>(static_cast<size_t>(defer_m_) * defer_Mt_);
+    const int di = static_cast<int>(d), fi = static_cast<int>(f);
+    for (const auto& [sid, li] : pending_) {
+      const WSet w = wset(sid, li, 0);
+      float* G = gf(sid, li);
+      gemm(di, 3 * di, R, w.xn1, di, true, w.dqkv, 3 * di, true, G + off.wqkv, 3 * di, tc::kAccF32);
+      gemm(di, di, R, w.o, di, true, w.dho, di, true, G + off.wo, di, tc::kAccF32);
+      gemm(di, 2 * fi, R, w.xn2, di, true, w.dgu, 2 * fi, true, G + off.wgu, 2 * fi, tc::kAccF32);
+      gemm(fi, di, R, w.a, fi, true, w.dhd, di, true, G + off.wd, di, tc::kAccF32);
+    }
+    pending_.clear();
   }
 
   // ------------------------------------------------------------ timed launch helpers
@@ -190,8 +288,8 @@ struct LlamaBlock final : BlockImpl {
     }
     return v;
   }
-  Cache cache_for(int mb, size_t applied, size_t Mt, size_t rows) {
-    return cache(static_cast<size_t>(cache_id(mb, applied)) - 100, Mt, rows);
+  Cache cache_for(int mb, size_t applied, size_t Mt, size_t rows, bool with_x) {
+    return cache(static_cast<size_t>(cache_id(mb, applied)) - 100, Mt, rows, with_x);
   }
 
   void mb_forward(int mb, const int* order, const void* xv, const void*, size_t rows, bool train,
@@ -234,7 +332,9 @@ struct LlamaBlock final : BlockImpl {
       const Range& r = D.part[static_cast<size_t>(sid - 1)];
       for (size_t li = 0; li < r.count(); ++li, ++slot) {
         if (!eng->mine(own)) continue;
-        layer_fwd(sid, li, cache_for(train ? mb : 0, slot, Mt, rows), h, rows, Mt);
+        const bool dfr = train && defer_;
+        const Cache c = cache_for(train ? mb : 0, slot, Mt, rows, !dfr);
+        layer_fwd(sid, li, c, dfr ? wset(sid, li, wk) : wset_local(c, nullptr, Mt), h, rows, Mt);
       }
     }
     eng->move(h, Mt * d * 4, at, static_cast<int>(D.s) + 1);
@@ -267,20 +367,32 @@ struct LlamaBlock final : BlockImpl {
     float* dh = buf<float>(slot_id(mb, 2), Mt * d);
     bf16* dh_bf = buf<bf16>(slot_id(mb, 3), Mt * d);
     float* dxn = buf<float>(45, Mt * d);
-    bf16* scratch_bf = buf<bf16>(46, Mt * std::max(3 * d, 2 * f));  // da / do staging
-    bf16* dgu = buf<bf16>(47, Mt * 2 * f);
+    bf16* scratch_bf = buf<bf16>(46, Mt * std::max(d, f));  // da / do staging
     float* Dsum = buf<float>(48, rows * H * T);
     const int nblk = llama::rmsnorm_bwd_blocks(Mt);
     float* gpart = buf<float>(49, static_cast<size_t>(nblk) * d);
     const std::vector<Applied> applied = applied_order(order);
+    const int me = eng->rank();
     int at = static_cast<int>(eng->desc().s) + 1;  // dL/dh_final sits at the de-embedding
+    bf16* cur = dh_bf;                              // where bf16(dh) currently lives
     for (size_t ai = applied.size(); ai-- > 0;) {
       const Applied& a = applied[ai];
       const int own = eng->owner_of_stage(a.sid);
-      if (eng->move(dh, Mt * d * 4, at, a.sid)) llama::f32_to_bf16(dh, dh_bf, Mt * d, st);
+      if (eng->move(dh, Mt * d * 4, at, a.sid)) {
+        llama::f32_to_bf16(dh, dh_bf, Mt * d, st);
+        cur = dh_bf;
+      }
       at = a.sid;
       if (!eng->mine(own)) continue;
-      layer_bwd(a.sid, a.li, cache_for(mb, ai, Mt, rows), dh, dh_bf, dxn, scratch_bf, dgu, Dsum, gpart, nblk, rows, Mt);
+      const Cache c = cache_for(mb, ai, Mt, rows, !defer_);
+      const WSet w = defer_ ? wset(a.sid, a.li, wk) : wset_local(c, dh_bf, Mt);
+      if (cur != w.dhd) CKF_CUDA(cudaMemcpyAsync(w.dhd, cur, Mt * d * 2, cudaMemcpyDeviceToDevice, st));
+      // bf16(dh) after this layer goes straight to where the next applied layer reads it
+      bf16* out = dh_bf;
+      if (defer_ && ai > 0 && eng->owner_of_stage(applied[ai - 1].sid) == me)
+        out = wset(applied[ai - 1].sid, applied[ai - 1].li, wk).dhd;
+      layer_bwd(a.sid, a.li, c, w, dh, out, dxn, scratch_bf, Dsum, gpart, nblk, rows, Mt);
+      cur = out;
     }
     eng->move(dh, Mt * d * 4, at, 0);
     if (eng->mine(eng->owner_of_embed())) {
@@ -299,67 +411,69 @@ struct LlamaBlock final : BlockImpl {
     return 2.0 * rows * H * static_cast<double>(T) * T * hd;  // QK^T + PV, causal half
   }
 
-  void layer_fwd(int sid, size_t li, const Cache& c, float* h, size_t rows, size_t Mt) {
+  void layer_fwd(int sid, size_t li, const Cache& c, const WSet& w, float* h, size_t rows, size_t Mt) {
     cudaStream_t st = eng->stream();
     const bf16* W = wbf(sid, li);
     const float* Wf = wf(sid, li);
     const int Mi = static_cast<int>(Mt), di = static_cast<int>(d), fi = static_cast<int>(f);
-    timed(KC_NORM, 0.0, Mt * d * 10.0, [&] { llama::rmsnorm_fwd(h, Wf + off.g1, Mt, d, c.xn1, c.rstd1, c.h_in, st); });
+    timed(KC_NORM, 0.0, Mt * d * 10.0, [&] { llama::rmsnorm_fwd(h, Wf + off.g1, Mt, d, w.xn1, c.rstd1, c.h_in, st); });
     if (hd == 64) {  // RoPE fused into the QKV GEMM epilogue (q and k column blocks)
-      gemm(Mi, 3 * di, di, c.xn1, di, false, W + off.wqkv, 3 * di, true, c.qkv, 3 * di, tc::kStoreBF16,
+      gemm(Mi, 3 * di, di, w.xn1, di, false, W + off.wqkv, 3 * di, true, c.qkv, 3 * di, tc::kStoreBF16,
            llama::rope_table(T, hd, st), static_cast<int>(2 * d));
     } else {
-      gemm(Mi, 3 * di, di, c.xn1, di, false, W + off.wqkv, 3 * di, true, c.qkv, 3 * di, tc::kStoreBF16);
+      gemm(Mi, 3 * di, di, w.xn1, di, false, W + off.wqkv, 3 * di, true, c.qkv, 3 * di, tc::kStoreBF16);
       timed(KC_NORM, 0.0, Mt * d * 8.0, [&] { llama::rope(c.qkv, Mt, T, d, H, 0, st); });
     }
     timed(KC_ATTN, attn_flops_fwd(rows), Mt * d * 8.0, [&] {
       if (llama::attn_fwd_tc_supported(T, hd))
-        llama::attn_fwd_tc(c.qkv, rows, T, H, hd, c.o, c.lse, st);  // tcgen05 + TMEM
+        llama::attn_fwd_tc(c.qkv, rows, T, H, hd, w.o, c.lse, st);  // tcgen05 + TMEM
       else
-        llama::attn_fwd(c.qkv, rows, T, H, hd, c.o, c.lse, st);
+        llama::attn_fwd(c.qkv, rows, T, H, hd, w.o, c.lse, st);
     });
-    gemm(Mi, di, di, c.o, di, false, W + off.wo, di, true, h, di, tc::kAccF32);
-    timed(KC_NORM, 0.0, Mt * d * 10.0, [&] { llama::rmsnorm_fwd(h, Wf + off.g2, Mt, d, c.xn2, c.rstd2, c.h_mid, st); });
-    gemm(Mi, 2 * fi, di, c.xn2, di, false, W + off.wgu, 2 * fi, true, c.gu, 2 * fi, tc::kStoreBF16);
-    timed(KC_NORM, 0.0, Mt * f * 6.0, [&] { llama::swiglu_fwd(c.gu, Mt, f, c.a, st); });
-    gemm(Mi, di, fi, c.a, fi, false, W + off.wd, di, true, h, di, tc::kAccF32);
+    gemm(Mi, di, di, w.o, di, false, W + off.wo, di, true, h, di, tc::kAccF32);
+    timed(KC_NORM, 0.0, Mt * d * 10.0, [&] { llama::rmsnorm_fwd(h, Wf + off.g2, Mt, d, w.xn2, c.rstd2, c.h_mid, st); });
+    gemm(Mi, 2 * fi, di, w.xn2, di, false, W + off.wgu, 2 * fi, true, c.gu, 2 * fi, tc::kStoreBF16);
+    timed(KC_NORM, 0.0, Mt * f * 6.0, [&] { llama::swiglu_fwd(c.gu, Mt, f, w.a, st); });
+    gemm(Mi, di, fi, w.a, fi, false, W + off.wd, di, true, h, di, tc::kAccF32);
   }
 
-  void layer_bwd(int sid, size_t li, const Cache& c, float* dh, bf16* dh_bf, float* dxn, bf16* sbf, bf16* dgu,
+  // w.dhd holds bf16(dh) on entry; bf16(dh) after the layer goes to dh_bf_out
+  void layer_bwd(int sid, size_t li, const Cache& c, const WSet& w, float* dh, bf16* dh_bf_out, float* dxn, bf16* sbf,
                  float* Dsum, float* gpart, int nblk, size_t rows, size_t Mt) {
     cudaStream_t st = eng->stream();
     const bf16* W = wbf(sid, li);
     const float* Wf = wf(sid, li);
     float* G = gf(sid, li);
     const int Mi = static_cast<int>(Mt), di = static_cast<int>(d), fi = static_cast<int>(f);
+    const bool now = !defer_;  // weight gradients now, or batched in flush_grads()
+    if (defer_ && std::find(pending_.begin(), pending_.end(), std::make_pair(sid, li)) == pending_.end())
+      pending_.emplace_back(sid, li);
     // MLP half: h_out = h_mid + swiglu(xn2 Wgu) Wd
     bf16* da = sbf;
-    gemm(fi, di, Mi, c.a, fi, true, dh_bf, di, true, G + off.wd, di, tc::kAccF32);             // gWd += a^T dh
-    gemm(Mi, fi, di, dh_bf, di, false, W + off.wd, di, false, da, fi, tc::kStoreBF16);         // da = dh Wd^T
-    timed(KC_NORM, 0.0, Mt * f * 10.0, [&] { llama::swiglu_bwd(c.gu, da, Mt, f, dgu, st); });
-    gemm(di, 2 * fi, Mi, c.xn2, di, true, dgu, 2 * fi, true, G + off.wgu, 2 * fi, tc::kAccF32);  // gWgu += xn2^T dgu
-    gemm(Mi, di, 2 * fi, dgu, 2 * fi, false, W + off.wgu, 2 * fi, false, dxn, di, tc::kStoreF32);  // dxn2 = dgu Wgu^T
+    if (now) gemm(fi, di, Mi, w.a, fi, true, w.dhd, di, true, G + off.wd, di, tc::kAccF32);   // gWd += a^T dh
+    gemm(Mi, fi, di, w.dhd, di, false, W + off.wd, di, false, da, fi, tc::kStoreBF16);       // da = dh Wd^T
+    timed(KC_NORM, 0.0, Mt * f * 10.0, [&] { llama::swiglu_bwd(c.gu, da, Mt, f, w.dgu, st); });
+    if (now) gemm(di, 2 * fi, Mi, w.xn2, di, true, w.dgu, 2 * fi, true, G + off.wgu, 2 * fi, tc::kAccF32);
+    gemm(Mi, di, 2 * fi, w.dgu, 2 * fi, false, W + off.wgu, 2 * fi, false, dxn, di, tc::kStoreF32);  // dxn2
     timed(KC_NORM, 0.0, Mt * d * 18.0, [&] {
-      llama::rmsnorm_bwd(dxn, c.h_mid, Wf + off.g2, c.rstd2, Mt, d, dh, dh_bf, gpart, st);
+      llama::rmsnorm_bwd(dxn, c.h_mid, Wf + off.g2, c.rstd2, Mt, d, dh, w.dho, gpart, st);
       llama::gain_fold(gpart, nblk, d, G + off.g2, st);
     });
     // attention half: h_mid = h_in + attn(rope(xn1 Wqkv)) Wo
     bf16* d_o = sbf;
-    gemm(di, di, Mi, c.o, di, true, dh_bf, di, true, G + off.wo, di, tc::kAccF32);             // gWo += o^T dh
-    gemm(Mi, di, di, dh_bf, di, false, W + off.wo, di, false, d_o, di, tc::kStoreBF16);        // do = dh Wo^T
-    bf16* dqkv = dgu;  // dgu is dead; Mt x 3d fits in Mt x 2f only if 3d <= 2f
-    if (3 * d > 2 * f) dqkv = static_cast<bf16*>(eng->ws(Mt * 3 * d * 2, 56));
+    if (now) gemm(di, di, Mi, w.o, di, true, w.dho, di, true, G + off.wo, di, tc::kAccF32);   // gWo += o^T dh
+    gemm(Mi, di, di, w.dho, di, false, W + off.wo, di, false, d_o, di, tc::kStoreBF16);      // do = dh Wo^T
     timed(KC_ATTN, 2.5 * attn_flops_fwd(rows), Mt * d * 16.0, [&] {
       if (llama::attn_fwd_tc_supported(T, hd))
-        llama::attn_bwd_tc(c.qkv, c.o, c.lse, d_o, rows, T, H, hd, dqkv, Dsum, st);  // tcgen05 + TMEM
+        llama::attn_bwd_tc(c.qkv, w.o, c.lse, d_o, rows, T, H, hd, w.dqkv, Dsum, st);  // tcgen05 + TMEM
       else
-        llama::attn_bwd(c.qkv, c.o, c.lse, d_o, rows, T, H, hd, dqkv, Dsum, st);
+        llama::attn_bwd(c.qkv, w.o, c.lse, d_o, rows, T, H, hd, w.dqkv, Dsum, st);
     });
-    timed(KC_NORM, 0.0, Mt * d * 8.0, [&] { llama::rope(dqkv, Mt, T, d, H, 1, st); });
-    gemm(di, 3 * di, Mi, c.xn1, di, true, dqkv, 3 * di, true, G + off.wqkv, 3 * di, tc::kAccF32);  // gWqkv += xn1^T dqkv
-    gemm(Mi, di, 3 * di, dqkv, 3 * di, false, W + off.wqkv, 3 * di, false, dxn, di, tc::kStoreF32);  // dxn1
+    timed(KC_NORM, 0.0, Mt * d * 8.0, [&] { llama::rope(w.dqkv, Mt, T, d, H, 1, st); });
+    if (now) gemm(di, 3 * di, Mi, w.xn1, di, true, w.dqkv, 3 * di, true, G + off.wqkv, 3 * di, tc::kAccF32);
+    gemm(Mi, di, 3 * di, w.dqkv, 3 * di, false, W + off.wqkv, 3 * di, false, dxn, di, tc::kStoreF32);  // dxn1
     timed(KC_NORM, 0.0, Mt * d * 18.0, [&] {
-      llama::rmsnorm_bwd(dxn, c.h_in, Wf + off.g1, c.rstd1, Mt, d, dh, dh_bf, gpart, st);
+      llama::rmsnorm_bwd(dxn, c.h_in, Wf + off.g1, c.rstd1, Mt, d, dh, dh_bf_out, gpart, st);
       llama::gain_fold(gpart, nblk, d, G + off.g1, st);
     });
   }

@@ -161,20 +161,22 @@ __global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(const float4* __restri
   }
 }
 
-// gg[c] += sum_b gpart[b, c]: 8 fixed residue classes of b per column, then a fixed-order fold
+// gg[c] += sum_b gpart[b, c]: a CTA owns 8 columns; its 32 slices sum the fixed
+// residue classes b = slice (mod 32) -- 32 independent loads in flight per column
+// instead of a serial walk -- then one thread per column folds the slices in order
 __global__ void gain_fold_kernel(const float* __restrict__ gpart, int nblk, int d, float* __restrict__ gg) {
-  __shared__ float part[8][33];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int c = blockIdx.x * 32 + lane;
+  __shared__ float part[32][9];
+  const int cl = threadIdx.x & 7, sl = threadIdx.x >> 3;
+  const int c = blockIdx.x * 8 + cl;
   float acc = 0.f;
   if (c < d)
-    for (int b = w; b < nblk; b += 8) acc += gpart[static_cast<size_t>(b) * d + c];
-  part[w][lane] = acc;
+    for (int b = sl; b < nblk; b += 32) acc += gpart[static_cast<size_t>(b) * d + c];
+  part[sl][cl] = acc;
   __syncthreads();
-  if (w == 0 && c < d) {
+  if (threadIdx.x < 8 && c < d) {
     float s = 0.f;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) s += part[k][lane];
+    for (int k = 0; k < 32; ++k) s += part[k][cl];
     gg[c] += s;
   }
 }
@@ -493,7 +495,7 @@ void rmsnorm_bwd(const float* dy, const float* x, const float* g, const float* r
 }
 
 void gain_fold(const float* gpart, int nblk, size_t d, float* gg, cudaStream_t s) {
-  gain_fold_kernel<<<static_cast<unsigned>((d + 31) / 32), 256, 0, s>>>(gpart, nblk, static_cast<int>(d), gg);
+  gain_fold_kernel<<<static_cast<unsigned>((d + 7) / 8), 256, 0, s>>>(gpart, nblk, static_cast<int>(d), gg);
   CKF_LAUNCH_CHECK();
 }
 
