@@ -182,6 +182,10 @@ def workload_config(args, w: dict) -> dict:
            "l2": "256 MiB memset between timed steps (outside the events)"}
     if w["block"] == "llama":
         cfg.update(vocab=w["output_dim"], heads=w["heads"])
+        # all stages resident on a rank => microbatches sharing an execution order run as
+        # one fused pass (Engine::run_iteration; cap 0 = fit to HBM, 1 = per microbatch)
+        cfg["microbatch_fusion"] = ("cap " + os.environ["CKF_MB_GROUP"]) if os.environ.get("CKF_MB_GROUP") else (
+            "auto (fit to HBM)" if P == 1 else "off (stages partitioned)")
     return cfg
 
 

@@ -259,6 +259,10 @@ int ckf_engine_set_edge_scalars(ckf_engine_t e, double lr, long step_embed, long
 
 /* iteration schedule: 0 = sequential (default on one GPU), 1 = GPipe (default once attached to >1 rank) */
 int ckf_engine_set_schedule(ckf_engine_t e, int mode);
+/* microbatch fusion when every stage is resident on this rank: microbatches sharing an
+ * execution order run as one forward+backward of up to `cap` microbatches (same
+ * arithmetic as pipeline.cpp:66-83; 0 = as many as HBM allows (default), 1 = off) */
+int ckf_engine_set_group_cap(ckf_engine_t e, int cap);
 /* Hop log for a VIRTUAL placement (stage -> rank), used to check on one GPU that
  * the engine's stage transfers match ckf_pipeline_plan: when enabled, every
  * cross-rank transfer the placement implies is recorded as (src, dst, bytes). */

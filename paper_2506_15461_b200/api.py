@@ -308,6 +308,10 @@ class Engine:
     def sync(self):
         check(lib().ckf_engine_sync(self._h))
 
+    def set_group_cap(self, cap: int):
+        """Microbatch fusion cap (0 = fit to HBM, 1 = one microbatch per pass)."""
+        check(lib().ckf_engine_set_group_cap(self._h, cap))
+
     def set_schedule(self, mode: int):
         """0 = forward+backward per microbatch, 1 = GPipe (all forwards, then all backwards)."""
         check(lib().ckf_engine_set_schedule(self._h, mode))

@@ -587,6 +587,10 @@ int ckf_engine_set_edge_scalars(ckf_engine_t e, double lr, long se, long sd) {
 int ckf_engine_set_schedule(ckf_engine_t e, int mode) {
   return guard([&] { E(e)->set_schedule(mode); });
 }
+
+int ckf_engine_set_group_cap(ckf_engine_t e, int cap) {
+  return guard([&] { E(e)->set_group_cap(cap); });
+}
 int ckf_engine_hop_log(ckf_engine_t e, int nranks, const int* stage_rank) {
   return guard([&] { E(e)->hop_log_enable(nranks, stage_rank); });
 }

@@ -97,6 +97,7 @@ Engine::Engine(const ckf_model_desc& in) {
   d_.heads = in.n_heads ? in.n_heads : 1;
   d_.T = in.seq_len ? in.seq_len : 1;
   d_.max_rows = in.max_rows ? in.max_rows : 256;
+  if (const char* g = std::getenv("CKF_MB_GROUP")) group_cap_ = std::max(0, std::atoi(g));
   d_.device = in.device;
   if (d_.block != CKF_BLOCK_MLP && d_.block != CKF_BLOCK_LLAMA) raise(1, "unknown block kind");
   if (d_.prec < CKF_FP64 || d_.prec > CKF_BF16) raise(1, "unknown precision");
@@ -377,6 +378,31 @@ void Engine::adam_group(ParamGroup& g, double lr, double gscale, double* omega_d
   kt_end(KC_ADAM, 0.0, static_cast<double>(g.n) * (8.0 * master_bytes() + (g.wlp ? 2.0 : 0.0)));
 }
 
+// Largest fused group (in microbatches of mb_rows) whose activations fit in half
+// of the HBM still free after the block's pending reservations; fitted once per
+// microbatch size so the choice (and hence the numerics) is stable across iterations.
+int Engine::fused_group_size(int m, size_t mb_rows) {
+  if (m < 2 || group_cap_ == 1) return 1;
+  const size_t bpt = impl_->group_bytes_per_token();
+  if (!bpt) return 1;
+  const size_t tok = mb_rows * (d_.block == CKF_BLOCK_LLAMA ? d_.T : 1);
+  int fit = 0;
+  for (const auto& e : group_fit_)
+    if (e.first == tok) fit = e.second;
+  if (!fit) {
+    size_t fr = 0, tot = 0;
+    CKF_CUDA(cudaMemGetInfo(&fr, &tot));
+    const size_t res = impl_->reserved_bytes();
+    const size_t budget = fr > res ? (fr - res) / 2 : 0;
+    fit = static_cast<int>(std::min<size_t>(64, budget / std::max<size_t>(1, bpt * tok)));
+    fit = std::max(fit, 1);
+    group_fit_.emplace_back(tok, fit);
+  }
+  int g = std::min(fit, m);
+  if (group_cap_ > 0) g = std::min(g, group_cap_);
+  return g;
+}
+
 void Engine::run_iteration(const int* orders, int m, const void* x, const void* y, size_t rows, bool on_device,
                            long iteration, double* loss, double* omegas) {
   CKF_CUDA(cudaSetDevice(d_.device));
@@ -436,7 +462,54 @@ void Engine::run_iteration(const int* orders, int m, const void* x, const void* 
   auto yk = [&](int k) { return yd ? yd + static_cast<size_t>(k) * mb * ycols * yelt : nullptr; };
   auto ok = [&](int k) { return orders + static_cast<size_t>(k) * d_.s; };
   impl_->begin_iteration(m, mb);
-  if (schedule_ == 0) {
+  size_t nloss = static_cast<size_t>(m);
+  bool resident = true;
+  for (size_t i = 0; i < d_.s; ++i) resident = resident && mine(owner_of_stage(static_cast<int>(i + 1)));
+  const int gsz = resident ? fused_group_size(m, mb) : 1;
+  if (gsz > 1) {
+    // All stages resident: microbatches sharing an execution order run as one
+    // fused forward + backward (GEMM M = group tokens instead of one microbatch).
+    // Same arithmetic as the reference's loop (pipeline.cpp:66-81): every token's
+    // loss gradient is still scaled by 1/(microbatch tokens), the weight gradients
+    // are summed over all tokens by the deferred W pass, and each group reports
+    // the sum of its members' mean losses.  Groups keep microbatch-index order
+    // within an order class; a class of non-contiguous microbatches (CheckFree+
+    // swapped_half) has its token rows gathered first.
+    std::vector<std::vector<int>> cls;
+    for (int k = 0; k < m; ++k) {
+      size_t c = 0;
+      for (; c < cls.size(); ++c)
+        if (std::equal(ok(k), ok(k) + d_.s, ok(cls[c][0]))) break;
+      if (c == cls.size()) cls.emplace_back();
+      cls[c].push_back(k);
+    }
+    std::vector<std::vector<int>> groups;
+    for (const auto& c : cls)
+      for (size_t i = 0; i < c.size(); i += static_cast<size_t>(gsz))
+        groups.emplace_back(c.begin() + static_cast<long>(i),
+                            c.begin() + static_cast<long>(std::min(c.size(), i + static_cast<size_t>(gsz))));
+    const size_t xrow = mb * xcols * xelt;
+    impl_->loss_rows = mb;
+    int woff = 0;
+    for (size_t j = 0; j < groups.size(); ++j) {
+      const auto& g = groups[j];
+      const char* xg = xk(g[0]);
+      bool contiguous = true;
+      for (size_t i = 1; i < g.size(); ++i) contiguous = contiguous && g[i] == g[0] + static_cast<int>(i);
+      if (!contiguous) {
+        char* gb = static_cast<char*>(ws(g.size() * xrow, 3));
+        for (size_t i = 0; i < g.size(); ++i)
+          CKF_CUDA(cudaMemcpyAsync(gb + i * xrow, xk(g[i]), xrow, cudaMemcpyDeviceToDevice, st_));
+        xg = gb;
+      }
+      impl_->wk = woff;
+      impl_->mb_forward(0, ok(g[0]), xg, nullptr, g.size() * mb, true, scal_ + j);
+      impl_->mb_backward(0, ok(g[0]), xg, g.size() * mb);
+      woff += static_cast<int>(g.size());
+    }
+    impl_->loss_rows = 0;
+    nloss = groups.size();
+  } else if (schedule_ == 0) {
     for (int k = 0; k < m; ++k) impl_->microbatch(k, ok(k), xk(k), yk(k), mb, true, scal_ + k);
   } else {
     // GPipe: all forwards, then all backwards in microbatch order (per-stage accumulation
@@ -461,13 +534,13 @@ void Engine::run_iteration(const int* orders, int m, const void* x, const void* 
                  "ncclAllReduce (data parallel)");
   }
   // mean loss in microbatch order, then *1/m (model.cpp:299-312, pipeline.cpp:82-83)
-  std::vector<double> losses(static_cast<size_t>(m));
+  std::vector<double> losses(nloss);
   const double inv = 1.0 / (static_cast<double>(m) * replicas_);
   for (size_t i = 0; i < d_.s; ++i) adam_group(stages_[i], stages_[i].lr, inv, scal_ + 2048 + i);
   adam_group(embed_, edge_lr, inv, scal_ + 3000);
   adam_group(deembed_, edge_lr, inv, scal_ + 3001);
   std::vector<double> om(d_.s);
-  CKF_CUDA(cudaMemcpyAsync(losses.data(), scal_, static_cast<size_t>(m) * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  CKF_CUDA(cudaMemcpyAsync(losses.data(), scal_, nloss * sizeof(double), cudaMemcpyDeviceToHost, st_));
   CKF_CUDA(cudaMemcpyAsync(om.data(), scal_ + 2048, d_.s * sizeof(double), cudaMemcpyDeviceToHost, st_));
   CKF_CUDA(cudaStreamSynchronize(st_));
   kt_collect();

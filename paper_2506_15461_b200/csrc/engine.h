@@ -97,7 +97,16 @@ struct BlockImpl {
     (void)rows;
   }
   virtual void flush_grads() {}
-  int wk = 0;  // position of the current microbatch within the iteration
+  // Device bytes one token of a fused microbatch group keeps live from its
+  // forward to its backward (activation cache over every resident layer, head
+  // logits, scratch).  0 = the block does not fuse microbatches.
+  virtual size_t group_bytes_per_token() const { return 0; }
+  // device bytes the block will still allocate this iteration (e.g. deferred-gradient inputs)
+  virtual size_t reserved_bytes() const { return 0; }
+  int wk = 0;  // position of the current microbatch within the iteration (in microbatches)
+  // Rows of ONE microbatch when a call carries a fused group of several (the
+  // loss and its gradient stay per-microbatch means, pipeline.cpp:66-83); 0 = rows.
+  size_t loss_rows = 0;
   // Predictions of forward(order, x) (MLP) into a device buffer of rows*out.
   virtual void predict(const int* order, const void* x, size_t rows, void* pred) = 0;
   Engine* eng;
@@ -157,6 +166,11 @@ class Engine {
     schedule_ = mode;
   }
   int schedule() const { return schedule_; }
+  // Microbatch fusion when every stage is resident on this rank (no stage hops):
+  // microbatches that share an execution order run as ONE forward + backward of
+  // up to group_cap microbatches (0 = as many as HBM allows, 1 = off).
+  void set_group_cap(int cap) { group_cap_ = cap < 0 ? 0 : cap; }
+  int group_cap() const { return group_cap_; }
   // move `bytes` of `buf` from rank src to rank dst (NCCL send/recv on the engine stream)
   void hop(void* buf, size_t bytes, int src, int dst);
   // Stage-boundary transfer between pipeline positions (codes: 0 = embedding,
@@ -204,6 +218,9 @@ class Engine {
   double* scal_ = nullptr;
   int rank_ = 0, nranks_ = 1;
   int schedule_ = 0;
+  int group_cap_ = 0;
+  std::vector<std::pair<size_t, int>> group_fit_;  // (microbatch tokens, fitted group size)
+  int fused_group_size(int m, size_t mb_rows);
   int replicas_ = 1, replica_ = 0;
   void* dp_comm_ = nullptr;  // ncclComm_t over the same pipeline rank of every replica
   bool log_hops_ = false;

@@ -217,9 +217,31 @@ struct LlamaBlock final : BlockImpl {
       const size_t have = (defer_m_ == m && defer_Mt_ == Mt && defer_) ? need : 0;  // already allocated
       want = need <= have + fr / 2;
     }
+    reserve_ = 0;
+    if (want) {
+      size_t layers = 0;
+      const Desc& D = eng->desc();
+      for (size_t i = 0; i < D.s; ++i)
+        if (eng->mine(eng->owner_of_stage(static_cast<int>(i + 1)))) layers += D.part[i].count();
+      const bool have = defer_m_ == m && defer_Mt_ == Mt && defer_;
+      reserve_ = have ? 0 : layers * static_cast<size_t>(m) * Mt * wrow_elems() * 2;
+    }
     defer_ = want;
     defer_m_ = want ? m : 1;
     defer_Mt_ = Mt;
+  }
+  size_t reserve_ = 0;
+  size_t reserved_bytes() const override { return reserve_; }
+  // per token of a fused group: the activation cache of every resident layer
+  // (cache(): h_in, h_mid, rstd1/2, lse, qkv, gu; the X inputs live in the
+  // deferred buffers), bf16 logits, and the per-call fp32 / bf16 scratch
+  size_t group_bytes_per_token() const override {
+    size_t layers = 0;
+    const Desc& D = eng->desc();
+    for (size_t i = 0; i < D.s; ++i)
+      if (eng->mine(eng->owner_of_stage(static_cast<int>(i + 1)))) layers += D.part[i].count();
+    const size_t per_layer = 8 * d + 8 + 4 * H + 6 * d + 4 * f + 8 * d + 4 * f;  // + X when not deferred
+    return layers * per_layer + 2 * V + 8 + 26 * d + 2 * std::max(d, f) + 4 * H + 64;
   }
 
   void flush_grads() override {
@@ -297,7 +319,8 @@ struct LlamaBlock final : BlockImpl {
     const Desc& D = eng->desc();
     cudaStream_t st = eng->stream();
     const size_t Mt = rows * T;
-    if (Mt > D.max_rows) raise(1, "microbatch tokens exceed the engine's max_rows (tokens per microbatch)");
+    const size_t Mmb = loss_rows ? loss_rows * T : Mt;  // tokens of ONE microbatch (fused groups carry several)
+    if (Mmb > D.max_rows) raise(1, "microbatch tokens exceed the engine's max_rows (tokens per microbatch)");
     const int* x = static_cast<const int*>(xv);
     const int Mi = static_cast<int>(Mt), di = static_cast<int>(d), Vi = static_cast<int>(V);
 
@@ -344,9 +367,9 @@ struct LlamaBlock final : BlockImpl {
     timed(KC_NORM, 0.0, Mt * d * 10.0, [&] { llama::rmsnorm_fwd(h, gF, Mt, d, xnF, rstdF, hF, st); });
     gemm(Mi, Vi, di, xnF, di, false, Einv, Vi, true, logits, Vi, tc::kStoreBF16);
     timed(KC_LOSS, 0.0, Mt * V * (train ? 6.0 : 2.0), [&] {
-      llama::xent_bf16(logits, lab, Mt, V, static_cast<float>(1.0 / static_cast<double>(Mt)), train ? 1 : 0,
+      llama::xent_bf16(logits, lab, Mt, V, static_cast<float>(1.0 / static_cast<double>(Mmb)), train ? 1 : 0,
                        row_loss, st);
-      llama::fold_mean(row_loss, Mt, 1.0 / static_cast<double>(Mt), loss_dev, st);
+      llama::fold_mean(row_loss, Mt, 1.0 / static_cast<double>(Mmb), loss_dev, st);  // sum of microbatch means
     });
     if (!train) return;
     // head backward (model.cpp:322-342): gE_inv += xnF^T dlogits, dh_final = rmsnorm'(dlogits E_inv^T)

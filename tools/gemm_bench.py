@@ -7,12 +7,16 @@ import torch
 import paper_2506_15461_b200  # noqa
 from paper_2506_15461_b200._native import check, lib
 
-SHAPES = [  # (name, M, N, K, a_mn, b_mn, epi)
-    ("qkv_fwd", 8192, 1536, 512, 0, 1, 0), ("o_fwd", 8192, 512, 512, 0, 1, 2), ("gu_fwd", 8192, 4096, 512, 0, 1, 0),
-    ("down_fwd", 8192, 512, 2048, 0, 1, 2), ("lmhead_fwd", 8192, 50304, 512, 0, 1, 0),
-    ("lmhead_dgrad", 8192, 512, 50304, 0, 0, 1), ("lmhead_wgrad", 512, 50304, 8192, 1, 1, 2),
-    ("gu_dgrad", 8192, 512, 4096, 0, 0, 1), ("gu_wgrad", 512, 4096, 8192, 1, 1, 2), ("qkv_wgrad", 512, 1536, 8192, 1, 1, 2),
-    ("sq4096", 4096, 4096, 4096, 0, 0, 0), ("sq8192", 8192, 8192, 8192, 0, 1, 0),
+SHAPES = [  # (name, M, N, K, a_mn, b_mn, epi): one fused LLaMA-124M step (65,536 tokens)
+    ("qkv_fwd", 65536, 1536, 512, 0, 1, 0), ("o_fwd", 65536, 512, 512, 0, 1, 2), ("gu_fwd", 65536, 4096, 512, 0, 1, 0),
+    ("down_fwd", 65536, 512, 2048, 0, 1, 2), ("down_dgrad", 65536, 2048, 512, 0, 0, 0),
+    ("gu_dgrad", 65536, 512, 4096, 0, 0, 1), ("o_dgrad", 65536, 512, 512, 0, 0, 0),
+    ("qkv_dgrad", 65536, 512, 1536, 0, 0, 1),
+    ("qkv_wgrad", 512, 1536, 65536, 1, 1, 2), ("o_wgrad", 512, 512, 65536, 1, 1, 2),
+    ("gu_wgrad", 512, 4096, 65536, 1, 1, 2), ("down_wgrad", 2048, 512, 65536, 1, 1, 2),
+    ("lmhead_fwd", 65536, 50304, 512, 0, 1, 0), ("lmhead_dgrad", 65536, 512, 50304, 0, 0, 1),
+    ("lmhead_wgrad", 512, 50304, 65536, 1, 1, 2),
+    ("sq8192", 8192, 8192, 8192, 0, 1, 0),
 ]
 
 def run(name, M, N, K, a_mn, b_mn, epi, bn=0, iters=20):
