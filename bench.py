@@ -260,6 +260,8 @@ def run_ours(args, w: dict):
             dist.barrier()
         torch.cuda.synchronize()
 
+    per_step = []  # device ms of every timed step, per timed pass (variance check)
+
     def timed(k, on_device, it0):
         evs = []
         for i in range(k):
@@ -271,6 +273,7 @@ def run_ours(args, w: dict):
             b.record(stream)
             evs.append((a, b))
         torch.cuda.synchronize()
+        per_step.append([round(a.elapsed_time(b), 3) for a, b in evs])
         return sum(a.elapsed_time(b) for a, b in evs)
 
     it = 1
@@ -374,6 +377,7 @@ def run_ours(args, w: dict):
             "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e_ms},
             "gpu_launches": launches, "roofline": roof, "step_tflops": step_tflops,
+            "step_ms": {"timed": per_step[0], "e2e": per_step[-1]},
             "flops_per_token": flops_per_token(w), "cpu_baseline": cpu, "clocks": clk.summary(),
             "recovery": rec, "recovery_sweep": sweep}
     print(json.dumps(line), flush=True)

@@ -134,6 +134,11 @@ int ckf_adam_device(int dtype, void* w, void* m, void* v, void* g, void* w_bf16,
  *   bn   = 0 (heuristic), 128 or 256: N tile.  Device pointers; lda/ldb % 8 == 0. */
 int ckf_gemm_bf16(int M, int N, int K, const void* A, int lda, int a_mn, const void* B, int ldb, int b_mn, void* C,
                   int ldc, int epi, float alpha, int bn, void* stream);
+/* Same GEMM with the fused SwiGLU epilogues of the LLaMA MLP (gemm_tc.h):
+ *   epi = 3 (forward, N = 2f, B MN-major): C = gu [M x 2f] bf16, aux = a [M x f] = silu(g) * u
+ *   epi = 4 (dgrad da = dY Wd^T, N = f, B K-major): aux = gu (read), C = dgu [M x 2f] bf16 (ldc = 2f) */
+int ckf_gemm_bf16_aux(int M, int N, int K, const void* A, int lda, int a_mn, const void* B, int ldb, int b_mn, void* C,
+                      int ldc, int epi, float alpha, int bn, void* aux, int ldaux, void* stream);
 
 /* Causal attention of the LLaMA block on device bf16 buffers: qkv [B*T x 3*H*hd]
  * (q | k | v column blocks), o [B*T x H*hd], lse [B*H*T] fp32 (natural log).

@@ -392,8 +392,16 @@ int ckf_adam_device(int dtype, void* w, void* m, void* v, void* g, void* w_bf16,
 
 int ckf_gemm_bf16(int M, int N, int K, const void* A, int lda, int a_mn, const void* B, int ldb, int b_mn, void* C,
                   int ldc, int epi, float alpha, int bn, void* stream) {
+  if (epi > 2) return guard([&] { ckf::raise(CKF_E_CONFIG, "gemm_bf16: epi must be 0, 1 or 2 (3/4: ckf_gemm_bf16_aux)"); });
+  return ckf_gemm_bf16_aux(M, N, K, A, lda, a_mn, B, ldb, b_mn, C, ldc, epi, alpha, bn, nullptr, 0, stream);
+}
+
+int ckf_gemm_bf16_aux(int M, int N, int K, const void* A, int lda, int a_mn, const void* B, int ldb, int b_mn, void* C,
+                      int ldc, int epi, float alpha, int bn, void* aux, int ldaux, void* stream) {
   return guard([&] {
-    if (epi < 0 || epi > 2) ckf::raise(CKF_E_CONFIG, "gemm_bf16: epi must be 0, 1 or 2");
+    if (epi < 0 || epi > 4) ckf::raise(CKF_E_CONFIG, "gemm_bf16: epi must be 0..4");
+    if ((epi == 3 && (a_mn || !b_mn)) || (epi == 4 && (a_mn || b_mn)))
+      ckf::raise(CKF_E_CONFIG, "gemm_bf16: SwiGLU epilogues take A K-major and B MN-major (3) / K-major (4)");
     if (bn != 0 && bn != 128 && bn != 256) ckf::raise(CKF_E_CONFIG, "gemm_bf16: bn must be 0, 128 or 256");
     ckf::tc::GemmDesc g;
     g.M = M;
@@ -410,6 +418,8 @@ int ckf_gemm_bf16(int M, int N, int K, const void* A, int lda, int a_mn, const v
     g.epi = epi;
     g.alpha = alpha;
     g.bn = bn;
+    g.aux = aux;
+    g.ldaux = ldaux;
     ckf::tc::gemm_bf16(g, static_cast<cudaStream_t>(stream));
   });
 }

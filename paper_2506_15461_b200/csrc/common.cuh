@@ -57,6 +57,19 @@ __host__ __device__ __forceinline__ uint64_t derive_key(uint64_t seed, uint64_t 
   return mix64(h ^ c);
 }
 
+// SwiGLU element math shared by the standalone kernels (llama_kernels.cu) and the
+// fused GEMM epilogues (gemm_tc.cu), so both produce the same bits.  Branch-free
+// (approximate reciprocal): the fused epilogue issues it from one warp per SM
+// sub-partition and needs the ILP.
+__device__ __forceinline__ float swiglu_sig(float g) { return __fdividef(1.f, 1.f + __expf(-g)); }
+__device__ __forceinline__ float swiglu_fwd1(float g, float u) { return g * swiglu_sig(g) * u; }
+// d = dL/da; writes dL/dg, dL/du
+__device__ __forceinline__ void swiglu_bwd1(float g, float u, float d, float& dg, float& du) {
+  const float sg = swiglu_sig(g);
+  dg = d * u * sg * (1.f + g * (1.f - sg));
+  du = d * g * sg;
+}
+
 __device__ __forceinline__ double counter_uniform_at(uint64_t key, uint64_t counter, double lo, double hi) {
   const uint64_t bits = mix64(key + counter * 0x9e3779b97f4a7c15ULL);
   const double u = __dmul_rn(static_cast<double>(bits >> 11), 0x1.0p-53);

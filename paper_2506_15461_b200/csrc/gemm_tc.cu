@@ -115,15 +115,19 @@ struct Params {
   int ldc;
   const float2* rope_tab;  // fused RoPE (bf16 epilogue): heads of 64 columns below rope_cols
   int rope_T, rope_cols;
+  int f;                   // kSwiGLU / kSwiGLUBwd: ffn width (column offset of the up half)
+  const __nv_bfloat16* gu; // kSwiGLUBwd: [M x 2f] gate/up activations (row pitch 2f)
 };
 
-template <int BN>
+template <int BN, int EPI>
 struct Cfg {
-  static constexpr int kStages = BN == 256 ? 4 : 6;
+  // kSwiGLUBwd trades one operand stage for 4 epilogue buffers per warp (g/u prefetch pairs)
+  static constexpr int kEpiBufs = EPI == kSwiGLUBwd ? 4 : 2;
+  static constexpr int kStages = (BN == 256 ? 4 : 6) - (EPI == kSwiGLUBwd ? 1 : 0);
   static constexpr uint32_t kBStage = BN * BK * 2;
   static constexpr uint32_t kStageBytes = kAStage + kBStage;
   static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
-  static constexpr uint32_t kEpiBytes = 4 * 2 * kStageBufBytes;
+  static constexpr uint32_t kEpiBytes = 4 * kEpiBufs * kStageBufBytes;
   static constexpr size_t kSmem = 1024 /*align slack*/ + kStages * kStageBytes + kEpiBytes + 256 /*barriers*/;
 };
 
@@ -132,12 +136,21 @@ struct Cfg {
 struct Unit {
   int mb, nb, tile, split, kb0, kb1;
 };
+// Tiles are rastered in bands of kRasterM M-tiles: within a band the M index runs
+// fastest, then N.  The ~148 tiles in flight then share a few A row-blocks and a
+// few B column-blocks, so each operand tile comes from HBM once and is re-read
+// from L2 (a plain M-fastest order over M = 65,536 tokens re-streams A from HBM
+// once per N-tile).
+constexpr int kRasterM = 16;
 __device__ __forceinline__ Unit unit_of(const Params& p, int u) {
   Unit w;
   w.split = u / p.tiles;
   w.tile = u % p.tiles;
-  w.mb = w.tile % p.nm;
-  w.nb = w.tile / p.nm;
+  const int band = w.tile / (kRasterM * p.nn);
+  const int in_band = w.tile - band * kRasterM * p.nn;
+  const int rows = min(kRasterM, p.nm - band * kRasterM);
+  w.mb = band * kRasterM + in_band % rows;
+  w.nb = in_band / rows;
   w.kb0 = w.split * p.kb_per_split;
   w.kb1 = min(p.nk, w.kb0 + p.kb_per_split);
   return w;
@@ -147,7 +160,7 @@ template <int BN, bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                 const __grid_constant__ CUtensorMap tmap_c, const __grid_constant__ CUtensorMap tmap_ws, Params p) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, EPI>;
   constexpr int ST = C::kStages;
   constexpr uint32_t IDESC = idesc_bf16_f32(BM, BN, A_MN, B_MN);
   extern __shared__ uint8_t smem_raw[];
@@ -159,14 +172,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + ST;
   uint64_t* tfull = empty + ST;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* lbar = tempty + 2;  // kSwiGLUBwd: per epilogue warp, one load barrier per g/u buffer pair
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lbar + 8);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmap_a);
     tma_prefetch(&tmap_b);
     tma_prefetch(&tmap_c);
-    if (p.splits > 1) tma_prefetch(&tmap_ws);
+    if (p.splits > 1 || EPI == kSwiGLU || EPI == kSwiGLUBwd) tma_prefetch(&tmap_ws);
   }
   if (warp == 1 && lane == 0) {
     for (int i = 0; i < ST; ++i) {
@@ -177,6 +191,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 4);
     }
+    for (int i = 0; i < 8; ++i) mbar_init(&lbar[i], 1);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<C::kTmemCols>(tmem_slot);
@@ -209,7 +224,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if constexpr (B_MN) {
 #pragma unroll
-            for (int c = 0; c < BN / 64; ++c) tma_load_2d(b + c * 8192, &tmap_b, &full[stage], w.nb * BN + c * 64, kb * BK);
+            for (int c = 0; c < BN / 64; ++c) {
+              int col = w.nb * BN + c * 64;
+              if constexpr (EPI == kSwiGLU)  // accumulator columns [0, BN/2) = gate, [BN/2, BN) = up
+                col = c * 64 < BN / 2 ? w.nb * (BN / 2) + c * 64 : p.f + w.nb * (BN / 2) + c * 64 - BN / 2;
+              tma_load_2d(b + c * 8192, &tmap_b, &full[stage], col, kb * BK);
+            }
           } else {
             tma_load_2d(b, &tmap_b, &full[stage], kb * BK, w.nb * BN);
           }
@@ -259,16 +279,148 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= 4) {
     // ---------------- epilogue: TMEM -> registers -> swizzled smem -> TMA store / reduce-add
     const int q = warp - 4;  // TMEM lane quarter (warp % 4)
-    uint8_t* stg = sEpi + q * 2 * kStageBufBytes;
+    uint8_t* stg = sEpi + q * C::kEpiBufs * kStageBufBytes;
     int acc = 0, sbuf = 0;
     uint32_t acc_phase = 0;
-    constexpr int CW = EPI == kStoreBF16 ? 64 : 32;  // columns per 128-byte staged row
+    constexpr int CW = EPI == kStoreF32 || EPI == kAccF32 ? 32 : 64;  // columns per 128-byte staged row
+    // one [32 rows x 64 bf16] chunk (packed pairs) -> swizzled staging -> TMA store
+    auto store_bf16_chunk = [&](const uint32_t* pk, const CUtensorMap* map, int x, int y) {
+      uint8_t* sb = stg + sbuf * kStageBufBytes;
+      if (lane == 0) bulk_wait_read<1>();
+      __syncwarp();
+      const uint32_t row = smem_u32(sb) + lane * 128;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) st_shared_v4(row + ((j ^ (lane & 7)) << 4), pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        if (y < p.M) tma_store_2d(map, sb, x, y);
+        bulk_commit();
+      }
+      sbuf ^= 1;
+    };
+    int cc = 0;               // kSwiGLUBwd: chunk counter of this warp's stream
+    bool first_unit = true;
     for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
       const Unit w = unit_of(p, u);
+      if constexpr (EPI == kSwiGLUBwd) {
+        if (first_unit && lane == 0) {  // first g/u chunk in flight before the accumulator is ready
+          const Unit w2 = w;
+          uint64_t* bar = &lbar[q * 2];
+          mbar_arrive_expect_tx(bar, 2 * kStageBufBytes);
+          tma_load_2d(stg, &tmap_ws, bar, w2.nb * BN, w2.mb * BM + q * 32);
+          tma_load_2d(stg + kStageBufBytes, &tmap_ws, bar, p.f + w2.nb * BN, w2.mb * BM + q * 32);
+        }
+        first_unit = false;
+      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t trow = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN);
       const int m0 = w.mb * BM + q * 32;
+      if constexpr (EPI == kSwiGLU) {
+        // gate columns [c0, c0+64) and the matching up columns [BN/2 + c0, ...)
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN / 2; c0 += 64) {
+          uint32_t g[64], v[64];
+          tmem_ld32(trow + c0, *reinterpret_cast<uint32_t(*)[32]>(&g[0]));
+          tmem_ld32(trow + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&g[32]));
+          tmem_ld32(trow + BN / 2 + c0, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+          tmem_ld32(trow + BN / 2 + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+          tmem_ld_wait();
+          if (c0 + 64 >= BN / 2) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+          }
+          const int n0 = w.nb * (BN / 2) + c0;
+          uint32_t pk[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) pk[j] = pack_bf16(__uint_as_float(g[2 * j]), __uint_as_float(g[2 * j + 1]));
+          store_bf16_chunk(pk, &tmap_c, n0, m0);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {  // g := bf16(g) as float (what the unfused kernel reads back)
+            g[2 * j] = pk[j] << 16;
+            g[2 * j + 1] = pk[j] & 0xffff0000u;
+          }
+#pragma unroll
+          for (int j = 0; j < 32; ++j) pk[j] = pack_bf16(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+          store_bf16_chunk(pk, &tmap_c, p.f + n0, m0);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float g0 = __uint_as_float(g[2 * j]), g1 = __uint_as_float(g[2 * j + 1]);
+            const float u0 = __uint_as_float(pk[j] << 16), u1 = __uint_as_float(pk[j] & 0xffff0000u);
+            pk[j] = pack_bf16(swiglu_fwd1(g0, u0), swiglu_fwd1(g1, u1));
+          }
+          store_bf16_chunk(pk, &tmap_ws, n0, m0);
+        }
+      } else if constexpr (EPI == kSwiGLUBwd) {
+        // g/u chunks arrive by TMA into this warp's buffer pairs, one chunk ahead of the
+        // math (chunk cc of the warp's stream uses pair cc & 1); dg/du overwrite them in
+        // place and leave by TMA store.  da = dY Wd^T never leaves the SM.
+        constexpr int NCH = BN / 64;
+        auto prefetch = [&](int uu, int c, int k) {  // lane 0
+          const Unit w2 = unit_of(p, uu);
+          uint8_t* gb = stg + (k & 1) * 2 * kStageBufBytes;
+          uint64_t* bar = &lbar[q * 2 + (k & 1)];
+          const int n0 = w2.nb * BN + c * 64, y = w2.mb * BM + q * 32;
+          mbar_arrive_expect_tx(bar, 2 * kStageBufBytes);
+          tma_load_2d(gb, &tmap_ws, bar, n0, y);
+          tma_load_2d(gb + kStageBufBytes, &tmap_ws, bar, p.f + n0, y);
+        };
+#pragma unroll 1
+        for (int c = 0; c < NCH; ++c, ++cc) {
+          const int n0 = w.nb * BN + c * 64;
+          if (lane == 0) {
+            const int nu = c + 1 < NCH ? u : u + static_cast<int>(gridDim.x);
+            if (nu < p.units) {
+              bulk_wait_read<0>();  // chunk cc-1's stores have left the pair we refill
+              prefetch(nu, c + 1 < NCH ? c + 1 : 0, cc + 1);
+            }
+          }
+          uint32_t r[64];
+          tmem_ld32(trow + c * 64, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+          tmem_ld32(trow + c * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+          tmem_ld_wait();
+          if (c + 1 == NCH) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+          }
+          mbar_wait(&lbar[q * 2 + (cc & 1)], (cc >> 1) & 1);
+          uint8_t* gb = stg + (cc & 1) * 2 * kStageBufBytes;
+          const uint32_t ga = smem_u32(gb) + lane * 128, ua = ga + kStageBufBytes;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint32_t off = (j ^ (lane & 7)) << 4;
+            const uint4 gq = ld_shared_v4(ga + off), uq = ld_shared_v4(ua + off);
+            const uint32_t gw[4] = {gq.x, gq.y, gq.z, gq.w}, uw[4] = {uq.x, uq.y, uq.z, uq.w};
+            uint32_t pg[4], pu[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              // da rounded to bf16 exactly as the unfused path stores it, then swiglu_bwd's arithmetic
+              const uint32_t dpk = pack_bf16(__uint_as_float(r[8 * j + 2 * e]), __uint_as_float(r[8 * j + 2 * e + 1]));
+              float dg0, du0, dg1, du1;
+              swiglu_bwd1(__uint_as_float(gw[e] << 16), __uint_as_float(uw[e] << 16), __uint_as_float(dpk << 16),
+                          dg0, du0);
+              swiglu_bwd1(__uint_as_float(gw[e] & 0xffff0000u), __uint_as_float(uw[e] & 0xffff0000u),
+                          __uint_as_float(dpk & 0xffff0000u), dg1, du1);
+              pg[e] = pack_bf16(dg0, dg1);
+              pu[e] = pack_bf16(du0, du1);
+            }
+            st_shared_v4(ga + off, pg[0], pg[1], pg[2], pg[3]);
+            st_shared_v4(ua + off, pu[0], pu[1], pu[2], pu[3]);
+          }
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            if (m0 < p.M && n0 < p.N) {
+              tma_store_2d(&tmap_c, gb, n0, m0);
+              tma_store_2d(&tmap_c, gb + kStageBufBytes, p.f + n0, m0);
+            }
+            bulk_commit();
+          }
+        }
+      } else {
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += CW) {
         uint32_t r[CW];
@@ -337,6 +489,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         sbuf ^= 1;
       }
+      }  // generic epilogues
       if (p.splits > 1) {
         // Deterministic split-K reduction (all units are co-resident: units <= grid):
         // 1) every warp publishes its stored partial rows, 2) once all 4*splits warps of the
@@ -450,13 +603,15 @@ int* split_flags(size_t n) {
 
 template <int BN, bool A_MN, bool B_MN, int EPI>
 void launch_t(const GemmDesc& g, int splits, cudaStream_t s) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, EPI>;
   const CUtensorMap ta = A_MN ? tma::make_2d_bf16(g.A, g.M, g.K, g.lda, 64, 64)
                               : tma::make_2d_bf16(g.A, g.K, g.M, g.lda, 64, BM);
   const CUtensorMap tb = B_MN ? tma::make_2d_bf16(g.B, g.N, g.K, g.ldb, 64, 64)
                               : tma::make_2d_bf16(g.B, g.K, g.N, g.ldb, 64, BN);
-  const CUtensorMap tcm = EPI == kStoreBF16 ? tma::make_2d_bf16(g.C, g.N, g.M, g.ldc, 64, 32)
-                                            : tma::make_2d_f32(g.C, g.N, g.M, g.ldc, 32, 32);
+  const bool c_bf16 = EPI == kStoreBF16 || EPI == kSwiGLU || EPI == kSwiGLUBwd;
+  // kSwiGLUBwd: C = dgu [M x 2f] although the GEMM's N is f
+  const CUtensorMap tcm = c_bf16 ? tma::make_2d_bf16(g.C, EPI == kSwiGLUBwd ? 2 * g.N : g.N, g.M, g.ldc, 64, 32)
+                                 : tma::make_2d_f32(g.C, g.N, g.M, g.ldc, 32, 32);
   Params p;
   p.M = g.M;
   p.N = g.N;
@@ -479,10 +634,21 @@ void launch_t(const GemmDesc& g, int splits, cudaStream_t s) {
   p.rope_tab = g.rope_tab;
   p.rope_T = g.rope_T;
   p.rope_cols = g.rope_cols;
+  p.f = EPI == kSwiGLU ? g.N / 2 : g.N;
+  p.gu = EPI == kSwiGLUBwd ? static_cast<const __nv_bfloat16*>(g.aux) : nullptr;
+  if constexpr (EPI == kSwiGLU || EPI == kSwiGLUBwd) {
+    if (!g.aux) raise(1, "gemm_bf16: the SwiGLU epilogues need aux");
+    if (EPI == kSwiGLU && (g.N % BN != 0 || (g.N / 2) % (BN / 2) != 0))
+      raise(1, "gemm_bf16: fused SwiGLU needs 2f % BN == 0");
+    if (EPI == kSwiGLUBwd && (g.N % 64 != 0 || g.ldc != 2 * g.N || (reinterpret_cast<uintptr_t>(g.aux) & 15)))
+      raise(1, "gemm_bf16: fused SwiGLU backward needs f % 64 == 0, ldc == 2f, 16-byte aligned gu");
+  }
   if (g.rope_tab && (EPI != kStoreBF16 || g.rope_T <= 0 || g.rope_cols % 64))
     raise(1, "gemm_bf16: fused RoPE needs the bf16 epilogue and 64-column heads");
-  const CUtensorMap twm = p.splits > 1 ? tma::make_2d_f32(p.ws, BN, static_cast<uint64_t>(p.units) * BM, BN, 32, 32)
-                                       : tcm;
+  const CUtensorMap twm = p.splits > 1    ? tma::make_2d_f32(p.ws, BN, static_cast<uint64_t>(p.units) * BM, BN, 32, 32)
+                          : EPI == kSwiGLU    ? tma::make_2d_bf16(g.aux, g.N / 2, g.M, g.ldaux, 64, 32)
+                          : EPI == kSwiGLUBwd ? tma::make_2d_bf16(g.aux, 2 * g.N, g.M, g.ldaux, 64, 32)
+                                              : tcm;
   auto kern = gemm_kernel<BN, A_MN, B_MN, EPI>;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
@@ -498,8 +664,12 @@ void launch_t(const GemmDesc& g, int splits, cudaStream_t s) {
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  static const bool pdl = [] {  // CKF_PDL=0: plain stream-ordered launches (A/B timing)
+    const char* v = std::getenv("CKF_PDL");
+    return !(v && v[0] == '0');
+  }();
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl ? 1 : 0;
   CKF_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, tcm, twm, p));
   CKF_LAUNCH_CHECK();
 }
@@ -513,6 +683,8 @@ void dispatch_bn(const GemmDesc& g, int splits, cudaStream_t s) {
   CKF_GEMM_EPIS(false, true)
   CKF_GEMM_EPIS(true, false)
   CKF_GEMM_EPIS(true, true)
+  CKF_GEMM_CASE(false, true, kSwiGLU)
+  CKF_GEMM_CASE(false, false, kSwiGLUBwd)
 #undef CKF_GEMM_EPIS
 #undef CKF_GEMM_CASE
   raise(1, "gemm_bf16: unsupported epilogue");
@@ -532,9 +704,10 @@ int pick_bn(int M, int N) {
 
 void gemm_bf16(const GemmDesc& g, cudaStream_t s) {
   if (g.M <= 0 || g.N <= 0 || g.K <= 0) return;
-  if (g.ldc % 4 != 0 && g.epi != kStoreBF16) raise(1, "gemm_bf16: fp32 C needs ldc % 4 == 0");
+  if (g.ldc % 4 != 0 && (g.epi == kStoreF32 || g.epi == kAccF32)) raise(1, "gemm_bf16: fp32 C needs ldc % 4 == 0");
   if (reinterpret_cast<uintptr_t>(g.C) % 16) raise(1, "gemm_bf16: C must be 16-byte aligned");
-  if (g.ldc % 8 != 0 && g.epi == kStoreBF16) raise(1, "gemm_bf16: bf16 C needs ldc % 8 == 0");
+  if (g.ldc % 8 != 0 && (g.epi == kStoreBF16 || g.epi == kSwiGLU || g.epi == kSwiGLUBwd))
+    raise(1, "gemm_bf16: bf16 C needs ldc % 8 == 0");
   int bn = g.bn ? g.bn : pick_bn(g.M, g.N);
   // Split-K (deterministic workspace reduction) only for the fp32-accumulate (weight-gradient)
   // epilogue, and only when no tile width fills the GPU: measured on B200

@@ -6,7 +6,13 @@
 
 namespace ckf::tc {
 
-enum Epi { kStoreBF16 = 0, kStoreF32 = 1, kAccF32 = 2 };
+// kSwiGLU (forward gate/up GEMM, B MN-major): output N = 2f columns [gate | up]; each
+//   tile computes matching gate and up columns, stores both (bf16, C = gu) and the
+//   activation a = silu(g) * u (bf16, aux [M x f], ld ldaux) from the bf16-rounded g, u.
+// kSwiGLUBwd (down-projection dgrad da = dh Wd^T, N = f): da never leaves the SM; the
+//   epilogue reads g, u from aux = gu [M x 2f] and stores dgu = [dg | du] (bf16, C, ldc 2f).
+//   Both are element-for-element the unfused swiglu_fwd / swiglu_bwd kernels.
+enum Epi { kStoreBF16 = 0, kStoreF32 = 1, kAccF32 = 2, kSwiGLU = 3, kSwiGLUBwd = 4 };
 
 // C[M,N] (epi) alpha * op(A) op(B), bf16 operands, fp32 accumulation.
 //   a_mn = false: A stored [M][lda] (K contiguous); true: A stored [K][lda] (M contiguous)
@@ -30,6 +36,8 @@ struct GemmDesc {
   // (j, j+32) pairs are rotated by rope_tab[(row % rope_T) * 32 + j] = (cos, sin)
   const float2* rope_tab = nullptr;
   int rope_T = 0, rope_cols = 0;
+  void* aux = nullptr;  // kSwiGLU: a (written); kSwiGLUBwd: gu (read)
+  int ldaux = 0;
 };
 
 void gemm_bf16(const GemmDesc& g, cudaStream_t s);

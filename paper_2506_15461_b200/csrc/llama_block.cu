@@ -262,8 +262,11 @@ struct LlamaBlock final : BlockImpl {
 
   // ------------------------------------------------------------ timed launch helpers
   void gemm(int M, int N, int K, const bf16* A, int lda, bool a_mn, const bf16* B, int ldb, bool b_mn, void* C,
-            int ldc, int epi, const float2* rope_tab = nullptr, int rope_cols = 0) {
+            int ldc, int epi, const float2* rope_tab = nullptr, int rope_cols = 0, void* aux = nullptr,
+            int ldaux = 0) {
     tc::GemmDesc g;
+    g.aux = aux;
+    g.ldaux = ldaux;
     g.rope_tab = rope_tab;
     g.rope_T = static_cast<int>(T);
     g.rope_cols = rope_cols;
@@ -281,7 +284,10 @@ struct LlamaBlock final : BlockImpl {
     g.epi = epi;
     eng->kt_begin();
     tc::gemm_bf16(g, eng->stream());
-    const double cb = epi == tc::kStoreBF16 ? 2.0 : epi == tc::kStoreF32 ? 4.0 : 8.0;
+    // bytes of C per output element: bf16 store; fp32 store; fp32 read+write; SwiGLU fwd
+    // (g, u stored + a: 3 bf16 per gate/up pair = 3 B per output); SwiGLU bwd (g, u read, dg, du written)
+    const double cb = epi == tc::kStoreBF16 ? 2.0 : epi == tc::kStoreF32 ? 4.0 : epi == tc::kAccF32 ? 8.0
+                    : epi == tc::kSwiGLU ? 3.0 : 8.0;
     eng->kt_end(KC_GEMM, 2.0 * M * N * K,
                 2.0 * (static_cast<double>(M) * K + static_cast<double>(K) * N) + cb * M * N);
   }
@@ -426,6 +432,12 @@ struct LlamaBlock final : BlockImpl {
     }
   }
 
+  // SwiGLU fused into the gate/up GEMM (forward) and the down-projection dgrad
+  // (backward) epilogues; CKF_FUSE_SWIGLU=0 selects the separate kernels (same bits)
+  static bool fuse_swiglu() {
+    const char* v = std::getenv("CKF_FUSE_SWIGLU");
+    return !(v && v[0] == '0');
+  }
   const bf16* wbf(int sid, size_t li) { return eng->stage(sid).wlp + li * off.total; }
   const float* wf(int sid, size_t li) { return static_cast<const float*>(eng->stage(sid).w) + li * off.total; }
   float* gf(int sid, size_t li) { return static_cast<float*>(eng->stage(sid).g) + li * off.total; }
@@ -455,8 +467,12 @@ struct LlamaBlock final : BlockImpl {
     });
     gemm(Mi, di, di, w.o, di, false, W + off.wo, di, true, h, di, tc::kAccF32);
     timed(KC_NORM, 0.0, Mt * d * 10.0, [&] { llama::rmsnorm_fwd(h, Wf + off.g2, Mt, d, w.xn2, c.rstd2, c.h_mid, st); });
-    gemm(Mi, 2 * fi, di, w.xn2, di, false, W + off.wgu, 2 * fi, true, c.gu, 2 * fi, tc::kStoreBF16);
-    timed(KC_NORM, 0.0, Mt * f * 6.0, [&] { llama::swiglu_fwd(c.gu, Mt, f, w.a, st); });
+    if (fuse_swiglu()) {  // a = silu(g) * u in the gate/up GEMM's epilogue
+      gemm(Mi, 2 * fi, di, w.xn2, di, false, W + off.wgu, 2 * fi, true, c.gu, 2 * fi, tc::kSwiGLU, nullptr, 0, w.a, fi);
+    } else {
+      gemm(Mi, 2 * fi, di, w.xn2, di, false, W + off.wgu, 2 * fi, true, c.gu, 2 * fi, tc::kStoreBF16);
+      timed(KC_NORM, 0.0, Mt * f * 6.0, [&] { llama::swiglu_fwd(c.gu, Mt, f, w.a, st); });
+    }
     gemm(Mi, di, fi, w.a, fi, false, W + off.wd, di, true, h, di, tc::kAccF32);
   }
 
@@ -474,8 +490,12 @@ struct LlamaBlock final : BlockImpl {
     // MLP half: h_out = h_mid + swiglu(xn2 Wgu) Wd
     bf16* da = sbf;
     if (now) gemm(fi, di, Mi, w.a, fi, true, w.dhd, di, true, G + off.wd, di, tc::kAccF32);   // gWd += a^T dh
-    gemm(Mi, fi, di, w.dhd, di, false, W + off.wd, di, false, da, fi, tc::kStoreBF16);       // da = dh Wd^T
-    timed(KC_NORM, 0.0, Mt * f * 10.0, [&] { llama::swiglu_bwd(c.gu, da, Mt, f, w.dgu, st); });
+    if (fuse_swiglu()) {  // da = dh Wd^T stays on chip; the epilogue emits dgu
+      gemm(Mi, fi, di, w.dhd, di, false, W + off.wd, di, false, w.dgu, 2 * fi, tc::kSwiGLUBwd, nullptr, 0, c.gu, 2 * fi);
+    } else {
+      gemm(Mi, fi, di, w.dhd, di, false, W + off.wd, di, false, da, fi, tc::kStoreBF16);  // da = dh Wd^T
+      timed(KC_NORM, 0.0, Mt * f * 10.0, [&] { llama::swiglu_bwd(c.gu, da, Mt, f, w.dgu, st); });
+    }
     if (now) gemm(di, 2 * fi, Mi, w.xn2, di, true, w.dgu, 2 * fi, true, G + off.wgu, 2 * fi, tc::kAccF32);
     gemm(Mi, di, 2 * fi, w.dgu, 2 * fi, false, W + off.wgu, 2 * fi, false, dxn, di, tc::kStoreF32);  // dxn2
     timed(KC_NORM, 0.0, Mt * d * 18.0, [&] {

@@ -254,7 +254,7 @@ __global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ gu, int ntok
     unpack8(*reinterpret_cast<const uint4*>(row + c), g);
     unpack8(*reinterpret_cast<const uint4*>(row + f + c), u);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) o[k] = g[k] / (1.f + __expf(-g[k])) * u[k];
+    for (int k = 0; k < 8; ++k) o[k] = swiglu_fwd1(g[k], u[k]);
     *reinterpret_cast<uint4*>(a + static_cast<size_t>(t) * f + c) = pack8(o);
   }
 }
@@ -271,11 +271,7 @@ __global__ void swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ gu, const __
     unpack8(*reinterpret_cast<const uint4*>(row + f + c), u);
     unpack8(*reinterpret_cast<const uint4*>(da + static_cast<size_t>(t) * f + c), dd);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const float sg = 1.f / (1.f + __expf(-g[k]));
-      dg[k] = dd[k] * u[k] * sg * (1.f + g[k] * (1.f - sg));
-      du[k] = dd[k] * g[k] * sg;
-    }
+    for (int k = 0; k < 8; ++k) swiglu_bwd1(g[k], u[k], dd[k], dg[k], du[k]);
     __nv_bfloat16* out = dgu + static_cast<size_t>(t) * 2 * f;
     *reinterpret_cast<uint4*>(out + c) = pack8(dg);
     *reinterpret_cast<uint4*>(out + f + c) = pack8(du);

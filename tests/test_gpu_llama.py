@@ -159,3 +159,21 @@ def test_fused_microbatch_groups_match_per_microbatch(cap):
     np.testing.assert_allclose(l2, l1, rtol=1e-3)
     for a, b in zip(d2, d1):
         assert _rel(a, b) < 5e-2
+
+
+def test_fused_swiglu_epilogues_bit_identical(monkeypatch):
+    # SwiGLU fused into the gate/up GEMM (fwd) and the down-projection dgrad (bwd)
+    # epilogues computes element-for-element what the separate kernels compute:
+    # identical losses and weights, bit for bit, over 2 iterations.
+    out = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("CKF_FUSE_SWIGLU", flag)
+        eng = _engine(SMALL, 2, lr=2e-3)
+        ls = [eng.run_iteration(build_schedule(2, False, SMALL.stages),
+                                LO.token_batch(29, 1, it, 4, SMALL.seq_len, SMALL.vocab), None, it)[0]
+              for it in (1, 2)]
+        out.append((ls, [eng.export_stage(s)[0] for s in range(1, SMALL.stages + 1)]))
+        eng.close()
+    assert out[0][0] == out[1][0]
+    for a, b in zip(out[0][1], out[1][1]):
+        assert np.array_equal(a, b)

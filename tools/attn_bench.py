@@ -15,7 +15,7 @@ def bench(fn, it=20):
     b.record(); torch.cuda.synchronize()
     return a.elapsed_time(b) / it
 
-for (B, T, H, hd) in [(8, 1024, 8, 64), (8, 1024, 16, 64), (2, 4096, 16, 128)]:
+for (B, T, H, hd) in [(64, 1024, 8, 64), (8, 1024, 8, 64), (64, 1024, 16, 64), (16, 4096, 16, 128)]:
     qkv = torch.randn(B * T, 3 * H * hd, device="cuda").bfloat16()
     o = torch.empty(B * T, H * hd, dtype=torch.bfloat16, device="cuda")
     lse = torch.empty(B * H * T, device="cuda")

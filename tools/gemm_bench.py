@@ -17,14 +17,20 @@ SHAPES = [  # (name, M, N, K, a_mn, b_mn, epi): one fused LLaMA-124M step (65,53
     ("lmhead_fwd", 65536, 50304, 512, 0, 1, 0), ("lmhead_dgrad", 65536, 512, 50304, 0, 0, 1),
     ("lmhead_wgrad", 512, 50304, 65536, 1, 1, 2),
     ("sq8192", 8192, 8192, 8192, 0, 1, 0),
+    # fused SwiGLU epilogues (compare with gu_fwd / down_dgrad above)
+    ("gu_fwd_swiglu", 65536, 4096, 512, 0, 1, 3), ("down_dgrad_swiglu", 65536, 2048, 512, 0, 0, 4),
 ]
 
 def run(name, M, N, K, a_mn, b_mn, epi, bn=0, iters=20):
     A = torch.randn((K, M) if a_mn else (M, K), device="cuda").bfloat16()
     B = torch.randn((K, N) if b_mn else (N, K), device="cuda").bfloat16()
-    C = torch.zeros((M, N), device="cuda", dtype=torch.bfloat16 if epi == 0 else torch.float32)
-    f = lambda: check(lib().ckf_gemm_bf16(M, N, K, A.data_ptr(), A.shape[1], a_mn, B.data_ptr(), B.shape[1], b_mn,
-                                          C.data_ptr(), N, epi, 1.0, bn, None))
+    cw = 2 * N if epi == 4 else N
+    C = torch.zeros((M, cw), device="cuda", dtype=torch.bfloat16 if epi in (0, 3, 4) else torch.float32)
+    aux = (torch.zeros((M, N // 2), device="cuda", dtype=torch.bfloat16) if epi == 3 else
+           torch.randn((M, 2 * N), device="cuda").bfloat16() if epi == 4 else None)
+    f = lambda: check(lib().ckf_gemm_bf16_aux(M, N, K, A.data_ptr(), A.shape[1], a_mn, B.data_ptr(), B.shape[1], b_mn,
+                                              C.data_ptr(), cw, epi, 1.0, bn, aux.data_ptr() if aux is not None else None,
+                                              aux.shape[1] if aux is not None else 0, None))
     a = A.t() if a_mn else A
     b = B if b_mn else B.t()
     g = lambda: torch.matmul(a, b)
@@ -42,8 +48,11 @@ def run(name, M, N, K, a_mn, b_mn, epi, bn=0, iters=20):
                       "ours_tflops": res["ours"][1], "cublas_ms": res["cublas"][0], "cublas_tflops": res["cublas"][1]}))
 
 if __name__ == "__main__":
+    only = [a for a in sys.argv[1:] if not a.startswith("-")]
     for s in SHAPES:
+        if only and s[0] not in only:
+            continue
         run(*s)
-        if len(sys.argv) > 1:
+        if "--bn" in sys.argv:
             for bn in (128, 256):
                 run(*s, bn=bn)
