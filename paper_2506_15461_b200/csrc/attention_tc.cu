@@ -327,221 +327,257 @@ __global__ void dsum_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bflo
   }
 }
 
-// writes 32 bf16 values (one 64-byte half of a 128-byte swizzled row segment) of row r into
-// a K-major SW128 operand buffer laid out as [K/64 chunks][128 rows][128 B]
-__device__ __forceinline__ void put32(uint32_t base, int r, int col0, const float (&v)[32]) {
-  const int ch = col0 >> 6, piece0 = (col0 & 63) >> 3;
-#pragma unroll
-  for (int p = 0; p < 4; ++p) {
-    const uint32_t w0 = pack_bf16(v[8 * p + 0], v[8 * p + 1]), w1 = pack_bf16(v[8 * p + 2], v[8 * p + 3]);
-    const uint32_t w2 = pack_bf16(v[8 * p + 4], v[8 * p + 5]), w3 = pack_bf16(v[8 * p + 6], v[8 * p + 7]);
-    st_shared_v4(base + ch * (128 * 128) + r * 128 + (((piece0 + p) ^ (r & 7)) << 4), w0, w1, w2, w3);
-  }
-}
-
+// Both backward kernels are persistent (one CTA per SM) over work units sorted
+// longest-first.  K/V (dK dV kernel) or Q/dO (dQ kernel) of a unit are
+// double-buffered in shared memory and the TMEM accumulators are double-
+// buffered (two sets), so a unit's set-up (operand loads, first S) and its
+// epilogue (TMEM -> global) overlap the neighbouring unit's tiles instead of
+// being paid once per CTA launch.  Tile / unit counters run across units, so
+// every mbarrier keeps a single phase sequence.
 struct SmemKV {  // dK / dV kernel
-  uint8_t k[kTile], v[kTile];
+  uint8_t k[2][kTile], v[2][kTile];
   uint8_t q[2][kTile], d_o[2][kTile];
   uint8_t p[kPBuf], ds[kPBuf];
-  float lse2[2][TQ], dsum[2][TQ];
-  uint64_t kv_full, qd_full[2], qd_empty[2], s_full, s_free, pd_full, pd_free, acc_full;
+  float lse[2][TQ], dsum[2][TQ];  // per-query lse / D of the tile, bulk-copied with its Q / dO
+  uint64_t kv_full[2], kv_empty[2], qd_full[2], qd_empty[2], s_full, s_free, pd_full, pd_free, acc_full[2],
+      acc_free[2];
   uint32_t tmem;
 };
 
-// One CTA per (128-key tile, sequence x head); loops over query tiles i >= key tile.
+// Unit u = (key tile kb, sequence x head bh), kb-major: kb = 0 (nqb query tiles) first.
 //   S^T = K Q^T, dP^T = V dO^T (TMEM)  ->  P^T = exp(S^T - lse), dS^T = P^T (dP^T - D)  (softmax warps,
 //   row = key)  ->  dV += P^T dO, dK += dS^T Q (TMEM accumulators, B operands MN-major from the tiles)
 __global__ void __launch_bounds__(kThreadsBwd, 1)
     attn_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
-                        const float* __restrict__ lse, const float* __restrict__ D, int T, int H,
+                        const float* __restrict__ lse, const float* __restrict__ D, int T, int H, int BH,
                         __nv_bfloat16* __restrict__ dqkv, float scale, float scale_log2, long long* __restrict__ dbg) {
   extern __shared__ uint8_t smem_raw[];
   const long long t_start = clock64();
+  long long tw[6] = {0, 0, 0, 0, 0, 0};  // CKF_ATTN_DEBUG phase cycles (softmax warp 4 lane 0 / MMA lane)
   SmemKV& sm = *reinterpret_cast<SmemKV*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nqb = T / TQ, kb = blockIdx.x;
-  const int bh = blockIdx.y, b = bh / H, h = bh % H;
-  const int row0 = b * T;
-  const int qcol = h * HD, kcol = (H + h) * HD, vcol = (2 * H + h) * HD, ocol = h * HD;
-  const int ntiles = nqb - kb;
+  const int nqb = T / TQ;
+  const int nunits = nqb * BH;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm_qkv);
     tma_prefetch(&tm_do);
   }
   if (warp == 1 && lane == 0) {
-    mbar_init(&sm.kv_full, 1);
     for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm.kv_full[i], 1);
+      mbar_init(&sm.kv_empty[i], 1);
       mbar_init(&sm.qd_full[i], 1);
       mbar_init(&sm.qd_empty[i], 1);
+      mbar_init(&sm.acc_full[i], 1);
+      mbar_init(&sm.acc_free[i], 8);
     }
     mbar_init(&sm.s_full, 1);
     mbar_init(&sm.s_free, 8);
     mbar_init(&sm.pd_full, 8);
     mbar_init(&sm.pd_free, 1);
-    mbar_init(&sm.acc_full, 1);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<512>(&sm.tmem);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = sm.tmem;  // S^T cols 0-127, dP^T 128-255, dV 256-319, dK 320-383
+  const uint32_t tmem = sm.tmem;  // S^T cols 0-127, dP^T 128-255, set 0: dV 256-319 dK 320-383, set 1: +128
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(&sm.kv_full, 2 * kTile);
-      tma_load_2d(sm.k, &tm_qkv, &sm.kv_full, kcol, row0 + kb * TK);
-      tma_load_2d(sm.v, &tm_qkv, &sm.kv_full, vcol, row0 + kb * TK);
-      for (int i = 0; i < ntiles; ++i) {
-        const int st = i & 1;
-        mbar_wait(&sm.qd_empty[st], ((i >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(&sm.qd_full[st], 2 * kTile);
-        const int qrow = row0 + (kb + i) * TQ;
-        tma_load_2d(sm.q[st], &tm_qkv, &sm.qd_full[st], qcol, qrow);
-        tma_load_2d(sm.d_o[st], &tm_do, &sm.qd_full[st], ocol, qrow);
+      int g = 0, lu = 0;
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lu) {
+        const int kb = u / BH, bh = u - kb * BH, b = bh / H, h = bh - b * H;
+        const int row0 = b * T;
+        const int kbuf = lu & 1;
+        mbar_wait(&sm.kv_empty[kbuf], ((lu >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&sm.kv_full[kbuf], 2 * kTile);
+        tma_load_2d(sm.k[kbuf], &tm_qkv, &sm.kv_full[kbuf], (H + h) * HD, row0 + kb * TK);
+        tma_load_2d(sm.v[kbuf], &tm_qkv, &sm.kv_full[kbuf], (2 * H + h) * HD, row0 + kb * TK);
+        for (int i = 0; i < nqb - kb; ++i, ++g) {
+          const int st = g & 1;
+          mbar_wait(&sm.qd_empty[st], ((g >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(&sm.qd_full[st], 2 * kTile + 2 * TQ * 4);
+          const int qrow = row0 + (kb + i) * TQ;
+          tma_load_2d(sm.q[st], &tm_qkv, &sm.qd_full[st], h * HD, qrow);
+          tma_load_2d(sm.d_o[st], &tm_do, &sm.qd_full[st], h * HD, qrow);
+          const size_t qo = static_cast<size_t>(bh) * T + (kb + i) * TQ;
+          bulk_load(sm.lse[st], lse + qo, TQ * 4, &sm.qd_full[st]);
+          bulk_load(sm.dsum[st], D + qo, TQ * 4, &sm.qd_full[st]);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t kIdS = idesc_bf16_f32(TK, TQ, false, false);  // [keys x q], K = hd
       constexpr uint32_t kIdA = idesc_bf16_f32(TK, HD, false, true);   // [keys x hd], K = q, B MN-major
-      mbar_wait(&sm.kv_full, 0);
-      const uint32_t ka = smem_u32(sm.k), va = smem_u32(sm.v);
       const uint32_t pa = smem_u32(sm.p), da = smem_u32(sm.ds);
-      auto issue_s = [&](int i) {  // S^T = K Q_i^T, dP^T = V dO_i^T
-        const int st = i & 1;
-        mbar_wait(&sm.qd_full[st], (i >> 1) & 1);
-        mbar_wait(&sm.s_free, (i & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t qa = smem_u32(sm.q[st]), oa = smem_u32(sm.d_o[st]);
+      int g = 0, lu = 0;
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lu) {
+        const int ntiles = nqb - u / BH;
+        const int kbuf = lu & 1;
+        const uint32_t acc = tmem + 256 + static_cast<uint32_t>(kbuf * 128);
+        mbar_wait(&sm.kv_full[kbuf], (lu >> 1) & 1);
+        const uint32_t ka = smem_u32(sm.k[kbuf]), va = smem_u32(sm.v[kbuf]);
+        auto issue_s = [&](int gi) {  // S^T = K Q^T, dP^T = V dO^T of global tile gi
+          const int st = gi & 1;
+          mbar_wait(&sm.qd_full[st], (gi >> 1) & 1);
+          mbar_wait(&sm.s_free, (gi & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t qa = smem_u32(sm.q[st]), oa = smem_u32(sm.d_o[st]);
 #pragma unroll
-        for (int k = 0; k < HD / 16; ++k) {
-          umma_bf16(tmem, umma_desc_sw128(ka + k * 32, 16, 1024), umma_desc_sw128(qa + k * 32, 16, 1024), kIdS,
-                    k > 0 ? 1u : 0u);
-          umma_bf16(tmem + 128, umma_desc_sw128(va + k * 32, 16, 1024), umma_desc_sw128(oa + k * 32, 16, 1024), kIdS,
-                    k > 0 ? 1u : 0u);
-        }
-        umma_commit(&sm.s_full);
-      };
-      issue_s(0);
-      for (int i = 0; i < ntiles; ++i) {
-        const int st = i & 1;
-        // the softmax warps release S^T/dP^T (s_free) as soon as they have loaded them, so the
-        // next tile's scores run on the tensor core while they still compute P / dS
-        if (i + 1 < ntiles) issue_s(i + 1);
-        mbar_wait(&sm.pd_full, i & 1);
-        tc_fence_after();
-        const uint32_t qa = smem_u32(sm.q[st]), oa = smem_u32(sm.d_o[st]);
+          for (int k = 0; k < HD / 16; ++k) {
+            umma_bf16(tmem, umma_desc_sw128(ka + k * 32, 16, 1024), umma_desc_sw128(qa + k * 32, 16, 1024), kIdS,
+                      k > 0 ? 1u : 0u);
+            umma_bf16(tmem + 128, umma_desc_sw128(va + k * 32, 16, 1024), umma_desc_sw128(oa + k * 32, 16, 1024),
+                      kIdS, k > 0 ? 1u : 0u);
+          }
+          umma_commit(&sm.s_full);
+        };
+        long long c0_ = clock64();
+        issue_s(g);  // overlaps the previous unit's epilogue
+        long long c1_ = clock64();
+        tw[0] += c1_ - c0_;
+        mbar_wait(&sm.acc_free[kbuf], ((lu >> 1) & 1) ^ 1);  // this accumulator set was drained two units ago
+        tw[1] += clock64() - c1_;
+        for (int i = 0; i < ntiles; ++i) {
+          const int gi = g + i, st = gi & 1;
+          c0_ = clock64();
+          if (i + 1 < ntiles) issue_s(gi + 1);
+          c1_ = clock64();
+          tw[0] += c1_ - c0_;
+          mbar_wait(&sm.pd_full, gi & 1);
+          tw[2] += clock64() - c1_;
+          tc_fence_after();
+          const uint32_t qa = smem_u32(sm.q[st]), oa = smem_u32(sm.d_o[st]);
 #pragma unroll
-        for (int k = 0; k < TQ / 16; ++k) {
-          const uint32_t aoff = (k >> 2) * (128 * 128) + (k & 3) * 32;
-          umma_bf16(tmem + 256, umma_desc_sw128(pa + aoff, 16, 1024), umma_desc_sw128(oa + k * 2048, 8192, 1024),
-                    kIdA, (i > 0 || k > 0) ? 1u : 0u);
-          umma_bf16(tmem + 320, umma_desc_sw128(da + aoff, 16, 1024), umma_desc_sw128(qa + k * 2048, 8192, 1024),
-                    kIdA, (i > 0 || k > 0) ? 1u : 0u);
+          for (int k = 0; k < TQ / 16; ++k) {
+            const uint32_t aoff = (k >> 2) * (128 * 128) + (k & 3) * 32;
+            umma_bf16(acc, umma_desc_sw128(pa + aoff, 16, 1024), umma_desc_sw128(oa + k * 2048, 8192, 1024), kIdA,
+                      (i > 0 || k > 0) ? 1u : 0u);
+            umma_bf16(acc + 64, umma_desc_sw128(da + aoff, 16, 1024), umma_desc_sw128(qa + k * 2048, 8192, 1024),
+                      kIdA, (i > 0 || k > 0) ? 1u : 0u);
+          }
+          umma_commit(&sm.pd_free);
+          umma_commit(&sm.qd_empty[st]);
         }
-        umma_commit(&sm.pd_free);
-        umma_commit(&sm.qd_empty[st]);
+        umma_commit(&sm.acc_full[kbuf]);
+        umma_commit(&sm.kv_empty[kbuf]);
+        g += ntiles;
       }
-      umma_commit(&sm.acc_full);
+      if (dbg) {
+        long long* d = dbg + 16 * blockIdx.x + 8;
+        d[0] = tw[0];  // issue_s incl. its qd_full / s_free waits
+        d[1] = tw[1];  // acc_free waits
+        d[2] = tw[2];  // pd_full waits
+        d[3] = clock64() - t_start;
+      }
     }
   } else if (warp >= 4) {
     const int sw = warp - 4, quarter = sw & 3, half = sw >> 2;
     const int r = quarter * 32 + lane;  // key row within the tile
     const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
-    long long w_bar = 0, w_s = 0, w_pd = 0, t_first = 0;
-    for (int i = 0; i < ntiles; ++i) {
-      const int st = i & 1;
-      const int q0 = (kb + i) * TQ;
-      // per-query lse / D of this tile staged in shared memory by the first 128 softmax threads
-      if (half == 0) {
-        sm.lse2[st][r] = lse[static_cast<size_t>(bh) * T + q0 + r] * kLog2e;
-        sm.dsum[st][r] = D[static_cast<size_t>(bh) * T + q0 + r];
-      }
-      const long long t0 = clock64();
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-      const long long t1 = clock64();
-      mbar_wait(&sm.s_full, i & 1);
-      const long long t2 = clock64();
-      if (i == 0) t_first = t2 - t_start;
-      tc_fence_after();
-      mbar_wait(&sm.pd_free, (i & 1) ^ 1);  // the previous tile's dV/dK MMAs have read P / dS
-      const long long t3 = clock64();
-      w_bar += t1 - t0;
-      w_s += t2 - t1;
-      w_pd += t3 - t2;
-      const uint32_t pbase = smem_u32(sm.p), dbase = smem_u32(sm.ds);
-#pragma unroll 1
-      for (int c0 = half * 64; c0 < half * 64 + 64; c0 += 32) {
-        uint32_t us[32], ud[32];
-        tmem_ld32(trow + c0, us);
-        tmem_ld32(trow + 128 + c0, ud);
+    const uint32_t pbase = smem_u32(sm.p), dbase = smem_u32(sm.ds);
+    const size_t ld = static_cast<size_t>(3) * H * HD;
+    int g = 0, lu = 0;
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lu) {
+      const int kb = u / BH, bh = u - kb * BH, b = bh / H, h = bh - b * H;
+      const int ntiles = nqb - kb;
+      for (int i = 0; i < ntiles; ++i) {
+        const int gi = g + i, st = gi & 1;
+        const long long a0 = clock64();
+        mbar_wait(&sm.s_full, gi & 1);
+        mbar_wait(&sm.qd_full[st], (gi >> 1) & 1);  // (already complete) makes the bulk-copied lse / D visible
+        tc_fence_after();
+        const long long a1 = clock64();
+        // this thread's 64 columns of S^T and dP^T in one go; the TMEM is released right away
+        // so the next tile's S^T / dP^T MMAs start while P / dS are computed from registers
+        uint32_t us[64], ud[64];
+        tmem_ld32(trow + half * 64, *reinterpret_cast<uint32_t(*)[32]>(&us[0]));
+        tmem_ld32(trow + half * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&us[32]));
+        tmem_ld32(trow + 128 + half * 64, *reinterpret_cast<uint32_t(*)[32]>(&ud[0]));
+        tmem_ld32(trow + 128 + half * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&ud[32]));
         tmem_ld_wait();
-        if (c0 == half * 64 + 32) {  // last TMEM read of this tile: let the next S^T / dP^T start
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&sm.s_free);
-        }
-        float pv[32], dv[32];
-        const float4* l4 = reinterpret_cast<const float4*>(&sm.lse2[st][c0]);
-        const float4* d4 = reinterpret_cast<const float4*>(&sm.dsum[st][c0]);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.s_free);
+        mbar_wait(&sm.pd_free, (gi & 1) ^ 1);  // the previous tile's dV/dK MMAs have read P / dS
+        const long long a2 = clock64();
+        tw[0] += a1 - a0;
+        tw[1] += a2 - a1;
+        const uint32_t rowoff = static_cast<uint32_t>(half * (128 * 128) + r * 128);
 #pragma unroll
-        for (int t4 = 0; t4 < 8; ++t4) {  // 128-bit broadcast reads of the per-query lse / D
-          const float4 lv = l4[t4], dvv = d4[t4];
-          const float la[4] = {lv.x, lv.y, lv.z, lv.w}, da[4] = {dvv.x, dvv.y, dvv.z, dvv.w};
+        for (int g8 = 0; g8 < 8; ++g8) {  // 8 columns (queries) at a time: P^T, dS^T -> bf16 -> swizzled smem
+          const int c = half * 64 + 8 * g8;
+          const float4 la = *reinterpret_cast<const float4*>(&sm.lse[st][c]);
+          const float4 lb = *reinterpret_cast<const float4*>(&sm.lse[st][c + 4]);
+          const float4 da4 = *reinterpret_cast<const float4*>(&sm.dsum[st][c]);
+          const float4 db4 = *reinterpret_cast<const float4*>(&sm.dsum[st][c + 4]);
+          const float lq[8] = {la.x, la.y, la.z, la.w, lb.x, lb.y, lb.z, lb.w};
+          const float dq8[8] = {da4.x, da4.y, da4.z, da4.w, db4.x, db4.y, db4.z, db4.w};
+          float pv[8], dv[8];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int t = 4 * t4 + e;
-            const float p = ex2(fmaf(__uint_as_float(us[t]), scale_log2, -la[e]));
-            pv[t] = p;
-            dv[t] = p * (__uint_as_float(ud[t]) - da[e]);
+          for (int e = 0; e < 8; ++e) {
+            const float p = ex2(fmaf(__uint_as_float(us[8 * g8 + e]), scale_log2, -lq[e] * kLog2e));
+            pv[e] = p;
+            dv[e] = p * (__uint_as_float(ud[8 * g8 + e]) - dq8[e]);
           }
-        }
-        if (i == 0) {  // diagonal tile: a query before the key sees nothing
+          if (i == 0) {  // diagonal tile: a query before the key sees nothing
 #pragma unroll
-          for (int t = 0; t < 32; ++t)
-            if (c0 + t < r) pv[t] = dv[t] = 0.f;
+            for (int e = 0; e < 8; ++e)
+              if (c + e < r) pv[e] = dv[e] = 0.f;
+          }
+          const uint32_t off = rowoff + ((g8 ^ (r & 7)) << 4);
+          st_shared_v4(pbase + off, pack_bf16(pv[0], pv[1]), pack_bf16(pv[2], pv[3]), pack_bf16(pv[4], pv[5]),
+                       pack_bf16(pv[6], pv[7]));
+          st_shared_v4(dbase + off, pack_bf16(dv[0], dv[1]), pack_bf16(dv[2], dv[3]), pack_bf16(dv[4], dv[5]),
+                       pack_bf16(dv[6], dv[7]));
         }
-        put32(pbase, r, c0, pv);
-        put32(dbase, r, c0, dv);
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.pd_full);
+        tw[2] += clock64() - a2;
+        tw[4] += 1;
       }
-      fence_proxy_async();
+      g += ntiles;
+      // ---------------- epilogue of this unit: column half 0 -> dV, half 1 -> dK (x scale)
+      const int aset = lu & 1;
+      const long long e0 = clock64();
+      mbar_wait(&sm.acc_full[aset], (lu >> 1) & 1);
+      tc_fence_after();
+      const int row0 = b * T;
+      __nv_bfloat16* dst = dqkv + (static_cast<size_t>(row0) + kb * TK + r) * ld +
+                           static_cast<size_t>(half ? (H + h) * HD : (2 * H + h) * HD);
+      const float mul = half ? scale : 1.f;
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        uint32_t w32[32];
+        tmem_ld32(trow + 256 + aset * 128 + half * 64 + hh * 32, w32);
+        tmem_ld_wait();
+#pragma unroll
+        for (int piece = 0; piece < 4; ++piece) {
+          uint4 w;
+          w.x = pack_bf16(__uint_as_float(w32[8 * piece + 0]) * mul, __uint_as_float(w32[8 * piece + 1]) * mul);
+          w.y = pack_bf16(__uint_as_float(w32[8 * piece + 2]) * mul, __uint_as_float(w32[8 * piece + 3]) * mul);
+          w.z = pack_bf16(__uint_as_float(w32[8 * piece + 4]) * mul, __uint_as_float(w32[8 * piece + 5]) * mul);
+          w.w = pack_bf16(__uint_as_float(w32[8 * piece + 6]) * mul, __uint_as_float(w32[8 * piece + 7]) * mul);
+          reinterpret_cast<uint4*>(dst + hh * 32)[piece] = w;
+        }
+      }
+      tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.pd_full);
-      asm volatile("bar.sync 1, 256;" ::: "memory");  // lse/D slots of this stage are reused two tiles later
+      if (lane == 0) mbar_arrive(&sm.acc_free[aset]);
+      tw[3] += clock64() - e0;
     }
     if (dbg && threadIdx.x == 128) {
-      long long* d = dbg + 8 * (blockIdx.y * gridDim.x + blockIdx.x);
-      d[0] = ntiles;
-      d[1] = t_first;
-      d[2] = w_s;
-      d[3] = w_pd;
-      d[4] = clock64() - t_start;
-      d[5] = w_bar;
-      d[6] = t_start;
-    }
-    // ---------------- epilogue: column half 0 -> dV, half 1 -> dK (x scale)
-    mbar_wait(&sm.acc_full, 0);
-    tc_fence_after();
-    const size_t ld = static_cast<size_t>(3) * H * HD;
-    const int which = half;
-    __nv_bfloat16* dst = dqkv + (static_cast<size_t>(row0) + kb * TK + r) * ld + static_cast<size_t>(which ? kcol : vcol);
-    const float mul = which ? scale : 1.f;
-#pragma unroll
-    for (int hh = 0; hh < 2; ++hh) {
-      uint32_t u[32];
-      tmem_ld32(trow + 256 + which * 64 + hh * 32, u);
-      tmem_ld_wait();
-#pragma unroll
-      for (int piece = 0; piece < 4; ++piece) {
-        uint4 w;
-        w.x = pack_bf16(__uint_as_float(u[8 * piece + 0]) * mul, __uint_as_float(u[8 * piece + 1]) * mul);
-        w.y = pack_bf16(__uint_as_float(u[8 * piece + 2]) * mul, __uint_as_float(u[8 * piece + 3]) * mul);
-        w.z = pack_bf16(__uint_as_float(u[8 * piece + 4]) * mul, __uint_as_float(u[8 * piece + 5]) * mul);
-        w.w = pack_bf16(__uint_as_float(u[8 * piece + 6]) * mul, __uint_as_float(u[8 * piece + 7]) * mul);
-        reinterpret_cast<uint4*>(dst + hh * 32)[piece] = w;
-      }
+      long long* d = dbg + 16 * blockIdx.x;
+      d[0] = tw[4];  // tiles
+      d[1] = tw[0];  // s_full waits
+      d[2] = tw[1];  // pd_free waits
+      d[3] = tw[2];  // softmax compute + P/dS stores
+      d[4] = tw[3];  // unit epilogues (incl. acc_full waits)
+      d[5] = clock64() - t_start;
     }
   }
   tc_fence_before();
@@ -551,157 +587,192 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
 }
 
 struct SmemQ {  // dQ kernel
-  uint8_t q[kTile], d_o[kTile];
+  uint8_t q[2][kTile], d_o[2][kTile];
   uint8_t k[2][kTile], v[2][kTile];
   uint8_t ds[kPBuf];
-  uint64_t qd_full, kv_full[2], kv_empty[2], s_full, s_free, ds_full, ds_free, acc_full;
+  float lse[2][TQ], dsum[2][TQ];  // per-query lse / D of the unit, bulk-copied with its Q / dO
+  uint64_t qd_full[2], qd_empty[2], kv_full[2], kv_empty[2], s_full, s_free, ds_full, ds_free, acc_full[2],
+      acc_free[2];
   uint32_t tmem;
 };
 
-// One CTA per (128-query tile, sequence x head); loops over key tiles j <= query tile.
+// Unit u = (query tile qb, sequence x head bh), longest (qb = nqb - 1) first.
 //   S = Q K^T, dP = dO V^T (TMEM) -> dS = P (dP - D) (softmax warps, row = query) -> dQ += dS K
 __global__ void __launch_bounds__(kThreadsBwd, 1)
     attn_dq_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
-                      const float* __restrict__ lse, const float* __restrict__ D, int T, int H,
+                      const float* __restrict__ lse, const float* __restrict__ D, int T, int H, int BH,
                       __nv_bfloat16* __restrict__ dqkv, float scale, float scale_log2) {
   extern __shared__ uint8_t smem_raw[];
   SmemQ& sm = *reinterpret_cast<SmemQ*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = T / TQ;
-  const int qb = nqb - 1 - static_cast<int>(blockIdx.x);
-  const int bh = blockIdx.y, b = bh / H, h = bh % H;
-  const int row0 = b * T;
-  const int qcol = h * HD, kcol = (H + h) * HD, vcol = (2 * H + h) * HD, ocol = h * HD;
-  const int nkb = qb + 1;
+  const int nunits = nqb * BH;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm_qkv);
     tma_prefetch(&tm_do);
   }
   if (warp == 1 && lane == 0) {
-    mbar_init(&sm.qd_full, 1);
     for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm.qd_full[i], 1);
+      mbar_init(&sm.qd_empty[i], 1);
       mbar_init(&sm.kv_full[i], 1);
       mbar_init(&sm.kv_empty[i], 1);
+      mbar_init(&sm.acc_full[i], 1);
+      mbar_init(&sm.acc_free[i], 8);
     }
     mbar_init(&sm.s_full, 1);
     mbar_init(&sm.s_free, 8);
     mbar_init(&sm.ds_full, 8);
     mbar_init(&sm.ds_free, 1);
-    mbar_init(&sm.acc_full, 1);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<512>(&sm.tmem);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = sm.tmem;  // S cols 0-127, dP 128-255, dQ 256-319
+  const uint32_t tmem = sm.tmem;  // S cols 0-127, dP 128-255, dQ set 0: 256-319, set 1: 320-383
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(&sm.qd_full, 2 * kTile);
-      tma_load_2d(sm.q, &tm_qkv, &sm.qd_full, qcol, row0 + qb * TQ);
-      tma_load_2d(sm.d_o, &tm_do, &sm.qd_full, ocol, row0 + qb * TQ);
-      for (int j = 0; j < nkb; ++j) {
-        const int st = j & 1;
-        mbar_wait(&sm.kv_empty[st], ((j >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(&sm.kv_full[st], 2 * kTile);
-        tma_load_2d(sm.k[st], &tm_qkv, &sm.kv_full[st], kcol, row0 + j * TK);
-        tma_load_2d(sm.v[st], &tm_qkv, &sm.kv_full[st], vcol, row0 + j * TK);
+      int g = 0, lu = 0;
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lu) {
+        const int qi = u / BH, bh = u - qi * BH, b = bh / H, h = bh - b * H;
+        const int qb = nqb - 1 - qi, row0 = b * T;
+        const int qbuf = lu & 1;
+        mbar_wait(&sm.qd_empty[qbuf], ((lu >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&sm.qd_full[qbuf], 2 * kTile + 2 * TQ * 4);
+        tma_load_2d(sm.q[qbuf], &tm_qkv, &sm.qd_full[qbuf], h * HD, row0 + qb * TQ);
+        tma_load_2d(sm.d_o[qbuf], &tm_do, &sm.qd_full[qbuf], h * HD, row0 + qb * TQ);
+        const size_t qo = static_cast<size_t>(bh) * T + qb * TQ;
+        bulk_load(sm.lse[qbuf], lse + qo, TQ * 4, &sm.qd_full[qbuf]);
+        bulk_load(sm.dsum[qbuf], D + qo, TQ * 4, &sm.qd_full[qbuf]);
+        for (int j = 0; j <= qb; ++j, ++g) {
+          const int st = g & 1;
+          mbar_wait(&sm.kv_empty[st], ((g >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(&sm.kv_full[st], 2 * kTile);
+          tma_load_2d(sm.k[st], &tm_qkv, &sm.kv_full[st], (H + h) * HD, row0 + j * TK);
+          tma_load_2d(sm.v[st], &tm_qkv, &sm.kv_full[st], (2 * H + h) * HD, row0 + j * TK);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t kIdS = idesc_bf16_f32(TQ, TK, false, false);  // [q x keys], K = hd
       constexpr uint32_t kIdQ = idesc_bf16_f32(TQ, HD, false, true);   // [q x hd], K = keys, B MN-major
-      mbar_wait(&sm.qd_full, 0);
-      const uint32_t qa = smem_u32(sm.q), oa = smem_u32(sm.d_o), da = smem_u32(sm.ds);
-      auto issue_s = [&](int j) {  // S = Q K_j^T, dP = dO V_j^T
-        const int st = j & 1;
-        mbar_wait(&sm.kv_full[st], (j >> 1) & 1);
-        mbar_wait(&sm.s_free, (j & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t ka = smem_u32(sm.k[st]), va = smem_u32(sm.v[st]);
+      const uint32_t da = smem_u32(sm.ds);
+      int g = 0, lu = 0;
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lu) {
+        const int nkb = nqb - u / BH;  // qb + 1
+        const int qbuf = lu & 1;
+        const uint32_t acc = tmem + 256 + static_cast<uint32_t>(qbuf * 64);
+        mbar_wait(&sm.qd_full[qbuf], (lu >> 1) & 1);
+        const uint32_t qa = smem_u32(sm.q[qbuf]), oa = smem_u32(sm.d_o[qbuf]);
+        auto issue_s = [&](int gj) {  // S = Q K^T, dP = dO V^T of global tile gj
+          const int st = gj & 1;
+          mbar_wait(&sm.kv_full[st], (gj >> 1) & 1);
+          mbar_wait(&sm.s_free, (gj & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t ka = smem_u32(sm.k[st]), va = smem_u32(sm.v[st]);
 #pragma unroll
-        for (int k = 0; k < HD / 16; ++k) {
-          umma_bf16(tmem, umma_desc_sw128(qa + k * 32, 16, 1024), umma_desc_sw128(ka + k * 32, 16, 1024), kIdS,
-                    k > 0 ? 1u : 0u);
-          umma_bf16(tmem + 128, umma_desc_sw128(oa + k * 32, 16, 1024), umma_desc_sw128(va + k * 32, 16, 1024), kIdS,
-                    k > 0 ? 1u : 0u);
+          for (int k = 0; k < HD / 16; ++k) {
+            umma_bf16(tmem, umma_desc_sw128(qa + k * 32, 16, 1024), umma_desc_sw128(ka + k * 32, 16, 1024), kIdS,
+                      k > 0 ? 1u : 0u);
+            umma_bf16(tmem + 128, umma_desc_sw128(oa + k * 32, 16, 1024), umma_desc_sw128(va + k * 32, 16, 1024),
+                      kIdS, k > 0 ? 1u : 0u);
+          }
+          umma_commit(&sm.s_full);
+        };
+        issue_s(g);
+        mbar_wait(&sm.acc_free[qbuf], ((lu >> 1) & 1) ^ 1);
+        for (int j = 0; j < nkb; ++j) {
+          const int gj = g + j, st = gj & 1;
+          if (j + 1 < nkb) issue_s(gj + 1);  // overlaps the softmax warps' dS of tile j
+          mbar_wait(&sm.ds_full, gj & 1);
+          tc_fence_after();
+          const uint32_t ka = smem_u32(sm.k[st]);
+#pragma unroll
+          for (int k = 0; k < TK / 16; ++k)
+            umma_bf16(acc, umma_desc_sw128(da + (k >> 2) * (128 * 128) + (k & 3) * 32, 16, 1024),
+                      umma_desc_sw128(ka + k * 2048, 8192, 1024), kIdQ, (j > 0 || k > 0) ? 1u : 0u);
+          umma_commit(&sm.ds_free);
+          umma_commit(&sm.kv_empty[st]);
         }
-        umma_commit(&sm.s_full);
-      };
-      issue_s(0);
-      for (int j = 0; j < nkb; ++j) {
-        const int st = j & 1;
-        if (j + 1 < nkb) issue_s(j + 1);  // overlaps the softmax warps' dS of tile j
-        mbar_wait(&sm.ds_full, j & 1);
-        tc_fence_after();
-        const uint32_t ka = smem_u32(sm.k[st]);
-#pragma unroll
-        for (int k = 0; k < TK / 16; ++k)
-          umma_bf16(tmem + 256, umma_desc_sw128(da + (k >> 2) * (128 * 128) + (k & 3) * 32, 16, 1024),
-                    umma_desc_sw128(ka + k * 2048, 8192, 1024), kIdQ, (j > 0 || k > 0) ? 1u : 0u);
-        umma_commit(&sm.ds_free);
-        umma_commit(&sm.kv_empty[st]);
+        umma_commit(&sm.acc_full[qbuf]);
+        umma_commit(&sm.qd_empty[qbuf]);
+        g += nkb;
       }
-      umma_commit(&sm.acc_full);
     }
   } else if (warp >= 4) {
     const int sw = warp - 4, quarter = sw & 3, half = sw >> 2;
     const int r = quarter * 32 + lane;
-    const int q = qb * TQ + r;
     const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
-    const float l2 = lse[static_cast<size_t>(bh) * T + q] * kLog2e;
-    const float dq = D[static_cast<size_t>(bh) * T + q];
     const uint32_t dbase = smem_u32(sm.ds);
-    for (int j = 0; j < nkb; ++j) {
-      mbar_wait(&sm.s_full, j & 1);
-      tc_fence_after();
-      mbar_wait(&sm.ds_free, (j & 1) ^ 1);
-#pragma unroll 1
-      for (int c0 = half * 64; c0 < half * 64 + 64; c0 += 32) {
-        uint32_t us[32], ud[32];
-        tmem_ld32(trow + c0, us);
-        tmem_ld32(trow + 128 + c0, ud);
-        tmem_ld_wait();
-        if (c0 == half * 64 + 32) {  // last TMEM read of this tile: let the next S / dP start
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&sm.s_free);
-        }
-        float dv[32];
-#pragma unroll
-        for (int t = 0; t < 32; ++t) {
-          const float p = ex2(fmaf(__uint_as_float(us[t]), scale_log2, -l2));
-          dv[t] = p * (__uint_as_float(ud[t]) - dq);
-        }
-        if (j == qb) {  // diagonal tile: keys after the query are invisible
-#pragma unroll
-          for (int t = 0; t < 32; ++t)
-            if (c0 + t > r) dv[t] = 0.f;
-        }
-        put32(dbase, r, c0, dv);
-      }
-      fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.ds_full);
-    }
-    mbar_wait(&sm.acc_full, 0);
-    tc_fence_after();
     const size_t ld = static_cast<size_t>(3) * H * HD;
-    __nv_bfloat16* qrow = dqkv + (static_cast<size_t>(row0) + q) * ld + static_cast<size_t>(qcol) + half * 32;
-    uint32_t u[32];
-    tmem_ld32(trow + 256 + half * 32, u);
-    tmem_ld_wait();
+    int g = 0, lu = 0;
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lu) {
+      const int qi = u / BH, bh = u - qi * BH, b = bh / H, h = bh - b * H;
+      const int qb = nqb - 1 - qi, nkb = qb + 1;
+      const int q = qb * TQ + r;
+      mbar_wait(&sm.qd_full[lu & 1], (lu >> 1) & 1);  // (complete before S) lse / D of the unit's queries
+      const float l2 = sm.lse[lu & 1][r] * kLog2e;
+      const float dq = sm.dsum[lu & 1][r];
+      for (int j = 0; j < nkb; ++j) {
+        const int gj = g + j;
+        mbar_wait(&sm.s_full, gj & 1);
+        tc_fence_after();
+        uint32_t us[64], ud[64];
+        tmem_ld32(trow + half * 64, *reinterpret_cast<uint32_t(*)[32]>(&us[0]));
+        tmem_ld32(trow + half * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&us[32]));
+        tmem_ld32(trow + 128 + half * 64, *reinterpret_cast<uint32_t(*)[32]>(&ud[0]));
+        tmem_ld32(trow + 128 + half * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&ud[32]));
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.s_free);  // the next S / dP may start
+        mbar_wait(&sm.ds_free, (gj & 1) ^ 1);
+        const uint32_t rowoff = static_cast<uint32_t>(half * (128 * 128) + r * 128);
 #pragma unroll
-    for (int piece = 0; piece < 4; ++piece) {
-      uint4 w;
-      w.x = pack_bf16(__uint_as_float(u[8 * piece + 0]) * scale, __uint_as_float(u[8 * piece + 1]) * scale);
-      w.y = pack_bf16(__uint_as_float(u[8 * piece + 2]) * scale, __uint_as_float(u[8 * piece + 3]) * scale);
-      w.z = pack_bf16(__uint_as_float(u[8 * piece + 4]) * scale, __uint_as_float(u[8 * piece + 5]) * scale);
-      w.w = pack_bf16(__uint_as_float(u[8 * piece + 6]) * scale, __uint_as_float(u[8 * piece + 7]) * scale);
-      reinterpret_cast<uint4*>(qrow)[piece] = w;
+        for (int g8 = 0; g8 < 8; ++g8) {
+          const int c = half * 64 + 8 * g8;
+          float dv[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float p = ex2(fmaf(__uint_as_float(us[8 * g8 + e]), scale_log2, -l2));
+            dv[e] = p * (__uint_as_float(ud[8 * g8 + e]) - dq);
+          }
+          if (j == qb) {  // diagonal tile: keys after the query are invisible
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              if (c + e > r) dv[e] = 0.f;
+          }
+          st_shared_v4(dbase + rowoff + ((g8 ^ (r & 7)) << 4), pack_bf16(dv[0], dv[1]), pack_bf16(dv[2], dv[3]),
+                       pack_bf16(dv[4], dv[5]), pack_bf16(dv[6], dv[7]));
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.ds_full);
+      }
+      g += nkb;
+      const int aset = lu & 1;
+      mbar_wait(&sm.acc_full[aset], (lu >> 1) & 1);
+      tc_fence_after();
+      __nv_bfloat16* qrow = dqkv + (static_cast<size_t>(b) * T + q) * ld + static_cast<size_t>(h * HD) + half * 32;
+      uint32_t w32[32];
+      tmem_ld32(trow + 256 + aset * 64 + half * 32, w32);
+      tmem_ld_wait();
+#pragma unroll
+      for (int piece = 0; piece < 4; ++piece) {
+        uint4 w;
+        w.x = pack_bf16(__uint_as_float(w32[8 * piece + 0]) * scale, __uint_as_float(w32[8 * piece + 1]) * scale);
+        w.y = pack_bf16(__uint_as_float(w32[8 * piece + 2]) * scale, __uint_as_float(w32[8 * piece + 3]) * scale);
+        w.z = pack_bf16(__uint_as_float(w32[8 * piece + 4]) * scale, __uint_as_float(w32[8 * piece + 5]) * scale);
+        w.w = pack_bf16(__uint_as_float(w32[8 * piece + 6]) * scale, __uint_as_float(w32[8 * piece + 7]) * scale);
+        reinterpret_cast<uint4*>(qrow)[piece] = w;
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.acc_free[aset]);
     }
   }
   tc_fence_before();
@@ -762,13 +833,20 @@ void attn_bwd_tc(const bf16* qkv, const bf16* o, const float* lse, const bf16* d
     attr = true;
   }
   const float scale = 1.f / sqrtf(static_cast<float>(hd));
-  dim3 grid(static_cast<unsigned>(T / TQ), static_cast<unsigned>(B * H));
+  static const int sms = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v > 0 ? v : 148;
+  }();
+  const int BH = static_cast<int>(B * H), units = static_cast<int>(T / TQ) * BH;
+  const unsigned grid = static_cast<unsigned>(std::min(units, sms));
   long long* dbg = attn_fwd_debug_buffer();
-  attn_dkdv_tc_kernel<<<grid, kThreadsBwd, smem_kv, s>>>(tq, td, lse, Dsum, static_cast<int>(T), static_cast<int>(H),
+  attn_dkdv_tc_kernel<<<grid, kThreadsBwd, smem_kv, s>>>(tq, td, lse, Dsum, static_cast<int>(T), static_cast<int>(H), BH,
                                                          dqkv, scale, scale * kLog2e, dbg ? dbg + 8 * 32768 : nullptr);
   CKF_LAUNCH_CHECK();
-  attn_dq_tc_kernel<<<grid, kThreadsBwd, smem_q, s>>>(tq, td, lse, Dsum, static_cast<int>(T), static_cast<int>(H), dqkv,
-                                                   scale, scale * kLog2e);
+  attn_dq_tc_kernel<<<grid, kThreadsBwd, smem_q, s>>>(tq, td, lse, Dsum, static_cast<int>(T), static_cast<int>(H), BH,
+                                                   dqkv, scale, scale * kLog2e);
   CKF_LAUNCH_CHECK();
 }
 

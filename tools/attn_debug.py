@@ -6,7 +6,7 @@ import numpy as np
 import torch
 import paper_2506_15461_b200  # noqa
 from paper_2506_15461_b200._native import check, lib
-B, T, H, hd = 8, 1024, 8, 64
+B, T, H, hd = int(os.environ.get('B', 64)), 1024, 8, 64
 qkv = torch.randn(B * T, 3 * H * hd, device="cuda").bfloat16()
 o = torch.empty(B * T, H * hd, dtype=torch.bfloat16, device="cuda")
 lse = torch.empty(B * H * T, device="cuda")
@@ -34,11 +34,11 @@ for _ in range(3):
     check(lib().ckf_attention_bwd(qkv.data_ptr(), o.data_ptr(), lse.data_ptr(), dout.data_ptr(), B, T, H, hd,
                                   dqkv.data_ptr(), Dd.data_ptr(), 2, None))
 torch.cuda.synchronize()
-buf2 = (C.c_longlong * (8 * (32768 + n)))()
-check(L.ckf_debug_attn_fwd_timings(buf2, 32768 + n))
-a = np.array(buf2[8 * 32768:]).reshape(n, 8)
-print("dkdv ctas", n, "cycles: total(max)", a[:, 4].max(), "mean", a[:, 4].mean())
-for nt in sorted(set(a[:, 0])):
-    s = a[a[:, 0] == nt]
-    print(f"ntiles={nt:3d} n={len(s):4d} first_S={s[:,1].mean():8.0f} wait_S={s[:,2].mean():8.0f} wait_PD={s[:,3].mean():8.0f} "
-          f"wait_bar={s[:,5].mean():8.0f} total={s[:,4].mean():8.0f} per_tile={(s[:,4]-s[:,1]).mean()/nt:7.0f}")
+buf2 = (C.c_longlong * (8 * 32768 + 16 * 148))()
+check(L.ckf_debug_attn_fwd_timings(buf2, 32768 + 2 * 148))
+a = np.array(buf2[8 * 32768:]).reshape(148, 16)
+t = a[:, 0].sum()
+print(f"dkdv (persistent, 148 CTAs): tiles/CTA {a[:,0].mean():.1f}  total cycles {a[:,5].mean():.0f}  per tile {a[:,5].sum()/t:.0f}")
+print(f"  softmax per tile: wait S {a[:,1].sum()/t:.0f}  wait pd_free {a[:,2].sum()/t:.0f}  compute {a[:,3].sum()/t:.0f}  "
+      f"epilogue/unit-share {a[:,4].sum()/t:.0f}")
+print(f"  MMA per tile: issue_s(+waits) {a[:,8].sum()/t:.0f}  acc_free wait {a[:,9].sum()/t:.0f}  pd_full wait {a[:,10].sum()/t:.0f}")

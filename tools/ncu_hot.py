@@ -5,8 +5,8 @@ raw = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "source", "--csv"], ca
 rows = list(csv.reader(io.StringIO(raw)))
 hdr_i = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
 hdr = rows[hdr_i]
-body = [r for r in rows[hdr_i + 1:] if len(r) == len(hdr)]
 si = hdr.index("Warp Stall Sampling (All Samples)")
+body = [r for r in rows[hdr_i + 1:] if len(r) == len(hdr) and r[si].isdigit()]
 tot = sum(int(r[si] or 0) for r in body)
 top = sorted(body, key=lambda r: -int(r[si] or 0))[: int(sys.argv[2]) if len(sys.argv) > 2 else 25]
 print(f"total samples {tot}")
