@@ -480,9 +480,39 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
     const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
     const uint32_t pbase = smem_u32(sm.p), dbase = smem_u32(sm.ds);
     const size_t ld = static_cast<size_t>(3) * H * HD;
+    // Unit epilogue (column half 0 -> dV, half 1 -> dK x scale), run one tile late: after the
+    // first tile of the next unit, when the accumulator set has long been complete.
+    auto epilogue = [&](int eu, int elu) {
+      const int ekb = eu / BH, ebh = eu - ekb * BH, eb = ebh / H, eh = ebh - eb * H;
+      const int aset = elu & 1;
+      const long long e0 = clock64();
+      mbar_wait(&sm.acc_full[aset], (elu >> 1) & 1);
+      tc_fence_after();
+      __nv_bfloat16* dst = dqkv + (static_cast<size_t>(eb) * T + ekb * TK + r) * ld +
+                           static_cast<size_t>(half ? (H + eh) * HD : (2 * H + eh) * HD);
+      const float mul = half ? scale : 1.f;
+      uint32_t w32[64];
+      tmem_ld32(trow + 256 + aset * 128 + half * 64, *reinterpret_cast<uint32_t(*)[32]>(&w32[0]));
+      tmem_ld32(trow + 256 + aset * 128 + half * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&w32[32]));
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.acc_free[aset]);
+#pragma unroll
+      for (int piece = 0; piece < 8; ++piece) {
+        uint4 w;
+        w.x = pack_bf16(__uint_as_float(w32[8 * piece + 0]) * mul, __uint_as_float(w32[8 * piece + 1]) * mul);
+        w.y = pack_bf16(__uint_as_float(w32[8 * piece + 2]) * mul, __uint_as_float(w32[8 * piece + 3]) * mul);
+        w.z = pack_bf16(__uint_as_float(w32[8 * piece + 4]) * mul, __uint_as_float(w32[8 * piece + 5]) * mul);
+        w.w = pack_bf16(__uint_as_float(w32[8 * piece + 6]) * mul, __uint_as_float(w32[8 * piece + 7]) * mul);
+        reinterpret_cast<uint4*>(dst)[piece] = w;
+      }
+      tw[3] += clock64() - e0;
+    };
+    int pend_u = -1, pend_lu = 0;
     int g = 0, lu = 0;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lu) {
-      const int kb = u / BH, bh = u - kb * BH, b = bh / H, h = bh - b * H;
+      const int kb = u / BH;
       const int ntiles = nqb - kb;
       for (int i = 0; i < ntiles; ++i) {
         const int gi = g + i, st = gi & 1;
@@ -510,12 +540,16 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
 #pragma unroll
         for (int g8 = 0; g8 < 8; ++g8) {  // 8 columns (queries) at a time: P^T, dS^T -> bf16 -> swizzled smem
           const int c = half * 64 + 8 * g8;
-          const float4 la = *reinterpret_cast<const float4*>(&sm.lse[st][c]);
-          const float4 lb = *reinterpret_cast<const float4*>(&sm.lse[st][c + 4]);
-          const float4 da4 = *reinterpret_cast<const float4*>(&sm.dsum[st][c]);
-          const float4 db4 = *reinterpret_cast<const float4*>(&sm.dsum[st][c + 4]);
-          const float lq[8] = {la.x, la.y, la.z, la.w, lb.x, lb.y, lb.z, lb.w};
-          const float dq8[8] = {da4.x, da4.y, da4.z, da4.w, db4.x, db4.y, db4.z, db4.w};
+          // broadcast 128-bit shared loads (explicit ld.shared: the struct reference is generic)
+          const uint32_t la_ = smem_u32(&sm.lse[st][c]), da_ = smem_u32(&sm.dsum[st][c]);
+          const uint4 la = ld_shared_v4(la_), lb = ld_shared_v4(la_ + 16);
+          const uint4 da4 = ld_shared_v4(da_), db4 = ld_shared_v4(da_ + 16);
+          const float lq[8] = {__uint_as_float(la.x), __uint_as_float(la.y), __uint_as_float(la.z),
+                               __uint_as_float(la.w), __uint_as_float(lb.x), __uint_as_float(lb.y),
+                               __uint_as_float(lb.z), __uint_as_float(lb.w)};
+          const float dq8[8] = {__uint_as_float(da4.x), __uint_as_float(da4.y), __uint_as_float(da4.z),
+                                __uint_as_float(da4.w), __uint_as_float(db4.x), __uint_as_float(db4.y),
+                                __uint_as_float(db4.z), __uint_as_float(db4.w)};
           float pv[8], dv[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
@@ -539,37 +573,16 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
         if (lane == 0) mbar_arrive(&sm.pd_full);
         tw[2] += clock64() - a2;
         tw[4] += 1;
-      }
-      g += ntiles;
-      // ---------------- epilogue of this unit: column half 0 -> dV, half 1 -> dK (x scale)
-      const int aset = lu & 1;
-      const long long e0 = clock64();
-      mbar_wait(&sm.acc_full[aset], (lu >> 1) & 1);
-      tc_fence_after();
-      const int row0 = b * T;
-      __nv_bfloat16* dst = dqkv + (static_cast<size_t>(row0) + kb * TK + r) * ld +
-                           static_cast<size_t>(half ? (H + h) * HD : (2 * H + h) * HD);
-      const float mul = half ? scale : 1.f;
-#pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        uint32_t w32[32];
-        tmem_ld32(trow + 256 + aset * 128 + half * 64 + hh * 32, w32);
-        tmem_ld_wait();
-#pragma unroll
-        for (int piece = 0; piece < 4; ++piece) {
-          uint4 w;
-          w.x = pack_bf16(__uint_as_float(w32[8 * piece + 0]) * mul, __uint_as_float(w32[8 * piece + 1]) * mul);
-          w.y = pack_bf16(__uint_as_float(w32[8 * piece + 2]) * mul, __uint_as_float(w32[8 * piece + 3]) * mul);
-          w.z = pack_bf16(__uint_as_float(w32[8 * piece + 4]) * mul, __uint_as_float(w32[8 * piece + 5]) * mul);
-          w.w = pack_bf16(__uint_as_float(w32[8 * piece + 6]) * mul, __uint_as_float(w32[8 * piece + 7]) * mul);
-          reinterpret_cast<uint4*>(dst + hh * 32)[piece] = w;
+        if (i == 0 && pend_u >= 0) {
+          epilogue(pend_u, pend_lu);
+          pend_u = -1;
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.acc_free[aset]);
-      tw[3] += clock64() - e0;
+      g += ntiles;
+      pend_u = u;
+      pend_lu = lu;
     }
+    if (pend_u >= 0) epilogue(pend_u, pend_lu);
     if (dbg && threadIdx.x == 128) {
       long long* d = dbg + 16 * blockIdx.x;
       d[0] = tw[4];  // tiles
@@ -709,14 +722,40 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
     const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
     const uint32_t dbase = smem_u32(sm.ds);
     const size_t ld = static_cast<size_t>(3) * H * HD;
+    // unit epilogue (dQ x scale), run one tile late like the dK / dV kernel's
+    auto epilogue = [&](int eu, int elu) {
+      const int eqi = eu / BH, ebh = eu - eqi * BH, eb = ebh / H, eh = ebh - eb * H;
+      const int eq = (nqb - 1 - eqi) * TQ + r;
+      const int aset = elu & 1;
+      mbar_wait(&sm.acc_full[aset], (elu >> 1) & 1);
+      tc_fence_after();
+      __nv_bfloat16* qrow = dqkv + (static_cast<size_t>(eb) * T + eq) * ld + static_cast<size_t>(eh * HD) + half * 32;
+      uint32_t w32[32];
+      tmem_ld32(trow + 256 + aset * 64 + half * 32, w32);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.acc_free[aset]);
+#pragma unroll
+      for (int piece = 0; piece < 4; ++piece) {
+        uint4 w;
+        w.x = pack_bf16(__uint_as_float(w32[8 * piece + 0]) * scale, __uint_as_float(w32[8 * piece + 1]) * scale);
+        w.y = pack_bf16(__uint_as_float(w32[8 * piece + 2]) * scale, __uint_as_float(w32[8 * piece + 3]) * scale);
+        w.z = pack_bf16(__uint_as_float(w32[8 * piece + 4]) * scale, __uint_as_float(w32[8 * piece + 5]) * scale);
+        w.w = pack_bf16(__uint_as_float(w32[8 * piece + 6]) * scale, __uint_as_float(w32[8 * piece + 7]) * scale);
+        reinterpret_cast<uint4*>(qrow)[piece] = w;
+      }
+    };
+    int pend_u = -1, pend_lu = 0;
     int g = 0, lu = 0;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lu) {
-      const int qi = u / BH, bh = u - qi * BH, b = bh / H, h = bh - b * H;
+      const int qi = u / BH;
       const int qb = nqb - 1 - qi, nkb = qb + 1;
-      const int q = qb * TQ + r;
       mbar_wait(&sm.qd_full[lu & 1], (lu >> 1) & 1);  // (complete before S) lse / D of the unit's queries
-      const float l2 = sm.lse[lu & 1][r] * kLog2e;
-      const float dq = sm.dsum[lu & 1][r];
+      float l2, dq;
+      asm volatile("ld.shared.f32 %0, [%1];" : "=f"(l2) : "r"(smem_u32(&sm.lse[lu & 1][r])));
+      asm volatile("ld.shared.f32 %0, [%1];" : "=f"(dq) : "r"(smem_u32(&sm.dsum[lu & 1][r])));
+      l2 *= kLog2e;
       for (int j = 0; j < nkb; ++j) {
         const int gj = g + j;
         mbar_wait(&sm.s_full, gj & 1);
@@ -752,28 +791,16 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.ds_full);
+        if (j == 0 && pend_u >= 0) {
+          epilogue(pend_u, pend_lu);
+          pend_u = -1;
+        }
       }
       g += nkb;
-      const int aset = lu & 1;
-      mbar_wait(&sm.acc_full[aset], (lu >> 1) & 1);
-      tc_fence_after();
-      __nv_bfloat16* qrow = dqkv + (static_cast<size_t>(b) * T + q) * ld + static_cast<size_t>(h * HD) + half * 32;
-      uint32_t w32[32];
-      tmem_ld32(trow + 256 + aset * 64 + half * 32, w32);
-      tmem_ld_wait();
-#pragma unroll
-      for (int piece = 0; piece < 4; ++piece) {
-        uint4 w;
-        w.x = pack_bf16(__uint_as_float(w32[8 * piece + 0]) * scale, __uint_as_float(w32[8 * piece + 1]) * scale);
-        w.y = pack_bf16(__uint_as_float(w32[8 * piece + 2]) * scale, __uint_as_float(w32[8 * piece + 3]) * scale);
-        w.z = pack_bf16(__uint_as_float(w32[8 * piece + 4]) * scale, __uint_as_float(w32[8 * piece + 5]) * scale);
-        w.w = pack_bf16(__uint_as_float(w32[8 * piece + 6]) * scale, __uint_as_float(w32[8 * piece + 7]) * scale);
-        reinterpret_cast<uint4*>(qrow)[piece] = w;
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.acc_free[aset]);
+      pend_u = u;
+      pend_lu = lu;
     }
+    if (pend_u >= 0) epilogue(pend_u, pend_lu);
   }
   tc_fence_before();
   __syncthreads();

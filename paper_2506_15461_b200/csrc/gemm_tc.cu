@@ -119,12 +119,14 @@ struct Params {
   const __nv_bfloat16* gu; // kSwiGLUBwd: [M x 2f] gate/up activations (row pitch 2f)
 };
 
-template <int BN, int EPI>
+template <int BN, int EPI, int NCTA>
 struct Cfg {
-  // kSwiGLUBwd trades one operand stage for 4 epilogue buffers per warp (g/u prefetch pairs)
+  // kSwiGLUBwd trades operand stages for 4 epilogue buffers per warp (g/u prefetch pairs).
+  // NCTA = 2 (CTA pair): each CTA holds BN/2 columns of B, so a stage is 32 KiB at BN = 256.
   static constexpr int kEpiBufs = EPI == kSwiGLUBwd ? 4 : 2;
-  static constexpr int kStages = (BN == 256 ? 4 : 6) - (EPI == kSwiGLUBwd ? 1 : 0);
-  static constexpr uint32_t kBStage = BN * BK * 2;
+  static constexpr int kStages = NCTA == 2 ? (EPI == kSwiGLUBwd ? 4 : 6)
+                                           : (BN == 256 ? 4 : 6) - (EPI == kSwiGLUBwd ? 1 : 0);
+  static constexpr uint32_t kBStage = (BN / NCTA) * BK * 2;
   static constexpr uint32_t kStageBytes = kAStage + kBStage;
   static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
   static constexpr uint32_t kEpiBytes = 4 * kEpiBufs * kStageBufBytes;
@@ -156,13 +158,20 @@ __device__ __forceinline__ Unit unit_of(const Params& p, int u) {
   return w;
 }
 
-template <int BN, bool A_MN, bool B_MN, int EPI>
+// NCTA = 2: CTA-pair (cluster of 2) tiles of 256 x BN: each CTA stages 128 rows of A and
+// BN/2 columns of B, the leader issues tcgen05.mma.cta_group::2 (M = 256), both CTAs hold
+// their 128 x BN accumulator rows in TMEM and run their own epilogue.
+template <int BN, bool A_MN, bool B_MN, int EPI, int NCTA>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                 const __grid_constant__ CUtensorMap tmap_c, const __grid_constant__ CUtensorMap tmap_ws, Params p) {
-  using C = Cfg<BN, EPI>;
+  using C = Cfg<BN, EPI, NCTA>;
   constexpr int ST = C::kStages;
-  constexpr uint32_t IDESC = idesc_bf16_f32(BM, BN, A_MN, B_MN);
+  constexpr uint32_t IDESC = idesc_bf16_f32(BM * NCTA, BN, A_MN, B_MN);
+  constexpr int BNC = BN / NCTA;  // B columns staged by this CTA
+  const uint32_t rank = NCTA == 2 ? cluster_ctarank() : 0;
+  const bool leader = rank == 0;
+  const int u0 = static_cast<int>(blockIdx.x) / NCTA, ustep = static_cast<int>(gridDim.x) / NCTA;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -189,14 +198,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 4);
+      mbar_init(&tempty[i], 4 * NCTA);  // the leader's counts both CTAs' epilogue warps
     }
     for (int i = 0; i < 8; ++i) mbar_init(&lbar[i], 1);
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<C::kTmemCols>(tmem_slot);
+  if (warp == 2) {
+    if constexpr (NCTA == 2)
+      tmem_alloc_2sm<C::kTmemCols>(tmem_slot);
+    else
+      tmem_alloc<C::kTmemCols>(tmem_slot);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (NCTA == 2)
+    cluster_sync_all();  // barriers of both CTAs initialised before any cross-CTA signal
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   // Programmatic dependent launch: the set-up above overlaps the previous kernel's tail;
@@ -209,29 +226,39 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ---------------- TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+      for (int u = u0; u < p.units; u += ustep) {
         const Unit w = unit_of(p, u);
+        const int arow = w.mb * BM * NCTA + static_cast<int>(rank) * BM;
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
           uint8_t* a = sA + stage * kAStage;
           uint8_t* b = sB + stage * C::kBStage;
+          // NCTA = 2: the leader's full barrier counts both CTAs' bytes; both CTAs' loads complete on it
+          const uint32_t fb = NCTA == 2 ? mapa_shared(&full[stage], 0) : smem_u32(&full[stage]);
+          if (leader) mbar_arrive_expect_tx(&full[stage], NCTA * C::kStageBytes);
+          auto load = [&](void* dst, const CUtensorMap* map, int c0, int c1) {
+            if constexpr (NCTA == 2)
+              tma_load_2d_pair(dst, map, fb, c0, c1);
+            else
+              tma_load_2d(dst, map, &full[stage], c0, c1);
+          };
           if constexpr (A_MN) {
 #pragma unroll
-            for (int c = 0; c < BM / 64; ++c) tma_load_2d(a + c * 8192, &tmap_a, &full[stage], w.mb * BM + c * 64, kb * BK);
+            for (int c = 0; c < BM / 64; ++c) load(a + c * 8192, &tmap_a, arow + c * 64, kb * BK);
           } else {
-            tma_load_2d(a, &tmap_a, &full[stage], kb * BK, w.mb * BM);
+            load(a, &tmap_a, kb * BK, arow);
           }
           if constexpr (B_MN) {
 #pragma unroll
-            for (int c = 0; c < BN / 64; ++c) {
-              int col = w.nb * BN + c * 64;
+            for (int c = 0; c < BNC / 64; ++c) {
+              const int cc = static_cast<int>(rank) * BNC + c * 64;  // column within the BN-wide tile
+              int col = w.nb * BN + cc;
               if constexpr (EPI == kSwiGLU)  // accumulator columns [0, BN/2) = gate, [BN/2, BN) = up
-                col = c * 64 < BN / 2 ? w.nb * (BN / 2) + c * 64 : p.f + w.nb * (BN / 2) + c * 64 - BN / 2;
-              tma_load_2d(b + c * 8192, &tmap_b, &full[stage], col, kb * BK);
+                col = cc < BN / 2 ? w.nb * (BN / 2) + cc : p.f + w.nb * (BN / 2) + cc - BN / 2;
+              load(b + c * 8192, &tmap_b, col, kb * BK);
             }
           } else {
-            tma_load_2d(b, &tmap_b, &full[stage], kb * BK, w.nb * BN);
+            load(b, &tmap_b, kb * BK, w.nb * BN + static_cast<int>(rank) * BNC);
           }
           if (++stage == ST) {
             stage = 0;
@@ -241,13 +268,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer
+    if (lane == 0 && leader) {
+      // ---------------- MMA issuer (the pair's leader issues for both CTAs)
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+      for (int u = u0; u < p.units; u += ustep) {
         const Unit w = unit_of(p, u);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
@@ -261,15 +288,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k = 0; k < BK / UK; ++k) {
             const uint64_t ad = A_MN ? umma_desc_sw128(a0 + k * 2048, 8192, 1024) : umma_desc_sw128(a0 + k * 32, 16, 1024);
             const uint64_t bd = B_MN ? umma_desc_sw128(b0 + k * 2048, 8192, 1024) : umma_desc_sw128(b0 + k * 32, 16, 1024);
-            umma_bf16(d, ad, bd, IDESC, (kb > w.kb0 || k > 0) ? 1u : 0u);
+            if constexpr (NCTA == 2)
+              umma_bf16_2sm(d, ad, bd, IDESC, (kb > w.kb0 || k > 0) ? 1u : 0u);
+            else
+              umma_bf16(d, ad, bd, IDESC, (kb > w.kb0 || k > 0) ? 1u : 0u);
           }
-          umma_commit(&empty[stage]);
+          if constexpr (NCTA == 2)
+            umma_commit_2sm(&empty[stage], 0x3);
+          else
+            umma_commit(&empty[stage]);
           if (++stage == ST) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit(&tfull[acc]);
+        if constexpr (NCTA == 2)
+          umma_commit_2sm(&tfull[acc], 0x3);
+        else
+          umma_commit(&tfull[acc]);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -299,24 +335,32 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       sbuf ^= 1;
     };
+    // the accumulator buffer goes back to the MMA issuer (the leader's barrier in a CTA pair)
+    auto release_acc = [&](int a) {
+      if constexpr (NCTA == 2)
+        mbar_arrive_cluster(mapa_shared(&tempty[a], 0));
+      else
+        mbar_arrive(&tempty[a]);
+    };
+    // first output row of this warp's 32 accumulator lanes
+    auto row0_of = [&](const Unit& wu) { return wu.mb * BM * NCTA + static_cast<int>(rank) * BM + q * 32; };
     int cc = 0;               // kSwiGLUBwd: chunk counter of this warp's stream
     bool first_unit = true;
-    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+    for (int u = u0; u < p.units; u += ustep) {
       const Unit w = unit_of(p, u);
       if constexpr (EPI == kSwiGLUBwd) {
         if (first_unit && lane == 0) {  // first g/u chunk in flight before the accumulator is ready
-          const Unit w2 = w;
           uint64_t* bar = &lbar[q * 2];
           mbar_arrive_expect_tx(bar, 2 * kStageBufBytes);
-          tma_load_2d(stg, &tmap_ws, bar, w2.nb * BN, w2.mb * BM + q * 32);
-          tma_load_2d(stg + kStageBufBytes, &tmap_ws, bar, p.f + w2.nb * BN, w2.mb * BM + q * 32);
+          tma_load_2d(stg, &tmap_ws, bar, w.nb * BN, row0_of(w));
+          tma_load_2d(stg + kStageBufBytes, &tmap_ws, bar, p.f + w.nb * BN, row0_of(w));
         }
         first_unit = false;
       }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t trow = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN);
-      const int m0 = w.mb * BM + q * 32;
+      const int m0 = row0_of(w);
       if constexpr (EPI == kSwiGLU) {
         // gate columns [c0, c0+64) and the matching up columns [BN/2 + c0, ...)
 #pragma unroll 1
@@ -330,7 +374,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (c0 + 64 >= BN / 2) {
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (lane == 0) release_acc(acc);
           }
           const int n0 = w.nb * (BN / 2) + c0;
           uint32_t pk[32];
@@ -362,7 +406,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const Unit w2 = unit_of(p, uu);
           uint8_t* gb = stg + (k & 1) * 2 * kStageBufBytes;
           uint64_t* bar = &lbar[q * 2 + (k & 1)];
-          const int n0 = w2.nb * BN + c * 64, y = w2.mb * BM + q * 32;
+          const int n0 = w2.nb * BN + c * 64, y = row0_of(w2);
           mbar_arrive_expect_tx(bar, 2 * kStageBufBytes);
           tma_load_2d(gb, &tmap_ws, bar, n0, y);
           tma_load_2d(gb + kStageBufBytes, &tmap_ws, bar, p.f + n0, y);
@@ -371,7 +415,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < NCH; ++c, ++cc) {
           const int n0 = w.nb * BN + c * 64;
           if (lane == 0) {
-            const int nu = c + 1 < NCH ? u : u + static_cast<int>(gridDim.x);
+            const int nu = c + 1 < NCH ? u : u + ustep;
             if (nu < p.units) {
               bulk_wait_read<0>();  // chunk cc-1's stores have left the pair we refill
               prefetch(nu, c + 1 < NCH ? c + 1 : 0, cc + 1);
@@ -384,7 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (c + 1 == NCH) {
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (lane == 0) release_acc(acc);
           }
           mbar_wait(&lbar[q * 2 + (cc & 1)], (cc >> 1) & 1);
           uint8_t* gb = stg + (cc & 1) * 2 * kStageBufBytes;
@@ -450,7 +494,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (c0 + CW >= BN) {  // last chunk loaded: hand the accumulator back to the MMA warp early
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
+          if (lane == 0) release_acc(acc);
         }
         uint8_t* sb = stg + sbuf * kStageBufBytes;
         if (lane == 0) bulk_wait_read<1>();  // the staging buffer used two stores ago is free
@@ -558,9 +602,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) bulk_wait_all();
   }
   tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  if (warp == 2) tmem_free<C::kTmemCols>(tmem_base);
+  if constexpr (NCTA == 2) {
+    cluster_sync_all();  // the leader's MMAs into the peer's TMEM are complete
+    tc_fence_after();
+    if (warp == 2) tmem_free_2sm<C::kTmemCols>(tmem_base);
+  } else {
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 2) tmem_free<C::kTmemCols>(tmem_base);
+  }
 }
 
 int num_sms() {
@@ -601,13 +651,13 @@ int* split_flags(size_t n) {
   return flags;
 }
 
-template <int BN, bool A_MN, bool B_MN, int EPI>
+template <int BN, bool A_MN, bool B_MN, int EPI, int NCTA>
 void launch_t(const GemmDesc& g, int splits, cudaStream_t s) {
-  using C = Cfg<BN, EPI>;
+  using C = Cfg<BN, EPI, NCTA>;
   const CUtensorMap ta = A_MN ? tma::make_2d_bf16(g.A, g.M, g.K, g.lda, 64, 64)
                               : tma::make_2d_bf16(g.A, g.K, g.M, g.lda, 64, BM);
   const CUtensorMap tb = B_MN ? tma::make_2d_bf16(g.B, g.N, g.K, g.ldb, 64, 64)
-                              : tma::make_2d_bf16(g.B, g.K, g.N, g.ldb, 64, BN);
+                              : tma::make_2d_bf16(g.B, g.K, g.N, g.ldb, 64, BN / NCTA);
   const bool c_bf16 = EPI == kStoreBF16 || EPI == kSwiGLU || EPI == kSwiGLUBwd;
   // kSwiGLUBwd: C = dgu [M x 2f] although the GEMM's N is f
   const CUtensorMap tcm = c_bf16 ? tma::make_2d_bf16(g.C, EPI == kSwiGLUBwd ? 2 * g.N : g.N, g.M, g.ldc, 64, 32)
@@ -617,7 +667,7 @@ void launch_t(const GemmDesc& g, int splits, cudaStream_t s) {
   p.N = g.N;
   p.K = g.K;
   p.alpha = g.alpha;
-  p.nm = (g.M + BM - 1) / BM;
+  p.nm = (g.M + BM * NCTA - 1) / (BM * NCTA);  // (pair) tiles along M
   p.nn = (g.N + BN - 1) / BN;
   p.tiles = p.nm * p.nn;
   p.nk = (g.K + BK - 1) / BK;
@@ -625,8 +675,8 @@ void launch_t(const GemmDesc& g, int splits, cudaStream_t s) {
   p.kb_per_split = (p.nk + p.splits - 1) / p.splits;
   p.splits = (p.nk + p.kb_per_split - 1) / p.kb_per_split;  // no empty split
   p.units = p.tiles * p.splits;
-  if (p.splits > 1 && (p.units > num_sms() || EPI != kAccF32 || g.N % 4 != 0)) p.splits = 1, p.units = p.tiles,
-                                                                                   p.kb_per_split = p.nk;
+  if (p.splits > 1 && (NCTA != 1 || p.units > num_sms() || EPI != kAccF32 || g.N % 4 != 0))
+    p.splits = 1, p.units = p.tiles, p.kb_per_split = p.nk;
   p.flags = p.splits > 1 ? split_flags(2 * static_cast<size_t>(p.tiles)) : nullptr;
   p.ws = p.splits > 1 ? split_workspace(static_cast<size_t>(p.units) * BM * BN * sizeof(float)) : nullptr;
   p.C = static_cast<float*>(g.C);
@@ -649,35 +699,39 @@ void launch_t(const GemmDesc& g, int splits, cudaStream_t s) {
                           : EPI == kSwiGLU    ? tma::make_2d_bf16(g.aux, g.N / 2, g.M, g.ldaux, 64, 32)
                           : EPI == kSwiGLUBwd ? tma::make_2d_bf16(g.aux, 2 * g.N, g.M, g.ldaux, 64, 32)
                                               : tcm;
-  auto kern = gemm_kernel<BN, A_MN, B_MN, EPI>;
+  auto kern = gemm_kernel<BN, A_MN, B_MN, EPI, NCTA>;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
     CKF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::kSmem)));
     attr_set = true;
   }
-  const int grid = std::min(p.units, num_sms());
+  const int grid = NCTA * std::min(p.units, num_sms() / NCTA);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(grid));
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = C::kSmem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;  // NCTA = 2: the CTA pair shares one TPC
+  attr[0].val.clusterDim.x = NCTA;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   static const bool pdl = [] {  // CKF_PDL=0: plain stream-ordered launches (A/B timing)
     const char* v = std::getenv("CKF_PDL");
     return !(v && v[0] == '0');
   }();
   cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.numAttrs = pdl ? 2 : 1;
   CKF_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, tcm, twm, p));
   CKF_LAUNCH_CHECK();
 }
 
-template <int BN>
+template <int BN, int NCTA>
 void dispatch_bn(const GemmDesc& g, int splits, cudaStream_t s) {
 #define CKF_GEMM_CASE(AM, BMN, E) \
-  if (g.a_mn == AM && g.b_mn == BMN && g.epi == E) return launch_t<BN, AM, BMN, E>(g, splits, s);
+  if (g.a_mn == AM && g.b_mn == BMN && g.epi == E) return launch_t<BN, AM, BMN, E, NCTA>(g, splits, s);
 #define CKF_GEMM_EPIS(AM, BMN) CKF_GEMM_CASE(AM, BMN, kStoreBF16) CKF_GEMM_CASE(AM, BMN, kStoreF32) CKF_GEMM_CASE(AM, BMN, kAccF32)
   CKF_GEMM_EPIS(false, false)
   CKF_GEMM_EPIS(false, true)
@@ -736,10 +790,21 @@ void gemm_bf16(const GemmDesc& g, cudaStream_t s) {
     }
   }
   if (splits > 1 && g.epi != kAccF32) raise(1, "gemm_bf16: split-K needs the fp32 accumulate epilogue");
+  // CTA pairs (256 x 256 tiles, cta_group::2) when the output is tiled without split-K: each SM
+  // stages half the B bytes per MMA FLOP in a 6-deep ring.  Measured on B200
+  // (profiles/r01_gemm_pair_vs_single.jsonl): +3-4 % on the stage GEMMs; single CTAs stay ahead
+  // for the fused SwiGLU epilogues and for N <= 512 with very short or very long K.
+  static const bool pair_ok = [] {
+    const char* v = std::getenv("CKF_GEMM_PAIR");
+    return !(v && v[0] == '0');
+  }();
+  const bool pair_shape = g.epi != kSwiGLU && g.epi != kSwiGLUBwd && !(g.N <= 512 && (g.K <= 512 || g.K >= 16384));
   if (bn == 128)
-    dispatch_bn<128>(g, splits, s);
+    dispatch_bn<128, 1>(g, splits, s);
+  else if (pair_ok && pair_shape && splits <= 1 && g.M >= 2 * BM)
+    dispatch_bn<256, 2>(g, splits, s);
   else
-    dispatch_bn<256>(g, splits, s);
+    dispatch_bn<256, 1>(g, splits, s);
 }
 
 }  // namespace tc
