@@ -327,6 +327,18 @@ __global__ void dsum_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bflo
   }
 }
 
+// Inverse rotary rotation of one 64-wide head row (pairs (j, j + 32)), in place on fp32
+// values: the transpose of the forward rotation (llama_kernels.cu rope_kernel, inverse = 1).
+__device__ __forceinline__ void rope_inverse64(uint32_t (&v)[64], const float2* __restrict__ cs) {
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const float2 t = __ldg(cs + j);
+    const float a = __uint_as_float(v[j]), b = __uint_as_float(v[j + 32]);
+    v[j] = __float_as_uint(a * t.x + b * t.y);
+    v[j + 32] = __float_as_uint(b * t.x - a * t.y);
+  }
+}
+
 // Both backward kernels are persistent (one CTA per SM) over work units sorted
 // longest-first.  K/V (dK dV kernel) or Q/dO (dQ kernel) of a unit are
 // double-buffered in shared memory and the TMEM accumulators are double-
@@ -350,7 +362,8 @@ struct SmemKV {  // dK / dV kernel
 __global__ void __launch_bounds__(kThreadsBwd, 1)
     attn_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
                         const float* __restrict__ lse, const float* __restrict__ D, int T, int H, int BH,
-                        __nv_bfloat16* __restrict__ dqkv, float scale, float scale_log2, long long* __restrict__ dbg) {
+                        __nv_bfloat16* __restrict__ dqkv, float scale, float scale_log2, const float2* __restrict__ rope,
+                        long long* __restrict__ dbg) {
   extern __shared__ uint8_t smem_raw[];
   const long long t_start = clock64();
   long long tw[6] = {0, 0, 0, 0, 0, 0};  // CKF_ATTN_DEBUG phase cycles (softmax warp 4 lane 0 / MMA lane)
@@ -498,6 +511,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.acc_free[aset]);
+      if (half && rope) rope_inverse64(w32, rope + static_cast<size_t>(ekb * TK + r) * 32);  // dK
 #pragma unroll
       for (int piece = 0; piece < 8; ++piece) {
         uint4 w;
@@ -614,7 +628,7 @@ struct SmemQ {  // dQ kernel
 __global__ void __launch_bounds__(kThreadsBwd, 1)
     attn_dq_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
                       const float* __restrict__ lse, const float* __restrict__ D, int T, int H, int BH,
-                      __nv_bfloat16* __restrict__ dqkv, float scale, float scale_log2) {
+                      __nv_bfloat16* __restrict__ dqkv, float scale, float scale_log2, const float2* __restrict__ rope) {
   extern __shared__ uint8_t smem_raw[];
   SmemQ& sm = *reinterpret_cast<SmemQ*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -729,22 +743,69 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
       const int aset = elu & 1;
       mbar_wait(&sm.acc_full[aset], (elu >> 1) & 1);
       tc_fence_after();
-      __nv_bfloat16* qrow = dqkv + (static_cast<size_t>(eb) * T + eq) * ld + static_cast<size_t>(eh * HD) + half * 32;
-      uint32_t w32[32];
-      tmem_ld32(trow + 256 + aset * 64 + half * 32, w32);
-      tmem_ld_wait();
+      // the column-half-0 warps write the whole 64-wide row (the rotary pairs (j, j + 32) span both
+      // halves), 16 pairs at a time
+      __nv_bfloat16* qrow = dqkv + (static_cast<size_t>(eb) * T + eq) * ld + static_cast<size_t>(eh * HD);
+      if (!rope) {  // no rotation: each column half writes its own 32 columns
+        uint32_t w32[32];
+        tmem_ld32(trow + 256 + aset * 64 + half * 32, w32);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.acc_free[aset]);
+#pragma unroll
+        for (int piece = 0; piece < 4; ++piece) {
+          uint4 w;
+          w.x = pack_bf16(__uint_as_float(w32[8 * piece + 0]) * scale, __uint_as_float(w32[8 * piece + 1]) * scale);
+          w.y = pack_bf16(__uint_as_float(w32[8 * piece + 2]) * scale, __uint_as_float(w32[8 * piece + 3]) * scale);
+          w.z = pack_bf16(__uint_as_float(w32[8 * piece + 4]) * scale, __uint_as_float(w32[8 * piece + 5]) * scale);
+          w.w = pack_bf16(__uint_as_float(w32[8 * piece + 6]) * scale, __uint_as_float(w32[8 * piece + 7]) * scale);
+          reinterpret_cast<uint4*>(qrow + half * 32)[piece] = w;
+        }
+        return;
+      }
+      if (half == 0) {
+#pragma unroll 1
+        for (int j0 = 0; j0 < 32; j0 += 16) {
+          uint32_t lo[16], hi[16];
+          tmem_ld16(trow + 256 + aset * 64 + j0, lo);
+          tmem_ld16(trow + 256 + aset * 64 + 32 + j0, hi);
+          tmem_ld_wait();
+          float a[16], b[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            a[j] = __uint_as_float(lo[j]) * scale;
+            b[j] = __uint_as_float(hi[j]) * scale;
+          }
+          {
+            const float2* cs = rope + static_cast<size_t>(eq) * 32 + j0;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const float2 t = __ldg(cs + j);
+              const float x = a[j], y = b[j];
+              a[j] = x * t.x + y * t.y;
+              b[j] = y * t.x - x * t.y;
+            }
+          }
+#pragma unroll
+          for (int piece = 0; piece < 2; ++piece) {
+            uint4 wa, wb;
+            wa.x = pack_bf16(a[8 * piece + 0], a[8 * piece + 1]);
+            wa.y = pack_bf16(a[8 * piece + 2], a[8 * piece + 3]);
+            wa.z = pack_bf16(a[8 * piece + 4], a[8 * piece + 5]);
+            wa.w = pack_bf16(a[8 * piece + 6], a[8 * piece + 7]);
+            wb.x = pack_bf16(b[8 * piece + 0], b[8 * piece + 1]);
+            wb.y = pack_bf16(b[8 * piece + 2], b[8 * piece + 3]);
+            wb.z = pack_bf16(b[8 * piece + 4], b[8 * piece + 5]);
+            wb.w = pack_bf16(b[8 * piece + 6], b[8 * piece + 7]);
+            reinterpret_cast<uint4*>(qrow + j0)[piece] = wa;
+            reinterpret_cast<uint4*>(qrow + 32 + j0)[piece] = wb;
+          }
+        }
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.acc_free[aset]);
-#pragma unroll
-      for (int piece = 0; piece < 4; ++piece) {
-        uint4 w;
-        w.x = pack_bf16(__uint_as_float(w32[8 * piece + 0]) * scale, __uint_as_float(w32[8 * piece + 1]) * scale);
-        w.y = pack_bf16(__uint_as_float(w32[8 * piece + 2]) * scale, __uint_as_float(w32[8 * piece + 3]) * scale);
-        w.z = pack_bf16(__uint_as_float(w32[8 * piece + 4]) * scale, __uint_as_float(w32[8 * piece + 5]) * scale);
-        w.w = pack_bf16(__uint_as_float(w32[8 * piece + 6]) * scale, __uint_as_float(w32[8 * piece + 7]) * scale);
-        reinterpret_cast<uint4*>(qrow)[piece] = w;
-      }
     };
     int pend_u = -1, pend_lu = 0;
     int g = 0, lu = 0;
@@ -842,7 +903,7 @@ void attn_fwd_tc(const bf16* qkv, size_t B, size_t T, size_t H, size_t hd, bf16*
 }
 
 void attn_bwd_tc(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, size_t B, size_t T, size_t H,
-                 size_t hd, bf16* dqkv, float* Dsum, cudaStream_t s) {
+                 size_t hd, bf16* dqkv, float* Dsum, cudaStream_t s, const float2* rope_tab) {
   if (!attn_fwd_tc_supported(T, hd)) raise(1, "tcgen05 attention: head_dim 64 and seq_len % 128 == 0");
   const size_t rows = B * T * H;
   dsum_kernel<<<static_cast<unsigned>((rows + 31) / 32), 256, 0, s>>>(o, dout, static_cast<int>(B), static_cast<int>(T),
@@ -870,10 +931,11 @@ void attn_bwd_tc(const bf16* qkv, const bf16* o, const float* lse, const bf16* d
   const unsigned grid = static_cast<unsigned>(std::min(units, sms));
   long long* dbg = attn_fwd_debug_buffer();
   attn_dkdv_tc_kernel<<<grid, kThreadsBwd, smem_kv, s>>>(tq, td, lse, Dsum, static_cast<int>(T), static_cast<int>(H), BH,
-                                                         dqkv, scale, scale * kLog2e, dbg ? dbg + 8 * 32768 : nullptr);
+                                                         dqkv, scale, scale * kLog2e, rope_tab,
+                                                         dbg ? dbg + 8 * 32768 : nullptr);
   CKF_LAUNCH_CHECK();
   attn_dq_tc_kernel<<<grid, kThreadsBwd, smem_q, s>>>(tq, td, lse, Dsum, static_cast<int>(T), static_cast<int>(H), BH,
-                                                   dqkv, scale, scale * kLog2e);
+                                                   dqkv, scale, scale * kLog2e, rope_tab);
   CKF_LAUNCH_CHECK();
 }
 
