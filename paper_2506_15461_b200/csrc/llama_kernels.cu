@@ -10,6 +10,7 @@
 
 #include "common.cuh"
 #include "llama_kernels.h"
+#include "sm100.cuh"
 
 namespace ckf::llama {
 namespace {
@@ -359,6 +360,186 @@ __global__ void __launch_bounds__(kXentThreads) xent_kernel(__nv_bfloat16* __res
   }
 }
 
+// Register-resident variant (V % 8 == 0, V / 8 <= NC * kXentThreads): each thread keeps its NC
+// 16-byte chunks of the row in registers, so the logits are read from HBM once and the
+// gradient overwrites them in place; exact two-pass max / sum (one exp2 per logit per pass).
+template <int NC>
+__global__ void __launch_bounds__(kXentThreads) xent_reg_kernel(__nv_bfloat16* __restrict__ logits,
+                                                                const int* __restrict__ labels, int V, float gscale,
+                                                                int grad, double* __restrict__ row_loss) {
+  __shared__ float red[kXentThreads / 32];
+  __shared__ float bcast[2];
+  constexpr float kL2e = 1.4426950408889634f;
+  const size_t r = blockIdx.x;
+  uint4* rv = reinterpret_cast<uint4*>(logits + r * static_cast<size_t>(V));
+  const int V8 = V / 8;
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  uint4 u[NC];
+  float m = -INFINITY;
+#pragma unroll
+  for (int k = 0; k < NC; ++k) {
+    const int c = threadIdx.x + k * kXentThreads;
+    u[k] = c < V8 ? rv[c] : make_uint4(0xff80ff80u, 0xff80ff80u, 0xff80ff80u, 0xff80ff80u);  // bf16 -inf
+    const uint32_t* q = reinterpret_cast<const uint32_t*>(&u[k]);
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      m = fmaxf(m, fmaxf(__uint_as_float(q[e] << 16), __uint_as_float(q[e] & 0xffff0000u)));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (l == 0) red[w] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float M = red[0];
+    for (int i = 1; i < kXentThreads / 32; ++i) M = fmaxf(M, red[i]);
+    bcast[0] = M;
+  }
+  __syncthreads();
+  const float M = bcast[0], Ml = M * kL2e;
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < NC; ++k) {
+    const uint32_t* q = reinterpret_cast<const uint32_t*>(&u[k]);
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      s += exp2f(fmaf(__uint_as_float(q[e] << 16), kL2e, -Ml)) +
+           exp2f(fmaf(__uint_as_float(q[e] & 0xffff0000u), kL2e, -Ml));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const int y = labels[r];
+  float xy = 0.f;
+  if (threadIdx.x == 0) xy = __bfloat162float(logits[r * static_cast<size_t>(V) + y]);
+  __syncthreads();  // red[] reuse; row[y] read before any gradient store
+  if (l == 0) red[w] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float S = 0.f;
+    for (int i = 0; i < kXentThreads / 32; ++i) S += red[i];
+    const float lse = M + __logf(S);
+    bcast[1] = lse;
+    row_loss[r] = static_cast<double>(lse) - static_cast<double>(xy);
+  }
+  if (!grad) return;
+  __syncthreads();
+  const float Ll = bcast[1] * kL2e;
+#pragma unroll
+  for (int k = 0; k < NC; ++k) {
+    const int c = threadIdx.x + k * kXentThreads;
+    if (c >= V8) continue;
+    const uint32_t* q = reinterpret_cast<const uint32_t*>(&u[k]);
+    uint4 o;
+    uint32_t* po = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int j = 8 * c + 2 * e;
+      const float g0 = (exp2f(fmaf(__uint_as_float(q[e] << 16), kL2e, -Ll)) - (j == y ? 1.f : 0.f)) * gscale;
+      const float g1 = (exp2f(fmaf(__uint_as_float(q[e] & 0xffff0000u), kL2e, -Ll)) - (j + 1 == y ? 1.f : 0.f)) * gscale;
+      const __nv_bfloat162 b = __floats2bfloat162_rn(g0, g1);
+      po[e] = *reinterpret_cast<const uint32_t*>(&b);
+    }
+    rv[c] = o;
+  }
+}
+
+// Persistent, row-pipelined variant (V % 8 == 0, 2 rows fit in shared memory): row i + 2 is
+// bulk-copied (cp.async.bulk) into shared memory while row i is reduced, so the logits are
+// read from HBM once, the gradient is written once, and the load latency is hidden.
+constexpr int kXentPipeThreads = 512;
+__global__ void __launch_bounds__(kXentPipeThreads, 1)
+    xent_pipe_kernel(__nv_bfloat16* __restrict__ logits, const int* __restrict__ labels, int rows, int V, float gscale,
+                     int grad, double* __restrict__ row_loss) {
+  extern __shared__ uint8_t xsm_raw[];
+  uint8_t* xsm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(xsm_raw) + 127) & ~uintptr_t(127));
+  const uint32_t rowb = static_cast<uint32_t>(V) * 2, rowb_al = (rowb + 127) & ~127u;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(xsm + 2 * rowb_al);
+  float* red = reinterpret_cast<float*>(bar + 2);
+  constexpr float kL2e = 1.4426950408889634f;
+  const int V8 = V / 8, w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    sm100::mbar_init(&bar[0], 1);
+    sm100::mbar_init(&bar[1], 1);
+    sm100::fence_barrier_init();
+  }
+  __syncthreads();
+  auto issue = [&](int i) {  // thread 0: row blockIdx.x + i * gridDim.x into buffer i & 1
+    const int r = static_cast<int>(blockIdx.x) + i * static_cast<int>(gridDim.x);
+    if (r >= rows) return;
+    sm100::mbar_arrive_expect_tx(&bar[i & 1], rowb);
+    sm100::bulk_load(xsm + (i & 1) * rowb_al, logits + static_cast<size_t>(r) * V, rowb, &bar[i & 1]);
+  };
+  if (threadIdx.x == 0) {
+    issue(0);
+    issue(1);
+  }
+  for (int i = 0;; ++i) {
+    const int r = static_cast<int>(blockIdx.x) + i * static_cast<int>(gridDim.x);
+    if (r >= rows) break;
+    const uint32_t base = sm100::smem_u32(xsm + (i & 1) * rowb_al);
+    sm100::mbar_wait(&bar[i & 1], (i >> 1) & 1);
+    float m = -INFINITY;
+    for (int c = threadIdx.x; c < V8; c += kXentPipeThreads) {
+      const uint4 u = sm100::ld_shared_v4(base + 16 * c);
+      const uint32_t q[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) m = fmaxf(m, fmaxf(__uint_as_float(q[e] << 16), __uint_as_float(q[e] & 0xffff0000u)));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (l == 0) red[w] = m;
+    __syncthreads();
+    float M = red[0];
+#pragma unroll
+    for (int k = 1; k < kXentPipeThreads / 32; ++k) M = fmaxf(M, red[k]);
+    const float Ml = M * kL2e;
+    float sum = 0.f;
+    for (int c = threadIdx.x; c < V8; c += kXentPipeThreads) {
+      const uint4 u = sm100::ld_shared_v4(base + 16 * c);
+      const uint32_t q[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        sum += exp2f(fmaf(__uint_as_float(q[e] << 16), kL2e, -Ml)) +
+               exp2f(fmaf(__uint_as_float(q[e] & 0xffff0000u), kL2e, -Ml));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    __syncthreads();  // red[] (max) consumed
+    if (l == 0) red[w] = sum;
+    __syncthreads();
+    float S = 0.f;
+#pragma unroll
+    for (int k = 0; k < kXentPipeThreads / 32; ++k) S += red[k];
+    const float lse = M + __logf(S);
+    const int y = labels[r];
+    if (threadIdx.x == 0) {
+      uint16_t hy;
+      asm volatile("ld.shared.u16 %0, [%1];" : "=h"(hy) : "r"(base + 2u * static_cast<uint32_t>(y)));
+      row_loss[r] = static_cast<double>(lse) - static_cast<double>(__uint_as_float(static_cast<uint32_t>(hy) << 16));
+    }
+    if (grad) {
+      const float Ll = lse * kL2e;
+      uint4* dst = reinterpret_cast<uint4*>(logits + static_cast<size_t>(r) * V);
+      for (int c = threadIdx.x; c < V8; c += kXentPipeThreads) {
+        const uint4 u = sm100::ld_shared_v4(base + 16 * c);
+        const uint32_t q[4] = {u.x, u.y, u.z, u.w};
+        uint32_t o[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int j = 8 * c + 2 * e;
+          const float g0 = (exp2f(fmaf(__uint_as_float(q[e] << 16), kL2e, -Ll)) - (j == y ? 1.f : 0.f)) * gscale;
+          const float g1 =
+              (exp2f(fmaf(__uint_as_float(q[e] & 0xffff0000u), kL2e, -Ll)) - (j + 1 == y ? 1.f : 0.f)) * gscale;
+          const __nv_bfloat162 b = __floats2bfloat162_rn(g0, g1);
+          o[e] = *reinterpret_cast<const uint32_t*>(&b);
+        }
+        dst[c] = make_uint4(o[0], o[1], o[2], o[3]);
+      }
+    }
+    __syncthreads();  // buffer i & 1 and red[] free
+    if (threadIdx.x == 0) issue(i + 2);
+  }
+}
+
 __global__ void fold_mean_kernel(const double* __restrict__ v, size_t n, double scale, double* __restrict__ out) {
   double acc = 0.0;
   for (size_t i = threadIdx.x; i < n; i += 1024) acc += v[i];
@@ -543,6 +724,39 @@ void swiglu_bwd(const bf16* gu, const bf16* da, size_t ntok, size_t f, bf16* dgu
 void xent_bf16(bf16* logits, const int* labels, size_t rows, size_t V, float grad_scale, int grad, double* row_loss,
                cudaStream_t s) {
   if (rows == 0) return;
+  const size_t v8 = V / 8, per = (v8 + kXentThreads - 1) / kXentThreads;
+  const int vi = static_cast<int>(V);
+  const size_t pipe_smem = 2 * ((V * 2 + 127) / 128 * 128) + 16 + 64 + 128;
+  if (V % 8 == 0 && pipe_smem <= 227 * 1024 && rows < (1u << 31)) {
+    static int sms = 0;
+    static size_t attr = 0;
+    if (!sms) {
+      int dev = 0;
+      CKF_CUDA(cudaGetDevice(&dev));
+      CKF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    if (pipe_smem > attr) {
+      CKF_CUDA(cudaFuncSetAttribute(xent_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(pipe_smem)));
+      attr = pipe_smem;
+    }
+    const unsigned grid = static_cast<unsigned>(std::min<size_t>(rows, static_cast<size_t>(sms)));
+    xent_pipe_kernel<<<grid, kXentPipeThreads, pipe_smem, s>>>(logits, labels, static_cast<int>(rows), vi, grad_scale,
+                                                             grad, row_loss);
+    CKF_LAUNCH_CHECK();
+    return;
+  }
+  if (V % 8 == 0 && per <= 16) {
+#define CKF_XENT_CASE(N)                                                                                          \
+  if (per <= N) {                                                                                                  \
+    xent_reg_kernel<N><<<static_cast<unsigned>(rows), kXentThreads, 0, s>>>(logits, labels, vi, grad_scale, grad, \
+                                                                         row_loss);                               \
+    CKF_LAUNCH_CHECK();                                                                                            \
+    return;                                                                                                        \
+  }
+    CKF_XENT_CASE(1) CKF_XENT_CASE(2) CKF_XENT_CASE(4) CKF_XENT_CASE(8) CKF_XENT_CASE(13) CKF_XENT_CASE(16)
+#undef CKF_XENT_CASE
+  }
   xent_kernel<<<static_cast<unsigned>(rows), kXentThreads, 0, s>>>(logits, labels, V, grad_scale, grad, row_loss);
   CKF_LAUNCH_CHECK();
 }
