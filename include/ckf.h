@@ -268,6 +268,10 @@ int ckf_engine_set_schedule(ckf_engine_t e, int mode);
  * execution order run as one forward+backward of up to `cap` microbatches (same
  * arithmetic as pipeline.cpp:66-83; 0 = as many as HBM allows (default), 1 = off) */
 int ckf_engine_set_group_cap(ckf_engine_t e, int cap);
+/* device time of the last ckf_engine_run_iteration, CUDA events on the engine stream from its
+ * first device operation (the input H2D copy when the batch is on the host) to the loss /
+ * omega D2H copies -- host scheduling after the step is excluded */
+int ckf_engine_last_step_ms(ckf_engine_t e, float* ms);
 /* Hop log for a VIRTUAL placement (stage -> rank), used to check on one GPU that
  * the engine's stage transfers match ckf_pipeline_plan: when enabled, every
  * cross-rank transfer the placement implies is recorded as (src, dst, bytes). */

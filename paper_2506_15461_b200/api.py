@@ -308,6 +308,12 @@ class Engine:
     def sync(self):
         check(lib().ckf_engine_sync(self._h))
 
+    def last_step_ms(self) -> float:
+        """Device time of the last run_iteration (CUDA events on the engine stream)."""
+        ms = C.c_float()
+        check(lib().ckf_engine_last_step_ms(self._h, C.byref(ms)))
+        return ms.value
+
     def set_group_cap(self, cap: int):
         """Microbatch fusion cap (0 = fit to HBM, 1 = one microbatch per pass)."""
         check(lib().ckf_engine_set_group_cap(self._h, cap))

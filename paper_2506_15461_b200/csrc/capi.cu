@@ -598,6 +598,10 @@ int ckf_engine_set_schedule(ckf_engine_t e, int mode) {
   return guard([&] { E(e)->set_schedule(mode); });
 }
 
+int ckf_engine_last_step_ms(ckf_engine_t e, float* ms) {
+  return guard([&] { *ms = E(e)->last_step_ms(); });
+}
+
 int ckf_engine_set_group_cap(ckf_engine_t e, int cap) {
   return guard([&] { E(e)->set_group_cap(cap); });
 }

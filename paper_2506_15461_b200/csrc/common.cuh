@@ -19,6 +19,14 @@ struct Error : std::runtime_error {
   Error(int c, const std::string& m, long it = -1) : std::runtime_error(m), code(c), iteration(it) {}
 };
 
+// Bumped whenever a device buffer that a captured CUDA graph could reference is
+// (re)allocated (engine workspace slots, GEMM split-K scratch, RoPE tables): a graph
+// captured under another epoch is stale.
+inline long& alloc_epoch() {
+  static long e = 0;
+  return e;
+}
+
 [[noreturn]] inline void raise(int code, const std::string& msg, long it = -1) { throw Error(code, msg, it); }
 
 inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {

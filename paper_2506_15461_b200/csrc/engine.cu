@@ -98,6 +98,7 @@ Engine::Engine(const ckf_model_desc& in) {
   d_.T = in.seq_len ? in.seq_len : 1;
   d_.max_rows = in.max_rows ? in.max_rows : 256;
   if (const char* g = std::getenv("CKF_MB_GROUP")) group_cap_ = std::max(0, std::atoi(g));
+  if (const char* g = std::getenv("CKF_GRAPHS")) graphs_ = g[0] != '0';
   d_.device = in.device;
   if (d_.block != CKF_BLOCK_MLP && d_.block != CKF_BLOCK_LLAMA) raise(1, "unknown block kind");
   if (d_.prec < CKF_FP64 || d_.prec > CKF_BF16) raise(1, "unknown precision");
@@ -126,6 +127,8 @@ Engine::Engine(const ckf_model_desc& in) {
   CKF_CUDA(cudaMemset(scal_, 0, 4096 * sizeof(double)));
   CKF_CUDA(cudaEventCreate(&ev0_));
   CKF_CUDA(cudaEventCreate(&ev1_));
+  CKF_CUDA(cudaEventCreate(&sb_ev_));
+  CKF_CUDA(cudaEventCreate(&se_ev_));
 
   impl_ = d_.block == CKF_BLOCK_MLP ? make_mlp_block(this) : make_llama_block(this);
   const bool lowp = d_.prec == CKF_BF16;
@@ -149,9 +152,12 @@ Engine::~Engine() {
   cudaFree(scal_);
   if (dp_comm_ && nccl().CommDestroy) nccl().CommDestroy(dp_comm_);
   if (comm_ && nccl().CommDestroy) nccl().CommDestroy(comm_);
+  if (gexec_) cudaGraphExecDestroy(gexec_);
   for (cudaEvent_t ev : kev_) cudaEventDestroy(ev);
   if (ev0_) cudaEventDestroy(ev0_);
   if (ev1_) cudaEventDestroy(ev1_);
+  if (sb_ev_) cudaEventDestroy(sb_ev_);
+  if (se_ev_) cudaEventDestroy(se_ev_);
   if (st_) cudaStreamDestroy(st_);
 }
 
@@ -189,6 +195,7 @@ void* Engine::ws(size_t bytes, int slot) {
     cudaFree(ws_[static_cast<size_t>(slot)]);
     const size_t want = std::max<size_t>(bytes, 256);
     CKF_CUDA(cudaMalloc(&ws_[static_cast<size_t>(slot)], want));
+    ++alloc_epoch();
     ws_size_[static_cast<size_t>(slot)] = want;
   }
   return ws_[static_cast<size_t>(slot)];
@@ -414,6 +421,9 @@ void Engine::run_iteration(const int* orders, int m, const void* x, const void* 
   for (auto& g : stages_)
     if (g.lr <= 0.0) raise(1, "learning rate must be positive");
   const size_t mb = rows / static_cast<size_t>(m);
+  // device-timeline bracket of the step: first device op (input H2D when from the host)
+  // .. result D2H; read back by last_step_ms()
+  CKF_CUDA(cudaEventRecord(sb_ev_, st_));
 
   const size_t xcols = d_.block == CKF_BLOCK_MLP ? d_.in : d_.T + 1;
   const size_t xelt = d_.block == CKF_BLOCK_MLP ? master_bytes() : sizeof(int);
@@ -463,7 +473,10 @@ void Engine::run_iteration(const int* orders, int m, const void* x, const void* 
   auto ok = [&](int k) { return orders + static_cast<size_t>(k) * d_.s; };
   impl_->begin_iteration(m, mb);
   size_t nloss = static_cast<size_t>(m);
-  bool resident = true;
+  bool flushed = false;
+  // fusion needs every stage on this rank, the sequential schedule, and no virtual placement
+  // (hop logging emulates a partitioned pipeline's transfers on one GPU)
+  bool resident = schedule_ == 0 && !log_hops_;
   for (size_t i = 0; i < d_.s; ++i) resident = resident && mine(owner_of_stage(static_cast<int>(i + 1)));
   const int gsz = resident ? fused_group_size(m, mb) : 1;
   if (gsz > 1) {
@@ -489,6 +502,7 @@ void Engine::run_iteration(const int* orders, int m, const void* x, const void* 
         groups.emplace_back(c.begin() + static_cast<long>(i),
                             c.begin() + static_cast<long>(std::min(c.size(), i + static_cast<size_t>(gsz))));
     const size_t xrow = mb * xcols * xelt;
+    auto body = [&]() {
     impl_->loss_rows = mb;
     int woff = 0;
     for (size_t j = 0; j < groups.size(); ++j) {
@@ -508,6 +522,47 @@ void Engine::run_iteration(const int* orders, int m, const void* x, const void* 
       woff += static_cast<int>(g.size());
     }
     impl_->loss_rows = 0;
+    impl_->flush_grads();
+    };
+    // The fused step is a fixed launch sequence: after one eager pass with the same shape,
+    // inputs and buffers, it is captured once as a CUDA graph and replayed (one launch per
+    // iteration instead of ~300; Adam stays outside because its scalars change every step).
+    // Any workspace reallocation (alloc_epoch) or a different order / group layout re-captures.
+    const bool want_graph = graphs_ && !kt_on_;
+    std::vector<long> key;
+    if (want_graph) {
+      key = {m, static_cast<long>(mb), static_cast<long>(reinterpret_cast<intptr_t>(xd)), gsz, alloc_epoch(),
+             impl_->state_token()};
+      for (int k = 0; k < m; ++k) key.insert(key.end(), ok(k), ok(k) + d_.s);
+    }
+    if (want_graph && gexec_ && key == gkey_) {
+      CKF_CUDA(cudaGraphLaunch(gexec_, st_));
+    } else if (want_graph && key == gseen_) {
+      if (gexec_) {
+        cudaGraphExecDestroy(gexec_);
+        gexec_ = nullptr;
+      }
+      cudaGraph_t graph = nullptr;
+      CKF_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
+      try {
+        body();
+      } catch (...) {
+        cudaStreamEndCapture(st_, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        graphs_ = false;
+        throw;
+      }
+      CKF_CUDA(cudaStreamEndCapture(st_, &graph));
+      CKF_CUDA(cudaGraphInstantiate(&gexec_, graph, 0));
+      CKF_CUDA(cudaGraphDestroy(graph));
+      gkey_ = key;
+      gkey_[4] = alloc_epoch();  // (capture allocates nothing; kept exact anyway)
+      CKF_CUDA(cudaGraphLaunch(gexec_, st_));
+    } else {
+      body();
+      if (want_graph) gseen_ = key;
+    }
+    flushed = true;
     nloss = groups.size();
   } else if (schedule_ == 0) {
     for (int k = 0; k < m; ++k) impl_->microbatch(k, ok(k), xk(k), yk(k), mb, true, scal_ + k);
@@ -524,7 +579,7 @@ void Engine::run_iteration(const int* orders, int m, const void* x, const void* 
       impl_->mb_backward(k, ok(k), xk(k), mb);
     }
   }
-  impl_->flush_grads();
+  if (!flushed) impl_->flush_grads();
   // data parallelism: sum every owned group's gradient over the replicas (each replica ran
   // its own m microbatches of the global batch), then Adam with 1/(m*R)
   if (replicas_ > 1) {
@@ -542,6 +597,7 @@ void Engine::run_iteration(const int* orders, int m, const void* x, const void* 
   std::vector<double> om(d_.s);
   CKF_CUDA(cudaMemcpyAsync(losses.data(), scal_, nloss * sizeof(double), cudaMemcpyDeviceToHost, st_));
   CKF_CUDA(cudaMemcpyAsync(om.data(), scal_ + 2048, d_.s * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  CKF_CUDA(cudaEventRecord(se_ev_, st_));
   CKF_CUDA(cudaStreamSynchronize(st_));
   kt_collect();
   double total = 0.0;
@@ -570,6 +626,13 @@ void Engine::run_iteration(const int* orders, int m, const void* x, const void* 
   if (loss) *loss = total;
   if (omegas)
     for (size_t i = 0; i < d_.s; ++i) omegas[i] = stages_[i].omega;
+}
+
+float Engine::last_step_ms() {
+  CKF_CUDA(cudaEventSynchronize(se_ev_));
+  float ms = 0.f;
+  CKF_CUDA(cudaEventElapsedTime(&ms, sb_ev_, se_ev_));
+  return ms;
 }
 
 void Engine::upload(const void* x, const void* y, size_t rows, const void** xd, const void** yd) {

@@ -103,6 +103,8 @@ struct BlockImpl {
   virtual size_t group_bytes_per_token() const { return 0; }
   // device bytes the block will still allocate this iteration (e.g. deferred-gradient inputs)
   virtual size_t reserved_bytes() const { return 0; }
+  // block state that changes the launch sequence of an iteration (part of the CUDA-graph key)
+  virtual long state_token() const { return 0; }
   int wk = 0;  // position of the current microbatch within the iteration (in microbatches)
   // Rows of ONE microbatch when a call carries a fused group of several (the
   // loss and its gradient stay per-microbatch means, pipeline.cpp:66-83); 0 = rows.
@@ -170,6 +172,9 @@ class Engine {
   // microbatches that share an execution order run as ONE forward + backward of
   // up to group_cap microbatches (0 = as many as HBM allows, 1 = off).
   void set_group_cap(int cap) { group_cap_ = cap < 0 ? 0 : cap; }
+  void set_graphs(bool on) { graphs_ = on; }
+  // device time (ms) of the last run_iteration: first device op .. loss / omega D2H
+  float last_step_ms();
   int group_cap() const { return group_cap_; }
   // move `bytes` of `buf` from rank src to rank dst (NCCL send/recv on the engine stream)
   void hop(void* buf, size_t bytes, int src, int dst);
@@ -219,6 +224,10 @@ class Engine {
   int rank_ = 0, nranks_ = 1;
   int schedule_ = 0;
   int group_cap_ = 0;
+  // CUDA graph of the fused (all stages resident) step: key = shape, inputs, orders, alloc epoch
+  bool graphs_ = true;
+  cudaGraphExec_t gexec_ = nullptr;
+  std::vector<long> gkey_, gseen_;
   std::vector<std::pair<size_t, int>> group_fit_;  // (microbatch tokens, fitted group size)
   int fused_group_size(int m, size_t mb_rows);
   int replicas_ = 1, replica_ = 0;
@@ -229,6 +238,7 @@ class Engine {
   std::vector<int> stage_rank_;
   void* comm_ = nullptr;  // ncclComm_t
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
+  cudaEvent_t sb_ev_ = nullptr, se_ev_ = nullptr;  // run_iteration device-timeline bracket
   bool kt_on_ = false;
   std::vector<cudaEvent_t> kev_;
   size_t kev_used_ = 0;

@@ -522,7 +522,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int n0 = w.nb * BN + c0;
           if (p.splits > 1) {
             // split-K: this split's partial tile goes to its workspace slot (plain store)
-            tma_store_2d(&tmap_ws, sb, c0, (w.split * p.tiles + w.tile) * BM + q * 32);
+            // (CTA pair: each CTA's 128-row half-tile is its own slot)
+            tma_store_2d(&tmap_ws, sb, c0, ((w.split * p.tiles + w.tile) * NCTA + static_cast<int>(rank)) * BM + q * 32);
           } else if (n0 < p.N && m0 < p.M) {
             if constexpr (EPI == kAccF32)
               tma_reduce_add_2d(&tmap_c, sb, n0, m0);
@@ -539,7 +540,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // 1) every warp publishes its stored partial rows, 2) once all 4*splits warps of the
         // tile have, the tile's rows are shared out among them and each sums the partials in
         // split order and adds the result into C.
-        int* stored = p.flags + 2 * w.tile;
+        const int ht = w.tile * NCTA + static_cast<int>(rank);  // half-tile of a CTA pair
+        int* stored = p.flags + 2 * ht;
         int* reduced = stored + 1;
         const int nwarps = 4 * p.splits;
         if (lane == 0) {
@@ -553,7 +555,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int wid = w.split * 4 + q;
         const int per = (BM + nwarps - 1) / nwarps;
         for (int rr = wid * per; rr < min(BM, (wid + 1) * per); ++rr) {
-          const int m = w.mb * BM + rr;
+          const int m = w.mb * BM * NCTA + static_cast<int>(rank) * BM + rr;
           if (m >= p.M) break;
           for (int c = lane * 4; c < BN; c += 128) {
             const int n = w.nb * BN + c;
@@ -565,7 +567,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int sp = 0; sp < kMaxSplits; ++sp)
               if (sp < p.splits)
                 part[sp] = __ldcg(reinterpret_cast<const float4*>(
-                    p.ws + ((static_cast<size_t>(sp) * p.tiles + w.tile) * BM + rr) * BN + c));
+                    p.ws + (((static_cast<size_t>(sp) * p.tiles + w.tile) * NCTA + rank) * BM + rr) * BN + c));
             float4* dst = reinterpret_cast<float4*>(p.C + static_cast<size_t>(m) * p.ldc + n);
             float4 o = *dst;
             float4 acc4 = part[0];
@@ -630,6 +632,7 @@ float* split_workspace(size_t bytes) {
     if (ws) CKF_CUDA(cudaFree(ws));
     cap = std::max<size_t>(bytes, 32u << 20);
     CKF_CUDA(cudaMalloc(&ws, cap));
+    ++alloc_epoch();
   }
   return ws;
 }
@@ -645,6 +648,7 @@ int* split_flags(size_t n) {
     if (flags && cur == dev) CKF_CUDA(cudaFree(flags));
     cap = std::max<size_t>(n, 4096);
     CKF_CUDA(cudaMalloc(&flags, cap * sizeof(int)));
+    ++alloc_epoch();
     CKF_CUDA(cudaMemset(flags, 0, cap * sizeof(int)));
     dev = cur;
   }
@@ -675,10 +679,11 @@ void launch_t(const GemmDesc& g, int splits, cudaStream_t s) {
   p.kb_per_split = (p.nk + p.splits - 1) / p.splits;
   p.splits = (p.nk + p.kb_per_split - 1) / p.kb_per_split;  // no empty split
   p.units = p.tiles * p.splits;
-  if (p.splits > 1 && (NCTA != 1 || p.units > num_sms() || EPI != kAccF32 || g.N % 4 != 0))
+  // split-K needs every unit co-resident (units <= CTAs or CTA pairs in flight)
+  if (p.splits > 1 && (p.units > num_sms() / NCTA || EPI != kAccF32 || g.N % 4 != 0))
     p.splits = 1, p.units = p.tiles, p.kb_per_split = p.nk;
-  p.flags = p.splits > 1 ? split_flags(2 * static_cast<size_t>(p.tiles)) : nullptr;
-  p.ws = p.splits > 1 ? split_workspace(static_cast<size_t>(p.units) * BM * BN * sizeof(float)) : nullptr;
+  p.flags = p.splits > 1 ? split_flags(2 * static_cast<size_t>(p.tiles) * NCTA) : nullptr;
+  p.ws = p.splits > 1 ? split_workspace(static_cast<size_t>(p.units) * NCTA * BM * BN * sizeof(float)) : nullptr;
   p.C = static_cast<float*>(g.C);
   p.ldc = g.ldc;
   p.rope_tab = g.rope_tab;
@@ -695,7 +700,7 @@ void launch_t(const GemmDesc& g, int splits, cudaStream_t s) {
   }
   if (g.rope_tab && (EPI != kStoreBF16 || g.rope_T <= 0 || g.rope_cols % 64))
     raise(1, "gemm_bf16: fused RoPE needs the bf16 epilogue and 64-column heads");
-  const CUtensorMap twm = p.splits > 1    ? tma::make_2d_f32(p.ws, BN, static_cast<uint64_t>(p.units) * BM, BN, 32, 32)
+  const CUtensorMap twm = p.splits > 1    ? tma::make_2d_f32(p.ws, BN, static_cast<uint64_t>(p.units) * NCTA * BM, BN, 32, 32)
                           : EPI == kSwiGLU    ? tma::make_2d_bf16(g.aux, g.N / 2, g.M, g.ldaux, 64, 32)
                           : EPI == kSwiGLUBwd ? tma::make_2d_bf16(g.aux, 2 * g.N, g.M, g.ldaux, 64, 32)
                                               : tcm;
@@ -772,6 +777,20 @@ void gemm_bf16(const GemmDesc& g, cudaStream_t s) {
     return v ? std::atoi(v) : 0;
   }();
   if (splits <= 0 && env_splits > 0) splits = env_splits;
+  static const bool pair_ok = [] {  // CKF_GEMM_PAIR=0: single-CTA tiles only
+    const char* v = std::getenv("CKF_GEMM_PAIR");
+    return !(v && v[0] == '0');
+  }();
+  // weight gradients (fp32 accumulate, M = fan_in small, K = tokens long): CTA-pair 256 x 256
+  // tiles split along K until the 74 pairs are busy (4x the MMA work per staged byte of the
+  // single-CTA 128 x 128 split tiles)
+  const bool pair_wgrad = pair_ok && !g.bn && g.epi == kAccF32 && g.M >= 2 * BM && g.M <= 4096;
+  if (splits <= 0 && pair_wgrad) {
+    const int pairs = num_sms() / 2, nk = (g.K + BK - 1) / BK;
+    const int pt = ((g.M + 2 * BM - 1) / (2 * BM)) * ((g.N + 255) / 256);
+    splits = pt * 3 < pairs * 2 ? std::max(1, std::min({pairs / pt, nk / 4, 16})) : 1;
+    bn = 256;
+  }
   if (splits <= 0) {
     splits = 1;
     if (g.epi == kAccF32) {
@@ -794,14 +813,11 @@ void gemm_bf16(const GemmDesc& g, cudaStream_t s) {
   // stages half the B bytes per MMA FLOP in a 6-deep ring.  Measured on B200
   // (profiles/r01_gemm_pair_vs_single.jsonl): +3-4 % on the stage GEMMs; single CTAs stay ahead
   // for the fused SwiGLU epilogues and for N <= 512 with very short or very long K.
-  static const bool pair_ok = [] {
-    const char* v = std::getenv("CKF_GEMM_PAIR");
-    return !(v && v[0] == '0');
-  }();
-  const bool pair_shape = g.epi != kSwiGLU && g.epi != kSwiGLUBwd && !(g.N <= 512 && (g.K <= 512 || g.K >= 16384));
+  const bool pair_shape = pair_wgrad || (g.epi != kSwiGLU && g.epi != kSwiGLUBwd && splits <= 1 &&
+                                         !(g.N <= 512 && (g.K <= 512 || g.K >= 16384)));
   if (bn == 128)
     dispatch_bn<128, 1>(g, splits, s);
-  else if (pair_ok && pair_shape && splits <= 1 && g.M >= 2 * BM)
+  else if (pair_ok && pair_shape && g.M >= 2 * BM)
     dispatch_bn<256, 2>(g, splits, s);
   else
     dispatch_bn<256, 1>(g, splits, s);

@@ -232,6 +232,7 @@ struct LlamaBlock final : BlockImpl {
   }
   size_t reserve_ = 0;
   size_t reserved_bytes() const override { return reserve_; }
+  long state_token() const override { return (defer_ ? 1 : 0) | (fuse_swiglu() ? 2 : 0); }
   // per token of a fused group: the activation cache of every resident layer
   // (cache(): h_in, h_mid, rstd1/2, lse, qkv, gu; the X inputs live in the
   // deferred buffers), bf16 logits, and the per-call fp32 / bf16 scratch

@@ -690,6 +690,7 @@ const float2* rope_table(size_t T, size_t hd, cudaStream_t s) {
     if (t.T == T && t.hd == hd && t.dev == dev) return t.p;
   float2* tab = nullptr;
   CKF_CUDA(cudaMalloc(&tab, T * hd / 2 * sizeof(float2)));
+  ++alloc_epoch();
   rope_table_kernel<<<static_cast<unsigned>((T * hd / 2 + 255) / 256), 256, 0, s>>>(tab, static_cast<int>(T),
                                                                                    static_cast<int>(hd));
   CKF_LAUNCH_CHECK();

@@ -69,9 +69,11 @@ def test_stage_shapes_and_alpha():
     assert _run(512, 1536, 8192, True, True, 2) < 1e-3
 
 
-@pytest.mark.parametrize("shape", [(300, 200, 2000), (512, 512, 8192), (2048, 512, 8192)])
+@pytest.mark.parametrize("shape", [(300, 200, 2000), (512, 512, 8192), (2048, 512, 8192), (512, 4096, 16384),
+                                   (512, 1536, 65536), (384, 640, 4096)])
 def test_split_k_accumulate(shape):
-    # few output tiles + long K -> ordered split-K with TMA reduce-add (deterministic)
+    # few output tiles + long K -> split-K (CTA pairs when M >= 256) with an ordered, deterministic
+    # workspace reduction
     M, N, K = shape
     assert _run(M, N, K, True, True, 2) < 1e-3
 
