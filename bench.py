@@ -403,7 +403,17 @@ def run_ours(args, w: dict):
     else:
         achieved = kby / (kms / 1e3) / 1e9
         roof = {"bound": "hbm", "unit": "GB/s", "peak": peaks["hbm_gbs"]}
-    roof.update(kernel_class=dom, achieved=achieved, frac=achieved / roof["peak"], traffic=None,
+    # measured DRAM traffic per launch of the dominant class: ncu capture committed under
+    # profiles/ (tools/ncu_traffic.py; same workload, one step's launches)
+    traffic, traffic_src = None, None
+    tp = os.path.join(ROOT, "profiles", f"r01_{dom}_dram_traffic.json")
+    if os.path.exists(tp) and args.workload == DEFAULT_WORKLOAD:
+        with open(tp) as f:
+            tj = json.load(f)
+        traffic = tj.get("traffic_per_launch_bytes")
+        traffic_src = f"profiles/{os.path.basename(tp)} ({tj.get('launches')} launches, ncu dram__bytes_read+write)"
+    roof.update(kernel_class=dom, achieved=achieved, frac=achieved / roof["peak"], traffic=traffic,
+                traffic_source=traffic_src,
                 peak_source=peak_src, launches=kn, share_of_step=kms / ms_prof,
                 timing="CUDA events around each launch on the engine stream, separate pass of the same steps",
                 per_launch={"ms": kms / max(kn, 1), "flops": kfl / max(kn, 1), "bytes": kby / max(kn, 1)},
