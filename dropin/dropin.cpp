@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstring>
 #include <fstream>
 #include <iterator>
 #include <map>
@@ -700,6 +701,157 @@ double reduction_error(const ParameterVector& w_prev, const ParameterVector& w_f
   const ParameterVector r = recover_checkfree(w_prev, w_next, omega_prev, omega_next);
   if (!r.same_shape(w_failed)) throw ConfigError("failed stage weights differ in shape");
   return kernels::sum_squared_diff(r.ptr(), w_failed.ptr(), r.size());
+}
+
+// ---- checkpointing baseline: value-semantics snapshot (checkpoint.cpp:70-83) and the
+//      "ckfree-ckpt v1" byte container (checkpoint.cpp:85-179), little-endian host
+CheckpointSnapshot checkpoint_save(const ModelState& model, long iteration, std::uint64_t data_cursor) {
+  return CheckpointSnapshot{iteration, data_cursor, model};
+}
+
+void checkpoint_restore(const CheckpointSnapshot& snapshot, ModelState& model, long& iteration,
+                        std::uint64_t& data_cursor) {
+  model = snapshot.model;
+  iteration = snapshot.iteration;
+  data_cursor = snapshot.data_cursor;
+}
+
+namespace {
+const std::string kCkptHeader = "ckfree-ckpt v1\n";
+
+class CkptWriter {
+ public:
+  void word(std::uint64_t v) {
+    for (int i = 0; i < 8; ++i) bytes.push_back(static_cast<std::uint8_t>(v >> (8 * i)));
+  }
+  void doubles(const double* p, std::size_t n) {  // length prefix, then the raw f64 bits
+    word(n);
+    for (std::size_t i = 0; i < n; ++i) {
+      std::uint64_t b;
+      std::memcpy(&b, p + i, 8);
+      word(b);
+    }
+  }
+  void doubles(const std::vector<double>& v) { doubles(v.data(), v.size()); }
+  std::vector<std::uint8_t> bytes;
+};
+
+class CkptReader {
+ public:
+  explicit CkptReader(const std::vector<std::uint8_t>& b) : b_(b) {}
+  std::uint64_t word() {
+    if (at_ + 8 > b_.size()) throw ParseError("checkpoint: truncated integer");
+    std::uint64_t v = 0;
+    for (int i = 7; i >= 0; --i) v = (v << 8) | b_[at_ + static_cast<std::size_t>(i)];
+    at_ += 8;
+    return v;
+  }
+  std::vector<double> doubles(std::size_t expect) {
+    const std::uint64_t n = word();
+    if (n != expect)
+      throw ParseError("checkpoint: array length " + std::to_string(n) + ", expected " + std::to_string(expect));
+    std::vector<double> v(n);
+    for (auto& x : v) {
+      const std::uint64_t bits = word();
+      std::memcpy(&x, &bits, 8);
+    }
+    return v;
+  }
+  bool done() const { return at_ == b_.size(); }
+  std::size_t at_ = 0;
+
+ private:
+  const std::vector<std::uint8_t>& b_;
+};
+}  // namespace
+
+std::vector<std::uint8_t> serialize_checkpoint(const CheckpointSnapshot& snapshot) {
+  const ModelState& m = snapshot.model;
+  CkptWriter w;
+  w.bytes.assign(kCkptHeader.begin(), kCkptHeader.end());
+  w.word(static_cast<std::uint64_t>(snapshot.iteration));
+  const EdgeState& e = m.edges;
+  w.doubles(e.layers.embed.values());
+  w.doubles(e.opt_embed.m);
+  w.doubles(e.opt_embed.v);
+  w.doubles(e.layers.deembed.values());
+  w.doubles(e.opt_deembed.m);
+  w.doubles(e.opt_deembed.v);
+  w.doubles(std::vector<double>{static_cast<double>(e.opt_embed.step), static_cast<double>(e.opt_deembed.step), e.lr});
+  for (const StageState& st : m.stages) w.doubles(st.flat_weights().values());
+  for (const StageState& st : m.stages) {
+    w.doubles(st.opt.m);
+    w.doubles(st.opt.v);
+    w.doubles(std::vector<double>{static_cast<double>(st.opt.step), st.omega, st.lr});
+  }
+  w.word(snapshot.data_cursor);
+  return std::move(w.bytes);
+}
+
+CheckpointSnapshot deserialize_checkpoint(const std::vector<std::uint8_t>& bytes, const ModelSpec& spec) {
+  if (bytes.size() < kCkptHeader.size() || !std::equal(kCkptHeader.begin(), kCkptHeader.end(), bytes.begin()))
+    throw ParseError("checkpoint: missing 'ckfree-ckpt v1' header");
+  CkptReader r(bytes);
+  r.at_ = kCkptHeader.size();
+  CheckpointSnapshot snap;
+  snap.iteration = static_cast<long>(r.word());
+  ModelState& m = snap.model;
+  m.spec = spec;
+  EdgeState& e = m.edges;
+  const std::size_t ne = spec.input_dim * spec.model_dim, nd = spec.model_dim * spec.output_dim;
+  e.layers.embed = ParameterVector(r.doubles(ne), {spec.input_dim, spec.model_dim});
+  e.opt_embed.m = r.doubles(ne);
+  e.opt_embed.v = r.doubles(ne);
+  e.layers.deembed = ParameterVector(r.doubles(nd), {spec.model_dim, spec.output_dim});
+  e.opt_deembed.m = r.doubles(nd);
+  e.opt_deembed.v = r.doubles(nd);
+  const std::vector<double> es = r.doubles(3);
+  e.opt_embed.step = static_cast<long>(es[0]);
+  e.opt_deembed.step = static_cast<long>(es[1]);
+  e.lr = es[2];
+  m.stages.resize(spec.num_stages);
+  for (std::size_t i = 0; i < spec.num_stages; ++i) {
+    StageState& st = m.stages[i];
+    st.stage_id = static_cast<int>(i + 1);
+    st.blocks.resize(spec.stage_range(st.stage_id).count());
+    for (ResidualBlock& b : st.blocks) {
+      b.w1 = ParameterVector::zeros({spec.model_dim, spec.hidden_dim});
+      b.w2 = ParameterVector::zeros({spec.hidden_dim, spec.model_dim});
+    }
+    const std::size_t n = st.param_count();
+    st.set_flat_weights(ParameterVector(r.doubles(n), {n}));
+  }
+  for (StageState& st : m.stages) {
+    st.opt.m = r.doubles(st.param_count());
+    st.opt.v = r.doubles(st.param_count());
+    const std::vector<double> sc = r.doubles(3);
+    st.opt.step = static_cast<long>(sc[0]);
+    st.omega = sc[1];
+    st.lr = sc[2];
+  }
+  snap.data_cursor = r.word();
+  if (!r.done()) throw ParseError("checkpoint: trailing bytes after data cursor");
+  return snap;
+}
+
+void save_checkpoint_file(const CheckpointSnapshot& snapshot, const std::string& path) {
+  const std::vector<std::uint8_t> b = serialize_checkpoint(snapshot);
+  std::FILE* f = std::fopen(path.c_str(), "wb");
+  if (!f) throw ConfigError("cannot open '" + path + "' for writing");
+  const std::size_t wrote = std::fwrite(b.data(), 1, b.size(), f);
+  std::fclose(f);
+  if (wrote != b.size()) throw ConfigError("short write to '" + path + "'");
+}
+
+CheckpointSnapshot load_checkpoint_file(const std::string& path, const ModelSpec& spec) {
+  std::FILE* f = std::fopen(path.c_str(), "rb");
+  if (!f) throw ConfigError("cannot open checkpoint file '" + path + "'");
+  std::vector<std::uint8_t> b;
+  std::uint8_t buf[1 << 16];
+  std::size_t got;
+  while ((got = std::fread(buf, 1, sizeof(buf), f)) > 0) b.insert(b.end(), buf, buf + got);
+  std::fclose(f);
+  return deserialize_checkpoint(b, spec);
 }
 
 }  // namespace ckfree::recovery

@@ -11,6 +11,7 @@ restates (paths relative to /root/reference/proj).
 """
 from __future__ import annotations
 
+import copy
 import math
 from dataclasses import dataclass, field
 
@@ -498,7 +499,7 @@ def _w_or_u(wp, wn, a, b):
 
 def run_experiment(cfg: dict, trace_text: str, seed: int):
     """trainer.cpp:63-119 + handle_failures :146-289 for the neighbour family,
-    no-failures and redundant.  Returns (evals[(iter, train, val)],
+    no-failures, redundant and the checkpointing baseline (:173-193, checkpoint.cpp:70-83).  Returns (evals[(iter, train, val)],
     events[(iter, stage, action, reduction_error, loss_spike)], unrecoverable)."""
     spec = Spec.from_cfg(cfg)
     kind = cfg.get("strategy", "no-failures")
@@ -538,6 +539,8 @@ def run_experiment(cfg: dict, trace_text: str, seed: int):
     if kind == "checkfree-plus":
         replica = (model.embed.copy(), model.deembed.copy())
     model_iter = 0
+    ckpt_interval = int(cfg.get("checkpoint-interval", 100))
+    snapshot = (copy.deepcopy(model), 0) if kind == "checkpointing" else None  # trainer.cpp:67-68
     unrecoverable = False
     slot = 0
     for slot in range(1, iters + 1):
@@ -547,7 +550,19 @@ def run_experiment(cfg: dict, trace_text: str, seed: int):
         model_iter += 1
         if kind == "checkfree-plus":
             replica = (model.embed.copy(), model.deembed.copy())
-        if kind != "no-failures" and slot in grouped:
+        if kind == "checkpointing" and model_iter % ckpt_interval == 0:  # trainer.cpp:83-85
+            snapshot = (copy.deepcopy(model), model_iter)
+        if kind == "checkpointing" and slot in grouped:
+            # roll every stage back (adjacent failures included); data replays by model iteration
+            stages = sorted(grouped[slot])
+            vpre = val_loss()
+            pre = [model.stages[st - 1].flat.copy() for st in stages]
+            model = copy.deepcopy(snapshot[0])
+            model_iter = snapshot[1]
+            vpost = val_loss()
+            evs += [(slot, st, "checkpoint_restore", sum_squares_fast(p0 - model.stages[st - 1].flat), vpost - vpre)
+                    for st, p0 in zip(stages, pre)]
+        elif kind != "no-failures" and slot in grouped:
             stages = sorted(grouped[slot])
             if any(b == a + 1 for a, b in zip(stages, stages[1:])):
                 evs += [(slot, st, "unrecoverable", 0.0, 0.0) for st in stages]

@@ -158,6 +158,13 @@ def trainer_goldens():
         ("checkfree_plus_swap_from_40", {"strategy": "checkfree-plus", "swap-from": 40}, trace_text(1, [1, 2, 3, 4], [(60, 1)])),
         ("s8_checkfree_plus_trace", {"strategy": "checkfree-plus", "layers": 8, "stages": 8, "iters": 60,
                                      "eval-interval": 5}, None),
+        # checkpointing baseline (trainer.cpp:173-193, checkpoint.cpp:70-83): rollback + data replay
+        ("checkpointing_s2_at50", {"strategy": "checkpointing", "checkpoint-interval": 20},
+         trace_text(1, [1, 2, 3, 4], [(50, 2)])),
+        ("checkpointing_edge_and_adjacent", {"strategy": "checkpointing", "checkpoint-interval": 15},
+         trace_text(1, [1, 2, 3, 4], [(20, 1), (47, 2), (47, 3), (80, 4)])),
+        ("checkpointing_at_snapshot", {"strategy": "checkpointing", "checkpoint-interval": 25},
+         trace_text(1, [1, 2, 3, 4], [(50, 3), (51, 3)])),
     ]
     for name, over, ttext in specs:
         cfg = dict(base)
@@ -178,6 +185,17 @@ def trainer_goldens():
 
 def main():
     os.makedirs(OUT, exist_ok=True)
+    if "--append-trainer" in sys.argv:  # add runs missing from trainer_runs.json, keep the others byte-identical
+        path = os.path.join(OUT, "trainer_runs.json")
+        with open(path) as f:
+            cur = json.load(f)
+        have = {r["name"] for r in cur["runs"]}
+        new = [r for r in trainer_goldens()["runs"] if r["name"] not in have]
+        cur["runs"].extend(new)
+        with open(path, "w") as f:
+            json.dump(cur, f, indent=1)
+        print("appended", [r["name"] for r in new])
+        return
     payload = {
         "rng": rng_goldens(),
         "failures": failure_goldens(),

@@ -153,6 +153,7 @@ Engine::~Engine() {
   if (dp_comm_ && nccl().CommDestroy) nccl().CommDestroy(dp_comm_);
   if (comm_ && nccl().CommDestroy) nccl().CommDestroy(comm_);
   if (gexec_) cudaGraphExecDestroy(gexec_);
+  for (auto& c : ckpt_) cudaFree(c.buf);
   for (cudaEvent_t ev : kev_) cudaEventDestroy(ev);
   if (ev0_) cudaEventDestroy(ev0_);
   if (ev1_) cudaEventDestroy(ev1_);
@@ -626,6 +627,82 @@ void Engine::run_iteration(const int* orders, int m, const void* x, const void* 
   if (loss) *loss = total;
   if (omegas)
     for (size_t i = 0; i < d_.s; ++i) omegas[i] = stages_[i].omega;
+}
+
+// ------------------------------------------------------------------ checkpointing baseline
+void Engine::checkpoint_save(long iteration) {
+  CKF_CUDA(cudaSetDevice(d_.device));
+  const size_t ng = d_.s + 2;
+  if (ckpt_.size() != ng) ckpt_.assign(ng, CkptGroup{});
+  auto grp = [&](size_t i) -> ParamGroup& { return i < d_.s ? stages_[i] : i == d_.s ? embed_ : deembed_; };
+  for (size_t i = 0; i < ng; ++i) {
+    ParamGroup& g = grp(i);
+    CkptGroup& c = ckpt_[i];
+    c.step = g.step;
+    c.omega = g.omega;
+    c.lr = g.lr;
+    if (!g.owned || g.n == 0) continue;
+    const size_t b = g.n * master_bytes();
+    const size_t need = 3 * b + (g.wlp ? g.n * sizeof(__nv_bfloat16) : 0);
+    if (c.bytes < need) {
+      cudaFree(c.buf);
+      CKF_CUDA(cudaMalloc(&c.buf, need));
+      c.bytes = need;
+    }
+    char* p = static_cast<char*>(c.buf);
+    CKF_CUDA(cudaMemcpyAsync(p, g.w, b, cudaMemcpyDeviceToDevice, st_));
+    CKF_CUDA(cudaMemcpyAsync(p + b, g.m, b, cudaMemcpyDeviceToDevice, st_));
+    CKF_CUDA(cudaMemcpyAsync(p + 2 * b, g.v, b, cudaMemcpyDeviceToDevice, st_));
+    if (g.wlp) CKF_CUDA(cudaMemcpyAsync(p + 3 * b, g.wlp, g.n * sizeof(__nv_bfloat16), cudaMemcpyDeviceToDevice, st_));
+  }
+  ckpt_edge_lr_ = edge_lr;
+  ckpt_iter_ = iteration;
+  ckpt_valid_ = true;
+  CKF_CUDA(cudaStreamSynchronize(st_));
+}
+
+long Engine::checkpoint_restore(const int* stages, int n_stages, double* red, float* ms) {
+  CKF_CUDA(cudaSetDevice(d_.device));
+  if (!ckpt_valid_) raise(1, "no checkpoint to restore");
+  auto grp = [&](size_t i) -> ParamGroup& { return i < d_.s ? stages_[i] : i == d_.s ? embed_ : deembed_; };
+  CKF_CUDA(cudaEventRecord(ev0_, st_));
+  for (int k = 0; k < n_stages; ++k) {  // reduction error of the failed stages (trainer.cpp:179-189)
+    const int sid = stages[k];
+    if (sid < 1 || sid > static_cast<int>(d_.s)) raise(1, "stage id out of range");
+    ParamGroup& g = stages_[static_cast<size_t>(sid - 1)];
+    if (!red || !g.owned || g.n == 0) continue;
+    if (fp64())
+      k::sum_sq_diff(static_cast<const double*>(g.w), static_cast<const double*>(ckpt_[sid - 1].buf), g.n,
+                     scal_ + 3200 + k, red_, st_);
+    else
+      k::sum_sq_diff(static_cast<const float*>(g.w), static_cast<const float*>(ckpt_[sid - 1].buf), g.n,
+                     scal_ + 3200 + k, red_, st_);
+  }
+  for (size_t i = 0; i < ckpt_.size(); ++i) {
+    ParamGroup& g = grp(i);
+    const CkptGroup& c = ckpt_[i];
+    g.step = c.step;
+    g.omega = c.omega;
+    g.lr = c.lr;
+    if (!g.owned || g.n == 0) continue;
+    const size_t b = g.n * master_bytes();
+    const char* p = static_cast<const char*>(c.buf);
+    CKF_CUDA(cudaMemcpyAsync(g.w, p, b, cudaMemcpyDeviceToDevice, st_));
+    CKF_CUDA(cudaMemcpyAsync(g.m, p + b, b, cudaMemcpyDeviceToDevice, st_));
+    CKF_CUDA(cudaMemcpyAsync(g.v, p + 2 * b, b, cudaMemcpyDeviceToDevice, st_));
+    if (g.wlp) CKF_CUDA(cudaMemcpyAsync(g.wlp, p + 3 * b, g.n * sizeof(__nv_bfloat16), cudaMemcpyDeviceToDevice, st_));
+    CKF_CUDA(cudaMemsetAsync(g.g, 0, b, st_));
+  }
+  edge_lr = ckpt_edge_lr_;
+  CKF_CUDA(cudaEventRecord(ev1_, st_));
+  std::vector<double> r(static_cast<size_t>(std::max(n_stages, 0)), 0.0);
+  if (red && n_stages > 0)
+    CKF_CUDA(cudaMemcpyAsync(r.data(), scal_ + 3200, r.size() * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  CKF_CUDA(cudaStreamSynchronize(st_));
+  if (red)
+    for (int k = 0; k < n_stages; ++k) red[k] = r[static_cast<size_t>(k)];
+  if (ms) CKF_CUDA(cudaEventElapsedTime(ms, ev0_, ev1_));
+  return ckpt_iter_;
 }
 
 float Engine::last_step_ms() {

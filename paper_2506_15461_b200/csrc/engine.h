@@ -138,6 +138,13 @@ class Engine {
   void predict_device(const int* order, const void* x_dev, size_t rows, void* pred_dev);
 
   void refresh_edge_replicas();
+  // Checkpointing baseline (recovery.hpp:88-108, checkpoint.cpp:70-83): a deep copy of every
+  // owned group's weights, Adam moments, bf16 shadow and scalars kept in HBM (device-to-device,
+  // no host round trip).  restore returns the snapshot's model iteration; *red (optional, per
+  // stage id 1..s) receives ||W_now - W_snapshot||^2 for the listed stages before the rollback.
+  void checkpoint_save(long iteration);
+  long checkpoint_restore(const int* stages, int n_stages, double* red, float* ms);
+  bool has_checkpoint() const { return ckpt_valid_; }
   void kill_stage(int sid);
   ckf_recovery_report recover_stage(int sid, int mode, int moments, double lr_bump, uint64_t reinit_seed,
                                     bool want_reduction_error);
@@ -239,6 +246,16 @@ class Engine {
   void* comm_ = nullptr;  // ncclComm_t
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
   cudaEvent_t sb_ev_ = nullptr, se_ev_ = nullptr;  // run_iteration device-timeline bracket
+  struct CkptGroup {
+    void* buf = nullptr;  // [w | m | v] master dtype, then the bf16 shadow
+    size_t bytes = 0;
+    long step = 0;
+    double omega = 0.0, lr = 0.0;
+  };
+  std::vector<CkptGroup> ckpt_;  // stages 1..s, then embed, deembed
+  double ckpt_edge_lr_ = 0.0;
+  long ckpt_iter_ = 0;
+  bool ckpt_valid_ = false;
   bool kt_on_ = false;
   std::vector<cudaEvent_t> kev_;
   size_t kev_used_ = 0;

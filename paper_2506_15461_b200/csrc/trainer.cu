@@ -79,6 +79,8 @@ class Trainer {
     const bool cfp = c_.strategy == "checkfree-plus";
     const int s = static_cast<int>(c_.stages);
     const auto std_order = host::standard_order(s);
+    const bool ckpt = c_.strategy == "checkpointing";
+    if (ckpt) model_.checkpoint_save(0);  // trainer.cpp:67-68
     if (cfp) model_.refresh_edge_replicas();
     {  // record_initial_eval (trainer.cpp:122-126)
       Batch first = make_batch(kStreamTrain, 1, c_.batch, 22);
@@ -96,6 +98,7 @@ class Trainer {
                            true, slot, &last_train_, om.data());
       ++model_iter_;
       if (cfp) model_.refresh_edge_replicas();
+      if (ckpt && model_iter_ % c_.checkpoint_interval == 0) model_.checkpoint_save(model_iter_);  // trainer.cpp:83-85
       if (c_.strategy != "no-failures") {
         auto ev = events_.find(slot);
         if (ev != events_.end() && !handle_failures(slot, ev->second)) {
@@ -180,8 +183,19 @@ class Trainer {
   // trainer.cpp:146-289 (neighbour family, redundant, no-failures)
   bool handle_failures(long slot, const std::vector<int>& stages) {
     const int s = static_cast<int>(c_.stages);
-    if (c_.strategy == "checkpointing")
-      host::fail(1, "the checkpointing baseline is not part of the B200 engine (SURVEY §8f rank 2)");
+    if (c_.strategy == "checkpointing") {
+      // trainer.cpp:173-193: roll every stage back to the last snapshot (any stage, adjacent
+      // failures included); data is addressed by model iteration, so the batches since the
+      // snapshot are replayed
+      const double vpre = val_loss();
+      std::vector<double> red(stages.size(), 0.0);
+      float ms = 0.f;
+      model_iter_ = model_.checkpoint_restore(stages.data(), static_cast<int>(stages.size()), red.data(), &ms);
+      const double vpost = val_loss();
+      for (size_t i = 0; i < stages.size(); ++i) add_event(slot, stages[i], "checkpoint_restore", red[i], 0.0, ms);
+      flush_events(vpost - vpre, true);
+      return true;
+    }
     for (size_t i = 0; i + 1 < stages.size(); ++i) {
       if (stages[i + 1] == stages[i] + 1) {
         for (int st : stages) add_event(slot, st, "unrecoverable", 0.0, 0.0, 0.0);

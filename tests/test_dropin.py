@@ -50,3 +50,29 @@ def test_reference_suite_passes_on_dropin(suite):
     cases, failed_cases, checks, failed_checks = map(int, m.groups())
     assert r.returncode == 0 and failed_cases == 0 and failed_checks == 0, tail
     assert cases > 0 and checks > 0
+
+
+def _ckpt_ref():
+    exe = os.path.join(ROOT, "oracle", "_ref", "ckpt_roundtrip_ref")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/ckpt_roundtrip_ref not built (needs /root/reference at build time)")
+    return subprocess.run([exe], capture_output=True, text=True, timeout=120)
+
+
+def test_reference_checkpoint_driver_roundtrips():
+    r = _ckpt_ref()
+    assert r.returncode == 0 and r.stdout.startswith("OK"), r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+def test_dropin_checkpoint_container_byte_identical_to_reference():
+    # tests/cpp/ckpt_roundtrip.cpp compiled against the reference and against the drop-in:
+    # same "ckfree-ckpt v1" bytes (size + digest) for the same model state, and both
+    # deserialize -> serialize to identical bytes (recovery.hpp:88-108)
+    exe = os.path.join(BIN, "ckpt_roundtrip_dropin")
+    if not os.path.exists(exe):
+        pytest.skip(f"{exe} not built")
+    want = _ckpt_ref().stdout.strip()
+    got = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert got.returncode == 0, got.stdout + got.stderr
+    assert got.stdout.strip() == want

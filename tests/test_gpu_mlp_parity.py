@@ -154,7 +154,8 @@ TRAINER_CASES = ["checkfree_s2_at50", "checkfree_plus_s1_at50", "checkfree_plus_
                  "checkfree_averaged_moments", "checkfree_plus_averaged_edge", "reinit_uniform_avg", "reinit_copy",
                  "reinit_random", "no_failures", "unrecoverable_adjacent", "checkfree_edge_unsupported",
                  "classification_checkfree", "relu_checkfree_plus", "failure_at_iter1", "checkfree_plus_swap_from_40",
-                 "s8_checkfree_plus_trace"]
+                 "s8_checkfree_plus_trace", "checkpointing_s2_at50", "checkpointing_edge_and_adjacent",
+                 "checkpointing_at_snapshot"]
 
 
 @pytest.mark.parametrize("name", TRAINER_CASES)
@@ -164,7 +165,7 @@ def test_trainer_fp64_matches_reference(trainer_goldens, name):
 
 
 @pytest.mark.parametrize("name", ["checkfree_s2_at50", "checkfree_plus_s1_at50", "checkfree_averaged_moments",
-                                  "classification_checkfree", "s8_checkfree_plus_trace"])
+                                  "classification_checkfree", "s8_checkfree_plus_trace", "checkpointing_s2_at50"])
 def test_trainer_fp32_loss_curve_within_1pct(trainer_goldens, name):
     run = next(r for r in trainer_goldens["runs"] if r["name"] == name)
     _compare_run(run, "fp32", rel_loss=1e-2, rel_red=1e-2)

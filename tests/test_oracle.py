@@ -105,7 +105,8 @@ def test_model_goldens(goldens):
 @pytest.mark.parametrize("name", ["checkfree_s2_at50", "checkfree_plus_s1_at50", "checkfree_averaged_moments",
                                   "checkfree_plus_averaged_edge", "reinit_copy", "reinit_random",
                                   "unrecoverable_adjacent", "checkfree_edge_unsupported", "classification_checkfree",
-                                  "relu_checkfree_plus", "checkfree_plus_swap_from_40"])
+                                  "relu_checkfree_plus", "checkfree_plus_swap_from_40", "checkpointing_s2_at50",
+                                  "checkpointing_edge_and_adjacent", "checkpointing_at_snapshot"])
 def test_trainer_loss_curves_match_reference(trainer_goldens, name):
     run = next(r for r in trainer_goldens["runs"] if r["name"] == name)
     cfg = dict(run["cfg"])
