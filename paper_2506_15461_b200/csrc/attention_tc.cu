@@ -16,6 +16,7 @@
 // Warp roles (256 threads): 0 TMA producer, 1 MMA issuer (one lane),
 // 2 TMEM allocator, 4..7 softmax / epilogue (query row = 32 (w-4) + lane).
 #include <cstdlib>
+#include <string>
 
 #include "common.cuh"
 #include "llama_kernels.h"
@@ -869,6 +870,460 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
   if (warp == 2) tmem_free<512>(tmem);
 }
 
+// ---------------------------------------------------------------- backward, ping-pong variant
+// Same math as the kernels above, with 64-wide inner tiles and TWO tiles in flight per CTA:
+// two S/dP TMEM buffers (128 columns each) and two groups of 4 softmax warps (group b owns
+// every tile of parity b, one TMEM lane quarter per warp).  While group b turns S(i) into
+// P / dS, the tensor core runs group 1-b's S(i+1) and the dV / dK (dQ) MMAs of tile i-1, so
+// the MMA <-> softmax hand-offs overlap instead of serialising.  TMEM: 2 x (S 64 | dP 64)
+// + 2 accumulator sets (dV|dK = 128, or dQ = 64) <= 512 columns.  Units, ordering, double-
+// buffered unit operands and the deferred unit epilogue are as in the kernels above.
+constexpr int PT = 64;                          // inner tile: queries (dK/dV kernel) or keys (dQ kernel)
+constexpr uint32_t kPTile64 = PT * HD * 2;      // 8 KiB: 64 rows x 64 hd
+constexpr uint32_t kPB = TQ * PT * 2;           // 16 KiB: P^T / dS^T [128 rows][64 cols] bf16, one SW128 chunk
+constexpr int kPPStages = 4;
+
+struct SmemKVpp {
+  uint8_t k[2][kTile], v[2][kTile];                    // unit operands (128 keys)
+  uint8_t q[kPPStages][kPTile64], d_o[kPPStages][kPTile64];
+  uint8_t p[2][kPB], ds[2][kPB];                        // per softmax group
+  float lse[kPPStages][PT], dsum[kPPStages][PT];
+  uint64_t kv_full[2], kv_empty[2], qd_full[kPPStages], qd_empty[kPPStages], s_full[2], s_free[2], pd_full[2],
+      pd_free[2], acc_full[2], acc_free[2];
+  uint32_t tmem;
+};
+
+__global__ void __launch_bounds__(kThreadsBwd, 1)
+    attn_dkdv_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv128, const __grid_constant__ CUtensorMap tm_qkv64,
+                        const __grid_constant__ CUtensorMap tm_do64, const float* __restrict__ lse,
+                        const float* __restrict__ D, int T, int H, int BH, __nv_bfloat16* __restrict__ dqkv,
+                        float scale, float scale_log2) {
+  extern __shared__ uint8_t smem_raw[];
+  SmemKVpp& sm = *reinterpret_cast<SmemKVpp*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nqb = T / TQ;
+  const int nunits = nqb * BH;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tm_qkv128);
+    tma_prefetch(&tm_qkv64);
+    tma_prefetch(&tm_do64);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm.kv_full[i], 1);
+      mbar_init(&sm.kv_empty[i], 1);
+      mbar_init(&sm.s_full[i], 1);
+      mbar_init(&sm.s_free[i], 4);
+      mbar_init(&sm.pd_full[i], 4);
+      mbar_init(&sm.pd_free[i], 1);
+      mbar_init(&sm.acc_full[i], 1);
+      mbar_init(&sm.acc_free[i], 8);
+    }
+    for (int i = 0; i < kPPStages; ++i) {
+      mbar_init(&sm.qd_full[i], 1);
+      mbar_init(&sm.qd_empty[i], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(&sm.tmem);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem;  // S^T[b] cols 128b..+63, dP^T[b] 128b+64..; acc set a: dV 256+128a, dK +64
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int g = 0, lu = 0;
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lu) {
+        const int kb = u / BH, bh = u - kb * BH, b = bh / H, h = bh - b * H;
+        const int row0 = b * T;
+        const int kbuf = lu & 1;
+        mbar_wait(&sm.kv_empty[kbuf], ((lu >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&sm.kv_full[kbuf], 2 * kTile);
+        tma_load_2d(sm.k[kbuf], &tm_qkv128, &sm.kv_full[kbuf], (H + h) * HD, row0 + kb * TK);
+        tma_load_2d(sm.v[kbuf], &tm_qkv128, &sm.kv_full[kbuf], (2 * H + h) * HD, row0 + kb * TK);
+        const int ntiles = 2 * (nqb - kb);
+        for (int i = 0; i < ntiles; ++i, ++g) {
+          const int st = g % kPPStages;
+          mbar_wait(&sm.qd_empty[st], ((g / kPPStages) & 1) ^ 1);
+          mbar_arrive_expect_tx(&sm.qd_full[st], 2 * kPTile64 + 2 * PT * 4);
+          const int q0 = kb * TK + i * PT;
+          tma_load_2d(sm.q[st], &tm_qkv64, &sm.qd_full[st], h * HD, row0 + q0);
+          tma_load_2d(sm.d_o[st], &tm_do64, &sm.qd_full[st], h * HD, row0 + q0);
+          const size_t qo = static_cast<size_t>(bh) * T + q0;
+          bulk_load(sm.lse[st], lse + qo, PT * 4, &sm.qd_full[st]);
+          bulk_load(sm.dsum[st], D + qo, PT * 4, &sm.qd_full[st]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t kIdS = idesc_bf16_f32(TK, PT, false, false);  // [keys x 64 q], K = hd
+      constexpr uint32_t kIdA = idesc_bf16_f32(TK, HD, false, true);   // [keys x hd], K = 64 q, B MN-major
+      int g = 0, lu = 0;
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lu) {
+        const int ntiles = 2 * (nqb - u / BH);
+        const int kbuf = lu & 1;
+        const uint32_t acc = tmem + 256 + static_cast<uint32_t>(kbuf * 128);
+        mbar_wait(&sm.kv_full[kbuf], (lu >> 1) & 1);
+        const uint32_t ka = smem_u32(sm.k[kbuf]), va = smem_u32(sm.v[kbuf]);
+        auto issue_s = [&](int gi) {  // S^T = K Q^T, dP^T = V dO^T of global tile gi into buffer gi & 1
+          const int st = gi % kPPStages, bb = gi & 1;
+          mbar_wait(&sm.qd_full[st], (gi / kPPStages) & 1);
+          mbar_wait(&sm.s_free[bb], ((gi >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t qa = smem_u32(sm.q[st]), oa = smem_u32(sm.d_o[st]);
+          const uint32_t sd = tmem + static_cast<uint32_t>(bb * 128);
+#pragma unroll
+          for (int k = 0; k < HD / 16; ++k) {
+            umma_bf16(sd, umma_desc_sw128(ka + k * 32, 16, 1024), umma_desc_sw128(qa + k * 32, 16, 1024), kIdS,
+                      k > 0 ? 1u : 0u);
+            umma_bf16(sd + 64, umma_desc_sw128(va + k * 32, 16, 1024), umma_desc_sw128(oa + k * 32, 16, 1024),
+                      kIdS, k > 0 ? 1u : 0u);
+          }
+          umma_commit(&sm.s_full[bb]);
+        };
+        issue_s(g);
+        issue_s(g + 1);
+        mbar_wait(&sm.acc_free[kbuf], ((lu >> 1) & 1) ^ 1);
+        for (int i = 0; i < ntiles; ++i) {
+          const int gi = g + i, st = gi % kPPStages, bb = gi & 1;
+          mbar_wait(&sm.pd_full[bb], (gi >> 1) & 1);
+          tc_fence_after();
+          const uint32_t qa = smem_u32(sm.q[st]), oa = smem_u32(sm.d_o[st]);
+          const uint32_t pa = smem_u32(sm.p[bb]), da = smem_u32(sm.ds[bb]);
+#pragma unroll
+          for (int k = 0; k < PT / 16; ++k) {
+            umma_bf16(acc, umma_desc_sw128(pa + k * 32, 16, 1024), umma_desc_sw128(oa + k * 2048, 8192, 1024), kIdA,
+                      (i > 0 || k > 0) ? 1u : 0u);
+            umma_bf16(acc + 64, umma_desc_sw128(da + k * 32, 16, 1024), umma_desc_sw128(qa + k * 2048, 8192, 1024),
+                      kIdA, (i > 0 || k > 0) ? 1u : 0u);
+          }
+          umma_commit(&sm.pd_free[bb]);
+          umma_commit(&sm.qd_empty[st]);
+          if (i + 2 < ntiles) issue_s(gi + 2);
+        }
+        umma_commit(&sm.acc_full[kbuf]);
+        umma_commit(&sm.kv_empty[kbuf]);
+        g += ntiles;
+      }
+    }
+  } else if (warp >= 4) {
+    const int sw = warp - 4, quarter = sw & 3, grp = sw >> 2;
+    const int r = quarter * 32 + lane;  // key row within the unit
+    const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+    const uint32_t pbase = smem_u32(sm.p[grp]), dbase = smem_u32(sm.ds[grp]);
+    const size_t ld = static_cast<size_t>(3) * H * HD;
+    // unit epilogue (group 0 -> dV, group 1 -> dK x scale), run after this group's first tile of
+    // the next unit so the accumulator set has long been complete
+    auto epilogue = [&](int eu, int elu) {
+      const int ekb = eu / BH, ebh = eu - ekb * BH, eb = ebh / H, eh = ebh - eb * H;
+      const int aset = elu & 1;
+      mbar_wait(&sm.acc_full[aset], (elu >> 1) & 1);
+      tc_fence_after();
+      __nv_bfloat16* dst = dqkv + (static_cast<size_t>(eb) * T + ekb * TK + r) * ld +
+                           static_cast<size_t>(grp ? (H + eh) * HD : (2 * H + eh) * HD);
+      const float mul = grp ? scale : 1.f;
+      uint32_t w32[64];
+      tmem_ld32(trow + 256 + aset * 128 + grp * 64, *reinterpret_cast<uint32_t(*)[32]>(&w32[0]));
+      tmem_ld32(trow + 256 + aset * 128 + grp * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&w32[32]));
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.acc_free[aset]);
+#pragma unroll
+      for (int piece = 0; piece < 8; ++piece) {
+        uint4 w;
+        w.x = pack_bf16(__uint_as_float(w32[8 * piece + 0]) * mul, __uint_as_float(w32[8 * piece + 1]) * mul);
+        w.y = pack_bf16(__uint_as_float(w32[8 * piece + 2]) * mul, __uint_as_float(w32[8 * piece + 3]) * mul);
+        w.z = pack_bf16(__uint_as_float(w32[8 * piece + 4]) * mul, __uint_as_float(w32[8 * piece + 5]) * mul);
+        w.w = pack_bf16(__uint_as_float(w32[8 * piece + 6]) * mul, __uint_as_float(w32[8 * piece + 7]) * mul);
+        reinterpret_cast<uint4*>(dst)[piece] = w;
+      }
+    };
+    int pend_u = -1, pend_lu = 0;
+    int g = 0, lu = 0;
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lu) {
+      const int ntiles = 2 * (nqb - u / BH);
+      for (int i = grp; i < ntiles; i += 2) {
+        const int gi = g + i, st = gi % kPPStages;
+        mbar_wait(&sm.s_full[grp], (gi >> 1) & 1);
+        mbar_wait(&sm.qd_full[st], (gi / kPPStages) & 1);  // (complete) lse / D of this tile visible
+        tc_fence_after();
+        uint32_t us[64], ud[64];
+        tmem_ld32(trow + grp * 128, *reinterpret_cast<uint32_t(*)[32]>(&us[0]));
+        tmem_ld32(trow + grp * 128 + 32, *reinterpret_cast<uint32_t(*)[32]>(&us[32]));
+        tmem_ld32(trow + grp * 128 + 64, *reinterpret_cast<uint32_t(*)[32]>(&ud[0]));
+        tmem_ld32(trow + grp * 128 + 96, *reinterpret_cast<uint32_t(*)[32]>(&ud[32]));
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.s_free[grp]);
+        mbar_wait(&sm.pd_free[grp], ((gi >> 1) & 1) ^ 1);  // this group's previous dV/dK MMAs read P / dS
+        const uint32_t rowoff = static_cast<uint32_t>(r * 128);
+        const uint32_t la_ = smem_u32(&sm.lse[st][0]), da_ = smem_u32(&sm.dsum[st][0]);
+#pragma unroll
+        for (int g8 = 0; g8 < 8; ++g8) {  // 8 queries at a time: P^T, dS^T -> bf16 -> swizzled smem
+          const uint4 la = ld_shared_v4(la_ + 32 * g8), lb = ld_shared_v4(la_ + 32 * g8 + 16);
+          const uint4 da4 = ld_shared_v4(da_ + 32 * g8), db4 = ld_shared_v4(da_ + 32 * g8 + 16);
+          const float lq[8] = {__uint_as_float(la.x), __uint_as_float(la.y), __uint_as_float(la.z),
+                               __uint_as_float(la.w), __uint_as_float(lb.x), __uint_as_float(lb.y),
+                               __uint_as_float(lb.z), __uint_as_float(lb.w)};
+          const float dq8[8] = {__uint_as_float(da4.x), __uint_as_float(da4.y), __uint_as_float(da4.z),
+                                __uint_as_float(da4.w), __uint_as_float(db4.x), __uint_as_float(db4.y),
+                                __uint_as_float(db4.z), __uint_as_float(db4.w)};
+          float pv[8], dv[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float pe = ex2(fmaf(__uint_as_float(us[8 * g8 + e]), scale_log2, -lq[e] * kLog2e));
+            pv[e] = pe;
+            dv[e] = pe * (__uint_as_float(ud[8 * g8 + e]) - dq8[e]);
+          }
+          if (i < 2) {  // diagonal: query kb*128 + 64 i + c sees key kb*128 + r iff 64 i + c >= r
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              if (PT * i + 8 * g8 + e < r) pv[e] = dv[e] = 0.f;
+          }
+          const uint32_t off = rowoff + ((g8 ^ (r & 7)) << 4);
+          st_shared_v4(pbase + off, pack_bf16(pv[0], pv[1]), pack_bf16(pv[2], pv[3]), pack_bf16(pv[4], pv[5]),
+                       pack_bf16(pv[6], pv[7]));
+          st_shared_v4(dbase + off, pack_bf16(dv[0], dv[1]), pack_bf16(dv[2], dv[3]), pack_bf16(dv[4], dv[5]),
+                       pack_bf16(dv[6], dv[7]));
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.pd_full[grp]);
+        if (i == grp && pend_u >= 0) {
+          epilogue(pend_u, pend_lu);
+          pend_u = -1;
+        }
+      }
+      g += ntiles;
+      pend_u = u;
+      pend_lu = lu;
+    }
+    if (pend_u >= 0) epilogue(pend_u, pend_lu);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_free<512>(tmem);
+}
+
+struct SmemQpp {  // dQ kernel, ping-pong
+  uint8_t q[2][kTile], d_o[2][kTile];                                // unit operands (128 queries)
+  uint8_t k[kPPStages][kPTile64], v[kPPStages][kPTile64];            // 64-key tiles
+  uint8_t ds[2][kPB];                                                 // per softmax group
+  float lse[2][TQ], dsum[2][TQ];
+  uint64_t qd_full[2], qd_empty[2], kv_full[kPPStages], kv_empty[kPPStages], s_full[2], s_free[2], ds_full[2],
+      ds_free[2], acc_full[2], acc_free[2];
+  uint32_t tmem;
+};
+
+// Unit u = (query tile qb, sequence x head bh), longest first; inner tiles of 64 keys.
+__global__ void __launch_bounds__(kThreadsBwd, 1)
+    attn_dq_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv128, const __grid_constant__ CUtensorMap tm_qkv64,
+                      const __grid_constant__ CUtensorMap tm_do128, const float* __restrict__ lse,
+                      const float* __restrict__ D, int T, int H, int BH, __nv_bfloat16* __restrict__ dqkv, float scale,
+                      float scale_log2) {
+  extern __shared__ uint8_t smem_raw[];
+  SmemQpp& sm = *reinterpret_cast<SmemQpp*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nqb = T / TQ;
+  const int nunits = nqb * BH;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tm_qkv128);
+    tma_prefetch(&tm_qkv64);
+    tma_prefetch(&tm_do128);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm.qd_full[i], 1);
+      mbar_init(&sm.qd_empty[i], 1);
+      mbar_init(&sm.s_full[i], 1);
+      mbar_init(&sm.s_free[i], 4);
+      mbar_init(&sm.ds_full[i], 4);
+      mbar_init(&sm.ds_free[i], 1);
+      mbar_init(&sm.acc_full[i], 1);
+      mbar_init(&sm.acc_free[i], 8);
+    }
+    for (int i = 0; i < kPPStages; ++i) {
+      mbar_init(&sm.kv_full[i], 1);
+      mbar_init(&sm.kv_empty[i], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(&sm.tmem);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem;  // S[b] cols 128b..+63, dP[b] 128b+64..; dQ set a: 256 + 64a
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int g = 0, lu = 0;
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lu) {
+        const int qi = u / BH, bh = u - qi * BH, b = bh / H, h = bh - b * H;
+        const int qb = nqb - 1 - qi, row0 = b * T;
+        const int qbuf = lu & 1;
+        mbar_wait(&sm.qd_empty[qbuf], ((lu >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&sm.qd_full[qbuf], 2 * kTile + 2 * TQ * 4);
+        tma_load_2d(sm.q[qbuf], &tm_qkv128, &sm.qd_full[qbuf], h * HD, row0 + qb * TQ);
+        tma_load_2d(sm.d_o[qbuf], &tm_do128, &sm.qd_full[qbuf], h * HD, row0 + qb * TQ);
+        const size_t qo = static_cast<size_t>(bh) * T + qb * TQ;
+        bulk_load(sm.lse[qbuf], lse + qo, TQ * 4, &sm.qd_full[qbuf]);
+        bulk_load(sm.dsum[qbuf], D + qo, TQ * 4, &sm.qd_full[qbuf]);
+        const int ntiles = 2 * (qb + 1);
+        for (int j = 0; j < ntiles; ++j, ++g) {
+          const int st = g % kPPStages;
+          mbar_wait(&sm.kv_empty[st], ((g / kPPStages) & 1) ^ 1);
+          mbar_arrive_expect_tx(&sm.kv_full[st], 2 * kPTile64);
+          tma_load_2d(sm.k[st], &tm_qkv64, &sm.kv_full[st], (H + h) * HD, row0 + j * PT);
+          tma_load_2d(sm.v[st], &tm_qkv64, &sm.kv_full[st], (2 * H + h) * HD, row0 + j * PT);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t kIdS = idesc_bf16_f32(TQ, PT, false, false);  // [q x 64 keys], K = hd
+      constexpr uint32_t kIdQ = idesc_bf16_f32(TQ, HD, false, true);   // [q x hd], K = 64 keys, B MN-major
+      int g = 0, lu = 0;
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lu) {
+        const int ntiles = 2 * (nqb - u / BH);
+        const int qbuf = lu & 1;
+        const uint32_t acc = tmem + 256 + static_cast<uint32_t>(qbuf * 64);
+        mbar_wait(&sm.qd_full[qbuf], (lu >> 1) & 1);
+        const uint32_t qa = smem_u32(sm.q[qbuf]), oa = smem_u32(sm.d_o[qbuf]);
+        auto issue_s = [&](int gj) {  // S = Q K^T, dP = dO V^T of global tile gj into buffer gj & 1
+          const int st = gj % kPPStages, bb = gj & 1;
+          mbar_wait(&sm.kv_full[st], (gj / kPPStages) & 1);
+          mbar_wait(&sm.s_free[bb], ((gj >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t ka = smem_u32(sm.k[st]), va = smem_u32(sm.v[st]);
+          const uint32_t sd = tmem + static_cast<uint32_t>(bb * 128);
+#pragma unroll
+          for (int k = 0; k < HD / 16; ++k) {
+            umma_bf16(sd, umma_desc_sw128(qa + k * 32, 16, 1024), umma_desc_sw128(ka + k * 32, 16, 1024), kIdS,
+                      k > 0 ? 1u : 0u);
+            umma_bf16(sd + 64, umma_desc_sw128(oa + k * 32, 16, 1024), umma_desc_sw128(va + k * 32, 16, 1024),
+                      kIdS, k > 0 ? 1u : 0u);
+          }
+          umma_commit(&sm.s_full[bb]);
+        };
+        issue_s(g);
+        issue_s(g + 1);
+        mbar_wait(&sm.acc_free[qbuf], ((lu >> 1) & 1) ^ 1);
+        for (int j = 0; j < ntiles; ++j) {
+          const int gj = g + j, st = gj % kPPStages, bb = gj & 1;
+          mbar_wait(&sm.ds_full[bb], (gj >> 1) & 1);
+          tc_fence_after();
+          const uint32_t ka = smem_u32(sm.k[st]), da = smem_u32(sm.ds[bb]);
+#pragma unroll
+          for (int k = 0; k < PT / 16; ++k)
+            umma_bf16(acc, umma_desc_sw128(da + k * 32, 16, 1024), umma_desc_sw128(ka + k * 2048, 8192, 1024), kIdQ,
+                      (j > 0 || k > 0) ? 1u : 0u);
+          umma_commit(&sm.ds_free[bb]);
+          umma_commit(&sm.kv_empty[st]);
+          if (j + 2 < ntiles) issue_s(gj + 2);
+        }
+        umma_commit(&sm.acc_full[qbuf]);
+        umma_commit(&sm.qd_empty[qbuf]);
+        g += ntiles;
+      }
+    }
+  } else if (warp >= 4) {
+    const int sw = warp - 4, quarter = sw & 3, grp = sw >> 2;
+    const int r = quarter * 32 + lane;  // query row within the unit
+    const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+    const uint32_t dbase = smem_u32(sm.ds[grp]);
+    const size_t ld = static_cast<size_t>(3) * H * HD;
+    // unit epilogue (dQ x scale; group b writes columns 32b..32b+31), one tile late
+    auto epilogue = [&](int eu, int elu) {
+      const int eqi = eu / BH, ebh = eu - eqi * BH, eb = ebh / H, eh = ebh - eb * H;
+      const int eq = (nqb - 1 - eqi) * TQ + r;
+      const int aset = elu & 1;
+      mbar_wait(&sm.acc_full[aset], (elu >> 1) & 1);
+      tc_fence_after();
+      uint32_t w32[32];
+      tmem_ld32(trow + 256 + aset * 64 + grp * 32, w32);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.acc_free[aset]);
+      __nv_bfloat16* qrow = dqkv + (static_cast<size_t>(eb) * T + eq) * ld + static_cast<size_t>(eh * HD) + grp * 32;
+#pragma unroll
+      for (int piece = 0; piece < 4; ++piece) {
+        uint4 w;
+        w.x = pack_bf16(__uint_as_float(w32[8 * piece + 0]) * scale, __uint_as_float(w32[8 * piece + 1]) * scale);
+        w.y = pack_bf16(__uint_as_float(w32[8 * piece + 2]) * scale, __uint_as_float(w32[8 * piece + 3]) * scale);
+        w.z = pack_bf16(__uint_as_float(w32[8 * piece + 4]) * scale, __uint_as_float(w32[8 * piece + 5]) * scale);
+        w.w = pack_bf16(__uint_as_float(w32[8 * piece + 6]) * scale, __uint_as_float(w32[8 * piece + 7]) * scale);
+        reinterpret_cast<uint4*>(qrow)[piece] = w;
+      }
+    };
+    int pend_u = -1, pend_lu = 0;
+    int g = 0, lu = 0;
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lu) {
+      const int qb = nqb - 1 - u / BH, ntiles = 2 * (qb + 1);
+      mbar_wait(&sm.qd_full[lu & 1], (lu >> 1) & 1);  // lse / D of the unit's queries
+      float l2, dq;
+      asm volatile("ld.shared.f32 %0, [%1];" : "=f"(l2) : "r"(smem_u32(&sm.lse[lu & 1][r])));
+      asm volatile("ld.shared.f32 %0, [%1];" : "=f"(dq) : "r"(smem_u32(&sm.dsum[lu & 1][r])));
+      l2 *= kLog2e;
+      for (int j = grp; j < ntiles; j += 2) {
+        const int gj = g + j;
+        mbar_wait(&sm.s_full[grp], (gj >> 1) & 1);
+        tc_fence_after();
+        uint32_t us[64], ud[64];
+        tmem_ld32(trow + grp * 128, *reinterpret_cast<uint32_t(*)[32]>(&us[0]));
+        tmem_ld32(trow + grp * 128 + 32, *reinterpret_cast<uint32_t(*)[32]>(&us[32]));
+        tmem_ld32(trow + grp * 128 + 64, *reinterpret_cast<uint32_t(*)[32]>(&ud[0]));
+        tmem_ld32(trow + grp * 128 + 96, *reinterpret_cast<uint32_t(*)[32]>(&ud[32]));
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.s_free[grp]);
+        mbar_wait(&sm.ds_free[grp], ((gj >> 1) & 1) ^ 1);
+        const uint32_t rowoff = static_cast<uint32_t>(r * 128);
+        const bool diag = j >= 2 * qb;  // keys 64 j + c vs query qb*128 + r: visible iff 64 j + c <= 128 qb + r
+#pragma unroll
+        for (int g8 = 0; g8 < 8; ++g8) {
+          float dv[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float pe = ex2(fmaf(__uint_as_float(us[8 * g8 + e]), scale_log2, -l2));
+            dv[e] = pe * (__uint_as_float(ud[8 * g8 + e]) - dq);
+          }
+          if (diag) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              if (PT * j + 8 * g8 + e > TQ * qb + r) dv[e] = 0.f;
+          }
+          st_shared_v4(dbase + rowoff + ((g8 ^ (r & 7)) << 4), pack_bf16(dv[0], dv[1]), pack_bf16(dv[2], dv[3]),
+                       pack_bf16(dv[4], dv[5]), pack_bf16(dv[6], dv[7]));
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.ds_full[grp]);
+        if (j == grp && pend_u >= 0) {
+          epilogue(pend_u, pend_lu);
+          pend_u = -1;
+        }
+      }
+      g += ntiles;
+      pend_u = u;
+      pend_lu = lu;
+    }
+    if (pend_u >= 0) epilogue(pend_u, pend_lu);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_free<512>(tmem);
+}
+
 }  // namespace
 
 bool attn_fwd_tc_supported(size_t T, size_t hd) { return hd == HD && T % TQ == 0; }
@@ -929,6 +1384,30 @@ void attn_bwd_tc(const bf16* qkv, const bf16* o, const float* lse, const bf16* d
   }();
   const int BH = static_cast<int>(B * H), units = static_cast<int>(T / TQ) * BH;
   const unsigned grid = static_cast<unsigned>(std::min(units, sms));
+  static const bool pp = [] {  // CKF_ATTN_BWD=serial: the one-tile-in-flight kernels above
+    const char* v = std::getenv("CKF_ATTN_BWD");
+    return !(v && std::string(v) == "serial");
+  }();
+  if (pp && !rope_tab) {
+    const CUtensorMap tq64 = tma::make_2d_bf16(qkv, 3 * H * hd, B * T, 3 * H * hd, 64, 64);
+    const CUtensorMap td64 = tma::make_2d_bf16(dout, H * hd, B * T, H * hd, 64, 64);
+    const size_t smem_kvp = sizeof(SmemKVpp) + 1024, smem_qp = sizeof(SmemQpp) + 1024;
+    static bool attr_pp = false;
+    if (!attr_pp) {
+      CKF_CUDA(cudaFuncSetAttribute(attn_dkdv_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem_kvp)));
+      CKF_CUDA(cudaFuncSetAttribute(attn_dq_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem_qp)));
+      attr_pp = true;
+    }
+    attn_dkdv_pp_kernel<<<grid, kThreadsBwd, smem_kvp, s>>>(tq, tq64, td64, lse, Dsum, static_cast<int>(T),
+                                                            static_cast<int>(H), BH, dqkv, scale, scale * kLog2e);
+    CKF_LAUNCH_CHECK();
+    attn_dq_pp_kernel<<<grid, kThreadsBwd, smem_qp, s>>>(tq, tq64, td, lse, Dsum, static_cast<int>(T),
+                                                        static_cast<int>(H), BH, dqkv, scale, scale * kLog2e);
+    CKF_LAUNCH_CHECK();
+    return;
+  }
   long long* dbg = attn_fwd_debug_buffer();
   attn_dkdv_tc_kernel<<<grid, kThreadsBwd, smem_kv, s>>>(tq, td, lse, Dsum, static_cast<int>(T), static_cast<int>(H), BH,
                                                          dqkv, scale, scale * kLog2e, rope_tab,
