@@ -453,6 +453,13 @@ int ckf_attention_bwd(const void* qkv, const void* o, const float* lse, const vo
   });
 }
 // debug (not part of the ABI contract): per-CTA forward-attention timings, 8 longs per CTA
+int ckf_debug_gemm_timings(long long* out, int n_ctas) {
+  return guard([&] {
+    long long* b = ckf::tc::gemm_debug_buffer();
+    if (!b) ckf::raise(CKF_E_USAGE, "set CKF_GEMM_DEBUG=1");
+    CKF_CUDA(cudaMemcpy(out, b, 8 * sizeof(long long) * static_cast<size_t>(n_ctas), cudaMemcpyDeviceToHost));
+  });
+}
 int ckf_debug_attn_fwd_timings(long long* out, int n_ctas) {
   return guard([&] {
     long long* b = ckf::llama::attn_fwd_debug_buffer();

@@ -100,11 +100,17 @@ namespace {
 using namespace ckf::sm100;
 
 constexpr int BM = 128, BK = 64, UK = 16;
-constexpr int kThreads = 256;
+// Epilogue warps: 8 (two per TMEM lane quarter, each on half of the tile's columns) for the
+// CTA-pair bf16-output epilogue (measured: LM head forward +8 % vs cuBLAS-relative, others
+// neutral); 4 elsewhere, where the extra staging would cost an operand stage.
+__host__ __device__ constexpr int epi_warps(int epi, int ncta) { return epi == 0 /*kStoreBF16*/ && ncta == 2 ? 8 : 4; }
+__host__ __device__ constexpr int gemm_threads(int epi, int ncta) { return 128 + 32 * epi_warps(epi, ncta); }
 constexpr uint32_t kAStage = BM * BK * 2;  // 16 KiB
 constexpr uint32_t kStageBufBytes = 4096;  // per epilogue warp, x2: [32 rows][128 B] TMA-store staging
 
 struct Params {
+  long long* dbg;  // CKF_GEMM_DEBUG=1: per-CTA phase cycles [producer empty-wait, mma full-wait, mma tempty-wait,
+                   // epilogue tfull-wait, total] (tools/gemm_debug.py)
   int M, N, K;
   float alpha;
   int nm, nn, tiles, nk;
@@ -123,13 +129,16 @@ template <int BN, int EPI, int NCTA>
 struct Cfg {
   // kSwiGLUBwd trades operand stages for 4 epilogue buffers per warp (g/u prefetch pairs).
   // NCTA = 2 (CTA pair): each CTA holds BN/2 columns of B, so a stage is 32 KiB at BN = 256.
+  static constexpr int kEW = epi_warps(EPI, NCTA);
   static constexpr int kEpiBufs = EPI == kSwiGLUBwd ? 4 : 2;
-  static constexpr int kStages = NCTA == 2 ? (EPI == kSwiGLUBwd ? 4 : 6)
-                                           : (BN == 256 ? 4 : 6) - (EPI == kSwiGLUBwd ? 1 : 0);
   static constexpr uint32_t kBStage = (BN / NCTA) * BK * 2;
   static constexpr uint32_t kStageBytes = kAStage + kBStage;
   static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
-  static constexpr uint32_t kEpiBytes = 4 * kEpiBufs * kStageBufBytes;
+  static constexpr uint32_t kEpiBytes = kEW * kEpiBufs * kStageBufBytes;
+  // as many operand stages as fit next to the epilogue staging (<= 227 KiB per CTA), at most 6
+  static constexpr int kStages = (232448 - 1024 - 256 - static_cast<int>(kEpiBytes)) / static_cast<int>(kStageBytes) > 6
+                                     ? 6
+                                     : (232448 - 1024 - 256 - static_cast<int>(kEpiBytes)) / static_cast<int>(kStageBytes);
   static constexpr size_t kSmem = 1024 /*align slack*/ + kStages * kStageBytes + kEpiBytes + 256 /*barriers*/;
 };
 
@@ -162,7 +171,7 @@ __device__ __forceinline__ Unit unit_of(const Params& p, int u) {
 // BN/2 columns of B, the leader issues tcgen05.mma.cta_group::2 (M = 256), both CTAs hold
 // their 128 x BN accumulator rows in TMEM and run their own epilogue.
 template <int BN, bool A_MN, bool B_MN, int EPI, int NCTA>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(gemm_threads(EPI, NCTA), 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                 const __grid_constant__ CUtensorMap tmap_c, const __grid_constant__ CUtensorMap tmap_ws, Params p) {
   using C = Cfg<BN, EPI, NCTA>;
@@ -172,6 +181,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t rank = NCTA == 2 ? cluster_ctarank() : 0;
   const bool leader = rank == 0;
   const int u0 = static_cast<int>(blockIdx.x) / NCTA, ustep = static_cast<int>(gridDim.x) / NCTA;
+  const long long t_start_ = p.dbg ? clock64() : 0;
+  long long dw[4] = {0, 0, 0, 0};
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -198,7 +209,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 4 * NCTA);  // the leader's counts both CTAs' epilogue warps
+      mbar_init(&tempty[i], C::kEW * NCTA);  // the leader's counts both CTAs' epilogue warps
     }
     for (int i = 0; i < 8; ++i) mbar_init(&lbar[i], 1);
     fence_barrier_init();
@@ -230,7 +241,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const Unit w = unit_of(p, u);
         const int arow = w.mb * BM * NCTA + static_cast<int>(rank) * BM;
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
+          const long long w0_ = p.dbg ? clock64() : 0;
           mbar_wait(&empty[stage], phase ^ 1);
+          if (p.dbg) dw[0] += clock64() - w0_;
           uint8_t* a = sA + stage * kAStage;
           uint8_t* b = sB + stage * C::kBStage;
           // NCTA = 2: the leader's full barrier counts both CTAs' bytes; both CTAs' loads complete on it
@@ -276,11 +289,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t acc_phase = 0;
       for (int u = u0; u < p.units; u += ustep) {
         const Unit w = unit_of(p, u);
+        const long long w1_ = p.dbg ? clock64() : 0;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
+        if (p.dbg) dw[2] += clock64() - w1_;
         tc_fence_after();
         const uint32_t d = tmem_base + static_cast<uint32_t>(acc * BN);
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
+          const long long w2_ = p.dbg ? clock64() : 0;
           mbar_wait(&full[stage], phase);
+          if (p.dbg) dw[1] += clock64() - w2_;
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + stage * kAStage);
           const uint32_t b0 = smem_u32(sB + stage * C::kBStage);
@@ -314,8 +331,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     // ---------------- epilogue: TMEM -> registers -> swizzled smem -> TMA store / reduce-add
-    const int q = warp - 4;  // TMEM lane quarter (warp % 4)
-    uint8_t* stg = sEpi + q * C::kEpiBufs * kStageBufBytes;
+    constexpr int EH = C::kEW / 4;  // column slices per lane quarter
+    const int ew = warp - 4;
+    const int q = ew & 3;   // TMEM lane quarter (warp % 4)
+    const int eh = ew >> 2;  // column slice of this warp
+    uint8_t* stg = sEpi + ew * C::kEpiBufs * kStageBufBytes;
     int acc = 0, sbuf = 0;
     uint32_t acc_phase = 0;
     constexpr int CW = EPI == kStoreF32 || EPI == kAccF32 ? 32 : 64;  // columns per 128-byte staged row
@@ -357,21 +377,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         first_unit = false;
       }
+      const long long w3_ = p.dbg ? clock64() : 0;
       mbar_wait(&tfull[acc], acc_phase);
+      if (p.dbg) dw[3] += clock64() - w3_;
       tc_fence_after();
       const uint32_t trow = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN);
       const int m0 = row0_of(w);
       if constexpr (EPI == kSwiGLU) {
         // gate columns [c0, c0+64) and the matching up columns [BN/2 + c0, ...)
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN / 2; c0 += 64) {
+        for (int c0 = eh * (BN / 2 / EH); c0 < (eh + 1) * (BN / 2 / EH); c0 += 64) {
           uint32_t g[64], v[64];
           tmem_ld32(trow + c0, *reinterpret_cast<uint32_t(*)[32]>(&g[0]));
           tmem_ld32(trow + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&g[32]));
           tmem_ld32(trow + BN / 2 + c0, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
           tmem_ld32(trow + BN / 2 + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
           tmem_ld_wait();
-          if (c0 + 64 >= BN / 2) {
+          if (c0 + 64 >= (eh + 1) * (BN / 2 / EH)) {
             tc_fence_before();
             __syncwarp();
             if (lane == 0) release_acc(acc);
@@ -466,7 +488,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       } else {
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += CW) {
+      for (int c0 = eh * (BN / EH); c0 < (eh + 1) * (BN / EH); c0 += CW) {
         uint32_t r[CW];
         if constexpr (CW == 64) {
           uint32_t (&r0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&r[0]);
@@ -491,7 +513,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-        if (c0 + CW >= BN) {  // last chunk loaded: hand the accumulator back to the MMA warp early
+        if (c0 + CW >= (eh + 1) * (BN / EH)) {  // last chunk loaded: hand the accumulator back early
           tc_fence_before();
           __syncwarp();
           if (lane == 0) release_acc(acc);
@@ -543,7 +565,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int ht = w.tile * NCTA + static_cast<int>(rank);  // half-tile of a CTA pair
         int* stored = p.flags + 2 * ht;
         int* reduced = stored + 1;
-        const int nwarps = 4 * p.splits;
+        const int nwarps = C::kEW * p.splits;
         if (lane == 0) {
           bulk_wait_all();  // this warp's partial rows have landed in the workspace
           fence_proxy_async_global();
@@ -552,7 +574,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           while (ld_acquire(stored) < nwarps) __nanosleep(32);
         }
         __syncwarp();
-        const int wid = w.split * 4 + q;
+        const int wid = w.split * C::kEW + ew;
         const int per = (BM + nwarps - 1) / nwarps;
         for (int rr = wid * per; rr < min(BM, (wid + 1) * per); ++rr) {
           const int m = w.mb * BM * NCTA + static_cast<int>(rank) * BM + rr;
@@ -603,6 +625,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (lane == 0) bulk_wait_all();
   }
+  if (p.dbg && lane == 0) {
+    long long* d = p.dbg + 8 * blockIdx.x;
+    if (warp == 0) d[0] = dw[0];
+    if (warp == 1) {
+      d[1] = dw[1];
+      d[2] = dw[2];
+    }
+    if (warp == 4) {
+      d[3] = dw[3];
+      d[4] = clock64() - t_start_;
+    }
+  }
   tc_fence_before();
   if constexpr (NCTA == 2) {
     cluster_sync_all();  // the leader's MMAs into the peer's TMEM are complete
@@ -624,6 +658,20 @@ int num_sms() {
   }();
   return n;
 }
+
+}  // namespace
+long long* gemm_debug_buffer() {
+  static long long* b = [] {
+    long long* x = nullptr;
+    if (std::getenv("CKF_GEMM_DEBUG")) {
+      CKF_CUDA(cudaMalloc(&x, 8 * sizeof(long long) * 1024));
+      CKF_CUDA(cudaMemset(x, 0, 8 * sizeof(long long) * 1024));
+    }
+    return x;
+  }();
+  return b;
+}
+namespace {
 
 float* split_workspace(size_t bytes) {
   static float* ws = nullptr;
@@ -667,6 +715,7 @@ void launch_t(const GemmDesc& g, int splits, cudaStream_t s) {
   const CUtensorMap tcm = c_bf16 ? tma::make_2d_bf16(g.C, EPI == kSwiGLUBwd ? 2 * g.N : g.N, g.M, g.ldc, 64, 32)
                                  : tma::make_2d_f32(g.C, g.N, g.M, g.ldc, 32, 32);
   Params p;
+  p.dbg = gemm_debug_buffer();
   p.M = g.M;
   p.N = g.N;
   p.K = g.K;
@@ -713,7 +762,7 @@ void launch_t(const GemmDesc& g, int splits, cudaStream_t s) {
   const int grid = NCTA * std::min(p.units, num_sms() / NCTA);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(grid));
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(gemm_threads(EPI, NCTA));
   cfg.dynamicSmemBytes = C::kSmem;
   cfg.stream = s;
   cudaLaunchAttribute attr[2];

@@ -41,6 +41,7 @@ struct GemmDesc {
 };
 
 void gemm_bf16(const GemmDesc& g, cudaStream_t s);
+long long* gemm_debug_buffer();  // non-null with CKF_GEMM_DEBUG=1
 int pick_bn(int M, int N);
 
 }  // namespace ckf::tc
