@@ -130,7 +130,11 @@ Engine::Engine(const ckf_model_desc& in) {
   CKF_CUDA(cudaEventCreate(&sb_ev_));
   CKF_CUDA(cudaEventCreate(&se_ev_));
 
-  impl_ = d_.block == CKF_BLOCK_MLP ? make_mlp_block(this) : make_llama_block(this);
+  if (d_.block == CKF_BLOCK_LLAMA && d_.prec == CKF_FP64)
+    raise(1, "the LLaMA block runs in bf16 (tensor cores) or fp32 (parity mode); fp64 parity is the MLP block's");
+  impl_ = d_.block == CKF_BLOCK_MLP  ? make_mlp_block(this)
+          : d_.prec == CKF_FP32      ? make_llama_f32_block(this)
+                                     : make_llama_block(this);
   const bool lowp = d_.prec == CKF_BF16;
   stages_.resize(d_.s);
   for (size_t i = 0; i < d_.s; ++i) alloc_group(stages_[i], impl_->stage_params(static_cast<int>(i + 1)), lowp);

@@ -271,6 +271,7 @@ class Engine {
 
 std::unique_ptr<BlockImpl> make_mlp_block(Engine* e);
 std::unique_ptr<BlockImpl> make_llama_block(Engine* e);
+std::unique_ptr<BlockImpl> make_llama_f32_block(Engine* e);  // fp32 parity mode (llama_f32.cu)
 
 std::vector<Range> even_partition(size_t layers, size_t stages);
 

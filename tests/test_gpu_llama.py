@@ -198,3 +198,58 @@ def test_cuda_graph_replay_bit_identical(monkeypatch):
     for a, b in zip(out[0][1], out[1][1]):
         assert np.array_equal(a, b)
     assert np.array_equal(out[0][2], out[1][2])
+
+
+def _engine_f32(spec, rows_per_mb, seed=3, lr=1e-3):
+    import paper_2506_15461_b200 as P
+    from paper_2506_15461_b200 import api
+    ms = api.ModelSpec.llama(spec.vocab, spec.d, spec.layers, spec.heads, spec.ffn, spec.seq_len, spec.stages,
+                             precision="fp32", max_tokens=rows_per_mb * spec.seq_len)
+    eng = P.Engine(ms)
+    eng.init(seed, lr)
+    return eng
+
+
+@pytest.mark.parametrize("swapped", [False, True])
+def test_fp32_parity_mode_microbatch(swapped):
+    # fp32 parity mode of the LLaMA block (llama_f32.cu): CUDA-core fp32 GEMMs and attention
+    # against the fp64 oracle -- loss 1e-5 relative, gradients 1e-4 relative Frobenius per group
+    eng = _engine_f32(SMALL, 2)
+    ref = LO.LModel(SMALL, 3, 1e-3)
+    toks = LO.token_batch(11, 1, 1, 2, SMALL.seq_len, SMALL.vocab)
+    order = build_schedule(2, True, SMALL.stages)[0] if swapped else standard_order(SMALL.stages)
+    eng.zero_grad()
+    lg = eng.accumulate(order, toks)
+    lo, gs, ge, gd = LO.microbatch(ref, order, toks)
+    assert abs(lg - lo) <= 1e-5 * abs(lo), (lg, lo)
+    for sid in range(1, SMALL.stages + 1):
+        e = _rel(eng.export_grad("stage", sid), gs[sid - 1])
+        assert e < 1e-4, (sid, e)
+    assert _rel(eng.export_grad("embed"), ge) < 1e-4
+    assert _rel(eng.export_grad("deembed"), gd) < 1e-4
+    eng.close()
+
+
+def test_fp32_parity_mode_loss_curve_and_recovery():
+    # 8 iterations (standard / CheckFree+ swapped orders alternating) then a CheckFree recovery:
+    # loss curve 1e-5 relative per point; recovered weights 1e-5 relative (north_star fp32 bars)
+    rows, m = 4, 2
+    eng = _engine_f32(SMALL, rows // m, lr=2e-3)
+    ref = LO.LModel(SMALL, 3, 2e-3)
+    for it in range(1, 9):
+        toks = LO.token_batch(21, 1, it, rows, SMALL.seq_len, SMALL.vocab)
+        sched = build_schedule(m, it % 2 == 0, SMALL.stages)
+        lg, omg = eng.run_iteration(sched, toks, None, it)
+        lo, omo = LO.run_iteration(ref, sched, toks)
+        assert abs(lg - lo) <= 1e-5 * abs(lo), (it, lg, lo)
+        np.testing.assert_allclose(omg, omo, rtol=2e-3)
+    import paper_2506_15461_b200 as P
+    wp, wn = eng.export_stage(1)[0], eng.export_stage(3)[0]
+    op, _, _ = eng.scalars(1)
+    on, _, _ = eng.scalars(3)
+    eng.kill_stage(2)
+    eng.recover_stage(2, mode=P._native.CKF_REC_CHECKFREE, reduction_error=False)
+    want, _ = recover_checkfree(ref.stages[0].flat, ref.stages[2].flat, ref.stages[0].omega, ref.stages[2].omega)
+    assert _rel(eng.export_stage(2)[0], want) <= 1e-5
+    assert _rel(wp, ref.stages[0].flat) <= 1e-5 and _rel(wn, ref.stages[2].flat) <= 1e-5
+    eng.close()
