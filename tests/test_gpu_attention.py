@@ -32,11 +32,12 @@ def _fwd(qkv, B, T, H, hd, impl):
 
 
 @pytest.mark.parametrize("impl", [1, 2])
-@pytest.mark.parametrize("shape", [(2, 128, 2, 64), (2, 256, 3, 64), (1, 1024, 2, 64), (2, 128, 2, 128)])
+@pytest.mark.parametrize("shape", [(2, 128, 2, 64), (2, 256, 3, 64), (1, 1024, 2, 64), (2, 128, 2, 128),
+                                   (2, 1024, 2, 128)])
 def test_forward_vs_torch(impl, shape):
     B, T, H, hd = shape
-    if impl == 2 and (hd != 64 or T % 128):
-        pytest.skip("tcgen05 kernel: hd 64, T % 128")
+    if impl == 2 and (hd not in (64, 128) or T % 128):
+        pytest.skip("tcgen05 kernel: hd 64 or 128, T % 128")
     import paper_2506_15461_b200  # noqa: F401
     torch.manual_seed(0)
     qkv = (torch.randn(B * T, 3 * H * hd, device="cuda") * 0.8).bfloat16()
@@ -61,12 +62,13 @@ def test_tcgen05_matches_mma_sync():
 
 
 @pytest.mark.parametrize("impl", [1, 2])
-@pytest.mark.parametrize("shape", [(2, 128, 2, 64), (1, 512, 2, 64), (2, 1024, 2, 64), (1, 512, 2, 128)])
+@pytest.mark.parametrize("shape", [(2, 128, 2, 64), (1, 512, 2, 64), (2, 1024, 2, 64), (1, 512, 2, 128),
+                                   (2, 1024, 3, 128)])
 def test_backward_vs_torch(shape, impl):
     from paper_2506_15461_b200._native import check, lib
     B, T, H, hd = shape
-    if impl == 2 and hd != 64:
-        pytest.skip("tcgen05 kernel: hd 64")
+    if impl == 2 and hd not in (64, 128):
+        pytest.skip("tcgen05 kernel: hd 64 or 128")
     torch.manual_seed(2)
     qkv = (torch.randn(B * T, 3 * H * hd, device="cuda") * 0.8).bfloat16()
     o, lse = _fwd(qkv, B, T, H, hd, 0)
