@@ -51,6 +51,10 @@ WORKLOADS = {
     # configs[2] shape on one GPU (LLaMA-500M, 8 stages)
     "llama-500m": dict(block="llama", precision="bf16", input_dim=50304, hidden_dim=4096, model_dim=1024,
                        output_dim=50304, layers=24, stages=8, microbatches=8, rows=64, seq_len=1024, heads=16),
+    # configs[3] model on one GPU (LLaMA-1.5B, 4 stages, T=4096, head_dim 128): one replica's
+    # 8 microbatches of one sequence each (the 8-GPU run adds DP2 over 4 pipeline ranks)
+    "llama-1.5b": dict(block="llama", precision="bf16", input_dim=50304, hidden_dim=5632, model_dim=2048,
+                       output_dim=50304, layers=24, stages=4, microbatches=8, rows=8, seq_len=4096, heads=16),
     "mlp-124m": dict(block="mlp", precision="fp32", input_dim=16, hidden_dim=2048, model_dim=512, output_dim=16,
                      layers=12, stages=4, microbatches=8, rows=65536, seq_len=1, heads=1),
 }
