@@ -542,12 +542,14 @@ void Engine::run_iteration(const int* orders, int m, const void* x, const void* 
     }
     if (want_graph && gexec_ && key == gkey_) {
       CKF_CUDA(cudaGraphLaunch(gexec_, st_));
+      launch_counter() += graph_kernels_;  // the replayed kernel nodes are this iteration's launches
     } else if (want_graph && key == gseen_) {
       if (gexec_) {
         cudaGraphExecDestroy(gexec_);
         gexec_ = nullptr;
       }
       cudaGraph_t graph = nullptr;
+      const long n0 = launch_counter();
       CKF_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
       try {
         body();
@@ -558,6 +560,7 @@ void Engine::run_iteration(const int* orders, int m, const void* x, const void* 
         throw;
       }
       CKF_CUDA(cudaStreamEndCapture(st_, &graph));
+      graph_kernels_ = launch_counter() - n0;  // kernels captured (not executed during capture)
       CKF_CUDA(cudaGraphInstantiate(&gexec_, graph, 0));
       CKF_CUDA(cudaGraphDestroy(graph));
       gkey_ = key;

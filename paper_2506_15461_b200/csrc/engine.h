@@ -235,6 +235,7 @@ class Engine {
   bool graphs_ = true;
   cudaGraphExec_t gexec_ = nullptr;
   std::vector<long> gkey_, gseen_;
+  long graph_kernels_ = 0;  // kernel launches inside the captured graph
   std::vector<std::pair<size_t, int>> group_fit_;  // (microbatch tokens, fitted group size)
   int fused_group_size(int m, size_t mb_rows);
   int replicas_ = 1, replica_ = 0;
