@@ -562,6 +562,7 @@ void Engine::run_iteration(const int* orders, int m, const void* x, const void* 
       CKF_CUDA(cudaStreamEndCapture(st_, &graph));
       graph_kernels_ = launch_counter() - n0;  // kernels captured (not executed during capture)
       CKF_CUDA(cudaGraphInstantiate(&gexec_, graph, 0));
+      CKF_CUDA(cudaGraphUpload(gexec_, st_));  // device-side setup now, not on the first replay
       CKF_CUDA(cudaGraphDestroy(graph));
       gkey_ = key;
       gkey_[4] = alloc_epoch();  // (capture allocates nothing; kept exact anyway)
