@@ -99,6 +99,11 @@ class ClockSampler:
         self._nvml = None
         self.power: list[float] = []
         self.temp: list[float] = []
+        # CKF_BENCH_CLOCKS="period_s[,full]" (default 0.1 s, clocks + reasons only; "full" adds power and
+        # temperature, whose NVML queries were seen to coincide with slow steps)
+        spec = os.environ.get("CKF_BENCH_CLOCKS", "0.1").split(",")
+        self.period = float(spec[0])
+        self.full = len(spec) > 1 and spec[1] == "full"
         try:
             import pynvml
             import torch
@@ -125,14 +130,15 @@ class ClockSampler:
                     sm = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
                     bits = int(get_reasons(h))
                     self.samples.append((sm, mx, {n for b, n in self.REASONS.items() if bits & b}))
-                    try:
-                        self.power.append(nv.nvmlDeviceGetPowerUsage(h) / 1000.0)
-                        self.temp.append(float(nv.nvmlDeviceGetTemperature(h, nv.NVML_TEMPERATURE_GPU)))
-                    except Exception:
-                        pass
+                    if self.full:
+                        try:
+                            self.power.append(nv.nvmlDeviceGetPowerUsage(h) / 1000.0)
+                            self.temp.append(float(nv.nvmlDeviceGetTemperature(h, nv.NVML_TEMPERATURE_GPU)))
+                        except Exception:
+                            pass
                 except Exception:
                     pass
-                self._stop.wait(0.05)
+                self._stop.wait(self.period)
             return
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
