@@ -233,7 +233,7 @@ def workload_config(args, w: dict) -> dict:
     cfg = {"parallelism": f"pp{P}" + (f"xdp{R}" if R > 1 else ""),"workload": args.workload, "block": w["block"], "stages": w["stages"],
            "microbatches": w["microbatches"], "layers": w["layers"], "model_dim": w["model_dim"],
            "hidden_dim": w["hidden_dim"], "tokens_per_step": tokens_per_step(w) * R, "seq_len": w["seq_len"],
-           "strategy": "checkfree", "placement": f"{w['stages']} stages on {P} pipeline rank(s) x {R} replica(s)",
+           "strategy": getattr(args, "strategy", "checkfree"), "placement": f"{w['stages']} stages on {P} pipeline rank(s) x {R} replica(s)",
            "l2": "256 MiB memset between timed steps (outside the events)"}
     if w["block"] == "llama":
         cfg.update(vocab=w["output_dim"], heads=w["heads"])
@@ -287,6 +287,8 @@ def run_ours(args, w: dict):
                              precision=w["precision"], max_rows=mb_rows, device=local)
     eng = P_.Engine(spec)
     eng.init(1, 3e-4)
+    if args.strategy == "redundant":
+        eng.set_redundant(True)
     if world > 1:
         uid = [P_.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
@@ -496,6 +498,9 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default=DEFAULT_WORKLOAD)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-recovery-sweep", action="store_true")
+    ap.add_argument("--strategy", choices=["checkfree", "redundant"], default="checkfree",
+                    help="redundant: the redundant-computation baseline measured (extra forward per stage, "
+                         "post-step replica refresh)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -272,6 +272,11 @@ int ckf_engine_set_group_cap(ckf_engine_t e, int cap);
  * first device operation (the input H2D copy when the batch is on the host) to the loss /
  * omega D2H copies -- host scheduling after the step is excluded */
 int ckf_engine_last_step_ms(ckf_engine_t e, float* ms);
+/* redundant-computation baseline (trainer.cpp:162-171), measured instead of modelled
+ * (cost_model.cpp:242-279): per microbatch one extra forward of every stage's layers (the
+ * downstream node's hot copy) and, after the optimizer step, a copy of every stage's master
+ * weights to its replica.  LLaMA bf16 block. */
+int ckf_engine_set_redundant(ckf_engine_t e, int on);
 /* Hop log for a VIRTUAL placement (stage -> rank), used to check on one GPU that
  * the engine's stage transfers match ckf_pipeline_plan: when enabled, every
  * cross-rank transfer the placement implies is recorded as (src, dst, bytes). */

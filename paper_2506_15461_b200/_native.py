@@ -98,6 +98,7 @@ def lib():
         "ckf_engine_init": (i, [eng, u64, dbl]),
         "ckf_engine_set_schedule": (i, [eng, i]), "ckf_engine_set_group_cap": (i, [eng, i]),
         "ckf_engine_last_step_ms": (i, [eng, C.POINTER(C.c_float)]),
+        "ckf_engine_set_redundant": (i, [eng, i]),
         "ckf_nccl_unique_id": (i, [vp, sz]), "ckf_engine_attach_comm": (i, [eng, vp, i, i, ip]),
         "ckf_engine_attach_comm_dp": (i, [eng, vp, i, i, ip, i]),
         "ckf_engine_run_iteration": (i, [eng, ip, i, vp, vp, sz, i, lng, dp, dp]),

@@ -308,6 +308,10 @@ class Engine:
     def sync(self):
         check(lib().ckf_engine_sync(self._h))
 
+    def set_redundant(self, on: bool):
+        """Redundant-computation baseline: extra forward per stage + post-step replica refresh."""
+        check(lib().ckf_engine_set_redundant(self._h, 1 if on else 0))
+
     def last_step_ms(self) -> float:
         """Device time of the last run_iteration (CUDA events on the engine stream)."""
         ms = C.c_float()

@@ -605,6 +605,10 @@ int ckf_engine_set_schedule(ckf_engine_t e, int mode) {
   return guard([&] { E(e)->set_schedule(mode); });
 }
 
+int ckf_engine_set_redundant(ckf_engine_t e, int on) {
+  return guard([&] { E(e)->set_redundant(on != 0); });
+}
+
 int ckf_engine_last_step_ms(ckf_engine_t e, float* ms) {
   return guard([&] { *ms = E(e)->last_step_ms(); });
 }

@@ -157,6 +157,7 @@ Engine::~Engine() {
   if (dp_comm_ && nccl().CommDestroy) nccl().CommDestroy(dp_comm_);
   if (comm_ && nccl().CommDestroy) nccl().CommDestroy(comm_);
   if (gexec_) cudaGraphExecDestroy(gexec_);
+  for (void* p : rc_replica_) cudaFree(p);
   for (auto& c : ckpt_) cudaFree(c.buf);
   for (cudaEvent_t ev : kev_) cudaEventDestroy(ev);
   if (ev0_) cudaEventDestroy(ev0_);
@@ -524,6 +525,7 @@ void Engine::run_iteration(const int* orders, int m, const void* x, const void* 
       impl_->wk = woff;
       impl_->mb_forward(0, ok(g[0]), xg, nullptr, g.size() * mb, true, scal_ + j);
       impl_->mb_backward(0, ok(g[0]), xg, g.size() * mb);
+      if (redundant_) impl_->redundant_forward(ok(g[0]), xg, g.size() * mb);
       woff += static_cast<int>(g.size());
     }
     impl_->loss_rows = 0;
@@ -537,7 +539,7 @@ void Engine::run_iteration(const int* orders, int m, const void* x, const void* 
     std::vector<long> key;
     if (want_graph) {
       key = {m, static_cast<long>(mb), static_cast<long>(reinterpret_cast<intptr_t>(xd)), gsz, alloc_epoch(),
-             impl_->state_token()};
+             impl_->state_token(), redundant_ ? 1L : 0L};
       for (int k = 0; k < m; ++k) key.insert(key.end(), ok(k), ok(k) + d_.s);
     }
     if (want_graph && gexec_ && key == gkey_) {
@@ -574,7 +576,10 @@ void Engine::run_iteration(const int* orders, int m, const void* x, const void* 
     flushed = true;
     nloss = groups.size();
   } else if (schedule_ == 0) {
-    for (int k = 0; k < m; ++k) impl_->microbatch(k, ok(k), xk(k), yk(k), mb, true, scal_ + k);
+    for (int k = 0; k < m; ++k) {
+      impl_->microbatch(k, ok(k), xk(k), yk(k), mb, true, scal_ + k);
+      if (redundant_) impl_->redundant_forward(ok(k), xk(k), mb);
+    }
   } else {
     // GPipe: all forwards, then all backwards in microbatch order (per-stage accumulation
     // order is the reference's, pipeline.cpp:66-81); hops are issued in one global order
@@ -603,6 +608,17 @@ void Engine::run_iteration(const int* orders, int m, const void* x, const void* 
   for (size_t i = 0; i < d_.s; ++i) adam_group(stages_[i], stages_[i].lr, inv, scal_ + 2048 + i);
   adam_group(embed_, edge_lr, inv, scal_ + 3000);
   adam_group(deembed_, edge_lr, inv, scal_ + 3001);
+  if (redundant_) {  // post-step refresh of every stage's hot copy
+    if (rc_replica_.size() != d_.s) rc_replica_.assign(d_.s, nullptr);
+    for (size_t i = 0; i < d_.s; ++i) {
+      ParamGroup& g = stages_[i];
+      if (!g.owned || g.n == 0) continue;
+      if (!rc_replica_[i]) CKF_CUDA(cudaMalloc(&rc_replica_[i], g.n * master_bytes()));
+      kt_begin();
+      CKF_CUDA(cudaMemcpyAsync(rc_replica_[i], g.w, g.n * master_bytes(), cudaMemcpyDeviceToDevice, st_));
+      kt_end(KC_RECOVER, 0.0, 2.0 * g.n * master_bytes());
+    }
+  }
   std::vector<double> om(d_.s);
   CKF_CUDA(cudaMemcpyAsync(losses.data(), scal_, nloss * sizeof(double), cudaMemcpyDeviceToHost, st_));
   CKF_CUDA(cudaMemcpyAsync(om.data(), scal_ + 2048, d_.s * sizeof(double), cudaMemcpyDeviceToHost, st_));

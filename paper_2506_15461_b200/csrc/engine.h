@@ -103,6 +103,13 @@ struct BlockImpl {
   virtual size_t group_bytes_per_token() const { return 0; }
   // device bytes the block will still allocate this iteration (e.g. deferred-gradient inputs)
   virtual size_t reserved_bytes() const { return 0; }
+  // redundant-computation baseline: one extra forward of every stage's layers for this microbatch
+  virtual void redundant_forward(const int* order, const void* x, size_t rows) {
+    (void)order;
+    (void)x;
+    (void)rows;
+    raise(1, "redundant computation is implemented for the LLaMA bf16 block");
+  }
   // block state that changes the launch sequence of an iteration (part of the CUDA-graph key)
   virtual long state_token() const { return 0; }
   int wk = 0;  // position of the current microbatch within the iteration (in microbatches)
@@ -180,6 +187,10 @@ class Engine {
   // up to group_cap microbatches (0 = as many as HBM allows, 1 = off).
   void set_group_cap(int cap) { group_cap_ = cap < 0 ? 0 : cap; }
   void set_graphs(bool on) { graphs_ = on; }
+  // Redundant-computation baseline, measured: every stage's forward runs a second time per
+  // microbatch (the downstream node's hot copy) and every stage's master weights are copied to
+  // its replica after the optimizer step (the post-step weight refresh of cost_model.cpp:271-279).
+  void set_redundant(bool on) { redundant_ = on; }
   // device time (ms) of the last run_iteration: first device op .. loss / omega D2H
   float last_step_ms();
   int group_cap() const { return group_cap_; }
@@ -236,6 +247,8 @@ class Engine {
   cudaGraphExec_t gexec_ = nullptr;
   std::vector<long> gkey_, gseen_;
   long graph_kernels_ = 0;  // kernel launches inside the captured graph
+  bool redundant_ = false;
+  std::vector<void*> rc_replica_;  // per stage: the hot copy's master weights
   std::vector<std::pair<size_t, int>> group_fit_;  // (microbatch tokens, fitted group size)
   int fused_group_size(int m, size_t mb_rows);
   int replicas_ = 1, replica_ = 0;

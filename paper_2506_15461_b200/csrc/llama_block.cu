@@ -367,6 +367,7 @@ struct LlamaBlock final : BlockImpl {
         layer_fwd(sid, li, c, dfr ? wset(sid, li, wk) : wset_local(c, nullptr, Mt), h, rows, Mt);
       }
     }
+    if (layers_only_) return;  // redundant-computation hot copy: the stages' forward only
     eng->move(h, Mt * d * 4, at, static_cast<int>(D.s) + 1);
     if (!eng->mine(eng->owner_of_deembed())) return;
     const float* gF = static_cast<const float*>(eng->deembed().w);
@@ -388,6 +389,17 @@ struct LlamaBlock final : BlockImpl {
       llama::rmsnorm_bwd(dxn, hF, gF, rstdF, Mt, d, dh, dh_bf, gpart, st);
       llama::gain_fold(gpart, nblk, d, gde, st);
     });
+  }
+
+  // Redundant computation (trainer.cpp:162-171, cost_model.cpp:242-279): the node after each
+  // stage holds a hot copy of it and runs its forward for every microbatch; on one GPU that is
+  // one extra forward of every stage's layers (activations discarded), after the microbatch's
+  // backward so the training caches are intact.
+  bool layers_only_ = false;
+  void redundant_forward(const int* order, const void* x, size_t rows) override {
+    layers_only_ = true;
+    mb_forward(0, order, x, nullptr, rows, false, nullptr);
+    layers_only_ = false;
   }
 
   void mb_backward(int mb, const int* order, const void*, size_t rows) override {

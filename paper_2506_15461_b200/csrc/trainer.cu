@@ -80,6 +80,9 @@ class Trainer {
     const int s = static_cast<int>(c_.stages);
     const auto std_order = host::standard_order(s);
     const bool ckpt = c_.strategy == "checkpointing";
+    // redundant computation runs its hot copies for real on the LLaMA block (measured overhead)
+    if (c_.strategy == "redundant" && desc_.block == CKF_BLOCK_LLAMA && desc_.precision == CKF_BF16)
+      model_.set_redundant(true);
     if (ckpt) model_.checkpoint_save(0);  // trainer.cpp:67-68
     if (cfp) model_.refresh_edge_replicas();
     {  // record_initial_eval (trainer.cpp:122-126)

@@ -253,3 +253,19 @@ def test_fp32_parity_mode_loss_curve_and_recovery():
     assert _rel(eng.export_stage(2)[0], want) <= 1e-5
     assert _rel(wp, ref.stages[0].flat) <= 1e-5 and _rel(wn, ref.stages[2].flat) <= 1e-5
     eng.close()
+
+
+def test_redundant_computation_mode_leaves_training_unchanged():
+    # the measured redundant-computation baseline (ckf_engine_set_redundant) runs hot-copy
+    # forwards and replica refreshes only: the training trajectory is bit-identical
+    out = []
+    for rc in (False, True):
+        eng = _engine(SMALL, 2, lr=2e-3)
+        eng.set_redundant(rc)
+        ls = [eng.run_iteration(build_schedule(4, False, SMALL.stages),
+                                LO.token_batch(37, 1, it, 8, SMALL.seq_len, SMALL.vocab), None, it)[0]
+              for it in (1, 2, 3)]
+        out.append((ls, eng.export_stage(2)[0]))
+        eng.close()
+    assert out[0][0] == out[1][0]
+    assert np.array_equal(out[0][1], out[1][1])
