@@ -165,7 +165,8 @@ class Trainer {
     evals_.push_back({slot, v});
     char buf[200];
     const double hours = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0_).count() / 3600.0;
-    std::snprintf(buf, sizeof(buf), "E,%ld,%.17g,%.17g,%.17g\n", slot, last_train_, v, hours);
+    // E,slot,train,val,measured wall hours,model iterations (slot minus checkpoint rollbacks)
+    std::snprintf(buf, sizeof(buf), "E,%ld,%.17g,%.17g,%.17g,%ld\n", slot, last_train_, v, hours, model_iter_);
     out_ << buf;
     return v;
   }
