@@ -9,7 +9,19 @@
 
 #include "engine.h"
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 namespace ckf {
+
+static bool step_debug() {  // CKF_STEP_DEBUG=1: per-step host / device split on stderr
+  static const bool on = [] {
+    const char* v = std::getenv("CKF_STEP_DEBUG");
+    return v && v[0] == '1';
+  }();
+  return on;
+}
 
 long& launch_counter() {
   static long n = 0;
@@ -128,7 +140,8 @@ Engine::Engine(const ckf_model_desc& in) {
   CKF_CUDA(cudaEventCreate(&ev0_));
   CKF_CUDA(cudaEventCreate(&ev1_));
   CKF_CUDA(cudaEventCreate(&sb_ev_));
-  CKF_CUDA(cudaEventCreate(&se_ev_));
+  CKF_CUDA(cudaEventCreate(&sg_ev_));
+  CKF_CUDA(cudaEventCreateWithFlags(&se_ev_, cudaEventBlockingSync));  // the step's final wait yields the CPU
 
   if (d_.block == CKF_BLOCK_LLAMA && d_.prec == CKF_FP64)
     raise(1, "the LLaMA block runs in bf16 (tensor cores) or fp32 (parity mode); fp64 parity is the MLP block's");
@@ -163,6 +176,7 @@ Engine::~Engine() {
   if (ev0_) cudaEventDestroy(ev0_);
   if (ev1_) cudaEventDestroy(ev1_);
   if (sb_ev_) cudaEventDestroy(sb_ev_);
+  if (sg_ev_) cudaEventDestroy(sg_ev_);
   if (se_ev_) cudaEventDestroy(se_ev_);
   if (st_) cudaStreamDestroy(st_);
 }
@@ -430,6 +444,8 @@ void Engine::run_iteration(const int* orders, int m, const void* x, const void* 
   // device-timeline bracket of the step: first device op (input H2D when from the host)
   // .. result D2H; read back by last_step_ms()
   CKF_CUDA(cudaEventRecord(sb_ev_, st_));
+  const auto host_t0 = std::chrono::steady_clock::now();
+  auto host_tg = host_t0;
 
   const size_t xcols = d_.block == CKF_BLOCK_MLP ? d_.in : d_.T + 1;
   const size_t xelt = d_.block == CKF_BLOCK_MLP ? master_bytes() : sizeof(int);
@@ -542,6 +558,10 @@ void Engine::run_iteration(const int* orders, int m, const void* x, const void* 
              impl_->state_token(), redundant_ ? 1L : 0L};
       for (int k = 0; k < m; ++k) key.insert(key.end(), ok(k), ok(k) + d_.s);
     }
+    if (step_debug()) {
+      host_tg = std::chrono::steady_clock::now();
+      CKF_CUDA(cudaEventRecord(sg_ev_, st_));
+    }
     if (want_graph && gexec_ && key == gkey_) {
       CKF_CUDA(cudaGraphLaunch(gexec_, st_));
       launch_counter() += graph_kernels_;  // the replayed kernel nodes are this iteration's launches
@@ -623,7 +643,19 @@ void Engine::run_iteration(const int* orders, int m, const void* x, const void* 
   CKF_CUDA(cudaMemcpyAsync(losses.data(), scal_, nloss * sizeof(double), cudaMemcpyDeviceToHost, st_));
   CKF_CUDA(cudaMemcpyAsync(om.data(), scal_ + 2048, d_.s * sizeof(double), cudaMemcpyDeviceToHost, st_));
   CKF_CUDA(cudaEventRecord(se_ev_, st_));
-  CKF_CUDA(cudaStreamSynchronize(st_));
+  // Block (not spin) until the step is done: a ~50 ms spin per step burns a whole core of
+  // the host's CPU quota, and quota throttling later stalls the launching thread for tens
+  // of ms right when the next step must be enqueued.
+  CKF_CUDA(cudaEventSynchronize(se_ev_));
+  if (step_debug()) {
+    float a = 0.f, b = 0.f;
+    cudaEventElapsedTime(&a, sb_ev_, sg_ev_);
+    cudaEventElapsedTime(&b, sg_ev_, se_ev_);
+    const double host = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - host_t0).count();
+    const double hg = std::chrono::duration<double, std::milli>(host_tg - host_t0).count();
+    std::fprintf(stderr, "step_debug start->graph %.3f ms graph->end %.3f ms host %.3f ms host-start->graph %.3f ms\n", a,
+                 b, host, hg);
+  }
   kt_collect();
   double total = 0.0;
   for (double l : losses) total += l;

@@ -260,6 +260,7 @@ class Engine {
   void* comm_ = nullptr;  // ncclComm_t
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
   cudaEvent_t sb_ev_ = nullptr, se_ev_ = nullptr;  // run_iteration device-timeline bracket
+  cudaEvent_t sg_ev_ = nullptr;  // CKF_STEP_DEBUG: just before the fused step's graph / body
   struct CkptGroup {
     void* buf = nullptr;  // [w | m | v] master dtype, then the bf16 shadow
     size_t bytes = 0;

@@ -557,7 +557,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI, NCTA), 1)
         sbuf ^= 1;
       }
       }  // generic epilogues
-      if (p.splits > 1) {
+      if (EPI == kAccF32 && p.splits > 1) {  // (split-K runs only with the accumulate epilogue)
         // Deterministic split-K reduction (all units are co-resident: units <= grid):
         // 1) every warp publishes its stored partial rows, 2) once all 4*splits warps of the
         // tile have, the tile's rows are shared out among them and each sums the partials in
@@ -576,37 +576,59 @@ __global__ void __launch_bounds__(gemm_threads(EPI, NCTA), 1)
         __syncwarp();
         const int wid = w.split * C::kEW + ew;
         const int per = (BM + nwarps - 1) / nwarps;
-        for (int rr = wid * per; rr < min(BM, (wid + 1) * per); ++rr) {
-          const int m = w.mb * BM * NCTA + static_cast<int>(rank) * BM + rr;
-          if (m >= p.M) break;
-          for (int c = lane * 4; c < BN; c += 128) {
+        const int r_lo = wid * per, r_hi = min(BM, (wid + 1) * per);
+        // this warp's rows as float4 slots, lanes along the columns (coalesced); kP slots per
+        // lane in flight at once -- C first, then each split's partials in split order -- so the
+        // reduction is bandwidth- rather than latency-bound.  Sum order per element as always:
+        // ((p0 + p1) + p2 ...) + C, deterministic.
+        constexpr int kP = 8, kQ = BN / 4;
+        const int nslot = (r_hi > r_lo ? r_hi - r_lo : 0) * kQ;
+        const size_t ws_base = (static_cast<size_t>(w.tile) * NCTA + rank) * BM;
+        const size_t ws_split = static_cast<size_t>(p.tiles) * NCTA * BM * BN;  // floats between splits
+        for (int base = lane; base < nslot; base += 32 * kP) {
+          float4 o[kP], acc4[kP];
+          float4* dst[kP];
+          size_t wofs[kP];
+          bool ok[kP];
+#pragma unroll
+          for (int i = 0; i < kP; ++i) {
+            const int idx = base + 32 * i;
+            const int rr = r_lo + idx / kQ, c = (idx % kQ) * 4;
+            const int m = w.mb * BM * NCTA + static_cast<int>(rank) * BM + rr;
             const int n = w.nb * BN + c;
-            if (n >= p.N) break;
-            // all partial loads in flight first (memory-level parallelism), then a fixed-order sum
-            constexpr int kMaxSplits = 16;
-            float4 part[kMaxSplits];
-#pragma unroll
-            for (int sp = 0; sp < kMaxSplits; ++sp)
-              if (sp < p.splits)
-                part[sp] = __ldcg(reinterpret_cast<const float4*>(
-                    p.ws + (((static_cast<size_t>(sp) * p.tiles + w.tile) * NCTA + rank) * BM + rr) * BN + c));
-            float4* dst = reinterpret_cast<float4*>(p.C + static_cast<size_t>(m) * p.ldc + n);
-            float4 o = *dst;
-            float4 acc4 = part[0];
-#pragma unroll
-            for (int sp = 1; sp < kMaxSplits; ++sp)
-              if (sp < p.splits) {
-                acc4.x += part[sp].x;
-                acc4.y += part[sp].y;
-                acc4.z += part[sp].z;
-                acc4.w += part[sp].w;
-              }
-            o.x += acc4.x;
-            o.y += acc4.y;
-            o.z += acc4.z;
-            o.w += acc4.w;
-            *dst = o;
+            ok[i] = idx < nslot && m < p.M && n < p.N;
+            dst[i] = reinterpret_cast<float4*>(p.C + static_cast<size_t>(ok[i] ? m : 0) * p.ldc + (ok[i] ? n : 0));
+            wofs[i] = (ws_base + rr) * BN + c;
+            if (ok[i]) o[i] = *dst[i];
           }
+#pragma unroll 1
+          for (int sp = 0; sp < p.splits; ++sp) {
+            float4 t[kP];
+#pragma unroll
+            for (int i = 0; i < kP; ++i)
+              if (ok[i]) t[i] = __ldcg(reinterpret_cast<const float4*>(p.ws + sp * ws_split + wofs[i]));
+#pragma unroll
+            for (int i = 0; i < kP; ++i)
+              if (ok[i]) {
+                if (sp == 0) {
+                  acc4[i] = t[i];
+                } else {
+                  acc4[i].x += t[i].x;
+                  acc4[i].y += t[i].y;
+                  acc4[i].z += t[i].z;
+                  acc4[i].w += t[i].w;
+                }
+              }
+          }
+#pragma unroll
+          for (int i = 0; i < kP; ++i)
+            if (ok[i]) {
+              o[i].x += acc4[i].x;
+              o[i].y += acc4[i].y;
+              o[i].z += acc4[i].z;
+              o[i].w += acc4[i].w;
+              *dst[i] = o[i];
+            }
         }
         __syncwarp();
         if (lane == 0) {
@@ -834,11 +856,15 @@ void gemm_bf16(const GemmDesc& g, cudaStream_t s) {
   // tiles split along K until the 74 pairs are busy (4x the MMA work per staged byte of the
   // single-CTA 128 x 128 split tiles)
   const bool pair_wgrad = pair_ok && !g.bn && g.epi == kAccF32 && g.M >= 2 * BM && g.M <= 4096;
+  static const int wg_bn = [] {  // CKF_GEMM_WG_BN=128: 256 x 128 pair tiles for the weight gradients
+    const char* v = std::getenv("CKF_GEMM_WG_BN");
+    return v && std::atoi(v) == 128 ? 128 : 256;
+  }();
+  if (pair_wgrad) bn = wg_bn;
   if (splits <= 0 && pair_wgrad) {
     const int pairs = num_sms() / 2, nk = (g.K + BK - 1) / BK;
-    const int pt = ((g.M + 2 * BM - 1) / (2 * BM)) * ((g.N + 255) / 256);
+    const int pt = ((g.M + 2 * BM - 1) / (2 * BM)) * ((g.N + bn - 1) / bn);
     splits = pt * 3 < pairs * 2 ? std::max(1, std::min({pairs / pt, nk / 4, 16})) : 1;
-    bn = 256;
   }
   if (splits <= 0) {
     splits = 1;
@@ -864,7 +890,9 @@ void gemm_bf16(const GemmDesc& g, cudaStream_t s) {
   // for the fused SwiGLU epilogues and for N <= 512 with very short or very long K.
   const bool pair_shape = pair_wgrad || (g.epi != kSwiGLU && g.epi != kSwiGLUBwd && splits <= 1 &&
                                          !(g.N <= 512 && (g.K <= 512 || g.K >= 16384)));
-  if (bn == 128)
+  if (bn == 128 && pair_wgrad)
+    dispatch_bn<128, 2>(g, splits, s);
+  else if (bn == 128)
     dispatch_bn<128, 1>(g, splits, s);
   else if (pair_ok && pair_shape && g.M >= 2 * BM)
     dispatch_bn<256, 2>(g, splits, s);

@@ -206,7 +206,10 @@ struct LlamaBlock final : BlockImpl {
     const char* env = std::getenv("CKF_WGRAD_DEFER");
     bool want = !(env && env[0] == '0') && m > 1;
     const size_t Mt = rows * T;
-    if (want) {
+    // the deferred buffers of this (m, Mt) already exist: nothing to size (and no
+    // cudaMemGetInfo, which can stall the launching thread for tens of ms on some hosts)
+    const bool allocated = want && defer_ && defer_m_ == m && defer_Mt_ == Mt;
+    if (want && !allocated) {
       size_t layers = 0;
       const Desc& D = eng->desc();
       for (size_t i = 0; i < D.s; ++i)
