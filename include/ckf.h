@@ -137,6 +137,11 @@ int ckf_gemm_bf16(int M, int N, int K, const void* A, int lda, int a_mn, const v
 /* Same GEMM with the fused SwiGLU epilogues of the LLaMA MLP (gemm_tc.h):
  *   epi = 3 (forward, N = 2f, B MN-major): C = gu [M x 2f] bf16, aux = a [M x f] = silu(g) * u
  *   epi = 4 (dgrad da = dY Wd^T, N = f, B K-major): aux = gu (read), C = dgu [M x 2f] bf16 (ldc = 2f) */
+// LLaMA head loss on DEVICE buffers (llama_kernels.cu xent_bf16): per-row loss lse - logit[label]
+// into row_loss (fp64); with grad != 0 the bf16 logits are overwritten in place by
+// grad_scale * (softmax - onehot).
+int ckf_xent_bf16(void* logits, const int* labels, size_t rows, size_t V, float grad_scale, int grad, double* row_loss,
+                  void* stream);
 int ckf_gemm_bf16_aux(int M, int N, int K, const void* A, int lda, int a_mn, const void* B, int ldb, int b_mn, void* C,
                       int ldc, int epi, float alpha, int bn, void* aux, int ldaux, void* stream);
 

@@ -396,6 +396,14 @@ int ckf_gemm_bf16(int M, int N, int K, const void* A, int lda, int a_mn, const v
   return ckf_gemm_bf16_aux(M, N, K, A, lda, a_mn, B, ldb, b_mn, C, ldc, epi, alpha, bn, nullptr, 0, stream);
 }
 
+int ckf_xent_bf16(void* logits, const int* labels, size_t rows, size_t V, float grad_scale, int grad, double* row_loss,
+                  void* stream) {
+  return guard([&] {
+    ckf::llama::xent_bf16(static_cast<__nv_bfloat16*>(logits), labels, rows, V, grad_scale, grad, row_loss,
+                          static_cast<cudaStream_t>(stream));
+  });
+}
+
 int ckf_gemm_bf16_aux(int M, int N, int K, const void* A, int lda, int a_mn, const void* B, int ldb, int b_mn, void* C,
                       int ldc, int epi, float alpha, int bn, void* aux, int ldaux, void* stream) {
   return guard([&] {
