@@ -36,6 +36,39 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// Packed fp32x2 arithmetic (FFMA2 / FADD2 / FMUL2) and the 3-input max (FMNMX3) of sm_100:
+// the softmax loops are issue-bound (a polynomial exp2 on the FMA pipe made them slower, so
+// MUFU is not the limit), and these halve their FMA / add / max instruction counts.
+using f32x2 = unsigned long long;
+__device__ __forceinline__ f32x2 f2(float a, float b) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2split(f32x2 v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ f32x2 ffma2(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f32x2 fadd2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f32x2 fmul2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
 // A [rows x HD] bf16 tile in shared memory as HD/64 K-major SW128 chunks of [rows][128 B]:
 // TMA brings each 64-column chunk; UMMA K step k (16 columns) reads chunk k/4 at byte 32 (k%4).
 template <int HD>
@@ -187,11 +220,13 @@ __global__ void __launch_bounds__(kThreads, FwdCfg<HD>::kMinBlocks)
     long long w_s = 0, w_p = 0, t_first = 0;
     for (int j = 0; j < nkb; ++j) {
       const int sb = j & 1, pb = j & 1;
-      const long long t0 = clock64();
+      const long long t0 = dbg ? clock64() : 0;
       mbar_wait(&sm.s_full[sb], (j >> 1) & 1);
-      const long long t1 = clock64();
-      if (j == 0) t_first = t1 - t_start;
-      w_s += t1 - t0;
+      if (dbg) {  // CKF_ATTN_DEBUG timings only
+        const long long t1 = clock64();
+        if (j == 0) t_first = t1 - t_start;
+        w_s += t1 - t0;
+      }
       tc_fence_after();
       uint32_t u[64];
       tmem_ld32(trow + sb * FK, *reinterpret_cast<uint32_t(*)[32]>(&u[0]));
@@ -202,20 +237,19 @@ __global__ void __launch_bounds__(kThreads, FwdCfg<HD>::kMinBlocks)
       if (lane == 0) mbar_arrive(&sm.s_free[sb]);
       const int kbase = j * FK;
       const int nvalid = min(FK, q - kbase + 1);  // keys <= q are visible (causal)
-      // row max of the visible scores: 8 independent chains (no 64-deep FMNMX dependency)
-      float mx8[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) mx8[i] = -INFINITY;
+      // row max of the visible scores: 4 independent 3-input max chains
+      float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
       if (nvalid >= FK) {
 #pragma unroll
-        for (int t = 0; t < FK; ++t) mx8[t & 7] = fmaxf(mx8[t & 7], __uint_as_float(u[t]));
+        for (int t = 0; t < FK; t += 2)
+          mx4[(t >> 1) & 3] = fmax3(mx4[(t >> 1) & 3], __uint_as_float(u[t]), __uint_as_float(u[t + 1]));
       } else {
 #pragma unroll
-        for (int t = 0; t < FK; ++t)
-          if (t < nvalid) mx8[t & 7] = fmaxf(mx8[t & 7], __uint_as_float(u[t]));
+        for (int t = 0; t < FK; t += 2)
+          mx4[(t >> 1) & 3] = fmax3(mx4[(t >> 1) & 3], t < nvalid ? __uint_as_float(u[t]) : -INFINITY,
+                                    t + 1 < nvalid ? __uint_as_float(u[t + 1]) : -INFINITY);
       }
-      const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * scale_log2;
+      const float mx = fmax3(fmaxf(mx4[0], mx4[1]), mx4[2], mx4[3]) * scale_log2;
       // lazy rescale: only when this tile's max exceeds the running max by > kRescale
       const bool need = mx > m + kRescale;
       const float mn = need ? mx : m;
@@ -237,27 +271,31 @@ __global__ void __launch_bounds__(kThreads, FwdCfg<HD>::kMinBlocks)
       }
       l *= alpha;
       m = mn;
-      const long long t2 = clock64();
+      const long long t2 = dbg ? clock64() : 0;
       mbar_wait(&sm.p_free[pb], ((j >> 1) & 1) ^ 1);  // P V_{j-2} has read this P buffer
-      w_p += clock64() - t2;
+      if (dbg) w_p += clock64() - t2;
       const uint32_t prow = smem_u32(sm.p[pb]) + r * 128;
+      const f32x2 sc2 = f2(scale_log2, scale_log2), nm2 = f2(-m, -m);
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {  // 32 keys at a time: P -> bf16 -> swizzled smem
         uint32_t w[16];
-        float l4[4] = {0.f, 0.f, 0.f, 0.f};
+        f32x2 l2[2] = {0ull, 0ull};  // (+0.f, +0.f) pairs
 #pragma unroll
         for (int t = 0; t < 32; t += 2) {
           const int tt = hf * 32 + t;
-          float p0 = ex2(fmaf(__uint_as_float(u[tt]), scale_log2, -m));
-          float p1 = ex2(fmaf(__uint_as_float(u[tt + 1]), scale_log2, -m));
+          float x0, x1;
+          f2split(ffma2(f2(__uint_as_float(u[tt]), __uint_as_float(u[tt + 1])), sc2, nm2), x0, x1);
+          float p0 = ex2(x0), p1 = ex2(x1);
           if (nvalid < FK) {
             p0 = tt < nvalid ? p0 : 0.f;
             p1 = tt + 1 < nvalid ? p1 : 0.f;
           }
-          l4[(t >> 1) & 3] += p0 + p1;
+          l2[(t >> 1) & 1] = fadd2(l2[(t >> 1) & 1], f2(p0, p1));
           w[t / 2] = pack_bf16(p0, p1);
         }
-        l += (l4[0] + l4[1]) + (l4[2] + l4[3]);
+        float la, lb;
+        f2split(fadd2(l2[0], l2[1]), la, lb);
+        l += la + lb;
 #pragma unroll
         for (int pc = 0; pc < 4; ++pc)
           st_shared_v4(prow + (((hf * 4 + pc) ^ (r & 7)) << 4), w[4 * pc], w[4 * pc + 1], w[4 * pc + 2],
@@ -572,11 +610,19 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
                                 __uint_as_float(da4.w), __uint_as_float(db4.x), __uint_as_float(db4.y),
                                 __uint_as_float(db4.z), __uint_as_float(db4.w)};
           float pv[8], dv[8];
+          const f32x2 sc2 = f2(scale_log2, scale_log2), nl2 = f2(-kLog2e, -kLog2e), neg2 = f2(-1.f, -1.f);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const float pe = ex2(fmaf(__uint_as_float(us[8 * g8 + e]), scale_log2, -lq[e] * kLog2e));
-            pv[e] = pe;
-            dv[e] = pe * (__uint_as_float(ud[8 * g8 + e]) - dq8[e]);
+          for (int e = 0; e < 8; e += 2) {  // pairs: P = 2^(S scale - lse log2e), dS = P (dP - D)
+            float x0, x1;
+            f2split(ffma2(f2(__uint_as_float(us[8 * g8 + e]), __uint_as_float(us[8 * g8 + e + 1])), sc2,
+                          fmul2(f2(lq[e], lq[e + 1]), nl2)),
+                    x0, x1);
+            pv[e] = ex2(x0);
+            pv[e + 1] = ex2(x1);
+            f2split(fmul2(f2(pv[e], pv[e + 1]),
+                          ffma2(f2(dq8[e], dq8[e + 1]), neg2,
+                                f2(__uint_as_float(ud[8 * g8 + e]), __uint_as_float(ud[8 * g8 + e + 1])))),
+                    dv[e], dv[e + 1]);
           }
           if (i < 2) {  // diagonal: query kb*128 + 64 i + c sees key kb*128 + r iff 64 i + c >= r
 #pragma unroll
@@ -801,10 +847,14 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
 #pragma unroll
         for (int g8 = 0; g8 < 8; ++g8) {
           float dv[8];
+          const f32x2 sc2 = f2(scale_log2, scale_log2), nl2 = f2(-l2, -l2), nd2 = f2(-dq, -dq);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const float pe = ex2(fmaf(__uint_as_float(us[8 * g8 + e]), scale_log2, -l2));
-            dv[e] = pe * (__uint_as_float(ud[8 * g8 + e]) - dq);
+          for (int e = 0; e < 8; e += 2) {  // pairs: dS = 2^(S scale - lse log2e) (dP - D)
+            float x0, x1;
+            f2split(ffma2(f2(__uint_as_float(us[8 * g8 + e]), __uint_as_float(us[8 * g8 + e + 1])), sc2, nl2), x0, x1);
+            f2split(fmul2(f2(ex2(x0), ex2(x1)),
+                          fadd2(f2(__uint_as_float(ud[8 * g8 + e]), __uint_as_float(ud[8 * g8 + e + 1])), nd2)),
+                    dv[e], dv[e + 1]);
           }
           if (diag) {
 #pragma unroll

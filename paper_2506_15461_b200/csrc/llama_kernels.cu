@@ -90,8 +90,10 @@ __global__ void __launch_bounds__(256) rmsnorm_fwd_kernel(const float4* __restri
   for (int i = 0; i < V4; ++i) {
     const size_t c = r * d4 + lane + 32 * i;
     const float4 gg = g[lane + 32 * i];
-    y[2 * c] = __floats2bfloat162_rn(v[i].x * rs * gg.x, v[i].y * rs * gg.y);
-    y[2 * c + 1] = __floats2bfloat162_rn(v[i].z * rs * gg.z, v[i].w * rs * gg.w);
+    const __nv_bfloat162 y0 = __floats2bfloat162_rn(v[i].x * rs * gg.x, v[i].y * rs * gg.y);
+    const __nv_bfloat162 y1 = __floats2bfloat162_rn(v[i].z * rs * gg.z, v[i].w * rs * gg.w);
+    reinterpret_cast<uint2*>(y)[c] = make_uint2(*reinterpret_cast<const uint32_t*>(&y0),
+                                                *reinterpret_cast<const uint32_t*>(&y1));  // one 8-byte store
     if (xcopy) xcopy[c] = v[i];
   }
 }
@@ -141,8 +143,9 @@ __global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(const float4* __restri
       o.w += rs * gg[i].w * a[i].w - b[i].w * coef;
       dh[c] = o;
       if (dh_bf) {
-        dh_bf[2 * c] = __floats2bfloat162_rn(o.x, o.y);
-        dh_bf[2 * c + 1] = __floats2bfloat162_rn(o.z, o.w);
+        const __nv_bfloat162 b0 = __floats2bfloat162_rn(o.x, o.y), b1 = __floats2bfloat162_rn(o.z, o.w);
+        reinterpret_cast<uint2*>(dh_bf)[c] = make_uint2(*reinterpret_cast<const uint32_t*>(&b0),
+                                                        *reinterpret_cast<const uint32_t*>(&b1));
       }
       gp[i].x += a[i].x * b[i].x * rs;
       gp[i].y += a[i].y * b[i].y * rs;
@@ -199,11 +202,10 @@ __global__ void rope_table_kernel(float2* __restrict__ tab, int T, int hd) {
 __global__ void rope_kernel(__nv_bfloat16* __restrict__ qkv, const float2* __restrict__ tab, int ntok, int T, int d,
                             int hd, int inverse) {
   const int half = hd / 2, per_head = half / 4, per_tok = 2 * d / 8;  // items per token (q and k)
-  const long long n = static_cast<long long>(ntok) * per_tok;
-  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int t = static_cast<int>(i / per_tok);
-    const int rem = static_cast<int>(i % per_tok);
+  const unsigned n = static_cast<unsigned>(ntok) * static_cast<unsigned>(per_tok);  // < 2^32 (host check)
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int t = static_cast<int>(i / static_cast<unsigned>(per_tok));  // 32-bit division
+    const int rem = static_cast<int>(i - static_cast<unsigned>(t) * static_cast<unsigned>(per_tok));
     const int hh = rem / per_head;  // 0..2H-1 (q heads then k heads)
     const int j = (rem % per_head) * 4;
     __nv_bfloat16* base = qkv + static_cast<size_t>(t) * 3 * d + static_cast<size_t>(hh) * hd;
@@ -717,6 +719,7 @@ void rope(bf16* qkv, size_t ntok, size_t T, size_t d, size_t heads, int inverse,
   if (hd % 8) raise(1, "head_dim must be a multiple of 8 for RoPE");
   const float2* tab = rope_table(T, hd, s);
   const size_t items = ntok * (2 * d / 8);
+  if (items >= (1ull << 32)) raise(1, "rope: too many tokens in one call");
   rope_kernel<<<grid_for(items, 256), 256, 0, s>>>(qkv, tab, static_cast<int>(ntok), static_cast<int>(T),
                                                    static_cast<int>(d), static_cast<int>(hd), inverse);
   CKF_LAUNCH_CHECK();

@@ -6,7 +6,7 @@ import numpy as np
 import torch
 import paper_2506_15461_b200  # noqa
 from paper_2506_15461_b200._native import check, lib
-B, T, H, hd = int(os.environ.get('B', 64)), 1024, 8, 64
+B, T, H, hd = (int(os.environ.get(k, v)) for k, v in (('B', 64), ('T', 1024), ('H', 8), ('HD', 64)))
 qkv = torch.randn(B * T, 3 * H * hd, device="cuda").bfloat16()
 o = torch.empty(B * T, H * hd, dtype=torch.bfloat16, device="cuda")
 lse = torch.empty(B * H * T, device="cuda")
