@@ -101,60 +101,65 @@ __global__ void __launch_bounds__(256) rmsnorm_fwd_kernel(const float4* __restri
 constexpr int kBwdRowsPerBlock = 16;  // 512 CTAs for 8192 rows: enough warps in flight per SM
 
 // dh += rstd*u - x*rstd^3*(u.x)/d with u = g*dy; gain partial += dy*x*rstd.
-// One warp per row, row and gain partials held in registers (lane owns
-// columns lane + 32 i), the 8 warps' partials folded in fixed order.
+// One warp per row (lane owns columns lane + 32 i); dy, x and dh of the row are loaded
+// together.  The gains and each warp's gain partials live in shared memory, not registers,
+// which keeps d = 512 at two 256-thread blocks per SM without spills (more rows in flight); the 8 warps'
+// partials are folded in fixed order.
 template <int V4>  // float4 per lane (d = 128 * V4)
-__global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(const float4* __restrict__ dy, const float4* __restrict__ x,
-                                                          const float4* __restrict__ g,
-                                                          const float* __restrict__ rstd, size_t rows,
-                                                          float4* __restrict__ dh,
-                                                          __nv_bfloat162* __restrict__ dh_bf,
-                                                          float* __restrict__ gpart) {
-  extern __shared__ float4 sg[];  // [kWarpsPerBlock][d4]
+__global__ void __launch_bounds__(256, (V4 <= 4 ? 2 : 1))
+    rmsnorm_bwd_kernel(const float4* __restrict__ dy, const float4* __restrict__ x, const float4* __restrict__ g,
+                       const float* __restrict__ rstd, size_t rows, float4* __restrict__ dh,
+                       __nv_bfloat162* __restrict__ dh_bf, float* __restrict__ gpart) {
+  extern __shared__ float4 sg[];  // [kWarpsPerBlock][d4] gain partials, then [d4] gains
   constexpr int d4 = 32 * V4;
+  float4* sgg = sg + kWarpsPerBlock * d4;
   const int w = threadIdx.x / 32, lane = threadIdx.x & 31;
-  float4 gp[V4], gg[V4];
+  float4* gpw = sg + static_cast<size_t>(w) * d4;
+  for (int c = threadIdx.x; c < d4; c += blockDim.x) sgg[c] = g[c];
 #pragma unroll
-  for (int i = 0; i < V4; ++i) {
-    gp[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    gg[i] = g[lane + 32 * i];
-  }
+  for (int i = 0; i < V4; ++i) gpw[lane + 32 * i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  __syncthreads();
   const size_t r0 = static_cast<size_t>(blockIdx.x) * kBwdRowsPerBlock;
   for (size_t r = r0 + w; r < r0 + kBwdRowsPerBlock && r < rows; r += kWarpsPerBlock) {
     const float rs = rstd[r];
-    float4 a[V4], b[V4];
+    float4 a[V4], b[V4], o4[V4];
     float dot = 0.f;
 #pragma unroll
-    for (int i = 0; i < V4; ++i) {
+    for (int i = 0; i < V4; ++i) {  // dy, x and the dh being accumulated into: all in flight at once
       a[i] = dy[r * d4 + lane + 32 * i];
       b[i] = x[r * d4 + lane + 32 * i];
-      dot += gg[i].x * a[i].x * b[i].x + gg[i].y * a[i].y * b[i].y + gg[i].z * a[i].z * b[i].z +
-             gg[i].w * a[i].w * b[i].w;
+      if (V4 <= 8) o4[i] = dh[r * d4 + lane + 32 * i];
+    }
+#pragma unroll
+    for (int i = 0; i < V4; ++i) {
+      const float4 gg = sgg[lane + 32 * i];
+      dot += gg.x * a[i].x * b[i].x + gg.y * a[i].y * b[i].y + gg.z * a[i].z * b[i].z + gg.w * a[i].w * b[i].w;
     }
     dot = warp_sum_f(dot);
     const float coef = rs * rs * rs * dot / static_cast<float>(4 * d4);
 #pragma unroll
     for (int i = 0; i < V4; ++i) {
       const size_t c = r * d4 + lane + 32 * i;
-      float4 o = dh[c];
-      o.x += rs * gg[i].x * a[i].x - b[i].x * coef;
-      o.y += rs * gg[i].y * a[i].y - b[i].y * coef;
-      o.z += rs * gg[i].z * a[i].z - b[i].z * coef;
-      o.w += rs * gg[i].w * a[i].w - b[i].w * coef;
+      const float4 gg = sgg[lane + 32 * i];
+      float4 o = V4 <= 8 ? o4[i] : dh[c];
+      o.x += rs * gg.x * a[i].x - b[i].x * coef;
+      o.y += rs * gg.y * a[i].y - b[i].y * coef;
+      o.z += rs * gg.z * a[i].z - b[i].z * coef;
+      o.w += rs * gg.w * a[i].w - b[i].w * coef;
       dh[c] = o;
       if (dh_bf) {
         const __nv_bfloat162 b0 = __floats2bfloat162_rn(o.x, o.y), b1 = __floats2bfloat162_rn(o.z, o.w);
         reinterpret_cast<uint2*>(dh_bf)[c] = make_uint2(*reinterpret_cast<const uint32_t*>(&b0),
                                                         *reinterpret_cast<const uint32_t*>(&b1));
       }
-      gp[i].x += a[i].x * b[i].x * rs;
-      gp[i].y += a[i].y * b[i].y * rs;
-      gp[i].z += a[i].z * b[i].z * rs;
-      gp[i].w += a[i].w * b[i].w * rs;
+      float4 gp = gpw[lane + 32 * i];
+      gp.x += a[i].x * b[i].x * rs;
+      gp.y += a[i].y * b[i].y * rs;
+      gp.z += a[i].z * b[i].z * rs;
+      gp.w += a[i].w * b[i].w * rs;
+      gpw[lane + 32 * i] = gp;
     }
   }
-#pragma unroll
-  for (int i = 0; i < V4; ++i) sg[static_cast<size_t>(w) * d4 + lane + 32 * i] = gp[i];
   __syncthreads();
   const float* sgf = reinterpret_cast<const float*>(sg);
   for (int c = threadIdx.x; c < 4 * d4; c += blockDim.x) {
@@ -656,7 +661,7 @@ int rmsnorm_bwd_blocks(size_t rows) { return static_cast<int>((rows + kBwdRowsPe
 template <int V4>
 void rmsnorm_bwd_t(const float* dy, const float* x, const float* g, const float* rstd, size_t rows, float* dh,
                    bf16* dh_bf, float* gpart, cudaStream_t s) {
-  const size_t smem = kWarpsPerBlock * V4 * 32 * sizeof(float4);
+  const size_t smem = (kWarpsPerBlock + 1) * V4 * 32 * sizeof(float4);  // partials + gains
   static bool attr = false;
   if (!attr) {
     CKF_CUDA(cudaFuncSetAttribute(rmsnorm_bwd_kernel<V4>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -1,6 +1,8 @@
 #!/usr/bin/env python
 """Summarise an ncu launch list (--metrics gpu__time_duration.sum --csv) by kernel:
-launches, total device time, share.  Usage: ncu_summary.py launches.csv [--skip N]"""
+launches, total device time, share.  Usage: ncu_summary.py launches.csv [--window MARKER]
+--window: only the launches from the first launch whose name contains MARKER up to (not
+including) the next one -- e.g. xent_pipe_kernel, once per training step."""
 import csv
 import collections
 import re
@@ -10,6 +12,11 @@ import sys
 def main():
     path = sys.argv[1]
     rows = [r for r in csv.reader(open(path)) if len(r) > 10 and r[0] != "ID"]
+    if "--window" in sys.argv:
+        mk = sys.argv[sys.argv.index("--window") + 1]
+        idx = [i for i, r in enumerate(rows) if mk in r[4]]
+        if len(idx) >= 2:
+            rows = rows[idx[0]:idx[1]]
     tot = collections.OrderedDict()
     for r in rows:
         name = re.sub(r"\(.*", "", r[4]).replace("void ", "")
