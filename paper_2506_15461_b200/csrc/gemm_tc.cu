@@ -503,10 +503,10 @@ __global__ void __launch_bounds__(gemm_threads(EPI, NCTA), 1)
         if constexpr (EPI == kStoreBF16) {
           // fused RoPE: this 64-column chunk is one head of q or k; rotate (j, j+32) in fp32
           if (p.rope_tab && w.nb * BN + c0 < p.rope_cols) {
-            const float2* cs = p.rope_tab + static_cast<size_t>((m0 + lane) % p.rope_T) * 32;
+            const float2* cs = p.rope_tab + (m0 + lane) % p.rope_T;  // pair-major: coalesced per j
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-              const float2 t = cs[j];
+              const float2 t = cs[static_cast<size_t>(j) * p.rope_T];
               const float x1 = __uint_as_float(r[j]), x2 = __uint_as_float(r[j + 32]);
               r[j] = __float_as_uint(x1 * t.x - x2 * t.y);
               r[j + 32] = __float_as_uint(x2 * t.x + x1 * t.y);

@@ -33,7 +33,8 @@ struct GemmDesc {
   int bn = 0;      // 0 = heuristic (128 or 256)
   int splits = 0;  // split-K factor; 0 = heuristic (kAccF32 only; ordered, deterministic)
   // fused rotary embedding (kStoreBF16 only): columns [0, rope_cols) are 64-wide heads whose
-  // (j, j+32) pairs are rotated by rope_tab[(row % rope_T) * 32 + j] = (cos, sin)
+  // (j, j+32) pairs are rotated by rope_tab[j * rope_T + row % rope_T] = (cos, sin) (the
+  // pair-major table: a warp's 32 consecutive rows read 32 adjacent entries)
   const float2* rope_tab = nullptr;
   int rope_T = 0, rope_cols = 0;
   void* aux = nullptr;  // kSwiGLU: a (written); kSwiGLUBwd: gu (read)

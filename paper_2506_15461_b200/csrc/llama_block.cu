@@ -470,7 +470,7 @@ struct LlamaBlock final : BlockImpl {
     timed(KC_NORM, 0.0, Mt * d * 10.0, [&] { llama::rmsnorm_fwd(h, Wf + off.g1, Mt, d, w.xn1, c.rstd1, c.h_in, st); });
     if (hd == 64) {  // RoPE fused into the QKV GEMM epilogue (q and k column blocks)
       gemm(Mi, 3 * di, di, w.xn1, di, false, W + off.wqkv, 3 * di, true, c.qkv, 3 * di, tc::kStoreBF16,
-           llama::rope_table(T, hd, st), static_cast<int>(2 * d));
+           llama::rope_table_pair_major(T, hd, st), static_cast<int>(2 * d));
     } else {
       gemm(Mi, 3 * di, di, w.xn1, di, false, W + off.wqkv, 3 * di, true, c.qkv, 3 * di, tc::kStoreBF16);
       timed(KC_NORM, 0.0, Mt * d * 8.0, [&] { llama::rope(c.qkv, Mt, T, d, H, 0, st); });

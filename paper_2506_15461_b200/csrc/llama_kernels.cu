@@ -192,11 +192,13 @@ __global__ void gain_fold_kernel(const float* __restrict__ gpart, int nblk, int 
 
 // ---------------------------------------------------------------- RoPE
 // cos/sin table [T][hd/2] (float2), built once per (T, hd) on the device
-__global__ void rope_table_kernel(float2* __restrict__ tab, int T, int hd) {
+__global__ void rope_table_kernel(float2* __restrict__ tab, int T, int hd, int pair_major) {
   const int half = hd / 2;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= T * half) return;
-  const int pos = i / half, j = i % half;
+  // [T][hd/2] (position-major) or [hd/2][T] (pair-major: consecutive positions adjacent, so
+  // a warp of consecutive rows reads one table entry each with coalesced loads)
+  const int pos = pair_major ? i % T : i / half, j = pair_major ? i / T : i % half;
   const double inv = exp2(-static_cast<double>(2 * j) / hd * log2(static_cast<double>(kRopeTheta)));
   double sn, cs;
   sincos(static_cast<double>(pos) * inv, &sn, &cs);
@@ -697,27 +699,30 @@ void gain_fold(const float* gpart, int nblk, size_t d, float* gg, cudaStream_t s
   CKF_LAUNCH_CHECK();
 }
 
-const float2* rope_table(size_t T, size_t hd, cudaStream_t s) {
-  // per-(T, hd) cos/sin table, built once per device
+static const float2* rope_table_impl(size_t T, size_t hd, int pair_major, cudaStream_t s) {
+  // per-(T, hd, layout) cos/sin table, built once per device
   struct Tab {
     size_t T, hd;
-    int dev;
+    int pm, dev;
     float2* p;
   };
   static std::vector<Tab> tabs;
   int dev = 0;
   CKF_CUDA(cudaGetDevice(&dev));
   for (auto& t : tabs)
-    if (t.T == T && t.hd == hd && t.dev == dev) return t.p;
+    if (t.T == T && t.hd == hd && t.pm == pair_major && t.dev == dev) return t.p;
   float2* tab = nullptr;
   CKF_CUDA(cudaMalloc(&tab, T * hd / 2 * sizeof(float2)));
   ++alloc_epoch();
   rope_table_kernel<<<static_cast<unsigned>((T * hd / 2 + 255) / 256), 256, 0, s>>>(tab, static_cast<int>(T),
-                                                                                   static_cast<int>(hd));
+                                                                                   static_cast<int>(hd), pair_major);
   CKF_LAUNCH_CHECK();
-  tabs.push_back({T, hd, dev, tab});
+  tabs.push_back({T, hd, pair_major, dev, tab});
   return tab;
 }
+
+const float2* rope_table(size_t T, size_t hd, cudaStream_t s) { return rope_table_impl(T, hd, 0, s); }
+const float2* rope_table_pair_major(size_t T, size_t hd, cudaStream_t s) { return rope_table_impl(T, hd, 1, s); }
 
 void rope(bf16* qkv, size_t ntok, size_t T, size_t d, size_t heads, int inverse, cudaStream_t s) {
   const size_t hd = d / heads;

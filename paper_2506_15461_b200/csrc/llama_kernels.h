@@ -38,6 +38,8 @@ void gain_fold(const float* gpart, int nblk, size_t d, float* gg, cudaStream_t s
 void rope(bf16* qkv, size_t ntok, size_t T, size_t d, size_t heads, int inverse, cudaStream_t s);
 // device cos/sin table [T][hd/2] (float2), built on first use (the QKV GEMM epilogue reads it)
 const float2* rope_table(size_t T, size_t hd, cudaStream_t s);
+// the same values laid out [hd/2][T] (the GEMM epilogue's fused RoPE reads it)
+const float2* rope_table_pair_major(size_t T, size_t hd, cudaStream_t s);
 
 // a = silu(gate) * up ; gu = [gate | up] (ntok x 2f)
 void swiglu_fwd(const bf16* gu, size_t ntok, size_t f, bf16* a, cudaStream_t s);
