@@ -237,70 +237,89 @@ __global__ void __launch_bounds__(kThreads, FwdCfg<HD>::kMinBlocks)
       if (lane == 0) mbar_arrive(&sm.s_free[sb]);
       const int kbase = j * FK;
       const int nvalid = min(FK, q - kbase + 1);  // keys <= q are visible (causal)
-      // row max of the visible scores: 4 independent 3-input max chains
-      float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-      if (nvalid >= FK) {
+      const uint32_t prow = smem_u32(sm.p[pb]) + r * 128;
+      // P = 2^(S scale - mc) -> bf16 -> swizzled smem (32 keys at a time); returns the row sum
+      auto write_p = [&](float mc) -> float {
+        const f32x2 sc2 = f2(scale_log2, scale_log2), nm2 = f2(-mc, -mc);
+        float lt = 0.f;
 #pragma unroll
-        for (int t = 0; t < FK; t += 2)
-          mx4[(t >> 1) & 3] = fmax3(mx4[(t >> 1) & 3], __uint_as_float(u[t]), __uint_as_float(u[t + 1]));
-      } else {
+        for (int hf = 0; hf < 2; ++hf) {
+          uint32_t w[16];
+          f32x2 l2[2] = {0ull, 0ull};  // (+0.f, +0.f) pairs
 #pragma unroll
-        for (int t = 0; t < FK; t += 2)
-          mx4[(t >> 1) & 3] = fmax3(mx4[(t >> 1) & 3], t < nvalid ? __uint_as_float(u[t]) : -INFINITY,
-                                    t + 1 < nvalid ? __uint_as_float(u[t + 1]) : -INFINITY);
-      }
-      const float mx = fmax3(fmaxf(mx4[0], mx4[1]), mx4[2], mx4[3]) * scale_log2;
-      // lazy rescale: only when this tile's max exceeds the running max by > kRescale
-      const bool need = mx > m + kRescale;
-      const float mn = need ? mx : m;
-      const float alpha = need ? ex2(m - mn) : 1.f;  // m = -inf on the first tile -> 0
-      if (__any_sync(0xffffffffu, need) && j > 0) {
-        // the previous P V must have landed before this warp rewrites its O rows
-        mbar_wait(&sm.p_free[(j - 1) & 1], ((j - 1) >> 1) & 1);
-        tc_fence_after();
+          for (int t = 0; t < 32; t += 2) {
+            const int tt = hf * 32 + t;
+            float x0, x1;
+            f2split(ffma2(f2(__uint_as_float(u[tt]), __uint_as_float(u[tt + 1])), sc2, nm2), x0, x1);
+            float p0 = ex2(x0), p1 = ex2(x1);
+            if (nvalid < FK) {
+              p0 = tt < nvalid ? p0 : 0.f;
+              p1 = tt + 1 < nvalid ? p1 : 0.f;
+            }
+            l2[(t >> 1) & 1] = fadd2(l2[(t >> 1) & 1], f2(p0, p1));
+            w[t / 2] = pack_bf16(p0, p1);
+          }
+          float la, lb;
+          f2split(fadd2(l2[0], l2[1]), la, lb);
+          lt += la + lb;
 #pragma unroll
-        for (int hf = 0; hf < HD / 32; ++hf) {
-          uint32_t ov[32];
-          tmem_ld32(trow + 128 + hf * 32, ov);
-          tmem_ld_wait();
-#pragma unroll
-          for (int t = 0; t < 32; ++t) ov[t] = __float_as_uint(__uint_as_float(ov[t]) * alpha);
-          tmem_st32(trow + 128 + hf * 32, ov);
+          for (int pc = 0; pc < 4; ++pc)
+            st_shared_v4(prow + (((hf * 4 + pc) ^ (r & 7)) << 4), w[4 * pc], w[4 * pc + 1], w[4 * pc + 2],
+                         w[4 * pc + 3]);
         }
-        tmem_st32_wait();
-      }
-      l *= alpha;
-      m = mn;
+        return lt;
+      };
       const long long t2 = dbg ? clock64() : 0;
       mbar_wait(&sm.p_free[pb], ((j >> 1) & 1) ^ 1);  // P V_{j-2} has read this P buffer
       if (dbg) w_p += clock64() - t2;
-      const uint32_t prow = smem_u32(sm.p[pb]) + r * 128;
-      const f32x2 sc2 = f2(scale_log2, scale_log2), nm2 = f2(-m, -m);
-#pragma unroll
-      for (int hf = 0; hf < 2; ++hf) {  // 32 keys at a time: P -> bf16 -> swizzled smem
-        uint32_t w[16];
-        f32x2 l2[2] = {0ull, 0ull};  // (+0.f, +0.f) pairs
-#pragma unroll
-        for (int t = 0; t < 32; t += 2) {
-          const int tt = hf * 32 + t;
-          float x0, x1;
-          f2split(ffma2(f2(__uint_as_float(u[tt]), __uint_as_float(u[tt + 1])), sc2, nm2), x0, x1);
-          float p0 = ex2(x0), p1 = ex2(x1);
-          if (nvalid < FK) {
-            p0 = tt < nvalid ? p0 : 0.f;
-            p1 = tt + 1 < nvalid ? p1 : 0.f;
-          }
-          l2[(t >> 1) & 1] = fadd2(l2[(t >> 1) & 1], f2(p0, p1));
-          w[t / 2] = pack_bf16(p0, p1);
-        }
-        float la, lb;
-        f2split(fadd2(l2[0], l2[1]), la, lb);
-        l += la + lb;
-#pragma unroll
-        for (int pc = 0; pc < 4; ++pc)
-          st_shared_v4(prow + (((hf * 4 + pc) ^ (r & 7)) << 4), w[4 * pc], w[4 * pc + 1], w[4 * pc + 2],
-                       w[4 * pc + 3]);
+      // Fast path (every tile after the first): P against the running max m with no max pass;
+      // kept when the tile's row sum stays <= 2^16 (so every P <= 2^16, finite).  Otherwise --
+      // a score above m + 16 in log2 units, or the first tile -- the tile is redone against its
+      // own max with the lazy rescale of O and l (only when it exceeds m by > kRescale).
+      float lt = 0.f;
+      bool slow = j == 0;
+      if (!slow) {
+        lt = write_p(m);
+        slow = __any_sync(0xffffffffu, !(lt <= 65536.f));
       }
+      if (slow) {
+        // row max of the visible scores: 4 independent 3-input max chains
+        float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        if (nvalid >= FK) {
+#pragma unroll
+          for (int t = 0; t < FK; t += 2)
+            mx4[(t >> 1) & 3] = fmax3(mx4[(t >> 1) & 3], __uint_as_float(u[t]), __uint_as_float(u[t + 1]));
+        } else {
+#pragma unroll
+          for (int t = 0; t < FK; t += 2)
+            mx4[(t >> 1) & 3] = fmax3(mx4[(t >> 1) & 3], t < nvalid ? __uint_as_float(u[t]) : -INFINITY,
+                                      t + 1 < nvalid ? __uint_as_float(u[t + 1]) : -INFINITY);
+        }
+        const float mx = fmax3(fmaxf(mx4[0], mx4[1]), mx4[2], mx4[3]) * scale_log2;
+        // lazy rescale: only when this tile's max exceeds the running max by > kRescale
+        const bool need = mx > m + kRescale;
+        const float mn = need ? mx : m;
+        const float alpha = need ? ex2(m - mn) : 1.f;  // m = -inf on the first tile -> 0
+        if (__any_sync(0xffffffffu, need) && j > 0) {
+          // the previous P V must have landed before this warp rewrites its O rows
+          mbar_wait(&sm.p_free[(j - 1) & 1], ((j - 1) >> 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int hf = 0; hf < HD / 32; ++hf) {
+            uint32_t ov[32];
+            tmem_ld32(trow + 128 + hf * 32, ov);
+            tmem_ld_wait();
+#pragma unroll
+            for (int t = 0; t < 32; ++t) ov[t] = __float_as_uint(__uint_as_float(ov[t]) * alpha);
+            tmem_st32(trow + 128 + hf * 32, ov);
+          }
+          tmem_st32_wait();
+        }
+        l *= alpha;
+        m = mn;
+        lt = write_p(m);
+      }
+      l += lt;
       fence_proxy_async();
       tc_fence_before();
       __syncwarp();

@@ -47,6 +47,28 @@ def test_forward_vs_torch(impl, shape):
     assert (lse - rl).abs().max().item() < 1e-3 * max(1.0, rl.abs().max().item())
 
 
+@pytest.mark.parametrize("hd", [64, 128])
+def test_forward_rising_scores_rescale_paths(hd):
+    """Scores that grow along the key axis (k_t = (1 + t/2) * a shared direction, q along it
+    too): every later 64-key tile beats the running max, which exercises the redo of a tile
+    against its own max and the lazy O / l rescale (the fast path keeps P <= 2^16)."""
+    import paper_2506_15461_b200  # noqa: F401
+    torch.manual_seed(3)
+    B, T, H = 1, 1024, 2
+    dirn = torch.randn(hd, device="cuda")
+    dirn = dirn / dirn.norm()
+    x = torch.randn(B * T, 3, H, hd, device="cuda") * 0.3
+    ramp = 1.0 + torch.arange(T, device="cuda", dtype=torch.float32) / 2.0  # ~23 log2 units per 64 keys
+    x[:, 0] += 4.0 * dirn  # q along the shared direction
+    x[:, 1] += ramp[:, None, None] * dirn  # k grows along it
+    qkv = x.reshape(B * T, 3 * H * hd).bfloat16()
+    o, lse = _fwd(qkv, B, T, H, hd, 2)
+    ro, rl = _ref(qkv, B, T, H, hd)
+    assert torch.isfinite(o.float()).all()
+    assert ((o.float() - ro).norm() / ro.norm()).item() < 2e-2
+    assert ((lse - rl).abs() / rl.abs().clamp(min=1.0)).max().item() < 1e-3
+
+
 def test_tcgen05_matches_mma_sync():
     import paper_2506_15461_b200  # noqa: F401
     torch.manual_seed(1)
