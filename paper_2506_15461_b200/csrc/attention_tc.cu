@@ -36,38 +36,9 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-// Packed fp32x2 arithmetic (FFMA2 / FADD2 / FMUL2) and the 3-input max (FMNMX3) of sm_100:
+// Packed fp32x2 arithmetic (FFMA2 / FADD2 / FMUL2, common.cuh) and the 3-input max (FMNMX3):
 // the softmax loops are issue-bound (a polynomial exp2 on the FMA pipe made them slower, so
 // MUFU is not the limit), and these halve their FMA / add / max instruction counts.
-using f32x2 = unsigned long long;
-__device__ __forceinline__ f32x2 f2(float a, float b) {
-  f32x2 r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-  return r;
-}
-__device__ __forceinline__ void f2split(f32x2 v, float& a, float& b) {
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
-}
-__device__ __forceinline__ f32x2 ffma2(f32x2 a, f32x2 b, f32x2 c) {
-  f32x2 d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
-__device__ __forceinline__ f32x2 fadd2(f32x2 a, f32x2 b) {
-  f32x2 d;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ f32x2 fmul2(f32x2 a, f32x2 b) {
-  f32x2 d;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ float fmax3(float a, float b, float c) {
-  float d;
-  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
-  return d;
-}
 
 // A [rows x HD] bf16 tile in shared memory as HD/64 K-major SW128 chunks of [rows][128 B]:
 // TMA brings each 64-column chunk; UMMA K step k (16 columns) reads chunk k/4 at byte 32 (k%4).

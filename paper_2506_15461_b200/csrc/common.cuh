@@ -69,13 +69,60 @@ __host__ __device__ __forceinline__ uint64_t derive_key(uint64_t seed, uint64_t 
 // fused GEMM epilogues (gemm_tc.cu), so both produce the same bits.  Branch-free
 // (approximate reciprocal): the fused epilogue issues it from one warp per SM
 // sub-partition and needs the ILP.
-__device__ __forceinline__ float swiglu_sig(float g) { return __fdividef(1.f, 1.f + __expf(-g)); }
-__device__ __forceinline__ float swiglu_fwd1(float g, float u) { return g * swiglu_sig(g) * u; }
-// d = dL/da; writes dL/dg, dL/du
-__device__ __forceinline__ void swiglu_bwd1(float g, float u, float d, float& dg, float& du) {
-  const float sg = swiglu_sig(g);
-  dg = d * u * sg * (1.f + g * (1.f - sg));
-  du = d * g * sg;
+// Packed fp32x2 arithmetic of sm_100 (FFMA2 / FADD2 / FMUL2: two IEEE fp32 operations per
+// instruction, each lane rounding exactly like its scalar counterpart) and the 3-input max.
+using f32x2 = unsigned long long;
+__device__ __forceinline__ f32x2 f2(float a, float b) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2split(f32x2 v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ f32x2 ffma2(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f32x2 fadd2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f32x2 fmul2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
+// SwiGLU on pairs of columns, one fixed instruction sequence shared by the fused GEMM
+// epilogues and the standalone kernels (so the two paths stay bit-identical):
+// sig(g) = rcp(1 + 2^(-g log2 e)) (MUFU ex2 / rcp), a = g sig(g) u,
+// dg = d u sig (1 + g (1 - sig)), du = d g sig.
+__device__ __forceinline__ f32x2 swiglu_sig2(f32x2 g) {
+  float e0, e1;
+  f2split(fmul2(g, f2(-1.4426950408889634f, -1.4426950408889634f)), e0, e1);
+  asm("ex2.approx.ftz.f32 %0, %0;" : "+f"(e0));
+  asm("ex2.approx.ftz.f32 %0, %0;" : "+f"(e1));
+  float d0, d1;
+  f2split(fadd2(f2(e0, e1), f2(1.f, 1.f)), d0, d1);
+  asm("rcp.approx.ftz.f32 %0, %0;" : "+f"(d0));
+  asm("rcp.approx.ftz.f32 %0, %0;" : "+f"(d1));
+  return f2(d0, d1);
+}
+__device__ __forceinline__ f32x2 swiglu_fwd2(f32x2 g, f32x2 u) { return fmul2(fmul2(g, swiglu_sig2(g)), u); }
+// d = dL/da; returns dL/dg, dL/du
+__device__ __forceinline__ void swiglu_bwd2(f32x2 g, f32x2 u, f32x2 d, f32x2& dg, f32x2& du) {
+  const f32x2 sg = swiglu_sig2(g), one = f2(1.f, 1.f);
+  du = fmul2(fmul2(d, g), sg);
+  const f32x2 inner = ffma2(g, ffma2(sg, f2(-1.f, -1.f), one), one);  // 1 + g (1 - sig)
+  dg = fmul2(fmul2(fmul2(d, u), sg), inner);
 }
 
 __device__ __forceinline__ double counter_uniform_at(uint64_t key, uint64_t counter, double lo, double hi) {

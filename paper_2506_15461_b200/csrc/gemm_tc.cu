@@ -415,7 +415,9 @@ __global__ void __launch_bounds__(gemm_threads(EPI, NCTA), 1)
           for (int j = 0; j < 32; ++j) {
             const float g0 = __uint_as_float(g[2 * j]), g1 = __uint_as_float(g[2 * j + 1]);
             const float u0 = __uint_as_float(pk[j] << 16), u1 = __uint_as_float(pk[j] & 0xffff0000u);
-            pk[j] = pack_bf16(swiglu_fwd1(g0, u0), swiglu_fwd1(g1, u1));
+            float a0, a1;
+            f2split(swiglu_fwd2(f2(g0, g1), f2(u0, u1)), a0, a1);
+            pk[j] = pack_bf16(a0, a1);
           }
           store_bf16_chunk(pk, &tmap_ws, n0, m0);
         }
@@ -466,10 +468,12 @@ __global__ void __launch_bounds__(gemm_threads(EPI, NCTA), 1)
               // da rounded to bf16 exactly as the unfused path stores it, then swiglu_bwd's arithmetic
               const uint32_t dpk = pack_bf16(__uint_as_float(r[8 * j + 2 * e]), __uint_as_float(r[8 * j + 2 * e + 1]));
               float dg0, du0, dg1, du1;
-              swiglu_bwd1(__uint_as_float(gw[e] << 16), __uint_as_float(uw[e] << 16), __uint_as_float(dpk << 16),
-                          dg0, du0);
-              swiglu_bwd1(__uint_as_float(gw[e] & 0xffff0000u), __uint_as_float(uw[e] & 0xffff0000u),
-                          __uint_as_float(dpk & 0xffff0000u), dg1, du1);
+              f32x2 dg2, du2;
+              swiglu_bwd2(f2(__uint_as_float(gw[e] << 16), __uint_as_float(gw[e] & 0xffff0000u)),
+                          f2(__uint_as_float(uw[e] << 16), __uint_as_float(uw[e] & 0xffff0000u)),
+                          f2(__uint_as_float(dpk << 16), __uint_as_float(dpk & 0xffff0000u)), dg2, du2);
+              f2split(dg2, dg0, dg1);
+              f2split(du2, du0, du1);
               pg[e] = pack_bf16(dg0, dg1);
               pu[e] = pack_bf16(du0, du1);
             }

@@ -264,7 +264,7 @@ __global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ gu, int ntok
     unpack8(*reinterpret_cast<const uint4*>(row + c), g);
     unpack8(*reinterpret_cast<const uint4*>(row + f + c), u);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) o[k] = swiglu_fwd1(g[k], u[k]);
+    for (int k = 0; k < 8; k += 2) f2split(swiglu_fwd2(f2(g[k], g[k + 1]), f2(u[k], u[k + 1])), o[k], o[k + 1]);
     *reinterpret_cast<uint4*>(a + static_cast<size_t>(t) * f + c) = pack8(o);
   }
 }
@@ -281,7 +281,12 @@ __global__ void swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ gu, const __
     unpack8(*reinterpret_cast<const uint4*>(row + f + c), u);
     unpack8(*reinterpret_cast<const uint4*>(da + static_cast<size_t>(t) * f + c), dd);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) swiglu_bwd1(g[k], u[k], dd[k], dg[k], du[k]);
+    for (int k = 0; k < 8; k += 2) {
+      f32x2 dg2, du2;
+      swiglu_bwd2(f2(g[k], g[k + 1]), f2(u[k], u[k + 1]), f2(dd[k], dd[k + 1]), dg2, du2);
+      f2split(dg2, dg[k], dg[k + 1]);
+      f2split(du2, du[k], du[k + 1]);
+    }
     __nv_bfloat16* out = dgu + static_cast<size_t>(t) * 2 * f;
     *reinterpret_cast<uint4*>(out + c) = pack8(dg);
     *reinterpret_cast<uint4*>(out + f + c) = pack8(du);
