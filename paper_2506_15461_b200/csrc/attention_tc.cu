@@ -513,6 +513,12 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
         mbar_wait(&sm.acc_free[aset], ((lu / NA) & 1) ^ 1);
         for (int i = 0; i < ntiles; ++i) {
           const int gi = g + i, st = gi % ST, bb = gi & 1;
+          // S/dP of tile i+2 go in as soon as this group's softmax has read S/dP of tile i
+          // (s_free), so they run under that softmax instead of after its dV/dK MMAs.  Needs a
+          // fourth Q/dO stage: with two, tile i+2 reuses the stage tile i's dV/dK still reads, and
+          // with three its load waits on tile i-1's MMAs (measured 13 % slower at hd 128).
+          if constexpr (ST >= 4)
+            if (i + 2 < ntiles) issue_s(gi + 2);
           mbar_wait(&sm.pd_full[bb], (gi >> 1) & 1);
           tc_fence_after();
           const uint32_t qa = smem_u32(sm.q[st]), oa = smem_u32(sm.d_o[st]);
@@ -526,7 +532,8 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
           }
           umma_commit(&sm.pd_free[bb]);
           umma_commit(&sm.qd_empty[st]);
-          if (i + 2 < ntiles) issue_s(gi + 2);
+          if constexpr (ST < 4)
+            if (i + 2 < ntiles) issue_s(gi + 2);
         }
         umma_commit(&sm.acc_full[aset]);
         umma_commit(&sm.kv_empty[kbuf]);
@@ -759,6 +766,9 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
         mbar_wait(&sm.acc_free[aset], ((lu >> 1) & 1) ^ 1);
         for (int j = 0; j < ntiles; ++j) {
           const int gj = g + j, st = gj % ST, bb = gj & 1;
+          // S/dP of tile j+2 as soon as this group's softmax has read tile j's (see dK dV)
+          if constexpr (ST >= 4)
+            if (j + 2 < ntiles) issue_s(gj + 2);
           mbar_wait(&sm.ds_full[bb], (gj >> 1) & 1);
           tc_fence_after();
           const uint32_t ka = smem_u32(sm.k[st]), da = smem_u32(sm.ds[bb]);
@@ -768,7 +778,8 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
                       kIdQ, (j > 0 || k > 0) ? 1u : 0u);
           umma_commit(&sm.ds_free[bb]);
           umma_commit(&sm.kv_empty[st]);
-          if (j + 2 < ntiles) issue_s(gj + 2);
+          if constexpr (ST < 4)
+            if (j + 2 < ntiles) issue_s(gj + 2);
         }
         umma_commit(&sm.acc_full[aset]);
         umma_commit(&sm.qd_empty[qbuf]);
