@@ -387,7 +387,7 @@ struct BwdCfg {
   static constexpr uint32_t kUnit = TK * HD * 2;   // 128-row unit operand tile
   static constexpr uint32_t kInner = PT * HD * 2;  // 64-row inner tile
   static constexpr int kNU = HD == 64 ? 2 : 1;     // unit operand buffers (dK dV kernel)
-  static constexpr int kSt = HD == 64 ? 4 : 2;     // inner-tile stages (dK dV kernel)
+  static constexpr int kSt = HD == 64 ? 4 : 3;     // inner-tile stages (dK dV kernel)
   static constexpr int kNAcc = HD == 64 ? 2 : 1;   // dV|dK accumulator sets (2 x HD columns each)
   static constexpr int kNUq = HD == 64 ? 2 : 1;    // unit operand buffers (dQ kernel)
   static constexpr int kStq = HD == 64 ? 4 : 3;    // inner-tile stages (dQ kernel)
