@@ -223,3 +223,24 @@ def test_cost_c_entry_points_exported():
     lib = ctypes.CDLL(so)
     for n in set(names):
         assert hasattr(lib, n), n
+
+
+@pytest.mark.gpu
+def test_measure_stage_seconds_and_b200_params(K):
+    """The B200 re-parameterisation path end to end on a small LLaMA: measured per-stage
+    forward / backward seconds feed CostParams::from_b200 and an iteration cost whose compute
+    term reproduces the measured iteration (stages x microbatches x (fwd + bwd))."""
+    import paper_2506_15461_b200 as P
+    from paper_2506_15461_b200 import api
+
+    spec = api.ModelSpec.llama(512, 128, 4, 2, 256, 64, 4, max_tokens=4 * 64)
+    eng = P.Engine(spec)
+    eng.init(1, 1e-3)
+    f, b, detail = K.measure_stage_seconds(eng, spec, 4 * 64, 4, reps=3, warmup=2)
+    assert 0 < f <= b and detail["iteration_s"] > 0
+    par = K.params_b200(f, b, 4 * 64, 128, eng.stage_params, max(eng.embed_params, eng.deembed_params),
+                        4 * eng.stage_params + eng.embed_params + eng.deembed_params, 4)
+    eng.close()
+    it = K.iteration_cost("checkfree", K.Profile.b200(4), par)
+    assert it["compute"] == pytest.approx(4 * 4 * (f + b), rel=1e-12)
+    assert it["compute"] == pytest.approx(detail["iteration_s"], rel=1e-6) or b == f
