@@ -280,6 +280,32 @@ def compare_strategies(cfg: dict, strategies, trace_text: str, profile, params: 
     return out if isinstance(profile, dict) else out[""]
 
 
+def milestones(evals_off, evals_on, fracs=(0.25, 0.5, 0.75, 0.9)):
+    """ablation_swap's milestones (experiment.cpp:370-385): validation-loss levels at fractions
+    of the swap-off run's total drop, and the first evaluated iteration at or below each level
+    in either run (-1: never).  evals = [(iteration, train, val, ...), ...]."""
+    v0, vf = evals_off[0][2], evals_off[-1][2]
+    rows = []
+    for frac in fracs:
+        level = v0 - frac * (v0 - vf)
+        first = lambda ev: next((e[0] for e in ev if e[2] <= level), -1)  # noqa: E731
+        rows.append({"level": level, "iter_off": first(evals_off), "iter_on": first(evals_on)})
+    return rows
+
+
+def ablation_swap(cfg: dict, seed: int) -> dict:
+    """ablation_swap (experiment.cpp:349-386) on the GPU trainer: paired zero-failure runs with
+    the standard and the swapped-half schedule, same seed, and the milestone table."""
+    s = int(cfg.get("stages", 4))
+    base = {k: v for k, v in cfg.items() if k not in ("p-hour", "p-iter", "trace", "target-loss")}
+    base["strategy"] = "no-failures"
+    from . import api
+    empty = api.generate_trace(seed, 0.0, float(cfg.get("iter-seconds", 120.0)), 1, list(range(1, s + 1)))
+    off = run_record({**base, "schedule": "standard"}, empty, seed)
+    on = run_record({**base, "schedule": "swapped-half"}, empty, seed)
+    return {"off": off, "on": on, "milestones": milestones(off["evals"], on["evals"])}
+
+
 def comparison_csv(rows) -> str:
     """experiment.cpp:277-285's schema + measured_hours."""
     out = ["# format_version=1",

@@ -244,3 +244,26 @@ def test_measure_stage_seconds_and_b200_params(K):
     it = K.iteration_cost("checkfree", K.Profile.b200(4), par)
     assert it["compute"] == pytest.approx(4 * 4 * (f + b), rel=1e-12)
     assert it["compute"] == pytest.approx(detail["iteration_s"], rel=1e-6) or b == f
+
+
+@pytest.mark.gpu
+def test_ablation_swap_milestones_match_oracle(K):
+    """ablation_swap (experiment.cpp:349-386): the GPU trainer's swap-off / swap-on runs give
+    the same milestone iterations as the fp64 oracle restatement of the reference trainer."""
+    import sys
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import ckfree_oracle as O
+    cfg = {"input-dim": 16, "hidden-dim": 64, "model-dim": 32, "output-dim": 16, "layers": 8, "stages": 4,
+           "batch": 256, "microbatches": 8, "lr": 0.0003, "eval-interval": 5, "val-size": 256, "iters": 60}
+    ab = K.ablation_swap(cfg, 1)
+    empty = "checkfree-trace v1 seed=1 p_hour=0 iter_s=120 stages=1,2,3,4\n"
+    ref = {}
+    for mode in ("standard", "swapped-half"):
+        evals, _, _ = O.run_experiment({**cfg, "strategy": "no-failures", "schedule": mode}, empty, 1)
+        ref[mode] = evals
+    want = K.milestones(ref["standard"], ref["swapped-half"])
+    got = ab["milestones"]
+    assert [(r["iter_off"], r["iter_on"]) for r in got] == [(r["iter_off"], r["iter_on"]) for r in want]
+    for g, w in zip(got, want):
+        assert g["level"] == pytest.approx(w["level"], rel=1e-9)
+    assert any(r["iter_off"] > 0 for r in got)
