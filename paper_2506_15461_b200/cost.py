@@ -306,6 +306,57 @@ def ablation_swap(cfg: dict, seed: int) -> dict:
     return {"off": off, "on": on, "milestones": milestones(off["evals"], on["evals"])}
 
 
+def estimate_delta(engine, x) -> dict:
+    """estimate_delta (experiment.cpp:305-345) on the GPU engine, residual-MLP model: for each
+    layer, param_ratio = ||W1, W2 of the layer|| / ||all weights (embed, de-embed, stages)|| and
+    func_ratio = ||F(x) - F_without_layer(x)|| / ||F(x)|| over the probe rows x (the reference
+    draws them from its task's validation set; here the caller passes them).  A layer is
+    omitted by zeroing its W2 on the device -- h + act(h W1) 0 = h exactly -- and restored."""
+    import numpy as np
+
+    from . import api
+
+    spec = engine.spec
+    if spec.block != "mlp":
+        raise NotImplementedError("estimate_delta is defined for the reference's residual-MLP blocks")
+    s, d, hd = spec.num_stages, spec.model_dim, spec.hidden_dim
+    order = list(range(1, s + 1))
+    emb, deemb = engine.export_edge(0)[0], engine.export_edge(1)[0]
+    stages = [np.array(engine.export_stage(i)[0], np.float64) for i in range(1, s + 1)]
+    allw = np.concatenate([np.ravel(emb), np.ravel(deemb)] + stages)
+    norm_all = float(np.sqrt(np.dot(allw, allw)))
+    full = engine.predict(order, x)
+    norm_out = float(np.sqrt(np.sum(full * full)))
+    part = api.even_partition(spec.num_layers, s)
+    rows, dp, df = [], 0.0, 0.0
+    for layer in range(1, spec.num_layers + 1):
+        sid = next(i + 1 for i, (a, b) in enumerate(part) if a <= layer <= b)
+        off = (layer - part[sid - 1][0]) * 2 * d * hd
+        w = stages[sid - 1]
+        blk = w[off:off + 2 * d * hd]
+        wnorm = float(np.sqrt(np.dot(blk, blk)))
+        masked = w.copy()
+        masked[off + d * hd:off + 2 * d * hd] = 0.0
+        engine.import_stage(sid, w=masked)
+        try:
+            pred = engine.predict(order, x)
+        finally:
+            engine.import_stage(sid, w=w)
+        diff = float(np.sqrt(np.sum((full - pred) ** 2)))
+        row = {"layer": layer, "param_ratio": wnorm / norm_all if norm_all > 0 else 0.0,
+               "func_ratio": diff / norm_out if norm_out > 0 else 0.0}
+        rows.append(row)
+        dp, df = max(dp, row["param_ratio"]), max(df, row["func_ratio"])
+    return {"rows": rows, "delta_param": dp, "delta_func": df}
+
+
+def delta_csv(report: dict) -> str:
+    """experiment.cpp:347-354's schema."""
+    out = ["# format_version=1", "layer,param_ratio,func_ratio"]
+    out += [f"{r['layer']},{r['param_ratio']:.17g},{r['func_ratio']:.17g}" for r in report["rows"]]
+    return "\n".join(out) + "\n"
+
+
 def comparison_csv(rows) -> str:
     """experiment.cpp:277-285's schema + measured_hours."""
     out = ["# format_version=1",

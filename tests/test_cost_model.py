@@ -267,3 +267,51 @@ def test_ablation_swap_milestones_match_oracle(K):
     for g, w in zip(got, want):
         assert g["level"] == pytest.approx(w["level"], rel=1e-9)
     assert any(r["iter_off"] > 0 for r in got)
+
+
+@pytest.mark.gpu
+def test_estimate_delta_matches_numpy_restatement(K):
+    """estimate_delta (experiment.cpp:305-345): per-layer parameter / function ratios of the
+    GPU engine's residual-MLP model against a numpy restatement that skips the layer; the
+    engine's weights are left as they were."""
+    import numpy as np
+
+    import paper_2506_15461_b200 as P
+    from paper_2506_15461_b200 import api
+
+    spec = api.ModelSpec(16, 64, 32, 16, 8, 4, precision="fp64", max_rows=64)
+    eng = P.Engine(spec)
+    eng.init(7, 1e-3)
+    x = np.random.default_rng(3).uniform(-1.0, 1.0, (64, 16))
+    before = eng.predict([1, 2, 3, 4], x)
+    rep = K.estimate_delta(eng, x)
+    assert np.array_equal(eng.predict([1, 2, 3, 4], x), before)
+
+    E = eng.export_edge(0)[0].reshape(16, 32)
+    D = eng.export_edge(1)[0].reshape(32, 16)
+    W = [eng.export_stage(s)[0] for s in range(1, 5)]
+    blocks = []
+    for w in W:
+        for b in range(2):
+            o = b * 2 * 32 * 64
+            blocks.append((w[o:o + 32 * 64].reshape(32, 64), w[o + 32 * 64:o + 2 * 32 * 64].reshape(64, 32)))
+
+    def fwd(skip=None):
+        h = x @ E
+        for i, (w1, w2) in enumerate(blocks):
+            if i != skip:
+                h = h + np.tanh(h @ w1) @ w2
+        return h @ D
+
+    full = fwd()
+    allw = np.concatenate([E.ravel(), D.ravel()] + W)
+    for i, row in enumerate(rep["rows"]):
+        w1, w2 = blocks[i]
+        pr = np.sqrt((w1 ** 2).sum() + (w2 ** 2).sum()) / np.linalg.norm(allw)
+        fr = np.linalg.norm(full - fwd(i)) / np.linalg.norm(full)
+        assert row["layer"] == i + 1
+        assert row["param_ratio"] == pytest.approx(pr, rel=1e-9)
+        assert row["func_ratio"] == pytest.approx(fr, rel=1e-6)
+    assert rep["delta_func"] == max(r["func_ratio"] for r in rep["rows"]) > 0
+    assert K.delta_csv(rep).splitlines()[1] == "layer,param_ratio,func_ratio"
+    eng.close()
