@@ -58,7 +58,9 @@ WORKLOADS = {
     "mlp-124m": dict(block="mlp", precision="fp32", input_dim=16, hidden_dim=2048, model_dim=512, output_dim=16,
                      layers=12, stages=4, microbatches=8, rows=65536, seq_len=1, heads=1),
 }
-DEFAULT_WORKLOAD = "llama-124m"
+# north_star target on one GPU: BASELINE.json configs[2], LLaMA-500M, 8 stages, CheckFree+
+DEFAULT_WORKLOAD = "llama-500m"
+DEFAULT_STRATEGY = "checkfree-plus"
 
 
 def flops_per_token(w: dict) -> float:
@@ -204,8 +206,12 @@ def run_reference_arm(args, w: dict):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    rows = max(w["microbatches"], 64 if w["block"] == "mlp" else 32)
-    cb = cpu_reference(w, max(1, args.steps), rows)
+    rows = ref_rows(w)
+    # each timed step is one reference iteration at `rows` rows; the number of timed iterations is
+    # capped so the whole arm ends within a few minutes at the large workloads (stated in `sample`)
+    probe = cpu_reference(w, 1, rows)
+    iters = max(1, min(args.steps, int(120.0 / max(probe["s_per_iter"], 1e-3))))
+    cb = cpu_reference(w, iters, rows)
     line = {"metric": METRIC, "value": cb["value"], "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": cb["s_per_iter"] * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -233,7 +239,9 @@ def workload_config(args, w: dict) -> dict:
     cfg = {"parallelism": f"pp{P}" + (f"xdp{R}" if R > 1 else ""),"workload": args.workload, "block": w["block"], "stages": w["stages"],
            "microbatches": w["microbatches"], "layers": w["layers"], "model_dim": w["model_dim"],
            "hidden_dim": w["hidden_dim"], "tokens_per_step": tokens_per_step(w) * R, "seq_len": w["seq_len"],
-           "strategy": getattr(args, "strategy", "checkfree"), "placement": f"{w['stages']} stages on {P} pipeline rank(s) x {R} replica(s)",
+           "strategy": getattr(args, "strategy", DEFAULT_STRATEGY),
+           "schedule": "swapped_half (swapped first/last-stage order at even microbatches) + per-step edge replica "
+                       "refresh" if getattr(args, "strategy", DEFAULT_STRATEGY) == "checkfree-plus" else "standard", "placement": f"{w['stages']} stages on {P} pipeline rank(s) x {R} replica(s)",
            "l2": "256 MiB memset between timed steps (outside the events)"}
     if w["block"] == "llama":
         cfg.update(vocab=w["output_dim"], heads=w["heads"])
@@ -289,12 +297,15 @@ def run_ours(args, w: dict):
     eng.init(1, 3e-4)
     if args.strategy == "redundant":
         eng.set_redundant(True)
+    cfp = args.strategy == "checkfree-plus"
+    if cfp:
+        eng.set_edge_replicas(True)  # trainer.cpp:83-84: E / E^-1 replicas refreshed inside every step
     if world > 1:
         uid = [P_.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         eng.attach_comm(uid[0], world, rank, [(sid - 1) * P // s for sid in range(1, s + 1)], R)
 
-    orders = np.array(api.build_schedule(w["microbatches"], False, s), np.int32)
+    orders = np.array(api.build_schedule(w["microbatches"], cfp, s), np.int32)  # pipeline.cpp:41-56
     gen = torch.Generator().manual_seed(1234 + rank // P)  # one batch per replica (weak scaling)
     xh, yh = make_batch(w, gen, local)
     xh, yh = xh.pin_memory(), (yh.pin_memory() if yh is not None else None)
@@ -383,15 +394,27 @@ def run_ours(args, w: dict):
     # stage-recovery latency (trainer.cpp:230-276 semantics, weights + moments + lr + omega), stage 2
     rec = None
     if world == 1 and s >= 3:
+        # kill-to-ready latency of an interior stage (CheckFree omega-average, trainer.cpp:230-276):
+        # one fused pass -- weights, Fresh moments, zeroed gradient, bf16 shadow -- CUDA events on the
+        # engine stream; algorithmic bytes 26 per fp32 parameter (read Wp, Wn; write W, m, v, g; bf16 W)
         lat = []
-        for _ in range(3):
+        for _ in range(5):
             eng.kill_stage(2)
-            r = eng.recover_stage(2, reduction_error=False)
-            lat.append(r.latency_ms)
-        pb = 4 if w["precision"] != "fp64" else 8
+            lat.append(eng.recover_stage(2, reduction_error=False).latency_ms)
         n_stage = eng.stage_params
-        rec = {"stage": 2, "stage_params": n_stage, "latency_ms": min(lat),
-               "avg_bytes": 3 * pb * n_stage, "avg_gbs_incl_moment_reset": None}
+        pb = 4 if w["precision"] != "fp64" else 8
+        nbytes = n_stage * (6 * pb + (2 if w["precision"] == "bf16" else 0))
+        med = statistics.median(lat)
+        rec = {"stage": 2, "stage_params": n_stage, "latency_ms": med, "latency_ms_min": min(lat),
+               "bytes": nbytes, "gbs": nbytes / (med / 1e3) / 1e9,
+               "what": "kill -> ready: omega-weighted weights, Fresh m/v, g = 0, bf16 shadow in one kernel"}
+        if cfp:
+            # CheckFree+ first-stage recovery: stage 1 := stage 2, E := its replica (recovery.cpp:90-101)
+            el = []
+            for _ in range(3):
+                eng.kill_stage(1)
+                el.append(eng.recover_stage(1, mode=P_._native.CKF_REC_EDGE, reduction_error=False).latency_ms)
+            rec["edge_stage1_latency_ms"] = statistics.median(el)
 
     if rank != 0:
         if world > 1:
@@ -399,7 +422,8 @@ def run_ours(args, w: dict):
         return
 
     peaks, peak_src = load_peaks()
-    sweep = recovery_sweep(P_, local, peaks["hbm_gbs"]) if (world == 1 and not args.no_recovery_sweep) else None
+    sweep = recovery_sweep(P_, local, peaks["hbm_gbs"], cpu=not args.no_cpu_baseline) \
+        if (world == 1 and not args.no_recovery_sweep) else None
     tok = tokens_per_step(w) * R  # every replica trains on its own batch
     value = tok / (ms / 1e3)
     e2e_value = tok / (e2e_ms / 1e3)
@@ -419,8 +443,12 @@ def run_ours(args, w: dict):
     # measured DRAM traffic per launch of the dominant class: ncu capture committed under
     # profiles/ (tools/ncu_traffic.py; same workload, one step's launches)
     traffic, traffic_src = None, None
-    tp = os.path.join(ROOT, "profiles", f"r01_{dom}_dram_traffic.json")
-    if os.path.exists(tp) and args.workload == DEFAULT_WORKLOAD:
+    # per-workload capture (tools/ncu_traffic.py): r02_<workload>_<class>_dram_traffic.json; the
+    # round-1 capture covers llama-124m
+    tp = os.path.join(ROOT, "profiles", f"r02_{args.workload}_{dom}_dram_traffic.json")
+    if not os.path.exists(tp) and args.workload == "llama-124m":
+        tp = os.path.join(ROOT, "profiles", f"r01_{dom}_dram_traffic.json")
+    if os.path.exists(tp):
         with open(tp) as f:
             tj = json.load(f)
         traffic = tj.get("traffic_per_launch_bytes")
@@ -433,16 +461,16 @@ def run_ours(args, w: dict):
                 classes={c: {"ms": v[0], "launches": v[1]} for c, v in kstats.items() if v[1]})
     step_tflops = flops_per_token(w) * tok / (ms / 1e3) / 1e12
 
-    if rec is not None and rec["latency_ms"] > 0:
-        rec["avg_gbs_incl_moment_reset"] = (rec["avg_bytes"] + 3 * (4 if w["precision"] != "fp64" else 8)
-                                            * rec["stage_params"]) / (rec["latency_ms"] / 1e3) / 1e9
+    if rec is not None:
+        rec["frac_hbm"] = rec["gbs"] / peaks["hbm_gbs"]
 
     h2d = xh.numel() * xh.element_size() + (yh.numel() * yh.element_size() if yh is not None else 0)
     d2h = 8 * (1 + s) + 8 * w["microbatches"]
-    cpu = None
+    cpu, cpu_llama = None, None
     if not args.no_cpu_baseline:
-        cpu = cpu_reference(w, 1, max(w["microbatches"], 64 if w["block"] == "mlp" else 32))
-        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        cpu = cpu_reference(w, 1, ref_rows(w))
+        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample", "s_per_iter")}
+        cpu_llama = cpu_llama_oracle()
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": {"fp32": "f32", "fp64": "f64", "bf16": "bf16"}[w["precision"]],
@@ -453,41 +481,89 @@ def run_ours(args, w: dict):
             "gpu_launches": launches, "roofline": roof, "step_tflops": step_tflops,
             "step_ms": {"timed": per_step[0], "e2e": per_step[-1]},
             "timing": "engine CUDA events per step (first device op .. result D2H), L2 flushed before each step",
-            "flops_per_token": flops_per_token(w), "cpu_baseline": cpu, "clocks": clk.summary(),
+            "flops_per_token": flops_per_token(w), "cpu_baseline": cpu, "cpu_baseline_llama_oracle": cpu_llama,
+            "clocks": clk.summary(),
             "recovery": rec, "recovery_sweep": sweep}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
-def recovery_sweep(P, local, hbm_peak):
-    """BASELINE.json configs[4]: omega-weighted neighbour-average reinit over stage sizes
-    10M-400M params (fp32 masters, recovery.cpp:57-73), HBM GB/s of the streaming kernel
-    (12 B/param algorithmic: read W_prev, W_next; write W_stage).  L2 flushed before each rep."""
+def recovery_sweep(P, local, hbm_peak, cpu=True):
+    """BASELINE.json configs[4]: omega-weighted neighbour-average reinit over stage sizes 10M-400M
+    params (fp32 masters, recovery.cpp:57-73, omega = (4, 1)).  Two passes per size, L2 flushed
+    before each rep, CUDA events: the engine's FUSED recovery (26 B/param: read W_prev, W_next;
+    write W, m, v, g; bf16 shadow) and the weights-only average (12 B/param).  Beside each point
+    the reference's own recover_checkfree (oracle/_ref, serial as shipped, fp64) on the host."""
     import torch
     dev = f"cuda:{local}"
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     out = []
-    for n in (10_000_000, 25_000_000, 50_000_000, 100_000_000, 200_000_000, 400_000_000):
-        wp = torch.rand(n, device=dev)
-        wn = torch.rand(n, device=dev)
-        ws = torch.empty(n, device=dev)
-        P.recover_device(wp, wn, ws, 4.0, 1.0)
+
+    def timeit(fn):
+        fn()
         times = []
         for _ in range(5):
             flush.zero_()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
-            P.recover_device(wp, wn, ws, 4.0, 1.0)
+            fn()
             b.record()
             torch.cuda.synchronize()
             times.append(a.elapsed_time(b))
-        ms = sorted(times)[len(times) // 2]
-        gbs = 12.0 * n / (ms / 1e3) / 1e9
-        out.append({"params": n, "ms": ms, "gbs": gbs, "frac_hbm": gbs / hbm_peak})
-        del wp, wn, ws
+        return sorted(times)[len(times) // 2]
+
+    refshim = None
+    if cpu:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import refshim  # noqa: F811  (baseline infrastructure only)
+    for n in (10_000_000, 25_000_000, 50_000_000, 100_000_000, 200_000_000, 400_000_000):
+        wp = torch.rand(n, device=dev)
+        wn = torch.rand(n, device=dev)
+        ws = torch.empty(n, device=dev)
+        m, v, g = torch.empty(n, device=dev), torch.empty(n, device=dev), torch.empty(n, device=dev)
+        wlp = torch.empty(n, device=dev, dtype=torch.bfloat16)
+        ms_f = timeit(lambda: P.api.recover_stage_device(wp, wn, ws, m, v, g, 4.0, 1.0, w_bf16=wlp))
+        ms_w = timeit(lambda: P.recover_device(wp, wn, ws, 4.0, 1.0))
+        pt = {"params": n, "ms": ms_f, "gbs": 26.0 * n / (ms_f / 1e3) / 1e9,
+              "frac_hbm": 26.0 * n / (ms_f / 1e3) / 1e9 / hbm_peak, "bytes_per_param": 26,
+              "weights_only": {"ms": ms_w, "gbs": 12.0 * n / (ms_w / 1e3) / 1e9,
+                               "frac_hbm": 12.0 * n / (ms_w / 1e3) / 1e9 / hbm_peak}}
+        if refshim is not None and refshim.available():
+            s_ref = refshim.time_recover_checkfree(n, 1)
+            pt["cpu_reference"] = {"ms": s_ref * 1e3, "gbs": 24.0 * n / s_ref / 1e9, "cores": 1,
+                                   "kind": "reference", "what": "recovery::recover_checkfree, fp64, serial as shipped"}
+        out.append(pt)
+        del wp, wn, ws, m, v, g, wlp
     torch.cuda.empty_cache()
     return out
+
+
+def ref_rows(w: dict) -> int:
+    """Rows per iteration of the reference arm's bounded sample: >= one row per microbatch and at
+    least 32, so per-iteration fixed costs (Adam over the fp64 stage vectors) do not dominate."""
+    return max(w["microbatches"], 64 if w["block"] == "mlp" else 32)
+
+
+def cpu_llama_oracle() -> dict:
+    """The LLaMA CPU oracle (oracle/llama_oracle.py, torch fp64 on the host cores) timed on
+    BASELINE.json configs[0]: tiny LLaMA (d=256, L=8, H=4, f=768, V=4096, T=128), 4 stages,
+    8 microbatches x 4 sequences = 4096 tokens per iteration, one iteration after a warm-up."""
+    import torch
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import llama_oracle as LO  # noqa: E402  (baseline infrastructure only)
+    torch.set_num_threads(os.cpu_count() or 1)
+    spec = LO.LSpec(vocab=4096, d=256, layers=8, heads=4, ffn=768, seq_len=128, stages=4)
+    model = LO.LModel(spec, 3, 3e-4)
+    sched = LO.build_schedule(8, False, 4)
+    toks = LO.token_batch(1, 1, 1, 32, 128, 4096)
+    LO.run_iteration(model, sched, toks)
+    t0 = time.perf_counter()
+    LO.run_iteration(model, sched, toks)
+    dt = time.perf_counter() - t0
+    return {"value": 32 * 128 / dt, "unit": "tokens/s", "cores": torch.get_num_threads(), "kind": "port",
+            "s_per_iter": dt, "sample": "LLaMA CPU oracle (torch fp64) on configs[0]: tiny LLaMA, 4 stages, "
+                                        "8 microbatches x 4 seq x T=128, 1 timed iteration after 1 warm-up"}
 
 
 def main():
@@ -499,8 +575,9 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default=DEFAULT_WORKLOAD)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-recovery-sweep", action="store_true")
-    ap.add_argument("--strategy", choices=["checkfree", "redundant"], default="checkfree",
-                    help="redundant: the redundant-computation baseline measured (extra forward per stage, "
+    ap.add_argument("--strategy", choices=["checkfree", "checkfree-plus", "redundant"], default=DEFAULT_STRATEGY,
+                    help="checkfree-plus: swapped_half orders + per-step edge replica refresh (default); "
+                         "redundant: the redundant-computation baseline measured (extra forward per stage, "
                          "post-step replica refresh)")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -116,6 +116,17 @@ int ckf_k_counter_uniform(uint64_t key, double lo, double hi, double* out, size_
  * (device double*, deterministic order).  op+on == 0 -> uniform (degenerate). */
 int ckf_recover_device(int dtype, const void* wp, const void* wn, void* out, size_t n, double op, double on,
                        double* old_out_sq, void* stream);
+/* The engine's fused stage recovery on raw device pointers -- ONE streaming pass
+ * (recovery.cpp:57-73 + trainer.cpp:230-276): w = (op*wp + on*wn)/(op+on) (degenerate
+ * 0,0 -> uniform), moments Fresh (averaged = 0: m = v = 0) or omega-weighted from mp/mn,
+ * vp/vn (averaged = 1, trainer.cpp:263-269), g = 0, bf16 shadow w_bf16 (may be NULL),
+ * optional ||w_old - w_new||^2 into *old_sq (device double).  wp / wn / mp / mn / vp / vn
+ * may be PEER pointers (another GPU's HBM mapped with CUDA IPC or peer access), which is
+ * how a replacement GPU pulls its neighbours over NVLink inside the kernel. */
+int ckf_recover_stage_device(int dtype, const void* wp, const void* wn, const void* mp, const void* mn,
+                             const void* vp, const void* vn, void* w, void* m, void* v, void* g, void* w_bf16,
+                             size_t n, double omega_prev, double omega_next, int averaged, double* old_sq,
+                             void* stream);
 /* fused Adam (kernels_serial.cpp:133-144) + omega = sum(g^2) (model.cpp:396):
  * g_eff = g_sum * grad_scale; w,m,v updated in place; if w_bf16 != NULL the bf16
  * shadow is rewritten; if zero_grad the accumulator is cleared for the next
@@ -199,6 +210,16 @@ int ckf_engine_init(ckf_engine_t e, uint64_t seed, double lr);
  * uid is a ckf_nccl_unique_id blob shared by all ranks (e.g. via torch.distributed). */
 int ckf_nccl_unique_id(void* uid_out, size_t cap);
 int ckf_engine_attach_comm(ckf_engine_t e, const void* uid, int nranks, int rank, const int* stage_rank);
+/* Placement only (no NCCL communicator): which rank owns which stage; the buffers of stages
+ * this rank does not own are released.  attach_comm = placement + NCCL.  Used on its own when
+ * only the peer-recovery path is exercised (ranks sharing one GPU through CUDA IPC). */
+int ckf_engine_set_placement(ckf_engine_t e, int nranks, int rank, const int* stage_rank, int replicas);
+/* Peer recovery over NVLink: CUDA IPC handles of this rank's stage buffers (w, m, v of every
+ * owned stage) as an opaque blob; every rank imports the other ranks' blobs and maps the
+ * stages it does not own, so recover_stage reads a failed stage's neighbours directly from
+ * the peers' HBM inside the recovery kernel (no staging copy).  *len = bytes written. */
+int ckf_engine_ipc_export(ckf_engine_t e, void* buf, size_t cap, size_t* len);
+int ckf_engine_ipc_import(ckf_engine_t e, const void* buf, size_t len);
 /* pipeline x data parallel (config 4: 4 stages x DP2): nranks = replicas * P; rank r is
  * pipeline rank r % P of replica r / P; stage_rank[] names PIPELINE ranks (0..P-1).  Each
  * replica runs its own microbatches; owned gradients are summed over the replicas
@@ -282,6 +303,10 @@ int ckf_engine_last_step_ms(ckf_engine_t e, float* ms);
  * downstream node's hot copy) and, after the optimizer step, a copy of every stage's master
  * weights to its replica.  LLaMA bf16 block. */
 int ckf_engine_set_redundant(ckf_engine_t e, int on);
+/* CheckFree+ per-step edge replica refresh inside the step (trainer.cpp:83-84): when on,
+ * ckf_engine_run_iteration ends with the replica copy of E / E^-1 (to the GPUs of stages 2 and
+ * s-1), inside the step's device bracket (ckf_engine_last_step_ms). */
+int ckf_engine_set_edge_replicas(ckf_engine_t e, int on);
 /* Hop log for a VIRTUAL placement (stage -> rank), used to check on one GPU that
  * the engine's stage transfers match ckf_pipeline_plan: when enabled, every
  * cross-rank transfer the placement implies is recorded as (src, dst, bytes). */

@@ -99,9 +99,12 @@ def lib():
         "ckf_engine_init": (i, [eng, u64, dbl]),
         "ckf_engine_set_schedule": (i, [eng, i]), "ckf_engine_set_group_cap": (i, [eng, i]),
         "ckf_engine_last_step_ms": (i, [eng, C.POINTER(C.c_float)]),
-        "ckf_engine_set_redundant": (i, [eng, i]),
+        "ckf_engine_set_redundant": (i, [eng, i]), "ckf_engine_set_edge_replicas": (i, [eng, i]),
         "ckf_nccl_unique_id": (i, [vp, sz]), "ckf_engine_attach_comm": (i, [eng, vp, i, i, ip]),
         "ckf_engine_attach_comm_dp": (i, [eng, vp, i, i, ip, i]),
+        "ckf_engine_set_placement": (i, [eng, i, i, ip, i]),
+        "ckf_engine_ipc_export": (i, [eng, vp, sz, C.POINTER(sz)]), "ckf_engine_ipc_import": (i, [eng, vp, sz]),
+        "ckf_recover_stage_device": (i, [i, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, dbl, dbl, i, vp, vp]),
         "ckf_engine_run_iteration": (i, [eng, ip, i, vp, vp, sz, i, lng, dp, dp]),
         "ckf_engine_eval_loss": (i, [eng, ip, vp, vp, sz, i, dp]),
         "ckf_engine_predict": (i, [eng, ip, dp, sz, dp]),

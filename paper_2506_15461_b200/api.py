@@ -135,6 +135,20 @@ def recover_device(wp, wn, out, omega_prev, omega_next, old_sq=None, stream=0):
                                    omega_next, old_sq.data_ptr() if old_sq is not None else None, stream or None))
 
 
+def recover_stage_device(wp, wn, w, m, v, g, omega_prev, omega_next, w_bf16=None, mp=None, mn=None, vp=None,
+                         vn=None, old_sq=None, stream=0):
+    """The engine's fused stage recovery (ckf_recover_stage_device) on torch CUDA tensors:
+    weights, moments (Fresh, or omega-weighted when mp/mn/vp/vn are given), g = 0, bf16 shadow and
+    the optional reduction error in ONE pass.  The neighbour tensors may live in a peer's HBM."""
+    import torch
+    dt = {torch.float64: N.CKF_FP64, torch.float32: N.CKF_FP32}[w.dtype]
+    avg = mp is not None
+    ptr = (lambda t: t.data_ptr() if t is not None else None)
+    check(lib().ckf_recover_stage_device(dt, ptr(wp), ptr(wn), ptr(mp), ptr(mn), ptr(vp), ptr(vn), ptr(w), ptr(m),
+                                         ptr(v), ptr(g), ptr(w_bf16), w.numel(), omega_prev, omega_next,
+                                         1 if avg else 0, ptr(old_sq), stream or None))
+
+
 def adam_device(w, m, v, g, lr, step, grad_scale=1.0, zero_grad=False, w_bf16=None, omega=None, stream=0):
     import math
     import torch
@@ -305,6 +319,24 @@ class Engine:
         buf = C.create_string_buffer(uid, 128)
         check(lib().ckf_engine_attach_comm_dp(self._h, buf, nranks, rank, _ip(sr), replicas))
 
+    def set_placement(self, nranks: int, rank: int, stage_rank, replicas: int = 1):
+        """Stage -> rank ownership without a communicator (attach_comm = this + NCCL)."""
+        sr = np.ascontiguousarray(stage_rank, np.int32)
+        check(lib().ckf_engine_set_placement(self._h, nranks, rank, _ip(sr), replicas))
+
+    def ipc_export(self) -> bytes:
+        """CUDA IPC handles of this rank's stage buffers (peer recovery over NVLink)."""
+        buf = C.create_string_buffer(1 << 16)
+        n = C.c_size_t(0)
+        check(lib().ckf_engine_ipc_export(self._h, buf, len(buf), C.byref(n)))
+        return buf.raw[:n.value]
+
+    def ipc_import(self, blobs):
+        """Maps the other ranks' stages (blobs from every rank's ipc_export; own entries skipped)."""
+        data = b"".join(blobs)
+        buf = C.create_string_buffer(data, max(1, len(data)))
+        check(lib().ckf_engine_ipc_import(self._h, buf, len(data)))
+
     def sync(self):
         check(lib().ckf_engine_sync(self._h))
 
@@ -317,6 +349,10 @@ class Engine:
         ms = C.c_float()
         check(lib().ckf_engine_last_step_ms(self._h, C.byref(ms)))
         return ms.value
+
+    def set_edge_replicas(self, on: bool):
+        """CheckFree+: refresh the edge replicas at the end of every run_iteration (trainer.cpp:83-84)."""
+        check(lib().ckf_engine_set_edge_replicas(self._h, 1 if on else 0))
 
     def set_group_cap(self, cap: int):
         """Microbatch fusion cap (0 = fit to HBM, 1 = one microbatch per pass)."""

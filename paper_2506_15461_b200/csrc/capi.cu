@@ -1,3 +1,4 @@
+#include <type_traits>
 // extern "C" entry points of include/ckf.h.  Nothing throws across this line:
 // every call maps internal errors to CKF_E_* codes + ckf_last_error().
 #include <algorithm>
@@ -372,6 +373,49 @@ int ckf_recover_device(int dtype, const void* wp, const void* wn, void* out, siz
   });
 }
 
+int ckf_recover_stage_device(int dtype, const void* wp, const void* wn, const void* mp, const void* mn,
+                             const void* vp, const void* vn, void* w, void* m, void* v, void* g, void* w_bf16,
+                             size_t n, double omega_prev, double omega_next, int averaged, double* old_sq,
+                             void* stream) {
+  return guard([&] {
+    if (omega_prev < 0.0 || omega_next < 0.0) ckf::raise(CKF_E_CONFIG, "gradient norms must be nonnegative");
+    if (averaged && (!mp || !mn || !vp || !vn)) ckf::raise(CKF_E_CONFIG, "averaged moments need mp, mn, vp, vn");
+    static thread_local ckf::ReduceScratch red;
+    if (!red.partials) CKF_CUDA(cudaMalloc(&red.partials, ckf::ReduceScratch::kMaxReduceBlocks * sizeof(double)));
+    auto run = [&](auto* tag) {
+      using T = std::remove_pointer_t<decltype(tag)>;
+      ckf::k::StageRecovery<T> r;
+      r.wp = static_cast<const T*>(wp);
+      r.wn = static_cast<const T*>(wn);
+      r.mp = static_cast<const T*>(mp);
+      r.mn = static_cast<const T*>(mn);
+      r.vp = static_cast<const T*>(vp);
+      r.vn = static_cast<const T*>(vn);
+      r.w = static_cast<T*>(w);
+      r.m = static_cast<T*>(m);
+      r.v = static_cast<T*>(v);
+      r.g = static_cast<T*>(g);
+      r.wlp = static_cast<__nv_bfloat16*>(w_bf16);
+      r.n = n;
+      r.op = omega_prev;
+      r.on = omega_next;
+      r.averaged = averaged != 0;
+      r.mop = omega_prev;
+      r.mon = omega_next;
+      r.old_sq = old_sq;
+      ckf::k::recover_stage(r, red, static_cast<cudaStream_t>(stream));
+    };
+    if (dtype == CKF_FP64) {
+      if (w_bf16) ckf::raise(CKF_E_CONFIG, "the fp64 parity precision keeps no bf16 shadow");
+      run(static_cast<double*>(nullptr));
+    } else if (dtype == CKF_FP32) {
+      run(static_cast<float*>(nullptr));
+    } else {
+      ckf::raise(CKF_E_CONFIG, "recover_stage: dtype must be CKF_FP64 or CKF_FP32 (master weights)");
+    }
+  });
+}
+
 int ckf_adam_device(int dtype, void* w, void* m, void* v, void* g, void* w_bf16, size_t n, double lr, double bc1,
                     double bc2, double grad_scale, int zero_grad, double* omega, void* stream) {
   return guard([&] {
@@ -515,6 +559,15 @@ int ckf_nccl_unique_id(void* uid_out, size_t cap) {
 int ckf_engine_attach_comm(ckf_engine_t e, const void* uid, int nranks, int rank, const int* stage_rank) {
   return guard([&] { E(e)->attach_comm(uid, nranks, rank, stage_rank, 1); });
 }
+int ckf_engine_set_placement(ckf_engine_t e, int nranks, int rank, const int* stage_rank, int replicas) {
+  return guard([&] { E(e)->set_placement(nranks, rank, stage_rank, replicas); });
+}
+int ckf_engine_ipc_export(ckf_engine_t e, void* buf, size_t cap, size_t* len) {
+  return guard([&] { *len = E(e)->ipc_export(buf, cap); });
+}
+int ckf_engine_ipc_import(ckf_engine_t e, const void* buf, size_t len) {
+  return guard([&] { E(e)->ipc_import(buf, len); });
+}
 int ckf_engine_attach_comm_dp(ckf_engine_t e, const void* uid, int nranks, int rank, const int* stage_rank,
                               int replicas) {
   return guard([&] { E(e)->attach_comm(uid, nranks, rank, stage_rank, replicas); });
@@ -619,6 +672,10 @@ int ckf_engine_set_redundant(ckf_engine_t e, int on) {
 
 int ckf_engine_last_step_ms(ckf_engine_t e, float* ms) {
   return guard([&] { *ms = E(e)->last_step_ms(); });
+}
+
+int ckf_engine_set_edge_replicas(ckf_engine_t e, int on) {
+  return guard([&] { E(e)->set_edge_replicas(on != 0); });
 }
 
 int ckf_engine_set_group_cap(ckf_engine_t e, int cap) {

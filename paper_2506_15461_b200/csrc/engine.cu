@@ -3,6 +3,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -171,6 +172,9 @@ Engine::~Engine() {
   if (comm_ && nccl().CommDestroy) nccl().CommDestroy(comm_);
   if (gexec_) cudaGraphExecDestroy(gexec_);
   for (void* p : rc_replica_) cudaFree(p);
+  for (auto& p : peer_)
+    for (void* q : {p.w, p.m, p.v})
+      if (q) cudaIpcCloseMemHandle(q);
   for (auto& c : ckpt_) cudaFree(c.buf);
   for (cudaEvent_t ev : kev_) cudaEventDestroy(ev);
   if (ev0_) cudaEventDestroy(ev0_);
@@ -275,7 +279,7 @@ void Engine::kt_collect() {
 }
 
 // ------------------------------------------------------------------ placement
-void Engine::attach_comm(const void* uid, int nranks, int rank, const int* stage_rank, int replicas) {
+void Engine::set_placement(int nranks, int rank, const int* stage_rank, int replicas) {
   if (nranks < 1 || rank < 0 || rank >= nranks) raise(1, "invalid rank / world size");
   if (replicas < 1 || nranks % replicas) raise(1, "world size must be a multiple of the replica count");
   const int P = nranks / replicas;  // pipeline ranks per replica
@@ -289,7 +293,21 @@ void Engine::attach_comm(const void* uid, int nranks, int rank, const int* stage
   rank_ = rank;
   nranks_ = nranks;
   if (nranks > 1) schedule_ = 1;
+  // release buffers of stages this rank does not own
+  for (size_t i = 0; i < d_.s; ++i) {
+    stages_[i].owned = stage_rank_[i] == rank_;
+    if (!stages_[i].owned) free_group(stages_[i]);
+  }
+  embed_.owned = owner_of_embed() == rank_;
+  deembed_.owned = owner_of_deembed() == rank_;
+  if (!embed_.owned) free_group(embed_);
+  if (!deembed_.owned) free_group(deembed_);
+}
+
+void Engine::attach_comm(const void* uid, int nranks, int rank, const int* stage_rank, int replicas) {
+  set_placement(nranks, rank, stage_rank, replicas);
   if (nranks > 1) {
+    const int P = nranks / replicas;
     NcclApi::Uid u;
     std::memcpy(u.b, uid, 128);
     CKF_CUDA(cudaSetDevice(d_.device));
@@ -300,15 +318,60 @@ void Engine::attach_comm(const void* uid, int nranks, int rank, const int* stage
       nccl_check(nccl().CommSplit(comm_, rank % P, replica_, &dp_comm_, nullptr), "ncclCommSplit");
     }
   }
-  // release buffers of stages this rank does not own
+}
+
+// ------------------------------------------------------------------ peer (IPC) mappings
+namespace {
+struct IpcEntry {
+  int32_t rank, replica, sid, kind;  // kind 0 = w, 1 = m, 2 = v
+  uint64_t bytes;
+  cudaIpcMemHandle_t h;
+};
+}  // namespace
+
+size_t Engine::ipc_export(void* buf, size_t cap) {
+  CKF_CUDA(cudaSetDevice(d_.device));
+  std::vector<IpcEntry> v;
   for (size_t i = 0; i < d_.s; ++i) {
-    stages_[i].owned = stage_rank_[i] == rank_;
-    if (!stages_[i].owned) free_group(stages_[i]);
+    ParamGroup& g = stages_[i];
+    if (!g.owned || g.n == 0) continue;
+    void* bufs[3] = {g.w, g.m, g.v};
+    for (int k = 0; k < 3; ++k) {
+      IpcEntry e{};
+      e.rank = rank_;
+      e.replica = replica_;
+      e.sid = static_cast<int32_t>(i + 1);
+      e.kind = k;
+      e.bytes = g.n * master_bytes();
+      CKF_CUDA(cudaIpcGetMemHandle(&e.h, bufs[k]));
+      v.push_back(e);
+    }
   }
-  embed_.owned = owner_of_embed() == rank_;
-  deembed_.owned = owner_of_deembed() == rank_;
-  if (!embed_.owned) free_group(embed_);
-  if (!deembed_.owned) free_group(deembed_);
+  const size_t need = v.size() * sizeof(IpcEntry);
+  if (need > cap) raise(1, "IPC export buffer too small (" + std::to_string(need) + " bytes needed)");
+  if (need) std::memcpy(buf, v.data(), need);
+  return need;
+}
+
+void Engine::ipc_import(const void* buf, size_t len) {
+  CKF_CUDA(cudaSetDevice(d_.device));
+  if (len % sizeof(IpcEntry)) raise(1, "malformed IPC blob");
+  if (peer_.size() != d_.s) peer_.assign(d_.s, PeerStage{});
+  const auto* e = static_cast<const IpcEntry*>(buf);
+  for (size_t i = 0; i < len / sizeof(IpcEntry); ++i) {
+    const IpcEntry& x = e[i];
+    if (x.rank == rank_ || x.replica != replica_) continue;  // own stages / other replicas' copies
+    if (x.sid < 1 || x.sid > static_cast<int>(d_.s) || x.kind < 0 || x.kind > 2) raise(1, "malformed IPC entry");
+    ParamGroup& g = stages_[static_cast<size_t>(x.sid - 1)];
+    if (g.owned) continue;
+    if (x.bytes != g.n * master_bytes()) raise(1, "IPC entry size differs from the stage's size");
+    void** slot = x.kind == 0 ? &peer_[x.sid - 1].w : x.kind == 1 ? &peer_[x.sid - 1].m : &peer_[x.sid - 1].v;
+    if (*slot) continue;
+    CKF_CUDA(cudaIpcOpenMemHandle(slot, x.h, cudaIpcMemLazyEnablePeerAccess));
+  }
+  peer_ready_ = true;
+  for (size_t i = 0; i < d_.s; ++i)
+    if (!stages_[i].owned && !(peer_[i].w && peer_[i].m && peer_[i].v)) peer_ready_ = false;
 }
 
 void Engine::hop(void* buf, size_t bytes, int src, int dst) {
@@ -639,6 +702,7 @@ void Engine::run_iteration(const int* orders, int m, const void* x, const void* 
       kt_end(KC_RECOVER, 0.0, 2.0 * g.n * master_bytes());
     }
   }
+  if (auto_replicas_) refresh_edge_replicas();  // CheckFree+ (trainer.cpp:83-84), inside the step
   std::vector<double> om(d_.s);
   CKF_CUDA(cudaMemcpyAsync(losses.data(), scal_, nloss * sizeof(double), cudaMemcpyDeviceToHost, st_));
   CKF_CUDA(cudaMemcpyAsync(om.data(), scal_ + 2048, d_.s * sizeof(double), cudaMemcpyDeviceToHost, st_));
@@ -963,6 +1027,9 @@ ckf_recovery_report Engine::recover_stage(int sid, int mode, int moments, double
   ParamGroup* nxp = mode != CKF_REC_EDGE && sid < s ? &stage(sid + 1) : nullptr;
   const bool avg = moments == CKF_MOM_AVERAGED && (mode == CKF_REC_CHECKFREE || mode == CKF_REC_EDGE);
 
+  // latency = kill-to-ready on the replacement GPU: the clock starts BEFORE any neighbour
+  // transfer, so a multi-GPU recovery's pull (or peer reads inside the kernel) is counted
+  if (local) CKF_CUDA(cudaEventRecord(ev0_, st_));
   // ---- bring the neighbour state this recovery reads onto F (peer pulls over NCCL;
   //      a no-op when everything is resident, e.g. on one GPU)
   std::vector<std::pair<void**, void*>> borrowed;  // (slot, temp) to undo
@@ -975,8 +1042,29 @@ ckf_recovery_report Engine::recover_stage(int sid, int mode, int moments, double
     }
     hop(local ? tmp : *slot, nbytes, src, F);
   };
+  // neighbours mapped from peer HBM (ipc_import): the recovery kernel reads them in place
+  auto peer_of = [&](ParamGroup* g) -> PeerStage* {
+    if (!g || g->owned || peer_.empty()) return nullptr;
+    PeerStage& p = peer_[static_cast<size_t>(g - stages_.data())];
+    return p.w ? &p : nullptr;
+  };
+  auto borrow_peer = [&](ParamGroup* g) {
+    PeerStage* p = peer_of(g);
+    if (!p || !local) return false;
+    for (auto [slot, src] : {std::make_pair(&g->w, p->w), std::make_pair(&g->m, p->m), std::make_pair(&g->v, p->v)}) {
+      borrowed.push_back({slot, *slot});
+      *slot = src;
+    }
+    return true;
+  };
+  // every rank imported every peer blob (ipc_import), so all ranks agree on peer_ready_ and
+  // the neighbours' owners skip the NCCL sends the replacement GPU no longer posts
+  if (peer_ready_) {
+    borrow_peer(nbp);
+    borrow_peer(nxp);
+  }
   if (nranks_ > 1) {
-    const bool need_prev = mode != CKF_REC_RANDOM;
+    const bool need_prev = mode != CKF_REC_RANDOM && !peer_ready_;
     if (nbp && need_prev) {
       const int src = owner_of_stage(mode == CKF_REC_EDGE ? (sid == 1 ? 2 : s - 1) : sid - 1);
       pull(&nbp->w, src, bytes, 60);
@@ -985,7 +1073,7 @@ ckf_recovery_report Engine::recover_stage(int sid, int mode, int moments, double
         pull(&nbp->v, src, bytes, 62);
       }
     }
-    if (nxp && (mode == CKF_REC_CHECKFREE || mode == CKF_REC_UNIFORM)) {
+    if (nxp && !peer_ready_ && (mode == CKF_REC_CHECKFREE || mode == CKF_REC_UNIFORM)) {
       const int src = owner_of_stage(sid + 1);
       pull(&nxp->w, src, bytes, 63);
       if (avg) {
@@ -1001,8 +1089,8 @@ ckf_recovery_report Engine::recover_stage(int sid, int mode, int moments, double
   }
 
   double* red_dev = want_red ? scal_ + 3500 : nullptr;
-  if (local) CKF_CUDA(cudaEventRecord(ev0_, st_));
   long new_step = 0;
+  bool fused = false;
   if (mode == CKF_REC_EDGE) {
     ParamGroup& nb = *nbp;
     ParamGroup& eg = sid == 1 ? embed_ : deembed_;
@@ -1062,40 +1150,73 @@ ckf_recovery_report Engine::recover_stage(int sid, int mode, int moments, double
         }
         CKF_CUDA(cudaMemcpyAsync(f.w, p.w, bytes, cudaMemcpyDeviceToDevice, st_));
       } else {
-        // the streaming omega-weighted average (recovery.cpp:57-73), optional ||old - new||^2 in the same pass
+        // CheckFree / uniform average: ONE streaming pass makes the stage ready -- weights
+        // (recovery.cpp:57-73), moments Fresh or omega-weighted (trainer.cpp:263-269), gradient
+        // accumulator zeroed, bf16 shadow, and ||old - new||^2 from the same read of the old W.
+        // The neighbour pointers may be peer mappings of another GPU's HBM.
         kt_begin();
+        auto run = [&](auto* tag) {
+          using T = std::remove_pointer_t<decltype(tag)>;
+          k::StageRecovery<T> r;
+          r.wp = static_cast<const T*>(p.w);
+          r.wn = static_cast<const T*>(n.w);
+          r.w = static_cast<T*>(f.w);
+          r.m = static_cast<T*>(f.m);
+          r.v = static_cast<T*>(f.v);
+          r.g = static_cast<T*>(f.g);
+          r.wlp = f.wlp;
+          r.n = f.n;
+          r.op = op;
+          r.on = on;
+          r.averaged = avg;
+          if (avg) {
+            r.mp = static_cast<const T*>(p.m);
+            r.mn = static_cast<const T*>(n.m);
+            r.vp = static_cast<const T*>(p.v);
+            r.vn = static_cast<const T*>(n.v);
+            r.mop = p.omega;
+            r.mon = n.omega;
+          }
+          r.old_sq = red_dev;
+          k::recover_stage(r, red_, st_);
+        };
         if (fp64())
-          k::recover(static_cast<const double*>(p.w), static_cast<const double*>(n.w), static_cast<double*>(f.w), f.n,
-                     op, on, red_dev, red_, st_);
+          run(static_cast<double*>(nullptr));
         else
-          k::recover(static_cast<const float*>(p.w), static_cast<const float*>(n.w), static_cast<float*>(f.w), f.n, op,
-                     on, red_dev, red_, st_);
-        kt_end(KC_RECOVER, 0.0, 3.0 * static_cast<double>(bytes));
+          run(static_cast<float*>(nullptr));
+        fused = true;
+        const double pb = static_cast<double>(master_bytes());
+        kt_end(KC_RECOVER, 0.0,
+               static_cast<double>(f.n) * (pb * (6.0 + (avg ? 4.0 : 0.0) + (want_red ? 1.0 : 0.0)) + (f.wlp ? 2.0 : 0.0)));
       }
-      if (avg) {
-        // omega-weighted moments (trainer.cpp:263-269)
-        const double wp = p.omega, wn = n.omega;
-        if (fp64()) {
-          k::weighted_or_uniform(static_cast<const double*>(p.m), static_cast<const double*>(n.m),
-                                 static_cast<double*>(f.m), f.n, wp, wn, st_);
-          k::weighted_or_uniform(static_cast<const double*>(p.v), static_cast<const double*>(n.v),
-                                 static_cast<double*>(f.v), f.n, wp, wn, st_);
+      if (!fused) {
+        if (avg) {
+          // omega-weighted moments (trainer.cpp:263-269)
+          const double wp = p.omega, wn = n.omega;
+          if (fp64()) {
+            k::weighted_or_uniform(static_cast<const double*>(p.m), static_cast<const double*>(n.m),
+                                   static_cast<double*>(f.m), f.n, wp, wn, st_);
+            k::weighted_or_uniform(static_cast<const double*>(p.v), static_cast<const double*>(n.v),
+                                   static_cast<double*>(f.v), f.n, wp, wn, st_);
+          } else {
+            k::weighted_or_uniform(static_cast<const float*>(p.m), static_cast<const float*>(n.m),
+                                   static_cast<float*>(f.m), f.n, wp, wn, st_);
+            k::weighted_or_uniform(static_cast<const float*>(p.v), static_cast<const float*>(n.v),
+                                   static_cast<float*>(f.v), f.n, wp, wn, st_);
+          }
         } else {
-          k::weighted_or_uniform(static_cast<const float*>(p.m), static_cast<const float*>(n.m),
-                                 static_cast<float*>(f.m), f.n, wp, wn, st_);
-          k::weighted_or_uniform(static_cast<const float*>(p.v), static_cast<const float*>(n.v),
-                                 static_cast<float*>(f.v), f.n, wp, wn, st_);
+          CKF_CUDA(cudaMemsetAsync(f.m, 0, bytes, st_));
+          CKF_CUDA(cudaMemsetAsync(f.v, 0, bytes, st_));
         }
-      } else {
-        CKF_CUDA(cudaMemsetAsync(f.m, 0, bytes, st_));
-        CKF_CUDA(cudaMemsetAsync(f.v, 0, bytes, st_));
       }
     }
     new_step = avg ? std::min(p.step, n.step) : 0;
   }
   if (local) {
-    CKF_CUDA(cudaMemsetAsync(f.g, 0, bytes, st_));
-    if (f.wlp) k::convert(static_cast<const float*>(f.w), f.wlp, f.n, st_);
+    if (!fused) {
+      CKF_CUDA(cudaMemsetAsync(f.g, 0, bytes, st_));
+      if (f.wlp) k::convert(static_cast<const float*>(f.w), f.wlp, f.n, st_);
+    }
     CKF_CUDA(cudaEventRecord(ev1_, st_));
   }
   f.step = new_step;
@@ -1103,6 +1224,12 @@ ckf_recovery_report Engine::recover_stage(int sid, int mode, int moments, double
   f.omega = 0.0;          // trainer.cpp:276
   if (local && want_red)
     CKF_CUDA(cudaMemcpyAsync(&rep.reduction_error, red_dev, sizeof(double), cudaMemcpyDeviceToHost, st_));
+  if (peer_ready_ && comm_) {
+    // the neighbours' owners must not update the weights the replacement GPU reads in place
+    // until its recovery kernel is done: an all-reduce enqueued behind it is the barrier
+    nccl_check(nccl().AllReduce(scal_ + 3600, scal_ + 3600, 1, /*ncclFloat64*/ 8, /*ncclSum*/ 0, comm_, st_),
+               "ncclAllReduce (recovery barrier)");
+  }
   CKF_CUDA(cudaStreamSynchronize(st_));
   kt_collect();
   for (auto it = borrowed.rbegin(); it != borrowed.rend(); ++it) *it->first = it->second;

@@ -173,6 +173,12 @@ class Engine {
   // nranks = replicas x P pipeline ranks; rank r is pipeline rank r % P of replica r / P;
   // stage_rank[s-1] names the pipeline rank (0..P-1) holding stage s in every replica
   void attach_comm(const void* uid, int nranks, int rank, const int* stage_rank, int replicas = 1);
+  // placement without a communicator (attach_comm = this + NCCL init)
+  void set_placement(int nranks, int rank, const int* stage_rank, int replicas = 1);
+  // peer recovery: CUDA IPC handles of the owned stages' w / m / v; import maps the other
+  // ranks' stages (same replica) so recover_stage reads neighbours straight from peer HBM
+  size_t ipc_export(void* buf, size_t cap);
+  void ipc_import(const void* buf, size_t len);
   std::vector<ParamGroup*> owned_groups();
   // 0 = sequential (forward+backward per microbatch, one live activation cache);
   // 1 = GPipe (all forwards, then all backwards in microbatch order: the ranks of
@@ -191,6 +197,8 @@ class Engine {
   // microbatch (the downstream node's hot copy) and every stage's master weights are copied to
   // its replica after the optimizer step (the post-step weight refresh of cost_model.cpp:271-279).
   void set_redundant(bool on) { redundant_ = on; }
+  // CheckFree+: refresh the edge replicas at the end of every run_iteration (trainer.cpp:83-84)
+  void set_edge_replicas(bool on) { auto_replicas_ = on; }
   // device time (ms) of the last run_iteration: first device op .. loss / omega D2H
   float last_step_ms();
   int group_cap() const { return group_cap_; }
@@ -248,6 +256,7 @@ class Engine {
   std::vector<long> gkey_, gseen_;
   long graph_kernels_ = 0;  // kernel launches inside the captured graph
   bool redundant_ = false;
+  bool auto_replicas_ = false;
   std::vector<void*> rc_replica_;  // per stage: the hot copy's master weights
   std::vector<std::pair<size_t, int>> group_fit_;  // (microbatch tokens, fitted group size)
   int fused_group_size(int m, size_t mb_rows);
@@ -257,6 +266,11 @@ class Engine {
   std::vector<int> vrank_;
   std::vector<long> hop_log_;
   std::vector<int> stage_rank_;
+  struct PeerStage {
+    void *w = nullptr, *m = nullptr, *v = nullptr;
+  };
+  std::vector<PeerStage> peer_;
+  bool peer_ready_ = false;  // every stage this rank does not own is mapped  // per stage id - 1: IPC mappings of stages owned by other ranks
   void* comm_ = nullptr;  // ncclComm_t
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
   cudaEvent_t sb_ev_ = nullptr, se_ev_ = nullptr;  // run_iteration device-timeline bracket

@@ -54,6 +54,27 @@ template <typename T> void recover(const T* wp, const T* wn, T* out, size_t n, d
 template <typename T> void weighted_or_uniform(const T* a, const T* b, T* out, size_t n, double op, double on,
                                                cudaStream_t s);
 
+// One streaming pass that makes a failed stage ready (trainer.cpp:230-276 for the
+// neighbour-average family): w = (op*Wp + on*Wn)/(op+on) (recovery.cpp:57-73; op = on = 1
+// for the uniform baseline), Adam moments Fresh (zero) or Averaged (omega-weighted, the
+// weighted_or_uniform policy of trainer.cpp:263-269), gradient accumulator zeroed, bf16
+// shadow refreshed, and optionally ||w_old - w_new||^2 (trainer.cpp:278-279) from the same
+// read.  wp / wn / mp / mn / vp / vn may be PEER pointers (another GPU's HBM mapped through
+// CUDA IPC / peer access): the same kernel pulls the neighbours over NVLink.
+template <typename T>
+struct StageRecovery {
+  const T *wp = nullptr, *wn = nullptr;                        // neighbour weights
+  const T *mp = nullptr, *mn = nullptr, *vp = nullptr, *vn = nullptr;  // neighbour moments (Averaged)
+  T *w = nullptr, *m = nullptr, *v = nullptr, *g = nullptr;   // the failed stage
+  __nv_bfloat16* wlp = nullptr;                                 // its bf16 shadow (may be null)
+  size_t n = 0;
+  double op = 1.0, on = 1.0;   // weight omegas (degenerate 0,0 -> uniform, recovery.cpp:63-68)
+  bool averaged = false;       // moments: false = Fresh (zero), true = omega-weighted
+  double mop = 0.0, mon = 0.0; // moment weights (the neighbours' omegas)
+  double* old_sq = nullptr;    // optional ||w_old - w_new||^2 (device double)
+};
+template <typename T> void recover_stage(const StageRecovery<T>& r, ReduceScratch& sc, cudaStream_t s);
+
 // NaN poison (simulated loss of a stage's GPU state)
 template <typename T> void poison(T* x, size_t n, cudaStream_t s);
 

@@ -337,6 +337,123 @@ __global__ void wavg_kernel(const T* __restrict__ a, const T* __restrict__ b, T*
   }
 }
 
+
+// ---------------------------------------------------------------- fused stage recovery
+// One pass over the stage (see StageRecovery in kernels.h).  fp32: 16-byte streams, UNROLL
+// independent float4 slots per thread in flight; loads of the neighbours are evict-first
+// (they are read once), stores streaming.  Algorithmic bytes per parameter (fp32):
+// read Wp, Wn (8) + write W (4) + write m, v, g (12) + bf16 shadow (2) = 26; Averaged adds
+// the four neighbour-moment reads (16); the reduction error adds the read of the old W (4).
+template <bool kAvg, bool kSq>
+__global__ void __launch_bounds__(256) recover_stage_f32x4_kernel(
+    const float4* __restrict__ wp, const float4* __restrict__ wn, const float4* __restrict__ mp,
+    const float4* __restrict__ mn, const float4* __restrict__ vp, const float4* __restrict__ vn,
+    float4* __restrict__ w, float4* __restrict__ m, float4* __restrict__ v, float4* __restrict__ g,
+    uint2* __restrict__ wlp, size_t n4, float a, float b, double ma, double mb, double mden, int mom_uniform,
+    double* __restrict__ partials) {
+  constexpr int U = 4;
+  double acc = 0.0;
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  auto mavg = [&](float x, float y) -> float {
+    return mom_uniform ? 0.5f * (x + y)
+                       : static_cast<float>((ma * static_cast<double>(x) + mb * static_cast<double>(y)) / mden);
+  };
+  for (size_t base = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; base < n4; base += stride * U) {
+    float4 p[U], q[U], o[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const size_t i = base + j * stride;
+      if (i < n4) {
+        p[j] = __ldcs(wp + i);
+        q[j] = __ldcs(wn + i);
+        if (kSq) o[j] = __ldcs(w + i);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const size_t i = base + j * stride;
+      if (i >= n4) break;
+      float4 r;
+      r.x = fmaf(a, p[j].x, b * q[j].x);
+      r.y = fmaf(a, p[j].y, b * q[j].y);
+      r.z = fmaf(a, p[j].z, b * q[j].z);
+      r.w = fmaf(a, p[j].w, b * q[j].w);
+      if (kSq) {
+        const double dx = static_cast<double>(o[j].x) - r.x, dy = static_cast<double>(o[j].y) - r.y;
+        const double dz = static_cast<double>(o[j].z) - r.z, dw = static_cast<double>(o[j].w) - r.w;
+        acc += dx * dx + dy * dy + dz * dz + dw * dw;
+      }
+      __stcs(w + i, r);
+      if (wlp) {
+        __nv_bfloat162 lo = __floats2bfloat162_rn(r.x, r.y), hi = __floats2bfloat162_rn(r.z, r.w);
+        uint2 pk;
+        pk.x = *reinterpret_cast<unsigned*>(&lo);
+        pk.y = *reinterpret_cast<unsigned*>(&hi);
+        __stcs(wlp + i, pk);
+      }
+      __stcs(g + i, z);
+      if (kAvg) {
+        const float4 a0 = __ldcs(mp + i), b0 = __ldcs(mn + i), a1 = __ldcs(vp + i), b1 = __ldcs(vn + i);
+        __stcs(m + i, make_float4(mavg(a0.x, b0.x), mavg(a0.y, b0.y), mavg(a0.z, b0.z), mavg(a0.w, b0.w)));
+        __stcs(v + i, make_float4(mavg(a1.x, b1.x), mavg(a1.y, b1.y), mavg(a1.z, b1.z), mavg(a1.w, b1.w)));
+      } else {
+        __stcs(m + i, z);
+        __stcs(v + i, z);
+      }
+    }
+  }
+  if (kSq) {
+    acc = block_sum<double, kThreads>(acc);
+    if (threadIdx.x == 0) partials[blockIdx.x] = acc;
+  }
+}
+
+// Scalar form (fp64 with the reference's exact expression order, or unaligned fp32).
+template <typename T>
+__global__ void recover_stage_kernel(StageRecovery<T> r, double a, double b, double denom, double mden,
+                                     int mom_uniform, double* __restrict__ partials) {
+  double acc = 0.0;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < r.n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    T x;
+    if constexpr (sizeof(T) == 8) {
+      x = __ddiv_rn(__dadd_rn(__dmul_rn(a, r.wp[i]), __dmul_rn(b, r.wn[i])), denom);  // recovery.cpp:71
+    } else {
+      x = fmaf(static_cast<float>(a), r.wp[i], static_cast<float>(b) * r.wn[i]);  // a, b pre-normalised
+    }
+    if (r.old_sq) {
+      const double d = static_cast<double>(r.w[i]) - static_cast<double>(x);
+      acc += d * d;
+    }
+    r.w[i] = x;
+    if (r.wlp) r.wlp[i] = __float2bfloat16(static_cast<float>(x));
+    r.g[i] = T(0);
+    if (r.averaged) {
+      if constexpr (sizeof(T) == 8) {
+        r.m[i] = mom_uniform ? __dmul_rn(0.5, __dadd_rn(r.mp[i], r.mn[i]))
+                             : __ddiv_rn(__dadd_rn(__dmul_rn(r.mop, r.mp[i]), __dmul_rn(r.mon, r.mn[i])), mden);
+        r.v[i] = mom_uniform ? __dmul_rn(0.5, __dadd_rn(r.vp[i], r.vn[i]))
+                             : __ddiv_rn(__dadd_rn(__dmul_rn(r.mop, r.vp[i]), __dmul_rn(r.mon, r.vn[i])), mden);
+      } else {
+        r.m[i] = mom_uniform ? 0.5f * (r.mp[i] + r.mn[i])
+                             : static_cast<float>((r.mop * static_cast<double>(r.mp[i]) +
+                                                   r.mon * static_cast<double>(r.mn[i])) / mden);
+        r.v[i] = mom_uniform ? 0.5f * (r.vp[i] + r.vn[i])
+                             : static_cast<float>((r.mop * static_cast<double>(r.vp[i]) +
+                                                   r.mon * static_cast<double>(r.vn[i])) / mden);
+      }
+    } else {
+      r.m[i] = T(0);
+      r.v[i] = T(0);
+    }
+  }
+  if (r.old_sq) {
+    acc = block_sum<double, kThreads>(acc);
+    if (threadIdx.x == 0) partials[blockIdx.x] = acc;
+  }
+}
+
 template <typename T>
 __global__ void poison_kernel(T* __restrict__ x, size_t n) {
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
@@ -514,6 +631,54 @@ void weighted_or_uniform(const T* a, const T* b, T* out, size_t n, double op, do
 }
 
 template <typename T>
+void recover_stage(const StageRecovery<T>& r, ReduceScratch& sc, cudaStream_t s) {
+  if (!r.n) return;
+  double a = r.op, b = r.on;
+  if (a + b == 0.0) a = b = 1.0;  // degenerate: uniform average (recovery.cpp:63-68)
+  const double denom = a + b;
+  const double mden = r.mop + r.mon;
+  const int mom_uniform = mden == 0.0 ? 1 : 0;
+  // the reduction-error partials need one fixed grid (deterministic fold); the plain pass
+  // keeps ~8 CTAs of 256 threads per SM streaming
+  if constexpr (sizeof(T) == 4) {
+    const float fa = static_cast<float>(a / denom), fb = static_cast<float>(b / denom);
+    uintptr_t al = reinterpret_cast<uintptr_t>(r.wp) | reinterpret_cast<uintptr_t>(r.wn) |
+                   reinterpret_cast<uintptr_t>(r.w) | reinterpret_cast<uintptr_t>(r.m) |
+                   reinterpret_cast<uintptr_t>(r.v) | reinterpret_cast<uintptr_t>(r.g);
+    if (r.averaged)
+      al |= reinterpret_cast<uintptr_t>(r.mp) | reinterpret_cast<uintptr_t>(r.mn) |
+            reinterpret_cast<uintptr_t>(r.vp) | reinterpret_cast<uintptr_t>(r.vn);
+    if (al % 16 == 0 && reinterpret_cast<uintptr_t>(r.wlp) % 8 == 0 && r.n % 4 == 0) {
+      const size_t n4 = r.n / 4;
+      const unsigned grid = r.old_sq ? reduce_grid(r.n / 4) : grid_for((n4 + 3) / 4, kThreads, kNumSMs * 8);
+      auto f4 = [](const float* p) { return reinterpret_cast<const float4*>(p); };
+      auto o4 = [](float* p) { return reinterpret_cast<float4*>(p); };
+      auto launch = [&](auto kern) {
+        kern<<<grid, kThreads, 0, s>>>(f4(r.wp), f4(r.wn), f4(r.mp), f4(r.mn), f4(r.vp), f4(r.vn), o4(r.w), o4(r.m),
+                                       o4(r.v), o4(r.g), reinterpret_cast<uint2*>(r.wlp), n4, fa, fb, r.mop, r.mon,
+                                       mden, mom_uniform, sc.partials);
+      };
+      if (r.averaged)
+        r.old_sq ? launch(recover_stage_f32x4_kernel<true, true>) : launch(recover_stage_f32x4_kernel<true, false>);
+      else
+        r.old_sq ? launch(recover_stage_f32x4_kernel<false, true>) : launch(recover_stage_f32x4_kernel<false, false>);
+      CKF_LAUNCH_CHECK();
+      if (r.old_sq) finish(sc, grid, r.old_sq, s);
+      return;
+    }
+    const unsigned grid = reduce_grid(r.n);
+    recover_stage_kernel<float><<<grid, kThreads, 0, s>>>(r, fa, fb, 1.0, mden, mom_uniform, sc.partials);
+    CKF_LAUNCH_CHECK();
+    if (r.old_sq) finish(sc, grid, r.old_sq, s);
+  } else {
+    const unsigned grid = reduce_grid(r.n);
+    recover_stage_kernel<T><<<grid, kThreads, 0, s>>>(r, a, b, denom, mden, mom_uniform, sc.partials);
+    CKF_LAUNCH_CHECK();
+    if (r.old_sq) finish(sc, grid, r.old_sq, s);
+  }
+}
+
+template <typename T>
 void poison(T* x, size_t n, cudaStream_t s) {
   if (!n) return;
   poison_kernel<T><<<grid_for(n, kThreads), kThreads, 0, s>>>(x, n);
@@ -539,7 +704,8 @@ void poison(T* x, size_t n, cudaStream_t s) {
   template void recover<T>(const T*, const T*, T*, size_t, double, double, double*, ReduceScratch&,          \
                            cudaStream_t);                                                                     \
   template void weighted_or_uniform<T>(const T*, const T*, T*, size_t, double, double, cudaStream_t);        \
-  template void poison<T>(T*, size_t, cudaStream_t);
+  template void poison<T>(T*, size_t, cudaStream_t);                                                         \
+  template void recover_stage<T>(const StageRecovery<T>&, ReduceScratch&, cudaStream_t);
 
 CKF_INST(double)
 CKF_INST(float)
