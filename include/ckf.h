@@ -166,6 +166,27 @@ int ckf_attention_fwd(const void* qkv, size_t B, size_t T, size_t H, size_t hd, 
 int ckf_attention_bwd(const void* qkv, const void* o, const float* lse, const void* dout, size_t B, size_t T,
                       size_t H, size_t hd, void* dqkv, float* Dsum, int impl, void* stream);
 
+/* LLaMA block bandwidth kernels on DEVICE buffers (llama_kernels.cu), exported so each is
+ * pinned on its own against fp32 torch at every width the workloads run:
+ *   rmsnorm_fwd: y = bf16(x * rsqrt(mean(x^2) + 1e-5) * g), rstd[row], xcopy (optional) = x
+ *   rmsnorm_bwd: dh += d rmsnorm(x)/dx . dy (fp32), dh_bf (optional) = bf16(dh), gg += gain grad
+ *   rope: rotary embedding (theta 1e4, pairs (j, j+hd/2), position t % T) in place on the q and
+ *         k column blocks of qkv [ntok x 3d]; inverse = 1 applies the transpose (backward)
+ *   swiglu_fwd: a = silu(gate) * up, gu = [gate | up] [ntok x 2f];  swiglu_bwd: dgu from da
+ *   embed_fwd: h = E[tok];  embed_bwd: gE[v] += sum of dh over tok == v (token order, deterministic)
+ *   gemm_qkv_rope: C = bf16(A B) with RoPE fused into the epilogue on the first 2d columns
+ *         (A [M x K] K-major, B [K x 3d] N-major; head_dim 64), as the QKV projection runs it */
+int ckf_llama_rmsnorm_fwd(const float* x, const float* g, size_t rows, size_t d, void* y_bf16, float* rstd,
+                          float* xcopy, void* stream);
+int ckf_llama_rmsnorm_bwd(const float* dy, const float* x, const float* g, const float* rstd, size_t rows, size_t d,
+                          float* dh, void* dh_bf16, float* gg, void* stream);
+int ckf_llama_rope(void* qkv, size_t ntok, size_t T, size_t d, size_t heads, int inverse, void* stream);
+int ckf_llama_swiglu_fwd(const void* gu, size_t ntok, size_t f, void* a, void* stream);
+int ckf_llama_swiglu_bwd(const void* gu, const void* da, size_t ntok, size_t f, void* dgu, void* stream);
+int ckf_llama_embed_fwd(const int* tok, size_t ntok, const float* E, size_t d, float* h, void* stream);
+int ckf_llama_embed_bwd(const int* tok, size_t ntok, const float* dh, size_t d, float* gE, void* stream);
+int ckf_gemm_qkv_rope(int M, int K, const void* A, const void* B, void* C, size_t T, size_t heads, void* stream);
+
 /* LLaMA token stream (csrc/tokens.cu): rows x (T+1) int32 ids keyed
  * (data_seed, stream, index) like the reference's batches (dataset.cpp:15-20),
  * generated on the device, copied to host `out`. */

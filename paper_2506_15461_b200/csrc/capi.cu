@@ -732,3 +732,87 @@ int ckf_run_experiment_to_dir(const char* kv, const char* trace_text, uint64_t s
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ LLaMA bandwidth kernels (standalone)
+namespace {
+void* scratch_ws(size_t bytes) {  // per-thread growable device scratch for the standalone entries
+  static thread_local void* p = nullptr;
+  static thread_local size_t have = 0;
+  if (bytes > have) {
+    if (p) CKF_CUDA(cudaFree(p));
+    CKF_CUDA(cudaMalloc(&p, bytes));
+    have = bytes;
+  }
+  return p;
+}
+}  // namespace
+
+int ckf_llama_rmsnorm_fwd(const float* x, const float* g, size_t rows, size_t d, void* y_bf16, float* rstd,
+                          float* xcopy, void* stream) {
+  return guard([&] {
+    ckf::llama::rmsnorm_fwd(x, g, rows, d, static_cast<__nv_bfloat16*>(y_bf16), rstd, xcopy,
+                            static_cast<cudaStream_t>(stream));
+  });
+}
+int ckf_llama_rmsnorm_bwd(const float* dy, const float* x, const float* g, const float* rstd, size_t rows, size_t d,
+                          float* dh, void* dh_bf16, float* gg, void* stream) {
+  return guard([&] {
+    auto st = static_cast<cudaStream_t>(stream);
+    const int nblk = ckf::llama::rmsnorm_bwd_blocks(rows);
+    float* gpart = static_cast<float*>(scratch_ws(static_cast<size_t>(nblk) * d * sizeof(float)));
+    ckf::llama::rmsnorm_bwd(dy, x, g, rstd, rows, d, dh, static_cast<__nv_bfloat16*>(dh_bf16), gpart, st);
+    ckf::llama::gain_fold(gpart, nblk, d, gg, st);
+    CKF_CUDA(cudaStreamSynchronize(st));
+  });
+}
+int ckf_llama_rope(void* qkv, size_t ntok, size_t T, size_t d, size_t heads, int inverse, void* stream) {
+  return guard([&] {
+    ckf::llama::rope(static_cast<__nv_bfloat16*>(qkv), ntok, T, d, heads, inverse, static_cast<cudaStream_t>(stream));
+  });
+}
+int ckf_llama_swiglu_fwd(const void* gu, size_t ntok, size_t f, void* a, void* stream) {
+  return guard([&] {
+    ckf::llama::swiglu_fwd(static_cast<const __nv_bfloat16*>(gu), ntok, f, static_cast<__nv_bfloat16*>(a),
+                           static_cast<cudaStream_t>(stream));
+  });
+}
+int ckf_llama_swiglu_bwd(const void* gu, const void* da, size_t ntok, size_t f, void* dgu, void* stream) {
+  return guard([&] {
+    ckf::llama::swiglu_bwd(static_cast<const __nv_bfloat16*>(gu), static_cast<const __nv_bfloat16*>(da), ntok, f,
+                           static_cast<__nv_bfloat16*>(dgu), static_cast<cudaStream_t>(stream));
+  });
+}
+int ckf_llama_embed_fwd(const int* tok, size_t ntok, const float* E, size_t d, float* h, void* stream) {
+  return guard([&] { ckf::llama::embed_fwd(tok, ntok, E, d, h, static_cast<cudaStream_t>(stream)); });
+}
+int ckf_llama_embed_bwd(const int* tok, size_t ntok, const float* dh, size_t d, float* gE, void* stream) {
+  return guard([&] {
+    auto st = static_cast<cudaStream_t>(stream);
+    ckf::llama::embed_bwd(tok, ntok, dh, d, gE, scratch_ws(ckf::llama::embed_bwd_scratch(ntok)), st);
+    CKF_CUDA(cudaStreamSynchronize(st));
+  });
+}
+int ckf_gemm_qkv_rope(int M, int K, const void* A, const void* B, void* C, size_t T, size_t heads, void* stream) {
+  return guard([&] {
+    if (K <= 0 || heads == 0 || K % static_cast<int>(heads) || K / static_cast<int>(heads) != 64)
+      ckf::raise(CKF_E_CONFIG, "gemm_qkv_rope: the fused RoPE epilogue serves head_dim 64 (K = d = 64 * heads)");
+    auto st = static_cast<cudaStream_t>(stream);
+    ckf::tc::GemmDesc g;
+    g.M = M;
+    g.N = 3 * K;
+    g.K = K;
+    g.A = static_cast<const __nv_bfloat16*>(A);
+    g.lda = K;
+    g.a_mn = false;
+    g.B = static_cast<const __nv_bfloat16*>(B);
+    g.ldb = 3 * K;
+    g.b_mn = true;
+    g.C = C;
+    g.ldc = 3 * K;
+    g.epi = ckf::tc::kStoreBF16;
+    g.rope_tab = ckf::llama::rope_table_pair_major(T, 64, st);
+    g.rope_T = static_cast<int>(T);
+    g.rope_cols = 2 * K;
+    ckf::tc::gemm_bf16(g, st);
+  });
+}

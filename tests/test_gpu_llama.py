@@ -3,8 +3,8 @@ against the CPU fp64 oracle (oracle/llama_oracle.py), through the C-ABI.
 
 Bars (stated here because the reference pins none of the LLaMA arithmetic):
   * token stream, init streams: bit-exact (integer / fp64->fp32 rounding)
-  * microbatch loss: 2e-2 relative;  gradients: 6e-2 relative Frobenius error
-    per parameter group (bf16 operands, fp32 accumulation)
+  * microbatch loss: 2e-4 relative;  gradients: 2.5e-2 relative Frobenius error
+    per parameter group (bf16 operands, fp32 accumulation; measured <= 8.8e-5 / 1.39 %)
   * loss curve over a short run: every point within 1% (north_star)
   * recovered weights: fp32 recovery kernel within 1e-5 relative (north_star)
   * two runs with the same seed: bit-identical losses (determinism)
@@ -18,7 +18,8 @@ pytestmark = pytest.mark.gpu
 import llama_oracle as LO  # noqa: E402
 from ckfree_oracle import build_schedule, derive_key, recover_checkfree, standard_order  # noqa: E402
 
-SMALL = LO.LSpec(vocab=512, d=128, layers=4, heads=2, ffn=256, seq_len=64, stages=4)
+# T = 128: the tcgen05 attention kernels (T % 128 == 0) run, as in every benched workload
+SMALL = LO.LSpec(vocab=512, d=128, layers=4, heads=2, ffn=256, seq_len=128, stages=4)
 
 
 def _engine(spec, rows_per_mb, seed=3, lr=1e-3):
@@ -51,6 +52,19 @@ def test_init_bit_exact():
     eng.close()
 
 
+# measured on the B200 (profiles/r02_parity_errors.jsonl): loss <= 8.8e-5, gradients <= 1.39 %
+LOSS_BAR, GRAD_BAR = 2e-4, 2.5e-2
+
+
+def _log(rec):
+    import json
+    import os
+    path = os.environ.get("CKF_PARITY_LOG")
+    if path:
+        with open(path, "a") as f:
+            f.write(json.dumps(rec) + "\n")
+
+
 def _rel(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
 
@@ -64,12 +78,13 @@ def test_microbatch_loss_and_gradients(swapped):
     eng.zero_grad()
     lg = eng.accumulate(order, toks)
     lo, gs, ge, gd = LO.microbatch(ref, order, toks)
-    assert abs(lg - lo) <= 2e-2 * abs(lo), (lg, lo)
+    errs = {"loss": abs(lg - lo) / abs(lo), "embed": _rel(eng.export_grad("embed"), ge),
+            "deembed": _rel(eng.export_grad("deembed"), gd)}
     for sid in range(1, SMALL.stages + 1):
-        e = _rel(eng.export_grad("stage", sid), gs[sid - 1])
-        assert e < 6e-2, (sid, e)
-    assert _rel(eng.export_grad("embed"), ge) < 6e-2
-    assert _rel(eng.export_grad("deembed"), gd) < 6e-2
+        errs[f"stage{sid}"] = _rel(eng.export_grad("stage", sid), gs[sid - 1])
+    _log({"test": "small_microbatch", "swapped": swapped, **errs})
+    assert errs["loss"] <= LOSS_BAR, errs
+    assert all(v <= GRAD_BAR for k, v in errs.items() if k != "loss"), errs
     # eval path == accumulate path loss
     assert abs(eng.eval_loss(order, toks) - lg) <= 1e-6 * abs(lg)
     eng.close()

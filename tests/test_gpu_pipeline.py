@@ -27,7 +27,7 @@ def _mlp_engine(seed=5):
 
 def _llama_engine(seed=3):
     import paper_2506_15461_b200 as P
-    spec = P.api.ModelSpec.llama(512, 128, 4, 2, 256, 64, 4, max_tokens=2 * 64)
+    spec = P.api.ModelSpec.llama(512, 128, 4, 2, 256, 128, 4, max_tokens=2 * 128)
     e = P.Engine(spec)
     e.init(seed, 1e-3)
     return e
@@ -37,7 +37,7 @@ def _batches(kind, it):
     rng = np.random.default_rng(100 + it)
     if kind == "mlp":
         return rng.uniform(-1, 1, (32, 16)), rng.uniform(-1, 1, (32, 16))
-    return LO.token_batch(9, 1, it, 8, 64, 512), None
+    return LO.token_batch(9, 1, it, 8, 128, 512), None
 
 
 @pytest.mark.parametrize("kind", ["mlp", "llama"])
@@ -75,6 +75,6 @@ def test_engine_transfers_follow_the_plan(kind, schedule, placement):
     log = e.hop_log()
     plan = [op for op in api.pipeline_plan(orders, placement, schedule) if op["kind"] == "xfer"]
     assert [(a, b) for a, b, _ in log] == [(op["rank"], op["arg"]) for op in plan]
-    per_mb = (8 * 32 * 8) if kind == "mlp" else (2 * 64 * 128 * 4)  # rows x width x bytes (fp64 MLP / fp32 LLaMA)
+    per_mb = (8 * 32 * 8) if kind == "mlp" else (2 * 128 * 128 * 4)  # rows x width x bytes (fp64 MLP / fp32 LLaMA)
     assert all(nb == per_mb for _, _, nb in log)
     e.close()
