@@ -234,6 +234,17 @@ def placement(world: int, s: int):
     raise SystemExit(f"{s} stages cannot be placed on {world} GPUs (need world | s or s | world)")
 
 
+def scaled_workload(w: dict, gpus: int) -> dict:
+    """Weak scaling over pipeline ranks: with the stages partitioned over P ranks the step runs
+    P x the microbatches (same tokens per microbatch), so every GPU pushes the same token-layers
+    per step as the single-GPU run (65,536 tokens x 24 layers at LLaMA-500M) and the 1F1B bubble
+    (P-1)/(m+P-1) stays ~10 %.  Data-parallel replicas each add their own batch."""
+    P, _ = placement(gpus, w["stages"])
+    if P == 1:
+        return w
+    return dict(w, microbatches=w["microbatches"] * P, rows=w["rows"] * P)
+
+
 def workload_config(args, w: dict) -> dict:
     P, R = placement(args.gpus, w["stages"])
     cfg = {"parallelism": f"pp{P}" + (f"xdp{R}" if R > 1 else ""),"workload": args.workload, "block": w["block"], "stages": w["stages"],
@@ -242,7 +253,10 @@ def workload_config(args, w: dict) -> dict:
            "strategy": getattr(args, "strategy", DEFAULT_STRATEGY),
            "schedule": "swapped_half (swapped first/last-stage order at even microbatches) + per-step edge replica "
                        "refresh" if getattr(args, "strategy", DEFAULT_STRATEGY) == "checkfree-plus" else "standard", "placement": f"{w['stages']} stages on {P} pipeline rank(s) x {R} replica(s)",
-           "l2": "256 MiB memset between timed steps (outside the events)"}
+           "l2": "256 MiB memset between timed steps (outside the events)",
+           "pipeline_schedule": "1F1B (host-planned global op order, transfers on send/recv streams over per-link "
+                                "NCCL communicators)" if P > 1 else "all stages resident (fused microbatch groups)",
+           "bubble_1f1b": (P - 1) / (w["microbatches"] + P - 1) if P > 1 else 0.0}
     if w["block"] == "llama":
         cfg.update(vocab=w["output_dim"], heads=w["heads"])
         # all stages resident on a rank => microbatches sharing an execution order run as
@@ -304,6 +318,7 @@ def run_ours(args, w: dict):
         uid = [P_.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         eng.attach_comm(uid[0], world, rank, [(sid - 1) * P // s for sid in range(1, s + 1)], R)
+        eng.exchange_peers()  # CUDA IPC mappings: recovery reads neighbours from the peers' HBM
 
     orders = np.array(api.build_schedule(w["microbatches"], cfp, s), np.int32)  # pipeline.cpp:41-56
     gen = torch.Generator().manual_seed(1234 + rank // P)  # one batch per replica (weak scaling)
@@ -393,21 +408,30 @@ def run_ours(args, w: dict):
 
     # stage-recovery latency (trainer.cpp:230-276 semantics, weights + moments + lr + omega), stage 2
     rec = None
-    if world == 1 and s >= 3:
+    if s >= 3:
         # kill-to-ready latency of an interior stage (CheckFree omega-average, trainer.cpp:230-276):
         # one fused pass -- weights, Fresh moments, zeroed gradient, bf16 shadow -- CUDA events on the
-        # engine stream; algorithmic bytes 26 per fp32 parameter (read Wp, Wn; write W, m, v, g; bf16 W)
+        # replacement GPU's stream; algorithmic bytes 26 per fp32 parameter (read Wp, Wn; write W, m,
+        # v, g; bf16 W).  N > 1: the first stage of pipeline rank 1, whose previous neighbour lives on
+        # rank 0 -- the kernel reads it from the peer's HBM over NVLink (CUDA IPC mapping); every rank
+        # takes part (the recovery is collective) and the latency is the replacement GPU's.
+        sid = 2 if P == 1 else min(s - 1, s // P + 1)
         lat = []
         for _ in range(5):
-            eng.kill_stage(2)
-            lat.append(eng.recover_stage(2, reduction_error=False).latency_ms)
+            eng.kill_stage(sid)
+            lat.append(eng.recover_stage(sid, reduction_error=False).latency_ms)
         n_stage = eng.stage_params
         pb = 4 if w["precision"] != "fp64" else 8
         nbytes = n_stage * (6 * pb + (2 if w["precision"] == "bf16" else 0))
         med = statistics.median(lat)
-        rec = {"stage": 2, "stage_params": n_stage, "latency_ms": med, "latency_ms_min": min(lat),
+        owner = lambda x: (x - 1) * P // s  # noqa: E731
+        remote = [n for n in (sid - 1, sid + 1) if owner(n) != owner(sid)]
+        rec = {"stage": sid, "stage_params": n_stage, "latency_ms": med, "latency_ms_min": min(lat),
                "bytes": nbytes, "gbs": nbytes / (med / 1e3) / 1e9,
+               "neighbours_on_peers": remote,
                "what": "kill -> ready: omega-weighted weights, Fresh m/v, g = 0, bf16 shadow in one kernel"}
+        if remote:
+            rec["nvlink_ingress_gbs"] = len(remote) * pb * n_stage / (med / 1e3) / 1e9
         if cfp:
             # CheckFree+ first-stage recovery: stage 1 := stage 2, E := its replica (recovery.cpp:90-101)
             el = []
@@ -582,7 +606,11 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    w = WORKLOADS[args.workload]
+    w = scaled_workload(WORKLOADS[args.workload], args.gpus)
+    if args.gpus > 1:
+        # NCCL init lines (rank count, transport) on stderr-side logging, for the scaling run's evidence
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     if args.impl == "reference":
         run_reference_arm(args, w)
     else:

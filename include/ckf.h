@@ -70,6 +70,11 @@ int ckf_build_schedule(int m, int swapped_half, int s, int* out);
  * transfer's destination rank), aux (transfer: 0 activations, 1 gradients).
  * schedule: 0 = forward+backward per microbatch (pipeline.cpp:66-81 order),
  * 1 = GPipe (all forwards, then all backwards in microbatch order). */
+/* schedule 2 = 1F1B (host-simulated list schedule, see host_logic.cpp): stage_cost (s forward time
+ * units, may be NULL = 1 each) and head_cost weigh the simulation; the engine uses its own costs
+ * (ckf_engine_plan_cost).  ckf_pipeline_plan is ckf_pipeline_plan_cost with unit costs. */
+int ckf_pipeline_plan_cost(int s, int m, const int* orders, const int* stage_rank, int schedule,
+                           const double* stage_cost, double head_cost, int* out, int cap_ops, int* n_ops);
 int ckf_pipeline_plan(int s, int m, const int* orders, const int* stage_rank, int schedule, int* out, int cap_ops,
                       int* n_ops);
 
@@ -241,6 +246,11 @@ int ckf_engine_set_placement(ckf_engine_t e, int nranks, int rank, const int* st
  * the peers' HBM inside the recovery kernel (no staging copy).  *len = bytes written. */
 int ckf_engine_ipc_export(ckf_engine_t e, void* buf, size_t cap, size_t* len);
 int ckf_engine_ipc_import(ckf_engine_t e, const void* buf, size_t len);
+/* Collective over the attached communicator: all-gathers every rank's IPC blob and imports
+ * them (ckf_engine_ipc_export / _import in one call). */
+int ckf_engine_exchange_peers(ckf_engine_t e);
+/* the per-stage forward costs and head cost the engine's 1F1B plan is simulated with */
+int ckf_engine_plan_cost(ckf_engine_t e, double* stage_cost, double* head_cost);
 /* pipeline x data parallel (config 4: 4 stages x DP2): nranks = replicas * P; rank r is
  * pipeline rank r % P of replica r / P; stage_rank[] names PIPELINE ranks (0..P-1).  Each
  * replica runs its own microbatches; owned gradients are summed over the replicas
@@ -360,6 +370,14 @@ int ckf_engine_kernel_stats(ckf_engine_t e, int cls, double* ms, long* launches,
  *     "U,reason").
  * ===================================================================== */
 int ckf_run_experiment(const char* kv_config, const char* trace_text, uint64_t seed, char* record, size_t cap);
+/* The same trainer as ONE rank of a multi-GPU run (one process per GPU): stages placed in
+ * contiguous blocks over nranks / replicas pipeline ranks (edges with stages 1 and s),
+ * `replicas` data-parallel copies (replica r trains on microbatches [r m/R, (r+1) m/R) of the
+ * global batch), stage transfers 1F1B over NCCL, recovery reading the neighbours from the
+ * peers' HBM.  Every rank calls it with the same arguments and the NCCL unique id of rank 0
+ * (ckf_nccl_unique_id); every rank returns the same record. */
+int ckf_run_experiment_rank(const char* kv_config, const char* trace_text, uint64_t seed, const void* nccl_uid,
+                            int nranks, int rank, int replicas, char* record, size_t cap);
 /* run_experiment_to_dir (src/experiment.cpp:202-213): the same run, writing
  * metrics.csv, events.csv, summary.json and config.resolved in the reference's
  * schema (format_version=1) into dir; wall_hours / recovery_s are measured. */

@@ -76,6 +76,8 @@ def lib():
         "ckf_consecutive_conflicts": (i, [cp, C.POINTER(lng), i, ip]),
         "ckf_hourly_to_per_iteration": (dbl, [dbl, dbl]),
         "ckf_even_partition": (i, [sz, sz, C.POINTER(sz)]), "ckf_build_schedule": (i, [i, i, i, ip]),
+        "ckf_pipeline_plan": (i, [i, i, ip, ip, i, ip, i, ip]),
+        "ckf_pipeline_plan_cost": (i, [i, i, ip, ip, i, dp, dbl, ip, i, ip]),
         "ckf_k_gemm_nn": (i, [dp, dp, dp, sz, sz, sz]), "ckf_k_gemm_nn_acc": (i, [dp, dp, dp, sz, sz, sz]),
         "ckf_k_gemm_nt_acc": (i, [dp, dp, dp, sz, sz, sz]), "ckf_k_gemm_tn_acc": (i, [dp, dp, dp, sz, sz, sz]),
         "ckf_k_add_inplace": (i, [dp, dp, sz]), "ckf_k_axpy": (i, [dbl, dp, dp, sz]), "ckf_k_scale": (i, [dbl, dp, sz]),
@@ -110,6 +112,8 @@ def lib():
         "ckf_engine_attach_comm_dp": (i, [eng, vp, i, i, ip, i]),
         "ckf_engine_set_placement": (i, [eng, i, i, ip, i]),
         "ckf_engine_ipc_export": (i, [eng, vp, sz, C.POINTER(sz)]), "ckf_engine_ipc_import": (i, [eng, vp, sz]),
+        "ckf_engine_exchange_peers": (i, [eng]),
+        "ckf_engine_plan_cost": (i, [eng, dp, dp]),
         "ckf_recover_stage_device": (i, [i, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, dbl, dbl, i, vp, vp]),
         "ckf_engine_run_iteration": (i, [eng, ip, i, vp, vp, sz, i, lng, dp, dp]),
         "ckf_engine_eval_loss": (i, [eng, ip, vp, vp, sz, i, dp]),
@@ -129,6 +133,7 @@ def lib():
         "ckf_engine_kernel_stats": (i, [eng, i, dp, C.POINTER(lng), dp, dp]),
         "ckf_run_experiment": (i, [cp, cp, u64, cp, sz]),
         "ckf_run_experiment_to_dir": (i, [cp, cp, u64, cp]),
+        "ckf_run_experiment_rank": (i, [cp, cp, u64, vp, i, i, i, cp, sz]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

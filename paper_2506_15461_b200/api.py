@@ -63,15 +63,18 @@ def build_schedule(m: int, swapped_half: bool, s: int):
 PLAN_KINDS = ("embed_fwd", "stage_fwd", "xfer", "head", "stage_bwd", "embed_bwd")
 
 
-def pipeline_plan(orders, stage_rank, schedule: int = 1):
-    """Global op sequence of one iteration for a stage -> rank placement (ckf_pipeline_plan)."""
+def pipeline_plan(orders, stage_rank, schedule: int = 1, stage_cost=None, head_cost: float = 1.0):
+    """Global op sequence of one iteration for a stage -> rank placement (ckf_pipeline_plan_cost);
+    schedule 0 sequential, 1 GPipe, 2 1F1B (weighted by stage_cost / head_cost)."""
     orders = np.ascontiguousarray(orders, np.int32)
     m, s = orders.shape
     sr = np.ascontiguousarray(stage_rank, np.int32)
     cap = 8 * m * (s + 4) + 16
     out = np.zeros(6 * cap, np.int32)
     n = C.c_int(0)
-    check(lib().ckf_pipeline_plan(s, m, _ip(orders.reshape(-1)), _ip(sr), schedule, _ip(out), cap, C.byref(n)))
+    sc = None if stage_cost is None else np.ascontiguousarray(stage_cost, np.float64)
+    check(lib().ckf_pipeline_plan_cost(s, m, _ip(orders.reshape(-1)), _ip(sr), schedule,
+                                       _dp(sc) if sc is not None else None, head_cost, _ip(out), cap, C.byref(n)))
     return [dict(phase=int(o[0]), mb=int(o[1]), kind=PLAN_KINDS[o[2]], rank=int(o[3]), arg=int(o[4]),
                  aux=int(o[5])) for o in out[:6 * n.value].reshape(-1, 6)]
 
@@ -337,6 +340,17 @@ class Engine:
         buf = C.create_string_buffer(data, max(1, len(data)))
         check(lib().ckf_engine_ipc_import(self._h, buf, len(data)))
 
+    def plan_cost(self):
+        """(per-stage forward costs, head cost) the engine's 1F1B plan is simulated with."""
+        sc = np.zeros(self.spec.num_stages, np.float64)
+        h = C.c_double()
+        check(lib().ckf_engine_plan_cost(self._h, _dp(sc), C.byref(h)))
+        return sc, h.value
+
+    def exchange_peers(self):
+        """Collective (after attach_comm): maps every other rank's stages for peer recovery."""
+        check(lib().ckf_engine_exchange_peers(self._h))
+
     def sync(self):
         check(lib().ckf_engine_sync(self._h))
 
@@ -402,12 +416,19 @@ def nccl_unique_id() -> bytes:
 
 
 # ------------------------------------------------------------- trainer
-def run_experiment(cfg: dict, trace_text: str, seed: int):
+def run_experiment(cfg: dict, trace_text: str, seed: int, comm=None):
     """harness::run_experiment (src/trainer.cpp:314-322) on the GPU engine.
+    comm = (nccl_uid, nranks, rank, replicas): this process is one rank of a multi-GPU run
+    (torchrun, one process per GPU; every rank passes rank 0's nccl_unique_id()).
     Returns (evals[(iter, train, val)], events[(iter, stage, action, red, spike, ms)], unrecoverable_reason|None)."""
     kv = ";".join(f"{k}={v}" for k, v in cfg.items()).encode()
     buf = C.create_string_buffer(1 << 22)
-    check(lib().ckf_run_experiment(kv, trace_text.encode(), seed, buf, len(buf)))
+    if comm is None:
+        check(lib().ckf_run_experiment(kv, trace_text.encode(), seed, buf, len(buf)))
+    else:
+        uid, nranks, rank, replicas = comm
+        ub = C.create_string_buffer(uid, 128)
+        check(lib().ckf_run_experiment_rank(kv, trace_text.encode(), seed, ub, nranks, rank, replicas, buf, len(buf)))
     evals, events, unrec = [], [], None
     for ln in buf.value.decode().splitlines():
         p = ln.split(",")

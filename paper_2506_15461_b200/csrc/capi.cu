@@ -17,8 +17,6 @@
 namespace ckf {
 void llama_token_batch(uint64_t data_seed, uint64_t stream, uint64_t index, size_t rows, size_t T, size_t V, int* out,
                        cudaStream_t s);
-std::string run_experiment(const std::string& kv, const std::string& trace_text, uint64_t seed,
-                           const std::string& dir);
 int nccl_unique_id(void* out, size_t cap);
 }  // namespace ckf
 
@@ -150,13 +148,16 @@ int ckf_parse_trace(const char* text, char* out, size_t cap) {
     std::memcpy(out, s.c_str(), s.size() + 1);
   });
 }
-int ckf_pipeline_plan(int s, int m, const int* orders, const int* stage_rank, int schedule, int* out, int cap_ops,
-                      int* n_ops) {
+int ckf_pipeline_plan_cost(int s, int m, const int* orders, const int* stage_rank, int schedule,
+                           const double* stage_cost, double head_cost, int* out, int cap_ops, int* n_ops) {
   return guard([&] {
     if (s < 1 || m < 1) ckf::raise(CKF_E_CONFIG, "pipeline plan needs s >= 1 and m >= 1");
+    ckf::host::PlanCost cost;
+    if (stage_cost) cost.stage.assign(stage_cost, stage_cost + s);
+    cost.head = head_cost;
     const auto ops = ckf::host::pipeline_plan(
         s, m, std::vector<int>(orders, orders + static_cast<size_t>(s) * static_cast<size_t>(m)),
-        std::vector<int>(stage_rank, stage_rank + s), schedule);
+        std::vector<int>(stage_rank, stage_rank + s), schedule, &cost);
     if (static_cast<int>(ops.size()) > cap_ops) ckf::raise(CKF_E_USAGE, "output buffer too small");
     for (size_t i = 0; i < ops.size(); ++i) {
       int* o = out + 6 * i;
@@ -169,6 +170,10 @@ int ckf_pipeline_plan(int s, int m, const int* orders, const int* stage_rank, in
     }
     *n_ops = static_cast<int>(ops.size());
   });
+}
+int ckf_pipeline_plan(int s, int m, const int* orders, const int* stage_rank, int schedule, int* out, int cap_ops,
+                      int* n_ops) {
+  return ckf_pipeline_plan_cost(s, m, orders, stage_rank, schedule, nullptr, 1.0, out, cap_ops, n_ops);
 }
 int ckf_consecutive_conflicts(const char* text, long* out, int cap_pairs, int* n_out) {
   return guard([&] {
@@ -568,6 +573,16 @@ int ckf_engine_ipc_export(ckf_engine_t e, void* buf, size_t cap, size_t* len) {
 int ckf_engine_ipc_import(ckf_engine_t e, const void* buf, size_t len) {
   return guard([&] { E(e)->ipc_import(buf, len); });
 }
+int ckf_engine_exchange_peers(ckf_engine_t e) {
+  return guard([&] { E(e)->exchange_peers(); });
+}
+int ckf_engine_plan_cost(ckf_engine_t e, double* stage_cost, double* head_cost) {
+  return guard([&] {
+    const auto c = E(e)->plan_cost();
+    std::copy(c.stage.begin(), c.stage.end(), stage_cost);
+    *head_cost = c.head;
+  });
+}
 int ckf_engine_attach_comm_dp(ckf_engine_t e, const void* uid, int nranks, int rank, const int* stage_rank,
                               int replicas) {
   return guard([&] { E(e)->attach_comm(uid, nranks, rank, stage_rank, replicas); });
@@ -719,6 +734,22 @@ int ckf_engine_kernel_stats(ckf_engine_t e, int cls, double* ms, long* launches,
 int ckf_run_experiment(const char* kv, const char* trace_text, uint64_t seed, char* record, size_t cap) {
   return guard([&] {
     const std::string r = ckf::run_experiment(kv ? kv : "", trace_text ? trace_text : "", seed, "");
+    if (r.size() + 1 > cap) ckf::raise(CKF_E_USAGE, "record buffer too small");
+    std::memcpy(record, r.c_str(), r.size() + 1);
+  });
+}
+
+int ckf_run_experiment_rank(const char* kv, const char* trace_text, uint64_t seed, const void* nccl_uid, int nranks,
+                            int rank, int replicas, char* record, size_t cap) {
+  return guard([&] {
+    if (!nccl_uid || nranks < 1 || rank < 0 || rank >= nranks || replicas < 1 || nranks % replicas)
+      ckf::raise(CKF_E_CONFIG, "invalid world / rank / replicas");
+    ckf::TrainerComm cm;
+    cm.uid = nccl_uid;
+    cm.nranks = nranks;
+    cm.rank = rank;
+    cm.replicas = replicas;
+    const std::string r = ckf::run_experiment(kv ? kv : "", trace_text ? trace_text : "", seed, "", &cm);
     if (r.size() + 1 > cap) ckf::raise(CKF_E_USAGE, "record buffer too small");
     std::memcpy(record, r.c_str(), r.size() + 1);
   });

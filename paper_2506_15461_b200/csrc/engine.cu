@@ -9,6 +9,7 @@
 #include <string>
 
 #include "engine.h"
+#include "host_logic.h"
 
 #include <chrono>
 #include <cstdio>
@@ -54,6 +55,7 @@ struct NcclApi {
   int (*Recv)(void*, size_t, int, int, void*, cudaStream_t) = nullptr;
   int (*AllReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
   int (*CommSplit)(void*, int, int, void**, void*) = nullptr;
+  int (*AllGather)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
   int (*GroupStart)() = nullptr;
   int (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(int) = nullptr;
@@ -75,6 +77,8 @@ NcclApi& nccl() {
       api.AllReduce = reinterpret_cast<int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t)>(
           dlsym(h, "ncclAllReduce"));
       api.CommSplit = reinterpret_cast<int (*)(void*, int, int, void**, void*)>(dlsym(h, "ncclCommSplit"));
+      api.AllGather =
+          reinterpret_cast<int (*)(const void*, void*, size_t, int, void*, cudaStream_t)>(dlsym(h, "ncclAllGather"));
       api.GroupStart = reinterpret_cast<int (*)()>(dlsym(h, "ncclGroupStart"));
       api.GroupEnd = reinterpret_cast<int (*)()>(dlsym(h, "ncclGroupEnd"));
       api.GetErrorString = reinterpret_cast<const char* (*)(int)>(dlsym(h, "ncclGetErrorString"));
@@ -135,6 +139,10 @@ Engine::Engine(const ckf_model_desc& in) {
 
   CKF_CUDA(cudaSetDevice(d_.device));
   CKF_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+  // side streams of the plan-driven pipeline (stage transfers) and of the data-parallel all-reduce
+  CKF_CUDA(cudaStreamCreateWithFlags(&sst_, cudaStreamNonBlocking));
+  CKF_CUDA(cudaStreamCreateWithFlags(&rst_, cudaStreamNonBlocking));
+  CKF_CUDA(cudaStreamCreateWithFlags(&dst_, cudaStreamNonBlocking));
   CKF_CUDA(cudaMalloc(&red_.partials, ReduceScratch::kMaxReduceBlocks * sizeof(double)));
   CKF_CUDA(cudaMalloc(&scal_, 4096 * sizeof(double)));
   CKF_CUDA(cudaMemset(scal_, 0, 4096 * sizeof(double)));
@@ -168,6 +176,11 @@ Engine::~Engine() {
   for (void* p : ws_) cudaFree(p);
   cudaFree(red_.partials);
   cudaFree(scal_);
+  for (cudaStream_t x : {sst_, rst_, dst_})
+    if (x) cudaStreamSynchronize(x);
+  for (auto& l : links_)
+    if (l.second && nccl().CommDestroy) nccl().CommDestroy(l.second);
+  for (cudaEvent_t ev : pev_) cudaEventDestroy(ev);
   if (dp_comm_ && nccl().CommDestroy) nccl().CommDestroy(dp_comm_);
   if (comm_ && nccl().CommDestroy) nccl().CommDestroy(comm_);
   if (gexec_) cudaGraphExecDestroy(gexec_);
@@ -183,6 +196,8 @@ Engine::~Engine() {
   if (sg_ev_) cudaEventDestroy(sg_ev_);
   if (se_ev_) cudaEventDestroy(se_ev_);
   if (st_) cudaStreamDestroy(st_);
+  for (cudaStream_t x : {sst_, rst_, dst_})
+    if (x) cudaStreamDestroy(x);
 }
 
 void Engine::alloc_group(ParamGroup& g, size_t n, bool lowp) {
@@ -292,7 +307,7 @@ void Engine::set_placement(int nranks, int rank, const int* stage_rank, int repl
   for (size_t i = 0; i < d_.s; ++i) stage_rank_[i] = replica_ * P + stage_rank[i];
   rank_ = rank;
   nranks_ = nranks;
-  if (nranks > 1) schedule_ = 1;
+  if (nranks > 1) schedule_ = impl_->supports_plan() ? 2 : 1;  // 1F1B where the block runs plan ops
   // release buffers of stages this rank does not own
   for (size_t i = 0; i < d_.s; ++i) {
     stages_[i].owned = stage_rank_[i] == rank_;
@@ -317,7 +332,147 @@ void Engine::attach_comm(const void* uid, int nranks, int rank, const int* stage
       if (!nccl().CommSplit) raise(7, "ncclCommSplit unavailable (NCCL >= 2.18 needed for replicas)");
       nccl_check(nccl().CommSplit(comm_, rank % P, replica_, &dp_comm_, nullptr), "ncclCommSplit");
     }
+    // one communicator per DIRECTED stage link of the pipeline (the links the standard and the
+    // CheckFree+ swapped routes use under this placement): on every rank a link's communicator
+    // is driven by exactly one stream (the source's send stream / the destination's recv
+    // stream).  ncclCommSplit is collective over the world: every rank walks the same link list.
+    if (P > 1 && nccl().CommSplit) {
+      std::vector<int> sr(stage_rank, stage_rank + d_.s);
+      std::vector<std::pair<int, int>> want;
+      for (int sw = 0; sw < (d_.s >= 4 ? 2 : 1); ++sw) {
+        const std::vector<int> o = host::build_schedule(2, sw == 1, static_cast<int>(d_.s));
+        for (const auto& op : host::pipeline_plan(static_cast<int>(d_.s), 2, o, sr, 1))
+          if (op.kind == host::PlanOp::kXfer) want.push_back({op.rank, op.arg});
+      }
+      std::sort(want.begin(), want.end());
+      want.erase(std::unique(want.begin(), want.end()), want.end());
+      const int me = rank % P;
+      for (size_t i = 0; i < want.size(); ++i) {
+        const auto [a, b] = want[i];
+        const bool in = me == a || me == b;
+        void* c = nullptr;
+        // color = link index x replicas + replica (each replica gets its own 2-rank communicator);
+        // key orders the source first
+        nccl_check(nccl().CommSplit(comm_, in ? static_cast<int>(i) * replicas + replica_ : -1 /*NCCL_SPLIT_NOCOLOR*/,
+                                    me == a ? 0 : 1, &c, nullptr),
+                   "ncclCommSplit (stage link)");
+        if (in) links_.push_back({{replica_ * P + a, replica_ * P + b}, c});
+      }
+    }
   }
+}
+
+void* Engine::link_comm(int src, int dst) {
+  for (auto& l : links_)
+    if (l.first.first == src && l.first.second == dst) return l.second;
+  raise(7, "no communicator for stage link " + std::to_string(src) + " -> " + std::to_string(dst));
+}
+
+cudaEvent_t Engine::plan_event() {
+  if (pev_used_ == pev_.size()) {
+    cudaEvent_t ev;
+    CKF_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    pev_.push_back(ev);
+  }
+  return pev_[pev_used_++];
+}
+
+host::PlanCost Engine::plan_cost() const {
+  host::PlanCost cost;
+  for (size_t i = 0; i < d_.s; ++i) cost.stage.push_back(static_cast<double>(d_.part[i].count()));
+  if (d_.block == CKF_BLOCK_LLAMA) {
+    const double layer = 4.0 * d_.d * d_.d + 3.0 * d_.d * d_.hid + 2.0 * d_.d * d_.T;  // per token, fwd
+    cost.head = static_cast<double>(d_.d) * static_cast<double>(d_.out) / layer;
+  }
+  return cost;
+}
+
+void Engine::grad_bucket_ready(void* g, size_t n) {
+  if (replicas_ <= 1 || !dp_comm_ || n == 0) return;
+  // this bucket's sum over the replicas on the data-parallel stream, behind the GEMMs that
+  // produced it; the optimizer step waits for the stream (run_iteration)
+  cudaEvent_t ev = plan_event();
+  CKF_CUDA(cudaEventRecord(ev, st_));
+  CKF_CUDA(cudaStreamWaitEvent(dst_, ev, 0));
+  nccl_check(nccl().AllReduce(g, g, n, fp64() ? /*ncclFloat64*/ 8 : /*ncclFloat32*/ 7, /*ncclSum*/ 0, dp_comm_, dst_),
+             "ncclAllReduce (data-parallel bucket)");
+  dp_pending_ = true;
+}
+
+// Plan-driven iteration (schedule 2): every rank walks the SAME global op order
+// (host::pipeline_plan, 1F1B) and executes its own share -- compute ops on the engine stream,
+// sends on the send stream behind an event of the producing op, receives on the recv stream with
+// the consuming op waiting on their event.  Each microbatch's buffers are private to it for the
+// iteration, so the only cross-stream hazards are a buffer received back after this rank sent it
+// (the recv waits for that send) and the end of the step (the engine stream joins both side
+// streams).  With a virtual placement (hop log) on one GPU every op runs here and a transfer is
+// a pointer hand-off.
+void Engine::run_plan(const int* orders, int m, const char* x, size_t mb, size_t xrow) {
+  const int s = static_cast<int>(d_.s);
+  const bool virt = log_hops_;
+  std::vector<int> placement(d_.s, 0);
+  for (size_t i = 0; i < d_.s; ++i) placement[i] = virt ? vrank_[i] : owner_of_stage(static_cast<int>(i + 1));
+  const host::PlanCost cost = plan_cost();
+  const std::vector<int> ov(orders, orders + static_cast<size_t>(m) * d_.s);
+  const int slots = host::plan_inflight_limit(m, placement);
+  const auto plan = host::pipeline_plan(s, m, ov, placement, 2, &cost, slots);
+  impl_->plan_begin(m, mb, slots, x);
+  std::vector<cudaEvent_t> pending(static_cast<size_t>(m) * 2, nullptr);  // recv landed (per mb, phase)
+  std::vector<cudaEvent_t> sent(static_cast<size_t>(m) * 2, nullptr);     // last send of the buffer
+  bool any_send = false, any_recv = false;
+  (void)xrow;
+  for (const auto& op : plan) {
+    const int k = op.mb;
+    if (op.kind == host::PlanOp::kXfer) {
+      size_t bytes = 0;
+      void* b = impl_->plan_buffer(k, op.aux, &bytes);
+      if (virt) {
+        hop_log_.push_back(op.rank);
+        hop_log_.push_back(op.arg);
+        hop_log_.push_back(static_cast<long>(bytes));
+        if (op.aux == 1) impl_->plan_received(k, 1);  // the receiving side's bf16(dh) refresh
+        continue;
+      }
+      const size_t slot = static_cast<size_t>(k) * 2 + static_cast<size_t>(op.aux);
+      if (op.rank == rank_) {  // send behind the producing op
+        cudaEvent_t ev = plan_event();
+        CKF_CUDA(cudaEventRecord(ev, st_));
+        CKF_CUDA(cudaStreamWaitEvent(sst_, ev, 0));
+        nccl_check(nccl().Send(b, bytes, /*ncclInt8*/ 0, 1, link_comm(op.rank, op.arg), sst_), "ncclSend (stage link)");
+        cudaEvent_t done = plan_event();
+        CKF_CUDA(cudaEventRecord(done, sst_));
+        sent[slot] = done;
+        any_send = true;
+      } else if (op.arg == rank_) {  // receive; the consuming op waits on it
+        if (sent[slot]) CKF_CUDA(cudaStreamWaitEvent(rst_, sent[slot], 0));
+        nccl_check(nccl().Recv(b, bytes, /*ncclInt8*/ 0, 0, link_comm(op.rank, op.arg), rst_), "ncclRecv (stage link)");
+        cudaEvent_t ev = plan_event();
+        CKF_CUDA(cudaEventRecord(ev, rst_));
+        pending[slot] = ev;
+        any_recv = true;
+      }
+      continue;
+    }
+    if (!virt && op.rank != rank_) continue;
+    for (int ph = 0; ph < 2; ++ph) {
+      cudaEvent_t& ev = pending[static_cast<size_t>(k) * 2 + static_cast<size_t>(ph)];
+      if (!ev) continue;
+      CKF_CUDA(cudaStreamWaitEvent(st_, ev, 0));
+      ev = nullptr;
+      if (ph == 1) impl_->plan_received(k, 1);
+    }
+    const int* o = orders + static_cast<size_t>(k) * d_.s;
+    impl_->plan_op(op.kind, k, op.arg, o, scal_ + k);
+  }
+  // the step's end joins the side streams (sends done reading, every receive consumed)
+  for (auto [flag, str] : {std::make_pair(any_send, sst_), std::make_pair(any_recv, rst_)}) {
+    if (!flag) continue;
+    cudaEvent_t ev = plan_event();
+    CKF_CUDA(cudaEventRecord(ev, str));
+    CKF_CUDA(cudaStreamWaitEvent(st_, ev, 0));
+  }
+  (void)x;
+  (void)s;
 }
 
 // ------------------------------------------------------------------ peer (IPC) mappings
@@ -557,6 +712,8 @@ void Engine::run_iteration(const int* orders, int m, const void* x, const void* 
   auto yk = [&](int k) { return yd ? yd + static_cast<size_t>(k) * mb * ycols * yelt : nullptr; };
   auto ok = [&](int k) { return orders + static_cast<size_t>(k) * d_.s; };
   impl_->begin_iteration(m, mb);
+  pev_used_ = 0;
+  dp_pending_ = false;
   size_t nloss = static_cast<size_t>(m);
   bool flushed = false;
   // fusion needs every stage on this rank, the sequential schedule, and no virtual placement
@@ -658,6 +815,8 @@ void Engine::run_iteration(const int* orders, int m, const void* x, const void* 
     }
     flushed = true;
     nloss = groups.size();
+  } else if (schedule_ == 2 && impl_->supports_plan()) {
+    run_plan(orders, m, xd, mb, mb * xcols * xelt);  // 1F1B over the placement (host::pipeline_plan)
   } else if (schedule_ == 0) {
     for (int k = 0; k < m; ++k) {
       impl_->microbatch(k, ok(k), xk(k), yk(k), mb, true, scal_ + k);
@@ -678,12 +837,25 @@ void Engine::run_iteration(const int* orders, int m, const void* x, const void* 
   }
   if (!flushed) impl_->flush_grads();
   // data parallelism: sum every owned group's gradient over the replicas (each replica ran
-  // its own m microbatches of the global batch), then Adam with 1/(m*R)
+  // its own m microbatches of the global batch), then Adam with 1/(m*R).  The stage groups were
+  // all-reduced layer by layer on the data-parallel stream while the remaining weight-gradient
+  // GEMMs ran (grad_bucket_ready); the edge groups (and everything, when the weight gradients
+  // were not deferred) follow here; the optimizer waits for the stream.
   if (replicas_ > 1) {
-    for (ParamGroup* g : owned_groups())
+    cudaEvent_t ev = plan_event();
+    CKF_CUDA(cudaEventRecord(ev, st_));
+    CKF_CUDA(cudaStreamWaitEvent(dst_, ev, 0));
+    for (ParamGroup* g : owned_groups()) {
+      const bool edge = g == &embed_ || g == &deembed_;
+      if (dp_pending_ && !edge) continue;
       nccl_check(nccl().AllReduce(g->g, g->g, g->n, fp64() ? /*ncclFloat64*/ 8 : /*ncclFloat32*/ 7, /*ncclSum*/ 0,
-                                  dp_comm_, st_),
+                                  dp_comm_, dst_),
                  "ncclAllReduce (data parallel)");
+    }
+    cudaEvent_t done = plan_event();
+    CKF_CUDA(cudaEventRecord(done, dst_));
+    CKF_CUDA(cudaStreamWaitEvent(st_, done, 0));
+    dp_pending_ = false;
   }
   // mean loss in microbatch order, then *1/m (model.cpp:299-312, pipeline.cpp:82-83)
   std::vector<double> losses(nloss);
@@ -889,12 +1061,55 @@ double Engine::eval_loss(const int* order, const void* x, const void* y, size_t 
     CKF_CUDA(cudaMemcpyAsync(ls.data(), scal_ + 4010, ls.size() * sizeof(double), cudaMemcpyDeviceToHost, st_));
     CKF_CUDA(cudaStreamSynchronize(st_));
     for (size_t i = 0; i < chunks.size(); ++i) l += ls[i] * static_cast<double>(chunks[i].second);
-    return l / static_cast<double>(rows);
+    return share_from_head(l / static_cast<double>(rows));
   }
   impl_->microbatch(0, order, x, y, rows, false, scal_ + 4000);
   CKF_CUDA(cudaMemcpyAsync(&l, scal_ + 4000, sizeof(double), cudaMemcpyDeviceToHost, st_));
   CKF_CUDA(cudaStreamSynchronize(st_));
-  return l;
+  return share_from_head(l);
+}
+
+// Multi-rank: the loss exists on the de-embedding owner only; every rank returns replica 0's value.
+double Engine::share_from_head(double v) {
+  if (nranks_ <= 1 || !comm_) return v;
+  const double mine_v = mine(owner_of_deembed()) && replica_ == 0 ? v : 0.0;
+  return allreduce_host({mine_v})[0];
+}
+
+std::vector<double> Engine::allreduce_host(const std::vector<double>& v) {
+  double* dv = scal_ + 3700;
+  if (v.size() > 200) raise(1, "allreduce_host: at most 200 values");
+  CKF_CUDA(cudaMemcpyAsync(dv, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice, st_));
+  nccl_check(nccl().AllReduce(dv, dv, v.size(), /*ncclFloat64*/ 8, /*ncclSum*/ 0, comm_, st_), "ncclAllReduce");
+  std::vector<double> out(v.size());
+  CKF_CUDA(cudaMemcpyAsync(out.data(), dv, v.size() * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  CKF_CUDA(cudaStreamSynchronize(st_));
+  return out;
+}
+
+// Peer mappings for recovery over NVLink: every rank's IPC blob (ipc_export) all-gathered over
+// the world communicator, then imported (stages of the same replica this rank does not own).
+void Engine::exchange_peers() {
+  if (nranks_ <= 1 || !comm_) return;
+  if (!nccl().AllGather) raise(7, "ncclAllGather unavailable");
+  constexpr size_t kBlob = 1 << 14;
+  std::vector<char> mine_b(kBlob + 8, 0);
+  const size_t n = ipc_export(mine_b.data() + 8, kBlob);
+  std::memcpy(mine_b.data(), &n, 8);
+  char* dev = static_cast<char*>(ws((kBlob + 8) * static_cast<size_t>(nranks_ + 1), 70));
+  CKF_CUDA(cudaMemcpyAsync(dev, mine_b.data(), kBlob + 8, cudaMemcpyHostToDevice, st_));
+  nccl_check(nccl().AllGather(dev, dev + kBlob + 8, kBlob + 8, /*ncclInt8*/ 0, comm_, st_), "ncclAllGather (IPC)");
+  std::vector<char> all((kBlob + 8) * static_cast<size_t>(nranks_));
+  CKF_CUDA(cudaMemcpyAsync(all.data(), dev + kBlob + 8, all.size(), cudaMemcpyDeviceToHost, st_));
+  CKF_CUDA(cudaStreamSynchronize(st_));
+  std::vector<char> cat;
+  for (int r = 0; r < nranks_; ++r) {
+    const char* b = all.data() + static_cast<size_t>(r) * (kBlob + 8);
+    size_t len = 0;
+    std::memcpy(&len, b, 8);
+    cat.insert(cat.end(), b + 8, b + 8 + len);
+  }
+  ipc_import(cat.data(), cat.size());
 }
 
 double Engine::accumulate(const int* order, const void* x, const void* y, size_t rows, bool on_device) {
@@ -1237,6 +1452,12 @@ ckf_recovery_report Engine::recover_stage(int sid, int mode, int moments, double
     float ms = 0.f;
     CKF_CUDA(cudaEventElapsedTime(&ms, ev0_, ev1_));
     rep.latency_ms = ms;
+  }
+  if (nranks_ > 1 && comm_) {  // every rank reports the replacement GPU's numbers (replica 0)
+    const bool src = local && replica_ == 0;
+    const auto v = allreduce_host({src ? rep.reduction_error : 0.0, src ? rep.latency_ms : 0.0});
+    rep.reduction_error = v[0];
+    rep.latency_ms = v[1];
   }
   return rep;
 }

@@ -13,10 +13,12 @@
 #include <cuda_runtime.h>
 
 #include <memory>
+#include <string>
 #include <vector>
 
 #include "../../include/ckf.h"
 #include "common.cuh"
+#include "host_logic.h"
 #include "kernels.h"
 
 namespace ckf {
@@ -112,6 +114,38 @@ struct BlockImpl {
   }
   // block state that changes the launch sequence of an iteration (part of the CUDA-graph key)
   virtual long state_token() const { return 0; }
+  // ---- plan-driven execution (schedule 2, 1F1B): the engine walks the global op order of
+  // host::pipeline_plan and hands this rank's ops to the block one at a time; transfers are the
+  // engine's (send / recv streams).  Microbatch k keeps its own residual-stream and gradient
+  // buffers for the whole iteration; activation caches rotate over `slots` microbatches (the
+  // plan keeps at most that many in flight per rank).
+  virtual bool supports_plan() const { return false; }
+  virtual void plan_begin(int m, size_t rows, int slots, const void* x) {
+    (void)m;
+    (void)rows;
+    (void)slots;
+    (void)x;
+  }
+  // kind: host::PlanOp kind (embed fwd, stage fwd, head, stage bwd, embed bwd); sid for stage ops
+  virtual void plan_op(int kind, int k, int sid, const int* order, double* loss_dev) {
+    (void)kind;
+    (void)k;
+    (void)sid;
+    (void)order;
+    (void)loss_dev;
+  }
+  // the buffer a transfer of microbatch k carries (phase 0: residual stream h, 1: its gradient dh)
+  virtual void* plan_buffer(int k, int phase, size_t* bytes) {
+    (void)k;
+    (void)phase;
+    *bytes = 0;
+    return nullptr;
+  }
+  // a transfer of microbatch k landed on this rank (compute-stream ordered)
+  virtual void plan_received(int k, int phase) {
+    (void)k;
+    (void)phase;
+  }
   int wk = 0;  // position of the current microbatch within the iteration (in microbatches)
   // Rows of ONE microbatch when a call carries a fused group of several (the
   // loss and its gradient stay per-microbatch means, pipeline.cpp:66-83); 0 = rows.
@@ -179,12 +213,25 @@ class Engine {
   // ranks' stages (same replica) so recover_stage reads neighbours straight from peer HBM
   size_t ipc_export(void* buf, size_t cap);
   void ipc_import(const void* buf, size_t len);
+  // collective: all-gathers every rank's IPC blob over NCCL and imports them
+  void exchange_peers();
+  // costs the 1F1B plan is simulated with: forward time units per stage (its layer count) and the
+  // head (LM head + loss + head backward) relative to one layer's forward FLOPs
+  host::PlanCost plan_cost() const;
+  // collective helpers over the world communicator (host doubles, summed)
+  std::vector<double> allreduce_host(const std::vector<double>& v);
+  double share_from_head(double v);
+  int replicas() const { return replicas_; }
+  int replica() const { return replica_; }
   std::vector<ParamGroup*> owned_groups();
   // 0 = sequential (forward+backward per microbatch, one live activation cache);
   // 1 = GPipe (all forwards, then all backwards in microbatch order: the ranks of
   //     a multi-GPU pipeline overlap; per-stage accumulation order is unchanged)
+  // 2 = 1F1B (plan-driven, host::pipeline_plan): per rank at most P microbatches in flight,
+  //     transfers on dedicated send / recv streams with one NCCL communicator per directed
+  //     link, overlapped with compute; per-stage accumulation still in microbatch order
   void set_schedule(int mode) {
-    if (mode != 0 && mode != 1) raise(1, "schedule must be 0 (sequential) or 1 (gpipe)");
+    if (mode < 0 || mode > 2) raise(1, "schedule must be 0 (sequential), 1 (gpipe) or 2 (1f1b)");
     schedule_ = mode;
   }
   int schedule() const { return schedule_; }
@@ -266,6 +313,21 @@ class Engine {
   std::vector<int> vrank_;
   std::vector<long> hop_log_;
   std::vector<int> stage_rank_;
+  // plan-driven (1F1B) executor: side streams, per-link communicators, event pool
+  void run_plan(const int* orders, int m, const char* x, size_t mb, size_t xrow);
+  void* link_comm(int src, int dst);
+  cudaEvent_t plan_event();
+  cudaStream_t sst_ = nullptr, rst_ = nullptr, dst_ = nullptr;  // send, recv, data-parallel streams
+  std::vector<std::pair<std::pair<int, int>, void*>> links_;    // (src, dst) -> ncclComm_t
+  std::vector<cudaEvent_t> pev_;
+  size_t pev_used_ = 0;
+ public:
+  // data-parallel gradient bucket ready (block calls it as each layer's weight gradients finish):
+  // the all-reduce of the replicas' sums runs on the data-parallel stream, overlapped with the
+  // remaining weight-gradient GEMMs
+  void grad_bucket_ready(void* g, size_t n);
+ private:
+  bool dp_pending_ = false;
   struct PeerStage {
     void *w = nullptr, *m = nullptr, *v = nullptr;
   };
@@ -303,5 +365,14 @@ std::unique_ptr<BlockImpl> make_llama_block(Engine* e);
 std::unique_ptr<BlockImpl> make_llama_f32_block(Engine* e);  // fp32 parity mode (llama_f32.cu)
 
 std::vector<Range> even_partition(size_t layers, size_t stages);
+
+// The failure-injected trainer (trainer.cu).  cm (optional): this process's place in a
+// multi-GPU run -- NCCL unique id, world size, rank, data-parallel replicas.
+struct TrainerComm {
+  const void* uid = nullptr;
+  int nranks = 1, rank = 0, replicas = 1;
+};
+std::string run_experiment(const std::string& kv, const std::string& trace_text, uint64_t seed,
+                           const std::string& dir, const TrainerComm* cm = nullptr);
 
 }  // namespace ckf

@@ -319,12 +319,42 @@ Trace Config::resolve_trace(uint64_t s) const {
 }
 
 // ------------------------------------------------------------------ pipeline plan
+int plan_inflight_limit(int m, const std::vector<int>& stage_rank) {
+  std::vector<int> r(stage_rank);
+  std::sort(r.begin(), r.end());
+  const int P = static_cast<int>(std::unique(r.begin(), r.end()) - r.begin());
+  return std::max(1, std::min(m, P));
+}
+
+namespace {
+// 1F1B list schedule.  A microbatch's route (embedding, its stages in execution order, head) is
+// cut into SEGMENTS: maximal runs of consecutive route positions on one rank.  The forward
+// segments run in route order; the segment holding the head also runs the loss and the head
+// backward; the backward segments walk the route back.  Each rank keeps two FIFO queues
+// (forward segments and backward segments, both ordered by microbatch then route position) and,
+// whenever it is idle, runs the head of its backward queue if that is ready, else the head of its
+// forward queue if that is ready and fewer than `limit` microbatches are in flight on the rank.
+// The earliest unfinished microbatch is always runnable (both queues are in microbatch order),
+// so the simulation cannot stall.  The segments and their transfers are then sorted by simulated
+// time (a transfer at its producer's finish time, before any segment starting at that time):
+// the result is a topological order of the iteration in which every rank's ops, and every
+// link's transfers, appear in the order that rank / link executes them.  Each rank issuing its
+// share of this one order onto in-order streams can therefore never deadlock, whatever the
+// real durations are.
+struct Seg {
+  int k, phase, rank, dep;
+  std::vector<PlanOp> ops;
+  double dur;
+  double start = -1, fin = -1;
+};
+}  // namespace
+
 std::vector<PlanOp> pipeline_plan(int s, int m, const std::vector<int>& orders, const std::vector<int>& stage_rank,
-                                  int schedule) {
+                                  int schedule, const PlanCost* cost, int limit) {
   if (s < 1 || m < 1) fail(1, "pipeline plan needs s >= 1 and m >= 1");
   if (orders.size() != static_cast<size_t>(s) * static_cast<size_t>(m)) fail(1, "orders must hold m*s stage ids");
   if (stage_rank.size() != static_cast<size_t>(s)) fail(1, "placement must name one rank per stage");
-  if (schedule != 0 && schedule != 1) fail(1, "schedule must be 0 (sequential) or 1 (gpipe)");
+  if (schedule < 0 || schedule > 2) fail(1, "schedule must be 0 (sequential), 1 (gpipe) or 2 (1f1b)");
   auto owner = [&](int code) {  // 0 embedding, 1..s stages, s+1 de-embedding
     const int sid = code <= 0 ? 1 : code > s ? s : code;
     return stage_rank[static_cast<size_t>(sid - 1)];
@@ -361,10 +391,160 @@ std::vector<PlanOp> pipeline_plan(int s, int m, const std::vector<int>& orders, 
       fwd(k);
       bwd(k);
     }
-  } else {
+    return ops;
+  }
+  if (schedule == 1) {
     for (int k = 0; k < m; ++k) fwd(k);
     for (int k = 0; k < m; ++k) bwd(k);
+    return ops;
   }
+
+  // ---- schedule 2: 1F1B list schedule
+  if (limit <= 0) limit = plan_inflight_limit(m, stage_rank);
+  auto scost = [&](int sid) {
+    return cost && cost->stage.size() == static_cast<size_t>(s) ? cost->stage[static_cast<size_t>(sid - 1)] : 1.0;
+  };
+  const double head_cost = cost ? cost->head : 1.0, embed_cost = cost ? cost->embed : 0.05;
+  int nranks = 0;
+  for (int r : stage_rank) nranks = std::max(nranks, r + 1);
+  std::vector<Seg> segs;
+  for (int k = 0; k < m; ++k) {
+    const int* o = orders.data() + static_cast<size_t>(k) * static_cast<size_t>(s);
+    // forward route: E, o[0..s-1], head
+    std::vector<int> route{0};
+    route.insert(route.end(), o, o + s);
+    route.push_back(s + 1);
+    int prev = -1;
+    for (size_t i = 0; i < route.size();) {
+      Seg g{k, 0, owner(route[i]), prev, {}, 0.0};
+      while (i < route.size() && owner(route[i]) == g.rank) {
+        const int c = route[i++];
+        if (c == 0) {
+          g.ops.push_back({0, k, PlanOp::kEmbedFwd, g.rank, 0, 0});
+          g.dur += embed_cost;
+        } else if (c == s + 1) {
+          g.ops.push_back({0, k, PlanOp::kHead, g.rank, 0, 0});
+          g.dur += 3.0 * head_cost;
+        } else {
+          g.ops.push_back({0, k, PlanOp::kStageFwd, g.rank, c, 0});
+          g.dur += scost(c);
+        }
+      }
+      segs.push_back(std::move(g));
+      prev = static_cast<int>(segs.size()) - 1;
+    }
+    // backward route: o[s-1..0], E
+    std::vector<int> broute(o, o + s);
+    std::reverse(broute.begin(), broute.end());
+    broute.push_back(0);
+    for (size_t i = 0; i < broute.size();) {
+      Seg g{k, 1, owner(broute[i]), prev, {}, 0.0};
+      while (i < broute.size() && owner(broute[i]) == g.rank) {
+        const int c = broute[i++];
+        if (c == 0) {
+          g.ops.push_back({1, k, PlanOp::kEmbedBwd, g.rank, 0, 0});
+          g.dur += embed_cost;
+        } else {
+          g.ops.push_back({1, k, PlanOp::kStageBwd, g.rank, c, 0});
+          g.dur += 2.0 * scost(c);
+        }
+      }
+      segs.push_back(std::move(g));
+      prev = static_cast<int>(segs.size()) - 1;
+    }
+  }
+  // per-rank FIFO queues (segments were appended in microbatch, then route order)
+  std::vector<std::vector<int>> qf(static_cast<size_t>(nranks)), qb(static_cast<size_t>(nranks));
+  std::vector<std::vector<int>> bleft(static_cast<size_t>(nranks), std::vector<int>(static_cast<size_t>(m), 0));
+  for (size_t i = 0; i < segs.size(); ++i) {
+    (segs[i].phase ? qb : qf)[static_cast<size_t>(segs[i].rank)].push_back(static_cast<int>(i));
+    if (segs[i].phase) ++bleft[static_cast<size_t>(segs[i].rank)][static_cast<size_t>(segs[i].k)];
+  }
+  std::vector<size_t> pf(static_cast<size_t>(nranks), 0), pb(static_cast<size_t>(nranks), 0);
+  std::vector<double> free_at(static_cast<size_t>(nranks), 0.0);
+  std::vector<std::vector<char>> started(static_cast<size_t>(nranks), std::vector<char>(static_cast<size_t>(m), 0));
+  std::vector<int> inflight(static_cast<size_t>(nranks), 0);
+  std::vector<int> busy(static_cast<size_t>(nranks), -1);  // segment running on the rank
+  size_t done = 0;
+  double t = 0.0;
+  auto ready = [&](int i) {
+    const int d = segs[static_cast<size_t>(i)].dep;
+    return d < 0 || (segs[static_cast<size_t>(d)].fin >= 0 && segs[static_cast<size_t>(d)].fin <= t);
+  };
+  while (done < segs.size()) {
+    // retire segments finishing by t
+    for (int r = 0; r < nranks; ++r) {
+      const int b = busy[static_cast<size_t>(r)];
+      if (b >= 0 && segs[static_cast<size_t>(b)].fin <= t) {
+        busy[static_cast<size_t>(r)] = -1;
+        ++done;
+        const Seg& g = segs[static_cast<size_t>(b)];
+        if (g.phase && --bleft[static_cast<size_t>(r)][static_cast<size_t>(g.k)] == 0) --inflight[static_cast<size_t>(r)];
+      }
+    }
+    bool progressed = false;
+    for (int r = 0; r < nranks; ++r) {
+      if (busy[static_cast<size_t>(r)] >= 0) continue;
+      const size_t ru = static_cast<size_t>(r);
+      int pick = -1;
+      if (pb[ru] < qb[ru].size() && ready(qb[ru][pb[ru]])) {
+        pick = qb[ru][pb[ru]++];
+      } else if (pf[ru] < qf[ru].size() && ready(qf[ru][pf[ru]])) {
+        const int c = qf[ru][pf[ru]];
+        const int k = segs[static_cast<size_t>(c)].k;
+        if (started[ru][static_cast<size_t>(k)] || inflight[ru] < limit) {
+          if (!started[ru][static_cast<size_t>(k)]) {
+            started[ru][static_cast<size_t>(k)] = 1;
+            if (bleft[ru][static_cast<size_t>(k)] > 0) ++inflight[ru];
+          }
+          pick = qf[ru][pf[ru]++];
+        }
+      }
+      if (pick < 0) continue;
+      Seg& g = segs[static_cast<size_t>(pick)];
+      g.start = t;
+      g.fin = t + std::max(g.dur, 1e-9);
+      busy[ru] = pick;
+      progressed = true;
+    }
+    // next event: the earliest running segment's finish
+    double nt = -1.0;
+    for (int r = 0; r < nranks; ++r) {
+      const int b = busy[static_cast<size_t>(r)];
+      if (b >= 0 && (nt < 0 || segs[static_cast<size_t>(b)].fin < nt)) nt = segs[static_cast<size_t>(b)].fin;
+    }
+    if (nt < 0) {
+      if (done < segs.size()) fail(1, "pipeline plan: 1F1B simulation stalled (internal error)");
+      break;
+    }
+    if (!progressed || nt > t) t = nt;
+  }
+  // flatten: segments at (start, 1, rank), transfers at (producer finish, 0, src)
+  struct Item {
+    double time;
+    int cls, rank;
+    size_t seq;
+    std::vector<PlanOp> ops;
+  };
+  std::vector<Item> items;
+  for (size_t i = 0; i < segs.size(); ++i) {
+    const Seg& g = segs[i];
+    items.push_back({g.start, 1, g.rank, i, g.ops});
+    // the transfer to the next segment of the same microbatch (if it runs on another rank)
+    for (size_t j = i + 1; j < segs.size() && segs[j].k == g.k; ++j) {
+      if (segs[j].dep != static_cast<int>(i)) continue;
+      if (segs[j].rank != g.rank) items.push_back({g.fin, 0, g.rank, i, {{segs[j].phase, g.k, PlanOp::kXfer, g.rank,
+                                                                          segs[j].rank, segs[j].phase}}});
+      break;
+    }
+  }
+  std::stable_sort(items.begin(), items.end(), [](const Item& a, const Item& b) {
+    if (a.time != b.time) return a.time < b.time;
+    if (a.cls != b.cls) return a.cls < b.cls;
+    if (a.rank != b.rank) return a.rank < b.rank;
+    return a.seq < b.seq;
+  });
+  for (auto& it : items) ops.insert(ops.end(), it.ops.begin(), it.ops.end());
   return ops;
 }
 

@@ -80,8 +80,21 @@ struct PlanOp {
   int arg;    // stage id (kStage*) or destination rank (kXfer)
   int aux;    // kXfer: 0 activations, 1 activation gradients
 };
+// schedule 2 = 1F1B: a list schedule simulated on the host (per rank: backward segments first,
+// forward and backward segments each in microbatch order, at most `limit` microbatches in
+// flight per rank) and flattened into ONE global order of ops and transfers that every rank
+// issues its share of (see pipeline_plan in host_logic.cpp).  cost: forward time units per
+// stage (index sid-1) and of the head (loss + head backward); the backward of a stage costs 2x.
+struct PlanCost {
+  std::vector<double> stage;
+  double head = 1.0;
+  double embed = 0.05;
+};
 std::vector<PlanOp> pipeline_plan(int s, int m, const std::vector<int>& orders, const std::vector<int>& stage_rank,
-                                  int schedule);
+                                  int schedule, const PlanCost* cost = nullptr, int limit = 0);
+// microbatches a rank can hold in flight under schedule 2 (activation cache slots): the number
+// of pipeline ranks, at most m
+int plan_inflight_limit(int m, const std::vector<int>& stage_rank);
 
 // ------------------------------------------------------------------ config
 struct Config {

@@ -260,6 +260,7 @@ struct LlamaBlock final : BlockImpl {
       gemm(di, di, R, w.o, di, true, w.dho, di, true, G + off.wo, di, tc::kAccF32);
       gemm(di, 2 * fi, R, w.xn2, di, true, w.dgu, 2 * fi, true, G + off.wgu, 2 * fi, tc::kAccF32);
       gemm(fi, di, R, w.a, fi, true, w.dhd, di, true, G + off.wd, di, tc::kAccF32);
+      eng->grad_bucket_ready(G, off.total);  // data parallel: this layer's all-reduce overlaps the next wgrads
     }
     pending_.clear();
   }
@@ -445,6 +446,145 @@ struct LlamaBlock final : BlockImpl {
       timed(KC_NORM, 0.0, Mt * d * 12.0, [&] {
         llama::embed_bwd(tok, Mt, dh, d, static_cast<float*>(eng->embed().g), sc, st);
       });
+    }
+  }
+
+  // ------------------------------------------------------------ plan-driven ops (schedule 2)
+  // Microbatch k owns h / dh / bf16(dh) buffers for the whole iteration (slot_id(k, 4/2/3)); its
+  // tokens and labels are split once per iteration; the activation caches rotate over `slots`
+  // (cache_for(k % slots, ...)), which the plan's in-flight limit makes safe.  Same kernels and
+  // arithmetic as mb_forward / mb_backward, one op of the global plan at a time.
+  bool supports_plan() const override { return true; }
+  int pslots_ = 1, pm_ = 0;
+  size_t prows_ = 0;
+  std::vector<bf16*> pcur_;  // per microbatch: where bf16(dh) currently lives
+  int* ptok_ = nullptr;
+  int* plab_ = nullptr;
+  void plan_begin(int m, size_t rows, int slots, const void* x) override {
+    pslots_ = std::max(1, slots);
+    pm_ = m;
+    prows_ = rows;
+    const size_t Mt = rows * T;
+    if (Mt > eng->desc().max_rows) raise(1, "microbatch tokens exceed the engine's max_rows (tokens per microbatch)");
+    pcur_.assign(static_cast<size_t>(m), nullptr);
+    ptok_ = buf<int>(57, static_cast<size_t>(m) * Mt);
+    plab_ = buf<int>(58, static_cast<size_t>(m) * Mt);
+    llama::split_tokens(static_cast<const int*>(x), static_cast<size_t>(m) * rows, T, ptok_, plab_, eng->stream());
+  }
+  float* ph(int k) { return buf<float>(slot_id(k, 4), prows_ * T * d); }
+  float* pdh(int k) { return buf<float>(slot_id(k, 2), prows_ * T * d); }
+  bf16* pdh_bf(int k) { return buf<bf16>(slot_id(k, 3), prows_ * T * d); }
+  void* plan_buffer(int k, int phase, size_t* bytes) override {
+    *bytes = prows_ * T * d * sizeof(float);
+    return phase == 0 ? static_cast<void*>(ph(k)) : static_cast<void*>(pdh(k));
+  }
+  void plan_received(int k, int phase) override {
+    if (phase != 1) return;
+    llama::f32_to_bf16(pdh(k), pdh_bf(k), prows_ * T * d, eng->stream());  // bf16(dh) for the next dgrad
+    pcur_[static_cast<size_t>(k)] = pdh_bf(k);
+  }
+  // position of stage sid's first layer in microbatch k's applied order
+  size_t applied_base(const int* order, int sid) const {
+    const Desc& D = eng->desc();
+    size_t a = 0;
+    for (size_t oi = 0; oi < D.s && order[oi] != sid; ++oi) a += D.part[static_cast<size_t>(order[oi] - 1)].count();
+    return a;
+  }
+  void plan_op(int kind, int k, int sid, const int* order, double* loss_dev) override {
+    cudaStream_t st = eng->stream();
+    const size_t rows = prows_, Mt = rows * T;
+    const int Mi = static_cast<int>(Mt), di = static_cast<int>(d), Vi = static_cast<int>(V);
+    const int* tok = ptok_ + static_cast<size_t>(k) * Mt;
+    const int* lab = plab_ + static_cast<size_t>(k) * Mt;
+    const int slot = k % pslots_;
+    wk = k;
+    switch (kind) {
+      case 0: {  // embedding (model.cpp:226)
+        float* h = ph(k);
+        timed(KC_NORM, 0.0, Mt * d * 8.0, [&] {
+          llama::embed_fwd(tok, Mt, static_cast<const float*>(eng->embed().w), d, h, st);
+        });
+        break;
+      }
+      case 1: {  // the stage's layers, forward (model.cpp:228-249)
+        float* h = ph(k);
+        const Range& r = eng->desc().part[static_cast<size_t>(sid - 1)];
+        const size_t a0 = applied_base(order, sid);
+        for (size_t li = 0; li < r.count(); ++li) {
+          const Cache c = cache_for(slot, a0 + li, Mt, rows, !defer_);
+          layer_fwd(sid, li, c, defer_ ? wset(sid, li, k) : wset_local(c, nullptr, Mt), h, rows, Mt);
+        }
+        break;
+      }
+      case 3: {  // head: loss + head backward (model.cpp:250-253, 322-342)
+        float* h = ph(k);
+        float* dh = pdh(k);
+        bf16* dh_bf = pdh_bf(k);
+        float* dxn = buf<float>(45, Mt * d);
+        const int nblk = llama::rmsnorm_bwd_blocks(Mt);
+        float* gpart = buf<float>(49, static_cast<size_t>(nblk) * d);
+        bf16* xnF = buf<bf16>(50, Mt * d);
+        float* rstdF = buf<float>(51, Mt);
+        float* hF = buf<float>(52, Mt * d);
+        bf16* logits = buf<bf16>(53, Mt * V);
+        double* row_loss = buf<double>(54, Mt);
+        const float* gF = static_cast<const float*>(eng->deembed().w);
+        const bf16* Einv = eng->deembed().wlp + d;
+        timed(KC_NORM, 0.0, Mt * d * 10.0, [&] { llama::rmsnorm_fwd(h, gF, Mt, d, xnF, rstdF, hF, st); });
+        gemm(Mi, Vi, di, xnF, di, false, Einv, Vi, true, logits, Vi, tc::kStoreBF16);
+        timed(KC_LOSS, 0.0, Mt * V * 6.0, [&] {
+          llama::xent_bf16(logits, lab, Mt, V, static_cast<float>(1.0 / static_cast<double>(Mt)), 1, row_loss, st);
+          llama::fold_mean(row_loss, Mt, 1.0 / static_cast<double>(Mt), loss_dev, st);
+        });
+        float* gde = static_cast<float*>(eng->deembed().g);
+        gemm(di, Vi, Mi, xnF, di, true, logits, Vi, true, gde + d, Vi, tc::kAccF32);
+        gemm(Mi, di, Vi, logits, Vi, false, Einv, Vi, false, dxn, di, tc::kStoreF32);
+        CKF_CUDA(cudaMemsetAsync(dh, 0, Mt * d * 4, st));
+        timed(KC_NORM, 0.0, Mt * d * 18.0, [&] {
+          llama::rmsnorm_bwd(dxn, hF, gF, rstdF, Mt, d, dh, dh_bf, gpart, st);
+          llama::gain_fold(gpart, nblk, d, gde, st);
+        });
+        pcur_[static_cast<size_t>(k)] = dh_bf;
+        break;
+      }
+      case 4: {  // the stage's layers, backward (model.cpp:343-372)
+        float* dh = pdh(k);
+        bf16* dh_bf = pdh_bf(k);
+        float* dxn = buf<float>(45, Mt * d);
+        bf16* scratch_bf = buf<bf16>(46, Mt * std::max(d, f));
+        float* Dsum = buf<float>(48, rows * H * T);
+        const int nblk = llama::rmsnorm_bwd_blocks(Mt);
+        float* gpart = buf<float>(49, static_cast<size_t>(nblk) * d);
+        const Range& r = eng->desc().part[static_cast<size_t>(sid - 1)];
+        const size_t a0 = applied_base(order, sid);
+        const std::vector<Applied> applied = applied_order(order);
+        bf16*& cur = pcur_[static_cast<size_t>(k)];
+        if (!cur) cur = dh_bf;
+        for (size_t li = r.count(); li-- > 0;) {
+          const size_t ai = a0 + li;
+          const Cache c = cache_for(slot, ai, Mt, rows, !defer_);
+          const WSet w = defer_ ? wset(sid, li, k) : wset_local(c, dh_bf, Mt);
+          if (cur != w.dhd) CKF_CUDA(cudaMemcpyAsync(w.dhd, cur, Mt * d * 2, cudaMemcpyDeviceToDevice, st));
+          // bf16(dh) after this layer goes straight to where the next applied layer reads it when
+          // that layer runs on this rank (the next op of this microbatch here)
+          bf16* out = dh_bf;
+          if (defer_ && ai > 0 && eng->mine(eng->owner_of_stage(applied[ai - 1].sid)))
+            out = wset(applied[ai - 1].sid, applied[ai - 1].li, k).dhd;
+          layer_bwd(sid, li, c, w, dh, out, dxn, scratch_bf, Dsum, gpart, nblk, rows, Mt);
+          cur = out;
+        }
+        break;
+      }
+      case 5: {  // embedding gradient (model.cpp:373-377)
+        void* sc = eng->ws(llama::embed_bwd_scratch(Mt), 55);
+        float* dh = pdh(k);
+        timed(KC_NORM, 0.0, Mt * d * 12.0, [&] {
+          llama::embed_bwd(tok, Mt, dh, d, static_cast<float*>(eng->embed().g), sc, st);
+        });
+        break;
+      }
+      default:
+        raise(1, "plan op kind not executable by the block");
     }
   }
 

@@ -58,10 +58,22 @@ struct Batch {
 
 class Trainer {
  public:
-  Trainer(const host::Config& c, const host::Trace& trace, uint64_t seed)
+  Trainer(const host::Config& c, const host::Trace& trace, uint64_t seed, const TrainerComm* cm = nullptr)
       : c_(c), seed_(seed), desc_(make_desc(c)), model_(desc_) {
     data_seed_ = host::derive_key(seed, kSeedTask);
     model_.init(host::derive_key(seed, kSeedModel), c.lr);
+    if (cm && cm->nranks > 1) {
+      // one process per GPU: contiguous stage blocks per pipeline rank (edges with stages 1 and s),
+      // `replicas` data-parallel copies; every rank runs this same loop (host logic replicated,
+      // losses / omegas / recovery reports shared by the engine), peer mappings for recovery
+      const int R = cm->replicas, P = cm->nranks / R;
+      if (c.microbatches % R) host::fail(1, "microbatches must be divisible by the data-parallel replicas");
+      if (c.batch % static_cast<size_t>(R)) host::fail(1, "batch must be divisible by the data-parallel replicas");
+      std::vector<int> sr(c.stages);
+      for (size_t i = 0; i < c.stages; ++i) sr[i] = static_cast<int>(i * static_cast<size_t>(P) / c.stages);
+      model_.attach_comm(cm->uid, cm->nranks, cm->rank, sr.data(), R);
+      model_.exchange_peers();
+    }
     if (desc_.block == CKF_BLOCK_MLP) {
       teacher_ = std::make_unique<Engine>(desc_);
       teacher_->init(host::derive_key(data_seed_, kStreamTeacher), 1.0);
@@ -97,8 +109,15 @@ class Trainer {
       const bool swap_now = !sw_sched_.empty() && slot > c_.swap_from;
       Batch b = make_batch(kStreamTrain, static_cast<uint64_t>(model_iter_ + 1), c_.batch, 22);
       std::vector<double> om(c_.stages);
-      model_.run_iteration(swap_now ? sw_sched_.data() : std_sched_.data(), c_.microbatches, b.x, b.y, b.rows,
-                           true, slot, &last_train_, om.data());
+      // data parallel: replica r trains on microbatches [r m/R, (r+1) m/R) of the global batch with
+      // their global execution orders (the mean over all m is restored by the all-reduce)
+      const int R = model_.replicas(), rr = model_.replica();
+      const int ml = c_.microbatches / R;
+      const size_t rows_l = b.rows / static_cast<size_t>(R);
+      const int* sched = (swap_now ? sw_sched_.data() : std_sched_.data()) + static_cast<size_t>(rr * ml) * c_.stages;
+      model_.run_iteration(sched, ml, row_ptr(b.x, rows_l * static_cast<size_t>(rr), true),
+                           row_ptr(b.y, rows_l * static_cast<size_t>(rr), false), rows_l, true, slot, &last_train_,
+                           om.data());
       ++model_iter_;
       if (cfp) model_.refresh_edge_replicas();
       if (ckpt && model_iter_ % c_.checkpoint_interval == 0) model_.checkpoint_save(model_iter_);  // trainer.cpp:83-85
@@ -155,6 +174,16 @@ class Trainer {
     b.x = x;
     CKF_CUDA(cudaDeviceSynchronize());
     return b;
+  }
+
+  // pointer to row r of a batch buffer (x: tokens / inputs, else targets / labels)
+  const void* row_ptr(const void* p, size_t r, bool is_x) const {
+    if (!p || r == 0) return p;
+    size_t bytes;
+    if (desc_.block == CKF_BLOCK_LLAMA) bytes = (c_.seq_len + 1) * sizeof(int);
+    else if (is_x) bytes = c_.input_dim * model_.master_bytes();
+    else bytes = c_.task == "regression" ? c_.output_dim * model_.master_bytes() : sizeof(int);
+    return static_cast<const char*>(p) + r * bytes;
   }
 
   double eval(const Batch& b, const std::vector<int>& order) { return model_.eval_loss(order.data(), b.x, b.y, b.rows, true); }
@@ -354,12 +383,12 @@ void write_records(const host::Config& c, uint64_t seed, const std::string& rec,
 }  // namespace
 
 std::string run_experiment(const std::string& kv, const std::string& trace_text, uint64_t seed,
-                           const std::string& dir) {
+                           const std::string& dir, const TrainerComm* cm) {
   host::Config c = host::Config::from_kv(kv);
   c.validate();
   host::Trace t = trace_text.empty() ? c.resolve_trace(seed) : host::parse_trace(trace_text);
   host::validate_trace(t);
-  Trainer tr(c, t, seed);
+  Trainer tr(c, t, seed, cm);
   std::string rec = tr.run();
   if (!dir.empty()) write_records(c, seed, rec, dir);
   return rec;

@@ -19,12 +19,23 @@ import torch.distributed as dist  # noqa: E402
 import torch.multiprocessing as mp  # noqa: E402
 
 CASES = [
-    # (stages, microbatches, swapped_half, placement, schedule)
+    # (stages, microbatches, swapped_half, placement, schedule); schedule 2 = 1F1B
     (4, 4, False, [0, 0, 1, 1], 1),
     (4, 4, True, [0, 0, 1, 1], 1),
     (4, 4, True, [0, 0, 1, 1], 0),
     (8, 6, True, [0, 0, 0, 0, 1, 1, 1, 1], 1),
     (8, 2, False, [0, 0, 0, 0, 1, 1, 1, 1], 0),
+    (4, 8, False, [0, 0, 1, 1], 2),
+    (4, 8, True, [0, 0, 1, 1], 2),
+    (8, 16, True, [0, 0, 0, 0, 1, 1, 1, 1], 2),
+    (4, 6, True, [0, 1, 0, 1], 2),  # interleaved placement: every route crosses the link 3x each way
+]
+# 4 ranks: one stage per rank (the swapped first/last-stage routes go 0 -> 1 -> 0 -> 2 -> 3 -> 2 -> 3)
+CASES4 = [
+    (4, 8, True, [0, 1, 2, 3], 2),
+    (4, 8, False, [0, 1, 2, 3], 2),
+    (8, 8, True, [0, 0, 1, 1, 2, 2, 3, 3], 2),
+    (4, 4, True, [0, 1, 2, 3], 1),
 ]
 N = 64  # toy activation width
 
@@ -85,12 +96,12 @@ def _inputs(s, m):
     return xs, ts, params
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, cases):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2506_15461_b200 import api
     results = []
-    for (s, m, swapped, placement, schedule) in CASES:
+    for (s, m, swapped, placement, schedule) in cases:
         plan = api.pipeline_plan(api.build_schedule(m, swapped, s), placement, schedule)
         xs, ts, params = _inputs(s, m)
 
@@ -116,19 +127,20 @@ def _worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
-def test_two_gloo_ranks_match_single_rank_bit_exactly():
+@pytest.mark.parametrize("world,cases", [(2, CASES), (4, CASES4)])
+def test_gloo_ranks_match_single_rank_bit_exactly(world, cases):
     from paper_2506_15461_b200 import api
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, cases)) for r in range(world)]
     for p in procs:
         p.start()
     got = q.get(timeout=240)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    for (s, m, swapped, placement, schedule), (tw, ls, nx) in zip(CASES, got):
+    for (s, m, swapped, placement, schedule), (tw, ls, nx) in zip(cases, got):
         plan1 = api.pipeline_plan(api.build_schedule(m, swapped, s), [0] * s, schedule)
         assert not any(op["kind"] == "xfer" for op in plan1)
         xs, ts, params = _inputs(s, m)
@@ -162,3 +174,63 @@ def test_plan_structure():
         for sid in range(1, 5):
             mbs = [op["mb"] for op in plan if op["kind"] == "stage_bwd" and op["arg"] == sid]
             assert mbs == sorted(mbs)
+
+
+def _check_1f1b(plan, orders, placement, m):
+    """Structure of a schedule-2 plan: a topological order of the iteration; on every rank the
+    stage backwards of each stage run in microbatch order (the reference's accumulation order)
+    and at most `limit` microbatches are in flight; every transfer joins consecutive ops of one
+    microbatch on different ranks."""
+    from paper_2506_15461_b200 import api
+    s = len(placement)
+    limit = min(m, len(set(placement)))
+    done = set()
+    inflight = {r: set() for r in set(placement)}
+    bwd_left = {}
+    for r in set(placement):
+        for k in range(m):
+            bwd_left[(r, k)] = sum(1 for sid in orders[k] if placement[sid - 1] == r) + (1 if r == placement[0] else 0)
+    last_bwd = {}
+    for op in plan:
+        k, kind = op["mb"], op["kind"]
+        if kind == "xfer":
+            continue
+        r = op["rank"]
+        # dependencies: forward route order, then head, then backward route order
+        if kind == "stage_fwd":
+            i = orders[k].index(op["arg"])
+            assert ((k, "stage_fwd", orders[k][i - 1]) if i else (k, "embed_fwd", 0)) in done
+        elif kind == "head":
+            assert (k, "stage_fwd", orders[k][-1]) in done
+        elif kind == "stage_bwd":
+            i = orders[k].index(op["arg"])
+            assert ((k, "stage_bwd", orders[k][i + 1]) if i < s - 1 else (k, "head", 0)) in done
+            assert last_bwd.get(op["arg"], -1) < k  # per-stage accumulation in microbatch order
+            last_bwd[op["arg"]] = k
+        elif kind == "embed_bwd":
+            assert (k, "stage_bwd", orders[k][0]) in done
+        if kind in ("embed_fwd", "stage_fwd") and kind != "head":
+            inflight[r].add(k)
+            assert len(inflight[r]) <= limit, (r, inflight[r])
+        if kind in ("stage_bwd", "embed_bwd"):
+            bwd_left[(r, k)] -= 1
+            if bwd_left[(r, k)] == 0:
+                inflight[r].discard(k)
+        done.add((k, kind, op["arg"] if kind.startswith("stage") else 0))
+    assert len(done) == m * (2 * s + 3)
+
+
+@pytest.mark.parametrize("s,m,placement", [(4, 8, [0, 0, 1, 1]), (8, 16, [0, 1, 2, 3, 4, 5, 6, 7]),
+                                           (8, 64, [0, 1, 2, 3, 4, 5, 6, 7]), (4, 8, [0, 1, 2, 3]),
+                                           (8, 12, [0, 0, 1, 1, 2, 2, 3, 3]), (4, 6, [0, 1, 0, 1])])
+@pytest.mark.parametrize("swapped", [False, True])
+def test_1f1b_plan_structure(s, m, placement, swapped):
+    from paper_2506_15461_b200 import api
+    orders = api.build_schedule(m, swapped, s)
+    plan = api.pipeline_plan(orders, placement, 2)
+    _check_1f1b(plan, orders, placement, m)
+    # the same transfers as GPipe (one per stage boundary crossing per direction), in another order
+    x2 = sorted((o["mb"], o["rank"], o["arg"], o["aux"]) for o in plan if o["kind"] == "xfer")
+    x1 = sorted((o["mb"], o["rank"], o["arg"], o["aux"]) for o in api.pipeline_plan(orders, placement, 1)
+                if o["kind"] == "xfer")
+    assert x1 == x2
