@@ -1,0 +1,85 @@
+#!/usr/bin/env python
+"""Tensor-pipe evidence for the tcgen05 kernels: ONE launch of every GEMM family of the
+LLaMA-500M step (65,536 tokens; d=1024, f=4096, V=50,304) and of both attention kernels,
+bracketed by cudaProfilerStart/Stop so that
+
+    ncu --profile-from-start off --metrics <tensor metrics> python tools/tensor_counter.py
+
+captures exactly those launches (warm-ups outside the range).  The algorithmic FLOPs of each
+launch (2 M N K; causal attention 2 B H T^2 hd forward, 2.5x that backward) are written to
+gpurun_out/tensor_flops.json in launch order; tools/tensor_table.py joins the two."""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2506_15461_b200  # noqa: E402,F401
+from paper_2506_15461_b200._native import check, lib  # noqa: E402
+
+T_ = 65536
+d, f, V = 1024, 4096, 50304
+SHAPES = [  # (name, M, N, K, a_mn, b_mn, epi)
+    ("qkv_fwd", T_, 3 * d, d, 0, 1, 0), ("o_fwd", T_, d, d, 0, 1, 2), ("gu_fwd_swiglu", T_, 2 * f, d, 0, 1, 3),
+    ("down_fwd", T_, d, f, 0, 1, 2), ("down_dgrad_swiglu", T_, f, d, 0, 0, 4), ("gu_dgrad", T_, d, 2 * f, 0, 0, 1),
+    ("o_dgrad", T_, d, d, 0, 0, 0), ("qkv_dgrad", T_, d, 3 * d, 0, 0, 1),
+    ("qkv_wgrad", d, 3 * d, T_, 1, 1, 2), ("o_wgrad", d, d, T_, 1, 1, 2), ("gu_wgrad", d, 2 * f, T_, 1, 1, 2),
+    ("down_wgrad", f, d, T_, 1, 1, 2),
+    ("lmhead_fwd", T_, V, d, 0, 1, 0), ("lmhead_dgrad", T_, d, V, 0, 0, 1), ("lmhead_wgrad", d, V, T_, 1, 1, 2),
+]
+ATTN = [(64, 1024, 16, 64), (16, 4096, 16, 128)]
+
+
+def gemm_call(M, N, K, a_mn, b_mn, epi):
+    A = torch.randn((K, M) if a_mn else (M, K), device="cuda").bfloat16()
+    B = (torch.randn((K, N) if b_mn else (N, K), device="cuda") * 0.05).bfloat16()
+    cw = 2 * N if epi == 4 else N
+    C = torch.zeros((M, cw), device="cuda", dtype=torch.bfloat16 if epi in (0, 3, 4) else torch.float32)
+    aux = (torch.zeros((M, N // 2), device="cuda", dtype=torch.bfloat16) if epi == 3 else
+           torch.randn((M, 2 * N), device="cuda").bfloat16() if epi == 4 else None)
+    keep = (A, B, C, aux)
+    return keep, lambda: check(lib().ckf_gemm_bf16_aux(
+        M, N, K, A.data_ptr(), A.shape[1], a_mn, B.data_ptr(), B.shape[1], b_mn, C.data_ptr(), cw, epi, 1.0, 0,
+        aux.data_ptr() if aux is not None else None, aux.shape[1] if aux is not None else 0, None))
+
+
+def main():
+    launches, calls, keep = [], [], []
+    for (name, M, N, K, a_mn, b_mn, epi) in SHAPES:
+        k, fn = gemm_call(M, N, K, a_mn, b_mn, epi)
+        keep.append(k)
+        calls.append(fn)
+        launches.append({"name": name, "kernel": "gemm", "flops": 2.0 * M * N * K, "M": M, "N": N, "K": K})
+    for (B, T, H, hd) in ATTN:
+        qkv = torch.randn(B * T, 3 * H * hd, device="cuda").bfloat16()
+        o = torch.empty(B * T, H * hd, dtype=torch.bfloat16, device="cuda")
+        lse = torch.empty(B * H * T, device="cuda")
+        dout = torch.randn(B * T, H * hd, device="cuda").bfloat16()
+        dqkv = torch.empty_like(qkv)
+        D = torch.empty(B * H * T, device="cuda")
+        keep.append((qkv, o, lse, dout, dqkv, D))
+        fl = 2.0 * B * H * T * T * hd
+        calls.append(lambda qkv=qkv, o=o, lse=lse, B=B, T=T, H=H, hd=hd: check(lib().ckf_attention_fwd(
+            qkv.data_ptr(), B, T, H, hd, o.data_ptr(), lse.data_ptr(), 2, None)))
+        launches.append({"name": f"attn_fwd_hd{hd}", "kernel": "attn_fwd", "flops": fl, "shape": [B, T, H, hd]})
+        calls.append(lambda qkv=qkv, o=o, lse=lse, dout=dout, dqkv=dqkv, D=D, B=B, T=T, H=H, hd=hd: check(
+            lib().ckf_attention_bwd(qkv.data_ptr(), o.data_ptr(), lse.data_ptr(), dout.data_ptr(), B, T, H, hd,
+                                    dqkv.data_ptr(), D.data_ptr(), 0, None)))
+        launches.append({"name": f"attn_bwd_hd{hd}", "kernel": "attn_bwd (dsum + dK/dV + dQ)", "flops": 2.5 * fl,
+                         "shape": [B, T, H, hd]})
+    for fn in calls:  # warm-up outside the profiled range (TMA descriptors, tables, first-touch)
+        fn()
+    torch.cuda.synchronize()
+    torch.cuda.cudart().cudaProfilerStart()
+    for fn in calls:
+        fn()
+    torch.cuda.synchronize()
+    torch.cuda.cudart().cudaProfilerStop()
+    os.makedirs("gpurun_out", exist_ok=True)
+    with open("gpurun_out/tensor_flops.json", "w") as fh:
+        json.dump(launches, fh, indent=1)
+
+
+if __name__ == "__main__":
+    main()
