@@ -158,6 +158,11 @@ def trainer_goldens():
         ("checkfree_plus_swap_from_40", {"strategy": "checkfree-plus", "swap-from": 40}, trace_text(1, [1, 2, 3, 4], [(60, 1)])),
         ("s8_checkfree_plus_trace", {"strategy": "checkfree-plus", "layers": 8, "stages": 8, "iters": 60,
                                      "eval-interval": 5}, None),
+        # redundant-computation baseline (trainer.cpp:162-171): the hot copy survives, state untouched
+        ("redundant_s2_at50", {"strategy": "redundant"}, trace_text(1, [2, 3], [(50, 2)])),
+        ("redundant_edges_and_middle", {"strategy": "redundant", "eligible": "all"},
+         trace_text(1, [1, 2, 3, 4], [(20, 1), (45, 4), (45, 2), (70, 3)])),
+        ("redundant_adjacent_unrecoverable", {"strategy": "redundant"}, trace_text(1, [2, 3], [(30, 2), (30, 3)])),
         # checkpointing baseline (trainer.cpp:173-193, checkpoint.cpp:70-83): rollback + data replay
         ("checkpointing_s2_at50", {"strategy": "checkpointing", "checkpoint-interval": 20},
          trace_text(1, [1, 2, 3, 4], [(50, 2)])),

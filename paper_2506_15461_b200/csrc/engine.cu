@@ -421,8 +421,12 @@ void Engine::run_plan(const int* orders, int m, const char* x, size_t mb, size_t
   std::vector<cudaEvent_t> sent(static_cast<size_t>(m) * 2, nullptr);     // last send of the buffer
   bool any_send = false, any_recv = false;
   (void)xrow;
+  static const char* kNames[] = {"ckf.plan.embed_fwd", "ckf.plan.stage_fwd", "ckf.plan.xfer", "ckf.plan.head",
+                                 "ckf.plan.stage_bwd", "ckf.plan.embed_bwd"};
   for (const auto& op : plan) {
     const int k = op.mb;
+    if (!virt && op.kind != host::PlanOp::kXfer && op.rank != rank_) continue;
+    NvtxRange nv(kNames[op.kind]);
     if (op.kind == host::PlanOp::kXfer) {
       size_t bytes = 0;
       void* b = impl_->plan_buffer(k, op.aux, &bytes);
@@ -531,6 +535,7 @@ void Engine::ipc_import(const void* buf, size_t len) {
 
 void Engine::hop(void* buf, size_t bytes, int src, int dst) {
   if (src == dst || bytes == 0) return;
+  NvtxRange nv("ckf.hop");
   if (rank_ == src) nccl_check(nccl().Send(buf, bytes, /*ncclInt8*/ 0, dst, comm_, st_), "ncclSend");
   if (rank_ == dst) nccl_check(nccl().Recv(buf, bytes, /*ncclInt8*/ 0, src, comm_, st_), "ncclRecv");
 }
@@ -650,6 +655,7 @@ int Engine::fused_group_size(int m, size_t mb_rows) {
 
 void Engine::run_iteration(const int* orders, int m, const void* x, const void* y, size_t rows, bool on_device,
                            long iteration, double* loss, double* omegas) {
+  NvtxRange nv_it("ckf.run_iteration");
   CKF_CUDA(cudaSetDevice(d_.device));
   if (m < 1) raise(1, "microbatch count must be positive");
   if (rows == 0 || rows % static_cast<size_t>(m) != 0)
@@ -759,12 +765,19 @@ void Engine::run_iteration(const int* orders, int m, const void* x, const void* 
         xg = gb;
       }
       impl_->wk = woff;
-      impl_->mb_forward(0, ok(g[0]), xg, nullptr, g.size() * mb, true, scal_ + j);
-      impl_->mb_backward(0, ok(g[0]), xg, g.size() * mb);
+      {
+        NvtxRange nv("ckf.group.fwd");
+        impl_->mb_forward(0, ok(g[0]), xg, nullptr, g.size() * mb, true, scal_ + j);
+      }
+      {
+        NvtxRange nv("ckf.group.bwd");
+        impl_->mb_backward(0, ok(g[0]), xg, g.size() * mb);
+      }
       if (redundant_) impl_->redundant_forward(ok(g[0]), xg, g.size() * mb);
       woff += static_cast<int>(g.size());
     }
     impl_->loss_rows = 0;
+    NvtxRange nv("ckf.wgrad_pass");
     impl_->flush_grads();
     };
     // The fused step is a fixed launch sequence: after one eager pass with the same shape,
@@ -860,6 +873,7 @@ void Engine::run_iteration(const int* orders, int m, const void* x, const void* 
   // mean loss in microbatch order, then *1/m (model.cpp:299-312, pipeline.cpp:82-83)
   std::vector<double> losses(nloss);
   const double inv = 1.0 / (static_cast<double>(m) * replicas_);
+  NvtxRange nv_adam("ckf.adam_omega");
   for (size_t i = 0; i < d_.s; ++i) adam_group(stages_[i], stages_[i].lr, inv, scal_ + 2048 + i);
   adam_group(embed_, edge_lr, inv, scal_ + 3000);
   adam_group(deembed_, edge_lr, inv, scal_ + 3001);
@@ -1218,6 +1232,7 @@ void Engine::kill_stage(int sid) {
 // ------------------------------------------------------------------ recovery
 ckf_recovery_report Engine::recover_stage(int sid, int mode, int moments, double lr_bump, uint64_t reinit_seed,
                                           bool want_red) {
+  NvtxRange nv_rec("ckf.recover_stage");
   CKF_CUDA(cudaSetDevice(d_.device));
   const int s = static_cast<int>(d_.s);
   if (sid < 1 || sid > s) raise(1, "stage id out of range");

@@ -21,7 +21,19 @@
 #include "host_logic.h"
 #include "kernels.h"
 
+#include <nvtx3/nvToolsExt.h>
+
 namespace ckf {
+
+// NVTX range over a scope (iteration, microbatch group, plan op, transfer, recovery, optimizer):
+// nsys / ncu --nvtx timelines show the pipeline structure.  Header-only NVTX3; a no-op unless a
+// tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 struct Range {
   size_t first = 0, last = 0;  // 1-based inclusive (model.hpp:24-28)

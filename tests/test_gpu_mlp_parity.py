@@ -155,7 +155,8 @@ TRAINER_CASES = ["checkfree_s2_at50", "checkfree_plus_s1_at50", "checkfree_plus_
                  "reinit_random", "no_failures", "unrecoverable_adjacent", "checkfree_edge_unsupported",
                  "classification_checkfree", "relu_checkfree_plus", "failure_at_iter1", "checkfree_plus_swap_from_40",
                  "s8_checkfree_plus_trace", "checkpointing_s2_at50", "checkpointing_edge_and_adjacent",
-                 "checkpointing_at_snapshot"]
+                 "checkpointing_at_snapshot", "redundant_s2_at50", "redundant_edges_and_middle",
+                 "redundant_adjacent_unrecoverable"]
 
 
 @pytest.mark.parametrize("name", TRAINER_CASES)
