@@ -13,10 +13,16 @@ def main():
     path = sys.argv[1]
     rows = [r for r in csv.reader(open(path)) if len(r) > 10 and r[0] != "ID"]
     if "--window" in sys.argv:
+        # MARKER[:N]: from the first launch whose name contains MARKER to its N-th next occurrence
+        # (N = launches of MARKER per step, e.g. 2 head-loss launches per CheckFree+ step)
         mk = sys.argv[sys.argv.index("--window") + 1]
+        n = 1
+        if ":" in mk:
+            mk, n = mk.rsplit(":", 1)
+            n = int(n)
         idx = [i for i, r in enumerate(rows) if mk in r[4]]
-        if len(idx) >= 2:
-            rows = rows[idx[0]:idx[1]]
+        if len(idx) >= n + 1:
+            rows = rows[idx[0]:idx[n]]
     tot = collections.OrderedDict()
     for r in rows:
         name = re.sub(r"\(.*", "", r[4]).replace("void ", "")

@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """DRAM traffic per GEMM launch from an ncu CSV capture
 (--metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum), written to
-profiles/r01_gemm_dram_traffic.json for bench.py's roofline.traffic.
+profiles/r0N_<workload>_gemm_dram_traffic.json for bench.py's roofline.traffic.
 Usage: ncu_traffic.py capture.csv out.json "<command that produced it>" """
 import csv, json, sys, re, collections
 
