@@ -59,6 +59,13 @@ __device__ __forceinline__ uint32_t kmajor_k(uint32_t base, int rows, int k) {
 constexpr int FK = 64;
 constexpr uint32_t kPTile = TQ * FK * 2;  // 16 KiB: P [128 rows][128 B]
 constexpr float kRescale = 8.f;
+constexpr int kFwdPolyDefault = 0;
+// per-tile clock instrumentation of the forward (tools/attn_debug.py): compiled in only with
+// -DCKF_ATTN_DEBUG_BUILD=1 (and CKF_ATTN_DEBUG=1 at run time), so the hot loop carries none of it
+#ifndef CKF_ATTN_DEBUG_BUILD
+#define CKF_ATTN_DEBUG_BUILD 0
+#endif
+constexpr bool kDbg = CKF_ATTN_DEBUG_BUILD != 0;  // exponential pairs (of 8) on the FMA pipe, forward
 
 template <int HD>
 struct FwdCfg {
@@ -83,7 +90,9 @@ struct Smem {
 
 __device__ __forceinline__ void tmem_st32_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-template <int HD>
+// POLY: of every 8 exponential pairs of a softmax row chunk, POLY run on the FMA pipe
+// (ex2_fma2), the rest on MUFU (CKF_ATTN_POLY selects; 0 = all MUFU)
+template <int HD, int POLY>
 __global__ void __launch_bounds__(kThreads, FwdCfg<HD>::kMinBlocks)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_kv,
                        int T, int H, __nv_bfloat16* __restrict__ o, float* __restrict__ lse, float scale_log2,
@@ -165,9 +174,18 @@ __global__ void __launch_bounds__(kThreads, FwdCfg<HD>::kMinBlocks)
         umma_commit(&sm.s_full[sb]);
         umma_commit(&sm.k_empty[ks]);
       };
+      // S runs two tiles ahead of the softmax: S_{j+2} goes into S_j's TMEM buffer as soon as the
+      // softmax warps have loaded S_j (early in their tile j), ahead of P_j V_j, so the next S is
+      // ready when the softmax finishes a tile instead of queueing behind P V
+      // (head_dim 64, three V stages; at head_dim 128 the two V stages would make S_{j+2} wait for
+      // K_{j+2}, which the producer loads only after P_{j-1} V_{j-1} freed a V stage -- there S_{j+1}
+      // is issued one tile ahead, before P_j V_j)
+      constexpr bool kEarly = HD == 64;
       issue_s(0);
+      if (kEarly && nkb > 1) issue_s(1);
       for (int j = 0; j < nkb; ++j) {
-        if (j + 1 < nkb) issue_s(j + 1);
+        if (kEarly && j + 2 < nkb) issue_s(j + 2);
+        if (!kEarly && j + 1 < nkb) issue_s(j + 1);
         const int pb = j & 1, vs = j % VS;
         mbar_wait(&sm.v_full[vs], (j / VS) & 1);
         mbar_wait(&sm.p_full[pb], (j >> 1) & 1);
@@ -191,9 +209,9 @@ __global__ void __launch_bounds__(kThreads, FwdCfg<HD>::kMinBlocks)
     long long w_s = 0, w_p = 0, t_first = 0;
     for (int j = 0; j < nkb; ++j) {
       const int sb = j & 1, pb = j & 1;
-      const long long t0 = dbg ? clock64() : 0;
+      const long long t0 = (kDbg && dbg) ? clock64() : 0;
       mbar_wait(&sm.s_full[sb], (j >> 1) & 1);
-      if (dbg) {  // CKF_ATTN_DEBUG timings only
+      if (kDbg && dbg) {  // CKF_ATTN_DEBUG timings only
         const long long t1 = clock64();
         if (j == 0) t_first = t1 - t_start;
         w_s += t1 - t0;
@@ -220,9 +238,16 @@ __global__ void __launch_bounds__(kThreads, FwdCfg<HD>::kMinBlocks)
 #pragma unroll
           for (int t = 0; t < 32; t += 2) {
             const int tt = hf * 32 + t;
-            float x0, x1;
-            f2split(ffma2(f2(__uint_as_float(u[tt]), __uint_as_float(u[tt + 1])), sc2, nm2), x0, x1);
-            float p0 = ex2(x0), p1 = ex2(x1);
+            const f32x2 xx = ffma2(f2(__uint_as_float(u[tt]), __uint_as_float(u[tt + 1])), sc2, nm2);
+            float p0, p1;
+            if ((t >> 1) % 8 < POLY) {
+              f2split(ex2_fma2(xx), p0, p1);
+            } else {
+              float x0, x1;
+              f2split(xx, x0, x1);
+              p0 = ex2(x0);
+              p1 = ex2(x1);
+            }
             if (nvalid < FK) {
               p0 = tt < nvalid ? p0 : 0.f;
               p1 = tt + 1 < nvalid ? p1 : 0.f;
@@ -240,9 +265,9 @@ __global__ void __launch_bounds__(kThreads, FwdCfg<HD>::kMinBlocks)
         }
         return lt;
       };
-      const long long t2 = dbg ? clock64() : 0;
+      const long long t2 = (kDbg && dbg) ? clock64() : 0;
       mbar_wait(&sm.p_free[pb], ((j >> 1) & 1) ^ 1);  // P V_{j-2} has read this P buffer
-      if (dbg) w_p += clock64() - t2;
+      if (kDbg && dbg) w_p += clock64() - t2;
       // Fast path (every tile after the first): P against the running max m with no max pass;
       // kept when the tile's row sum stays <= 2^16 (so every P <= 2^16, finite).  Otherwise --
       // a score above m + 16 in log2 units, or the first tile -- the tile is redone against its
@@ -318,7 +343,7 @@ __global__ void __launch_bounds__(kThreads, FwdCfg<HD>::kMinBlocks)
       }
     }
     lse[static_cast<size_t>(bh) * T + q] = (m + log2f(l)) * kLn2;
-    if (dbg && threadIdx.x == 128) {
+    if (kDbg && dbg && threadIdx.x == 128) {
       long long* d = dbg + 8 * (blockIdx.y * gridDim.x + blockIdx.x);
       d[0] = nkb;
       d[1] = t_first;
@@ -900,17 +925,23 @@ void fwd_launch(const bf16* qkv, size_t B, size_t T, size_t H, bf16* o, float* l
   const CUtensorMap tm = tma::make_2d_bf16(qkv, 3 * H * HD, B * T, 3 * H * HD, 64, 128);
   const CUtensorMap tkv = tma::make_2d_bf16(qkv, 3 * H * HD, B * T, 3 * H * HD, 64, FK);
   const size_t smem = sizeof(Smem<HD>) + 1024;
+  static const int poly = [] {
+    const char* v = std::getenv("CKF_ATTN_POLY");
+    return v ? std::atoi(v) : (HD == 64 ? kFwdPolyDefault : 0);
+  }();
+  auto kern = poly >= 4 ? attn_fwd_tc_kernel<HD, 4>
+              : poly == 3 ? attn_fwd_tc_kernel<HD, 3>
+              : poly == 2 ? attn_fwd_tc_kernel<HD, 2>
+              : poly == 1 ? attn_fwd_tc_kernel<HD, 1> : attn_fwd_tc_kernel<HD, 0>;
   static bool attr = false;
   if (!attr) {
-    CKF_CUDA(cudaFuncSetAttribute(attn_fwd_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
+    CKF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     attr = true;
   }
   const float scale_log2 = kLog2e / sqrtf(static_cast<float>(HD));
   dim3 grid(static_cast<unsigned>(T / TQ), static_cast<unsigned>(B * H));
   long long* dbg = attn_fwd_debug_buffer();
-  attn_fwd_tc_kernel<HD><<<grid, kThreads, smem, s>>>(tm, tkv, static_cast<int>(T), static_cast<int>(H), o, lse,
-                                                      scale_log2, dbg);
+  kern<<<grid, kThreads, smem, s>>>(tm, tkv, static_cast<int>(T), static_cast<int>(H), o, lse, scale_log2, dbg);
   CKF_LAUNCH_CHECK();
 }
 

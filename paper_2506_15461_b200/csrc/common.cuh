@@ -101,6 +101,31 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
   return d;
 }
 
+// 2^x for a pair on the FMA / ALU pipes -- the MUFU offload of FlashAttention-4: the softmax of
+// a head_dim-64 tile needs one exponential per 256 MMA FLOPs, which at 16 MUFU results / clk / SM
+// caps the tensor pipe near half of its peak, while the issue slots have room.  x = j + f with
+// j = rint(x) (the 1.5 * 2^23 trick), 2^f by a degree-3 minimax polynomial on [-0.5, 0.5]
+// (relative error 7.5e-5, below a bf16 half-ulp of 2e-3), 2^j added into the exponent field.
+// x is clamped at -125 (the result is then ~2^-125, zero for a bf16 probability).
+__device__ __forceinline__ f32x2 ex2_fma2(f32x2 x) {
+  float a, b;
+  f2split(x, a, b);
+  const f32x2 xc = f2(fmaxf(a, -125.f), fmaxf(b, -125.f));
+  const f32x2 t = fadd2(xc, f2(12582912.f, 12582912.f));  // low mantissa bits = rint(x)
+  const f32x2 j = fadd2(t, f2(-12582912.f, -12582912.f));
+  const f32x2 fr = ffma2(j, f2(-1.f, -1.f), xc);            // f = x - j in [-0.5, 0.5]
+  f32x2 p = ffma2(fr, f2(0.05517083778977394f, 0.05517083778977394f),
+                  f2(0.24260935187339783f, 0.24260935187339783f));
+  p = ffma2(fr, p, f2(0.6932609677314758f, 0.6932609677314758f));
+  p = ffma2(fr, p, f2(0.9999281764030457f, 0.9999281764030457f));
+  float pa, pb, ta, tb;
+  f2split(p, pa, pb);
+  f2split(t, ta, tb);
+  // bits(t) = 0x4B400000 + j, and 0x4B400000 << 23 vanishes mod 2^32: this adds j to the exponent
+  return f2(__uint_as_float(__float_as_uint(pa) + (__float_as_uint(ta) << 23)),
+            __uint_as_float(__float_as_uint(pb) + (__float_as_uint(tb) << 23)));
+}
+
 // SwiGLU on pairs of columns, one fixed instruction sequence shared by the fused GEMM
 // epilogues and the standalone kernels (so the two paths stay bit-identical):
 // sig(g) = rcp(1 + 2^(-g log2 e)) (MUFU ex2 / rcp), a = g sig(g) u,
