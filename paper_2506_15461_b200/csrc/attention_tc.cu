@@ -59,13 +59,16 @@ __device__ __forceinline__ uint32_t kmajor_k(uint32_t base, int rows, int k) {
 constexpr int FK = 64;
 constexpr uint32_t kPTile = TQ * FK * 2;  // 16 KiB: P [128 rows][128 B]
 constexpr float kRescale = 8.f;
-constexpr int kFwdPolyDefault = 0;
+// exponential pairs (of 8) on the FMA pipe in the head_dim-64 forward (measured at [64, 1024, 16,
+// 64]: 0 -> 347.5 us, 1 -> 336.0, 2 -> 339.3, 3 -> 359.6, 4 -> 395.7; head_dim 128 is fastest with 0)
+constexpr int kFwdPolyDefault = 1;
 // per-tile clock instrumentation of the forward (tools/attn_debug.py): compiled in only with
 // -DCKF_ATTN_DEBUG_BUILD=1 (and CKF_ATTN_DEBUG=1 at run time), so the hot loop carries none of it
 #ifndef CKF_ATTN_DEBUG_BUILD
 #define CKF_ATTN_DEBUG_BUILD 0
 #endif
-constexpr bool kDbg = CKF_ATTN_DEBUG_BUILD != 0;  // exponential pairs (of 8) on the FMA pipe, forward
+constexpr bool kDbg = CKF_ATTN_DEBUG_BUILD != 0;
+constexpr int kBwdPolyDefault = 0;  // exponential pairs (of 8) on the FMA pipe, forward
 
 template <int HD>
 struct FwdCfg {
@@ -412,10 +415,10 @@ struct BwdCfg {
   static constexpr uint32_t kUnit = TK * HD * 2;   // 128-row unit operand tile
   static constexpr uint32_t kInner = PT * HD * 2;  // 64-row inner tile
   static constexpr int kNU = HD == 64 ? 2 : 1;     // unit operand buffers (dK dV kernel)
-  static constexpr int kSt = HD == 64 ? 4 : 3;     // inner-tile stages (dK dV kernel)
+  static constexpr int kSt = HD == 64 ? 5 : 3;     // inner-tile stages (dK dV kernel)
   static constexpr int kNAcc = HD == 64 ? 2 : 1;   // dV|dK accumulator sets (2 x HD columns each)
   static constexpr int kNUq = HD == 64 ? 2 : 1;    // unit operand buffers (dQ kernel)
-  static constexpr int kStq = HD == 64 ? 4 : 3;    // inner-tile stages (dQ kernel)
+  static constexpr int kStq = HD == 64 ? 5 : 3;    // inner-tile stages (dQ kernel)
 };
 
 template <int HD>
@@ -433,7 +436,7 @@ struct SmemKVpp {
 // Unit u = (key tile kb, sequence x head bh), kb-major: kb = 0 (longest) first.
 //   S^T = K Q^T, dP^T = V dO^T (TMEM) -> P^T = exp(S^T - lse), dS^T = P^T (dP^T - D) (softmax,
 //   row = key) -> dV += P^T dO, dK += dS^T Q (TMEM accumulators, B operands MN-major)
-template <int HD>
+template <int HD, int POLY>
 __global__ void __launch_bounds__(kThreadsBwd, 1)
     attn_dkdv_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv128, const __grid_constant__ CUtensorMap tm_qkv64,
                         const __grid_constant__ CUtensorMap tm_do64, const float* __restrict__ lse,
@@ -533,17 +536,21 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
           }
           umma_commit(&sm.s_full[bb]);
         };
+        // S/dP run LA tiles ahead of the dV/dK MMAs.  LA = 3 (five Q/dO stages, head_dim 64):
+        // tile i+3 goes into tile i+1's S/dP buffer as soon as the OTHER group's softmax has read
+        // it, before this iteration waits for tile i's P / dS -- with LA = 2 it was queued behind
+        // tile i's dV/dK and the next softmax waited on it (ncu: long-scoreboard at s_full).
+        // LA = 2 needs four stages (with two, tile i+2 reuses the stage tile i's dV/dK still
+        // reads; with three its load waits on tile i-1's MMAs: 13 % slower at hd 128).
+        constexpr int LA = ST >= 5 ? 3 : ST >= 4 ? 2 : 0;
         issue_s(g);
         issue_s(g + 1);
+        if (LA >= 3 && ntiles > 2) issue_s(g + 2);
         mbar_wait(&sm.acc_free[aset], ((lu / NA) & 1) ^ 1);
         for (int i = 0; i < ntiles; ++i) {
           const int gi = g + i, st = gi % ST, bb = gi & 1;
-          // S/dP of tile i+2 go in as soon as this group's softmax has read S/dP of tile i
-          // (s_free), so they run under that softmax instead of after its dV/dK MMAs.  Needs a
-          // fourth Q/dO stage: with two, tile i+2 reuses the stage tile i's dV/dK still reads, and
-          // with three its load waits on tile i-1's MMAs (measured 13 % slower at hd 128).
-          if constexpr (ST >= 4)
-            if (i + 2 < ntiles) issue_s(gi + 2);
+          if constexpr (LA >= 2)
+            if (i + LA < ntiles) issue_s(gi + LA);
           mbar_wait(&sm.pd_full[bb], (gi >> 1) & 1);
           tc_fence_after();
           const uint32_t qa = smem_u32(sm.q[st]), oa = smem_u32(sm.d_o[st]);
@@ -635,12 +642,16 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
           const f32x2 sc2 = f2(scale_log2, scale_log2), nl2 = f2(-kLog2e, -kLog2e), neg2 = f2(-1.f, -1.f);
 #pragma unroll
           for (int e = 0; e < 8; e += 2) {  // pairs: P = 2^(S scale - lse log2e), dS = P (dP - D)
-            float x0, x1;
-            f2split(ffma2(f2(__uint_as_float(us[8 * g8 + e]), __uint_as_float(us[8 * g8 + e + 1])), sc2,
-                          fmul2(f2(lq[e], lq[e + 1]), nl2)),
-                    x0, x1);
-            pv[e] = ex2(x0);
-            pv[e + 1] = ex2(x1);
+            const f32x2 xx = ffma2(f2(__uint_as_float(us[8 * g8 + e]), __uint_as_float(us[8 * g8 + e + 1])), sc2,
+                                   fmul2(f2(lq[e], lq[e + 1]), nl2));
+            if ((g8 * 4 + e / 2) % 8 < POLY) {  // this pair's exponentials on the FMA pipe
+              f2split(ex2_fma2(xx), pv[e], pv[e + 1]);
+            } else {
+              float x0, x1;
+              f2split(xx, x0, x1);
+              pv[e] = ex2(x0);
+              pv[e + 1] = ex2(x1);
+            }
             f2split(fmul2(f2(pv[e], pv[e + 1]),
                           ffma2(f2(dq8[e], dq8[e + 1]), neg2,
                                 f2(__uint_as_float(ud[8 * g8 + e]), __uint_as_float(ud[8 * g8 + e + 1])))),
@@ -691,7 +702,7 @@ struct SmemQpp {  // dQ kernel
 
 // Unit u = (query tile qb, sequence x head bh), longest first; inner tiles of 64 keys.
 //   S = Q K^T, dP = dO V^T (TMEM) -> dS = P (dP - D) (softmax, row = query) -> dQ += dS K
-template <int HD>
+template <int HD, int POLY>
 __global__ void __launch_bounds__(kThreadsBwd, 1)
     attn_dq_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv128, const __grid_constant__ CUtensorMap tm_qkv64,
                       const __grid_constant__ CUtensorMap tm_do128, const float* __restrict__ lse,
@@ -786,14 +797,15 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
           }
           umma_commit(&sm.s_full[bb]);
         };
+        constexpr int LA = ST >= 5 ? 3 : ST >= 4 ? 2 : 0;  // S/dP lookahead (see dK dV)
         issue_s(g);
         issue_s(g + 1);
+        if (LA >= 3 && ntiles > 2) issue_s(g + 2);
         mbar_wait(&sm.acc_free[aset], ((lu >> 1) & 1) ^ 1);
         for (int j = 0; j < ntiles; ++j) {
           const int gj = g + j, st = gj % ST, bb = gj & 1;
-          // S/dP of tile j+2 as soon as this group's softmax has read tile j's (see dK dV)
-          if constexpr (ST >= 4)
-            if (j + 2 < ntiles) issue_s(gj + 2);
+          if constexpr (LA >= 2)
+            if (j + LA < ntiles) issue_s(gj + LA);
           mbar_wait(&sm.ds_full[bb], (gj >> 1) & 1);
           tc_fence_after();
           const uint32_t ka = smem_u32(sm.k[st]), da = smem_u32(sm.ds[bb]);
@@ -876,10 +888,17 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
           const f32x2 sc2 = f2(scale_log2, scale_log2), nl2 = f2(-l2, -l2), nd2 = f2(-dq, -dq);
 #pragma unroll
           for (int e = 0; e < 8; e += 2) {  // pairs: dS = 2^(S scale - lse log2e) (dP - D)
-            float x0, x1;
-            f2split(ffma2(f2(__uint_as_float(us[8 * g8 + e]), __uint_as_float(us[8 * g8 + e + 1])), sc2, nl2), x0, x1);
-            f2split(fmul2(f2(ex2(x0), ex2(x1)),
-                          fadd2(f2(__uint_as_float(ud[8 * g8 + e]), __uint_as_float(ud[8 * g8 + e + 1])), nd2)),
+            const f32x2 xx =
+                ffma2(f2(__uint_as_float(us[8 * g8 + e]), __uint_as_float(us[8 * g8 + e + 1])), sc2, nl2);
+            f32x2 pp;
+            if ((g8 * 4 + e / 2) % 8 < POLY) {  // this pair's exponentials on the FMA pipe
+              pp = ex2_fma2(xx);
+            } else {
+              float x0, x1;
+              f2split(xx, x0, x1);
+              pp = f2(ex2(x0), ex2(x1));
+            }
+            f2split(fmul2(pp, fadd2(f2(__uint_as_float(ud[8 * g8 + e]), __uint_as_float(ud[8 * g8 + e + 1])), nd2)),
                     dv[e], dv[e + 1]);
           }
           if (diag) {
@@ -957,22 +976,29 @@ void bwd_launch(const bf16* qkv, const bf16* o, const float* lse, const bf16* do
   const CUtensorMap td = tma::make_2d_bf16(dout, H * HD, B * T, H * HD, 64, 128);
   const CUtensorMap td64 = tma::make_2d_bf16(dout, H * HD, B * T, H * HD, 64, 64);
   const size_t smem_kv = sizeof(SmemKVpp<HD>) + 1024, smem_q = sizeof(SmemQpp<HD>) + 1024;
+  // exponential pairs (of 8) on the FMA pipe in the backward kernels (CKF_ATTN_BWD_POLY overrides)
+  static const int poly = [] {
+    const char* v = std::getenv("CKF_ATTN_BWD_POLY");
+    return v ? std::atoi(v) : kBwdPolyDefault;
+  }();
+  auto kkv = poly >= 3 ? attn_dkdv_pp_kernel<HD, 3> : poly == 2 ? attn_dkdv_pp_kernel<HD, 2>
+             : poly == 1 ? attn_dkdv_pp_kernel<HD, 1> : attn_dkdv_pp_kernel<HD, 0>;
+  auto kq = poly >= 3 ? attn_dq_pp_kernel<HD, 3> : poly == 2 ? attn_dq_pp_kernel<HD, 2>
+            : poly == 1 ? attn_dq_pp_kernel<HD, 1> : attn_dq_pp_kernel<HD, 0>;
   static bool attr = false;
   if (!attr) {
-    CKF_CUDA(cudaFuncSetAttribute(attn_dkdv_pp_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem_kv)));
-    CKF_CUDA(cudaFuncSetAttribute(attn_dq_pp_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem_q)));
+    CKF_CUDA(cudaFuncSetAttribute(kkv, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_kv)));
+    CKF_CUDA(cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_q)));
     attr = true;
   }
   const float scale = 1.f / sqrtf(static_cast<float>(HD));
   const int BH = static_cast<int>(B * H), units = static_cast<int>(T / TQ) * BH;
   const unsigned grid = static_cast<unsigned>(std::min(units, num_sms_attn()));
-  attn_dkdv_pp_kernel<HD><<<grid, kThreadsBwd, smem_kv, s>>>(tq, tq64, td64, lse, Dsum, static_cast<int>(T),
-                                                             static_cast<int>(H), BH, dqkv, scale, scale * kLog2e);
+  kkv<<<grid, kThreadsBwd, smem_kv, s>>>(tq, tq64, td64, lse, Dsum, static_cast<int>(T), static_cast<int>(H), BH, dqkv,
+                                         scale, scale * kLog2e);
   CKF_LAUNCH_CHECK();
-  attn_dq_pp_kernel<HD><<<grid, kThreadsBwd, smem_q, s>>>(tq, tq64, td, lse, Dsum, static_cast<int>(T),
-                                                         static_cast<int>(H), BH, dqkv, scale, scale * kLog2e);
+  kq<<<grid, kThreadsBwd, smem_q, s>>>(tq, tq64, td, lse, Dsum, static_cast<int>(T), static_cast<int>(H), BH, dqkv,
+                                       scale, scale * kLog2e);
   CKF_LAUNCH_CHECK();
 }
 
