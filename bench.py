@@ -254,8 +254,10 @@ def workload_config(args, w: dict) -> dict:
            "schedule": "swapped_half (swapped first/last-stage order at even microbatches) + per-step edge replica "
                        "refresh" if getattr(args, "strategy", DEFAULT_STRATEGY) == "checkfree-plus" else "standard", "placement": f"{w['stages']} stages on {P} pipeline rank(s) x {R} replica(s)",
            "l2": "256 MiB memset between timed steps (outside the events)",
-           "pipeline_schedule": "1F1B (host-planned global op order, transfers on send/recv streams over per-link "
-                                "NCCL communicators)" if P > 1 else "all stages resident (fused microbatch groups)",
+           "pipeline_schedule": ("1F1B (host-planned global op order; transfers on send/recv streams, "
+                                 + ("per-link NCCL communicators)" if os.environ.get("CKF_TRANSPORT") == "nccl"
+                                    else "peer-memory copies into the next rank's mailbox + device flags)"))
+                                if P > 1 else "all stages resident (fused microbatch groups)",
            "bubble_1f1b": (P - 1) / (w["microbatches"] + P - 1) if P > 1 else 0.0}
     if w["block"] == "llama":
         cfg.update(vocab=w["output_dim"], heads=w["heads"])
@@ -318,6 +320,10 @@ def run_ours(args, w: dict):
         uid = [P_.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         eng.attach_comm(uid[0], world, rank, [(sid - 1) * P // s for sid in range(1, s + 1)], R)
+        if P > 1 and w["block"] == "llama" and os.environ.get("CKF_TRANSPORT", "peer") != "nccl":
+            # 1F1B stage transfers through peer memory: copies into the next rank's mailbox over
+            # NVLink + flags in its HBM (CKF_TRANSPORT=nccl: NCCL send/recv on per-link communicators)
+            eng.enable_peer_transport(w["microbatches"])
         eng.exchange_peers()  # CUDA IPC mappings: recovery reads neighbours from the peers' HBM
 
     orders = np.array(api.build_schedule(w["microbatches"], cfp, s), np.int32)  # pipeline.cpp:41-56

@@ -249,6 +249,13 @@ int ckf_engine_ipc_import(ckf_engine_t e, const void* buf, size_t len);
 /* Collective over the attached communicator: all-gathers every rank's IPC blob and imports
  * them (ckf_engine_ipc_export / _import in one call). */
 int ckf_engine_exchange_peers(ckf_engine_t e);
+/* Peer-memory stage transport (no NCCL on the data path): allocates this rank's mailbox of
+ * 2 x max_microbatches buffers (residual stream / gradient of one microbatch, fp32) and flags;
+ * call on every rank BEFORE the IPC exchange (ckf_engine_exchange_peers, or ipc_export /
+ * ipc_import).  1F1B transfers then copy straight into the receiver's mailbox over
+ * NVLink (copy engine) and signal it through a flag in its HBM (release / acquire, system
+ * scope) that its recv stream waits on. */
+int ckf_engine_enable_peer_transport(ckf_engine_t e, int max_microbatches);
 /* the per-stage forward costs and head cost the engine's 1F1B plan is simulated with */
 int ckf_engine_plan_cost(ckf_engine_t e, double* stage_cost, double* head_cost);
 /* pipeline x data parallel (config 4: 4 stages x DP2): nranks = replicas * P; rank r is

@@ -113,7 +113,7 @@ def lib():
         "ckf_engine_set_placement": (i, [eng, i, i, ip, i]),
         "ckf_engine_ipc_export": (i, [eng, vp, sz, C.POINTER(sz)]), "ckf_engine_ipc_import": (i, [eng, vp, sz]),
         "ckf_engine_exchange_peers": (i, [eng]),
-        "ckf_engine_plan_cost": (i, [eng, dp, dp]),
+        "ckf_engine_plan_cost": (i, [eng, dp, dp]), "ckf_engine_enable_peer_transport": (i, [eng, i]),
         "ckf_recover_stage_device": (i, [i, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, dbl, dbl, i, vp, vp]),
         "ckf_engine_run_iteration": (i, [eng, ip, i, vp, vp, sz, i, lng, dp, dp]),
         "ckf_engine_eval_loss": (i, [eng, ip, vp, vp, sz, i, dp]),

@@ -340,6 +340,11 @@ class Engine:
         buf = C.create_string_buffer(data, max(1, len(data)))
         check(lib().ckf_engine_ipc_import(self._h, buf, len(data)))
 
+    def enable_peer_transport(self, max_microbatches: int):
+        """Stage transfers through peer memory (mailbox + flags, CUDA IPC) instead of NCCL;
+        call on every rank before the IPC exchange."""
+        check(lib().ckf_engine_enable_peer_transport(self._h, max_microbatches))
+
     def plan_cost(self):
         """(per-stage forward costs, head cost) the engine's 1F1B plan is simulated with."""
         sc = np.zeros(self.spec.num_stages, np.float64)

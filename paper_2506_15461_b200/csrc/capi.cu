@@ -576,6 +576,9 @@ int ckf_engine_ipc_import(ckf_engine_t e, const void* buf, size_t len) {
 int ckf_engine_exchange_peers(ckf_engine_t e) {
   return guard([&] { E(e)->exchange_peers(); });
 }
+int ckf_engine_enable_peer_transport(ckf_engine_t e, int max_microbatches) {
+  return guard([&] { E(e)->enable_peer_transport(max_microbatches); });
+}
 int ckf_engine_plan_cost(ckf_engine_t e, double* stage_cost, double* head_cost) {
   return guard([&] {
     const auto c = E(e)->plan_cost();

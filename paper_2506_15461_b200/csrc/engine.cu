@@ -188,6 +188,12 @@ Engine::~Engine() {
   for (auto& p : peer_)
     for (void* q : {p.w, p.m, p.v})
       if (q) cudaIpcCloseMemHandle(q);
+  for (void* q : peer_mbox_)
+    if (q) cudaIpcCloseMemHandle(q);
+  for (uint64_t* q : peer_flags_)
+    if (q) cudaIpcCloseMemHandle(q);
+  cudaFree(mbox_);
+  cudaFree(flags_);
   for (auto& c : ckpt_) cudaFree(c.buf);
   for (cudaEvent_t ev : kev_) cudaEventDestroy(ev);
   if (ev0_) cudaEventDestroy(ev0_);
@@ -377,6 +383,29 @@ cudaEvent_t Engine::plan_event() {
   return pev_[pev_used_++];
 }
 
+void Engine::enable_peer_transport(int max_m) {
+  CKF_CUDA(cudaSetDevice(d_.device));
+  if (max_m < 1) raise(1, "peer transport: max microbatches must be positive");
+  if (d_.block != CKF_BLOCK_LLAMA || !impl_->supports_plan())
+    raise(1, "peer transport carries the plan-driven (LLaMA) pipeline's stage transfers");
+  if (mbox_) {
+    cudaFree(mbox_);
+    cudaFree(flags_);
+  }
+  mbox_m_ = max_m;
+  mbox_slot_ = (d_.max_rows * d_.d * sizeof(float) + 255) / 256 * 256;
+  CKF_CUDA(cudaMalloc(&mbox_, 2 * static_cast<size_t>(max_m) * mbox_slot_));
+  CKF_CUDA(cudaMalloc(&flags_, 2 * static_cast<size_t>(max_m) * sizeof(uint64_t)));
+  CKF_CUDA(cudaMemset(flags_, 0, 2 * static_cast<size_t>(max_m) * sizeof(uint64_t)));
+  plan_epoch_ = 0;
+}
+
+void* Engine::mailbox(int k, int phase) const {
+  if (!mbox_) return nullptr;
+  if (k < 0 || k >= mbox_m_) raise(1, "peer transport: microbatch beyond the mailbox (enable it with more)");
+  return static_cast<char*>(mbox_) + (static_cast<size_t>(k) * 2 + static_cast<size_t>(phase)) * mbox_slot_;
+}
+
 host::PlanCost Engine::plan_cost() const {
   host::PlanCost cost;
   for (size_t i = 0; i < d_.s; ++i) cost.stage.push_back(static_cast<double>(d_.part[i].count()));
@@ -421,6 +450,13 @@ void Engine::run_plan(const int* orders, int m, const char* x, size_t mb, size_t
   std::vector<cudaEvent_t> sent(static_cast<size_t>(m) * 2, nullptr);     // last send of the buffer
   bool any_send = false, any_recv = false;
   (void)xrow;
+  const bool peer = !virt && peer_transport();
+  if (peer && static_cast<int>(peer_mbox_.size()) != nranks_) raise(1, "peer transport: IPC exchange missing");
+  if (peer && m > mbox_m_) raise(1, "peer transport: more microbatches than the mailbox holds");
+  ++plan_epoch_;
+  if (peer && plan_epoch_ >= (1ull << 55)) raise(1, "peer transport: epoch overflow");
+  std::vector<std::vector<uint32_t>> arrivals(static_cast<size_t>(std::max(nranks_, 1)),
+                                               std::vector<uint32_t>(static_cast<size_t>(m) * 2, 0));
   static const char* kNames[] = {"ckf.plan.embed_fwd", "ckf.plan.stage_fwd", "ckf.plan.xfer", "ckf.plan.head",
                                  "ckf.plan.stage_bwd", "ckf.plan.embed_bwd"};
   for (const auto& op : plan) {
@@ -438,6 +474,32 @@ void Engine::run_plan(const int* orders, int m, const char* x, size_t mb, size_t
         continue;
       }
       const size_t slot = static_cast<size_t>(k) * 2 + static_cast<size_t>(op.aux);
+      if (peer) {
+        // peer-memory transport: the sender's copy engine writes straight into the receiver's
+        // mailbox over NVLink, then a one-thread kernel raises the receiver's flag (release);
+        // the receiver's recv stream spins on it (acquire).  Flag value = iteration epoch and the
+        // arrival count of this (microbatch, phase) at that rank -- every rank walks the whole
+        // plan, so both sides count the same.
+        const uint64_t val = (plan_epoch_ << 8) | static_cast<uint64_t>(++arrivals[static_cast<size_t>(op.arg)][slot]);
+        if (op.rank == rank_) {
+          if (op.arg >= static_cast<int>(peer_mbox_.size()) || !peer_mbox_[static_cast<size_t>(op.arg)])
+            raise(1, "peer transport: rank " + std::to_string(op.arg) + "'s mailbox is not mapped (IPC exchange)");
+          cudaEvent_t ev = plan_event();
+          CKF_CUDA(cudaEventRecord(ev, st_));
+          CKF_CUDA(cudaStreamWaitEvent(sst_, ev, 0));
+          char* dstp = static_cast<char*>(peer_mbox_[static_cast<size_t>(op.arg)]) + slot * mbox_slot_;
+          CKF_CUDA(cudaMemcpyAsync(dstp, b, bytes, cudaMemcpyDeviceToDevice, sst_));
+          k::flag_signal(peer_flags_[static_cast<size_t>(op.arg)] + slot, val, sst_);
+          any_send = true;
+        } else if (op.arg == rank_) {
+          k::flag_wait(flags_ + slot, val, rst_);
+          cudaEvent_t ev = plan_event();
+          CKF_CUDA(cudaEventRecord(ev, rst_));
+          pending[slot] = ev;
+          any_recv = true;
+        }
+        continue;
+      }
       if (op.rank == rank_) {  // send behind the producing op
         cudaEvent_t ev = plan_event();
         CKF_CUDA(cudaEventRecord(ev, st_));
@@ -506,6 +568,21 @@ size_t Engine::ipc_export(void* buf, size_t cap) {
       v.push_back(e);
     }
   }
+  if (mbox_) {  // peer transport: mailbox and flags
+    void* bufs[2] = {mbox_, flags_};
+    const uint64_t sizes[2] = {2ull * static_cast<uint64_t>(mbox_m_) * mbox_slot_,
+                               2ull * static_cast<uint64_t>(mbox_m_) * sizeof(uint64_t)};
+    for (int k = 0; k < 2; ++k) {
+      IpcEntry e{};
+      e.rank = rank_;
+      e.replica = replica_;
+      e.sid = 0;
+      e.kind = 3 + k;
+      e.bytes = sizes[k];
+      CKF_CUDA(cudaIpcGetMemHandle(&e.h, bufs[k]));
+      v.push_back(e);
+    }
+  }
   const size_t need = v.size() * sizeof(IpcEntry);
   if (need > cap) raise(1, "IPC export buffer too small (" + std::to_string(need) + " bytes needed)");
   if (need) std::memcpy(buf, v.data(), need);
@@ -520,6 +597,17 @@ void Engine::ipc_import(const void* buf, size_t len) {
   for (size_t i = 0; i < len / sizeof(IpcEntry); ++i) {
     const IpcEntry& x = e[i];
     if (x.rank == rank_ || x.replica != replica_) continue;  // own stages / other replicas' copies
+    if (x.kind == 3 || x.kind == 4) {  // a peer's transport mailbox / flags
+      if (x.rank < 0 || x.rank >= nranks_) raise(1, "malformed IPC entry (rank)");
+      if (peer_mbox_.size() != static_cast<size_t>(nranks_)) {
+        peer_mbox_.assign(static_cast<size_t>(nranks_), nullptr);
+        peer_flags_.assign(static_cast<size_t>(nranks_), nullptr);
+      }
+      void** slot = x.kind == 3 ? &peer_mbox_[static_cast<size_t>(x.rank)]
+                                : reinterpret_cast<void**>(&peer_flags_[static_cast<size_t>(x.rank)]);
+      if (!*slot) CKF_CUDA(cudaIpcOpenMemHandle(slot, x.h, cudaIpcMemLazyEnablePeerAccess));
+      continue;
+    }
     if (x.sid < 1 || x.sid > static_cast<int>(d_.s) || x.kind < 0 || x.kind > 2) raise(1, "malformed IPC entry");
     ParamGroup& g = stages_[static_cast<size_t>(x.sid - 1)];
     if (g.owned) continue;
@@ -910,8 +998,9 @@ void Engine::run_iteration(const int* orders, int m, const void* x, const void* 
   double total = 0.0;
   for (double l : losses) total += l;
   total *= inv;  // this replica's share of the global mean loss
-  if (nranks_ > 1) {
+  if (nranks_ > 1 && comm_) {
     // every rank learns every stage's omega (the recovery reads its neighbours') and the loss
+    // (placement without a communicator -- the peer-transport tests -- returns this rank's own)
     std::vector<double> v(d_.s + 1, 0.0);
     for (size_t i = 0; i < d_.s; ++i) v[i] = stages_[i].owned && replica_ == 0 ? om[i] : 0.0;
     v[d_.s] = mine(owner_of_deembed()) ? total : 0.0;

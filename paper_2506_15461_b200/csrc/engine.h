@@ -227,6 +227,15 @@ class Engine {
   void ipc_import(const void* buf, size_t len);
   // collective: all-gathers every rank's IPC blob over NCCL and imports them
   void exchange_peers();
+  // Peer-memory stage transport for the plan-driven pipeline: a mailbox of 2 x max_m microbatch
+  // buffers (residual stream / its gradient, max_rows x d fp32 each) and 2 x max_m flags, both
+  // exported with the IPC blob; transfers then copy straight into the receiver's mailbox (peer
+  // HBM) and signal its flag instead of going through NCCL.  Enable on every rank BEFORE the
+  // IPC exchange.
+  void enable_peer_transport(int max_m);
+  bool peer_transport() const { return mbox_ != nullptr; }
+  // this rank's mailbox slot of microbatch k (phase 0: h, 1: dh); null without the transport
+  void* mailbox(int k, int phase) const;
   // costs the 1F1B plan is simulated with: forward time units per stage (its layer count) and the
   // head (LM head + loss + head backward) relative to one layer's forward FLOPs
   host::PlanCost plan_cost() const;
@@ -344,6 +353,14 @@ class Engine {
     void *w = nullptr, *m = nullptr, *v = nullptr;
   };
   std::vector<PeerStage> peer_;
+  // peer transport: own mailbox / flags, and every other rank's (IPC-mapped), by global rank
+  void* mbox_ = nullptr;
+  uint64_t* flags_ = nullptr;
+  int mbox_m_ = 0;
+  size_t mbox_slot_ = 0;  // bytes per microbatch buffer
+  std::vector<void*> peer_mbox_;
+  std::vector<uint64_t*> peer_flags_;
+  uint64_t plan_epoch_ = 0;
   bool peer_ready_ = false;  // every stage this rank does not own is mapped  // per stage id - 1: IPC mappings of stages owned by other ranks
   void* comm_ = nullptr;  // ncclComm_t
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;

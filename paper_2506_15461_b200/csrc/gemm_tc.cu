@@ -892,7 +892,17 @@ void gemm_bf16(const GemmDesc& g, cudaStream_t s) {
   // stages half the B bytes per MMA FLOP in a 6-deep ring.  Measured on B200
   // (profiles/r01_gemm_pair_vs_single.jsonl): +3-4 % on the stage GEMMs; single CTAs stay ahead
   // for the fused SwiGLU epilogues and for N <= 512 with very short or very long K.
-  const bool pair_shape = pair_wgrad || (g.epi != kSwiGLU && g.epi != kSwiGLUBwd && splits <= 1 &&
+  // The SwiGLU forward (gate/up GEMM, 128 x 256 single-CTA tiles are operand-bandwidth bound:
+  // 96 B / clk / SM of A + B at the tensor peak) runs as CTA pairs too -- B multicast, 6 operand
+  // stages: 481.7 -> 424.6 us at [32,768 x 8,192 x 1,024] (500M).  The backward epilogue
+  // (g / u in, dg / du out: 8 B per element) is HBM-bound and gains nothing (320 vs 325 us).
+  // CKF_GEMM_SWIGLU_PAIR=0 / 2: single CTAs for both / pairs for both.
+  static const int swiglu_pair = [] {
+    const char* v = std::getenv("CKF_GEMM_SWIGLU_PAIR");
+    return v ? std::atoi(v) : 1;
+  }();
+  const bool swiglu_single = (g.epi == kSwiGLU && swiglu_pair == 0) || (g.epi == kSwiGLUBwd && swiglu_pair != 2);
+  const bool pair_shape = pair_wgrad || (!swiglu_single && splits <= 1 &&
                                          !(g.N <= 512 && (g.K <= 512 || g.K >= 16384)));
   if (bn == 128 && pair_wgrad)
     dispatch_bn<128, 2>(g, splits, s);

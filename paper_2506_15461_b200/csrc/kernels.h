@@ -75,6 +75,13 @@ struct StageRecovery {
 };
 template <typename T> void recover_stage(const StageRecovery<T>& r, ReduceScratch& sc, cudaStream_t s);
 
+// Peer-memory stage transfers (the IPC transport of the plan-driven pipeline): the sender's
+// stream copies a microbatch buffer into the receiver's mailbox (peer HBM over NVLink), then
+// flag_signal stores `value` into the receiver's flag with system-scope release semantics; the
+// receiver's stream runs flag_wait, which spins (acquire) until the flag reaches `value`.
+void flag_signal(uint64_t* flag, uint64_t value, cudaStream_t s);
+void flag_wait(const uint64_t* flag, uint64_t value, cudaStream_t s);
+
 // NaN poison (simulated loss of a stage's GPU state)
 template <typename T> void poison(T* x, size_t n, cudaStream_t s);
 

@@ -471,8 +471,16 @@ struct LlamaBlock final : BlockImpl {
     plab_ = buf<int>(58, static_cast<size_t>(m) * Mt);
     llama::split_tokens(static_cast<const int*>(x), static_cast<size_t>(m) * rows, T, ptok_, plab_, eng->stream());
   }
-  float* ph(int k) { return buf<float>(slot_id(k, 4), prows_ * T * d); }
-  float* pdh(int k) { return buf<float>(slot_id(k, 2), prows_ * T * d); }
+  // with the peer transport the residual stream and its gradient live in the engine's mailbox
+  // (peers copy into it); otherwise in per-microbatch workspace slots
+  float* ph(int k) {
+    if (void* p = eng->mailbox(k, 0)) return static_cast<float*>(p);
+    return buf<float>(slot_id(k, 4), prows_ * T * d);
+  }
+  float* pdh(int k) {
+    if (void* p = eng->mailbox(k, 1)) return static_cast<float*>(p);
+    return buf<float>(slot_id(k, 2), prows_ * T * d);
+  }
   bf16* pdh_bf(int k) { return buf<bf16>(slot_id(k, 3), prows_ * T * d); }
   void* plan_buffer(int k, int phase, size_t* bytes) override {
     *bytes = prows_ * T * d * sizeof(float);

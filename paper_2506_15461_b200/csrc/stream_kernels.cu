@@ -454,6 +454,24 @@ __global__ void recover_stage_kernel(StageRecovery<T> r, double a, double b, dou
   }
 }
 
+// ---------------------------------------------------------------- peer-memory signalling
+__global__ void flag_signal_kernel(uint64_t* flag, uint64_t value) {
+  __threadfence_system();  // the mailbox copy issued before on this stream is complete; publish it
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(value) : "memory");
+}
+__global__ void flag_wait_kernel(const uint64_t* flag, uint64_t value) {
+  uint64_t v;
+  // bounded: a transfer that never arrives (a broken plan) traps after ~60 s of polling instead
+  // of holding the GPU forever
+  const long long t0 = clock64();
+  for (;;) {
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+    if (v >= value) break;
+    __nanosleep(256);
+    if (clock64() - t0 > 120000000000LL) __trap();
+  }
+}
+
 template <typename T>
 __global__ void poison_kernel(T* __restrict__ x, size_t n) {
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
@@ -676,6 +694,15 @@ void recover_stage(const StageRecovery<T>& r, ReduceScratch& sc, cudaStream_t s)
     CKF_LAUNCH_CHECK();
     if (r.old_sq) finish(sc, grid, r.old_sq, s);
   }
+}
+
+void flag_signal(uint64_t* flag, uint64_t value, cudaStream_t s) {
+  flag_signal_kernel<<<1, 1, 0, s>>>(flag, value);
+  CKF_LAUNCH_CHECK();
+}
+void flag_wait(const uint64_t* flag, uint64_t value, cudaStream_t s) {
+  flag_wait_kernel<<<1, 1, 0, s>>>(flag, value);
+  CKF_LAUNCH_CHECK();
 }
 
 template <typename T>

@@ -7,6 +7,7 @@
 // GPU (counter-RNG inputs, teacher forward) for the MLP block; the LLaMA block
 // uses the counter-RNG token process of llama_block.cu.
 #include <algorithm>
+#include <cstdlib>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -72,6 +73,10 @@ class Trainer {
       std::vector<int> sr(c.stages);
       for (size_t i = 0; i < c.stages; ++i) sr[i] = static_cast<int>(i * static_cast<size_t>(P) / c.stages);
       model_.attach_comm(cm->uid, cm->nranks, cm->rank, sr.data(), R);
+      // stage transfers through peer memory (mailbox + flags over NVLink) unless CKF_TRANSPORT=nccl
+      const char* tr = std::getenv("CKF_TRANSPORT");
+      if (P > 1 && desc_.block == CKF_BLOCK_LLAMA && desc_.precision == CKF_BF16 && !(tr && std::string(tr) == "nccl"))
+        model_.enable_peer_transport(c.microbatches / R);
       model_.exchange_peers();
     }
     if (desc_.block == CKF_BLOCK_MLP) {

@@ -168,3 +168,81 @@ def test_peer_recovery_through_ipc_equals_resident(averaged):
     assert np.array_equal(w, w1) and np.array_equal(m, m1) and np.array_equal(v, v1)
     assert (om, step) == e.scalars(2)[::2] and lat > 0
     e.close()
+
+
+# ----------------------------------------------------------------- 1F1B across processes, peer-memory transport
+def _pipe_worker(rank, port, placement, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    import paper_2506_15461_b200 as P
+    import llama_oracle as LO
+    spec = P.api.ModelSpec.llama(512, 128, 4, 2, 256, 128, 4, max_tokens=2 * 128)
+    e = P.Engine(spec)
+    e.init(3, 1e-3)
+    e.set_placement(2, rank, placement)  # -> schedule 2 (1F1B plan)
+    e.enable_peer_transport(8)
+    blobs = [None, None]
+    dist.all_gather_object(blobs, e.ipc_export())
+    e.ipc_import(blobs)
+    dist.barrier()
+    out = []
+    for it in (1, 2, 3):
+        toks = LO.token_batch(9, 1, it, 8, 128, 512)
+        loss, om = e.run_iteration(P.api.build_schedule(4, it != 2, 4), toks, None, it)
+        out.append((loss, [float(x) for x in om]))
+        dist.barrier()  # iteration boundary (the NCCL all-reduce of loss / omega plays it with a communicator)
+    w = {s: e.export_stage(s)[0] for s in range(1, 5) if placement[s - 1] == rank}
+    edges = {}
+    if placement[0] == rank:
+        edges["embed"] = e.export_edge(0)[0]
+    if placement[3] == rank:
+        edges["deembed"] = e.export_edge(1)[0]
+    q.put((rank, out, w, edges))
+    dist.barrier()
+    e.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("placement", [[0, 0, 1, 1], [0, 1, 0, 1]])
+def test_1f1b_two_processes_peer_transport_bit_identical(placement):
+    # Two processes share one GPU, each owning half of the stages; the plan-driven executor runs
+    # the 1F1B schedule across them with the peer-memory transport (copies into the other
+    # process's mailbox through CUDA IPC, flags raised / awaited in device memory, send / recv
+    # streams) -- the multi-GPU data path minus NVLink.  Losses, omegas and every weight must be
+    # bit-identical to the single-process sequential run (the interleaved placement sends every
+    # microbatch across the boundary three times each way, CheckFree+ orders included).
+    import torch.multiprocessing as mp
+    import paper_2506_15461_b200 as P
+    import llama_oracle as LO
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pipe_worker, args=(r, port, placement, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(2):
+        r, out, w, edges = q.get(timeout=300)
+        res[r] = (out, w, edges)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    spec = P.api.ModelSpec.llama(512, 128, 4, 2, 256, 128, 4, max_tokens=2 * 128)
+    e = P.Engine(spec)
+    e.init(3, 1e-3)
+    e.set_group_cap(1)
+    ref = []
+    for it in (1, 2, 3):
+        toks = LO.token_batch(9, 1, it, 8, 128, 512)
+        ref.append(e.run_iteration(P.api.build_schedule(4, it != 2, 4), toks, None, it))
+    head = placement[3]
+    for it in range(3):
+        assert res[head][0][it][0] == ref[it][0]  # the loss lives on the head's rank
+        for s in range(1, 5):
+            assert res[placement[s - 1]][0][it][1][s - 1] == ref[it][1][s - 1]  # omega on the stage's owner
+    for s in range(1, 5):
+        assert np.array_equal(res[placement[s - 1]][1][s], e.export_stage(s)[0])
+    assert np.array_equal(res[placement[0]][2]["embed"], e.export_edge(0)[0])
+    assert np.array_equal(res[placement[3]][2]["deembed"], e.export_edge(1)[0])
+    e.close()
