@@ -68,7 +68,7 @@ constexpr int kFwdPolyDefault = 1;
 #define CKF_ATTN_DEBUG_BUILD 0
 #endif
 constexpr bool kDbg = CKF_ATTN_DEBUG_BUILD != 0;
-constexpr int kBwdPolyDefault = 0;  // exponential pairs (of 8) on the FMA pipe, forward
+constexpr int kBwdSplitDefault = 1;  // 2 measured no faster (1084.7 vs 1087.8 us at [64, 1024, 16, 64])  // exponential pairs (of 8) on the FMA pipe, forward
 
 template <int HD>
 struct FwdCfg {
@@ -436,8 +436,12 @@ struct SmemKVpp {
 // Unit u = (key tile kb, sequence x head bh), kb-major: kb = 0 (longest) first.
 //   S^T = K Q^T, dP^T = V dO^T (TMEM) -> P^T = exp(S^T - lse), dS^T = P^T (dP^T - D) (softmax,
 //   row = key) -> dV += P^T dO, dK += dS^T Q (TMEM accumulators, B operands MN-major)
-template <int HD, int POLY>
-__global__ void __launch_bounds__(kThreadsBwd, 1)
+// SPLIT: softmax warps per TMEM lane quarter per group -- 2 splits each key row's 64 queries
+// between two warps (32 each): P and dS are elementwise given lse / D, so the halves never
+// communicate, and twice the warps per SM sub-partition hide the latency of the per-thread
+// chains (the single-warp softmax issued one instruction every few cycles).
+template <int HD, int POLY, int SPLIT>
+__global__ void __launch_bounds__(128 + 256 * SPLIT, 1)
     attn_dkdv_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv128, const __grid_constant__ CUtensorMap tm_qkv64,
                         const __grid_constant__ CUtensorMap tm_do64, const float* __restrict__ lse,
                         const float* __restrict__ D, int T, int H, int BH, __nv_bfloat16* __restrict__ dqkv,
@@ -463,13 +467,13 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&sm.s_full[i], 1);
-      mbar_init(&sm.s_free[i], 4);
-      mbar_init(&sm.pd_full[i], 4);
+      mbar_init(&sm.s_free[i], 4 * SPLIT);
+      mbar_init(&sm.pd_full[i], 4 * SPLIT);
       mbar_init(&sm.pd_free[i], 1);
     }
     for (int i = 0; i < NA; ++i) {
       mbar_init(&sm.acc_full[i], 1);
-      mbar_init(&sm.acc_free[i], 8);
+      mbar_init(&sm.acc_free[i], 8 * SPLIT);
     }
     for (int i = 0; i < ST; ++i) {
       mbar_init(&sm.qd_full[i], 1);
@@ -573,7 +577,9 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
       }
     }
   } else if (warp >= 4) {
-    const int sw = warp - 4, quarter = sw & 3, grp = sw >> 2;
+    // sw = grp * 4 SPLIT + half * 4 + quarter
+    const int sw = warp - 4, quarter = sw & 3, half = (sw >> 2) % SPLIT, grp = sw / (4 * SPLIT);
+    constexpr int QW = PT / SPLIT;  // queries of a tile per softmax thread
     const int r = quarter * 32 + lane;  // key row within the unit
     const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
     const uint32_t pbase = smem_u32(sm.p[grp]), dbase = smem_u32(sm.ds[grp]);
@@ -589,7 +595,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
                            static_cast<size_t>(grp ? (H + eh) * HD : (2 * H + eh) * HD);
       const float mul = grp ? scale : 1.f;
 #pragma unroll 1
-      for (int c0 = 0; c0 < HD; c0 += 32) {
+      for (int c0 = half * (HD / SPLIT); c0 < (half + 1) * (HD / SPLIT); c0 += 32) {
         uint32_t w32[32];
         tmem_ld32(trow + 256 + aset * 2 * HD + grp * HD + c0, w32);
         tmem_ld_wait();
@@ -616,11 +622,12 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
         mbar_wait(&sm.s_full[grp], (gi >> 1) & 1);
         mbar_wait(&sm.qd_full[st], (gi / ST) & 1);  // (complete) lse / D of this tile visible
         tc_fence_after();
-        uint32_t us[64], ud[64];
-        tmem_ld32(trow + grp * 128, *reinterpret_cast<uint32_t(*)[32]>(&us[0]));
-        tmem_ld32(trow + grp * 128 + 32, *reinterpret_cast<uint32_t(*)[32]>(&us[32]));
-        tmem_ld32(trow + grp * 128 + 64, *reinterpret_cast<uint32_t(*)[32]>(&ud[0]));
-        tmem_ld32(trow + grp * 128 + 96, *reinterpret_cast<uint32_t(*)[32]>(&ud[32]));
+        uint32_t us[QW], ud[QW];
+#pragma unroll
+        for (int c = 0; c < QW; c += 32) {
+          tmem_ld32(trow + grp * 128 + half * QW + c, *reinterpret_cast<uint32_t(*)[32]>(&us[c]));
+          tmem_ld32(trow + grp * 128 + 64 + half * QW + c, *reinterpret_cast<uint32_t(*)[32]>(&ud[c]));
+        }
         tmem_ld_wait();
         tc_fence_before();
         __syncwarp();
@@ -629,7 +636,8 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
         const uint32_t rowoff = static_cast<uint32_t>(r * 128);
         const uint32_t la_ = smem_u32(&sm.lse[st][0]), da_ = smem_u32(&sm.dsum[st][0]);
 #pragma unroll
-        for (int g8 = 0; g8 < 8; ++g8) {  // 8 queries at a time: P^T, dS^T -> bf16 -> swizzled smem
+        for (int lg = 0; lg < QW / 8; ++lg) {  // 8 queries at a time: P^T, dS^T -> bf16 -> swizzled smem
+          const int g8 = half * (QW / 8) + lg;
           const uint4 la = ld_shared_v4(la_ + 32 * g8), lb = ld_shared_v4(la_ + 32 * g8 + 16);
           const uint4 da4 = ld_shared_v4(da_ + 32 * g8), db4 = ld_shared_v4(da_ + 32 * g8 + 16);
           const float lq[8] = {__uint_as_float(la.x), __uint_as_float(la.y), __uint_as_float(la.z),
@@ -642,7 +650,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
           const f32x2 sc2 = f2(scale_log2, scale_log2), nl2 = f2(-kLog2e, -kLog2e), neg2 = f2(-1.f, -1.f);
 #pragma unroll
           for (int e = 0; e < 8; e += 2) {  // pairs: P = 2^(S scale - lse log2e), dS = P (dP - D)
-            const f32x2 xx = ffma2(f2(__uint_as_float(us[8 * g8 + e]), __uint_as_float(us[8 * g8 + e + 1])), sc2,
+            const f32x2 xx = ffma2(f2(__uint_as_float(us[8 * lg + e]), __uint_as_float(us[8 * lg + e + 1])), sc2,
                                    fmul2(f2(lq[e], lq[e + 1]), nl2));
             if ((g8 * 4 + e / 2) % 8 < POLY) {  // this pair's exponentials on the FMA pipe
               f2split(ex2_fma2(xx), pv[e], pv[e + 1]);
@@ -654,7 +662,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
             }
             f2split(fmul2(f2(pv[e], pv[e + 1]),
                           ffma2(f2(dq8[e], dq8[e + 1]), neg2,
-                                f2(__uint_as_float(ud[8 * g8 + e]), __uint_as_float(ud[8 * g8 + e + 1])))),
+                                f2(__uint_as_float(ud[8 * lg + e]), __uint_as_float(ud[8 * lg + e + 1])))),
                     dv[e], dv[e + 1]);
           }
           if (i < 2) {  // diagonal: query kb*128 + 64 i + c sees key kb*128 + r iff 64 i + c >= r
@@ -976,15 +984,16 @@ void bwd_launch(const bf16* qkv, const bf16* o, const float* lse, const bf16* do
   const CUtensorMap td = tma::make_2d_bf16(dout, H * HD, B * T, H * HD, 64, 128);
   const CUtensorMap td64 = tma::make_2d_bf16(dout, H * HD, B * T, H * HD, 64, 64);
   const size_t smem_kv = sizeof(SmemKVpp<HD>) + 1024, smem_q = sizeof(SmemQpp<HD>) + 1024;
-  // exponential pairs (of 8) on the FMA pipe in the backward kernels (CKF_ATTN_BWD_POLY overrides)
-  static const int poly = [] {
-    const char* v = std::getenv("CKF_ATTN_BWD_POLY");
-    return v ? std::atoi(v) : kBwdPolyDefault;
+  // CKF_ATTN_BWD_SPLIT=1|2: softmax warps per TMEM lane quarter per group in the dK dV kernel
+  // (CKF_ATTN_BWD_POLY: FMA-pipe exponential pairs of 8 in the backward -- measured no gain, so
+  // only the all-MUFU kernels are built: profiles/r02_attention_bwd_poly_sweep.jsonl)
+  static const int split = [] {
+    const char* v = std::getenv("CKF_ATTN_BWD_SPLIT");
+    return v ? std::atoi(v) : kBwdSplitDefault;
   }();
-  auto kkv = poly >= 3 ? attn_dkdv_pp_kernel<HD, 3> : poly == 2 ? attn_dkdv_pp_kernel<HD, 2>
-             : poly == 1 ? attn_dkdv_pp_kernel<HD, 1> : attn_dkdv_pp_kernel<HD, 0>;
-  auto kq = poly >= 3 ? attn_dq_pp_kernel<HD, 3> : poly == 2 ? attn_dq_pp_kernel<HD, 2>
-            : poly == 1 ? attn_dq_pp_kernel<HD, 1> : attn_dq_pp_kernel<HD, 0>;
+  auto kkv = split >= 2 ? attn_dkdv_pp_kernel<HD, 0, 2> : attn_dkdv_pp_kernel<HD, 0, 1>;
+  const int kv_threads = 128 + 256 * (split >= 2 ? 2 : 1);
+  auto kq = attn_dq_pp_kernel<HD, 0>;
   static bool attr = false;
   if (!attr) {
     CKF_CUDA(cudaFuncSetAttribute(kkv, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_kv)));
@@ -994,8 +1003,8 @@ void bwd_launch(const bf16* qkv, const bf16* o, const float* lse, const bf16* do
   const float scale = 1.f / sqrtf(static_cast<float>(HD));
   const int BH = static_cast<int>(B * H), units = static_cast<int>(T / TQ) * BH;
   const unsigned grid = static_cast<unsigned>(std::min(units, num_sms_attn()));
-  kkv<<<grid, kThreadsBwd, smem_kv, s>>>(tq, tq64, td64, lse, Dsum, static_cast<int>(T), static_cast<int>(H), BH, dqkv,
-                                         scale, scale * kLog2e);
+  kkv<<<grid, kv_threads, smem_kv, s>>>(tq, tq64, td64, lse, Dsum, static_cast<int>(T), static_cast<int>(H), BH, dqkv,
+                                        scale, scale * kLog2e);
   CKF_LAUNCH_CHECK();
   kq<<<grid, kThreadsBwd, smem_q, s>>>(tq, tq64, td, lse, Dsum, static_cast<int>(T), static_cast<int>(H), BH, dqkv,
                                        scale, scale * kLog2e);
