@@ -295,11 +295,23 @@ def run_ours(args, w: dict):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # CKF_BENCH_SAME_GPU=1 (tests only): every rank on cuda:0, gloo for the host plumbing, no NCCL
+    # -- the N>1 pipeline path (placement, 1F1B across processes over the peer transport, peer
+    # recovery) runs as a FUNCTIONAL check on a one-GPU box; its timings are time-sliced, not
+    # performance numbers, and the JSON says so
+    same_gpu = world > 1 and os.environ.get("CKF_BENCH_SAME_GPU") == "1"
+    if same_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if same_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     s = w["stages"]
     P, R = placement(world, s)
+    if same_gpu and (R > 1 or w["block"] != "llama"):
+        raise SystemExit("CKF_BENCH_SAME_GPU covers the LLaMA pipeline without data-parallel replicas")
 
     mb_rows = w["rows"] // w["microbatches"]
     if w["block"] == "llama":
@@ -316,7 +328,13 @@ def run_ours(args, w: dict):
     cfp = args.strategy == "checkfree-plus"
     if cfp:
         eng.set_edge_replicas(True)  # trainer.cpp:83-84: E / E^-1 replicas refreshed inside every step
-    if world > 1:
+    if same_gpu:
+        eng.set_placement(world, rank, [(sid - 1) * P // s for sid in range(1, s + 1)], R)
+        eng.enable_peer_transport(w["microbatches"])
+        blobs = [None] * world
+        dist.all_gather_object(blobs, eng.ipc_export())
+        eng.ipc_import(blobs)
+    elif world > 1:
         uid = [P_.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         eng.attach_comm(uid[0], world, rank, [(sid - 1) * P // s for sid in range(1, s + 1)], R)
@@ -341,8 +359,12 @@ def run_ours(args, w: dict):
 
     def step(it, on_device):
         if on_device:
-            return eng.run_iteration(orders, xd, yd, it, on_device=True)
-        return eng.run_iteration(orders, xh.numpy(), yh.numpy() if yh is not None else None, it)
+            r = eng.run_iteration(orders, xd, yd, it, on_device=True)
+        else:
+            r = eng.run_iteration(orders, xh.numpy(), yh.numpy() if yh is not None else None, it)
+        if same_gpu:  # the iteration boundary the NCCL loss / omega all-reduce provides otherwise
+            dist.barrier()
+        return r
 
     def barrier():
         if world > 1:
@@ -408,7 +430,7 @@ def run_ours(args, w: dict):
     ms = ms_total / args.steps
     e2e_ms = e2e_total / args.steps
     if world > 1:
-        t = torch.tensor([ms, e2e_ms], dtype=torch.float64, device=f"cuda:{local}")
+        t = torch.tensor([ms, e2e_ms], dtype=torch.float64, device="cpu" if same_gpu else f"cuda:{local}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, e2e_ms = t.tolist()
 
@@ -426,6 +448,10 @@ def run_ours(args, w: dict):
         for _ in range(5):
             eng.kill_stage(sid)
             lat.append(eng.recover_stage(sid, reduction_error=False).latency_ms)
+            if same_gpu:  # no communicator: share the replacement GPU's latency, fence the peers
+                lt = torch.tensor([lat[-1]], dtype=torch.float64)
+                dist.all_reduce(lt, op=dist.ReduceOp.MAX)
+                lat[-1] = float(lt.item())
         n_stage = eng.stage_params
         pb = 4 if w["precision"] != "fp64" else 8
         nbytes = n_stage * (6 * pb + (2 if w["precision"] == "bf16" else 0))
@@ -441,10 +467,10 @@ def run_ours(args, w: dict):
         if cfp:
             # CheckFree+ first-stage recovery: stage 1 := stage 2, E := its replica (recovery.cpp:90-101)
             el = []
-            for _ in range(3):
+            for _ in range(3 if not same_gpu else 0):  # (the edge replica pull needs NCCL across ranks)
                 eng.kill_stage(1)
                 el.append(eng.recover_stage(1, mode=P_._native.CKF_REC_EDGE, reduction_error=False).latency_ms)
-            rec["edge_stage1_latency_ms"] = statistics.median(el)
+            rec["edge_stage1_latency_ms"] = statistics.median(el) if el else None
 
     if rank != 0:
         if world > 1:
@@ -514,6 +540,10 @@ def run_ours(args, w: dict):
             "flops_per_token": flops_per_token(w), "cpu_baseline": cpu, "cpu_baseline_llama_oracle": cpu_llama,
             "clocks": clk.summary(),
             "recovery": rec, "recovery_sweep": sweep}
+    if same_gpu:
+        line["functional_same_gpu"] = ("CKF_BENCH_SAME_GPU: all ranks time-slice ONE GPU (peer transport over CUDA "
+                                       "IPC, gloo host plumbing) -- a functional check of the N>1 path, not a "
+                                       "performance number")
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
