@@ -577,7 +577,7 @@ def recovery_sweep(P, local, hbm_peak, cpu=True):
     if cpu:
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         import refshim  # noqa: F811  (baseline infrastructure only)
-    for n in (10_000_000, 25_000_000, 50_000_000, 100_000_000, 200_000_000, 400_000_000):
+    for n in (10_000_000, 12_585_984, 25_000_000, 50_337_792, 100_000_000, 200_000_000, 400_000_000):
         wp = torch.rand(n, device=dev)
         wn = torch.rand(n, device=dev)
         ws = torch.empty(n, device=dev)

@@ -1,3 +1,5 @@
+#include <cstdlib>
+#include <type_traits>
 // Bandwidth-bound kernels of the engine: counter-RNG init, activations,
 // losses, fused Adam + omega, omega-weighted recovery, reductions.
 //
@@ -13,6 +15,10 @@ namespace ckf::k {
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kRecoverU = 4;             // float4 slots in flight per thread (fused recovery)
+// grid cap of the fused recovery, CTAs of 256 per SM: 16 measured best (tools/recover_tune.py,
+// profiles/r02_recover_tune.jsonl: 12.6 M params 0.839 -> 0.852 of HBM, 50.3 M 0.891 -> 0.907)
+constexpr int kRecoverBlocksPerSM = 16;
 
 unsigned reduce_grid(size_t n) {
   size_t g = (n + kThreads * 8 - 1) / (kThreads * 8);
@@ -344,14 +350,13 @@ __global__ void wavg_kernel(const T* __restrict__ a, const T* __restrict__ b, T*
 // (they are read once), stores streaming.  Algorithmic bytes per parameter (fp32):
 // read Wp, Wn (8) + write W (4) + write m, v, g (12) + bf16 shadow (2) = 26; Averaged adds
 // the four neighbour-moment reads (16); the reduction error adds the read of the old W (4).
-template <bool kAvg, bool kSq>
+template <bool kAvg, bool kSq, int U>
 __global__ void __launch_bounds__(256) recover_stage_f32x4_kernel(
     const float4* __restrict__ wp, const float4* __restrict__ wn, const float4* __restrict__ mp,
     const float4* __restrict__ mn, const float4* __restrict__ vp, const float4* __restrict__ vn,
     float4* __restrict__ w, float4* __restrict__ m, float4* __restrict__ v, float4* __restrict__ g,
     uint2* __restrict__ wlp, size_t n4, float a, float b, double ma, double mb, double mden, int mom_uniform,
     double* __restrict__ partials) {
-  constexpr int U = 4;
   double acc = 0.0;
   const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
   const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -668,7 +673,16 @@ void recover_stage(const StageRecovery<T>& r, ReduceScratch& sc, cudaStream_t s)
             reinterpret_cast<uintptr_t>(r.vp) | reinterpret_cast<uintptr_t>(r.vn);
     if (al % 16 == 0 && reinterpret_cast<uintptr_t>(r.wlp) % 8 == 0 && r.n % 4 == 0) {
       const size_t n4 = r.n / 4;
-      const unsigned grid = r.old_sq ? reduce_grid(r.n / 4) : grid_for((n4 + 3) / 4, kThreads, kNumSMs * 8);
+      static const int tune_u = [] {  // CKF_RECOVER_U / CKF_RECOVER_BPS: tuning overrides
+        const char* v = std::getenv("CKF_RECOVER_U");
+        return v ? std::atoi(v) : kRecoverU;
+      }();
+      static const int tune_bps = [] {
+        const char* v = std::getenv("CKF_RECOVER_BPS");
+        return v ? std::atoi(v) : kRecoverBlocksPerSM;
+      }();
+      const unsigned grid = r.old_sq ? reduce_grid(r.n / 4)
+                                     : grid_for((n4 + tune_u - 1) / tune_u, kThreads, kNumSMs * tune_bps);
       auto f4 = [](const float* p) { return reinterpret_cast<const float4*>(p); };
       auto o4 = [](float* p) { return reinterpret_cast<float4*>(p); };
       auto launch = [&](auto kern) {
@@ -676,10 +690,21 @@ void recover_stage(const StageRecovery<T>& r, ReduceScratch& sc, cudaStream_t s)
                                        o4(r.v), o4(r.g), reinterpret_cast<uint2*>(r.wlp), n4, fa, fb, r.mop, r.mon,
                                        mden, mom_uniform, sc.partials);
       };
+      auto pick = [&](auto avg, auto sq) {
+        constexpr bool A = decltype(avg)::value, Q = decltype(sq)::value;
+        if (tune_u >= 8)
+          launch(recover_stage_f32x4_kernel<A, Q, 8>);
+        else if (tune_u >= 4)
+          launch(recover_stage_f32x4_kernel<A, Q, 4>);
+        else
+          launch(recover_stage_f32x4_kernel<A, Q, 2>);
+      };
+      using T_ = std::true_type;
+      using F_ = std::false_type;
       if (r.averaged)
-        r.old_sq ? launch(recover_stage_f32x4_kernel<true, true>) : launch(recover_stage_f32x4_kernel<true, false>);
+        r.old_sq ? pick(T_{}, T_{}) : pick(T_{}, F_{});
       else
-        r.old_sq ? launch(recover_stage_f32x4_kernel<false, true>) : launch(recover_stage_f32x4_kernel<false, false>);
+        r.old_sq ? pick(F_{}, T_{}) : pick(F_{}, F_{});
       CKF_LAUNCH_CHECK();
       if (r.old_sq) finish(sc, grid, r.old_sq, s);
       return;
