@@ -338,33 +338,41 @@ void Engine::attach_comm(const void* uid, int nranks, int rank, const int* stage
       if (!nccl().CommSplit) raise(7, "ncclCommSplit unavailable (NCCL >= 2.18 needed for replicas)");
       nccl_check(nccl().CommSplit(comm_, rank % P, replica_, &dp_comm_, nullptr), "ncclCommSplit");
     }
-    // one communicator per DIRECTED stage link of the pipeline (the links the standard and the
-    // CheckFree+ swapped routes use under this placement): on every rank a link's communicator
-    // is driven by exactly one stream (the source's send stream / the destination's recv
-    // stream).  ncclCommSplit is collective over the world: every rank walks the same link list.
-    if (P > 1 && nccl().CommSplit) {
-      std::vector<int> sr(stage_rank, stage_rank + d_.s);
-      std::vector<std::pair<int, int>> want;
-      for (int sw = 0; sw < (d_.s >= 4 ? 2 : 1); ++sw) {
-        const std::vector<int> o = host::build_schedule(2, sw == 1, static_cast<int>(d_.s));
-        for (const auto& op : host::pipeline_plan(static_cast<int>(d_.s), 2, o, sr, 1))
-          if (op.kind == host::PlanOp::kXfer) want.push_back({op.rank, op.arg});
-      }
-      std::sort(want.begin(), want.end());
-      want.erase(std::unique(want.begin(), want.end()), want.end());
-      const int me = rank % P;
-      for (size_t i = 0; i < want.size(); ++i) {
-        const auto [a, b] = want[i];
-        const bool in = me == a || me == b;
-        void* c = nullptr;
-        // color = link index x replicas + replica (each replica gets its own 2-rank communicator);
-        // key orders the source first
-        nccl_check(nccl().CommSplit(comm_, in ? static_cast<int>(i) * replicas + replica_ : -1 /*NCCL_SPLIT_NOCOLOR*/,
-                                    me == a ? 0 : 1, &c, nullptr),
-                   "ncclCommSplit (stage link)");
-        if (in) links_.push_back({{replica_ * P + a, replica_ * P + b}, c});
-      }
-    }
+  }
+}
+
+// One communicator per DIRECTED stage link of the pipeline (the links the standard and the
+// CheckFree+ swapped routes use under this placement): on every rank a link's communicator is
+// driven by exactly one stream (the source's send stream / the destination's recv stream).
+// Created on the first NCCL-transport plan iteration -- every rank reaches it in the same
+// iteration, and ncclCommSplit is collective over the world, so every rank walks the same list.
+void Engine::ensure_links() {
+  if (links_ready_ || nranks_ <= 1 || !comm_) return;
+  links_ready_ = true;  // (a rank on no link still took part in every split)
+  if (!nccl().CommSplit) raise(7, "ncclCommSplit unavailable (NCCL >= 2.18 needed for the stage links)");
+  const int P = nranks_ / replicas_;
+  if (P <= 1) return;
+  std::vector<int> sr(d_.s);
+  for (size_t i = 0; i < d_.s; ++i) sr[i] = stage_rank_[i] - replica_ * P;
+  std::vector<std::pair<int, int>> want;
+  for (int sw = 0; sw < (d_.s >= 4 ? 2 : 1); ++sw) {
+    const std::vector<int> o = host::build_schedule(2, sw == 1, static_cast<int>(d_.s));
+    for (const auto& op : host::pipeline_plan(static_cast<int>(d_.s), 2, o, sr, 1))
+      if (op.kind == host::PlanOp::kXfer) want.push_back({op.rank, op.arg});
+  }
+  std::sort(want.begin(), want.end());
+  want.erase(std::unique(want.begin(), want.end()), want.end());
+  const int me = rank_ % P;
+  for (size_t i = 0; i < want.size(); ++i) {
+    const auto [a, b] = want[i];
+    const bool in = me == a || me == b;
+    void* c = nullptr;
+    // color = link index x replicas + replica (each replica its own 2-rank communicator); the
+    // source gets key 0
+    nccl_check(nccl().CommSplit(comm_, in ? static_cast<int>(i) * replicas_ + replica_ : -1 /*NCCL_SPLIT_NOCOLOR*/,
+                                me == a ? 0 : 1, &c, nullptr),
+               "ncclCommSplit (stage link)");
+    if (in) links_.push_back({{replica_ * P + a, replica_ * P + b}, c});
   }
 }
 
@@ -451,6 +459,7 @@ void Engine::run_plan(const int* orders, int m, const char* x, size_t mb, size_t
   bool any_send = false, any_recv = false;
   (void)xrow;
   const bool peer = !virt && peer_transport();
+  if (!virt && !peer) ensure_links();
   if (peer && static_cast<int>(peer_mbox_.size()) != nranks_) raise(1, "peer transport: IPC exchange missing");
   if (peer && m > mbox_m_) raise(1, "peer transport: more microbatches than the mailbox holds");
   ++plan_epoch_;

@@ -337,6 +337,8 @@ class Engine {
   // plan-driven (1F1B) executor: side streams, per-link communicators, event pool
   void run_plan(const int* orders, int m, const char* x, size_t mb, size_t xrow);
   void* link_comm(int src, int dst);
+  void ensure_links();
+  bool links_ready_ = false;
   cudaEvent_t plan_event();
   cudaStream_t sst_ = nullptr, rst_ = nullptr, dst_ = nullptr;  // send, recv, data-parallel streams
   std::vector<std::pair<std::pair<int, int>, void*>> links_;    // (src, dst) -> ncclComm_t
