@@ -74,7 +74,9 @@ template <int HD>
 struct FwdCfg {
   static constexpr uint32_t kQ = TQ * HD * 2, kK = FK * HD * 2;
   static constexpr int kKSt = HD == 64 ? 4 : 3, kVSt = HD == 64 ? 3 : 2;
-  static constexpr int kMinBlocks = HD == 64 ? 2 : 1;  // 104 KiB vs 144 KiB of shared memory
+  // 104 KiB vs 144 KiB of shared memory; two hd-128 CTAs per SM with 2 K / 1 V stages (112 KiB)
+  // measured 1.7x slower (1697 -> 2887 us at [16, 4096, 16, 128]): the single V stage serialises
+  static constexpr int kMinBlocks = HD == 64 ? 2 : 1;
 };
 
 template <int HD>
