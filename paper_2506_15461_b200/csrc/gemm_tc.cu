@@ -115,7 +115,9 @@ struct Params {
   float alpha;
   int nm, nn, tiles, nk;
   int splits, kb_per_split, units;
-  int* flags;    // split-K: 2 counters per tile (partials stored, reduction done), self-resetting
+  int* flags;    // split-K: 4 counters per half-tile (co-resident: stored, reduced; otherwise one per
+                 // lane quarter), self-resetting
+  int coresident;  // split-K units all in flight at once (waiting reduction) or not (last-arriver)
   float* ws;     // split-K partial tiles: [units][BM][BN] fp32
   float* C;      // split-K: fp32 C (row pitch ldc) the reduced tile is added into
   int ldc;
@@ -562,87 +564,110 @@ __global__ void __launch_bounds__(gemm_threads(EPI, NCTA), 1)
       }
       }  // generic epilogues
       if (EPI == kAccF32 && p.splits > 1) {  // (split-K runs only with the accumulate epilogue)
-        // Deterministic split-K reduction (all units are co-resident: units <= grid):
-        // 1) every warp publishes its stored partial rows, 2) once all 4*splits warps of the
-        // tile have, the tile's rows are shared out among them and each sums the partials in
-        // split order and adds the result into C.
         const int ht = w.tile * NCTA + static_cast<int>(rank);  // half-tile of a CTA pair
-        int* stored = p.flags + 2 * ht;
-        int* reduced = stored + 1;
-        const int nwarps = C::kEW * p.splits;
-        if (lane == 0) {
-          bulk_wait_all();  // this warp's partial rows have landed in the workspace
-          fence_proxy_async_global();
-          __threadfence();
-          atomicAdd(stored, 1);
-          while (ld_acquire(stored) < nwarps) __nanosleep(32);
-        }
-        __syncwarp();
-        const int wid = w.split * C::kEW + ew;
-        const int per = (BM + nwarps - 1) / nwarps;
-        const int r_lo = wid * per, r_hi = min(BM, (wid + 1) * per);
-        // this warp's rows as float4 slots, lanes along the columns (coalesced); kP slots per
-        // lane in flight at once -- C first, then each split's partials in split order -- so the
-        // reduction is bandwidth- rather than latency-bound.  Sum order per element as always:
-        // ((p0 + p1) + p2 ...) + C, deterministic.
-        constexpr int kP = 8, kQ = BN / 4;
-        const int nslot = (r_hi > r_lo ? r_hi - r_lo : 0) * kQ;
-        const size_t ws_base = (static_cast<size_t>(w.tile) * NCTA + rank) * BM;
-        const size_t ws_split = static_cast<size_t>(p.tiles) * NCTA * BM * BN;  // floats between splits
-        for (int base = lane; base < nslot; base += 32 * kP) {
-          float4 o[kP], acc4[kP];
-          float4* dst[kP];
-          size_t wofs[kP];
-          bool ok[kP];
+        // sums partial rows [r_lo, r_hi) of this half-tile over the splits, in split order, into C:
+        // float4 slots, lanes along the columns (coalesced); kP slots per lane in flight at once --
+        // C first, then each split's partials -- so the reduction is bandwidth- rather than
+        // latency-bound.  Sum order per element as always: ((p0 + p1) + p2 ...) + C, deterministic.
+        auto reduce_rows = [&](int r_lo, int r_hi) {
+          constexpr int kP = 8, kQ = BN / 4;
+          const int nslot = (r_hi > r_lo ? r_hi - r_lo : 0) * kQ;
+          const size_t ws_base = (static_cast<size_t>(w.tile) * NCTA + rank) * BM;
+          const size_t ws_split = static_cast<size_t>(p.tiles) * NCTA * BM * BN;  // floats between splits
+          for (int base = lane; base < nslot; base += 32 * kP) {
+            float4 o[kP], acc4[kP];
+            float4* dst[kP];
+            size_t wofs[kP];
+            bool ok[kP];
 #pragma unroll
-          for (int i = 0; i < kP; ++i) {
-            const int idx = base + 32 * i;
-            const int rr = r_lo + idx / kQ, c = (idx % kQ) * 4;
-            const int m = w.mb * BM * NCTA + static_cast<int>(rank) * BM + rr;
-            const int n = w.nb * BN + c;
-            ok[i] = idx < nslot && m < p.M && n < p.N;
-            dst[i] = reinterpret_cast<float4*>(p.C + static_cast<size_t>(ok[i] ? m : 0) * p.ldc + (ok[i] ? n : 0));
-            wofs[i] = (ws_base + rr) * BN + c;
-            if (ok[i]) o[i] = *dst[i];
-          }
+            for (int i = 0; i < kP; ++i) {
+              const int idx = base + 32 * i;
+              const int rr = r_lo + idx / kQ, c = (idx % kQ) * 4;
+              const int m = w.mb * BM * NCTA + static_cast<int>(rank) * BM + rr;
+              const int n = w.nb * BN + c;
+              ok[i] = idx < nslot && m < p.M && n < p.N;
+              dst[i] = reinterpret_cast<float4*>(p.C + static_cast<size_t>(ok[i] ? m : 0) * p.ldc + (ok[i] ? n : 0));
+              wofs[i] = (ws_base + rr) * BN + c;
+              if (ok[i]) o[i] = *dst[i];
+            }
 #pragma unroll 1
-          for (int sp = 0; sp < p.splits; ++sp) {
-            float4 t[kP];
+            for (int sp = 0; sp < p.splits; ++sp) {
+              float4 t[kP];
 #pragma unroll
-            for (int i = 0; i < kP; ++i)
-              if (ok[i]) t[i] = __ldcg(reinterpret_cast<const float4*>(p.ws + sp * ws_split + wofs[i]));
+              for (int i = 0; i < kP; ++i)
+                if (ok[i]) t[i] = __ldcg(reinterpret_cast<const float4*>(p.ws + sp * ws_split + wofs[i]));
+#pragma unroll
+              for (int i = 0; i < kP; ++i)
+                if (ok[i]) {
+                  if (sp == 0) {
+                    acc4[i] = t[i];
+                  } else {
+                    acc4[i].x += t[i].x;
+                    acc4[i].y += t[i].y;
+                    acc4[i].z += t[i].z;
+                    acc4[i].w += t[i].w;
+                  }
+                }
+            }
 #pragma unroll
             for (int i = 0; i < kP; ++i)
               if (ok[i]) {
-                if (sp == 0) {
-                  acc4[i] = t[i];
-                } else {
-                  acc4[i].x += t[i].x;
-                  acc4[i].y += t[i].y;
-                  acc4[i].z += t[i].z;
-                  acc4[i].w += t[i].w;
-                }
+                o[i].x += acc4[i].x;
+                o[i].y += acc4[i].y;
+                o[i].z += acc4[i].z;
+                o[i].w += acc4[i].w;
+                *dst[i] = o[i];
               }
           }
-#pragma unroll
-          for (int i = 0; i < kP; ++i)
-            if (ok[i]) {
-              o[i].x += acc4[i].x;
-              o[i].y += acc4[i].y;
-              o[i].z += acc4[i].z;
-              o[i].w += acc4[i].w;
-              *dst[i] = o[i];
-            }
-        }
-        __syncwarp();
-        if (lane == 0) {
-          __threadfence();
-          if (atomicAdd(reduced, 1) == nwarps - 1) {  // last one out resets the tile's counters
-            atomicExch(stored, 0);
-            atomicExch(reduced, 0);
+        };
+        if (p.coresident) {
+          // All units co-resident (units <= CTAs in flight): 1) every warp publishes its stored
+          // partial rows, 2) once all 4*splits warps of the tile have, the tile's rows are shared
+          // out among them and each reduces its share.
+          int* stored = p.flags + 4 * ht;
+          int* reduced = stored + 1;
+          const int nwarps = C::kEW * p.splits;
+          if (lane == 0) {
+            bulk_wait_all();  // this warp's partial rows have landed in the workspace
+            fence_proxy_async_global();
+            __threadfence();
+            atomicAdd(stored, 1);
+            while (ld_acquire(stored) < nwarps) __nanosleep(32);
           }
+          __syncwarp();
+          const int wid = w.split * C::kEW + ew;
+          const int per = (BM + nwarps - 1) / nwarps;
+          reduce_rows(wid * per, min(BM, (wid + 1) * per));
+          __syncwarp();
+          if (lane == 0) {
+            __threadfence();
+            if (atomicAdd(reduced, 1) == nwarps - 1) {  // last one out resets the tile's counters
+              atomicExch(stored, 0);
+              atomicExch(reduced, 0);
+            }
+          }
+          __syncwarp();
+        } else {
+          // More units than CTAs in flight (split counts chosen for wave balance): no waiting --
+          // the LAST of the tile's `splits` warps of this lane quarter (the arrival that completes
+          // the count) reduces the quarter's 32 rows; the others move on.  Same sums, same order.
+          int* cnt = p.flags + 4 * ht + q;
+          int last = 0;
+          if (lane == 0) {
+            bulk_wait_all();
+            fence_proxy_async_global();
+            __threadfence();
+            last = atomicAdd(cnt, 1) == p.splits - 1 ? 1 : 0;
+            __threadfence();
+          }
+          last = __shfl_sync(0xffffffffu, last, 0);
+          if (last) {
+            reduce_rows(q * 32, q * 32 + 32);
+            __syncwarp();
+            if (lane == 0) atomicExch(cnt, 0);
+          }
+          __syncwarp();
         }
-        __syncwarp();
       }
       if (++acc == 2) {
         acc = 0;
@@ -754,10 +779,11 @@ void launch_t(const GemmDesc& g, int splits, cudaStream_t s) {
   p.kb_per_split = (p.nk + p.splits - 1) / p.splits;
   p.splits = (p.nk + p.kb_per_split - 1) / p.kb_per_split;  // no empty split
   p.units = p.tiles * p.splits;
-  // split-K needs every unit co-resident (units <= CTAs or CTA pairs in flight)
-  if (p.splits > 1 && (p.units > num_sms() / NCTA || EPI != kAccF32 || g.N % 4 != 0))
-    p.splits = 1, p.units = p.tiles, p.kb_per_split = p.nk;
-  p.flags = p.splits > 1 ? split_flags(2 * static_cast<size_t>(p.tiles) * NCTA) : nullptr;
+  if (p.splits > 1 && (EPI != kAccF32 || g.N % 4 != 0)) p.splits = 1, p.units = p.tiles, p.kb_per_split = p.nk;
+  // co-resident: every unit in flight at once (units <= CTAs or CTA pairs) -> the waiting,
+  // shared reduction; otherwise the last-arriver reduction per lane quarter
+  p.coresident = p.units <= num_sms() / NCTA ? 1 : 0;
+  p.flags = p.splits > 1 ? split_flags(4 * static_cast<size_t>(p.tiles) * NCTA) : nullptr;
   p.ws = p.splits > 1 ? split_workspace(static_cast<size_t>(p.units) * NCTA * BM * BN * sizeof(float)) : nullptr;
   p.C = static_cast<float*>(g.C);
   p.ldc = g.ldc;
@@ -866,9 +892,27 @@ void gemm_bf16(const GemmDesc& g, cudaStream_t s) {
   }();
   if (pair_wgrad) bn = wg_bn;
   if (splits <= 0 && pair_wgrad) {
+    // split count by wave balance over the 74 pairs: time ~ ceil(tiles * s / pairs) / s of a tile
+    // plus a per-split reduction term (e.g. QKV wgrad at d = 1024: 48 pair tiles -> s = 3, 144
+    // units in two waves = 0.67 tile times instead of 1.0 with 26 pairs idle)
     const int pairs = num_sms() / 2, nk = (g.K + BK - 1) / BK;
     const int pt = ((g.M + 2 * BM - 1) / (2 * BM)) * ((g.N + bn - 1) / bn);
-    splits = pt * 3 < pairs * 2 ? std::max(1, std::min({pairs / pt, nk / 4, 16})) : 1;
+    static const double red_cost = [] {
+      const char* v = std::getenv("CKF_GEMM_SPLIT_COST");
+      return v ? std::atof(v) : 0.04;
+    }();
+    double best = 1e30;
+    splits = 1;
+    // only a grid that leaves pairs idle is split: a multi-wave grid pays the reduction traffic for
+    // nothing (measured: gate/up wgrad, 128 pair tiles, 4 splits 427.9 us vs 388.8 unsplit)
+    for (int sk = 1; sk <= 16 && nk / sk >= 4 && pt < pairs; ++sk) {
+      const double waves = static_cast<double>((pt * sk + pairs - 1) / pairs);
+      const double t = waves / sk + (sk > 1 ? red_cost * sk : 0.0);
+      if (t < best - 1e-9) {
+        best = t;
+        splits = sk;
+      }
+    }
   }
   if (splits <= 0) {
     splits = 1;
