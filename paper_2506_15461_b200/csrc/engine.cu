@@ -1103,9 +1103,26 @@ long Engine::checkpoint_restore(const int* stages, int n_stages, double* red, fl
   if (red && n_stages > 0)
     CKF_CUDA(cudaMemcpyAsync(r.data(), scal_ + 3200, r.size() * sizeof(double), cudaMemcpyDeviceToHost, st_));
   CKF_CUDA(cudaStreamSynchronize(st_));
+  float t = 0.f;
+  CKF_CUDA(cudaEventElapsedTime(&t, ev0_, ev1_));
+  if (nranks_ > 1 && comm_) {
+    // multi-rank: each failed stage's reduction error comes from its owner (replica 0); the
+    // restore time is the slowest rank's
+    std::vector<double> v(r.size() + 1, 0.0);
+    for (int k = 0; k < n_stages; ++k) {
+      const int sid = stages[k];
+      v[static_cast<size_t>(k)] = replica_ == 0 && stages_[static_cast<size_t>(sid - 1)].owned ? r[static_cast<size_t>(k)] : 0.0;
+    }
+    const auto all = allreduce_host(v);
+    for (size_t k = 0; k < r.size(); ++k) r[k] = all[k];
+    std::vector<double> tv(static_cast<size_t>(nranks_), 0.0);
+    tv[static_cast<size_t>(rank_)] = t;
+    const auto ts = allreduce_host(tv);
+    for (double x : ts) t = std::max(t, static_cast<float>(x));
+  }
   if (red)
     for (int k = 0; k < n_stages; ++k) red[k] = r[static_cast<size_t>(k)];
-  if (ms) CKF_CUDA(cudaEventElapsedTime(ms, ev0_, ev1_));
+  if (ms) *ms = t;
   return ckpt_iter_;
 }
 
