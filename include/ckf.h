@@ -160,6 +160,18 @@ int ckf_xent_bf16(void* logits, const int* labels, size_t rows, size_t V, float 
                   void* stream);
 int ckf_gemm_bf16_aux(int M, int N, int K, const void* A, int lda, int a_mn, const void* B, int ldb, int b_mn, void* C,
                       int ldc, int epi, float alpha, int bn, void* aux, int ldaux, void* stream);
+// Fused LM head + cross-entropy on DEVICE buffers (head_xent.cu; replaces the logits GEMM ->
+// softmax_xent_loss_grad -> head backward GEMMs of proj/src/model.cpp:250-253,322-342 and
+// proj/src/kernels_serial.cpp:163-185 without a logits tensor): xn [M x d] bf16, Einv [d x V] bf16,
+// labels [M]; row_loss[i] = logsumexp - logit[label] (fp64); train != 0: dxn [M x d] fp32 =
+// dlogits Einv^T (stored), gEinv [d x V] fp32 += xn^T dlogits, dlogits = grad_scale (softmax -
+// onehot).  Optional h [M x d] fp32, rstd [M], gain [d] (xn = bf16(h rstd gain), the final
+// RMSNorm's input): the weight gradient's scaled rows are then rounded once from them (NULL: from
+// xn).  ws: ckf_lm_head_xent_workspace(M, d, V) bytes of device memory.
+size_t ckf_lm_head_xent_workspace(size_t M, size_t d, size_t V);
+int ckf_lm_head_xent(const void* xn, const void* Einv, const int* labels, size_t M, size_t d, size_t V, float grad_scale,
+                     int train, double* row_loss, float* dxn, float* gEinv, const float* h, const float* rstd,
+                     const float* gain, void* ws, void* stream);
 
 /* Causal attention of the LLaMA block on device bf16 buffers: qkv [B*T x 3*H*hd]
  * (q | k | v column blocks), o [B*T x H*hd], lse [B*H*T] fp32 (natural log).

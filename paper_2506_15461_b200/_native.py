@@ -91,6 +91,8 @@ def lib():
         "ckf_recover_device": (i, [i, vp, vp, vp, sz, dbl, dbl, vp, vp]),
         "ckf_gemm_bf16": (i, [i, i, i, vp, i, i, vp, i, i, vp, i, i, C.c_float, i, vp]),
         "ckf_xent_bf16": (i, [vp, vp, C.c_size_t, C.c_size_t, C.c_float, i, vp, vp]),
+        "ckf_lm_head_xent_workspace": (C.c_size_t, [sz, sz, sz]),
+        "ckf_lm_head_xent": (i, [vp, vp, vp, sz, sz, sz, C.c_float, i, vp, vp, vp, vp, vp, vp, vp, vp]),
         "ckf_gemm_bf16_aux": (i, [i, i, i, vp, i, i, vp, i, i, vp, i, i, C.c_float, i, vp, i, vp]),
         "ckf_attention_fwd": (i, [vp, sz, sz, sz, sz, vp, vp, i, vp]),
         "ckf_attention_bwd": (i, [vp, vp, vp, vp, sz, sz, sz, sz, vp, vp, i, vp]),

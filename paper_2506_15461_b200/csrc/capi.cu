@@ -453,6 +453,35 @@ int ckf_xent_bf16(void* logits, const int* labels, size_t rows, size_t V, float 
   });
 }
 
+size_t ckf_lm_head_xent_workspace(size_t M, size_t d, size_t V) { return ckf::llama::head_xent_workspace(M, d, V); }
+
+int ckf_lm_head_xent(const void* xn, const void* Einv, const int* labels, size_t M, size_t d, size_t V, float grad_scale,
+                     int train, double* row_loss, float* dxn, float* gEinv, const float* h, const float* rstd,
+                     const float* gain, void* ws, void* stream) {
+  const float* hrows = h;
+  return guard([&] {
+    ckf::llama::HeadXent h;
+    h.xn = static_cast<const __nv_bfloat16*>(xn);
+    h.Einv = static_cast<const __nv_bfloat16*>(Einv);
+    h.labels = labels;
+    h.M = static_cast<int>(M);
+    h.d = static_cast<int>(d);
+    h.V = static_cast<int>(V);
+    h.grad_scale = grad_scale;
+    h.train = train != 0;
+    h.row_loss = row_loss;
+    h.dxn = dxn;
+    h.gEinv = gEinv;
+    h.ws = ws;
+    h.h = hrows;
+    h.rstd = rstd;
+    h.gain = gain;
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    ckf::llama::head_xent(h, [&](const ckf::tc::GemmDesc& g) { ckf::tc::gemm_bf16(g, st); },
+                          [](const std::function<void()>& f) { f(); }, st);
+  });
+}
+
 int ckf_gemm_bf16_aux(int M, int N, int K, const void* A, int lda, int a_mn, const void* B, int ldb, int b_mn, void* C,
                       int ldc, int epi, float alpha, int bn, void* aux, int ldaux, void* stream) {
   return guard([&] {

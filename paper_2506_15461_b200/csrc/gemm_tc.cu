@@ -103,7 +103,9 @@ constexpr int BM = 128, BK = 64, UK = 16;
 // Epilogue warps: 8 (two per TMEM lane quarter, each on half of the tile's columns) for the
 // CTA-pair bf16-output epilogue (measured: LM head forward +8 % vs cuBLAS-relative, others
 // neutral); 4 elsewhere, where the extra staging would cost an operand stage.
-__host__ __device__ constexpr int epi_warps(int epi, int ncta) { return epi == 0 /*kStoreBF16*/ && ncta == 2 ? 8 : 4; }
+__host__ __device__ constexpr int epi_warps(int epi, int ncta) {
+  return (epi == kStoreBF16 || epi == kXentFwd) && ncta == 2 ? 8 : 4;
+}
 __host__ __device__ constexpr int gemm_threads(int epi, int ncta) { return 128 + 32 * epi_warps(epi, ncta); }
 constexpr uint32_t kAStage = BM * BK * 2;  // 16 KiB
 constexpr uint32_t kStageBufBytes = 4096;  // per epilogue warp, x2: [32 rows][128 B] TMA-store staging
@@ -125,7 +127,24 @@ struct Params {
   int rope_T, rope_cols;
   int f;                   // kSwiGLU / kSwiGLUBwd: ffn width (column offset of the up half)
   const __nv_bfloat16* gu; // kSwiGLUBwd: [M x 2f] gate/up activations (row pitch 2f)
+  const float* row_scale;  // kStoreF32: per-row scale instead of alpha
+  const int* gate;         // no work when *gate == 0
+  XentArgs xent;           // kXentFwd
 };
+
+// ordered-int encoding of a float (monotonic under signed int compare) for atomicMax
+__device__ __forceinline__ int f2ord(float f) {
+  const int i = __float_as_int(f);
+  return i >= 0 ? i : i ^ 0x7fffffff;
+}
+__device__ __forceinline__ float ord2f(int k) { return __int_as_float(k >= 0 ? k : k ^ 0x7fffffff); }
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+constexpr float kLog2eF = 1.4426950408889634f;
+constexpr float kXentGuardExp = 5.184705528587072e21f;  // exp(kXentGuard)
 
 template <int BN, int EPI, int NCTA>
 struct Cfg {
@@ -233,13 +252,15 @@ __global__ void __launch_bounds__(gemm_threads(EPI, NCTA), 1)
   // nothing global is read or written before the previous grid has fully completed.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  // gated launch (a rerun decided on the device): every role sees zero units
+  const int units = (p.gate && *reinterpret_cast<const volatile int*>(p.gate) == 0) ? 0 : p.units;
 
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = u0; u < p.units; u += ustep) {
+      for (int u = u0; u < units; u += ustep) {
         const Unit w = unit_of(p, u);
         const int arow = w.mb * BM * NCTA + static_cast<int>(rank) * BM;
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
@@ -289,7 +310,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI, NCTA), 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int u = u0; u < p.units; u += ustep) {
+      for (int u = u0; u < units; u += ustep) {
         const Unit w = unit_of(p, u);
         const long long w1_ = p.dbg ? clock64() : 0;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -368,7 +389,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI, NCTA), 1)
     auto row0_of = [&](const Unit& wu) { return wu.mb * BM * NCTA + static_cast<int>(rank) * BM + q * 32; };
     int cc = 0;               // kSwiGLUBwd: chunk counter of this warp's stream
     bool first_unit = true;
-    for (int u = u0; u < p.units; u += ustep) {
+    for (int u = u0; u < units; u += ustep) {
       const Unit w = unit_of(p, u);
       if constexpr (EPI == kSwiGLUBwd) {
         if (first_unit && lane == 0) {  // first g/u chunk in flight before the accumulator is ready
@@ -385,7 +406,65 @@ __global__ void __launch_bounds__(gemm_threads(EPI, NCTA), 1)
       tc_fence_after();
       const uint32_t trow = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN);
       const int m0 = row0_of(w);
-      if constexpr (EPI == kSwiGLU) {
+      if constexpr (EPI == kXentFwd) {
+        // LM head + cross-entropy (gemm_tc.h): this thread's row is m0 + lane; e = 2^(l log2e - c log2e)
+        const int mrow = m0 + lane;
+        const bool rok = mrow < p.M;
+        const int lab = rok ? __ldg(p.xent.labels + mrow) : -1;
+        const float cr = rok ? fmaxf(__ldg(p.xent.c + mrow), ord2f(p.xent.vmax[mrow])) : 0.f;
+        const f32x2 lg2 = f2(kLog2eF, kLog2eF), ncl = f2(-cr * kLog2eF, -cr * kLog2eF);
+        float ps = 0.f;
+#pragma unroll 1
+        for (int c0 = eh * (BN / EH); c0 < (eh + 1) * (BN / EH); c0 += 64) {
+          uint32_t r[64];
+          tmem_ld32(trow + c0, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+          tmem_ld32(trow + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+          tmem_ld_wait();
+          if (c0 + 64 >= (eh + 1) * (BN / EH)) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) release_acc(acc);
+          }
+          const int n0 = w.nb * BN + c0;
+          const int yo = lab - n0;
+          if (static_cast<unsigned>(yo) < 64u) {  // the label column is in this chunk: its exact fp32 logit
+            float v = 0.f;
+#pragma unroll
+            for (int j = 0; j < 64; ++j) v = j == yo ? __uint_as_float(r[j]) : v;
+            p.xent.ly[mrow] = v;
+          }
+          const int nval = p.N - n0;  // columns of this chunk inside the vocabulary
+          uint32_t pk[32];
+          f32x2 s2[2] = {0ull, 0ull};
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            float e0, e1;
+            f2split(ffma2(f2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1])), lg2, ncl), e0, e1);
+            e0 = ex2_approx(e0);
+            e1 = ex2_approx(e1);
+            if (nval < 64) {
+              e0 = 2 * j < nval ? e0 : 0.f;
+              e1 = 2 * j + 1 < nval ? e1 : 0.f;
+            }
+            s2[j & 1] = fadd2(s2[j & 1], f2(e0, e1));
+            pk[j] = pack_bf16(e0, e1);
+          }
+          float sa, sb;
+          f2split(fadd2(s2[0], s2[1]), sa, sb);
+          const float sc = sa + sb;
+          ps += sc;
+          if (rok && !(sc <= kXentGuardExp)) {  // a logit too far above the shift (rare): flag a rerun
+            float lm = -INFINITY;
+#pragma unroll
+            for (int j = 0; j < 64; ++j)
+              if (j < nval) lm = fmaxf(lm, __uint_as_float(r[j]));
+            atomicMax(p.xent.vmax + mrow, f2ord(lm));
+            *p.xent.flag = 1;
+          }
+          if (p.xent.store) store_bf16_chunk(pk, &tmap_c, n0, m0);
+        }
+        if (rok) p.xent.psum[static_cast<size_t>(w.nb * EH + eh) * p.M + mrow] = ps;
+      } else if constexpr (EPI == kSwiGLU) {
         // gate columns [c0, c0+64) and the matching up columns [BN/2 + c0, ...)
 #pragma unroll 1
         for (int c0 = eh * (BN / 2 / EH); c0 < (eh + 1) * (BN / 2 / EH); c0 += 64) {
@@ -442,7 +521,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI, NCTA), 1)
           const int n0 = w.nb * BN + c * 64;
           if (lane == 0) {
             const int nu = c + 1 < NCH ? u : u + ustep;
-            if (nu < p.units) {
+            if (nu < units) {
               bulk_wait_read<0>();  // chunk cc-1's stores have left the pair we refill
               prefetch(nu, c + 1 < NCH ? c + 1 : 0, cc + 1);
             }
@@ -493,6 +572,8 @@ __global__ void __launch_bounds__(gemm_threads(EPI, NCTA), 1)
           }
         }
       } else {
+      float rsc = p.alpha;  // kStoreF32 with a per-row scale: this lane's row
+      if (EPI == kStoreF32 && p.row_scale) rsc = m0 + lane < p.M ? __ldg(p.row_scale + m0 + lane) : 0.f;
 #pragma unroll 1
       for (int c0 = eh * (BN / EH); c0 < (eh + 1) * (BN / EH); c0 += CW) {
         uint32_t r[CW];
@@ -537,10 +618,10 @@ __global__ void __launch_bounds__(gemm_threads(EPI, NCTA), 1)
             c = pack_bf16(__uint_as_float(r[8 * j + 4]) * p.alpha, __uint_as_float(r[8 * j + 5]) * p.alpha);
             d = pack_bf16(__uint_as_float(r[8 * j + 6]) * p.alpha, __uint_as_float(r[8 * j + 7]) * p.alpha);
           } else {
-            a = __float_as_uint(__uint_as_float(r[4 * j + 0]) * p.alpha);
-            b = __float_as_uint(__uint_as_float(r[4 * j + 1]) * p.alpha);
-            c = __float_as_uint(__uint_as_float(r[4 * j + 2]) * p.alpha);
-            d = __float_as_uint(__uint_as_float(r[4 * j + 3]) * p.alpha);
+            a = __float_as_uint(__uint_as_float(r[4 * j + 0]) * rsc);
+            b = __float_as_uint(__uint_as_float(r[4 * j + 1]) * rsc);
+            c = __float_as_uint(__uint_as_float(r[4 * j + 2]) * rsc);
+            d = __float_as_uint(__uint_as_float(r[4 * j + 3]) * rsc);
           }
           st_shared_v4(row + ((j ^ (lane & 7)) << 4), a, b, c, d);
         }
@@ -761,7 +842,7 @@ void launch_t(const GemmDesc& g, int splits, cudaStream_t s) {
                               : tma::make_2d_bf16(g.A, g.K, g.M, g.lda, 64, BM);
   const CUtensorMap tb = B_MN ? tma::make_2d_bf16(g.B, g.N, g.K, g.ldb, 64, 64)
                               : tma::make_2d_bf16(g.B, g.K, g.N, g.ldb, 64, BN / NCTA);
-  const bool c_bf16 = EPI == kStoreBF16 || EPI == kSwiGLU || EPI == kSwiGLUBwd;
+  const bool c_bf16 = EPI == kStoreBF16 || EPI == kSwiGLU || EPI == kSwiGLUBwd || EPI == kXentFwd;
   // kSwiGLUBwd: C = dgu [M x 2f] although the GEMM's N is f
   const CUtensorMap tcm = c_bf16 ? tma::make_2d_bf16(g.C, EPI == kSwiGLUBwd ? 2 * g.N : g.N, g.M, g.ldc, 64, 32)
                                  : tma::make_2d_f32(g.C, g.N, g.M, g.ldc, 32, 32);
@@ -792,6 +873,12 @@ void launch_t(const GemmDesc& g, int splits, cudaStream_t s) {
   p.rope_cols = g.rope_cols;
   p.f = EPI == kSwiGLU ? g.N / 2 : g.N;
   p.gu = EPI == kSwiGLUBwd ? static_cast<const __nv_bfloat16*>(g.aux) : nullptr;
+  p.row_scale = g.row_scale;
+  p.gate = g.gate;
+  p.xent = g.xent;
+  if (EPI == kXentFwd && (!g.xent.labels || !g.xent.c || !g.xent.vmax || !g.xent.psum || !g.xent.ly || !g.xent.flag))
+    raise(1, "gemm_bf16: the cross-entropy epilogue needs labels, c, vmax, psum, ly and flag");
+  if (g.row_scale && EPI != kStoreF32) raise(1, "gemm_bf16: row_scale needs the fp32 store epilogue");
   if constexpr (EPI == kSwiGLU || EPI == kSwiGLUBwd) {
     if (!g.aux) raise(1, "gemm_bf16: the SwiGLU epilogues need aux");
     if (EPI == kSwiGLU && (g.N % BN != 0 || (g.N / 2) % (BN / 2) != 0))
@@ -845,6 +932,9 @@ void dispatch_bn(const GemmDesc& g, int splits, cudaStream_t s) {
   CKF_GEMM_EPIS(true, true)
   CKF_GEMM_CASE(false, true, kSwiGLU)
   CKF_GEMM_CASE(false, false, kSwiGLUBwd)
+  if constexpr (BN == 256 && NCTA == 2) {  // the partial-sum layout assumes 256-wide pair tiles, 8 warps
+    CKF_GEMM_CASE(false, true, kXentFwd)
+  }
 #undef CKF_GEMM_EPIS
 #undef CKF_GEMM_CASE
   raise(1, "gemm_bf16: unsupported epilogue");
@@ -868,6 +958,10 @@ void gemm_bf16(const GemmDesc& g, cudaStream_t s) {
   if (reinterpret_cast<uintptr_t>(g.C) % 16) raise(1, "gemm_bf16: C must be 16-byte aligned");
   if (g.ldc % 8 != 0 && (g.epi == kStoreBF16 || g.epi == kSwiGLU || g.epi == kSwiGLUBwd))
     raise(1, "gemm_bf16: bf16 C needs ldc % 8 == 0");
+  if (g.epi == kXentFwd) {
+    if (g.a_mn || !g.b_mn || g.splits > 1) raise(1, "gemm_bf16: the cross-entropy epilogue needs A K-major, B MN-major");
+    return dispatch_bn<256, 2>(g, 1, s);
+  }
   int bn = g.bn ? g.bn : pick_bn(g.M, g.N);
   // Split-K (deterministic workspace reduction) only for the fp32-accumulate (weight-gradient)
   // epilogue, and only when no tile width fills the GPU: measured on B200

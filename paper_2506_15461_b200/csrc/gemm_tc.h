@@ -12,7 +12,27 @@ namespace ckf::tc {
 // kSwiGLUBwd (down-projection dgrad da = dh Wd^T, N = f): da never leaves the SM; the
 //   epilogue reads g, u from aux = gu [M x 2f] and stores dgu = [dg | du] (bf16, C, ldc 2f).
 //   Both are element-for-element the unfused swiglu_fwd / swiglu_bwd kernels.
-enum Epi { kStoreBF16 = 0, kStoreF32 = 1, kAccF32 = 2, kSwiGLU = 3, kSwiGLUBwd = 4 };
+// kXentFwd (LM head forward, A = xn K-major, B = E_inv MN-major, N = V; CTA pairs, 256-wide
+//   tiles, 8 epilogue warps): the logits never leave the SM.  Per row i with shift c_i
+//   (xent.c, max'ed with the decoded xent.vmax) the epilogue forms e = exp(l - c_i) in fp32,
+//   stores Q = bf16(e) into C when xent.store (the loss gradient up to a row scale, see
+//   head_xent.cu), writes the fp32 partial row sum of e of each 128-column half tile to
+//   xent.psum[(nb * 2 + half) * M + i], the fp32 logit of the label column to xent.ly[i], and
+//   -- when a logit exceeds c_i + kXentGuard -- raises xent.flag and atomically maxes the
+//   row's logit into xent.vmax (ordered-int encoding) so a gated rerun can use the true max.
+enum Epi { kStoreBF16 = 0, kStoreF32 = 1, kAccF32 = 2, kSwiGLU = 3, kSwiGLUBwd = 4, kXentFwd = 5 };
+constexpr float kXentGuard = 50.f;
+// number of per-row partial sums kXentFwd writes for a vocabulary of V columns
+inline int xent_partials(int V) { return 2 * ((V + 255) / 256); }
+struct XentArgs {
+  const int* labels = nullptr;  // [M] label column of each row
+  const float* c = nullptr;     // [M] per-row shift
+  int* vmax = nullptr;          // [M] ordered-int max of guard-violating logits (sentinel = none)
+  float* psum = nullptr;        // [xent_partials(N) x M]
+  float* ly = nullptr;          // [M] label logit
+  int* flag = nullptr;          // set to 1 on a guard violation
+  int store = 1;                // store Q (training) or not (loss only)
+};
 
 // C[M,N] (epi) alpha * op(A) op(B), bf16 operands, fp32 accumulation.
 //   a_mn = false: A stored [M][lda] (K contiguous); true: A stored [K][lda] (M contiguous)
@@ -39,6 +59,12 @@ struct GemmDesc {
   int rope_T = 0, rope_cols = 0;
   void* aux = nullptr;  // kSwiGLU: a (written); kSwiGLUBwd: gu (read)
   int ldaux = 0;
+  // kStoreF32: per-row output scale (C[i,:] = row_scale[i] * acc) instead of alpha
+  const float* row_scale = nullptr;
+  // launch gate: when non-null the kernel reads *gate after its predecessor finished and does no
+  // work if it is 0 (a rerun that a device flag decides, without a host round trip)
+  const int* gate = nullptr;
+  XentArgs xent;
 };
 
 void gemm_bf16(const GemmDesc& g, cudaStream_t s);

@@ -245,7 +245,9 @@ struct LlamaBlock final : BlockImpl {
     for (size_t i = 0; i < D.s; ++i)
       if (eng->mine(eng->owner_of_stage(static_cast<int>(i + 1)))) layers += D.part[i].count();
     const size_t per_layer = 8 * d + 8 + 4 * H + 6 * d + 4 * f + 8 * d + 4 * f;  // + X when not deferred
-    return layers * per_layer + 2 * V + 8 + 26 * d + 2 * std::max(d, f) + 4 * H + 64;
+    // head: Q (2 V) + the fused loss's partial sums and row scalars + xs (head_xent_workspace)
+    const size_t head = 2 * V + 4 * std::max<size_t>(tc::xent_partials(static_cast<int>(V)), 256) + 24 + 2 * d;
+    return layers * per_layer + head + 8 + 26 * d + 2 * std::max(d, f) + 4 * H + 64;
   }
 
   void flush_grads() override {
@@ -287,14 +289,69 @@ struct LlamaBlock final : BlockImpl {
     g.C = C;
     g.ldc = ldc;
     g.epi = epi;
+    gemm_desc(g);
+  }
+  void gemm_desc(const tc::GemmDesc& g) {
     eng->kt_begin();
     tc::gemm_bf16(g, eng->stream());
     // bytes of C per output element: bf16 store; fp32 store; fp32 read+write; SwiGLU fwd
     // (g, u stored + a: 3 bf16 per gate/up pair = 3 B per output); SwiGLU bwd (g, u read, dg, du written)
-    const double cb = epi == tc::kStoreBF16 ? 2.0 : epi == tc::kStoreF32 ? 4.0 : epi == tc::kAccF32 ? 8.0
-                    : epi == tc::kSwiGLU ? 3.0 : 8.0;
-    eng->kt_end(KC_GEMM, 2.0 * M * N * K,
-                2.0 * (static_cast<double>(M) * K + static_cast<double>(K) * N) + cb * M * N);
+    const int epi = g.epi;
+    const double M = g.M, N = g.N, K = g.K;
+    const double cb = epi == tc::kStoreBF16 || epi == tc::kXentFwd ? 2.0 : epi == tc::kStoreF32 ? 4.0
+                    : epi == tc::kAccF32 ? 8.0 : epi == tc::kSwiGLU ? 3.0 : 8.0;
+    eng->kt_end(KC_GEMM, 2.0 * M * N * K, 2.0 * (M * K + K * N) + cb * M * N);
+  }
+
+  // LM head + mean token cross-entropy, and (train) the head backward into gE_inv and dxn
+  // (model.cpp:250-253, 322-342; kernels_serial.cpp:163-185).  Fused (head_xent.cu: no logits
+  // tensor, no pass over [tokens x V] outside the GEMMs) unless CKF_HEAD_FUSED=0 selects the
+  // bf16-logits path (logits GEMM -> xent_bf16 in place -> GEMMs on the bf16 gradient).
+  static bool head_fused() {
+    static const bool v = [] {
+      const char* e = std::getenv("CKF_HEAD_FUSED");
+      return !(e && e[0] == '0');
+    }();
+    return v;
+  }
+  void head(const bf16* xnF, const float* hF, const float* rstdF, const float* gF, const bf16* Einv, const int* lab,
+            size_t Mt, size_t Mmb, bool train, double* row_loss, double* loss_dev, float* dxn, float* gde) {
+    cudaStream_t st = eng->stream();
+    const int Mi = static_cast<int>(Mt), di = static_cast<int>(d), Vi = static_cast<int>(V);
+    const float gs = static_cast<float>(1.0 / static_cast<double>(Mmb));
+    if (head_fused()) {
+      llama::HeadXent hx;
+      hx.xn = xnF;
+      hx.Einv = Einv;
+      hx.labels = lab;
+      hx.M = Mi;
+      hx.d = di;
+      hx.V = Vi;
+      hx.grad_scale = gs;
+      hx.train = train;
+      hx.row_loss = row_loss;
+      hx.dxn = dxn;
+      hx.gEinv = gde + d;
+      hx.ws = eng->ws(llama::head_xent_workspace(Mt, d, V), 53);
+      hx.h = hF;
+      hx.rstd = rstdF;
+      hx.gain = gF;
+      const double P = tc::xent_partials(Vi);
+      llama::head_xent(
+          hx, [&](const tc::GemmDesc& g) { gemm_desc(g); },
+          [&](const std::function<void()>& f) { timed(KC_LOSS, 0.0, Mt * (P * 4.0 + 4.0 * d + 24.0), f); }, st);
+      timed(KC_LOSS, 0.0, Mt * 8.0, [&] { llama::fold_mean(row_loss, Mt, 1.0 / static_cast<double>(Mmb), loss_dev, st); });
+      return;
+    }
+    bf16* logits = buf<bf16>(53, Mt * V);
+    gemm(Mi, Vi, di, xnF, di, false, Einv, Vi, true, logits, Vi, tc::kStoreBF16);
+    timed(KC_LOSS, 0.0, Mt * V * (train ? 6.0 : 2.0), [&] {
+      llama::xent_bf16(logits, lab, Mt, V, gs, train ? 1 : 0, row_loss, st);
+      llama::fold_mean(row_loss, Mt, 1.0 / static_cast<double>(Mmb), loss_dev, st);  // sum of microbatch means
+    });
+    if (!train) return;
+    gemm(di, Vi, Mi, xnF, di, true, logits, Vi, true, gde + d, Vi, tc::kAccF32);
+    gemm(Mi, di, Vi, logits, Vi, false, Einv, Vi, false, dxn, di, tc::kStoreF32);
   }
   template <typename F>
   void timed(int cls, double flops, double bytes, F&& f) {
@@ -333,7 +390,6 @@ struct LlamaBlock final : BlockImpl {
     const size_t Mmb = loss_rows ? loss_rows * T : Mt;  // tokens of ONE microbatch (fused groups carry several)
     if (Mmb > D.max_rows) raise(1, "microbatch tokens exceed the engine's max_rows (tokens per microbatch)");
     const int* x = static_cast<const int*>(xv);
-    const int Mi = static_cast<int>(Mt), di = static_cast<int>(d), Vi = static_cast<int>(V);
 
     int* tok = buf<int>(slot_id(mb, 0), Mt);
     int* lab = buf<int>(slot_id(mb, 1), Mt);
@@ -346,7 +402,6 @@ struct LlamaBlock final : BlockImpl {
     bf16* xnF = buf<bf16>(50, Mt * d);
     float* rstdF = buf<float>(51, Mt);
     float* hF = buf<float>(52, Mt * d);
-    bf16* logits = buf<bf16>(53, Mt * V);
     double* row_loss = buf<double>(54, Mt);
 
     llama::split_tokens(x, rows, T, tok, lab, st);
@@ -377,17 +432,10 @@ struct LlamaBlock final : BlockImpl {
     const float* gF = static_cast<const float*>(eng->deembed().w);
     const bf16* Einv = eng->deembed().wlp + d;
     timed(KC_NORM, 0.0, Mt * d * 10.0, [&] { llama::rmsnorm_fwd(h, gF, Mt, d, xnF, rstdF, hF, st); });
-    gemm(Mi, Vi, di, xnF, di, false, Einv, Vi, true, logits, Vi, tc::kStoreBF16);
-    timed(KC_LOSS, 0.0, Mt * V * (train ? 6.0 : 2.0), [&] {
-      llama::xent_bf16(logits, lab, Mt, V, static_cast<float>(1.0 / static_cast<double>(Mmb)), train ? 1 : 0,
-                       row_loss, st);
-      llama::fold_mean(row_loss, Mt, 1.0 / static_cast<double>(Mmb), loss_dev, st);  // sum of microbatch means
-    });
-    if (!train) return;
-    // head backward (model.cpp:322-342): gE_inv += xnF^T dlogits, dh_final = rmsnorm'(dlogits E_inv^T)
+    // head, loss and head backward (model.cpp:322-342): gE_inv += xnF^T dlogits, dxn = dlogits E_inv^T
     float* gde = static_cast<float*>(eng->deembed().g);
-    gemm(di, Vi, Mi, xnF, di, true, logits, Vi, true, gde + d, Vi, tc::kAccF32);
-    gemm(Mi, di, Vi, logits, Vi, false, Einv, Vi, false, dxn, di, tc::kStoreF32);
+    head(xnF, hF, rstdF, gF, Einv, lab, Mt, Mmb, train, row_loss, loss_dev, dxn, gde);
+    if (!train) return;
     CKF_CUDA(cudaMemsetAsync(dh, 0, Mt * d * 4, st));
     timed(KC_NORM, 0.0, Mt * d * 18.0, [&] {
       llama::rmsnorm_bwd(dxn, hF, gF, rstdF, Mt, d, dh, dh_bf, gpart, st);
@@ -501,7 +549,6 @@ struct LlamaBlock final : BlockImpl {
   void plan_op(int kind, int k, int sid, const int* order, double* loss_dev) override {
     cudaStream_t st = eng->stream();
     const size_t rows = prows_, Mt = rows * T;
-    const int Mi = static_cast<int>(Mt), di = static_cast<int>(d), Vi = static_cast<int>(V);
     const int* tok = ptok_ + static_cast<size_t>(k) * Mt;
     const int* lab = plab_ + static_cast<size_t>(k) * Mt;
     const int slot = k % pslots_;
@@ -534,19 +581,12 @@ struct LlamaBlock final : BlockImpl {
         bf16* xnF = buf<bf16>(50, Mt * d);
         float* rstdF = buf<float>(51, Mt);
         float* hF = buf<float>(52, Mt * d);
-        bf16* logits = buf<bf16>(53, Mt * V);
         double* row_loss = buf<double>(54, Mt);
         const float* gF = static_cast<const float*>(eng->deembed().w);
         const bf16* Einv = eng->deembed().wlp + d;
         timed(KC_NORM, 0.0, Mt * d * 10.0, [&] { llama::rmsnorm_fwd(h, gF, Mt, d, xnF, rstdF, hF, st); });
-        gemm(Mi, Vi, di, xnF, di, false, Einv, Vi, true, logits, Vi, tc::kStoreBF16);
-        timed(KC_LOSS, 0.0, Mt * V * 6.0, [&] {
-          llama::xent_bf16(logits, lab, Mt, V, static_cast<float>(1.0 / static_cast<double>(Mt)), 1, row_loss, st);
-          llama::fold_mean(row_loss, Mt, 1.0 / static_cast<double>(Mt), loss_dev, st);
-        });
         float* gde = static_cast<float*>(eng->deembed().g);
-        gemm(di, Vi, Mi, xnF, di, true, logits, Vi, true, gde + d, Vi, tc::kAccF32);
-        gemm(Mi, di, Vi, logits, Vi, false, Einv, Vi, false, dxn, di, tc::kStoreF32);
+        head(xnF, hF, rstdF, gF, Einv, lab, Mt, Mt, true, row_loss, loss_dev, dxn, gde);
         CKF_CUDA(cudaMemsetAsync(dh, 0, Mt * d * 4, st));
         timed(KC_NORM, 0.0, Mt * d * 18.0, [&] {
           llama::rmsnorm_bwd(dxn, hF, gF, rstdF, Mt, d, dh, dh_bf, gpart, st);

@@ -8,6 +8,9 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <functional>
+
+#include "gemm_tc.h"
 
 namespace ckf::llama {
 
@@ -50,6 +53,31 @@ void swiglu_bwd(const bf16* gu, const bf16* da, size_t ntok, size_t f, bf16* dgu
 // overwritten (in place) with (softmax - onehot) * grad_scale when grad != 0
 void xent_bf16(bf16* logits, const int* labels, size_t rows, size_t V, float grad_scale, int grad, double* row_loss,
                cudaStream_t s);
+// fused LM head + cross-entropy (head_xent.cu): row_loss[i] = lse_i - l_i,label (fp64), and when
+// train: dxn = dlogits E_inv^T (fp32 store), gEinv += xn^T dlogits, dlogits = grad_scale (softmax -
+// onehot) -- without a logits tensor.  xn [M x d] bf16, Einv [d x V] bf16 (row pitch V); ws >=
+// head_xent_workspace(M, d, V) bytes.  gemm runs each GEMM (the caller's timing wrapper around
+// tc::gemm_bf16); loss_kernels wraps the two small kernels likewise.
+struct HeadXent {
+  const bf16* xn = nullptr;
+  const bf16* Einv = nullptr;
+  const int* labels = nullptr;
+  int M = 0, d = 0, V = 0;
+  float grad_scale = 1.f;
+  bool train = true;
+  double* row_loss = nullptr;
+  float* dxn = nullptr;
+  float* gEinv = nullptr;
+  void* ws = nullptr;
+  // optional: the fp32 rows xn was normalised from (xn = bf16(h rstd g)); then the scaled copy for
+  // the weight gradient is ONE rounding of s h rstd g instead of a second rounding of xn
+  const float* h = nullptr;
+  const float* rstd = nullptr;
+  const float* gain = nullptr;
+};
+size_t head_xent_workspace(size_t M, size_t d, size_t V);
+void head_xent(const HeadXent& h, const std::function<void(const tc::GemmDesc&)>& gemm,
+               const std::function<void(const std::function<void()>&)>& loss_kernels, cudaStream_t s);
 // *out = scale * sum(row_loss[0..rows)) in fixed order
 void fold_mean(const double* row_loss, size_t rows, double scale, double* out, cudaStream_t s);
 

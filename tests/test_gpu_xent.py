@@ -39,3 +39,90 @@ def test_xent_bf16_matches_torch_fp32(rows, V):
     torch.cuda.synchronize()
     assert torch.equal(keep, logits)
     assert torch.equal(row2, row_loss)
+
+
+# ------------------------------------------------------------------ fused LM head + cross-entropy
+# head_xent.cu via ckf_lm_head_xent: logits = xn E_inv never materialised; against torch fp32 of
+# the same op (loss, dxn = dlogits E_inv^T, gE_inv = xn^T dlogits).  The unfused path's own error
+# (bf16 logits -> xent_bf16 -> the two GEMMs on bf16 dlogits) is measured beside it: the fused
+# gradients round each operand once, like it, and must be as close to fp32.
+def _head_case(M, d, V, spike=False, seed=0):
+    g = torch.Generator(device="cuda").manual_seed(seed + M + V)
+    h = torch.randn(M, d, device="cuda", generator=g) * 3.0
+    gain = 1.0 + 0.1 * torch.randn(d, device="cuda", generator=g)
+    rstd = torch.rsqrt(h.pow(2).mean(dim=1) + 1e-5)
+    xn = (h * rstd[:, None] * gain).bfloat16()
+    E = (torch.randn(d, V, device="cuda", generator=g) * (2.0 / d ** 0.5)).bfloat16()
+    if spike:  # column 3000 aligned with row 0: its logit sits ~200 above the first-tile maximum
+        E[:, 3000] = (xn[0].float() * (200.0 / xn[0].float().pow(2).sum())).bfloat16()
+    labels = torch.randint(0, V, (M,), device="cuda", generator=g, dtype=torch.int32)
+    return xn, E, labels, (h, rstd, gain)
+
+
+def _head_fused(xn, E, labels, scale, train, rows=None):
+    from paper_2506_15461_b200._native import check, lib
+    M, d = xn.shape
+    V = E.shape[1]
+    ws = torch.empty(lib().ckf_lm_head_xent_workspace(M, d, V), dtype=torch.uint8, device="cuda")
+    row_loss = torch.zeros(M, device="cuda", dtype=torch.float64)
+    dxn = torch.full((M, d), float("nan"), device="cuda")
+    gE = torch.zeros(d, V, device="cuda")
+    h, rstd, gain = (t.data_ptr() for t in rows) if rows is not None else (None, None, None)
+    check(lib().ckf_lm_head_xent(xn.data_ptr(), E.data_ptr(), labels.data_ptr(), M, d, V, scale, int(train),
+                                 row_loss.data_ptr(), dxn.data_ptr(), gE.data_ptr(), h, rstd, gain, ws.data_ptr(),
+                                 None))
+    torch.cuda.synchronize()
+    return row_loss, dxn, gE
+
+
+def _rel(a, b):
+    return ((a - b).norm() / b.norm()).item()
+
+
+@pytest.mark.parametrize("M,d,V,spike", [(300, 256, 50304, False), (64, 128, 512, False), (1000, 1024, 50304, False),
+                                         (257, 128, 4096, True)])
+def test_fused_head_xent_matches_torch_fp32(M, d, V, spike):
+    from paper_2506_15461_b200._native import check, lib
+    xn, E, labels, rows = _head_case(M, d, V, spike)
+    scale = 1.0 / M
+    x32, E32 = xn.float(), E.float()
+    logits = x32 @ E32
+    lse = torch.logsumexp(logits, dim=1)
+    ref_loss = lse - logits.gather(1, labels.long()[:, None])[:, 0]
+    dl = (torch.softmax(logits, dim=1) - torch.nn.functional.one_hot(labels.long(), V).float()) * scale
+    ref_dxn = dl @ E32.t()
+    # the weight gradient against the unrounded rows (both paths round them once)
+    h, rstd, gain = rows
+    ref_gE = (h * rstd[:, None] * gain).t() @ dl
+
+    # the unfused path on the same inputs, as the engine ran it: bf16 logits, xent_bf16 in place, the
+    # two tcgen05 GEMMs on the bf16 gradient (dgrad fp32 store, wgrad fp32 accumulate)
+    lg = logits.bfloat16()
+    rl = torch.zeros(M, device="cuda", dtype=torch.float64)
+    check(lib().ckf_xent_bf16(lg.data_ptr(), labels.data_ptr(), M, V, scale, 1, rl.data_ptr(), None))
+    u_dxn_t = torch.empty(M, d, device="cuda")
+    u_gE_t = torch.zeros(d, V, device="cuda")
+    check(lib().ckf_gemm_bf16(M, d, V, lg.data_ptr(), V, 0, E.data_ptr(), V, 0, u_dxn_t.data_ptr(), d, 1, 1.0, 0, None))
+    check(lib().ckf_gemm_bf16(d, V, M, xn.data_ptr(), d, 1, lg.data_ptr(), V, 1, u_gE_t.data_ptr(), V, 2, 1.0, 0, None))
+    torch.cuda.synchronize()
+    u_dxn, u_gE = _rel(u_dxn_t, ref_dxn), _rel(u_gE_t, ref_gE)
+
+    for with_rows in (True, False):
+        row_loss, dxn, gE = _head_fused(xn, E, labels, scale, True, rows if with_rows else None)
+        assert torch.isfinite(dxn).all() and torch.isfinite(gE).all()
+        loss_err = ((row_loss.float() - ref_loss).abs() / (1.0 + ref_loss.abs())).max().item()
+        e_dxn, e_gE = _rel(dxn, ref_dxn), _rel(gE, ref_gE)
+        print(f"fused head M={M} d={d} V={V} spike={spike} rows={with_rows}: loss {loss_err:.2e}, "
+              f"dxn {e_dxn:.2e} (unfused {u_dxn:.2e}), gE {e_gE:.2e} (unfused {u_gE:.2e})")
+        # Bars: the loss from fp32 logits (measured <= 8e-7); each gradient operand is one bf16
+        # rounding (2^-9 relative, RMS ~1.1e-3) -- measured 1.6-1.7e-3 (dxn) and 2.1-2.4e-3 (gE; 2.6-3.0e-3
+        # from xn, rounded twice).  The unfused path's error is the same size but depends on how bf16
+        # represents 1/M: all its label entries round alike (M = 1000: 7.4e-4, M = 300: 2.1e-3).
+        assert loss_err <= 2e-5, loss_err
+        assert e_dxn <= 3e-3 and u_dxn <= 3e-3, (e_dxn, u_dxn)
+        assert e_gE <= (3e-3 if with_rows else 4e-3) and u_gE <= 3e-3, (e_gE, u_gE)
+
+    # loss only: the same row losses, no gradient written
+    rl2, dxn2, gE2 = _head_fused(xn, E, labels, scale, False)
+    assert torch.equal(rl2, row_loss)
+    assert torch.isnan(dxn2).all() and (gE2 == 0).all()
