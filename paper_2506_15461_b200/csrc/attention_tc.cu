@@ -634,7 +634,9 @@ __global__ void __launch_bounds__(128 + 256 * SPLIT, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.s_free[grp]);
-        mbar_wait(&sm.pd_free[grp], ((gi >> 1) & 1) ^ 1);  // this group's previous dV/dK MMAs read P / dS
+        // P^T / dS^T are computed into packed registers while this group's previous dV / dK MMAs
+        // may still be reading the shared buffers; the wait for them comes just before the stores
+        uint32_t pkp[QW / 2], pkd[QW / 2];
         const uint32_t rowoff = static_cast<uint32_t>(r * 128);
         const uint32_t la_ = smem_u32(&sm.lse[st][0]), da_ = smem_u32(&sm.dsum[st][0]);
 #pragma unroll
@@ -672,11 +674,19 @@ __global__ void __launch_bounds__(128 + 256 * SPLIT, 1)
             for (int e = 0; e < 8; ++e)
               if (PT * i + 8 * g8 + e < r) pv[e] = dv[e] = 0.f;
           }
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            pkp[4 * lg + e] = pack_bf16(pv[2 * e], pv[2 * e + 1]);
+            pkd[4 * lg + e] = pack_bf16(dv[2 * e], dv[2 * e + 1]);
+          }
+        }
+        mbar_wait(&sm.pd_free[grp], ((gi >> 1) & 1) ^ 1);  // this group's previous dV/dK MMAs read P / dS
+#pragma unroll
+        for (int lg = 0; lg < QW / 8; ++lg) {
+          const int g8 = half * (QW / 8) + lg;
           const uint32_t off = rowoff + ((g8 ^ (r & 7)) << 4);
-          st_shared_v4(pbase + off, pack_bf16(pv[0], pv[1]), pack_bf16(pv[2], pv[3]), pack_bf16(pv[4], pv[5]),
-                       pack_bf16(pv[6], pv[7]));
-          st_shared_v4(dbase + off, pack_bf16(dv[0], dv[1]), pack_bf16(dv[2], dv[3]), pack_bf16(dv[4], dv[5]),
-                       pack_bf16(dv[6], dv[7]));
+          st_shared_v4(pbase + off, pkp[4 * lg], pkp[4 * lg + 1], pkp[4 * lg + 2], pkp[4 * lg + 3]);
+          st_shared_v4(dbase + off, pkd[4 * lg], pkd[4 * lg + 1], pkd[4 * lg + 2], pkd[4 * lg + 3]);
         }
         fence_proxy_async();
         __syncwarp();
@@ -889,7 +899,7 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.s_free[grp]);
-        mbar_wait(&sm.ds_free[grp], ((gj >> 1) & 1) ^ 1);
+        uint32_t pkd[32];  // dS computed before the wait for this group's previous dQ MMA (see dK dV)
         const uint32_t rowoff = static_cast<uint32_t>(r * 128);
         const bool diag = j >= 2 * qb;  // keys 64 j + c vs query qb*128 + r: visible iff 64 j + c <= 128 qb + r
 #pragma unroll
@@ -916,9 +926,14 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
             for (int e = 0; e < 8; ++e)
               if (PT * j + 8 * g8 + e > TQ * qb + r) dv[e] = 0.f;
           }
-          st_shared_v4(dbase + rowoff + ((g8 ^ (r & 7)) << 4), pack_bf16(dv[0], dv[1]), pack_bf16(dv[2], dv[3]),
-                       pack_bf16(dv[4], dv[5]), pack_bf16(dv[6], dv[7]));
+#pragma unroll
+          for (int e = 0; e < 4; ++e) pkd[4 * g8 + e] = pack_bf16(dv[2 * e], dv[2 * e + 1]);
         }
+        mbar_wait(&sm.ds_free[grp], ((gj >> 1) & 1) ^ 1);
+#pragma unroll
+        for (int g8 = 0; g8 < 8; ++g8)
+          st_shared_v4(dbase + rowoff + ((g8 ^ (r & 7)) << 4), pkd[4 * g8], pkd[4 * g8 + 1], pkd[4 * g8 + 2],
+                       pkd[4 * g8 + 3]);
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.ds_full[grp]);
