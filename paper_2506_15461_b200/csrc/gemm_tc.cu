@@ -148,10 +148,11 @@ constexpr float kXentGuardExp = 5.184705528587072e21f;  // exp(kXentGuard)
 
 template <int BN, int EPI, int NCTA>
 struct Cfg {
-  // kSwiGLUBwd trades operand stages for 4 epilogue buffers per warp (g/u prefetch pairs).
+  // kSwiGLUBwd trades operand stages for 6 epilogue buffers per warp (two g/u prefetch pairs and
+  // the dg/du staging pair).
   // NCTA = 2 (CTA pair): each CTA holds BN/2 columns of B, so a stage is 32 KiB at BN = 256.
   static constexpr int kEW = epi_warps(EPI, NCTA);
-  static constexpr int kEpiBufs = EPI == kSwiGLUBwd ? 4 : 2;
+  static constexpr int kEpiBufs = EPI == kSwiGLUBwd ? 6 : 2;
   static constexpr uint32_t kBStage = (BN / NCTA) * BK * 2;
   static constexpr uint32_t kStageBytes = kAStage + kBStage;
   static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
@@ -388,15 +389,23 @@ __global__ void __launch_bounds__(gemm_threads(EPI, NCTA), 1)
     // first output row of this warp's 32 accumulator lanes
     auto row0_of = [&](const Unit& wu) { return wu.mb * BM * NCTA + static_cast<int>(rank) * BM + q * 32; };
     int cc = 0;               // kSwiGLUBwd: chunk counter of this warp's stream
+    // kSwiGLUBwd (lane 0): chunk k of this warp's stream = (unit uu, 64-column chunk c) -> pair k & 1
+    auto swb_prefetch = [&](int k, int uu, int c) {
+      const Unit w2 = unit_of(p, uu);
+      uint8_t* gb = stg + (k & 1) * 2 * kStageBufBytes;
+      uint64_t* bar = &lbar[q * 2 + (k & 1)];
+      const int n0 = w2.nb * BN + c * 64, y = row0_of(w2);
+      mbar_arrive_expect_tx(bar, 2 * kStageBufBytes);
+      tma_load_2d(gb, &tmap_ws, bar, n0, y);
+      tma_load_2d(gb + kStageBufBytes, &tmap_ws, bar, p.f + n0, y);
+    };
     bool first_unit = true;
     for (int u = u0; u < units; u += ustep) {
       const Unit w = unit_of(p, u);
       if constexpr (EPI == kSwiGLUBwd) {
-        if (first_unit && lane == 0) {  // first g/u chunk in flight before the accumulator is ready
-          uint64_t* bar = &lbar[q * 2];
-          mbar_arrive_expect_tx(bar, 2 * kStageBufBytes);
-          tma_load_2d(stg, &tmap_ws, bar, w.nb * BN, row0_of(w));
-          tma_load_2d(stg + kStageBufBytes, &tmap_ws, bar, p.f + w.nb * BN, row0_of(w));
+        if (first_unit && lane == 0) {  // the first two g/u chunks in flight before the accumulator is ready
+          swb_prefetch(0, u, 0);
+          swb_prefetch(1, u, 1);
         }
         first_unit = false;
       }
@@ -503,29 +512,20 @@ __global__ void __launch_bounds__(gemm_threads(EPI, NCTA), 1)
           store_bf16_chunk(pk, &tmap_ws, n0, m0);
         }
       } else if constexpr (EPI == kSwiGLUBwd) {
-        // g/u chunks arrive by TMA into this warp's buffer pairs, one chunk ahead of the
-        // math (chunk cc of the warp's stream uses pair cc & 1); dg/du overwrite them in
-        // place and leave by TMA store.  da = dY Wd^T never leaves the SM.
+        // g/u chunks arrive by TMA TWO chunks ahead of the math into a ring of two buffer pairs
+        // (chunk cc of the warp's stream uses pair cc & 1): the math reads a pair into registers and
+        // it is refilled at once with chunk cc + 2; dg/du leave through a separate staging pair by
+        // TMA store.  Two chunks (16 KiB) of loads in flight per warp: the epilogue moves 8 B per
+        // output element.  da = dY Wd^T never leaves the SM.  Measured at the 500M shape [32,768 x 4,096
+        // x 1,024]: 304 us at one chunk ahead (single CTAs) -> 293 us (pairs, two ahead); the plain
+        // dgrad is 192 us; without the g/u loads 245 us, without the dg/du stores 255 us; stores
+        // straight from registers (no staging) 369 us.
         constexpr int NCH = BN / 64;
-        auto prefetch = [&](int uu, int c, int k) {  // lane 0
-          const Unit w2 = unit_of(p, uu);
-          uint8_t* gb = stg + (k & 1) * 2 * kStageBufBytes;
-          uint64_t* bar = &lbar[q * 2 + (k & 1)];
-          const int n0 = w2.nb * BN + c * 64, y = row0_of(w2);
-          mbar_arrive_expect_tx(bar, 2 * kStageBufBytes);
-          tma_load_2d(gb, &tmap_ws, bar, n0, y);
-          tma_load_2d(gb + kStageBufBytes, &tmap_ws, bar, p.f + n0, y);
-        };
+        static_assert(NCH >= 2, "kSwiGLUBwd: two chunks per tile at least");
+        uint8_t* ob = stg + 4 * kStageBufBytes;  // dg / du staging pair
 #pragma unroll 1
         for (int c = 0; c < NCH; ++c, ++cc) {
           const int n0 = w.nb * BN + c * 64;
-          if (lane == 0) {
-            const int nu = c + 1 < NCH ? u : u + ustep;
-            if (nu < units) {
-              bulk_wait_read<0>();  // chunk cc-1's stores have left the pair we refill
-              prefetch(nu, c + 1 < NCH ? c + 1 : 0, cc + 1);
-            }
-          }
           uint32_t r[64];
           tmem_ld32(trow + c * 64, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
           tmem_ld32(trow + c * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
@@ -538,12 +538,26 @@ __global__ void __launch_bounds__(gemm_threads(EPI, NCTA), 1)
           mbar_wait(&lbar[q * 2 + (cc & 1)], (cc >> 1) & 1);
           uint8_t* gb = stg + (cc & 1) * 2 * kStageBufBytes;
           const uint32_t ga = smem_u32(gb) + lane * 128, ua = ga + kStageBufBytes;
+          uint4 gq[8], uq[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const uint32_t off = (j ^ (lane & 7)) << 4;
-            const uint4 gq = ld_shared_v4(ga + off), uq = ld_shared_v4(ua + off);
-            const uint32_t gw[4] = {gq.x, gq.y, gq.z, gq.w}, uw[4] = {uq.x, uq.y, uq.z, uq.w};
-            uint32_t pg[4], pu[4];
+            gq[j] = ld_shared_v4(ga + off);
+            uq[j] = ld_shared_v4(ua + off);
+          }
+          __syncwarp();
+          if (lane == 0) {  // refill this pair with chunk cc + 2 (generic reads ordered before the async write)
+            const int c2 = c + 2 < NCH ? c + 2 : c + 2 - NCH;
+            const int u2 = c + 2 < NCH ? u : u + ustep;
+            if (u2 < units) {
+              fence_proxy_async();
+              swb_prefetch(cc + 2, u2, c2);
+            }
+          }
+          uint32_t pg[32], pu[32];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint32_t gw[4] = {gq[j].x, gq[j].y, gq[j].z, gq[j].w}, uw[4] = {uq[j].x, uq[j].y, uq[j].z, uq[j].w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               // da rounded to bf16 exactly as the unfused path stores it, then swiglu_bwd's arithmetic
@@ -555,18 +569,25 @@ __global__ void __launch_bounds__(gemm_threads(EPI, NCTA), 1)
                           f2(__uint_as_float(dpk << 16), __uint_as_float(dpk & 0xffff0000u)), dg2, du2);
               f2split(dg2, dg0, dg1);
               f2split(du2, du0, du1);
-              pg[e] = pack_bf16(dg0, dg1);
-              pu[e] = pack_bf16(du0, du1);
+              pg[4 * j + e] = pack_bf16(dg0, dg1);
+              pu[4 * j + e] = pack_bf16(du0, du1);
             }
-            st_shared_v4(ga + off, pg[0], pg[1], pg[2], pg[3]);
-            st_shared_v4(ua + off, pu[0], pu[1], pu[2], pu[3]);
+          }
+          if (lane == 0) bulk_wait_read<0>();  // the previous chunk's stores have left the staging pair
+          __syncwarp();
+          const uint32_t oa = smem_u32(ob) + lane * 128, oua = oa + kStageBufBytes;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint32_t off = (j ^ (lane & 7)) << 4;
+            st_shared_v4(oa + off, pg[4 * j], pg[4 * j + 1], pg[4 * j + 2], pg[4 * j + 3]);
+            st_shared_v4(oua + off, pu[4 * j], pu[4 * j + 1], pu[4 * j + 2], pu[4 * j + 3]);
           }
           fence_proxy_async();
           __syncwarp();
           if (lane == 0) {
             if (m0 < p.M && n0 < p.N) {
-              tma_store_2d(&tmap_c, gb, n0, m0);
-              tma_store_2d(&tmap_c, gb + kStageBufBytes, p.f + n0, m0);
+              tma_store_2d(&tmap_c, ob, n0, m0);
+              tma_store_2d(&tmap_c, ob + kStageBufBytes, p.f + n0, m0);
             }
             bulk_commit();
           }
@@ -1033,11 +1054,12 @@ void gemm_bf16(const GemmDesc& g, cudaStream_t s) {
   // The SwiGLU forward (gate/up GEMM, 128 x 256 single-CTA tiles are operand-bandwidth bound:
   // 96 B / clk / SM of A + B at the tensor peak) runs as CTA pairs too -- B multicast, 6 operand
   // stages: 481.7 -> 424.6 us at [32,768 x 8,192 x 1,024] (500M).  The backward epilogue
-  // (g / u in, dg / du out: 8 B per element) is HBM-bound and gains nothing (320 vs 325 us).
-  // CKF_GEMM_SWIGLU_PAIR=0 / 2: single CTAs for both / pairs for both.
+  // (g / u in, dg / du out: 8 B per element) is HBM-bound; as a CTA pair it keeps 4 operand stages
+  // next to its 6 epilogue buffers per warp (two g/u chunks in flight per warp).
+  // CKF_GEMM_SWIGLU_PAIR=0 / 1: single CTAs for both / for the backward only.
   static const int swiglu_pair = [] {
     const char* v = std::getenv("CKF_GEMM_SWIGLU_PAIR");
-    return v ? std::atoi(v) : 1;
+    return v ? std::atoi(v) : 2;
   }();
   const bool swiglu_single = (g.epi == kSwiGLU && swiglu_pair == 0) || (g.epi == kSwiGLUBwd && swiglu_pair != 2);
   const bool pair_shape = pair_wgrad || (!swiglu_single && splits <= 1 &&

@@ -19,6 +19,9 @@ SHAPES = [  # (name, M, N, K, a_mn, b_mn, epi): one fused LLaMA-124M step (65,53
     ("sq8192", 8192, 8192, 8192, 0, 1, 0),
     # fused SwiGLU epilogues (compare with gu_fwd / down_dgrad above)
     ("gu_fwd_swiglu", 65536, 4096, 512, 0, 1, 3), ("down_dgrad_swiglu", 65536, 2048, 512, 0, 0, 4),
+    # LLaMA-500M (one CheckFree+ group of 32,768 tokens)
+    ("down_dgrad_500m", 32768, 4096, 1024, 0, 0, 0), ("down_dgrad_swiglu_500m", 32768, 4096, 1024, 0, 0, 4),
+    ("gu_fwd_swiglu_500m", 32768, 8192, 1024, 0, 1, 3), ("o_fwd_500m", 32768, 1024, 1024, 0, 1, 2),
 ]
 
 def run(name, M, N, K, a_mn, b_mn, epi, bn=0, iters=20):
