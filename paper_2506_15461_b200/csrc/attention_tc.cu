@@ -12,6 +12,7 @@
 // (tile, head) units longest-first, two inner tiles in flight (ping-pong softmax groups).
 //
 // Warp roles: 0 TMA producer, 1 MMA issuer (one lane), 2 TMEM allocator, 4.. softmax.
+#include <algorithm>
 #include <cstdlib>
 #include <string>
 
@@ -445,11 +446,17 @@ struct SmemKVpp {
 template <int HD, int POLY, int SPLIT>
 __global__ void __launch_bounds__(128 + 256 * SPLIT, 1)
     attn_dkdv_pp_kernel(const __grid_constant__ CUtensorMap tm_qkv128, const __grid_constant__ CUtensorMap tm_qkv64,
-                        const __grid_constant__ CUtensorMap tm_do64, const float* __restrict__ lse,
+                        const __grid_constant__ CUtensorMap tm_do64, const __grid_constant__ CUtensorMap tm_dst,
+                        int store_ds, const float* __restrict__ lse,
                         const float* __restrict__ D, int T, int H, int BH, __nv_bfloat16* __restrict__ dqkv,
-                        float scale, float scale_log2) {
+                        float scale, float scale_log2, long long* __restrict__ dbg) {
   using C = BwdCfg<HD>;
   constexpr int NU = C::kNU, ST = C::kSt, NA = C::kNAcc;
+  // CKF_ATTN_DEBUG timings (compiled in only with -DCKF_ATTN_DEBUG_BUILD=1): [0] tiles, [1] softmax
+  // wait S, [2] wait pd_free, [3] compute, [4] epilogue, [5] total, [8] MMA issue_s (+ its waits),
+  // [9] acc_free wait, [10] pd_full wait -- softmax numbers from warp 4 (group 0, lane quarter 0)
+  const long long t_start = kDbg ? clock64() : 0;
+  long long tw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   extern __shared__ uint8_t smem_raw[];
   SmemKVpp<HD>& sm =
       *reinterpret_cast<SmemKVpp<HD>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -527,6 +534,7 @@ __global__ void __launch_bounds__(128 + 256 * SPLIT, 1)
         mbar_wait(&sm.kv_full[kbuf], (lu / NU) & 1);
         const uint32_t ka = smem_u32(sm.k[kbuf]), va = smem_u32(sm.v[kbuf]);
         auto issue_s = [&](int gi) {  // S^T = K Q^T, dP^T = V dO^T of global tile gi into buffer gi & 1
+          const long long ti = kDbg ? clock64() : 0;
           const int st = gi % ST, bb = gi & 1;
           mbar_wait(&sm.qd_full[st], (gi / ST) & 1);
           mbar_wait(&sm.s_free[bb], ((gi >> 1) & 1) ^ 1);
@@ -541,6 +549,7 @@ __global__ void __launch_bounds__(128 + 256 * SPLIT, 1)
                       umma_desc_sw128(kmajor_k(oa, PT, k), 16, 1024), kIdS, k > 0 ? 1u : 0u);
           }
           umma_commit(&sm.s_full[bb]);
+          if (kDbg) tw[0] += clock64() - ti;
         };
         // S/dP run LA tiles ahead of the dV/dK MMAs.  LA = 3 (five Q/dO stages, head_dim 64):
         // tile i+3 goes into tile i+1's S/dP buffer as soon as the OTHER group's softmax has read
@@ -552,12 +561,16 @@ __global__ void __launch_bounds__(128 + 256 * SPLIT, 1)
         issue_s(g);
         issue_s(g + 1);
         if (LA >= 3 && ntiles > 2) issue_s(g + 2);
+        const long long ta = kDbg ? clock64() : 0;
         mbar_wait(&sm.acc_free[aset], ((lu / NA) & 1) ^ 1);
+        if (kDbg) tw[1] += clock64() - ta;
         for (int i = 0; i < ntiles; ++i) {
           const int gi = g + i, st = gi % ST, bb = gi & 1;
           if constexpr (LA >= 2)
             if (i + LA < ntiles) issue_s(gi + LA);
+          const long long tp = kDbg ? clock64() : 0;
           mbar_wait(&sm.pd_full[bb], (gi >> 1) & 1);
+          if (kDbg) tw[2] += clock64() - tp;
           tc_fence_after();
           const uint32_t qa = smem_u32(sm.q[st]), oa = smem_u32(sm.d_o[st]);
           const uint32_t pa = smem_u32(sm.p[bb]), da = smem_u32(sm.ds[bb]);
@@ -576,6 +589,12 @@ __global__ void __launch_bounds__(128 + 256 * SPLIT, 1)
         umma_commit(&sm.acc_full[aset]);
         umma_commit(&sm.kv_empty[kbuf]);
         g += ntiles;
+      }
+      if (kDbg && dbg) {
+        long long* d = dbg + 16 * blockIdx.x;
+        d[8] = tw[0];
+        d[9] = tw[1];
+        d[10] = tw[2];
       }
     }
   } else if (warp >= 4) {
@@ -621,8 +640,14 @@ __global__ void __launch_bounds__(128 + 256 * SPLIT, 1)
       const int ntiles = 2 * (nqb - u / BH);
       for (int i = grp; i < ntiles; i += 2) {
         const int gi = g + i, st = gi % ST;
+        const long long t0 = kDbg ? clock64() : 0;
         mbar_wait(&sm.s_full[grp], (gi >> 1) & 1);
         mbar_wait(&sm.qd_full[st], (gi / ST) & 1);  // (complete) lse / D of this tile visible
+        const long long t1 = kDbg ? clock64() : 0;
+        if (kDbg) {
+          tw[0] += 1;
+          tw[1] += t1 - t0;
+        }
         tc_fence_after();
         uint32_t us[QW], ud[QW];
 #pragma unroll
@@ -631,6 +656,7 @@ __global__ void __launch_bounds__(128 + 256 * SPLIT, 1)
           tmem_ld32(trow + grp * 128 + 64 + half * QW + c, *reinterpret_cast<uint32_t(*)[32]>(&ud[c]));
         }
         tmem_ld_wait();
+        if (kDbg) tw[5] += clock64() - t1;
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.s_free[grp]);
@@ -680,7 +706,17 @@ __global__ void __launch_bounds__(128 + 256 * SPLIT, 1)
             pkd[4 * lg + e] = pack_bf16(dv[2 * e], dv[2 * e + 1]);
           }
         }
+        const long long t2 = kDbg ? clock64() : 0;
         mbar_wait(&sm.pd_free[grp], ((gi >> 1) & 1) ^ 1);  // this group's previous dV/dK MMAs read P / dS
+        if (store_ds) {  // ... and the previous dS^T store has left this warp's slab
+          if (lane == 0) bulk_wait_read<0>();
+          __syncwarp();
+        }
+        const long long t3 = kDbg ? clock64() : 0;
+        if (kDbg) {
+          tw[2] += t3 - t2;
+          tw[3] += t2 - t1;
+        }
 #pragma unroll
         for (int lg = 0; lg < QW / 8; ++lg) {
           const int g8 = half * (QW / 8) + lg;
@@ -690,9 +726,21 @@ __global__ void __launch_bounds__(128 + 256 * SPLIT, 1)
         }
         fence_proxy_async();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.pd_full[grp]);
+        if (lane == 0) {
+          mbar_arrive(&sm.pd_full[grp]);
+          if (store_ds) {  // this warp's 32 key rows of dS^T -> its [64 keys x 64 queries] tile for the dQ GEMM
+            const int kb = u / BH, bh = u - kb * BH, n64 = T / PT;
+            const int j = kb * 2 + (quarter >> 1), t = kb * 2 + i;  // 64-key block, 64-query block
+            tma_store_2d(&tm_dst, reinterpret_cast<const uint8_t*>(sm.ds[grp]) + quarter * 32 * 128, 0,
+                         ((bh * n64 + j) * n64 + t) * PT + (quarter & 1) * 32);
+            bulk_commit();
+          }
+        }
+        if (kDbg) tw[3] += clock64() - t3;
         if (i == grp && pend_u >= 0) {
+          const long long t4 = kDbg ? clock64() : 0;
           epilogue(pend_u, pend_lu);
+          if (kDbg) tw[4] += clock64() - t4;
           pend_u = -1;
         }
       }
@@ -701,6 +749,13 @@ __global__ void __launch_bounds__(128 + 256 * SPLIT, 1)
       pend_lu = lu;
     }
     if (pend_u >= 0) epilogue(pend_u, pend_lu);
+    if (store_ds && lane == 0) bulk_wait_all();
+    if (kDbg && dbg && warp == 4 && lane == 0) {
+      long long* d = dbg + 16 * blockIdx.x;
+      for (int k = 0; k < 5; ++k) d[k] = tw[k];
+      d[5] = clock64() - t_start;
+      d[6] = tw[5];
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -954,6 +1009,142 @@ __global__ void __launch_bounds__(kThreadsBwd, 1)
   if (warp == 2) tmem_free<512>(tmem);
 }
 
+
+// dQ from the stored dS^T (attn_dkdv_pp_kernel, store_ds): dQ[q, :] = scale sum_key dS^T[key, q] K[key, :]
+// -- a causal batched GEMM with no S / dP recompute and no exponentials.  Persistent over units
+// (query tile qb, sequence x head bh) longest first; 64-key inner tiles: A = dS^T tile (MN-major,
+// two [64 keys][64 q] SW128 chunks), B = K tile (MN-major, HD/64 [64 keys][64 hd] chunks) by TMA
+// into a 6-deep ring; dQ accumulates in TMEM (two accumulator sets, HD columns each), epilogue
+// warps 4..7 scale, round and store while the next unit runs.
+template <int HD>
+struct SmemDQ {
+  static constexpr int kSt = 6;
+  uint8_t a[kSt][2 * 8192];
+  uint8_t b[kSt][PT * HD * 2];
+  uint64_t full[kSt], empty[kSt], acc_full[2], acc_free[2];
+  uint32_t tmem;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(256, 1)
+    attn_dq_gemm_kernel(const __grid_constant__ CUtensorMap tm_dst, const __grid_constant__ CUtensorMap tm_qkv64,
+                        int T, int H, int BH, __nv_bfloat16* __restrict__ dqkv, float scale) {
+  using SM = SmemDQ<HD>;
+  constexpr int ST = SM::kSt;
+  extern __shared__ uint8_t smem_raw[];
+  SM& sm = *reinterpret_cast<SM*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nqb = T / TQ, nunits = nqb * BH;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tm_dst);
+    tma_prefetch(&tm_qkv64);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int i = 0; i < ST; ++i) {
+      mbar_init(&sm.full[i], 1);
+      mbar_init(&sm.empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm.acc_full[i], 1);
+      mbar_init(&sm.acc_free[i], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<2 * HD>(&sm.tmem);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem;
+  if (warp == 0) {
+    if (lane == 0) {
+      int g = 0;
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const int qi = u / BH, bh = u - qi * BH, b = bh / H, h = bh - b * H;
+        const int qb = nqb - 1 - qi, ntiles = 2 * (qb + 1);
+        for (int j = 0; j < ntiles; ++j, ++g) {
+          const int st = g % ST;
+          mbar_wait(&sm.empty[st], ((g / ST) & 1) ^ 1);
+          mbar_arrive_expect_tx(&sm.full[st], 2 * 8192 + PT * HD * 2);
+          const int n64 = T / PT, tile = (bh * n64 + j) * n64 + 2 * qb;  // dS^T tiles (j, 2qb) and (j, 2qb + 1)
+          tma_load_2d(sm.a[st], &tm_dst, &sm.full[st], 0, tile * PT);
+          tma_load_2d(sm.a[st] + 8192, &tm_dst, &sm.full[st], 0, (tile + 1) * PT);
+          tma_tile<HD>(sm.b[st], &tm_qkv64, &sm.full[st], (H + h) * HD, b * T + j * PT, PT);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t kId = idesc_bf16_f32(TQ, HD, true, true);
+      int g = 0, lu = 0;
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lu) {
+        const int qb = nqb - 1 - u / BH, ntiles = 2 * (qb + 1), aset = lu & 1;
+        mbar_wait(&sm.acc_free[aset], ((lu >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t acc = tmem + static_cast<uint32_t>(aset * HD);
+        for (int j = 0; j < ntiles; ++j, ++g) {
+          const int st = g % ST;
+          mbar_wait(&sm.full[st], (g / ST) & 1);
+          tc_fence_after();
+          const uint32_t aa = smem_u32(sm.a[st]), ba = smem_u32(sm.b[st]);
+#pragma unroll
+          for (int k = 0; k < PT / 16; ++k)
+            umma_bf16(acc, umma_desc_sw128(aa + k * 2048, 8192, 1024), umma_desc_sw128(ba + k * 2048, PT * 128, 1024),
+                      kId, (j > 0 || k > 0) ? 1u : 0u);
+          umma_commit(&sm.empty[st]);
+        }
+        umma_commit(&sm.acc_full[aset]);
+      }
+    }
+  } else if (warp >= 4) {
+    const int quarter = warp - 4, r = quarter * 32 + lane;
+    const size_t ld = static_cast<size_t>(3) * H * HD;
+    int lu = 0;
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lu) {
+      const int qi = u / BH, bh = u - qi * BH, b = bh / H, h = bh - b * H;
+      const int q = (nqb - 1 - qi) * TQ + r, aset = lu & 1;
+      mbar_wait(&sm.acc_full[aset], (lu >> 1) & 1);
+      tc_fence_after();
+      __nv_bfloat16* qrow = dqkv + (static_cast<size_t>(b) * T + q) * ld + static_cast<size_t>(h) * HD;
+      const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(aset * HD);
+#pragma unroll 1
+      for (int c0 = 0; c0 < HD; c0 += 32) {
+        uint32_t w32[32];
+        tmem_ld32(trow + c0, w32);
+        tmem_ld_wait();
+#pragma unroll
+        for (int piece = 0; piece < 4; ++piece) {
+          uint4 w;
+          w.x = pack_bf16(__uint_as_float(w32[8 * piece + 0]) * scale, __uint_as_float(w32[8 * piece + 1]) * scale);
+          w.y = pack_bf16(__uint_as_float(w32[8 * piece + 2]) * scale, __uint_as_float(w32[8 * piece + 3]) * scale);
+          w.z = pack_bf16(__uint_as_float(w32[8 * piece + 4]) * scale, __uint_as_float(w32[8 * piece + 5]) * scale);
+          w.w = pack_bf16(__uint_as_float(w32[8 * piece + 6]) * scale, __uint_as_float(w32[8 * piece + 7]) * scale);
+          reinterpret_cast<uint4*>(qrow + c0)[piece] = w;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.acc_free[aset]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_free<2 * HD>(tmem);
+}
+
+// dS^T scratch for the stored-dS backward: B*H*T*T bf16 per launch chunk (grown on demand)
+bf16* dst_buffer(size_t elems) {
+  static bf16* buf = nullptr;
+  static size_t cap = 0;
+  if (elems > cap) {
+    if (buf) CKF_CUDA(cudaFree(buf));
+    CKF_CUDA(cudaMalloc(&buf, elems * sizeof(bf16)));
+    cap = elems;
+    ++alloc_epoch();
+  }
+  return buf;
+}
+
 int num_sms_attn() {
   static const int sms = [] {
     int dev = 0, v = 0;
@@ -996,11 +1187,6 @@ void bwd_launch(const bf16* qkv, const bf16* o, const float* lse, const bf16* do
   dsum_kernel<HD><<<static_cast<unsigned>((rows * (HD / 8) + 255) / 256), 256, 0, s>>>(
       o, dout, static_cast<int>(B), static_cast<int>(T), static_cast<int>(H), Dsum);
   CKF_LAUNCH_CHECK();
-  const CUtensorMap tq = tma::make_2d_bf16(qkv, 3 * H * HD, B * T, 3 * H * HD, 64, 128);
-  const CUtensorMap tq64 = tma::make_2d_bf16(qkv, 3 * H * HD, B * T, 3 * H * HD, 64, 64);
-  const CUtensorMap td = tma::make_2d_bf16(dout, H * HD, B * T, H * HD, 64, 128);
-  const CUtensorMap td64 = tma::make_2d_bf16(dout, H * HD, B * T, H * HD, 64, 64);
-  const size_t smem_kv = sizeof(SmemKVpp<HD>) + 1024, smem_q = sizeof(SmemQpp<HD>) + 1024;
   // CKF_ATTN_BWD_SPLIT=1|2: softmax warps per TMEM lane quarter per group in the dK dV kernel
   // (CKF_ATTN_BWD_POLY: FMA-pipe exponential pairs of 8 in the backward -- measured no gain, so
   // only the all-MUFU kernels are built: profiles/r02_attention_bwd_poly_sweep.jsonl)
@@ -1008,24 +1194,62 @@ void bwd_launch(const bf16* qkv, const bf16* o, const float* lse, const bf16* do
     const char* v = std::getenv("CKF_ATTN_BWD_SPLIT");
     return v ? std::atoi(v) : kBwdSplitDefault;
   }();
+  // dQ from the dS^T the dK dV kernel stores (one GEMM pass, no recompute) unless CKF_ATTN_DQ=recompute
+  // selects the dQ kernel that recomputes S, dP and dS (the split-2 dK dV kernel stores no dS^T)
+  static const bool stored_ds = [] {
+    const char* v = std::getenv("CKF_ATTN_DQ");
+    return !(v && std::string(v) == "recompute") && split < 2;
+  }();
   auto kkv = split >= 2 ? attn_dkdv_pp_kernel<HD, 0, 2> : attn_dkdv_pp_kernel<HD, 0, 1>;
   const int kv_threads = 128 + 256 * (split >= 2 ? 2 : 1);
   auto kq = attn_dq_pp_kernel<HD, 0>;
+  auto kg = attn_dq_gemm_kernel<HD>;
+  const size_t smem_kv = sizeof(SmemKVpp<HD>) + 1024, smem_q = sizeof(SmemQpp<HD>) + 1024,
+               smem_g = sizeof(SmemDQ<HD>) + 1024;
   static bool attr = false;
   if (!attr) {
     CKF_CUDA(cudaFuncSetAttribute(kkv, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_kv)));
     CKF_CUDA(cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_q)));
+    CKF_CUDA(cudaFuncSetAttribute(kg, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_g)));
     attr = true;
   }
   const float scale = 1.f / sqrtf(static_cast<float>(HD));
-  const int BH = static_cast<int>(B * H), units = static_cast<int>(T / TQ) * BH;
-  const unsigned grid = static_cast<unsigned>(std::min(units, num_sms_attn()));
-  kkv<<<grid, kv_threads, smem_kv, s>>>(tq, tq64, td64, lse, Dsum, static_cast<int>(T), static_cast<int>(H), BH, dqkv,
-                                        scale, scale * kLog2e);
-  CKF_LAUNCH_CHECK();
-  kq<<<grid, kThreadsBwd, smem_q, s>>>(tq, tq64, td, lse, Dsum, static_cast<int>(T), static_cast<int>(H), BH, dqkv,
-                                       scale, scale * kLog2e);
-  CKF_LAUNCH_CHECK();
+  long long* dbg = attn_fwd_debug_buffer();
+  // sequences per pass: the dS^T scratch (B_c H T^2 bf16) stays within ~1.1 GB
+  const size_t per_seq = H * T * T * sizeof(bf16);
+  const size_t bc = stored_ds ? std::max<size_t>(1, std::min<size_t>(B, 1100000000ull / per_seq)) : B;
+  bf16* dst = stored_ds ? dst_buffer(bc * H * T * T) : nullptr;
+  const size_t ld = 3 * H * HD;
+  for (size_t b0 = 0; b0 < B; b0 += bc) {
+    const size_t nb = std::min(bc, B - b0);
+    const bf16* q_c = qkv + b0 * T * ld;
+    const bf16* do_c = dout + b0 * T * H * HD;
+    bf16* dq_c = dqkv + b0 * T * ld;
+    const float* lse_c = lse + b0 * H * T;
+    const float* D_c = Dsum + b0 * H * T;
+    const CUtensorMap tq = tma::make_2d_bf16(q_c, ld, nb * T, ld, 64, 128);
+    const CUtensorMap tq64 = tma::make_2d_bf16(q_c, ld, nb * T, ld, 64, 64);
+    const CUtensorMap td = tma::make_2d_bf16(do_c, H * HD, nb * T, H * HD, 64, 128);
+    const CUtensorMap td64 = tma::make_2d_bf16(do_c, H * HD, nb * T, H * HD, 64, 64);
+    // dS^T as contiguous [64 keys][64 queries] tiles (8 KiB each; tile (bh, key block j, query block t)
+    // at row ((bh n64 + j) n64 + t) 64 of a [* x 64] matrix): 32-row slabs stored by the dK dV warps,
+    // whole tiles loaded by dQ -- every transfer is one contiguous run of DRAM
+    const size_t n64 = T / PT;
+    const CUtensorMap tds32 = stored_ds ? tma::make_2d_bf16(dst, 64, nb * H * n64 * n64 * 64, 64, 64, 32) : tq;
+    const CUtensorMap tds64 = stored_ds ? tma::make_2d_bf16(dst, 64, nb * H * n64 * n64 * 64, 64, 64, 64) : tq;
+    const int BH = static_cast<int>(nb * H), units = static_cast<int>(T / TQ) * BH;
+    const unsigned grid = static_cast<unsigned>(std::min(units, num_sms_attn()));
+    kkv<<<grid, kv_threads, smem_kv, s>>>(tq, tq64, td64, tds32, stored_ds ? 1 : 0, lse_c, D_c, static_cast<int>(T),
+                                          static_cast<int>(H), BH, dq_c, scale, scale * kLog2e,
+                                          dbg ? dbg + 8 * 32768 : nullptr);
+    CKF_LAUNCH_CHECK();
+    if (stored_ds)
+      kg<<<grid, 256, smem_g, s>>>(tds64, tq64, static_cast<int>(T), static_cast<int>(H), BH, dq_c, scale);
+    else
+      kq<<<grid, kThreadsBwd, smem_q, s>>>(tq, tq64, td, lse_c, D_c, static_cast<int>(T), static_cast<int>(H), BH, dq_c,
+                                           scale, scale * kLog2e);
+    CKF_LAUNCH_CHECK();
+  }
 }
 
 }  // namespace
