@@ -1,6 +1,7 @@
 // Causal attention on the 5th-generation tensor cores, head_dim 64 or 128.
 //
-// Forward: one CTA per (128-query tile, sequence x head).  Q, K, V tiles arrive by TMA
+// Forward: one CTA per (128-query tile, sequence x head) -- at head_dim 128 per PAIR of query
+// tiles, each with its own softmax warp group and MMA issuer, sharing the K / V stages.  Q, K, V tiles arrive by TMA
 // straight from the packed qkv activation (2-D tensor maps, boxes of 64 columns, 128-byte
 // swizzle: K-major for Q and K, MN-major for V as the PV B operand; a 128-wide head is
 // two such column chunks).  S = Q K^T accumulates in TMEM, the softmax warps turn it into
@@ -26,7 +27,6 @@ namespace {
 using namespace ckf::sm100;
 
 constexpr int TQ = 128, TK = 128;
-constexpr int kThreads = 256;
 constexpr int kThreadsBwd = 384;  // backward: 8 softmax warps (2 groups x one per TMEM lane quarter)
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
@@ -63,6 +63,12 @@ constexpr float kRescale = 8.f;
 // exponential pairs (of 8) on the FMA pipe in the head_dim-64 forward (measured at [64, 1024, 16,
 // 64]: 0 -> 347.5 us, 1 -> 336.0, 2 -> 339.3, 3 -> 359.6, 4 -> 395.7; head_dim 128 is fastest with 0)
 constexpr int kFwdPolyDefault = 1;
+// query tiles per forward CTA (FwdCfg), measured (profiles/r02_attention_fwd_ng_sweep.jsonl):
+// head_dim 128: 1694 -> 1159 us at [16, 4096, 16, 128] with two (the single-tile CTA fits only
+// once per SM: 4 softmax warps); head_dim 64: two single-tile CTAs per SM stay ahead (335 vs 379 us
+// at [64, 1024, 16, 64])
+template <int HD>
+constexpr int kFwdNgDefault = HD == 128 ? 2 : 1;
 // per-tile clock instrumentation of the forward (tools/attn_debug.py): compiled in only with
 // -DCKF_ATTN_DEBUG_BUILD=1 (and CKF_ATTN_DEBUG=1 at run time), so the hot loop carries none of it
 #ifndef CKF_ATTN_DEBUG_BUILD
@@ -71,26 +77,35 @@ constexpr int kFwdPolyDefault = 1;
 constexpr bool kDbg = CKF_ATTN_DEBUG_BUILD != 0;
 constexpr int kBwdSplitDefault = 1;  // 2 measured no faster (1084.7 vs 1087.8 us at [64, 1024, 16, 64])  // exponential pairs (of 8) on the FMA pipe, forward
 
-template <int HD>
+// NG query tiles per CTA (NG = 2: query tiles 2c and 2c+1 share every K / V tile the producer
+// loads; two softmax warp groups, one per tile, each on its own S pair and O in TMEM, so the
+// tensor core runs one group's S / P V while the other group is in its softmax).
+template <int HD, int NG>
 struct FwdCfg {
   static constexpr uint32_t kQ = TQ * HD * 2, kK = FK * HD * 2;
-  static constexpr int kKSt = HD == 64 ? 4 : 3, kVSt = HD == 64 ? 3 : 2;
-  // 104 KiB vs 144 KiB of shared memory; two hd-128 CTAs per SM with 2 K / 1 V stages (112 KiB)
+  static constexpr int kKSt = HD == 64 ? 4 : 3, kVSt = HD == 64 ? 3 : (NG == 2 ? 3 : 2);
+  // NG = 1: 104 KiB vs 144 KiB of shared memory; two hd-128 CTAs per SM with 2 K / 1 V stages (112 KiB)
   // measured 1.7x slower (1697 -> 2887 us at [16, 4096, 16, 128]): the single V stage serialises
-  static constexpr int kMinBlocks = HD == 64 ? 2 : 1;
+  static constexpr int kMinBlocks = HD == 64 && NG == 1 ? 2 : 1;
+  static constexpr int kThreads = 128 + 128 * NG;
+  // TMEM: group g's S pair at columns g*128 + {0, 64}, its O at NG*128 + g*HD
+  static constexpr int kTmemCols = NG * 128 + NG * HD <= 256 ? 256 : 512;
+  // S_{j+2} issued two tiles ahead (into the buffer the softmax has just loaded) when a third V
+  // stage lets the producer run that far ahead
+  static constexpr bool kEarly = kVSt >= 3;
 };
 
-template <int HD>
+template <int HD, int NG>
 struct Smem {
-  using C = FwdCfg<HD>;
-  uint8_t q[C::kQ];
+  using C = FwdCfg<HD, NG>;
+  uint8_t q[NG][C::kQ];
   uint8_t k[C::kKSt][C::kK];
   uint8_t v[C::kVSt][C::kK];
-  uint8_t p[2][kPTile];
+  uint8_t p[NG][2][kPTile];
   uint64_t q_full;
   uint64_t k_full[C::kKSt], k_empty[C::kKSt], v_full[C::kVSt], v_empty[C::kVSt];
-  uint64_t s_full[2], s_free[2], p_full[2], p_free[2];
-  uint64_t o_full;
+  uint64_t s_full[NG][2], s_free[NG][2], p_full[NG][2], p_free[NG][2];
+  uint64_t o_full[NG];
   uint32_t tmem;
 };
 
@@ -98,21 +113,23 @@ __device__ __forceinline__ void tmem_st32_wait() { asm volatile("tcgen05.wait::s
 
 // POLY: of every 8 exponential pairs of a softmax row chunk, POLY run on the FMA pipe
 // (ex2_fma2), the rest on MUFU (CKF_ATTN_POLY selects; 0 = all MUFU)
-template <int HD, int POLY>
-__global__ void __launch_bounds__(kThreads, FwdCfg<HD>::kMinBlocks)
+template <int HD, int POLY, int NG>
+__global__ void __launch_bounds__(FwdCfg<HD, NG>::kThreads, FwdCfg<HD, NG>::kMinBlocks)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_kv,
                        int T, int H, __nv_bfloat16* __restrict__ o, float* __restrict__ lse, float scale_log2,
                        long long* __restrict__ dbg) {
-  using C = FwdCfg<HD>;
+  using C = FwdCfg<HD, NG>;
   constexpr int KS = C::kKSt, VS = C::kVSt;
   extern __shared__ uint8_t smem_raw[];
   const long long t_start = clock64();
-  Smem<HD>& sm = *reinterpret_cast<Smem<HD>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  Smem<HD, NG>& sm =
+      *reinterpret_cast<Smem<HD, NG>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = T / TQ;
-  const int qb = nqb - 1 - static_cast<int>(blockIdx.x);  // heavy (late) query tiles first
+  // heavy (late) query tiles first; NG = 2: tiles qb0 = 2c and 2c + 1
+  const int qb0 = NG * (nqb / NG - 1 - static_cast<int>(blockIdx.x));
   const int bh = blockIdx.y, b = bh / H, h = bh % H;
-  const int nkb = 2 * qb + 2;  // causal: 64-key tiles 0 .. 2qb+1
+  const int nkb_last = 2 * (qb0 + NG - 1) + 2;  // causal: 64-key tiles of the last query tile
   const int row0 = b * T;
   const int qcol = h * HD, kcol = (H + h) * HD, vcol = (2 * H + h) * HD;
 
@@ -122,35 +139,40 @@ __global__ void __launch_bounds__(kThreads, FwdCfg<HD>::kMinBlocks)
   }
   if (warp == 1 && lane == 0) {
     mbar_init(&sm.q_full, 1);
+    // a K / V stage is released by every group's issuer (the last query tile's two extra key
+    // tiles are released by one issuer only: the producer never waits on those again)
     for (int i = 0; i < KS; ++i) {
       mbar_init(&sm.k_full[i], 1);
-      mbar_init(&sm.k_empty[i], 1);
+      mbar_init(&sm.k_empty[i], NG);
     }
     for (int i = 0; i < VS; ++i) {
       mbar_init(&sm.v_full[i], 1);
-      mbar_init(&sm.v_empty[i], 1);
+      mbar_init(&sm.v_empty[i], NG);
     }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&sm.s_full[i], 1);
-      mbar_init(&sm.s_free[i], 4);
-      mbar_init(&sm.p_full[i], 4);
-      mbar_init(&sm.p_free[i], 1);
+    for (int g = 0; g < NG; ++g) {
+      for (int i = 0; i < 2; ++i) {
+        mbar_init(&sm.s_full[g][i], 1);
+        mbar_init(&sm.s_free[g][i], 4);
+        mbar_init(&sm.p_full[g][i], 4);
+        mbar_init(&sm.p_free[g][i], 1);
+      }
+      mbar_init(&sm.o_full[g], 1);
     }
-    mbar_init(&sm.o_full, 1);
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<256>(&sm.tmem);
+  if (warp == 2) tmem_alloc<C::kTmemCols>(&sm.tmem);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = sm.tmem;  // S[0] cols 0-63, S[1] 64-127, O 128 .. 128+HD
+  const uint32_t tmem = sm.tmem;
 
   if (warp == 0) {
     if (lane == 0) {
-      // ---------------- TMA producer: Q once, then K_j and V_j (each exactly once)
-      mbar_arrive_expect_tx(&sm.q_full, C::kQ);
-      tma_tile<HD>(sm.q, &tm_qkv, &sm.q_full, qcol, row0 + qb * TQ, TQ);
-      for (int j = 0; j < nkb; ++j) {
+      // ---------------- TMA producer: the Q tiles once, then K_j and V_j (each exactly once)
+      mbar_arrive_expect_tx(&sm.q_full, NG * C::kQ);
+#pragma unroll
+      for (int g = 0; g < NG; ++g) tma_tile<HD>(sm.q[g], &tm_qkv, &sm.q_full, qcol, row0 + (qb0 + g) * TQ, TQ);
+      for (int j = 0; j < nkb_last; ++j) {
         const int ks = j % KS, vs = j % VS;
         mbar_wait(&sm.k_empty[ks], ((j / KS) & 1) ^ 1);
         mbar_arrive_expect_tx(&sm.k_full[ks], C::kK);
@@ -160,33 +182,37 @@ __global__ void __launch_bounds__(kThreads, FwdCfg<HD>::kMinBlocks)
         tma_tile<HD>(sm.v[vs], &tm_kv, &sm.v_full[vs], vcol, row0 + j * FK, FK);
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 || (NG == 2 && warp == 3)) {
     if (lane == 0) {
-      // ---------------- MMA issuer: S_{j+1} is issued before P_j is awaited
+      // ---------------- MMA issuers, one per query tile (warp 1: group 0, warp 3: group 1): the
+      // groups share the K / V stages (released by both issuers) but are otherwise independent,
+      // so one group's softmax overlaps the other's MMAs as two CTAs per SM would.
+      // S_{j+1} (or S_{j+2}) is issued before P_j is awaited.
+      const int g = warp == 1 ? 0 : 1;
+      const int nkb = 2 * (qb0 + g) + 2;
       constexpr uint32_t kIdS = idesc_bf16_f32(TQ, FK, false, false);  // S = Q K^T  (128 x 64)
       constexpr uint32_t kIdO = idesc_bf16_f32(TQ, HD, false, true);   // O += P V   (V MN-major)
       mbar_wait(&sm.q_full, 0);
-      const uint32_t qa = smem_u32(sm.q);
+      const uint32_t qa = smem_u32(sm.q[g]);
       auto issue_s = [&](int j) {
         const int ks = j % KS, sb = j & 1;
         mbar_wait(&sm.k_full[ks], (j / KS) & 1);
-        mbar_wait(&sm.s_free[sb], ((j >> 1) & 1) ^ 1);
+        mbar_wait(&sm.s_free[g][sb], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t ka = smem_u32(sm.k[ks]);
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k)
-          umma_bf16(tmem + sb * FK, umma_desc_sw128(kmajor_k(qa, TQ, k), 16, 1024),
+          umma_bf16(tmem + g * 128 + sb * FK, umma_desc_sw128(kmajor_k(qa, TQ, k), 16, 1024),
                     umma_desc_sw128(kmajor_k(ka, FK, k), 16, 1024), kIdS, k > 0 ? 1u : 0u);
-        umma_commit(&sm.s_full[sb]);
+        umma_commit(&sm.s_full[g][sb]);
         umma_commit(&sm.k_empty[ks]);
       };
-      // S runs two tiles ahead of the softmax: S_{j+2} goes into S_j's TMEM buffer as soon as the
-      // softmax warps have loaded S_j (early in their tile j), ahead of P_j V_j, so the next S is
-      // ready when the softmax finishes a tile instead of queueing behind P V
-      // (head_dim 64, three V stages; at head_dim 128 the two V stages would make S_{j+2} wait for
-      // K_{j+2}, which the producer loads only after P_{j-1} V_{j-1} freed a V stage -- there S_{j+1}
-      // is issued one tile ahead, before P_j V_j)
-      constexpr bool kEarly = HD == 64;
+      // S runs two tiles ahead of the softmax when a third V stage allows it: S_{j+2} goes into
+      // S_j's TMEM buffer as soon as the softmax warps have loaded S_j (early in their tile j),
+      // ahead of P_j V_j, so the next S is ready when the softmax finishes a tile instead of
+      // queueing behind P V.  With two V stages S_{j+2} would wait for K_{j+2}, which the producer
+      // loads only after P_{j-1} V_{j-1} freed a V stage -- there S_{j+1} is issued one tile ahead.
+      constexpr bool kEarly = C::kEarly;
       issue_s(0);
       if (kEarly && nkb > 1) issue_s(1);
       for (int j = 0; j < nkb; ++j) {
@@ -194,29 +220,33 @@ __global__ void __launch_bounds__(kThreads, FwdCfg<HD>::kMinBlocks)
         if (!kEarly && j + 1 < nkb) issue_s(j + 1);
         const int pb = j & 1, vs = j % VS;
         mbar_wait(&sm.v_full[vs], (j / VS) & 1);
-        mbar_wait(&sm.p_full[pb], (j >> 1) & 1);
+        mbar_wait(&sm.p_full[g][pb], (j >> 1) & 1);
         tc_fence_after();
-        const uint32_t pa = smem_u32(sm.p[pb]), va = smem_u32(sm.v[vs]);
+        const uint32_t pa = smem_u32(sm.p[g][pb]), va = smem_u32(sm.v[vs]);
 #pragma unroll
         for (int k = 0; k < FK / 16; ++k)  // V MN-major: chunks of 64 hd columns FK*128 bytes apart
-          umma_bf16(tmem + 128, umma_desc_sw128(pa + k * 32, 16, 1024),
+          umma_bf16(tmem + NG * 128 + g * HD, umma_desc_sw128(pa + k * 32, 16, 1024),
                     umma_desc_sw128(va + k * 2048, FK * 128, 1024), kIdO, (j > 0 || k > 0) ? 1u : 0u);
-        umma_commit(&sm.p_free[pb]);
+        umma_commit(&sm.p_free[g][pb]);
         umma_commit(&sm.v_empty[vs]);
       }
-      umma_commit(&sm.o_full);
+      umma_commit(&sm.o_full[g]);
     }
   } else if (warp >= 4) {
     // ---------------- softmax: one query row per thread, online with lazy rescaling
-    const int r = (warp - 4) * 32 + lane;
+    const int g = (warp - 4) >> 2, wq = (warp - 4) & 3;  // group, TMEM lane quarter (= warp % 4)
+    const int r = wq * 32 + lane;
+    const int qb = qb0 + g;
     const int q = qb * TQ + r;
-    const uint32_t trow = tmem + (static_cast<uint32_t>((warp - 4) * 32) << 16);
+    const int nkb = 2 * qb + 2;
+    const uint32_t trow = tmem + (static_cast<uint32_t>(wq * 32) << 16);
+    const uint32_t tS = trow + g * 128, tO = trow + NG * 128 + g * HD;
     float m = -INFINITY, l = 0.f;  // m: running max of S * scale_log2
     long long w_s = 0, w_p = 0, t_first = 0;
     for (int j = 0; j < nkb; ++j) {
       const int sb = j & 1, pb = j & 1;
       const long long t0 = (kDbg && dbg) ? clock64() : 0;
-      mbar_wait(&sm.s_full[sb], (j >> 1) & 1);
+      mbar_wait(&sm.s_full[g][sb], (j >> 1) & 1);
       if (kDbg && dbg) {  // CKF_ATTN_DEBUG timings only
         const long long t1 = clock64();
         if (j == 0) t_first = t1 - t_start;
@@ -224,15 +254,15 @@ __global__ void __launch_bounds__(kThreads, FwdCfg<HD>::kMinBlocks)
       }
       tc_fence_after();
       uint32_t u[64];
-      tmem_ld32(trow + sb * FK, *reinterpret_cast<uint32_t(*)[32]>(&u[0]));
-      tmem_ld32(trow + sb * FK + 32, *reinterpret_cast<uint32_t(*)[32]>(&u[32]));
+      tmem_ld32(tS + sb * FK, *reinterpret_cast<uint32_t(*)[32]>(&u[0]));
+      tmem_ld32(tS + sb * FK + 32, *reinterpret_cast<uint32_t(*)[32]>(&u[32]));
       tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.s_free[sb]);
+      if (lane == 0) mbar_arrive(&sm.s_free[g][sb]);
       const int kbase = j * FK;
       const int nvalid = min(FK, q - kbase + 1);  // keys <= q are visible (causal)
-      const uint32_t prow = smem_u32(sm.p[pb]) + r * 128;
+      const uint32_t prow = smem_u32(sm.p[g][pb]) + r * 128;
       // P = 2^(S scale - mc) -> bf16 -> swizzled smem (32 keys at a time); returns the row sum
       auto write_p = [&](float mc) -> float {
         const f32x2 sc2 = f2(scale_log2, scale_log2), nm2 = f2(-mc, -mc);
@@ -272,7 +302,7 @@ __global__ void __launch_bounds__(kThreads, FwdCfg<HD>::kMinBlocks)
         return lt;
       };
       const long long t2 = (kDbg && dbg) ? clock64() : 0;
-      mbar_wait(&sm.p_free[pb], ((j >> 1) & 1) ^ 1);  // P V_{j-2} has read this P buffer
+      mbar_wait(&sm.p_free[g][pb], ((j >> 1) & 1) ^ 1);  // P V_{j-2} has read this P buffer
       if (kDbg && dbg) w_p += clock64() - t2;
       // Fast path (every tile after the first): P against the running max m with no max pass;
       // kept when the tile's row sum stays <= 2^16 (so every P <= 2^16, finite).  Otherwise --
@@ -304,16 +334,16 @@ __global__ void __launch_bounds__(kThreads, FwdCfg<HD>::kMinBlocks)
         const float alpha = need ? ex2(m - mn) : 1.f;  // m = -inf on the first tile -> 0
         if (__any_sync(0xffffffffu, need) && j > 0) {
           // the previous P V must have landed before this warp rewrites its O rows
-          mbar_wait(&sm.p_free[(j - 1) & 1], ((j - 1) >> 1) & 1);
+          mbar_wait(&sm.p_free[g][(j - 1) & 1], ((j - 1) >> 1) & 1);
           tc_fence_after();
 #pragma unroll
           for (int hf = 0; hf < HD / 32; ++hf) {
             uint32_t ov[32];
-            tmem_ld32(trow + 128 + hf * 32, ov);
+            tmem_ld32(tO + hf * 32, ov);
             tmem_ld_wait();
 #pragma unroll
             for (int t = 0; t < 32; ++t) ov[t] = __float_as_uint(__uint_as_float(ov[t]) * alpha);
-            tmem_st32(trow + 128 + hf * 32, ov);
+            tmem_st32(tO + hf * 32, ov);
           }
           tmem_st32_wait();
         }
@@ -325,10 +355,10 @@ __global__ void __launch_bounds__(kThreads, FwdCfg<HD>::kMinBlocks)
       fence_proxy_async();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.p_full[pb]);
+      if (lane == 0) mbar_arrive(&sm.p_full[g][pb]);
     }
     // ---------------- epilogue: O / l -> bf16, lse
-    mbar_wait(&sm.o_full, 0);
+    mbar_wait(&sm.o_full[g], 0);
     tc_fence_after();
     const float inv = 1.f / l;
     const size_t ldo = static_cast<size_t>(H) * HD;
@@ -336,7 +366,7 @@ __global__ void __launch_bounds__(kThreads, FwdCfg<HD>::kMinBlocks)
 #pragma unroll
     for (int hf = 0; hf < HD / 32; ++hf) {
       uint32_t u[32];
-      tmem_ld32(trow + 128 + hf * 32, u);
+      tmem_ld32(tO + hf * 32, u);
       tmem_ld_wait();
 #pragma unroll
       for (int piece = 0; piece < 4; ++piece) {
@@ -365,7 +395,7 @@ __global__ void __launch_bounds__(kThreads, FwdCfg<HD>::kMinBlocks)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 2) tmem_free<256>(tmem);
+  if (warp == 2) tmem_free<C::kTmemCols>(tmem);
 }
 
 // ---------------------------------------------------------------- backward
@@ -1155,29 +1185,44 @@ int num_sms_attn() {
   return sms;
 }
 
-template <int HD>
-void fwd_launch(const bf16* qkv, size_t B, size_t T, size_t H, bf16* o, float* lse, cudaStream_t s) {
+template <int HD, int NG>
+void fwd_launch_ng(const bf16* qkv, size_t B, size_t T, size_t H, bf16* o, float* lse, int poly, cudaStream_t s) {
   const CUtensorMap tm = tma::make_2d_bf16(qkv, 3 * H * HD, B * T, 3 * H * HD, 64, 128);
   const CUtensorMap tkv = tma::make_2d_bf16(qkv, 3 * H * HD, B * T, 3 * H * HD, 64, FK);
-  const size_t smem = sizeof(Smem<HD>) + 1024;
+  const size_t smem = sizeof(Smem<HD, NG>) + 1024;
+  auto kern = poly >= 4 ? attn_fwd_tc_kernel<HD, 4, NG>
+              : poly == 3 ? attn_fwd_tc_kernel<HD, 3, NG>
+              : poly == 2 ? attn_fwd_tc_kernel<HD, 2, NG>
+              : poly == 1 ? attn_fwd_tc_kernel<HD, 1, NG> : attn_fwd_tc_kernel<HD, 0, NG>;
+  static bool attr[5] = {false, false, false, false, false};
+  const int pi = std::min(std::max(poly, 0), 4);
+  if (!attr[pi]) {
+    CKF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    attr[pi] = true;
+  }
+  const float scale_log2 = kLog2e / sqrtf(static_cast<float>(HD));
+  dim3 grid(static_cast<unsigned>(T / (TQ * NG)), static_cast<unsigned>(B * H));
+  long long* dbg = attn_fwd_debug_buffer();
+  kern<<<grid, FwdCfg<HD, NG>::kThreads, smem, s>>>(tm, tkv, static_cast<int>(T), static_cast<int>(H), o, lse,
+                                                   scale_log2, dbg);
+  CKF_LAUNCH_CHECK();
+}
+
+template <int HD>
+void fwd_launch(const bf16* qkv, size_t B, size_t T, size_t H, bf16* o, float* lse, cudaStream_t s) {
   static const int poly = [] {
     const char* v = std::getenv("CKF_ATTN_POLY");
     return v ? std::atoi(v) : (HD == 64 ? kFwdPolyDefault : 0);
   }();
-  auto kern = poly >= 4 ? attn_fwd_tc_kernel<HD, 4>
-              : poly == 3 ? attn_fwd_tc_kernel<HD, 3>
-              : poly == 2 ? attn_fwd_tc_kernel<HD, 2>
-              : poly == 1 ? attn_fwd_tc_kernel<HD, 1> : attn_fwd_tc_kernel<HD, 0>;
-  static bool attr = false;
-  if (!attr) {
-    CKF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    attr = true;
-  }
-  const float scale_log2 = kLog2e / sqrtf(static_cast<float>(HD));
-  dim3 grid(static_cast<unsigned>(T / TQ), static_cast<unsigned>(B * H));
-  long long* dbg = attn_fwd_debug_buffer();
-  kern<<<grid, kThreads, smem, s>>>(tm, tkv, static_cast<int>(T), static_cast<int>(H), o, lse, scale_log2, dbg);
-  CKF_LAUNCH_CHECK();
+  // CKF_ATTN_FWD_NG=1|2: query tiles per CTA (2 needs seq_len % 256 == 0)
+  static const int ng = [] {
+    const char* v = std::getenv("CKF_ATTN_FWD_NG");
+    return v ? std::atoi(v) : kFwdNgDefault<HD>;
+  }();
+  if (ng >= 2 && T % (2 * TQ) == 0)
+    fwd_launch_ng<HD, 2>(qkv, B, T, H, o, lse, poly, s);
+  else
+    fwd_launch_ng<HD, 1>(qkv, B, T, H, o, lse, poly, s);
 }
 
 template <int HD>
