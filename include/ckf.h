@@ -176,8 +176,11 @@ int ckf_lm_head_xent(const void* xn, const void* Einv, const int* labels, size_t
 /* Causal attention of the LLaMA block on device bf16 buffers: qkv [B*T x 3*H*hd]
  * (q | k | v column blocks), o [B*T x H*hd], lse [B*H*T] fp32 (natural log).
  * impl: 0 = default for the shape, 1 = mma.sync flash kernel, 2 = tcgen05/TMEM
- * kernel (head_dim 64, T % 128 == 0).  Backward: dout [B*T x H*hd] ->
- * dqkv [B*T x 3*H*hd]; Dsum = [B*H*T] fp32 scratch. */
+ * kernel (head_dim 64 or 128, T % 128 == 0).  Backward: dout [B*T x H*hd] ->
+ * dqkv [B*T x 3*H*hd]; Dsum = [B*H*T] fp32 scratch.  Backward impl | CKF_ATTN_ROPE_BWD:
+ * the dq / dk blocks leave with the RoPE backward (ckf_llama_rope inverse = 1) applied --
+ * fused into the tcgen05 kernel's dK and dQ epilogues (one bf16 rounding instead of two). */
+#define CKF_ATTN_ROPE_BWD 16
 int ckf_attention_fwd(const void* qkv, size_t B, size_t T, size_t H, size_t hd, void* o, float* lse, int impl,
                       void* stream);
 int ckf_attention_bwd(const void* qkv, const void* o, const float* lse, const void* dout, size_t B, size_t T,

@@ -53,6 +53,61 @@ __device__ __forceinline__ uint32_t kmajor_k(uint32_t base, int rows, int k) {
   return base + static_cast<uint32_t>((k >> 2) * rows * 128 + (k & 3) * 32);
 }
 
+// One row of a head's gradient (HD fp32 accumulator columns at TMEM address trow) times mul ->
+// bf16 at dst; with rope (pair-major cos/sin table [HD/2][T]) the inverse rotation of position
+// pos is applied first, in fp32 (the RoPE backward fused into the epilogue: (j, j + HD/2) pairs,
+// x1' = x1 c + x2 s, x2' = x2 c - x1 s -- the transpose of the forward rotation).
+template <int HD>
+__device__ __forceinline__ void store_head_row(uint32_t trow, float mul, __nv_bfloat16* dst, const float2* rope,
+                                               int pos, int T) {
+  auto st8 = [&](__nv_bfloat16* p, const float* v) {
+    uint4 w;
+    w.x = pack_bf16(v[0], v[1]);
+    w.y = pack_bf16(v[2], v[3]);
+    w.z = pack_bf16(v[4], v[5]);
+    w.w = pack_bf16(v[6], v[7]);
+    *reinterpret_cast<uint4*>(p) = w;
+  };
+  if (rope) {
+#pragma unroll 1
+    for (int c0 = 0; c0 < HD / 2; c0 += 32) {
+      uint32_t a[32], b[32];
+      tmem_ld32(trow + c0, a);
+      tmem_ld32(trow + HD / 2 + c0, b);
+      tmem_ld_wait();
+      const float2* cs = rope + static_cast<size_t>(c0) * T + pos;
+#pragma unroll
+      for (int piece = 0; piece < 4; ++piece) {
+        float y1[8], y2[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int j = 8 * piece + e;
+          const float2 t = __ldg(cs + static_cast<size_t>(j) * T);
+          const float x1 = __uint_as_float(a[j]) * mul, x2 = __uint_as_float(b[j]) * mul;
+          y1[e] = x1 * t.x + x2 * t.y;
+          y2[e] = x2 * t.x - x1 * t.y;
+        }
+        st8(dst + c0 + 8 * piece, y1);
+        st8(dst + HD / 2 + c0 + 8 * piece, y2);
+      }
+    }
+  } else {
+#pragma unroll 1
+    for (int c0 = 0; c0 < HD; c0 += 32) {
+      uint32_t w32[32];
+      tmem_ld32(trow + c0, w32);
+      tmem_ld_wait();
+#pragma unroll
+      for (int piece = 0; piece < 4; ++piece) {
+        float v[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(w32[8 * piece + e]) * mul;
+        st8(dst + c0 + 8 * piece, v);
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------- forward
 // 128 queries x 64-key tiles: S double-buffered in TMEM (2 x 64 columns) + O (HD columns).
 // m is only raised when a tile's max exceeds it by more than kRescale (P stays <= 2^kRescale,
@@ -479,7 +534,7 @@ __global__ void __launch_bounds__(128 + 256 * SPLIT, 1)
                         const __grid_constant__ CUtensorMap tm_do64, const __grid_constant__ CUtensorMap tm_dst,
                         int store_ds, const float* __restrict__ lse,
                         const float* __restrict__ D, int T, int H, int BH, __nv_bfloat16* __restrict__ dqkv,
-                        float scale, float scale_log2, long long* __restrict__ dbg) {
+                        float scale, float scale_log2, const float2* __restrict__ rope, long long* __restrict__ dbg) {
   using C = BwdCfg<HD>;
   constexpr int NU = C::kNU, ST = C::kSt, NA = C::kNAcc;
   // CKF_ATTN_DEBUG timings (compiled in only with -DCKF_ATTN_DEBUG_BUILD=1): [0] tiles, [1] softmax
@@ -645,6 +700,9 @@ __global__ void __launch_bounds__(128 + 256 * SPLIT, 1)
       __nv_bfloat16* dst = dqkv + (static_cast<size_t>(eb) * T + ekb * TK + r) * ld +
                            static_cast<size_t>(grp ? (H + eh) * HD : (2 * H + eh) * HD);
       const float mul = grp ? scale : 1.f;
+      if constexpr (SPLIT == 1) {  // dK with the inverse RoPE of key position ekb * TK + r when rope is given
+        store_head_row<HD>(trow + 256 + aset * 2 * HD + grp * HD, mul, dst, grp ? rope : nullptr, ekb * TK + r, T);
+      } else {
 #pragma unroll 1
       for (int c0 = half * (HD / SPLIT); c0 < (half + 1) * (HD / SPLIT); c0 += 32) {
         uint32_t w32[32];
@@ -659,6 +717,7 @@ __global__ void __launch_bounds__(128 + 256 * SPLIT, 1)
           w.w = pack_bf16(__uint_as_float(w32[8 * piece + 6]) * mul, __uint_as_float(w32[8 * piece + 7]) * mul);
           reinterpret_cast<uint4*>(dst + c0)[piece] = w;
         }
+      }
       }
       tc_fence_before();
       __syncwarp();
@@ -1058,7 +1117,8 @@ struct SmemDQ {
 template <int HD>
 __global__ void __launch_bounds__(256, 1)
     attn_dq_gemm_kernel(const __grid_constant__ CUtensorMap tm_dst, const __grid_constant__ CUtensorMap tm_qkv64,
-                        int T, int H, int BH, __nv_bfloat16* __restrict__ dqkv, float scale) {
+                        int T, int H, int BH, __nv_bfloat16* __restrict__ dqkv, float scale,
+                        const float2* __restrict__ rope) {
   using SM = SmemDQ<HD>;
   constexpr int ST = SM::kSt;
   extern __shared__ uint8_t smem_raw[];
@@ -1136,21 +1196,7 @@ __global__ void __launch_bounds__(256, 1)
       tc_fence_after();
       __nv_bfloat16* qrow = dqkv + (static_cast<size_t>(b) * T + q) * ld + static_cast<size_t>(h) * HD;
       const uint32_t trow = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(aset * HD);
-#pragma unroll 1
-      for (int c0 = 0; c0 < HD; c0 += 32) {
-        uint32_t w32[32];
-        tmem_ld32(trow + c0, w32);
-        tmem_ld_wait();
-#pragma unroll
-        for (int piece = 0; piece < 4; ++piece) {
-          uint4 w;
-          w.x = pack_bf16(__uint_as_float(w32[8 * piece + 0]) * scale, __uint_as_float(w32[8 * piece + 1]) * scale);
-          w.y = pack_bf16(__uint_as_float(w32[8 * piece + 2]) * scale, __uint_as_float(w32[8 * piece + 3]) * scale);
-          w.z = pack_bf16(__uint_as_float(w32[8 * piece + 4]) * scale, __uint_as_float(w32[8 * piece + 5]) * scale);
-          w.w = pack_bf16(__uint_as_float(w32[8 * piece + 6]) * scale, __uint_as_float(w32[8 * piece + 7]) * scale);
-          reinterpret_cast<uint4*>(qrow + c0)[piece] = w;
-        }
-      }
+      store_head_row<HD>(trow, scale, qrow, rope, q, T);  // (inverse RoPE of query position q when given)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.acc_free[aset]);
@@ -1227,7 +1273,7 @@ void fwd_launch(const bf16* qkv, size_t B, size_t T, size_t H, bf16* o, float* l
 
 template <int HD>
 void bwd_launch(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, size_t B, size_t T, size_t H,
-                bf16* dqkv, float* Dsum, cudaStream_t s) {
+                bf16* dqkv, float* Dsum, bool rope, cudaStream_t s) {
   const size_t rows = B * T * H;
   dsum_kernel<HD><<<static_cast<unsigned>((rows * (HD / 8) + 255) / 256), 256, 0, s>>>(
       o, dout, static_cast<int>(B), static_cast<int>(T), static_cast<int>(H), Dsum);
@@ -1260,6 +1306,9 @@ void bwd_launch(const bf16* qkv, const bf16* o, const float* lse, const bf16* do
   }
   const float scale = 1.f / sqrtf(static_cast<float>(HD));
   long long* dbg = attn_fwd_debug_buffer();
+  // the RoPE backward of dq / dk in the dK and dQ-GEMM epilogues (otherwise a separate pass below)
+  const bool rope_fused = rope && split < 2 && stored_ds;
+  const float2* rtab = rope_fused ? rope_table_pair_major(T, HD, s) : nullptr;
   // sequences per pass: the dS^T scratch (B_c H T^2 bf16) stays within ~1.1 GB
   const size_t per_seq = H * T * T * sizeof(bf16);
   const size_t bc = stored_ds ? std::max<size_t>(1, std::min<size_t>(B, 1100000000ull / per_seq)) : B;
@@ -1285,16 +1334,17 @@ void bwd_launch(const bf16* qkv, const bf16* o, const float* lse, const bf16* do
     const int BH = static_cast<int>(nb * H), units = static_cast<int>(T / TQ) * BH;
     const unsigned grid = static_cast<unsigned>(std::min(units, num_sms_attn()));
     kkv<<<grid, kv_threads, smem_kv, s>>>(tq, tq64, td64, tds32, stored_ds ? 1 : 0, lse_c, D_c, static_cast<int>(T),
-                                          static_cast<int>(H), BH, dq_c, scale, scale * kLog2e,
+                                          static_cast<int>(H), BH, dq_c, scale, scale * kLog2e, rtab,
                                           dbg ? dbg + 8 * 32768 : nullptr);
     CKF_LAUNCH_CHECK();
     if (stored_ds)
-      kg<<<grid, 256, smem_g, s>>>(tds64, tq64, static_cast<int>(T), static_cast<int>(H), BH, dq_c, scale);
+      kg<<<grid, 256, smem_g, s>>>(tds64, tq64, static_cast<int>(T), static_cast<int>(H), BH, dq_c, scale, rtab);
     else
       kq<<<grid, kThreadsBwd, smem_q, s>>>(tq, tq64, td, lse_c, D_c, static_cast<int>(T), static_cast<int>(H), BH, dq_c,
                                            scale, scale * kLog2e);
     CKF_LAUNCH_CHECK();
   }
+  if (rope && !rope_fused) llama::rope(dqkv, B * T, T, H * HD, H, 1, s);
 }
 
 }  // namespace
@@ -1320,12 +1370,12 @@ void attn_fwd_tc(const bf16* qkv, size_t B, size_t T, size_t H, size_t hd, bf16*
 }
 
 void attn_bwd_tc(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, size_t B, size_t T, size_t H,
-                 size_t hd, bf16* dqkv, float* Dsum, cudaStream_t s) {
+                 size_t hd, bf16* dqkv, float* Dsum, cudaStream_t s, bool rope_inverse) {
   if (!attn_fwd_tc_supported(T, hd)) raise(1, "tcgen05 attention: head_dim 64 or 128 and seq_len % 128 == 0");
   if (hd == 64)
-    bwd_launch<64>(qkv, o, lse, dout, B, T, H, dqkv, Dsum, s);
+    bwd_launch<64>(qkv, o, lse, dout, B, T, H, dqkv, Dsum, rope_inverse, s);
   else
-    bwd_launch<128>(qkv, o, lse, dout, B, T, H, dqkv, Dsum, s);
+    bwd_launch<128>(qkv, o, lse, dout, B, T, H, dqkv, Dsum, rope_inverse, s);
 }
 
 }  // namespace ckf::llama

@@ -526,16 +526,19 @@ int ckf_attention_fwd(const void* qkv, size_t B, size_t T, size_t H, size_t hd, 
 int ckf_attention_bwd(const void* qkv, const void* o, const float* lse, const void* dout, size_t B, size_t T,
                       size_t H, size_t hd, void* dqkv, float* Dsum, int impl, void* stream) {
   return guard([&] {
+    const bool rope = (impl & CKF_ATTN_ROPE_BWD) != 0;
+    impl &= ~CKF_ATTN_ROPE_BWD;
     const bool tc = impl == 2 || (impl == 0 && ckf::llama::attn_fwd_tc_supported(T, hd));
     if (tc) {
       ckf::llama::attn_bwd_tc(static_cast<const __nv_bfloat16*>(qkv), static_cast<const __nv_bfloat16*>(o), lse,
                               static_cast<const __nv_bfloat16*>(dout), B, T, H, hd, static_cast<__nv_bfloat16*>(dqkv),
-                              Dsum, static_cast<cudaStream_t>(stream));
+                              Dsum, static_cast<cudaStream_t>(stream), rope);
       return;
     }
     ckf::llama::attn_bwd(static_cast<const __nv_bfloat16*>(qkv), static_cast<const __nv_bfloat16*>(o), lse,
                          static_cast<const __nv_bfloat16*>(dout), B, T, H, hd, static_cast<__nv_bfloat16*>(dqkv), Dsum,
                          static_cast<cudaStream_t>(stream));
+    if (rope) ckf::llama::rope(static_cast<__nv_bfloat16*>(dqkv), B * T, T, H * hd, H, 1, static_cast<cudaStream_t>(stream));
   });
 }
 // debug (not part of the ABI contract): per-CTA forward-attention timings, 8 longs per CTA

@@ -710,13 +710,14 @@ struct LlamaBlock final : BlockImpl {
     bf16* d_o = sbf;
     if (now) gemm(di, di, Mi, w.o, di, true, w.dho, di, true, G + off.wo, di, tc::kAccF32);   // gWo += o^T dh
     gemm(Mi, di, di, w.dho, di, false, W + off.wo, di, false, d_o, di, tc::kStoreBF16);      // do = dh Wo^T
+    const bool attn_tc = llama::attn_fwd_tc_supported(T, hd);
     timed(KC_ATTN, 2.5 * attn_flops_fwd(rows), Mt * d * 16.0, [&] {
-      if (llama::attn_fwd_tc_supported(T, hd))
-        llama::attn_bwd_tc(c.qkv, w.o, c.lse, d_o, rows, T, H, hd, w.dqkv, Dsum, st);  // tcgen05 + TMEM
+      if (attn_tc)  // tcgen05 + TMEM, the RoPE backward in its dK / dQ epilogues
+        llama::attn_bwd_tc(c.qkv, w.o, c.lse, d_o, rows, T, H, hd, w.dqkv, Dsum, st, true);
       else
         llama::attn_bwd(c.qkv, w.o, c.lse, d_o, rows, T, H, hd, w.dqkv, Dsum, st);
     });
-    timed(KC_NORM, 0.0, Mt * d * 8.0, [&] { llama::rope(w.dqkv, Mt, T, d, H, 1, st); });
+    if (!attn_tc) timed(KC_NORM, 0.0, Mt * d * 8.0, [&] { llama::rope(w.dqkv, Mt, T, d, H, 1, st); });
     if (now) gemm(di, 3 * di, Mi, w.xn1, di, true, w.dqkv, 3 * di, true, G + off.wqkv, 3 * di, tc::kAccF32);
     gemm(Mi, di, 3 * di, w.dqkv, 3 * di, false, W + off.wqkv, 3 * di, false, dxn, di, tc::kStoreF32);  // dxn1
     timed(KC_NORM, 0.0, Mt * d * 18.0, [&] {

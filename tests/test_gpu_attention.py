@@ -108,3 +108,41 @@ def test_backward_vs_torch(shape, impl):
         a = dqkv.float()[:, blk * H * hd:(blk + 1) * H * hd]
         b = g[:, blk * H * hd:(blk + 1) * H * hd]
         assert ((a - b).norm() / b.norm()).item() < 3e-2, blk
+
+
+@pytest.mark.parametrize("shape", [(2, 256, 2, 64), (1, 1024, 3, 64), (1, 512, 2, 128), (1, 1024, 2, 128)])
+def test_backward_with_fused_rope_inverse(shape):
+    """impl | CKF_ATTN_ROPE_BWD (16): the dK / dQ epilogues apply the RoPE backward in fp32 before the
+    single bf16 rounding.  Checked against the fp32-torch attention gradient rotated by the
+    fp64 inverse RoPE (3e-2 per block, as the plain backward) and against the unfused
+    backward + ckf_llama_rope pass (two roundings: 1e-2); dv must be bit-identical to the plain
+    backward (no rotation on v)."""
+    from paper_2506_15461_b200._native import check, lib
+    from test_gpu_llama_kernels import _rope_ref
+    B, T, H, hd = shape
+    torch.manual_seed(5)
+    qkv = (torch.randn(B * T, 3 * H * hd, device="cuda") * 0.8).bfloat16()
+    o, lse = _fwd(qkv, B, T, H, hd, 0)
+    dout = torch.randn(B * T, H * hd, device="cuda").bfloat16()
+    Dsum = torch.empty(B * H * T, device="cuda")
+    fused = torch.zeros(B * T, 3 * H * hd, dtype=torch.bfloat16, device="cuda")
+    plain = torch.zeros_like(fused)
+    check(lib().ckf_attention_bwd(qkv.data_ptr(), o.data_ptr(), lse.data_ptr(), dout.data_ptr(), B, T, H, hd,
+                                  fused.data_ptr(), Dsum.data_ptr(), 2 | 16, None))
+    check(lib().ckf_attention_bwd(qkv.data_ptr(), o.data_ptr(), lse.data_ptr(), dout.data_ptr(), B, T, H, hd,
+                                  plain.data_ptr(), Dsum.data_ptr(), 2, None))
+    torch.cuda.synchronize()
+    d = H * hd
+    assert torch.equal(fused[:, 2 * d:], plain[:, 2 * d:])
+    two = plain.clone()
+    check(lib().ckf_llama_rope(two.data_ptr(), B * T, T, d, H, 1, None))
+    x = qkv.float().requires_grad_(True)
+    ro, _ = _ref(x, B, T, H, hd)
+    ro.backward(dout.float())
+    want = _rope_ref(x.grad.detach(), T, d, H, 1).float()
+    for blk in range(2):
+        a = fused.float()[:, blk * d:(blk + 1) * d]
+        b = want[:, blk * d:(blk + 1) * d]
+        c = two.float()[:, blk * d:(blk + 1) * d]
+        assert ((a - b).norm() / b.norm()).item() < 3e-2, blk
+        assert ((a - c).norm() / c.norm()).item() < 1e-2, blk
