@@ -130,6 +130,12 @@ constexpr int kFwdNgDefault = HD == 128 ? 2 : 1;
 #define CKF_ATTN_DEBUG_BUILD 0
 #endif
 constexpr bool kDbg = CKF_ATTN_DEBUG_BUILD != 0;
+// bottleneck experiments on the dK dV kernel (debug builds only): 1 = no softmax math (P / dS
+// constant), 2 = no MMAs issued (barriers still committed)
+#ifndef CKF_ATTN_BWD_EXPERIMENT
+#define CKF_ATTN_BWD_EXPERIMENT 0
+#endif
+constexpr int kBwdExp = CKF_ATTN_BWD_EXPERIMENT;
 constexpr int kBwdSplitDefault = 1;  // 2 measured no faster (1084.7 vs 1087.8 us at [64, 1024, 16, 64])  // exponential pairs (of 8) on the FMA pipe, forward
 
 // NG query tiles per CTA (NG = 2: query tiles 2c and 2c+1 share every K / V tile the producer
@@ -238,7 +244,7 @@ __global__ void __launch_bounds__(FwdCfg<HD, NG>::kThreads, FwdCfg<HD, NG>::kMin
       }
     }
   } else if (warp == 1 || (NG == 2 && warp == 3)) {
-    if (lane == 0) {
+    {  // whole warp; elect.sync issues (umma_*_w)
       // ---------------- MMA issuers, one per query tile (warp 1: group 0, warp 3: group 1): the
       // groups share the K / V stages (released by both issuers) but are otherwise independent,
       // so one group's softmax overlaps the other's MMAs as two CTAs per SM would.
@@ -257,10 +263,10 @@ __global__ void __launch_bounds__(FwdCfg<HD, NG>::kThreads, FwdCfg<HD, NG>::kMin
         const uint32_t ka = smem_u32(sm.k[ks]);
 #pragma unroll
         for (int k = 0; k < HD / 16; ++k)
-          umma_bf16(tmem + g * 128 + sb * FK, umma_desc_sw128(kmajor_k(qa, TQ, k), 16, 1024),
+          umma_bf16_w(tmem + g * 128 + sb * FK, umma_desc_sw128(kmajor_k(qa, TQ, k), 16, 1024),
                     umma_desc_sw128(kmajor_k(ka, FK, k), 16, 1024), kIdS, k > 0 ? 1u : 0u);
-        umma_commit(&sm.s_full[g][sb]);
-        umma_commit(&sm.k_empty[ks]);
+        umma_commit_w(&sm.s_full[g][sb]);
+        umma_commit_w(&sm.k_empty[ks]);
       };
       // S runs two tiles ahead of the softmax when a third V stage allows it: S_{j+2} goes into
       // S_j's TMEM buffer as soon as the softmax warps have loaded S_j (early in their tile j),
@@ -280,12 +286,12 @@ __global__ void __launch_bounds__(FwdCfg<HD, NG>::kThreads, FwdCfg<HD, NG>::kMin
         const uint32_t pa = smem_u32(sm.p[g][pb]), va = smem_u32(sm.v[vs]);
 #pragma unroll
         for (int k = 0; k < FK / 16; ++k)  // V MN-major: chunks of 64 hd columns FK*128 bytes apart
-          umma_bf16(tmem + NG * 128 + g * HD, umma_desc_sw128(pa + k * 32, 16, 1024),
+          umma_bf16_w(tmem + NG * 128 + g * HD, umma_desc_sw128(pa + k * 32, 16, 1024),
                     umma_desc_sw128(va + k * 2048, FK * 128, 1024), kIdO, (j > 0 || k > 0) ? 1u : 0u);
-        umma_commit(&sm.p_free[g][pb]);
-        umma_commit(&sm.v_empty[vs]);
+        umma_commit_w(&sm.p_free[g][pb]);
+        umma_commit_w(&sm.v_empty[vs]);
       }
-      umma_commit(&sm.o_full[g]);
+      umma_commit_w(&sm.o_full[g]);
     }
   } else if (warp >= 4) {
     // ---------------- softmax: one query row per thread, online with lazy rescaling
@@ -608,7 +614,7 @@ __global__ void __launch_bounds__(128 + 256 * SPLIT, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // the whole warp runs the issue loop; elect.sync picks the issuing lane (umma_*_w)
       constexpr uint32_t kIdS = idesc_bf16_f32(TK, PT, false, false);  // [keys x 64 q], K = hd
       constexpr uint32_t kIdA = idesc_bf16_f32(TK, HD, false, true);   // [keys x hd], K = 64 q, B MN-major
       int g = 0, lu = 0;
@@ -628,12 +634,13 @@ __global__ void __launch_bounds__(128 + 256 * SPLIT, 1)
           const uint32_t sd = tmem + static_cast<uint32_t>(bb * 128);
 #pragma unroll
           for (int k = 0; k < HD / 16; ++k) {
-            umma_bf16(sd, umma_desc_sw128(kmajor_k(ka, TK, k), 16, 1024),
+            if constexpr (kBwdExp == 2) continue;
+            umma_bf16_w(sd, umma_desc_sw128(kmajor_k(ka, TK, k), 16, 1024),
                       umma_desc_sw128(kmajor_k(qa, PT, k), 16, 1024), kIdS, k > 0 ? 1u : 0u);
-            umma_bf16(sd + 64, umma_desc_sw128(kmajor_k(va, TK, k), 16, 1024),
+            umma_bf16_w(sd + 64, umma_desc_sw128(kmajor_k(va, TK, k), 16, 1024),
                       umma_desc_sw128(kmajor_k(oa, PT, k), 16, 1024), kIdS, k > 0 ? 1u : 0u);
           }
-          umma_commit(&sm.s_full[bb]);
+          umma_commit_w(&sm.s_full[bb]);
           if (kDbg) tw[0] += clock64() - ti;
         };
         // S/dP run LA tiles ahead of the dV/dK MMAs.  LA = 3 (five Q/dO stages, head_dim 64):
@@ -661,21 +668,22 @@ __global__ void __launch_bounds__(128 + 256 * SPLIT, 1)
           const uint32_t pa = smem_u32(sm.p[bb]), da = smem_u32(sm.ds[bb]);
 #pragma unroll
           for (int k = 0; k < PT / 16; ++k) {  // B MN-major: HD/64 chunks of [64 q][128 B], PT*128 apart
-            umma_bf16(acc, umma_desc_sw128(pa + k * 32, 16, 1024), umma_desc_sw128(oa + k * 2048, PT * 128, 1024),
+            if constexpr (kBwdExp == 2) continue;
+            umma_bf16_w(acc, umma_desc_sw128(pa + k * 32, 16, 1024), umma_desc_sw128(oa + k * 2048, PT * 128, 1024),
                       kIdA, (i > 0 || k > 0) ? 1u : 0u);
-            umma_bf16(acc + HD, umma_desc_sw128(da + k * 32, 16, 1024),
+            umma_bf16_w(acc + HD, umma_desc_sw128(da + k * 32, 16, 1024),
                       umma_desc_sw128(qa + k * 2048, PT * 128, 1024), kIdA, (i > 0 || k > 0) ? 1u : 0u);
           }
-          umma_commit(&sm.pd_free[bb]);
-          umma_commit(&sm.qd_empty[st]);
+          umma_commit_w(&sm.pd_free[bb]);
+          umma_commit_w(&sm.qd_empty[st]);
           if constexpr (ST < 4)
             if (i + 2 < ntiles) issue_s(gi + 2);
         }
-        umma_commit(&sm.acc_full[aset]);
-        umma_commit(&sm.kv_empty[kbuf]);
+        umma_commit_w(&sm.acc_full[aset]);
+        umma_commit_w(&sm.kv_empty[kbuf]);
         g += ntiles;
       }
-      if (kDbg && dbg) {
+      if (kDbg && dbg && lane == 0) {
         long long* d = dbg + 16 * blockIdx.x;
         d[8] = tw[0];
         d[9] = tw[1];
@@ -756,6 +764,11 @@ __global__ void __launch_bounds__(128 + 256 * SPLIT, 1)
         const uint32_t la_ = smem_u32(&sm.lse[st][0]), da_ = smem_u32(&sm.dsum[st][0]);
 #pragma unroll
         for (int lg = 0; lg < QW / 8; ++lg) {  // 8 queries at a time: P^T, dS^T -> bf16 -> swizzled smem
+          if constexpr (kBwdExp == 1) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) pkp[4 * lg + e] = pkd[4 * lg + e] = us[8 * lg + e] ^ ud[8 * lg + e];
+            continue;
+          }
           const int g8 = half * (QW / 8) + lg;
           const uint4 la = ld_shared_v4(la_ + 32 * g8), lb = ld_shared_v4(la_ + 32 * g8 + 16);
           const uint4 da4 = ld_shared_v4(da_ + 32 * g8), db4 = ld_shared_v4(da_ + 32 * g8 + 16);
@@ -1163,7 +1176,7 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // whole warp; elect.sync issues (umma_*_w)
       constexpr uint32_t kId = idesc_bf16_f32(TQ, HD, true, true);
       int g = 0, lu = 0;
       for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lu) {
@@ -1178,11 +1191,11 @@ __global__ void __launch_bounds__(256, 1)
           const uint32_t aa = smem_u32(sm.a[st]), ba = smem_u32(sm.b[st]);
 #pragma unroll
           for (int k = 0; k < PT / 16; ++k)
-            umma_bf16(acc, umma_desc_sw128(aa + k * 2048, 8192, 1024), umma_desc_sw128(ba + k * 2048, PT * 128, 1024),
+            umma_bf16_w(acc, umma_desc_sw128(aa + k * 2048, 8192, 1024), umma_desc_sw128(ba + k * 2048, PT * 128, 1024),
                       kId, (j > 0 || k > 0) ? 1u : 0u);
-          umma_commit(&sm.empty[st]);
+          umma_commit_w(&sm.empty[st]);
         }
-        umma_commit(&sm.acc_full[aset]);
+        umma_commit_w(&sm.acc_full[aset]);
       }
     }
   } else if (warp >= 4) {
