@@ -305,8 +305,9 @@ __global__ void __launch_bounds__(gemm_threads(EPI, NCTA), 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && leader) {
-      // ---------------- MMA issuer (the pair's leader issues for both CTAs)
+    if (leader) {
+      // ---------------- MMA issuer (the pair's leader issues for both CTAs): the whole warp runs
+      // the loop (descriptors in uniform registers), elect.sync picks the issuing lane
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -330,23 +331,23 @@ __global__ void __launch_bounds__(gemm_threads(EPI, NCTA), 1)
             const uint64_t ad = A_MN ? umma_desc_sw128(a0 + k * 2048, 8192, 1024) : umma_desc_sw128(a0 + k * 32, 16, 1024);
             const uint64_t bd = B_MN ? umma_desc_sw128(b0 + k * 2048, 8192, 1024) : umma_desc_sw128(b0 + k * 32, 16, 1024);
             if constexpr (NCTA == 2)
-              umma_bf16_2sm(d, ad, bd, IDESC, (kb > w.kb0 || k > 0) ? 1u : 0u);
+              umma_bf16_2sm_w(d, ad, bd, IDESC, (kb > w.kb0 || k > 0) ? 1u : 0u);
             else
-              umma_bf16(d, ad, bd, IDESC, (kb > w.kb0 || k > 0) ? 1u : 0u);
+              umma_bf16_w(d, ad, bd, IDESC, (kb > w.kb0 || k > 0) ? 1u : 0u);
           }
           if constexpr (NCTA == 2)
-            umma_commit_2sm(&empty[stage], 0x3);
+            umma_commit_2sm_w(&empty[stage], 0x3);
           else
-            umma_commit(&empty[stage]);
+            umma_commit_w(&empty[stage]);
           if (++stage == ST) {
             stage = 0;
             phase ^= 1;
           }
         }
         if constexpr (NCTA == 2)
-          umma_commit_2sm(&tfull[acc], 0x3);
+          umma_commit_2sm_w(&tfull[acc], 0x3);
         else
-          umma_commit(&tfull[acc]);
+          umma_commit_w(&tfull[acc]);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
