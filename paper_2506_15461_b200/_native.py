@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libckf.so")
+# CKF_LIB_PATH: an alternative build of the same library (A/B timing tools only)
+LIB_PATH = os.environ.get("CKF_LIB_PATH") or os.path.join(HERE, "libckf.so")
 
 CKF_OK, CKF_E_CONFIG, CKF_E_DIVERGENCE, CKF_E_USAGE, CKF_E_PARSE, CKF_E_UNSUPPORTED_RECOVERY, CKF_E_CUDA, \
     CKF_E_NCCL = range(8)

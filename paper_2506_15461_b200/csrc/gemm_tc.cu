@@ -257,7 +257,15 @@ __global__ void __launch_bounds__(gemm_threads(EPI, NCTA), 1)
   const int units = (p.gate && *reinterpret_cast<const volatile int*>(p.gate) == 0) ? 0 : p.units;
 
   if (warp == 0) {
-    if (lane == 0) {
+    // the whole warp runs the producer loop (elect.sync issues) except for the weight gradients
+    // (A MN-major), whose split-K epilogue shares the SM sub-partition with this warp: there one
+    // lane runs it (measured: wgrad families 5-20 % slower with a converged producer, the others
+    // 1-2 % faster)
+#ifndef CKF_GEMM_WARP_PRODUCER
+#define CKF_GEMM_WARP_PRODUCER 1
+#endif
+    constexpr bool kWP = CKF_GEMM_WARP_PRODUCER == 2 || (CKF_GEMM_WARP_PRODUCER == 1 && !A_MN);
+    if (kWP || lane == 0) {
       // ---------------- TMA producer
       int stage = 0;
       uint32_t phase = 0;
@@ -272,10 +280,19 @@ __global__ void __launch_bounds__(gemm_threads(EPI, NCTA), 1)
           uint8_t* b = sB + stage * C::kBStage;
           // NCTA = 2: the leader's full barrier counts both CTAs' bytes; both CTAs' loads complete on it
           const uint32_t fb = NCTA == 2 ? mapa_shared(&full[stage], 0) : smem_u32(&full[stage]);
-          if (leader) mbar_arrive_expect_tx(&full[stage], NCTA * C::kStageBytes);
+          if (leader) {
+            if constexpr (kWP)
+              mbar_arrive_expect_tx_w(&full[stage], NCTA * C::kStageBytes);
+            else
+              mbar_arrive_expect_tx(&full[stage], NCTA * C::kStageBytes);
+          }
           auto load = [&](void* dst, const CUtensorMap* map, int c0, int c1) {
-            if constexpr (NCTA == 2)
+            if constexpr (NCTA == 2 && kWP)
+              tma_load_2d_pair_w(dst, map, fb, c0, c1);
+            else if constexpr (NCTA == 2)
               tma_load_2d_pair(dst, map, fb, c0, c1);
+            else if constexpr (kWP)
+              tma_load_2d_w(dst, map, &full[stage], c0, c1);
             else
               tma_load_2d(dst, map, &full[stage], c0, c1);
           };
