@@ -136,6 +136,9 @@ constexpr bool kDbg = CKF_ATTN_DEBUG_BUILD != 0;
 #define CKF_ATTN_BWD_EXPERIMENT 0
 #endif
 constexpr int kBwdExp = CKF_ATTN_BWD_EXPERIMENT;
+#ifndef CKF_ATTN_P_TMEM
+#define CKF_ATTN_P_TMEM 1
+#endif
 constexpr int kBwdSplitDefault = 1;  // 2 measured no faster (1084.7 vs 1087.8 us at [64, 1024, 16, 64])  // exponential pairs (of 8) on the FMA pipe, forward
 
 // NG query tiles per CTA (NG = 2: query tiles 2c and 2c+1 share every K / V tile the producer
@@ -154,6 +157,9 @@ struct FwdCfg {
   // S_{j+2} issued two tiles ahead (into the buffer the softmax has just loaded) when a third V
   // stage lets the producer run that far ahead
   static constexpr bool kEarly = kVSt >= 3;
+  // P in TMEM (A operand of P V from tensor memory: no shared-memory round trip, no proxy fence):
+  // columns 192 + 32 pb next to S pair 0-127 and O 128-191 -- head_dim 64, one query tile
+  static constexpr bool kPTmem = HD == 64 && NG == 1 && CKF_ATTN_P_TMEM;
 };
 
 template <int HD, int NG>
@@ -162,7 +168,7 @@ struct Smem {
   uint8_t q[NG][C::kQ];
   uint8_t k[C::kKSt][C::kK];
   uint8_t v[C::kVSt][C::kK];
-  uint8_t p[NG][2][kPTile];
+  uint8_t p[C::kPTmem ? 1 : NG][C::kPTmem ? 1 : 2][C::kPTmem ? 16 : kPTile];
   uint64_t q_full;
   uint64_t k_full[C::kKSt], k_empty[C::kKSt], v_full[C::kVSt], v_empty[C::kVSt];
   uint64_t s_full[NG][2], s_free[NG][2], p_full[NG][2], p_free[NG][2];
@@ -283,11 +289,19 @@ __global__ void __launch_bounds__(FwdCfg<HD, NG>::kThreads, FwdCfg<HD, NG>::kMin
         mbar_wait(&sm.v_full[vs], (j / VS) & 1);
         mbar_wait(&sm.p_full[g][pb], (j >> 1) & 1);
         tc_fence_after();
-        const uint32_t pa = smem_u32(sm.p[g][pb]), va = smem_u32(sm.v[vs]);
+        const uint32_t va = smem_u32(sm.v[vs]);
+        if constexpr (C::kPTmem) {
 #pragma unroll
-        for (int k = 0; k < FK / 16; ++k)  // V MN-major: chunks of 64 hd columns FK*128 bytes apart
-          umma_bf16_w(tmem + NG * 128 + g * HD, umma_desc_sw128(pa + k * 32, 16, 1024),
-                    umma_desc_sw128(va + k * 2048, FK * 128, 1024), kIdO, (j > 0 || k > 0) ? 1u : 0u);
+          for (int k = 0; k < FK / 16; ++k)  // P from TMEM: 8 packed columns per 16 keys
+            umma_bf16_ts_w(tmem + 128, tmem + 192 + pb * 32 + k * 8, umma_desc_sw128(va + k * 2048, FK * 128, 1024),
+                           kIdO, (j > 0 || k > 0) ? 1u : 0u);
+        } else {
+          const uint32_t pa = smem_u32(sm.p[g][pb]);
+#pragma unroll
+          for (int k = 0; k < FK / 16; ++k)  // V MN-major: chunks of 64 hd columns FK*128 bytes apart
+            umma_bf16_w(tmem + NG * 128 + g * HD, umma_desc_sw128(pa + k * 32, 16, 1024),
+                        umma_desc_sw128(va + k * 2048, FK * 128, 1024), kIdO, (j > 0 || k > 0) ? 1u : 0u);
+        }
         umma_commit_w(&sm.p_free[g][pb]);
         umma_commit_w(&sm.v_empty[vs]);
       }
@@ -323,7 +337,7 @@ __global__ void __launch_bounds__(FwdCfg<HD, NG>::kThreads, FwdCfg<HD, NG>::kMin
       if (lane == 0) mbar_arrive(&sm.s_free[g][sb]);
       const int kbase = j * FK;
       const int nvalid = min(FK, q - kbase + 1);  // keys <= q are visible (causal)
-      const uint32_t prow = smem_u32(sm.p[g][pb]) + r * 128;
+      const uint32_t prow = C::kPTmem ? 0u : smem_u32(sm.p[g][pb]) + r * 128;
       // P = 2^(S scale - mc) -> bf16 -> swizzled smem (32 keys at a time); returns the row sum
       auto write_p = [&](float mc) -> float {
         const f32x2 sc2 = f2(scale_log2, scale_log2), nm2 = f2(-mc, -mc);
@@ -355,10 +369,14 @@ __global__ void __launch_bounds__(FwdCfg<HD, NG>::kThreads, FwdCfg<HD, NG>::kMin
           float la, lb;
           f2split(fadd2(l2[0], l2[1]), la, lb);
           lt += la + lb;
+          if constexpr (C::kPTmem) {
+            tmem_st16(trow + 192 + pb * 32 + hf * 16, w);
+          } else {
 #pragma unroll
-          for (int pc = 0; pc < 4; ++pc)
-            st_shared_v4(prow + (((hf * 4 + pc) ^ (r & 7)) << 4), w[4 * pc], w[4 * pc + 1], w[4 * pc + 2],
-                         w[4 * pc + 3]);
+            for (int pc = 0; pc < 4; ++pc)
+              st_shared_v4(prow + (((hf * 4 + pc) ^ (r & 7)) << 4), w[4 * pc], w[4 * pc + 1], w[4 * pc + 2],
+                           w[4 * pc + 3]);
+          }
         }
         return lt;
       };
@@ -413,7 +431,10 @@ __global__ void __launch_bounds__(FwdCfg<HD, NG>::kThreads, FwdCfg<HD, NG>::kMin
         lt = write_p(m);
       }
       l += lt;
-      fence_proxy_async();
+      if constexpr (C::kPTmem)
+        tmem_st_wait();  // P in TMEM before the MMA reads it
+      else
+        fence_proxy_async();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.p_full[g][pb]);
