@@ -195,7 +195,7 @@ int ckf_attention_bwd(const void* qkv, const void* o, const float* lse, const vo
  *   swiglu_fwd: a = silu(gate) * up, gu = [gate | up] [ntok x 2f];  swiglu_bwd: dgu from da
  *   embed_fwd: h = E[tok];  embed_bwd: gE[v] += sum of dh over tok == v (token order, deterministic)
  *   gemm_qkv_rope: C = bf16(A B) with RoPE fused into the epilogue on the first 2d columns
- *         (A [M x K] K-major, B [K x 3d] N-major; head_dim 64), as the QKV projection runs it */
+ *         (A [M x K] K-major, B [K x 3d] N-major; head_dim 64 or 128), as the QKV projection runs it */
 int ckf_llama_rmsnorm_fwd(const float* x, const float* g, size_t rows, size_t d, void* y_bf16, float* rstd,
                           float* xcopy, void* stream);
 int ckf_llama_rmsnorm_bwd(const float* dy, const float* x, const float* g, const float* rstd, size_t rows, size_t d,

@@ -860,8 +860,9 @@ int ckf_llama_embed_bwd(const int* tok, size_t ntok, const float* dh, size_t d, 
 }
 int ckf_gemm_qkv_rope(int M, int K, const void* A, const void* B, void* C, size_t T, size_t heads, void* stream) {
   return guard([&] {
-    if (K <= 0 || heads == 0 || K % static_cast<int>(heads) || K / static_cast<int>(heads) != 64)
-      ckf::raise(CKF_E_CONFIG, "gemm_qkv_rope: the fused RoPE epilogue serves head_dim 64 (K = d = 64 * heads)");
+    const int hd = heads ? K / static_cast<int>(heads) : 0;
+    if (K <= 0 || heads == 0 || K % static_cast<int>(heads) || (hd != 64 && hd != 128))
+      ckf::raise(CKF_E_CONFIG, "gemm_qkv_rope: the fused RoPE epilogue serves head_dim 64 or 128 (K = d = hd * heads)");
     auto st = static_cast<cudaStream_t>(stream);
     ckf::tc::GemmDesc g;
     g.M = M;
@@ -876,9 +877,10 @@ int ckf_gemm_qkv_rope(int M, int K, const void* A, const void* B, void* C, size_
     g.C = C;
     g.ldc = 3 * K;
     g.epi = ckf::tc::kStoreBF16;
-    g.rope_tab = ckf::llama::rope_table_pair_major(T, 64, st);
+    g.rope_tab = ckf::llama::rope_table_pair_major(T, hd, st);
     g.rope_T = static_cast<int>(T);
     g.rope_cols = 2 * K;
+    g.rope_hd = hd;
     ckf::tc::gemm_bf16(g, st);
   });
 }

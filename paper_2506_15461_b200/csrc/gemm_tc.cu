@@ -123,8 +123,8 @@ struct Params {
   float* ws;     // split-K partial tiles: [units][BM][BN] fp32
   float* C;      // split-K: fp32 C (row pitch ldc) the reduced tile is added into
   int ldc;
-  const float2* rope_tab;  // fused RoPE (bf16 epilogue): heads of 64 columns below rope_cols
-  int rope_T, rope_cols;
+  const float2* rope_tab;  // fused RoPE (bf16 epilogue): heads of rope_hd (64 or 128) columns below rope_cols
+  int rope_T, rope_cols, rope_hd;
   int f;                   // kSwiGLU / kSwiGLUBwd: ffn width (column offset of the up half)
   const __nv_bfloat16* gu; // kSwiGLUBwd: [M x 2f] gate/up activations (row pitch 2f)
   const float* row_scale;  // kStoreF32: per-row scale instead of alpha
@@ -610,6 +610,36 @@ __global__ void __launch_bounds__(gemm_threads(EPI, NCTA), 1)
             bulk_commit();
           }
         }
+      } else if (EPI == kStoreBF16 && p.rope_tab && p.rope_hd == 128 && w.nb * BN < p.rope_cols) {
+        // fused RoPE on 128-column heads: the warp's slice is whole heads; pairs (j, j+64) are the
+        // two 64-column chunks of a head, rotated in fp32 and stored as two bf16 chunks
+        const float2* cs = p.rope_tab + (m0 + lane) % p.rope_T;  // pair-major: coalesced per j
+#pragma unroll 1
+        for (int c0 = eh * (BN / EH); c0 < (eh + 1) * (BN / EH); c0 += 128) {
+          uint32_t ra[64], rb[64];
+          tmem_ld32(trow + c0, *reinterpret_cast<uint32_t(*)[32]>(&ra[0]));
+          tmem_ld32(trow + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&ra[32]));
+          tmem_ld32(trow + c0 + 64, *reinterpret_cast<uint32_t(*)[32]>(&rb[0]));
+          tmem_ld32(trow + c0 + 96, *reinterpret_cast<uint32_t(*)[32]>(&rb[32]));
+          tmem_ld_wait();
+          if (c0 + 128 >= (eh + 1) * (BN / EH)) {  // last chunks loaded: hand the accumulator back early
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) release_acc(acc);
+          }
+          uint32_t pa[32], pb[32];
+#pragma unroll
+          for (int j = 0; j < 64; j += 2) {
+            const float2 t0 = cs[static_cast<size_t>(j) * p.rope_T], t1 = cs[static_cast<size_t>(j + 1) * p.rope_T];
+            const float x10 = __uint_as_float(ra[j]), x20 = __uint_as_float(rb[j]);
+            const float x11 = __uint_as_float(ra[j + 1]), x21 = __uint_as_float(rb[j + 1]);
+            pa[j / 2] = pack_bf16((x10 * t0.x - x20 * t0.y) * p.alpha, (x11 * t1.x - x21 * t1.y) * p.alpha);
+            pb[j / 2] = pack_bf16((x20 * t0.x + x10 * t0.y) * p.alpha, (x21 * t1.x + x11 * t1.y) * p.alpha);
+          }
+          const int n0 = w.nb * BN + c0;
+          store_bf16_chunk(pa, &tmap_c, n0, m0);
+          store_bf16_chunk(pb, &tmap_c, n0 + 64, m0);
+        }
       } else {
       float rsc = p.alpha;  // kStoreF32 with a per-row scale: this lane's row
       if (EPI == kStoreF32 && p.row_scale) rsc = m0 + lane < p.M ? __ldg(p.row_scale + m0 + lane) : 0.f;
@@ -910,6 +940,7 @@ void launch_t(const GemmDesc& g, int splits, cudaStream_t s) {
   p.rope_tab = g.rope_tab;
   p.rope_T = g.rope_T;
   p.rope_cols = g.rope_cols;
+  p.rope_hd = g.rope_hd;
   p.f = EPI == kSwiGLU ? g.N / 2 : g.N;
   p.gu = EPI == kSwiGLUBwd ? static_cast<const __nv_bfloat16*>(g.aux) : nullptr;
   p.row_scale = g.row_scale;
@@ -925,8 +956,10 @@ void launch_t(const GemmDesc& g, int splits, cudaStream_t s) {
     if (EPI == kSwiGLUBwd && (g.N % 64 != 0 || g.ldc != 2 * g.N || (reinterpret_cast<uintptr_t>(g.aux) & 15)))
       raise(1, "gemm_bf16: fused SwiGLU backward needs f % 64 == 0, ldc == 2f, 16-byte aligned gu");
   }
-  if (g.rope_tab && (EPI != kStoreBF16 || g.rope_T <= 0 || g.rope_cols % 64))
-    raise(1, "gemm_bf16: fused RoPE needs the bf16 epilogue and 64-column heads");
+  if (g.rope_tab && (EPI != kStoreBF16 || g.rope_T <= 0 || g.rope_cols % 64 || (g.rope_hd != 64 && g.rope_hd != 128)))
+    raise(1, "gemm_bf16: fused RoPE needs the bf16 epilogue and 64- or 128-column heads");
+  if (g.rope_tab && g.rope_hd == 128 && (g.rope_cols % BN != 0 || (BN / C::kEW * 4) % 128 != 0))
+    raise(1, "gemm_bf16: 128-column RoPE heads need rope_cols % BN == 0 and 128-column epilogue slices");
   const CUtensorMap twm = p.splits > 1    ? tma::make_2d_f32(p.ws, BN, static_cast<uint64_t>(p.units) * NCTA * BM, BN, 32, 32)
                           : EPI == kSwiGLU    ? tma::make_2d_bf16(g.aux, g.N / 2, g.M, g.ldaux, 64, 32)
                           : EPI == kSwiGLUBwd ? tma::make_2d_bf16(g.aux, 2 * g.N, g.M, g.ldaux, 64, 32)

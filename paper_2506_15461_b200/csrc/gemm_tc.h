@@ -55,8 +55,10 @@ struct GemmDesc {
   // fused rotary embedding (kStoreBF16 only): columns [0, rope_cols) are 64-wide heads whose
   // (j, j+32) pairs are rotated by rope_tab[j * rope_T + row % rope_T] = (cos, sin) (the
   // pair-major table: a warp's 32 consecutive rows read 32 adjacent entries)
+  // rope_hd = 128: heads of 128 columns, pairs (j, j+64) spanning two 64-column chunks of one
+  // epilogue warp's slice (rope_cols % 256 == 0)
   const float2* rope_tab = nullptr;
-  int rope_T = 0, rope_cols = 0;
+  int rope_T = 0, rope_cols = 0, rope_hd = 64;
   void* aux = nullptr;  // kSwiGLU: a (written); kSwiGLUBwd: gu (read)
   int ldaux = 0;
   // kStoreF32: per-row output scale (C[i,:] = row_scale[i] * acc) instead of alpha

@@ -277,6 +277,7 @@ struct LlamaBlock final : BlockImpl {
     g.rope_tab = rope_tab;
     g.rope_T = static_cast<int>(T);
     g.rope_cols = rope_cols;
+    g.rope_hd = static_cast<int>(hd);
     g.M = M;
     g.N = N;
     g.K = K;
@@ -656,7 +657,7 @@ struct LlamaBlock final : BlockImpl {
     const float* Wf = wf(sid, li);
     const int Mi = static_cast<int>(Mt), di = static_cast<int>(d), fi = static_cast<int>(f);
     timed(KC_NORM, 0.0, Mt * d * 10.0, [&] { llama::rmsnorm_fwd(h, Wf + off.g1, Mt, d, w.xn1, c.rstd1, c.h_in, st); });
-    if (hd == 64) {  // RoPE fused into the QKV GEMM epilogue (q and k column blocks)
+    if (hd == 64 || (hd == 128 && (2 * d) % 256 == 0)) {  // RoPE fused into the QKV GEMM epilogue (q, k blocks)
       gemm(Mi, 3 * di, di, w.xn1, di, false, W + off.wqkv, 3 * di, true, c.qkv, 3 * di, tc::kStoreBF16,
            llama::rope_table_pair_major(T, hd, st), static_cast<int>(2 * d));
     } else {

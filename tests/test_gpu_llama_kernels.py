@@ -200,12 +200,14 @@ def test_fused_swiglu_epilogues_at_workload_widths(d, f):
     assert float((da.float() - da_ref).norm() / da_ref.norm()) < 4e-3
 
 
-@pytest.mark.parametrize("T,d", [(1024, 512), (1024, 1024), (128, 256)])
-def test_qkv_gemm_with_fused_rope(T, d):
-    # the QKV projection's epilogue applies RoPE to the fp32 accumulators before the bf16 store:
+@pytest.mark.parametrize("T,d,hd", [(1024, 512, 64), (1024, 1024, 64), (128, 256, 64), (4096, 2048, 128),
+                                    (1024, 1024, 128), (256, 256, 128)])
+def test_qkv_gemm_with_fused_rope(T, d, hd):
+    # the QKV projection's epilogue applies RoPE to the fp32 accumulators before the bf16 store
+    # (64-column heads: pairs inside one chunk; 128-column heads: pairs across a warp's two chunks):
     # within one bf16 rounding (plus the fp32 accumulation order) of the fp32 reference
     check, L = _lib()
-    heads = d // 64
+    heads = d // hd
     g = torch.Generator(device="cuda").manual_seed(T + d)
     M = 2 * T
     A = torch.randn(M, d, device="cuda", generator=g).bfloat16()
