@@ -522,6 +522,34 @@ __global__ void dsum_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bflo
 // keeps one of each in the dK dV kernel), and a unit's epilogue runs one tile late,
 // overlapping the next unit.  Tile / unit counters run across units, so every mbarrier keeps a
 // single phase sequence.
+// Persistent backward kernels: each CTA walks pairs of units of the same (sequence, head) -- the
+// longest (index pi) then the shortest (index n-1-pi) -- so every pair has the same total length
+// (load balance without a longest-first order across heads) and the second unit re-reads the
+// operand tiles the first just pulled through L2 (the K tiles of dQ, the Q / dO tiles of dK dV)
+// instead of DRAM.  Unit ids keep the u = idx * BH + bh encoding (idx 0 = longest).
+struct UnitIter {
+  int s, half;
+};
+__device__ __forceinline__ bool next_unit(UnitIter& it, int n, int BH, int& u) {
+  const int npairs = (n + 1) / 2;
+  while (it.s < npairs * BH) {
+    const int pi = it.s / BH, bh = it.s - pi * BH;
+    const int idx = it.half ? n - 1 - pi : pi;
+    const bool valid = !(it.half && n - 1 - pi == pi);  // odd n: the middle unit once
+    if (it.half) {
+      it.half = 0;
+      it.s += static_cast<int>(gridDim.x);
+    } else {
+      it.half = 1;
+    }
+    if (valid) {
+      u = idx * BH + bh;
+      return true;
+    }
+  }
+  return false;
+}
+
 constexpr int PT = 64;                 // inner tile: queries (dK/dV kernel) or keys (dQ kernel)
 constexpr uint32_t kPB = TQ * PT * 2;  // 16 KiB: P^T / dS^T [128 rows][64 cols] bf16, one SW128 chunk
 
@@ -612,7 +640,8 @@ __global__ void __launch_bounds__(128 + 256 * SPLIT, 1)
   if (warp == 0) {
     if (lane == 0) {
       int g = 0, lu = 0;
-      for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lu) {
+      UnitIter it_{static_cast<int>(blockIdx.x), 0};
+      for (int u = 0; next_unit(it_, nqb, BH, u); ++lu) {
         const int kb = u / BH, bh = u - kb * BH, b = bh / H, h = bh - b * H;
         const int row0 = b * T;
         const int kbuf = lu % NU;
@@ -639,7 +668,8 @@ __global__ void __launch_bounds__(128 + 256 * SPLIT, 1)
       constexpr uint32_t kIdS = idesc_bf16_f32(TK, PT, false, false);  // [keys x 64 q], K = hd
       constexpr uint32_t kIdA = idesc_bf16_f32(TK, HD, false, true);   // [keys x hd], K = 64 q, B MN-major
       int g = 0, lu = 0;
-      for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lu) {
+      UnitIter it_{static_cast<int>(blockIdx.x), 0};
+      for (int u = 0; next_unit(it_, nqb, BH, u); ++lu) {
         const int ntiles = 2 * (nqb - u / BH);
         const int kbuf = lu % NU, aset = lu % NA;
         const uint32_t acc = tmem + 256 + static_cast<uint32_t>(aset * 2 * HD);
@@ -754,7 +784,8 @@ __global__ void __launch_bounds__(128 + 256 * SPLIT, 1)
     };
     int pend_u = -1, pend_lu = 0;
     int g = 0, lu = 0;
-    for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lu) {
+    UnitIter it_{static_cast<int>(blockIdx.x), 0};
+    for (int u = 0; next_unit(it_, nqb, BH, u); ++lu) {
       const int ntiles = 2 * (nqb - u / BH);
       for (int i = grp; i < ntiles; i += 2) {
         const int gi = g + i, st = gi % ST;
@@ -1182,7 +1213,8 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 0) {
     if (lane == 0) {
       int g = 0;
-      for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+      UnitIter it_{static_cast<int>(blockIdx.x), 0};
+      for (int u = 0; next_unit(it_, nqb, BH, u);) {
         const int qi = u / BH, bh = u - qi * BH, b = bh / H, h = bh - b * H;
         const int qb = nqb - 1 - qi, ntiles = 2 * (qb + 1);
         for (int j = 0; j < ntiles; ++j, ++g) {
@@ -1200,7 +1232,8 @@ __global__ void __launch_bounds__(256, 1)
     {  // whole warp; elect.sync issues (umma_*_w)
       constexpr uint32_t kId = idesc_bf16_f32(TQ, HD, true, true);
       int g = 0, lu = 0;
-      for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lu) {
+      UnitIter it_{static_cast<int>(blockIdx.x), 0};
+      for (int u = 0; next_unit(it_, nqb, BH, u); ++lu) {
         const int qb = nqb - 1 - u / BH, ntiles = 2 * (qb + 1), aset = lu & 1;
         mbar_wait(&sm.acc_free[aset], ((lu >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -1223,7 +1256,8 @@ __global__ void __launch_bounds__(256, 1)
     const int quarter = warp - 4, r = quarter * 32 + lane;
     const size_t ld = static_cast<size_t>(3) * H * HD;
     int lu = 0;
-    for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lu) {
+    UnitIter it_{static_cast<int>(blockIdx.x), 0};
+      for (int u = 0; next_unit(it_, nqb, BH, u); ++lu) {
       const int qi = u / BH, bh = u - qi * BH, b = bh / H, h = bh - b * H;
       const int q = (nqb - 1 - qi) * TQ + r, aset = lu & 1;
       mbar_wait(&sm.acc_full[aset], (lu >> 1) & 1);
@@ -1366,7 +1400,10 @@ void bwd_launch(const bf16* qkv, const bf16* o, const float* lse, const bf16* do
     const CUtensorMap tds32 = stored_ds ? tma::make_2d_bf16(dst, 64, nb * H * n64 * n64 * 64, 64, 64, 32) : tq;
     const CUtensorMap tds64 = stored_ds ? tma::make_2d_bf16(dst, 64, nb * H * n64 * n64 * 64, 64, 64, 64) : tq;
     const int BH = static_cast<int>(nb * H), units = static_cast<int>(T / TQ) * BH;
-    const unsigned grid = static_cast<unsigned>(std::min(units, num_sms_attn()));
+    // unit pairs (next_unit): one per CTA slot
+    const int pairs = static_cast<int>((T / TQ + 1) / 2) * BH;
+    const unsigned grid = static_cast<unsigned>(std::min(pairs, num_sms_attn()));
+    (void)units;
     kkv<<<grid, kv_threads, smem_kv, s>>>(tq, tq64, td64, tds32, stored_ds ? 1 : 0, lse_c, D_c, static_cast<int>(T),
                                           static_cast<int>(H), BH, dq_c, scale, scale * kLog2e, rtab,
                                           dbg ? dbg + 8 * 32768 : nullptr);
