@@ -40,6 +40,6 @@ a = np.array(buf2[8 * 32768:]).reshape(148, 16)
 t = a[:, 0].sum()
 print(f"dkdv (persistent, 148 CTAs): tiles/CTA {a[:,0].mean():.1f}  total cycles {a[:,5].mean():.0f}  per tile {a[:,5].sum()/t:.0f}")
 print(f"  softmax per tile: wait S {a[:,1].sum()/t:.0f}  wait pd_free {a[:,2].sum()/t:.0f}  compute {a[:,3].sum()/t:.0f} "
-      f"(of which TMEM loads {a[:,6].sum()/t:.0f})  "
+      f"(of which TMEM loads {a[:,6].sum()/t:.0f})  store phase {a[:,7].sum()/t:.0f}  "
       f"epilogue/unit-share {a[:,4].sum()/t:.0f}")
 print(f"  MMA per tile: issue_s(+waits) {a[:,8].sum()/t:.0f}  acc_free wait {a[:,9].sum()/t:.0f}  pd_full wait {a[:,10].sum()/t:.0f}")
