@@ -22,7 +22,12 @@ echo "gemm launches per step: $NG"
 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
     -k regex:gemm_kernel -c $NG --csv --log-file $O/r02_gemm_traffic.csv $B > $O/r02_gemm_traffic.log 2>&1
 python tools/ncu_traffic.py $O/r02_gemm_traffic.csv $O/r02_llama-500m_gemm_dram_traffic.json "$B (first step, $NG GEMM launches)"
-for K in "gemm_kernel<256, 0, 1, 3" "gemm_kernel<256, 0, 0, 4" "gemm_kernel<256, 1, 1, 2" "gemm_kernel<256, 0, 1, 5" attn_fwd_tc attn_dkdv attn_dq_gemm; do
+# (demangled names read "gemm_kernel<(int)256, (bool)0, ...": "." matches the parentheses)
+KLIST=("gemm_kernel<.int.256, .bool.0, .bool.1, .int.3" "gemm_kernel<.int.256, .bool.0, .bool.0, .int.4"
+       "gemm_kernel<.int.256, .bool.1, .bool.1, .int.2" "gemm_kernel<.int.256, .bool.0, .bool.1, .int.5"
+       attn_fwd_tc attn_dkdv attn_dq_gemm)
+[ -n "${ONLY_GEMM:-}" ] && KLIST=("${KLIST[@]:0:4}")
+for K in "${KLIST[@]}"; do
   T=$(echo "$K" | tr -c 'a-zA-Z0-9' '_')
   ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:${K}" -s 2 -c 1 -o $O/r02_full_$T -f $B \
       > $O/r02_full_$T.log 2>&1
