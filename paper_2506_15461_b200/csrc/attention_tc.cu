@@ -532,16 +532,17 @@ __global__ void dsum_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bflo
 // single phase sequence.
 // Persistent backward kernels: each CTA walks pairs of units of the same (sequence, head) -- the
 // longest (index pi) then the shortest (index n-1-pi) -- so every pair has the same total length
-// (load balance without a longest-first order across heads) and the second unit re-reads the
-// operand tiles the first just pulled through L2 (the K tiles of dQ, the Q / dO tiles of dK dV)
-// instead of DRAM.  Unit ids keep the u = idx * BH + bh encoding (idx 0 = longest).
+// (load balance without a longest-first order across heads) and the units that share operand
+// tiles (the K tiles of dQ, the Q / dO tiles of dK dV) run at the same time.  Unit ids keep the u = idx * BH + bh encoding (idx 0 = longest).
 struct UnitIter {
   int s, half;
 };
 __device__ __forceinline__ bool next_unit(UnitIter& it, int n, int BH, int& u) {
   const int npairs = (n + 1) / 2;
   while (it.s < npairs * BH) {
-    const int pi = it.s / BH, bh = it.s - pi * BH;
+    // sequence x head major: the pairs of one (sequence, head) run side by side on neighbouring
+    // CTAs, so each K (dQ) / Q, dO (dK dV) tile comes from DRAM about once
+    const int bh = it.s / npairs, pi = it.s - bh * npairs;
     const int idx = it.half ? n - 1 - pi : pi;
     const bool valid = !(it.half && n - 1 - pi == pi);  // odd n: the middle unit once
     if (it.half) {
