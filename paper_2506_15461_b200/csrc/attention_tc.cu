@@ -144,6 +144,12 @@ constexpr int kBwdExp = CKF_ATTN_BWD_EXPERIMENT;
 #ifndef CKF_ATTN_BWD_STORE_EARLY
 #define CKF_ATTN_BWD_STORE_EARLY 0
 #endif
+// dK dV MMA issue: 2 = two issuer warps (warp 1: S / dP of every tile as soon as its Q / dO stage
+// and the group's S buffer allow; warp 3: the dV / dK accumulation in tile order), 1 = one warp
+// interleaving both (an S waiting on a Q / dO load then held back the dV / dK of the tile before)
+#ifndef CKF_ATTN_BWD_ISSUERS
+#define CKF_ATTN_BWD_ISSUERS 2
+#endif
 #ifndef CKF_ATTN_P_TMEM
 #define CKF_ATTN_P_TMEM 1
 #endif
@@ -601,6 +607,7 @@ __global__ void __launch_bounds__(128 + 256 * SPLIT, 1)
                         float scale, float scale_log2, const float2* __restrict__ rope, long long* __restrict__ dbg) {
   using C = BwdCfg<HD>;
   constexpr int NU = C::kNU, ST = C::kSt, NA = C::kNAcc;
+  constexpr bool kTwoIss = CKF_ATTN_BWD_ISSUERS == 2;
   // CKF_ATTN_DEBUG timings (compiled in only with -DCKF_ATTN_DEBUG_BUILD=1): [0] tiles, [1] softmax
   // wait S, [2] wait pd_free, [3] compute, [4] epilogue, [5] total, [8] MMA issue_s (+ its waits),
   // [9] acc_free wait, [10] pd_full wait -- softmax numbers from warp 4 (group 0, lane quarter 0)
@@ -635,7 +642,7 @@ __global__ void __launch_bounds__(128 + 256 * SPLIT, 1)
     }
     for (int i = 0; i < ST; ++i) {
       mbar_init(&sm.qd_full[i], 1);
-      mbar_init(&sm.qd_empty[i], 1);
+      mbar_init(&sm.qd_empty[i], kTwoIss ? 2 : 1);  // two issuers: released by both (S/dP and dV/dK)
     }
     fence_barrier_init();
   }
@@ -670,6 +677,84 @@ __global__ void __launch_bounds__(128 + 256 * SPLIT, 1)
           bulk_load(sm.lse[st], lse + qo, PT * 4, &sm.qd_full[st]);
           bulk_load(sm.dsum[st], D + qo, PT * 4, &sm.qd_full[st]);
         }
+      }
+    }
+  } else if (kTwoIss && (warp == 1 || warp == 3)) {
+    // two issuer warps (whole warp each; elect.sync issues).  Warp 1: S^T = K Q^T and dP^T = V dO^T
+    // of every tile into its group's buffer, as soon as the tile's Q / dO stage is loaded and the
+    // group's softmax has read the buffer's previous tile; it releases the K / V unit buffer.
+    // Warp 3: dV += P^T dO, dK += dS^T Q in tile order (deterministic accumulation).  A Q / dO
+    // stage is free once both have read it.
+    constexpr uint32_t kIdS = idesc_bf16_f32(TK, PT, false, false);  // [keys x 64 q], K = hd
+    constexpr uint32_t kIdA = idesc_bf16_f32(TK, HD, false, true);   // [keys x hd], K = 64 q, B MN-major
+    int g = 0, lu = 0;
+    UnitIter it_{static_cast<int>(blockIdx.x), 0};
+    if (warp == 1) {
+      for (int u = 0; next_unit(it_, nqb, BH, u); ++lu) {
+        const int ntiles = 2 * (nqb - u / BH);
+        const int kbuf = lu % NU;
+        mbar_wait(&sm.kv_full[kbuf], (lu / NU) & 1);
+        const uint32_t ka = smem_u32(sm.k[kbuf]), va = smem_u32(sm.v[kbuf]);
+        for (int i = 0; i < ntiles; ++i) {
+          const long long ti = kDbg ? clock64() : 0;
+          const int gi = g + i, st = gi % ST, bb = gi & 1;
+          mbar_wait(&sm.qd_full[st], (gi / ST) & 1);
+          mbar_wait(&sm.s_free[bb], ((gi >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t qa = smem_u32(sm.q[st]), oa = smem_u32(sm.d_o[st]);
+          const uint32_t sd = tmem + static_cast<uint32_t>(bb * 128);
+#pragma unroll
+          for (int k = 0; k < HD / 16; ++k) {
+            if constexpr (kBwdExp == 2) continue;
+            umma_bf16_w(sd, umma_desc_sw128(kmajor_k(ka, TK, k), 16, 1024),
+                        umma_desc_sw128(kmajor_k(qa, PT, k), 16, 1024), kIdS, k > 0 ? 1u : 0u);
+            umma_bf16_w(sd + 64, umma_desc_sw128(kmajor_k(va, TK, k), 16, 1024),
+                        umma_desc_sw128(kmajor_k(oa, PT, k), 16, 1024), kIdS, k > 0 ? 1u : 0u);
+          }
+          umma_commit_w(&sm.s_full[bb]);
+          umma_commit_w(&sm.qd_empty[st]);
+          if (kDbg) tw[0] += clock64() - ti;
+        }
+        umma_commit_w(&sm.kv_empty[kbuf]);
+        g += ntiles;
+      }
+    } else {
+      for (int u = 0; next_unit(it_, nqb, BH, u); ++lu) {
+        const int ntiles = 2 * (nqb - u / BH);
+        const int aset = lu % NA;
+        const uint32_t acc = tmem + 256 + static_cast<uint32_t>(aset * 2 * HD);
+        const long long ta = kDbg ? clock64() : 0;
+        mbar_wait(&sm.acc_free[aset], ((lu / NA) & 1) ^ 1);
+        if (kDbg) tw[1] += clock64() - ta;
+        for (int i = 0; i < ntiles; ++i) {
+          const int gi = g + i, st = gi % ST, bb = gi & 1;
+          const long long tp = kDbg ? clock64() : 0;
+          mbar_wait(&sm.pd_full[bb], (gi >> 1) & 1);
+          if (kDbg) tw[2] += clock64() - tp;
+          tc_fence_after();
+          const uint32_t qa = smem_u32(sm.q[st]), oa = smem_u32(sm.d_o[st]);
+          const uint32_t pa = smem_u32(sm.p[bb]), da = smem_u32(sm.ds[bb]);
+#pragma unroll
+          for (int k = 0; k < PT / 16; ++k) {  // B MN-major: HD/64 chunks of [64 q][128 B], PT*128 apart
+            if constexpr (kBwdExp == 2) continue;
+            umma_bf16_w(acc, umma_desc_sw128(pa + k * 32, 16, 1024), umma_desc_sw128(oa + k * 2048, PT * 128, 1024),
+                        kIdA, (i > 0 || k > 0) ? 1u : 0u);
+            umma_bf16_w(acc + HD, umma_desc_sw128(da + k * 32, 16, 1024),
+                        umma_desc_sw128(qa + k * 2048, PT * 128, 1024), kIdA, (i > 0 || k > 0) ? 1u : 0u);
+          }
+          umma_commit_w(&sm.pd_free[bb]);
+          umma_commit_w(&sm.qd_empty[st]);
+        }
+        umma_commit_w(&sm.acc_full[aset]);
+        g += ntiles;
+      }
+    }
+    if (kDbg && dbg && lane == 0) {
+      long long* d = dbg + 16 * blockIdx.x;
+      if (warp == 1) d[8] = tw[0];
+      if (warp == 3) {
+        d[9] = tw[1];
+        d[10] = tw[2];
       }
     }
   } else if (warp == 1) {
