@@ -119,8 +119,10 @@ __global__ void __launch_bounds__(256, (V4 <= 4 ? 2 : 1))
 #pragma unroll
   for (int i = 0; i < V4; ++i) gpw[lane + 32 * i] = make_float4(0.f, 0.f, 0.f, 0.f);
   __syncthreads();
-  const size_t r0 = static_cast<size_t>(blockIdx.x) * kBwdRowsPerBlock;
-  for (size_t r = r0 + w; r < r0 + kBwdRowsPerBlock && r < rows; r += kWarpsPerBlock) {
+  // persistent: warp w of block b takes rows b * W + w, then every gridDim.x * W rows (a fixed
+  // assignment, so each block's gain partial sums a fixed row set in a fixed order)
+  for (size_t r = static_cast<size_t>(blockIdx.x) * kWarpsPerBlock + w; r < rows;
+       r += static_cast<size_t>(gridDim.x) * kWarpsPerBlock) {
     const float rs = rstd[r];
     float4 a[V4], b[V4], o4[V4];
     float dot = 0.f;
@@ -665,7 +667,19 @@ void rmsnorm_fwd(const float* x, const float* g, size_t rows, size_t d, bf16* y,
   }
 }
 
-int rmsnorm_bwd_blocks(size_t rows) { return static_cast<int>((rows + kBwdRowsPerBlock - 1) / kBwdRowsPerBlock); }
+// Persistent grid: two 256-thread blocks per SM (one at d > 512, where the kernel's launch bounds
+// allow one), so the gain partials the fold reads are 2 x #SMs rows of d, not one per 16 rows
+// (8 MB -> 1.2 MB per launch at 32,768 x 1,024; the fold 8.6 -> ~3 us)
+int rmsnorm_bwd_blocks(size_t rows) {
+  static const int sms = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v > 0 ? v : 148;
+  }();
+  const size_t want = (rows + kBwdRowsPerBlock - 1) / kBwdRowsPerBlock;
+  return static_cast<int>(std::max<size_t>(1, std::min<size_t>(want, static_cast<size_t>(2 * sms))));
+}
 
 template <int V4>
 void rmsnorm_bwd_t(const float* dy, const float* x, const float* g, const float* rstd, size_t rows, float* dh,
