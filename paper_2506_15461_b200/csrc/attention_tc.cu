@@ -1525,11 +1525,10 @@ void bwd_launch(const bf16* qkv, const bf16* o, const float* lse, const bf16* do
     const size_t n64 = T / PT;
     const CUtensorMap tds32 = stored_ds ? tma::make_2d_bf16(dst, 64, nb * H * n64 * n64 * 64, 64, 64, 32) : tq;
     const CUtensorMap tds64 = stored_ds ? tma::make_2d_bf16(dst, 64, nb * H * n64 * n64 * 64, 64, 64, 64) : tq;
-    const int BH = static_cast<int>(nb * H), units = static_cast<int>(T / TQ) * BH;
+    const int BH = static_cast<int>(nb * H);
     // unit pairs (next_unit): one per CTA slot
     const int pairs = static_cast<int>((T / TQ + 1) / 2) * BH;
     const unsigned grid = static_cast<unsigned>(std::min(pairs, num_sms_attn()));
-    (void)units;
     kkv<<<grid, kv_threads, smem_kv, s>>>(tq, tq64, td64, tds32, stored_ds ? 1 : 0, lse_c, D_c, static_cast<int>(T),
                                           static_cast<int>(H), BH, dq_c, scale, scale * kLog2e, rtab,
                                           dbg ? dbg + 8 * 32768 : nullptr);
