@@ -206,6 +206,12 @@ int ckf_llama_swiglu_bwd(const void* gu, const void* da, size_t ntok, size_t f, 
 int ckf_llama_embed_fwd(const int* tok, size_t ntok, const float* E, size_t d, float* h, void* stream);
 int ckf_llama_embed_bwd(const int* tok, size_t ntok, const float* dh, size_t d, float* gE, void* stream);
 int ckf_gemm_qkv_rope(int M, int K, const void* A, const void* B, void* C, size_t T, size_t heads, void* stream);
+/* O-projection dgrad with the attention backward's D in its epilogue, as the LLaMA block runs it:
+ * dO = bf16(dH W^T) (dH [M x K] K-major, W [N x K] = Wo stored [K][N] read K-major, N = K = d)
+ * into C [M x N], and D[(b * H + h) * T + q] = sum over the head's columns of bf16(dO) * O for
+ * row = b * T + q, O [M x N] bf16, heads of hd = N / heads (64 or 128) columns. */
+int ckf_gemm_o_dgrad_dsum(int M, int K, const void* A, const void* B, void* C, const void* O, float* D, size_t T,
+                          size_t heads, void* stream);
 
 /* LLaMA token stream (csrc/tokens.cu): rows x (T+1) int32 ids keyed
  * (data_seed, stream, index) like the reference's batches (dataset.cpp:15-20),

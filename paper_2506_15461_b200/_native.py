@@ -104,6 +104,7 @@ def lib():
         "ckf_llama_swiglu_fwd": (i, [vp, sz, sz, vp, vp]), "ckf_llama_swiglu_bwd": (i, [vp, vp, sz, sz, vp, vp]),
         "ckf_llama_embed_fwd": (i, [vp, sz, vp, sz, vp, vp]), "ckf_llama_embed_bwd": (i, [vp, sz, vp, sz, vp, vp]),
         "ckf_gemm_qkv_rope": (i, [i, i, vp, vp, vp, sz, sz, vp]),
+        "ckf_gemm_o_dgrad_dsum": (i, [i, i, vp, vp, vp, vp, vp, sz, sz, vp]),
         "ckf_adam_device": (i, [i, vp, vp, vp, vp, vp, sz, dbl, dbl, dbl, dbl, i, vp, vp]),
         "ckf_engine_create": (i, [C.POINTER(ModelDesc), C.POINTER(eng)]), "ckf_engine_destroy": (i, [eng]),
         "ckf_engine_param_counts": (i, [eng, C.POINTER(sz), C.POINTER(sz), C.POINTER(sz)]),

@@ -1467,11 +1467,13 @@ void fwd_launch(const bf16* qkv, size_t B, size_t T, size_t H, bf16* o, float* l
 
 template <int HD>
 void bwd_launch(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, size_t B, size_t T, size_t H,
-                bf16* dqkv, float* Dsum, bool rope, cudaStream_t s) {
+                bf16* dqkv, float* Dsum, bool rope, bool d_ready, cudaStream_t s) {
   const size_t rows = B * T * H;
-  dsum_kernel<HD><<<static_cast<unsigned>((rows * (HD / 8) + 255) / 256), 256, 0, s>>>(
-      o, dout, static_cast<int>(B), static_cast<int>(T), static_cast<int>(H), Dsum);
-  CKF_LAUNCH_CHECK();
+  if (!d_ready) {
+    dsum_kernel<HD><<<static_cast<unsigned>((rows * (HD / 8) + 255) / 256), 256, 0, s>>>(
+        o, dout, static_cast<int>(B), static_cast<int>(T), static_cast<int>(H), Dsum);
+    CKF_LAUNCH_CHECK();
+  }
   // CKF_ATTN_BWD_SPLIT=1|2: softmax warps per TMEM lane quarter per group in the dK dV kernel
   // (CKF_ATTN_BWD_POLY: FMA-pipe exponential pairs of 8 in the backward -- measured no gain, so
   // only the all-MUFU kernels are built: profiles/r02_attention_bwd_poly_sweep.jsonl)
@@ -1566,12 +1568,12 @@ void attn_fwd_tc(const bf16* qkv, size_t B, size_t T, size_t H, size_t hd, bf16*
 }
 
 void attn_bwd_tc(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, size_t B, size_t T, size_t H,
-                 size_t hd, bf16* dqkv, float* Dsum, cudaStream_t s, bool rope_inverse) {
+                 size_t hd, bf16* dqkv, float* Dsum, cudaStream_t s, bool rope_inverse, bool d_ready) {
   if (!attn_fwd_tc_supported(T, hd)) raise(1, "tcgen05 attention: head_dim 64 or 128 and seq_len % 128 == 0");
   if (hd == 64)
-    bwd_launch<64>(qkv, o, lse, dout, B, T, H, dqkv, Dsum, rope_inverse, s);
+    bwd_launch<64>(qkv, o, lse, dout, B, T, H, dqkv, Dsum, rope_inverse, d_ready, s);
   else
-    bwd_launch<128>(qkv, o, lse, dout, B, T, H, dqkv, Dsum, rope_inverse, s);
+    bwd_launch<128>(qkv, o, lse, dout, B, T, H, dqkv, Dsum, rope_inverse, d_ready, s);
 }
 
 }  // namespace ckf::llama

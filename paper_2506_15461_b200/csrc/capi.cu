@@ -858,6 +858,30 @@ int ckf_llama_embed_bwd(const int* tok, size_t ntok, const float* dh, size_t d, 
     CKF_CUDA(cudaStreamSynchronize(st));
   });
 }
+int ckf_gemm_o_dgrad_dsum(int M, int K, const void* A, const void* B, void* C, const void* O, float* D, size_t T,
+                          size_t heads, void* stream) {
+  return guard([&] {
+    const int hd = heads ? K / static_cast<int>(heads) : 0;
+    if (K <= 0 || heads == 0 || K % static_cast<int>(heads) || (hd != 64 && hd != 128) || T == 0 || M % T)
+      ckf::raise(CKF_E_CONFIG, "gemm_o_dgrad_dsum: head_dim 64 or 128, M a multiple of T");
+    ckf::tc::GemmDesc g;
+    g.M = M;
+    g.N = K;
+    g.K = K;
+    g.A = static_cast<const __nv_bfloat16*>(A);
+    g.lda = K;
+    g.B = static_cast<const __nv_bfloat16*>(B);
+    g.ldb = K;
+    g.C = C;
+    g.ldc = K;
+    g.epi = ckf::tc::kStoreBF16;
+    g.dsum_o = static_cast<const __nv_bfloat16*>(O);
+    g.dsum_out = D;
+    g.dsum_T = static_cast<int>(T);
+    g.dsum_hd = hd;
+    ckf::tc::gemm_bf16(g, static_cast<cudaStream_t>(stream));
+  });
+}
 int ckf_gemm_qkv_rope(int M, int K, const void* A, const void* B, void* C, size_t T, size_t heads, void* stream) {
   return guard([&] {
     const int hd = heads ? K / static_cast<int>(heads) : 0;

@@ -129,6 +129,9 @@ struct Params {
   const __nv_bfloat16* gu; // kSwiGLUBwd: [M x 2f] gate/up activations (row pitch 2f)
   const float* row_scale;  // kStoreF32: per-row scale instead of alpha
   const int* gate;         // no work when *gate == 0
+  const __nv_bfloat16* dsum_o;  // kStoreBF16: D = rowsum(bf16(C) . O) per head (gemm_tc.h)
+  float* dsum_out;
+  int dsum_T, dsum_hd;
   XentArgs xent;           // kXentFwd
 };
 
@@ -643,6 +646,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI, NCTA), 1)
       } else {
       float rsc = p.alpha;  // kStoreF32 with a per-row scale: this lane's row
       if (EPI == kStoreF32 && p.row_scale) rsc = m0 + lane < p.M ? __ldg(p.row_scale + m0 + lane) : 0.f;
+      float dacc = 0.f;  // D epilogue: the running dot of the current head
 #pragma unroll 1
       for (int c0 = eh * (BN / EH); c0 < (eh + 1) * (BN / EH); c0 += CW) {
         uint32_t r[CW];
@@ -678,6 +682,15 @@ __global__ void __launch_bounds__(gemm_threads(EPI, NCTA), 1)
         if (lane == 0) bulk_wait_read<1>();  // the staging buffer used two stores ago is free
         __syncwarp();
         const uint32_t row = smem_u32(sb) + lane * 128;
+        // D epilogue: this row's O for the chunk's 64 columns (8 x 16 B in flight; loading them one
+        // chunk ahead measured slower: the extra live registers spill)
+        const bool dsum = EPI == kStoreBF16 && p.dsum_o != nullptr && m0 + lane < p.M;
+        uint4 ov[8];
+        if (EPI == kStoreBF16 && dsum) {
+          const uint4* op = reinterpret_cast<const uint4*>(p.dsum_o + static_cast<size_t>(m0 + lane) * p.N + w.nb * BN + c0);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) ov[j] = __ldg(op + j);
+        }
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           uint32_t a, b, c, d;
@@ -686,6 +699,14 @@ __global__ void __launch_bounds__(gemm_threads(EPI, NCTA), 1)
             b = pack_bf16(__uint_as_float(r[8 * j + 2]) * p.alpha, __uint_as_float(r[8 * j + 3]) * p.alpha);
             c = pack_bf16(__uint_as_float(r[8 * j + 4]) * p.alpha, __uint_as_float(r[8 * j + 5]) * p.alpha);
             d = pack_bf16(__uint_as_float(r[8 * j + 6]) * p.alpha, __uint_as_float(r[8 * j + 7]) * p.alpha);
+            if (dsum) {  // bf16(dO) . O in fp32, the dsum kernel's operands
+              const uint32_t dq[4] = {a, b, c, d}, oq[4] = {ov[j].x, ov[j].y, ov[j].z, ov[j].w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                dacc = fmaf(__uint_as_float(dq[e] << 16), __uint_as_float(oq[e] << 16), dacc);
+                dacc = fmaf(__uint_as_float(dq[e] & 0xffff0000u), __uint_as_float(oq[e] & 0xffff0000u), dacc);
+              }
+            }
           } else {
             a = __float_as_uint(__uint_as_float(r[4 * j + 0]) * rsc);
             b = __float_as_uint(__uint_as_float(r[4 * j + 1]) * rsc);
@@ -711,6 +732,15 @@ __global__ void __launch_bounds__(gemm_threads(EPI, NCTA), 1)
           bulk_commit();
         }
         sbuf ^= 1;
+        if (EPI == kStoreBF16 && p.dsum_o && ((w.nb * BN + c0 + CW) % p.dsum_hd) == 0) {  // head complete
+          const int mrow = m0 + lane;
+          if (mrow < p.M) {
+            const int hh = (w.nb * BN + c0 + CW) / p.dsum_hd - 1, H = p.N / p.dsum_hd;
+            const int b = mrow / p.dsum_T, q = mrow - b * p.dsum_T;
+            p.dsum_out[(static_cast<size_t>(b) * H + hh) * p.dsum_T + q] = dacc;
+          }
+          dacc = 0.f;
+        }
       }
       }  // generic epilogues
       if (EPI == kAccF32 && p.splits > 1) {  // (split-K runs only with the accumulate epilogue)
@@ -946,6 +976,13 @@ void launch_t(const GemmDesc& g, int splits, cudaStream_t s) {
   p.row_scale = g.row_scale;
   p.gate = g.gate;
   p.xent = g.xent;
+  p.dsum_o = g.dsum_o;
+  p.dsum_out = g.dsum_out;
+  p.dsum_T = g.dsum_T;
+  p.dsum_hd = g.dsum_hd;
+  if (g.dsum_o && (EPI != kStoreBF16 || !g.dsum_out || g.dsum_T <= 0 || (g.dsum_hd != 64 && g.dsum_hd != 128) ||
+                   g.N % g.dsum_hd != 0 || g.M % g.dsum_T != 0 || g.rope_tab || (BN * 4 / C::kEW) % g.dsum_hd != 0))
+    raise(1, "gemm_bf16: the D epilogue needs the bf16 store, 64/128-column heads aligned to the epilogue slices, no RoPE");
   if (EPI == kXentFwd && (!g.xent.labels || !g.xent.c || !g.xent.vmax || !g.xent.psum || !g.xent.ly || !g.xent.flag))
     raise(1, "gemm_bf16: the cross-entropy epilogue needs labels, c, vmax, psum, ly and flag");
   if (g.row_scale && EPI != kStoreF32) raise(1, "gemm_bf16: row_scale needs the fp32 store epilogue");

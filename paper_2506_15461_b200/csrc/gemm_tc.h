@@ -63,6 +63,12 @@ struct GemmDesc {
   int ldaux = 0;
   // kStoreF32: per-row output scale (C[i,:] = row_scale[i] * acc) instead of alpha
   const float* row_scale = nullptr;
+  // kStoreBF16 only: the attention backward's D = rowsum(dO . O) per (row, head) from the bf16-rounded
+  // output (C = dO of the O-projection dgrad) and dsum_o (O, [M x N], row pitch N): heads of
+  // dsum_hd (64 or 128) columns; D[(b * H + h) * T + q] for row = b * T + q, H = N / dsum_hd
+  const __nv_bfloat16* dsum_o = nullptr;
+  float* dsum_out = nullptr;
+  int dsum_T = 0, dsum_hd = 64;
   // launch gate: when non-null the kernel reads *gate after its predecessor finished and does no
   // work if it is 0 (a rerun that a device flag decides, without a host round trip)
   const int* gate = nullptr;

@@ -643,6 +643,15 @@ struct LlamaBlock final : BlockImpl {
     const char* v = std::getenv("CKF_FUSE_SWIGLU");
     return !(v && v[0] == '0');
   }
+  // the attention backward's D = rowsum(dO . O) in the O-projection dgrad's epilogue (CKF_FUSE_DSUM=0:
+  // the separate dsum kernel)
+  static bool fuse_dsum() {
+    static const bool on = [] {
+      const char* v = std::getenv("CKF_FUSE_DSUM");
+      return !(v && v[0] == '0');
+    }();
+    return on;
+  }
   const bf16* wbf(int sid, size_t li) { return eng->stage(sid).wlp + li * off.total; }
   const float* wf(int sid, size_t li) { return static_cast<const float*>(eng->stage(sid).w) + li * off.total; }
   float* gf(int sid, size_t li) { return static_cast<float*>(eng->stage(sid).g) + li * off.total; }
@@ -710,11 +719,30 @@ struct LlamaBlock final : BlockImpl {
     // attention half: h_mid = h_in + attn(rope(xn1 Wqkv)) Wo
     bf16* d_o = sbf;
     if (now) gemm(di, di, Mi, w.o, di, true, w.dho, di, true, G + off.wo, di, tc::kAccF32);   // gWo += o^T dh
-    gemm(Mi, di, di, w.dho, di, false, W + off.wo, di, false, d_o, di, tc::kStoreBF16);      // do = dh Wo^T
     const bool attn_tc = llama::attn_fwd_tc_supported(T, hd);
+    {  // do = dh Wo^T; with the tcgen05 attention its epilogue also forms D = rowsum(do . o) per head
+      tc::GemmDesc g;
+      g.M = Mi;
+      g.N = di;
+      g.K = di;
+      g.A = w.dho;
+      g.lda = di;
+      g.B = W + off.wo;
+      g.ldb = di;
+      g.C = d_o;
+      g.ldc = di;
+      g.epi = tc::kStoreBF16;
+      if (attn_tc && fuse_dsum()) {
+        g.dsum_o = w.o;
+        g.dsum_out = Dsum;
+        g.dsum_T = static_cast<int>(T);
+        g.dsum_hd = static_cast<int>(hd);
+      }
+      gemm_desc(g);
+    }
     timed(KC_ATTN, 2.5 * attn_flops_fwd(rows), Mt * d * 16.0, [&] {
       if (attn_tc)  // tcgen05 + TMEM, the RoPE backward in its dK / dQ epilogues
-        llama::attn_bwd_tc(c.qkv, w.o, c.lse, d_o, rows, T, H, hd, w.dqkv, Dsum, st, true);
+        llama::attn_bwd_tc(c.qkv, w.o, c.lse, d_o, rows, T, H, hd, w.dqkv, Dsum, st, true, fuse_dsum());
       else
         llama::attn_bwd(c.qkv, w.o, c.lse, d_o, rows, T, H, hd, w.dqkv, Dsum, st);
     });

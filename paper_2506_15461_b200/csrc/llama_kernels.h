@@ -95,8 +95,9 @@ bool attn_fwd_tc_supported(size_t T, size_t hd);
 long long* attn_fwd_debug_buffer();  // non-null only with CKF_ATTN_DEBUG=1
 void attn_fwd_tc(const bf16* qkv, size_t B, size_t T, size_t H, size_t hd, bf16* o, float* lse, cudaStream_t s);
 // rope_inverse: dq / dk leave with the RoPE backward applied (fused into the dK and dQ epilogues)
+// d_ready: Dsum already holds D = rowsum(dout . o) (the O-projection dgrad's epilogue formed it)
 void attn_bwd_tc(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, size_t B, size_t T, size_t H,
-                 size_t hd, bf16* dqkv, float* Dsum, cudaStream_t s, bool rope_inverse = false);
+                 size_t hd, bf16* dqkv, float* Dsum, cudaStream_t s, bool rope_inverse = false, bool d_ready = false);
 // dqkv [B*T x 3*H*hd]; Dsum scratch [B*H*T] fp32.  Deterministic (no atomics).
 void attn_bwd(const bf16* qkv, const bf16* o, const float* lse, const bf16* dout, size_t B, size_t T, size_t H,
               size_t hd, bf16* dqkv, float* Dsum, cudaStream_t s);

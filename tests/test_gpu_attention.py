@@ -146,3 +146,29 @@ def test_backward_with_fused_rope_inverse(shape):
         c = two.float()[:, blk * d:(blk + 1) * d]
         assert ((a - b).norm() / b.norm()).item() < 3e-2, blk
         assert ((a - c).norm() / c.norm()).item() < 1e-2, blk
+
+
+@pytest.mark.parametrize("M,d,hd,T", [(2048, 1024, 64, 1024), (1024, 512, 64, 256), (4096, 2048, 128, 4096),
+                                       (512, 256, 128, 256)])
+def test_o_dgrad_gemm_with_fused_dsum(M, d, hd, T):
+    """The O-projection dgrad's epilogue forms the attention backward's D = rowsum(bf16(dO) . O) per
+    head: dO within one bf16 rounding of fp32 torch, D against torch's sum over the same bf16
+    operands (fp32 summation-order differences only: 1e-4 relative to the row's |dO| |O|)."""
+    from paper_2506_15461_b200._native import check, lib
+    g = torch.Generator(device="cuda").manual_seed(M + d)
+    A = torch.randn(M, d, generator=g, device="cuda").bfloat16()
+    W = (torch.randn(d, d, generator=g, device="cuda") / d ** 0.5).bfloat16()  # Wo stored [K][N]
+    O = torch.randn(M, d, generator=g, device="cuda").bfloat16()
+    C = torch.empty(M, d, dtype=torch.bfloat16, device="cuda")
+    H = d // hd
+    D = torch.full((M // T * H * T,), float("nan"), device="cuda")
+    check(lib().ckf_gemm_o_dgrad_dsum(M, d, A.data_ptr(), W.data_ptr(), C.data_ptr(), O.data_ptr(), D.data_ptr(),
+                                      T, H, None))
+    torch.cuda.synchronize()
+    want = A.float() @ W.float().t()
+    assert float((C.float() - want).norm() / want.norm()) < 4e-3
+    prod = (C.float() * O.float()).view(M // T, T, H, hd)
+    Dw = prod.sum(-1).permute(0, 2, 1).reshape(-1)
+    scale = (C.float().abs() * O.float().abs()).view(M // T, T, H, hd).sum(-1).permute(0, 2, 1).reshape(-1)
+    assert torch.isfinite(D).all()
+    assert float(((D - Dw).abs() / scale.clamp_min(1e-6)).max()) < 1e-4
