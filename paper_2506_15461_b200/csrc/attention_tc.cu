@@ -165,7 +165,11 @@ struct FwdCfg {
   // NG = 1: 104 KiB vs 144 KiB of shared memory; two hd-128 CTAs per SM with 2 K / 1 V stages (112 KiB)
   // measured 1.7x slower (1697 -> 2887 us at [16, 4096, 16, 128]): the single V stage serialises
   static constexpr int kMinBlocks = HD == 64 && NG == 1 ? 2 : 1;
-  static constexpr int kThreads = 128 + 128 * NG;
+  // one query tile: 6 warps -- producer + TMEM allocator (0), MMA issuer (1), softmax (2..5, TMEM lane
+  // quarter = warp % 4) -- so two CTAs per SM get 170 registers per thread instead of 128 (no spills);
+  // two tiles: producer (0), issuers (1, 3), allocator (2), softmax (4..11)
+  static constexpr int kThreads = NG == 1 ? 192 : 128 + 128 * NG;
+  static constexpr int kSoftWarp0 = NG == 1 ? 2 : 4, kAllocWarp = NG == 1 ? 0 : 2;
   // TMEM: group g's S pair at columns g*128 + {0, 64}, its O at NG*128 + g*HD
   static constexpr int kTmemCols = NG * 128 + NG * HD <= 256 ? 256 : 512;
   // S_{j+2} issued two tiles ahead (into the buffer the softmax has just loaded) when a third V
@@ -241,7 +245,7 @@ __global__ void __launch_bounds__(FwdCfg<HD, NG>::kThreads, FwdCfg<HD, NG>::kMin
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<C::kTmemCols>(&sm.tmem);
+  if (warp == C::kAllocWarp) tmem_alloc<C::kTmemCols>(&sm.tmem);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -321,9 +325,9 @@ __global__ void __launch_bounds__(FwdCfg<HD, NG>::kThreads, FwdCfg<HD, NG>::kMin
       }
       umma_commit_w(&sm.o_full[g]);
     }
-  } else if (warp >= 4) {
+  } else if (warp >= C::kSoftWarp0) {
     // ---------------- softmax: one query row per thread, online with lazy rescaling
-    const int g = (warp - 4) >> 2, wq = (warp - 4) & 3;  // group, TMEM lane quarter (= warp % 4)
+    const int g = (warp - C::kSoftWarp0) >> 2, wq = warp & 3;  // group, TMEM lane quarter (= warp % 4)
     const int r = wq * 32 + lane;
     const int qb = qb0 + g;
     const int q = qb * TQ + r;
@@ -475,7 +479,7 @@ __global__ void __launch_bounds__(FwdCfg<HD, NG>::kThreads, FwdCfg<HD, NG>::kMin
       }
     }
     lse[static_cast<size_t>(bh) * T + q] = (m + log2f(l)) * kLn2;
-    if (kDbg && dbg && threadIdx.x == 128) {
+    if (kDbg && dbg && threadIdx.x == C::kSoftWarp0 * 32) {
       long long* d = dbg + 8 * (blockIdx.y * gridDim.x + blockIdx.x);
       d[0] = nkb;
       d[1] = t_first;
@@ -491,7 +495,7 @@ __global__ void __launch_bounds__(FwdCfg<HD, NG>::kThreads, FwdCfg<HD, NG>::kMin
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 2) tmem_free<C::kTmemCols>(tmem);
+  if (warp == C::kAllocWarp) tmem_free<C::kTmemCols>(tmem);
 }
 
 // ---------------------------------------------------------------- backward

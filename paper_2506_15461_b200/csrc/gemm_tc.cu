@@ -104,7 +104,7 @@ constexpr int BM = 128, BK = 64, UK = 16;
 // CTA-pair bf16-output epilogue (measured: LM head forward +8 % vs cuBLAS-relative, others
 // neutral); 4 elsewhere, where the extra staging would cost an operand stage.
 __host__ __device__ constexpr int epi_warps(int epi, int ncta) {
-  return (epi == kStoreBF16 || epi == kXentFwd) && ncta == 2 ? 8 : 4;
+  return (epi == kStoreBF16 || epi == kBF16Dsum || epi == kXentFwd) && ncta == 2 ? 8 : 4;
 }
 __host__ __device__ constexpr int gemm_threads(int epi, int ncta) { return 128 + 32 * epi_warps(epi, ncta); }
 constexpr uint32_t kAStage = BM * BK * 2;  // 16 KiB
@@ -684,23 +684,24 @@ __global__ void __launch_bounds__(gemm_threads(EPI, NCTA), 1)
         const uint32_t row = smem_u32(sb) + lane * 128;
         // D epilogue: this row's O for the chunk's 64 columns (8 x 16 B in flight; loading them one
         // chunk ahead measured slower: the extra live registers spill)
-        const bool dsum = EPI == kStoreBF16 && p.dsum_o != nullptr && m0 + lane < p.M;
-        uint4 ov[8];
-        if (EPI == kStoreBF16 && dsum) {
+        const bool dsum = EPI == kBF16Dsum && m0 + lane < p.M;
+        uint4 ov[EPI == kBF16Dsum ? 8 : 1];
+        if (EPI == kBF16Dsum && dsum) {
           const uint4* op = reinterpret_cast<const uint4*>(p.dsum_o + static_cast<size_t>(m0 + lane) * p.N + w.nb * BN + c0);
 #pragma unroll
-          for (int j = 0; j < 8; ++j) ov[j] = __ldg(op + j);
+          for (int j = 0; j < (EPI == kBF16Dsum ? 8 : 1); ++j) ov[j] = __ldg(op + j);
         }
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           uint32_t a, b, c, d;
-          if constexpr (EPI == kStoreBF16) {
+          if constexpr (EPI == kStoreBF16 || EPI == kBF16Dsum) {
             a = pack_bf16(__uint_as_float(r[8 * j + 0]) * p.alpha, __uint_as_float(r[8 * j + 1]) * p.alpha);
             b = pack_bf16(__uint_as_float(r[8 * j + 2]) * p.alpha, __uint_as_float(r[8 * j + 3]) * p.alpha);
             c = pack_bf16(__uint_as_float(r[8 * j + 4]) * p.alpha, __uint_as_float(r[8 * j + 5]) * p.alpha);
             d = pack_bf16(__uint_as_float(r[8 * j + 6]) * p.alpha, __uint_as_float(r[8 * j + 7]) * p.alpha);
-            if (dsum) {  // bf16(dO) . O in fp32, the dsum kernel's operands
-              const uint32_t dq[4] = {a, b, c, d}, oq[4] = {ov[j].x, ov[j].y, ov[j].z, ov[j].w};
+            if (EPI == kBF16Dsum && dsum) {  // bf16(dO) . O in fp32, the dsum kernel's operands
+              const uint4 o4 = ov[EPI == kBF16Dsum ? j : 0];
+              const uint32_t dq[4] = {a, b, c, d}, oq[4] = {o4.x, o4.y, o4.z, o4.w};
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
                 dacc = fmaf(__uint_as_float(dq[e] << 16), __uint_as_float(oq[e] << 16), dacc);
@@ -732,7 +733,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI, NCTA), 1)
           bulk_commit();
         }
         sbuf ^= 1;
-        if (EPI == kStoreBF16 && p.dsum_o && ((w.nb * BN + c0 + CW) % p.dsum_hd) == 0) {  // head complete
+        if (EPI == kBF16Dsum && ((w.nb * BN + c0 + CW) % p.dsum_hd) == 0) {  // head complete
           const int mrow = m0 + lane;
           if (mrow < p.M) {
             const int hh = (w.nb * BN + c0 + CW) / p.dsum_hd - 1, H = p.N / p.dsum_hd;
@@ -941,7 +942,7 @@ void launch_t(const GemmDesc& g, int splits, cudaStream_t s) {
                               : tma::make_2d_bf16(g.A, g.K, g.M, g.lda, 64, BM);
   const CUtensorMap tb = B_MN ? tma::make_2d_bf16(g.B, g.N, g.K, g.ldb, 64, 64)
                               : tma::make_2d_bf16(g.B, g.K, g.N, g.ldb, 64, BN / NCTA);
-  const bool c_bf16 = EPI == kStoreBF16 || EPI == kSwiGLU || EPI == kSwiGLUBwd || EPI == kXentFwd;
+  const bool c_bf16 = EPI == kStoreBF16 || EPI == kBF16Dsum || EPI == kSwiGLU || EPI == kSwiGLUBwd || EPI == kXentFwd;
   // kSwiGLUBwd: C = dgu [M x 2f] although the GEMM's N is f
   const CUtensorMap tcm = c_bf16 ? tma::make_2d_bf16(g.C, EPI == kSwiGLUBwd ? 2 * g.N : g.N, g.M, g.ldc, 64, 32)
                                  : tma::make_2d_f32(g.C, g.N, g.M, g.ldc, 32, 32);
@@ -980,7 +981,7 @@ void launch_t(const GemmDesc& g, int splits, cudaStream_t s) {
   p.dsum_out = g.dsum_out;
   p.dsum_T = g.dsum_T;
   p.dsum_hd = g.dsum_hd;
-  if (g.dsum_o && (EPI != kStoreBF16 || !g.dsum_out || g.dsum_T <= 0 || (g.dsum_hd != 64 && g.dsum_hd != 128) ||
+  if (EPI == kBF16Dsum && (!g.dsum_o || !g.dsum_out || g.dsum_T <= 0 || (g.dsum_hd != 64 && g.dsum_hd != 128) ||
                    g.N % g.dsum_hd != 0 || g.M % g.dsum_T != 0 || g.rope_tab || (BN * 4 / C::kEW) % g.dsum_hd != 0))
     raise(1, "gemm_bf16: the D epilogue needs the bf16 store, 64/128-column heads aligned to the epilogue slices, no RoPE");
   if (EPI == kXentFwd && (!g.xent.labels || !g.xent.c || !g.xent.vmax || !g.xent.psum || !g.xent.ly || !g.xent.flag))
@@ -1041,6 +1042,7 @@ void dispatch_bn(const GemmDesc& g, int splits, cudaStream_t s) {
   CKF_GEMM_EPIS(true, true)
   CKF_GEMM_CASE(false, true, kSwiGLU)
   CKF_GEMM_CASE(false, false, kSwiGLUBwd)
+  CKF_GEMM_CASE(false, false, kBF16Dsum)
   if constexpr (BN == 256 && NCTA == 2) {  // the partial-sum layout assumes 256-wide pair tiles, 8 warps
     CKF_GEMM_CASE(false, true, kXentFwd)
   }
@@ -1061,11 +1063,16 @@ int pick_bn(int M, int N) {
   return cost(128) < cost(256) ? 128 : 256;
 }
 
-void gemm_bf16(const GemmDesc& g, cudaStream_t s) {
-  if (g.M <= 0 || g.N <= 0 || g.K <= 0) return;
+void gemm_bf16(const GemmDesc& g0, cudaStream_t s) {
+  if (g0.M <= 0 || g0.N <= 0 || g0.K <= 0) return;
+  GemmDesc g = g0;
+  if (g.dsum_o) {  // the D epilogue is its own instantiation (bf16 store + D)
+    if (g.epi != kStoreBF16) raise(1, "gemm_bf16: dsum_o needs the bf16 store epilogue");
+    g.epi = kBF16Dsum;
+  }
   if (g.ldc % 4 != 0 && (g.epi == kStoreF32 || g.epi == kAccF32)) raise(1, "gemm_bf16: fp32 C needs ldc % 4 == 0");
   if (reinterpret_cast<uintptr_t>(g.C) % 16) raise(1, "gemm_bf16: C must be 16-byte aligned");
-  if (g.ldc % 8 != 0 && (g.epi == kStoreBF16 || g.epi == kSwiGLU || g.epi == kSwiGLUBwd))
+  if (g.ldc % 8 != 0 && (g.epi == kStoreBF16 || g.epi == kBF16Dsum || g.epi == kSwiGLU || g.epi == kSwiGLUBwd))
     raise(1, "gemm_bf16: bf16 C needs ldc % 8 == 0");
   if (g.epi == kXentFwd) {
     if (g.a_mn || !g.b_mn || g.splits > 1) raise(1, "gemm_bf16: the cross-entropy epilogue needs A K-major, B MN-major");

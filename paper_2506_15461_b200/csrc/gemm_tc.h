@@ -20,7 +20,9 @@ namespace ckf::tc {
 //   xent.psum[(nb * 2 + half) * M + i], the fp32 logit of the label column to xent.ly[i], and
 //   -- when a logit exceeds c_i + kXentGuard -- raises xent.flag and atomically maxes the
 //   row's logit into xent.vmax (ordered-int encoding) so a gated rerun can use the true max.
-enum Epi { kStoreBF16 = 0, kStoreF32 = 1, kAccF32 = 2, kSwiGLU = 3, kSwiGLUBwd = 4, kXentFwd = 5 };
+// kBF16Dsum: kStoreBF16 plus the attention backward's D (dsum_* below); selected internally when
+// dsum_o is set, a separate instantiation so the other bf16-store GEMMs keep their registers
+enum Epi { kStoreBF16 = 0, kStoreF32 = 1, kAccF32 = 2, kSwiGLU = 3, kSwiGLUBwd = 4, kXentFwd = 5, kBF16Dsum = 6 };
 constexpr float kXentGuard = 50.f;
 // number of per-row partial sums kXentFwd writes for a vocabulary of V columns
 inline int xent_partials(int V) { return 2 * ((V + 255) / 256); }
