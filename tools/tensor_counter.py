@@ -28,7 +28,9 @@ SHAPES = [  # (name, M, N, K, a_mn, b_mn, epi)
     ("down_wgrad", f, d, T_, 1, 1, 2),
     ("lmhead_fwd", T_, V, d, 0, 1, 0), ("lmhead_dgrad", T_, d, V, 0, 0, 1), ("lmhead_wgrad", d, V, T_, 1, 1, 2),
 ]
-ATTN = [(64, 1024, 16, 64), (16, 4096, 16, 128)]
+# attention shapes whose dS^T scratch fits one backward pass (bwd = dsum + dK/dV + dQ: 3 launches):
+# one 500M class half-step (32 sequences of 1,024) and two 4,096-token sequences at head_dim 128
+ATTN = [(32, 1024, 16, 64), (2, 4096, 16, 128)]
 
 
 def gemm_call(M, N, K, a_mn, b_mn, epi):
