@@ -49,6 +49,17 @@ for (B, T, H, hd) in [(2, 256, 2, 64), (1, 256, 2, 128)]:
     check(L.ckf_attention_fwd(qkv.data_ptr(), B, T, H, hd, o.data_ptr(), lse.data_ptr(), 2, None))
     check(L.ckf_attention_bwd(qkv.data_ptr(), o.data_ptr(), lse.data_ptr(), dout.data_ptr(), B, T, H, hd,
                               dqkv.data_ptr(), D.data_ptr(), 0, None))
+    # the RoPE backward fused into the dK / dQ epilogues (CKF_ATTN_ROPE_BWD)
+    check(L.ckf_attention_bwd(qkv.data_ptr(), o.data_ptr(), lse.data_ptr(), dout.data_ptr(), B, T, H, hd,
+                              dqkv.data_ptr(), D.data_ptr(), 2 | 16, None))
+    # the O-projection dgrad with the attention backward's D in its epilogue, and the QKV GEMM with RoPE
+    d_ = H * hd
+    W = torch.randn(d_, d_, device=dev).bfloat16()
+    dO = torch.empty(B * T, d_, device=dev, dtype=torch.bfloat16)
+    check(L.ckf_gemm_o_dgrad_dsum(B * T, d_, dout.data_ptr(), W.data_ptr(), dO.data_ptr(), o.data_ptr(), D.data_ptr(),
+                                  T, H, None))
+    Wq = torch.randn(d_, 3 * d_, device=dev).bfloat16()
+    check(L.ckf_gemm_qkv_rope(B * T, d_, o.data_ptr(), Wq.data_ptr(), qkv.data_ptr(), T, H, None))
     torch.cuda.synchronize()
     print("attention", (B, T, H, hd), flush=True)
 
