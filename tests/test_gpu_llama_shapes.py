@@ -2,14 +2,17 @@
 the CPU fp64 oracle (oracle/llama_oracle.py): one microbatch forward + backward
 through the C-ABI, two stages of one layer each, every kernel on its benched
 path -- tcgen05 attention (T % 128 == 0; head_dim 64 and 128), RMSNorm V4 = 4 /
-8 / 16 (d = 512 / 1024 / 2048), fused RoPE (head_dim 64) or the RoPE kernel
-(head_dim 128), fused SwiGLU epilogues, the LM head at V = 50,304 -- and, at the
+8 / 16 (d = 512 / 1024 / 2048), RoPE fused into the QKV GEMM and the attention backward's
+epilogues (head_dim 64 and 128), D in the O-projection dgrad's epilogue, fused SwiGLU
+epilogues, the LM head at V = 50,304 -- and, at the
 124M shape, one fused run_iteration (deferred W pass, microbatch fusion) whose
 loss, omegas and Adam update are compared with the oracle's iteration.
 
 Bars (bf16 operands, fp32 accumulation; measured on the B200 (profiles/r02_parity_errors.jsonl,
 DESIGN.md §5) and set at ~2x the largest measured value): loss 2e-5 relative (measured
-<= 7.8e-6); per-group gradient 1.5e-2 relative Frobenius (measured 0.66-0.89 %); omega 3e-3
+<= 7.8e-6; 1.2e-5 at the 1.5B shape with the end-of-round kernels,
+profiles/r02_parity_errors_v7.jsonl); per-group gradient 1.5e-2 relative Frobenius (measured
+0.66-0.90 %); omega 3e-3
 (measured <= 1.1e-3); Adam's first update: sign disagreement on <= 1 % of the clearly moved
 entries (measured 0.34 %).
 The fp32 parity mode (llama_f32.cu) is held to 1e-5 (loss) / 1e-4 (gradients) at
