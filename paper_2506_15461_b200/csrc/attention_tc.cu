@@ -12,7 +12,10 @@
 // Backward (dK dV kernel + dQ kernel, deterministic, no atomics): persistent over
 // (tile, head) units longest-first, two inner tiles in flight (ping-pong softmax groups).
 //
-// Warp roles: 0 TMA producer, 1 MMA issuer (one lane), 2 TMEM allocator, 4.. softmax.
+// Warp roles: forward (one query tile) 0 TMA producer + TMEM allocator, 1 MMA issuer, 2..5 softmax;
+// forward (two query tiles) 0 producer, 1 / 3 MMA issuers, 2 allocator, 4..11 softmax; dK dV 0
+// producer, 1 S / dP issuer, 2 allocator, 3 dV / dK issuer, 4..11 softmax.  MMA issuers run
+// warp-converged with elect.sync (sm100.cuh umma_*_w).
 #include <algorithm>
 #include <cstdlib>
 #include <string>

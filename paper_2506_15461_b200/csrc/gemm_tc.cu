@@ -11,8 +11,9 @@
 //   wgrad    dW += X^T dY  A=X MN-major,  B=dY MN-major     (epilogue += fp32)
 //
 // Persistent, warp-specialised (one CTA per SM):
-//   warp 0      TMA producer (one elected lane), kStages-deep smem ring
-//   warp 1      MMA issuer (one lane): 128 x BN x 16 tcgen05.mma, commits
+//   warp 0      TMA producer, kStages-deep smem ring (warp-converged, elect.sync issues; one lane
+//               for the weight gradients)
+//   warp 1      MMA issuer (warp-converged, elect.sync issues): 128 x BN x 16 tcgen05.mma, commits
 //   warp 2      TMEM allocator (2 x BN fp32 columns: double-buffered accumulators)
 //   warps 4..7  epilogue: tcgen05.ld 32 lanes x 32 columns, fused store /
 //               fp32 accumulate, so tile i's epilogue overlaps tile i+1's MMAs.
