@@ -139,14 +139,6 @@ constexpr bool kDbg = CKF_ATTN_DEBUG_BUILD != 0;
 #define CKF_ATTN_BWD_EXPERIMENT 0
 #endif
 constexpr int kBwdExp = CKF_ATTN_BWD_EXPERIMENT;
-// dK dV softmax store order: 0 = compute all 64 queries, wait for the group's P / dS buffers, store;
-// 1 = wait first, store every 8-query group as computed; 2 = wait after the first half.  The
-// register-only micro-benchmark (tools/ubench/softmax_bwd_ubench.cu) favours 1 (2479 -> 1863 cycles
-// per tile and warp), but in the kernel the earlier buffer wait costs more: [64, 1024, 16, 64] bwd
-// 1002 (0) / 1014 (1) / 1000 (2) us, same-box A/B -- 0 kept
-#ifndef CKF_ATTN_BWD_STORE_EARLY
-#define CKF_ATTN_BWD_STORE_EARLY 0
-#endif
 // dK dV MMA issue: 2 = two issuer warps (warp 1: S / dP of every tile as soon as its Q / dO stage
 // and the group's S buffer allow; warp 3: the dV / dK accumulation in tile order), 1 = one warp
 // interleaving both (an S waiting on a Q / dO load then held back the dV / dK of the tile before)
@@ -915,35 +907,8 @@ __global__ void __launch_bounds__(128 + 256 * SPLIT, 1)
         uint32_t pkp[QW / 2], pkd[QW / 2];
         const uint32_t rowoff = static_cast<uint32_t>(r * 128);
         const uint32_t la_ = smem_u32(&sm.lse[st][0]), da_ = smem_u32(&sm.dsum[st][0]);
-        // 1: wait first, store each group as computed; 2: compute the first half, wait, store it, then
-        // compute and store the second half group by group
-        constexpr int kSEm = CKF_ATTN_BWD_STORE_EARLY;
-        constexpr bool kSE = kSEm != 0;
-        long long t2 = 0, t3 = 0;
-        auto wait_buffers = [&] {
-          t2 = kDbg ? clock64() : 0;
-          mbar_wait(&sm.pd_free[grp], ((gi >> 1) & 1) ^ 1);  // this group's previous dV/dK MMAs read P / dS
-          if (store_ds) {  // ... and the previous dS^T store has left this warp's slab
-            if (lane == 0) bulk_wait_read<0>();
-            __syncwarp();
-          }
-          t3 = kDbg ? clock64() : 0;
-        };
-        if constexpr (kSEm == 1) wait_buffers();
 #pragma unroll
-        for (int lg = 0; lg < QW / 8; ++lg) {  // 8 queries at a time: P^T, dS^T -> bf16 -> swizzled smem
-          if constexpr (kSEm == 2) {
-            if (lg == QW / 16) {  // first half computed: wait for the buffers, store it
-              wait_buffers();
-#pragma unroll
-              for (int l2 = 0; l2 < QW / 16; ++l2) {
-                const int h8 = half * (QW / 8) + l2;
-                const uint32_t off = rowoff + ((h8 ^ (r & 7)) << 4);
-                st_shared_v4(pbase + off, pkp[4 * l2], pkp[4 * l2 + 1], pkp[4 * l2 + 2], pkp[4 * l2 + 3]);
-                st_shared_v4(dbase + off, pkd[4 * l2], pkd[4 * l2 + 1], pkd[4 * l2 + 2], pkd[4 * l2 + 3]);
-              }
-            }
-          }
+        for (int lg = 0; lg < QW / 8; ++lg) {  // 8 queries at a time: P^T, dS^T -> bf16 -> packed registers
           if constexpr (kBwdExp == 1) {
 #pragma unroll
             for (int e = 0; e < 4; ++e) pkp[4 * lg + e] = pkd[4 * lg + e] = us[8 * lg + e] ^ ud[8 * lg + e];
@@ -987,28 +952,28 @@ __global__ void __launch_bounds__(128 + 256 * SPLIT, 1)
             pkp[4 * lg + e] = pack_bf16(pv[2 * e], pv[2 * e + 1]);
             pkd[4 * lg + e] = pack_bf16(dv[2 * e], dv[2 * e + 1]);
           }
-          if (kSEm == 1 || (kSEm == 2 && lg >= QW / 16)) {
-            const uint32_t off = rowoff + ((g8 ^ (r & 7)) << 4);
-            st_shared_v4(pbase + off, pkp[4 * lg], pkp[4 * lg + 1], pkp[4 * lg + 2], pkp[4 * lg + 3]);
-            st_shared_v4(dbase + off, pkd[4 * lg], pkd[4 * lg + 1], pkd[4 * lg + 2], pkd[4 * lg + 3]);
-          }
         }
-        if constexpr (!kSE) {
-          wait_buffers();
+        // then the wait for this group's previous dV / dK MMAs (they read P / dS) and the previous dS^T
+        // store (it reads this warp's slab), then the stores (storing each 8-query group as computed,
+        // after an earlier wait, measured slower in the kernel: DESIGN.md §4.2)
+        const long long t2 = kDbg ? clock64() : 0;
+        mbar_wait(&sm.pd_free[grp], ((gi >> 1) & 1) ^ 1);
+        if (store_ds) {
+          if (lane == 0) bulk_wait_read<0>();
+          __syncwarp();
+        }
+        const long long t3 = kDbg ? clock64() : 0;
 #pragma unroll
-          for (int lg = 0; lg < QW / 8; ++lg) {
-            const int g8 = half * (QW / 8) + lg;
-            const uint32_t off = rowoff + ((g8 ^ (r & 7)) << 4);
-            st_shared_v4(pbase + off, pkp[4 * lg], pkp[4 * lg + 1], pkp[4 * lg + 2], pkp[4 * lg + 3]);
-            st_shared_v4(dbase + off, pkd[4 * lg], pkd[4 * lg + 1], pkd[4 * lg + 2], pkd[4 * lg + 3]);
-          }
+        for (int lg = 0; lg < QW / 8; ++lg) {
+          const int g8 = half * (QW / 8) + lg;
+          const uint32_t off = rowoff + ((g8 ^ (r & 7)) << 4);
+          st_shared_v4(pbase + off, pkp[4 * lg], pkp[4 * lg + 1], pkp[4 * lg + 2], pkp[4 * lg + 3]);
+          st_shared_v4(dbase + off, pkd[4 * lg], pkd[4 * lg + 1], pkd[4 * lg + 2], pkd[4 * lg + 3]);
         }
         if (kDbg) {
           tw[2] += t3 - t2;
-          tw[3] += kSE ? clock64() - t3 : t2 - t1;
-          if (kSE) tw[3] += t2 - t1;
+          tw[3] += t2 - t1;
         }
-        const long long t5 = kDbg ? clock64() : 0;
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) {
@@ -1021,8 +986,7 @@ __global__ void __launch_bounds__(128 + 256 * SPLIT, 1)
             bulk_commit();
           }
         }
-        if (kDbg) tw[6] += clock64() - (kSE ? t5 : t3);  // store phase (P / dS to smem unless early, fence,
-                                                         // arrive, dS^T TMA store)
+        if (kDbg) tw[6] += clock64() - t3;  // store phase (P / dS to smem, fence, arrive, dS^T TMA store)
         if (i == grp && pend_u >= 0) {
           const long long t4 = kDbg ? clock64() : 0;
           epilogue(pend_u, pend_lu);
