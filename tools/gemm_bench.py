@@ -22,6 +22,8 @@ SHAPES = [  # (name, M, N, K, a_mn, b_mn, epi): one fused LLaMA-124M step (65,53
     # LLaMA-500M (one CheckFree+ group of 32,768 tokens)
     ("down_dgrad_500m", 32768, 4096, 1024, 0, 0, 0), ("down_dgrad_swiglu_500m", 32768, 4096, 1024, 0, 0, 4),
     ("gu_fwd_swiglu_500m", 32768, 8192, 1024, 0, 1, 3), ("o_fwd_500m", 32768, 1024, 1024, 0, 1, 2),
+    ("qkv_fwd_500m", 32768, 3072, 1024, 0, 1, 0), ("down_fwd_500m", 32768, 1024, 4096, 0, 1, 2),
+    ("gu_dgrad_500m", 32768, 1024, 8192, 0, 0, 1), ("qkv_dgrad_500m", 32768, 1024, 3072, 0, 0, 1),
 ]
 
 def run(name, M, N, K, a_mn, b_mn, epi, bn=0, iters=20):
