@@ -102,10 +102,15 @@ using namespace ckf::sm100;
 
 constexpr int BM = 128, BK = 64, UK = 16;
 // Epilogue warps: 8 (two per TMEM lane quarter, each on half of the tile's columns) for the
-// CTA-pair bf16-output epilogue (measured: LM head forward +8 % vs cuBLAS-relative, others
-// neutral); 4 elsewhere, where the extra staging would cost an operand stage.
+// CTA-pair LM head + loss epilogue; 4 elsewhere -- the plain bf16 store included
+// (CKF_GEMM_BF16_EW8=1 gives it 8): its 32 KiB less staging buys a sixth operand stage, which the
+// MMA warp's full-stage waits needed (QKV forward 144.5 -> 140.8 us, O dgrad 52.4 -> 50.9 us at
+// the 500M shapes, same-box A/B; tools/gemm_debug.py)
+#ifndef CKF_GEMM_BF16_EW8
+#define CKF_GEMM_BF16_EW8 0
+#endif
 __host__ __device__ constexpr int epi_warps(int epi, int ncta) {
-  return (epi == kStoreBF16 || epi == kBF16Dsum || epi == kXentFwd) && ncta == 2 ? 8 : 4;
+  return ((CKF_GEMM_BF16_EW8 && (epi == kStoreBF16 || epi == kBF16Dsum)) || epi == kXentFwd) && ncta == 2 ? 8 : 4;
 }
 __host__ __device__ constexpr int gemm_threads(int epi, int ncta) { return 128 + 32 * epi_warps(epi, ncta); }
 constexpr uint32_t kAStage = BM * BK * 2;  // 16 KiB
