@@ -106,6 +106,11 @@ constexpr int BM = 128, BK = 64, UK = 16;
 // (CKF_GEMM_BF16_EW8=1 gives it 8): its 32 KiB less staging buys a sixth operand stage, which the
 // MMA warp's full-stage waits needed (QKV forward 144.5 -> 140.8 us, O dgrad 52.4 -> 50.9 us at
 // the 500M shapes, same-box A/B; tools/gemm_debug.py)
+// kSwiGLUBwd: g/u chunks in flight per epilogue warp (each a 2 x 4 KiB buffer pair); one ahead
+// frees a fifth operand stage but measured slower (296.0 -> 301.4 us at [32,768 x 4,096 x 1,024])
+#ifndef CKF_SWB_AHEAD
+#define CKF_SWB_AHEAD 2
+#endif
 #ifndef CKF_GEMM_BF16_EW8
 #define CKF_GEMM_BF16_EW8 0
 #endif
@@ -161,7 +166,7 @@ struct Cfg {
   // the dg/du staging pair).
   // NCTA = 2 (CTA pair): each CTA holds BN/2 columns of B, so a stage is 32 KiB at BN = 256.
   static constexpr int kEW = epi_warps(EPI, NCTA);
-  static constexpr int kEpiBufs = EPI == kSwiGLUBwd ? 6 : 2;
+  static constexpr int kEpiBufs = EPI == kSwiGLUBwd ? 2 * CKF_SWB_AHEAD + 2 : 2;
   static constexpr uint32_t kBStage = (BN / NCTA) * BK * 2;
   static constexpr uint32_t kStageBytes = kAStage + kBStage;
   static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
@@ -417,10 +422,11 @@ __global__ void __launch_bounds__(gemm_threads(EPI, NCTA), 1)
     auto row0_of = [&](const Unit& wu) { return wu.mb * BM * NCTA + static_cast<int>(rank) * BM + q * 32; };
     int cc = 0;               // kSwiGLUBwd: chunk counter of this warp's stream
     // kSwiGLUBwd (lane 0): chunk k of this warp's stream = (unit uu, 64-column chunk c) -> pair k & 1
+    constexpr int kSWA = CKF_SWB_AHEAD;
     auto swb_prefetch = [&](int k, int uu, int c) {
       const Unit w2 = unit_of(p, uu);
-      uint8_t* gb = stg + (k & 1) * 2 * kStageBufBytes;
-      uint64_t* bar = &lbar[q * 2 + (k & 1)];
+      uint8_t* gb = stg + (k % kSWA) * 2 * kStageBufBytes;
+      uint64_t* bar = &lbar[q * 2 + (k % kSWA)];
       const int n0 = w2.nb * BN + c * 64, y = row0_of(w2);
       mbar_arrive_expect_tx(bar, 2 * kStageBufBytes);
       tma_load_2d(gb, &tmap_ws, bar, n0, y);
@@ -430,9 +436,8 @@ __global__ void __launch_bounds__(gemm_threads(EPI, NCTA), 1)
     for (int u = u0; u < units; u += ustep) {
       const Unit w = unit_of(p, u);
       if constexpr (EPI == kSwiGLUBwd) {
-        if (first_unit && lane == 0) {  // the first two g/u chunks in flight before the accumulator is ready
-          swb_prefetch(0, u, 0);
-          swb_prefetch(1, u, 1);
+        if (first_unit && lane == 0) {  // the first g/u chunks in flight before the accumulator is ready
+          for (int k = 0; k < kSWA; ++k) swb_prefetch(k, u, k);
         }
         first_unit = false;
       }
@@ -549,7 +554,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI, NCTA), 1)
         // straight from registers (no staging) 369 us.
         constexpr int NCH = BN / 64;
         static_assert(NCH >= 2, "kSwiGLUBwd: two chunks per tile at least");
-        uint8_t* ob = stg + 4 * kStageBufBytes;  // dg / du staging pair
+        uint8_t* ob = stg + 2 * kSWA * kStageBufBytes;  // dg / du staging pair
 #pragma unroll 1
         for (int c = 0; c < NCH; ++c, ++cc) {
           const int n0 = w.nb * BN + c * 64;
@@ -562,8 +567,8 @@ __global__ void __launch_bounds__(gemm_threads(EPI, NCTA), 1)
             __syncwarp();
             if (lane == 0) release_acc(acc);
           }
-          mbar_wait(&lbar[q * 2 + (cc & 1)], (cc >> 1) & 1);
-          uint8_t* gb = stg + (cc & 1) * 2 * kStageBufBytes;
+          mbar_wait(&lbar[q * 2 + (cc % kSWA)], (cc / kSWA) & 1);
+          uint8_t* gb = stg + (cc % kSWA) * 2 * kStageBufBytes;
           const uint32_t ga = smem_u32(gb) + lane * 128, ua = ga + kStageBufBytes;
           uint4 gq[8], uq[8];
 #pragma unroll
@@ -573,12 +578,12 @@ __global__ void __launch_bounds__(gemm_threads(EPI, NCTA), 1)
             uq[j] = ld_shared_v4(ua + off);
           }
           __syncwarp();
-          if (lane == 0) {  // refill this pair with chunk cc + 2 (generic reads ordered before the async write)
-            const int c2 = c + 2 < NCH ? c + 2 : c + 2 - NCH;
-            const int u2 = c + 2 < NCH ? u : u + ustep;
+          if (lane == 0) {  // refill this pair with chunk cc + kSWA (generic reads ordered before the async write)
+            const int c2 = c + kSWA < NCH ? c + kSWA : c + kSWA - NCH;
+            const int u2 = c + kSWA < NCH ? u : u + ustep;
             if (u2 < units) {
               fence_proxy_async();
-              swb_prefetch(cc + 2, u2, c2);
+              swb_prefetch(cc + kSWA, u2, c2);
             }
           }
           uint32_t pg[32], pu[32];
