@@ -567,6 +567,15 @@ __device__ __forceinline__ bool next_unit(UnitIter& it, int n, int BH, int& u) {
 constexpr int PT = 64;                 // inner tile: queries (dK/dV kernel) or keys (dQ kernel)
 constexpr uint32_t kPB = TQ * PT * 2;  // 16 KiB: P^T / dS^T [128 rows][64 cols] bf16, one SW128 chunk
 
+// Stored dS^T, causal tiles only: key block j (64 keys) keeps query blocks t = 2 (j / 2) .. n64 - 1
+// (from its 128-key unit's diagonal on), rows of one sequence x head in key-block order:
+//   tile(bh, j, t) = bh * ds_tiles(n64) + ds_row(n64, j) + t - 2 (j / 2)
+__host__ __device__ __forceinline__ int ds_row(int n64, int j) {
+  const int p = j >> 1;
+  return 2 * p * (n64 - p + 1) + (j & 1) * (n64 - 2 * p);
+}
+__host__ __device__ __forceinline__ int ds_tiles(int n64) { return n64 * n64 / 2 + n64; }
+
 template <int HD>
 struct BwdCfg {
   static constexpr uint32_t kUnit = TK * HD * 2;   // 128-row unit operand tile
@@ -980,9 +989,9 @@ __global__ void __launch_bounds__(128 + 256 * SPLIT, 1)
           mbar_arrive(&sm.pd_full[grp]);
           if (store_ds) {  // this warp's 32 key rows of dS^T -> its [64 keys x 64 queries] tile for the dQ GEMM
             const int kb = u / BH, bh = u - kb * BH, n64 = T / PT;
-            const int j = kb * 2 + (quarter >> 1), t = kb * 2 + i;  // 64-key block, 64-query block
+            const int j = kb * 2 + (quarter >> 1);  // 64-key block; 64-query block t = 2 kb + i
             tma_store_2d(&tm_dst, reinterpret_cast<const uint8_t*>(sm.ds[grp]) + quarter * 32 * 128, 0,
-                         ((bh * n64 + j) * n64 + t) * PT + (quarter & 1) * 32);
+                         (bh * ds_tiles(n64) + ds_row(n64, j) + i) * PT + (quarter & 1) * 32);
             bulk_commit();
           }
         }
@@ -1318,7 +1327,8 @@ __global__ void __launch_bounds__(256, 1)
           const int st = g % ST;
           mbar_wait(&sm.empty[st], ((g / ST) & 1) ^ 1);
           mbar_arrive_expect_tx(&sm.full[st], 2 * 8192 + PT * HD * 2);
-          const int n64 = T / PT, tile = (bh * n64 + j) * n64 + 2 * qb;  // dS^T tiles (j, 2qb) and (j, 2qb + 1)
+          // dS^T tiles (j, 2qb) and (j, 2qb + 1), adjacent in the causal layout (2qb >= 2 (j / 2))
+          const int n64 = T / PT, tile = bh * ds_tiles(n64) + ds_row(n64, j) + 2 * qb - 2 * (j >> 1);
           tma_load_2d(sm.a[st], &tm_dst, &sm.full[st], 0, tile * PT);
           tma_load_2d(sm.a[st] + 8192, &tm_dst, &sm.full[st], 0, (tile + 1) * PT);
           tma_tile<HD>(sm.b[st], &tm_qkv64, &sm.full[st], (H + h) * HD, b * T + j * PT, PT);
@@ -1373,7 +1383,8 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 2) tmem_free<2 * HD>(tmem);
 }
 
-// dS^T scratch for the stored-dS backward: B*H*T*T bf16 per launch chunk (grown on demand)
+// dS^T scratch for the stored-dS backward: B H ds_tiles(T / 64) 64 x 64 bf16 tiles per launch chunk
+// (grown on demand)
 bf16* dst_buffer(size_t elems) {
   static bf16* buf = nullptr;
   static size_t cap = 0;
@@ -1476,10 +1487,17 @@ void bwd_launch(const bf16* qkv, const bf16* o, const float* lse, const bf16* do
   // the RoPE backward of dq / dk in the dK and dQ-GEMM epilogues (otherwise a separate pass below)
   const bool rope_fused = rope && split < 2 && stored_ds;
   const float2* rtab = rope_fused ? rope_table_pair_major(T, HD, s) : nullptr;
-  // sequences per pass: the dS^T scratch (B_c H T^2 bf16) stays within ~1.1 GB
-  const size_t per_seq = H * T * T * sizeof(bf16);
-  const size_t bc = stored_ds ? std::max<size_t>(1, std::min<size_t>(B, 1100000000ull / per_seq)) : B;
-  bf16* dst = stored_ds ? dst_buffer(bc * H * T * T) : nullptr;
+  // sequences per pass: the dS^T scratch (B_c H ds_tiles tiles) stays within ~2.5 GB -- each pass
+  // pays a partial last wave in both kernels, so few passes (profiles/r02_attention_ds_chunk_sweep.jsonl:
+  // hd 128 at [16, 4096, 16, 128] 3,970 us in 8 passes, 3,462 in 2, 3,494 in 1)
+  const size_t tiles_seq = H * static_cast<size_t>(ds_tiles(static_cast<int>(T / PT)));
+  const size_t per_seq = tiles_seq * PT * PT * sizeof(bf16);
+  static const size_t ds_bytes = [] {  // CKF_ATTN_DS_BYTES: the dS^T scratch budget per pass
+    const char* v = std::getenv("CKF_ATTN_DS_BYTES");
+    return v ? static_cast<size_t>(std::atoll(v)) : static_cast<size_t>(2500000000ull);
+  }();
+  const size_t bc = stored_ds ? std::max<size_t>(1, std::min<size_t>(B, ds_bytes / per_seq)) : B;
+  bf16* dst = stored_ds ? dst_buffer(bc * tiles_seq * PT * PT) : nullptr;
   const size_t ld = 3 * H * HD;
   for (size_t b0 = 0; b0 < B; b0 += bc) {
     const size_t nb = std::min(bc, B - b0);
@@ -1492,12 +1510,12 @@ void bwd_launch(const bf16* qkv, const bf16* o, const float* lse, const bf16* do
     const CUtensorMap tq64 = tma::make_2d_bf16(q_c, ld, nb * T, ld, 64, 64);
     const CUtensorMap td = tma::make_2d_bf16(do_c, H * HD, nb * T, H * HD, 64, 128);
     const CUtensorMap td64 = tma::make_2d_bf16(do_c, H * HD, nb * T, H * HD, 64, 64);
-    // dS^T as contiguous [64 keys][64 queries] tiles (8 KiB each; tile (bh, key block j, query block t)
-    // at row ((bh n64 + j) n64 + t) 64 of a [* x 64] matrix): 32-row slabs stored by the dK dV warps,
-    // whole tiles loaded by dQ -- every transfer is one contiguous run of DRAM
-    const size_t n64 = T / PT;
-    const CUtensorMap tds32 = stored_ds ? tma::make_2d_bf16(dst, 64, nb * H * n64 * n64 * 64, 64, 64, 32) : tq;
-    const CUtensorMap tds64 = stored_ds ? tma::make_2d_bf16(dst, 64, nb * H * n64 * n64 * 64, 64, 64, 64) : tq;
+    // dS^T as contiguous [64 keys][64 queries] tiles (8 KiB each; causal tiles only, tile (bh, key
+    // block j, query block t) at row 64 ds_tile(...) of a [* x 64] matrix, ds_row above): 32-row slabs
+    // stored by the dK dV warps, whole tiles loaded by dQ -- every transfer is one contiguous run of DRAM
+    const size_t ds_rows = nb * tiles_seq * PT;
+    const CUtensorMap tds32 = stored_ds ? tma::make_2d_bf16(dst, 64, ds_rows, 64, 64, 32) : tq;
+    const CUtensorMap tds64 = stored_ds ? tma::make_2d_bf16(dst, 64, ds_rows, 64, 64, 64) : tq;
     const int BH = static_cast<int>(nb * H);
     // unit pairs (next_unit): one per CTA slot
     const int pairs = static_cast<int>((T / TQ + 1) / 2) * BH;
