@@ -172,3 +172,48 @@ def test_o_dgrad_gemm_with_fused_dsum(M, d, hd, T):
     scale = (C.float().abs() * O.float().abs()).view(M // T, T, H, hd).sum(-1).permute(0, 2, 1).reshape(-1)
     assert torch.isfinite(D).all()
     assert float(((D - Dw).abs() / scale.clamp_min(1e-6)).max()) < 1e-4
+
+
+_CHUNK_SCRIPT = r"""
+import sys, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2506_15461_b200  # noqa: F401
+from paper_2506_15461_b200._native import check, lib
+B, T, H, hd = (int(v) for v in sys.argv[2:6])
+torch.manual_seed(5)
+qkv = (torch.randn(B * T, 3 * H * hd, device="cuda") * 0.8).bfloat16()
+o = torch.empty(B * T, H * hd, dtype=torch.bfloat16, device="cuda")
+lse = torch.empty(B * H * T, device="cuda")
+check(lib().ckf_attention_fwd(qkv.data_ptr(), B, T, H, hd, o.data_ptr(), lse.data_ptr(), 2, None))
+dout = torch.randn(B * T, H * hd, device="cuda").bfloat16()
+dqkv = torch.zeros(B * T, 3 * H * hd, dtype=torch.bfloat16, device="cuda")
+D = torch.empty(B * H * T, device="cuda")
+check(lib().ckf_attention_bwd(qkv.data_ptr(), o.data_ptr(), lse.data_ptr(), dout.data_ptr(), B, T, H, hd,
+                              dqkv.data_ptr(), D.data_ptr(), 0, None))
+torch.cuda.synchronize()
+torch.save(dqkv.cpu(), sys.argv[6])
+"""
+
+
+@pytest.mark.parametrize("shape", [(3, 512, 2, 64), (3, 512, 2, 128)])
+def test_backward_one_pass_per_sequence_is_bit_identical(shape, tmp_path):
+    """The stored-dS backward runs in passes of as many sequences as the causal dS^T scratch
+    budget holds (CKF_ATTN_DS_BYTES, read once per process).  A budget below one sequence forces a
+    pass per sequence; each sequence's arithmetic is the same either way, so dq / dk / dv must be
+    bit-identical to the single-pass run."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for budget in (None, "1"):
+        env = dict(os.environ)
+        env.pop("CKF_ATTN_DS_BYTES", None)
+        if budget:
+            env["CKF_ATTN_DS_BYTES"] = budget
+        path = str(tmp_path / f"dqkv_{budget}.pt")
+        subprocess.run([sys.executable, "-c", _CHUNK_SCRIPT, root, *map(str, shape), path], env=env, check=True,
+                       timeout=600)
+        outs.append(torch.load(path))
+    assert torch.equal(outs[0], outs[1])
+    assert outs[0].float().abs().sum().item() > 0
