@@ -185,7 +185,11 @@ struct Smem {
   uint64_t q_full;
   uint64_t k_full[C::kKSt], k_empty[C::kKSt], v_full[C::kVSt], v_empty[C::kVSt];
   uint64_t s_full[NG][2], s_free[NG][2], p_full[NG][2], p_free[NG][2];
-  uint64_t o_full[NG];
+  uint64_t o_full[NG], o_free[NG];
+  // persistent CTAs: the unit ring (written by the producer, read by the issuers and softmax warps)
+  // and the Q buffer's release by the unit's last S MMAs
+  uint64_t unit_full[2], unit_empty[2], q_empty;
+  int unit[2];
   uint32_t tmem;
 };
 
@@ -197,7 +201,7 @@ template <int HD, int POLY, int NG>
 __global__ void __launch_bounds__(FwdCfg<HD, NG>::kThreads, FwdCfg<HD, NG>::kMinBlocks)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_kv,
                        int T, int H, __nv_bfloat16* __restrict__ o, float* __restrict__ lse, float scale_log2,
-                       long long* __restrict__ dbg) {
+                       int BH, int* __restrict__ ctr, long long* __restrict__ dbg) {
   using C = FwdCfg<HD, NG>;
   constexpr int KS = C::kKSt, VS = C::kVSt;
   extern __shared__ uint8_t smem_raw[];
@@ -206,12 +210,25 @@ __global__ void __launch_bounds__(FwdCfg<HD, NG>::kThreads, FwdCfg<HD, NG>::kMin
       *reinterpret_cast<Smem<HD, NG>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = T / TQ;
-  // heavy (late) query tiles first; NG = 2: tiles qb0 = 2c and 2c + 1
-  const int qb0 = NG * (nqb / NG - 1 - static_cast<int>(blockIdx.x));
-  const int bh = blockIdx.y, b = bh / H, h = bh % H;
-  const int nkb_last = 2 * (qb0 + NG - 1) + 2;  // causal: 64-key tiles of the last query tile
-  const int row0 = b * T;
-  const int qcol = h * HD, kcol = (H + h) * HD, vcol = (2 * H + h) * HD;
+  // Work unit u = (sequence x head bh, query tile pair c): bh = u / nqu, heavy (late) query tiles
+  // first within a sequence x head; NG = 2: tiles qb0 = 2c and 2c + 1.  ctr == nullptr: one unit
+  // per CTA, u = (blockIdx.y, blockIdx.x).  Otherwise the CTAs are persistent and take units in
+  // that same order from the counter (the CTA that draws the last past-the-end ticket resets it
+  // for the next launch): each CTA loads the next unit's Q while its softmax finishes the current
+  // one and keeps its TMEM allocation, instead of paying a CTA start per 128 queries.
+  const int nqu = nqb / NG, nunits = nqu * BH;
+  struct UnitPos {
+    int qb0, bh, row0, h;
+  };
+  auto unit_pos = [&](int u) {
+    UnitPos w;
+    w.bh = u / nqu;
+    w.qb0 = NG * (nqu - 1 - (u - w.bh * nqu));
+    const int b = w.bh / H;
+    w.h = w.bh - b * H;
+    w.row0 = b * T;
+    return w;
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm_qkv);
@@ -219,8 +236,8 @@ __global__ void __launch_bounds__(FwdCfg<HD, NG>::kThreads, FwdCfg<HD, NG>::kMin
   }
   if (warp == 1 && lane == 0) {
     mbar_init(&sm.q_full, 1);
-    // a K / V stage is released by every group's issuer (the last query tile's two extra key
-    // tiles are released by one issuer only: the producer never waits on those again)
+    // a K / V stage is released by every group's issuer (group 0 releases the last query tile's
+    // two extra key tiles without reading them)
     for (int i = 0; i < KS; ++i) {
       mbar_init(&sm.k_full[i], 1);
       mbar_init(&sm.k_empty[i], NG);
@@ -237,7 +254,13 @@ __global__ void __launch_bounds__(FwdCfg<HD, NG>::kThreads, FwdCfg<HD, NG>::kMin
         mbar_init(&sm.p_free[g][i], 1);
       }
       mbar_init(&sm.o_full[g], 1);
+      mbar_init(&sm.o_free[g], 4);
     }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm.unit_full[i], 1);
+      mbar_init(&sm.unit_empty[i], 5 * NG);  // every issuer and softmax warp
+    }
+    mbar_init(&sm.q_empty, NG);
     fence_barrier_init();
   }
   if (warp == C::kAllocWarp) tmem_alloc<C::kTmemCols>(&sm.tmem);
@@ -248,18 +271,40 @@ __global__ void __launch_bounds__(FwdCfg<HD, NG>::kThreads, FwdCfg<HD, NG>::kMin
 
   if (warp == 0) {
     if (lane == 0) {
-      // ---------------- TMA producer: the Q tiles once, then K_j and V_j (each exactly once)
-      mbar_arrive_expect_tx(&sm.q_full, NG * C::kQ);
+      // ---------------- TMA producer: per unit the Q tiles once (after the previous unit's last S
+      // MMAs), then K_j and V_j (each exactly once); jj counts K / V tiles over the CTA's units
+      int jj = 0;
+      for (int k = 0;; ++k) {
+        int u = -1;
+        if (ctr) {
+          const int t = atomicAdd(ctr, 1);
+          if (t < nunits)
+            u = t;
+          else if (t == nunits + static_cast<int>(gridDim.x) - 1)
+            atomicExch(ctr, 0);  // every CTA has drawn its last ticket: reset for the next launch
+        } else if (k == 0) {
+          u = static_cast<int>(blockIdx.y) * nqu + static_cast<int>(blockIdx.x);
+        }
+        mbar_wait(&sm.unit_empty[k & 1], ((k >> 1) & 1) ^ 1);
+        sm.unit[k & 1] = u;
+        mbar_arrive(&sm.unit_full[k & 1]);
+        if (u < 0) break;
+        const UnitPos w = unit_pos(u);
+        const int nkb_last = 2 * (w.qb0 + NG - 1) + 2;  // causal: 64-key tiles of the last query tile
+        const int qcol = w.h * HD, kcol = (H + w.h) * HD, vcol = (2 * H + w.h) * HD;
+        mbar_wait(&sm.q_empty, (k & 1) ^ 1);
+        mbar_arrive_expect_tx(&sm.q_full, NG * C::kQ);
 #pragma unroll
-      for (int g = 0; g < NG; ++g) tma_tile<HD>(sm.q[g], &tm_qkv, &sm.q_full, qcol, row0 + (qb0 + g) * TQ, TQ);
-      for (int j = 0; j < nkb_last; ++j) {
-        const int ks = j % KS, vs = j % VS;
-        mbar_wait(&sm.k_empty[ks], ((j / KS) & 1) ^ 1);
-        mbar_arrive_expect_tx(&sm.k_full[ks], C::kK);
-        tma_tile<HD>(sm.k[ks], &tm_kv, &sm.k_full[ks], kcol, row0 + j * FK, FK);
-        mbar_wait(&sm.v_empty[vs], ((j / VS) & 1) ^ 1);
-        mbar_arrive_expect_tx(&sm.v_full[vs], C::kK);
-        tma_tile<HD>(sm.v[vs], &tm_kv, &sm.v_full[vs], vcol, row0 + j * FK, FK);
+        for (int g = 0; g < NG; ++g) tma_tile<HD>(sm.q[g], &tm_qkv, &sm.q_full, qcol, w.row0 + (w.qb0 + g) * TQ, TQ);
+        for (int j = 0; j < nkb_last; ++j, ++jj) {
+          const int ks = jj % KS, vs = jj % VS;
+          mbar_wait(&sm.k_empty[ks], ((jj / KS) & 1) ^ 1);
+          mbar_arrive_expect_tx(&sm.k_full[ks], C::kK);
+          tma_tile<HD>(sm.k[ks], &tm_kv, &sm.k_full[ks], kcol, w.row0 + j * FK, FK);
+          mbar_wait(&sm.v_empty[vs], ((jj / VS) & 1) ^ 1);
+          mbar_arrive_expect_tx(&sm.v_full[vs], C::kK);
+          tma_tile<HD>(sm.v[vs], &tm_kv, &sm.v_full[vs], vcol, w.row0 + j * FK, FK);
+        }
       }
     }
   } else if (warp == 1 || (NG == 2 && warp == 3)) {
@@ -269,15 +314,25 @@ __global__ void __launch_bounds__(FwdCfg<HD, NG>::kThreads, FwdCfg<HD, NG>::kMin
       // so one group's softmax overlaps the other's MMAs as two CTAs per SM would.
       // S_{j+1} (or S_{j+2}) is issued before P_j is awaited.
       const int g = warp == 1 ? 0 : 1;
-      const int nkb = 2 * (qb0 + g) + 2;
       constexpr uint32_t kIdS = idesc_bf16_f32(TQ, FK, false, false);  // S = Q K^T  (128 x 64)
       constexpr uint32_t kIdO = idesc_bf16_f32(TQ, HD, false, true);   // O += P V   (V MN-major)
-      mbar_wait(&sm.q_full, 0);
       const uint32_t qa = smem_u32(sm.q[g]);
+      // jj0: the producer's K / V tile count at this unit's start; tg: this group's tile count
+      // (S / P buffers and their phases run on over the CTA's units)
+      int jj0 = 0, tg = 0;
+      for (int un = 0;; ++un) {
+      mbar_wait(&sm.unit_full[un & 1], (un >> 1) & 1);
+      const int u = sm.unit[un & 1];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.unit_empty[un & 1]);
+      if (u < 0) break;
+      const int qb0 = unit_pos(u).qb0;
+      const int nkb = 2 * (qb0 + g) + 2, nkb_last = 2 * (qb0 + NG - 1) + 2;
+      mbar_wait(&sm.q_full, un & 1);
       auto issue_s = [&](int j) {
-        const int ks = j % KS, sb = j & 1;
-        mbar_wait(&sm.k_full[ks], (j / KS) & 1);
-        mbar_wait(&sm.s_free[g][sb], ((j >> 1) & 1) ^ 1);
+        const int ks = (jj0 + j) % KS, sb = (tg + j) & 1;
+        mbar_wait(&sm.k_full[ks], ((jj0 + j) / KS) & 1);
+        mbar_wait(&sm.s_free[g][sb], (((tg + j) >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t ka = smem_u32(sm.k[ks]);
 #pragma unroll
@@ -286,6 +341,7 @@ __global__ void __launch_bounds__(FwdCfg<HD, NG>::kThreads, FwdCfg<HD, NG>::kMin
                     umma_desc_sw128(kmajor_k(ka, FK, k), 16, 1024), kIdS, k > 0 ? 1u : 0u);
         umma_commit_w(&sm.s_full[g][sb]);
         umma_commit_w(&sm.k_empty[ks]);
+        if (j == nkb - 1) umma_commit_w(&sm.q_empty);  // the unit's last S: its Q buffer may be refilled
       };
       // S runs two tiles ahead of the softmax when a third V stage allows it: S_{j+2} goes into
       // S_j's TMEM buffer as soon as the softmax warps have loaded S_j (early in their tile j),
@@ -298,16 +354,18 @@ __global__ void __launch_bounds__(FwdCfg<HD, NG>::kThreads, FwdCfg<HD, NG>::kMin
       for (int j = 0; j < nkb; ++j) {
         if (kEarly && j + 2 < nkb) issue_s(j + 2);
         if (!kEarly && j + 1 < nkb) issue_s(j + 1);
-        const int pb = j & 1, vs = j % VS;
-        mbar_wait(&sm.v_full[vs], (j / VS) & 1);
-        mbar_wait(&sm.p_full[g][pb], (j >> 1) & 1);
+        const int pb = (tg + j) & 1, vs = (jj0 + j) % VS;
+        mbar_wait(&sm.v_full[vs], ((jj0 + j) / VS) & 1);
+        mbar_wait(&sm.p_full[g][pb], ((tg + j) >> 1) & 1);
+        // the first P V of a unit overwrites O: the softmax warps have read the previous unit's O
+        if (j == 0 && un > 0) mbar_wait(&sm.o_free[g], (un - 1) & 1);
         tc_fence_after();
         const uint32_t va = smem_u32(sm.v[vs]);
         if constexpr (C::kPTmem) {
 #pragma unroll
           for (int k = 0; k < FK / 16; ++k)  // P from TMEM: 8 packed columns per 16 keys
             umma_bf16_ts_w(tmem + 128, tmem + 192 + pb * 32 + k * 8, umma_desc_sw128(va + k * 2048, FK * 128, 1024),
-                           kIdO, (j > 0 || k > 0) ? 1u : 0u);
+                           kIdO, (j > 0 || k > 0) ? 1u : 0u);  // k: the MMA's K step
         } else {
           const uint32_t pa = smem_u32(sm.p[g][pb]);
 #pragma unroll
@@ -319,25 +377,44 @@ __global__ void __launch_bounds__(FwdCfg<HD, NG>::kThreads, FwdCfg<HD, NG>::kMin
         umma_commit_w(&sm.v_empty[vs]);
       }
       umma_commit_w(&sm.o_full[g]);
+      // NG = 2: the second tile's two extra K / V tiles are released by group 0 too (once loaded,
+      // so the arrival counts toward that use of the stage), or the next unit's loads would wait
+      for (int j = nkb; j < nkb_last; ++j) {
+        const int ks = (jj0 + j) % KS, vs = (jj0 + j) % VS;
+        mbar_wait(&sm.k_full[ks], ((jj0 + j) / KS) & 1);
+        umma_commit_w(&sm.k_empty[ks]);
+        mbar_wait(&sm.v_full[vs], ((jj0 + j) / VS) & 1);
+        umma_commit_w(&sm.v_empty[vs]);
+      }
+      jj0 += nkb_last;
+      tg += nkb;
+      }
     }
   } else if (warp >= C::kSoftWarp0) {
     // ---------------- softmax: one query row per thread, online with lazy rescaling
     const int g = (warp - C::kSoftWarp0) >> 2, wq = warp & 3;  // group, TMEM lane quarter (= warp % 4)
     const int r = wq * 32 + lane;
-    const int qb = qb0 + g;
-    const int q = qb * TQ + r;
-    const int nkb = 2 * qb + 2;
     const uint32_t trow = tmem + (static_cast<uint32_t>(wq * 32) << 16);
     const uint32_t tS = trow + g * 128, tO = trow + NG * 128 + g * HD;
-    float m = -INFINITY, l = 0.f;  // m: running max of S * scale_log2
     long long w_s = 0, w_p = 0, t_first = 0;
+    int tg = 0, nkb = 0;  // tg: this group's tile count over the CTA's units (S / P buffer phases)
+    for (int un = 0;; ++un) {
+    mbar_wait(&sm.unit_full[un & 1], (un >> 1) & 1);
+    const int u = sm.unit[un & 1];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.unit_empty[un & 1]);
+    if (u < 0) break;
+    const UnitPos w = unit_pos(u);
+    const int qb = w.qb0 + g, q = qb * TQ + r, row0 = w.row0, h = w.h, bh = w.bh;
+    nkb = 2 * qb + 2;
+    float m = -INFINITY, l = 0.f;  // m: running max of S * scale_log2
     for (int j = 0; j < nkb; ++j) {
-      const int sb = j & 1, pb = j & 1;
+      const int jt = tg + j, sb = jt & 1, pb = jt & 1;
       const long long t0 = (kDbg && dbg) ? clock64() : 0;
-      mbar_wait(&sm.s_full[g][sb], (j >> 1) & 1);
+      mbar_wait(&sm.s_full[g][sb], (jt >> 1) & 1);
       if (kDbg && dbg) {  // CKF_ATTN_DEBUG timings only
         const long long t1 = clock64();
-        if (j == 0) t_first = t1 - t_start;
+        if (j == 0 && un == 0) t_first = t1 - t_start;
         w_s += t1 - t0;
       }
       tc_fence_after();
@@ -394,7 +471,7 @@ __global__ void __launch_bounds__(FwdCfg<HD, NG>::kThreads, FwdCfg<HD, NG>::kMin
         return lt;
       };
       const long long t2 = (kDbg && dbg) ? clock64() : 0;
-      mbar_wait(&sm.p_free[g][pb], ((j >> 1) & 1) ^ 1);  // P V_{j-2} has read this P buffer
+      mbar_wait(&sm.p_free[g][pb], ((jt >> 1) & 1) ^ 1);  // P V_{j-2} has read this P buffer
       if (kDbg && dbg) w_p += clock64() - t2;
       // Fast path (every tile after the first): P against the running max m with no max pass;
       // kept when the tile's row sum stays <= 2^16 (so every P <= 2^16, finite).  Otherwise --
@@ -426,7 +503,7 @@ __global__ void __launch_bounds__(FwdCfg<HD, NG>::kThreads, FwdCfg<HD, NG>::kMin
         const float alpha = need ? ex2(m - mn) : 1.f;  // m = -inf on the first tile -> 0
         if (__any_sync(0xffffffffu, need) && j > 0) {
           // the previous P V must have landed before this warp rewrites its O rows
-          mbar_wait(&sm.p_free[g][(j - 1) & 1], ((j - 1) >> 1) & 1);
+          mbar_wait(&sm.p_free[g][(jt - 1) & 1], ((jt - 1) >> 1) & 1);
           tc_fence_after();
 #pragma unroll
           for (int hf = 0; hf < HD / 32; ++hf) {
@@ -452,8 +529,8 @@ __global__ void __launch_bounds__(FwdCfg<HD, NG>::kThreads, FwdCfg<HD, NG>::kMin
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.p_full[g][pb]);
     }
-    // ---------------- epilogue: O / l -> bf16, lse
-    mbar_wait(&sm.o_full[g], 0);
+    // ---------------- epilogue: O / l -> bf16, lse; then O is free for the next unit's P V
+    mbar_wait(&sm.o_full[g], un & 1);
     tc_fence_after();
     const float inv = 1.f / l;
     const size_t ldo = static_cast<size_t>(H) * HD;
@@ -474,7 +551,12 @@ __global__ void __launch_bounds__(FwdCfg<HD, NG>::kThreads, FwdCfg<HD, NG>::kMin
       }
     }
     lse[static_cast<size_t>(bh) * T + q] = (m + log2f(l)) * kLn2;
-    if (kDbg && dbg && threadIdx.x == C::kSoftWarp0 * 32) {
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.o_free[g]);
+    tg += nkb;
+    }
+    if (kDbg && dbg && !ctr && threadIdx.x == C::kSoftWarp0 * 32) {
       long long* d = dbg + 8 * (blockIdx.y * gridDim.x + blockIdx.x);
       d[0] = nkb;
       d[1] = t_first;
@@ -1407,6 +1489,20 @@ int num_sms_attn() {
   return sms;
 }
 
+// the persistent forward's unit counter (zero between launches: the kernel resets it), per device
+int* attn_fwd_counter() {
+  static int* ctr[64] = {};
+  int dev = 0;
+  CKF_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) raise(1, "attention: device index out of range");
+  if (!ctr[dev]) {
+    CKF_CUDA(cudaMalloc(&ctr[dev], sizeof(int)));
+    CKF_CUDA(cudaMemset(ctr[dev], 0, sizeof(int)));
+    ++alloc_epoch();
+  }
+  return ctr[dev];
+}
+
 template <int HD, int NG>
 void fwd_launch_ng(const bf16* qkv, size_t B, size_t T, size_t H, bf16* o, float* lse, int poly, cudaStream_t s) {
   const CUtensorMap tm = tma::make_2d_bf16(qkv, 3 * H * HD, B * T, 3 * H * HD, 64, 128);
@@ -1423,10 +1519,19 @@ void fwd_launch_ng(const bf16* qkv, size_t B, size_t T, size_t H, bf16* o, float
     attr[pi] = true;
   }
   const float scale_log2 = kLog2e / sqrtf(static_cast<float>(HD));
-  dim3 grid(static_cast<unsigned>(T / (TQ * NG)), static_cast<unsigned>(B * H));
+  const int nqu = static_cast<int>(T / (TQ * NG)), BH = static_cast<int>(B * H);
+  // persistent CTAs; CKF_ATTN_FWD_PERSIST=0: one CTA per unit
+  static const bool persist_env = [] {
+    const char* v = std::getenv("CKF_ATTN_FWD_PERSIST");
+    return !(v && v[0] == '0');
+  }();
   long long* dbg = attn_fwd_debug_buffer();
+  int* ctr = persist_env && !dbg ? attn_fwd_counter() : nullptr;
+  const int units = nqu * BH;
+  const dim3 grid = ctr ? dim3(static_cast<unsigned>(std::min(units, FwdCfg<HD, NG>::kMinBlocks * num_sms_attn())))
+                        : dim3(static_cast<unsigned>(nqu), static_cast<unsigned>(BH));
   kern<<<grid, FwdCfg<HD, NG>::kThreads, smem, s>>>(tm, tkv, static_cast<int>(T), static_cast<int>(H), o, lse,
-                                                   scale_log2, dbg);
+                                                   scale_log2, BH, ctr, dbg);
   CKF_LAUNCH_CHECK();
 }
 

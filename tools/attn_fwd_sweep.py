@@ -18,7 +18,7 @@ def bench(fn, it=20):
     return a.elapsed_time(b) / it
 
 
-shapes = [(64, 1024, 16, 64), (16, 4096, 16, 128), (32, 2048, 16, 128)]
+shapes = [(64, 1024, 16, 64), (32, 1024, 16, 64), (64, 1024, 8, 64), (16, 4096, 16, 128), (32, 2048, 16, 128)]
 for (B, T, H, hd) in shapes:
     qkv = torch.randn(B * T, 3 * H * hd, device="cuda").bfloat16()
     o = torch.empty(B * T, H * hd, dtype=torch.bfloat16, device="cuda")
