@@ -217,3 +217,43 @@ def test_backward_one_pass_per_sequence_is_bit_identical(shape, tmp_path):
         outs.append(torch.load(path))
     assert torch.equal(outs[0], outs[1])
     assert outs[0].float().abs().sum().item() > 0
+
+
+_FWD_SCRIPT = r"""
+import sys, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2506_15461_b200  # noqa: F401
+from paper_2506_15461_b200._native import check, lib
+outs = []
+for (B, T, H, hd) in [(1, 128, 1, 64), (3, 1024, 5, 64), (2, 512, 3, 128), (1, 128, 1, 64), (3, 1024, 5, 64)]:
+    torch.manual_seed(B * 1000 + T + H + hd)
+    qkv = (torch.randn(B * T, 3 * H * hd, device="cuda") * 0.8).bfloat16()
+    o = torch.empty(B * T, H * hd, dtype=torch.bfloat16, device="cuda")
+    lse = torch.empty(B * H * T, device="cuda")
+    check(lib().ckf_attention_fwd(qkv.data_ptr(), B, T, H, hd, o.data_ptr(), lse.data_ptr(), 2, None))
+    torch.cuda.synchronize()
+    outs.append((o.cpu(), lse.cpu()))
+torch.save(outs, sys.argv[2])
+"""
+
+
+def test_forward_persistent_ctas_bit_identical_to_one_cta_per_unit(tmp_path):
+    """The persistent forward (CTAs drawing units from a counter that the last CTA resets) against
+    one CTA per unit (CKF_ATTN_FWD_PERSIST=0, read once per process): a unit's arithmetic is the
+    same either way, so outputs and lse are bit-identical -- over a launch sequence with fewer
+    units than CTAs, more units than CTAs, both head dims, and repeated shapes (a counter left
+    non-zero by one launch would skip units of the next)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = []
+    for persist in ("1", "0"):
+        env = dict(os.environ)
+        env["CKF_ATTN_FWD_PERSIST"] = persist
+        path = str(tmp_path / f"fwd_{persist}.pt")
+        subprocess.run([sys.executable, "-c", _FWD_SCRIPT, root, path], env=env, check=True, timeout=600)
+        res.append(torch.load(path))
+    for (o1, l1), (o0, l0) in zip(*res):
+        assert torch.equal(o1, o0) and torch.equal(l1, l0)
+    assert torch.equal(res[0][0][0], res[0][3][0]) and torch.equal(res[0][1][0], res[0][4][0])
