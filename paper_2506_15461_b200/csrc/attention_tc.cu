@@ -1489,7 +1489,8 @@ int num_sms_attn() {
   return sms;
 }
 
-// the persistent forward's unit counter (zero between launches: the kernel resets it), per device
+// the persistent forward's unit counter (zero between launches: the kernel resets it), per device;
+// forwards on one device must not overlap (the engine issues all compute on its one stream)
 int* attn_fwd_counter() {
   static int* ctr[64] = {};
   int dev = 0;
