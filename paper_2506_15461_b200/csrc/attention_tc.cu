@@ -17,6 +17,7 @@
 // producer, 1 S / dP issuer, 2 allocator, 3 dV / dK issuer, 4..11 softmax.  MMA issuers run
 // warp-converged with elect.sync (sm100.cuh umma_*_w).
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <string>
 
@@ -1489,19 +1490,22 @@ int num_sms_attn() {
   return sms;
 }
 
-// the persistent forward's unit counter (zero between launches: the kernel resets it), per device;
-// forwards on one device must not overlap (the engine issues all compute on its one stream)
+// the persistent forward's unit counters (zero between launches: the kernel resets its own), per
+// device: a ring of 256 taken in turn, so forwards launched on different streams at once use
+// different counters
 int* attn_fwd_counter() {
+  constexpr int kRing = 256;
   static int* ctr[64] = {};
+  static std::atomic<unsigned> next[64];
   int dev = 0;
   CKF_CUDA(cudaGetDevice(&dev));
   if (dev < 0 || dev >= 64) raise(1, "attention: device index out of range");
   if (!ctr[dev]) {
-    CKF_CUDA(cudaMalloc(&ctr[dev], sizeof(int)));
-    CKF_CUDA(cudaMemset(ctr[dev], 0, sizeof(int)));
+    CKF_CUDA(cudaMalloc(&ctr[dev], kRing * sizeof(int)));
+    CKF_CUDA(cudaMemset(ctr[dev], 0, kRing * sizeof(int)));
     ++alloc_epoch();
   }
-  return ctr[dev];
+  return ctr[dev] + next[dev].fetch_add(1, std::memory_order_relaxed) % kRing;
 }
 
 template <int HD, int NG>
