@@ -146,6 +146,11 @@ constexpr int kBwdExp = CKF_ATTN_BWD_EXPERIMENT;
 #ifndef CKF_ATTN_BWD_ISSUERS
 #define CKF_ATTN_BWD_ISSUERS 2
 #endif
+// CKF_ATTN_P_ALIAS=1: two query tiles per CTA (hd 128) write P into the TMEM columns of the S it
+// came from (the P V MMA reads it there; the next S into that buffer is issued after that P V)
+#ifndef CKF_ATTN_P_ALIAS
+#define CKF_ATTN_P_ALIAS 1
+#endif
 #ifndef CKF_ATTN_P_TMEM
 #define CKF_ATTN_P_TMEM 1
 #endif
@@ -157,7 +162,9 @@ constexpr int kBwdSplitDefault = 1;  // 2 measured no faster (1084.7 vs 1087.8 u
 template <int HD, int NG>
 struct FwdCfg {
   static constexpr uint32_t kQ = TQ * HD * 2, kK = FK * HD * 2;
-  static constexpr int kKSt = HD == 64 ? 4 : 3, kVSt = HD == 64 ? 3 : (NG == 2 ? 3 : 2);
+  // P aliased onto S in TMEM (two query tiles): no P buffers in shared memory, two more K / V stages
+  static constexpr bool kPAlias = NG == 2 && CKF_ATTN_P_ALIAS;
+  static constexpr int kKSt = HD == 64 ? 4 : (kPAlias ? 5 : 3), kVSt = HD == 64 ? 3 : (NG == 2 ? (kPAlias ? 5 : 3) : 2);
   // NG = 1: 104 KiB vs 144 KiB of shared memory; two hd-128 CTAs per SM with 2 K / 1 V stages (112 KiB)
   // measured 1.7x slower (1697 -> 2887 us at [16, 4096, 16, 128]): the single V stage serialises
   static constexpr int kMinBlocks = HD == 64 && NG == 1 ? 2 : 1;
@@ -182,7 +189,7 @@ struct Smem {
   uint8_t q[NG][C::kQ];
   uint8_t k[C::kKSt][C::kK];
   uint8_t v[C::kVSt][C::kK];
-  uint8_t p[C::kPTmem ? 1 : NG][C::kPTmem ? 1 : 2][C::kPTmem ? 16 : kPTile];
+  uint8_t p[C::kPTmem || C::kPAlias ? 1 : NG][C::kPTmem || C::kPAlias ? 1 : 2][C::kPTmem || C::kPAlias ? 16 : kPTile];
   uint64_t q_full;
   uint64_t k_full[C::kKSt], k_empty[C::kKSt], v_full[C::kVSt], v_empty[C::kVSt];
   uint64_t s_full[NG][2], s_free[NG][2], p_full[NG][2], p_free[NG][2];
@@ -333,7 +340,7 @@ __global__ void __launch_bounds__(FwdCfg<HD, NG>::kThreads, FwdCfg<HD, NG>::kMin
       auto issue_s = [&](int j) {
         const int ks = (jj0 + j) % KS, sb = (tg + j) & 1;
         mbar_wait(&sm.k_full[ks], ((jj0 + j) / KS) & 1);
-        mbar_wait(&sm.s_free[g][sb], (((tg + j) >> 1) & 1) ^ 1);
+        if constexpr (!C::kPAlias) mbar_wait(&sm.s_free[g][sb], (((tg + j) >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t ka = smem_u32(sm.k[ks]);
 #pragma unroll
@@ -349,12 +356,14 @@ __global__ void __launch_bounds__(FwdCfg<HD, NG>::kThreads, FwdCfg<HD, NG>::kMin
       // ahead of P_j V_j, so the next S is ready when the softmax finishes a tile instead of
       // queueing behind P V.  With two V stages S_{j+2} would wait for K_{j+2}, which the producer
       // loads only after P_{j-1} V_{j-1} freed a V stage -- there S_{j+1} is issued one tile ahead.
-      constexpr bool kEarly = C::kEarly;
+      // P aliased onto S: S_{j+2} reuses S_j's columns, which hold P_j until P_j V_j has read them,
+      // so it is issued right after that P V (tcgen05 MMAs of one CTA run in issue order)
+      constexpr bool kEarly = C::kEarly && !C::kPAlias;
       issue_s(0);
-      if (kEarly && nkb > 1) issue_s(1);
+      if ((kEarly || C::kPAlias) && nkb > 1) issue_s(1);
       for (int j = 0; j < nkb; ++j) {
         if (kEarly && j + 2 < nkb) issue_s(j + 2);
-        if (!kEarly && j + 1 < nkb) issue_s(j + 1);
+        if (!kEarly && !C::kPAlias && j + 1 < nkb) issue_s(j + 1);
         const int pb = (tg + j) & 1, vs = (jj0 + j) % VS;
         mbar_wait(&sm.v_full[vs], ((jj0 + j) / VS) & 1);
         mbar_wait(&sm.p_full[g][pb], ((tg + j) >> 1) & 1);
@@ -367,6 +376,11 @@ __global__ void __launch_bounds__(FwdCfg<HD, NG>::kThreads, FwdCfg<HD, NG>::kMin
           for (int k = 0; k < FK / 16; ++k)  // P from TMEM: 8 packed columns per 16 keys
             umma_bf16_ts_w(tmem + 128, tmem + 192 + pb * 32 + k * 8, umma_desc_sw128(va + k * 2048, FK * 128, 1024),
                            kIdO, (j > 0 || k > 0) ? 1u : 0u);  // k: the MMA's K step
+        } else if constexpr (C::kPAlias) {
+#pragma unroll
+          for (int k = 0; k < FK / 16; ++k)  // P in the first 32 columns of its S buffer
+            umma_bf16_ts_w(tmem + NG * 128 + g * HD, tmem + g * 128 + pb * FK + k * 8,
+                           umma_desc_sw128(va + k * 2048, FK * 128, 1024), kIdO, (j > 0 || k > 0) ? 1u : 0u);
         } else {
           const uint32_t pa = smem_u32(sm.p[g][pb]);
 #pragma unroll
@@ -376,6 +390,7 @@ __global__ void __launch_bounds__(FwdCfg<HD, NG>::kThreads, FwdCfg<HD, NG>::kMin
         }
         umma_commit_w(&sm.p_free[g][pb]);
         umma_commit_w(&sm.v_empty[vs]);
+        if (C::kPAlias && j + 2 < nkb) issue_s(j + 2);
       }
       umma_commit_w(&sm.o_full[g]);
       // NG = 2: the second tile's two extra K / V tiles are released by group 0 too (once loaded,
@@ -423,12 +438,14 @@ __global__ void __launch_bounds__(FwdCfg<HD, NG>::kThreads, FwdCfg<HD, NG>::kMin
       tmem_ld32(tS + sb * FK, *reinterpret_cast<uint32_t(*)[32]>(&u[0]));
       tmem_ld32(tS + sb * FK + 32, *reinterpret_cast<uint32_t(*)[32]>(&u[32]));
       tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.s_free[g][sb]);
+      if constexpr (!C::kPAlias) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.s_free[g][sb]);
+      }
       const int kbase = j * FK;
       const int nvalid = min(FK, q - kbase + 1);  // keys <= q are visible (causal)
-      const uint32_t prow = C::kPTmem ? 0u : smem_u32(sm.p[g][pb]) + r * 128;
+      const uint32_t prow = C::kPTmem || C::kPAlias ? 0u : smem_u32(sm.p[g][pb]) + r * 128;
       // P = 2^(S scale - mc) -> bf16 -> swizzled smem (32 keys at a time); returns the row sum
       auto write_p = [&](float mc) -> float {
         const f32x2 sc2 = f2(scale_log2, scale_log2), nm2 = f2(-mc, -mc);
@@ -462,6 +479,8 @@ __global__ void __launch_bounds__(FwdCfg<HD, NG>::kThreads, FwdCfg<HD, NG>::kMin
           lt += la + lb;
           if constexpr (C::kPTmem) {
             tmem_st16(trow + 192 + pb * 32 + hf * 16, w);
+          } else if constexpr (C::kPAlias) {
+            tmem_st16(tS + sb * FK + hf * 16, w);  // over the S values this thread has loaded
           } else {
 #pragma unroll
             for (int pc = 0; pc < 4; ++pc)
@@ -522,7 +541,7 @@ __global__ void __launch_bounds__(FwdCfg<HD, NG>::kThreads, FwdCfg<HD, NG>::kMin
         lt = write_p(m);
       }
       l += lt;
-      if constexpr (C::kPTmem)
+      if constexpr (C::kPTmem || C::kPAlias)
         tmem_st_wait();  // P in TMEM before the MMA reads it
       else
         fence_proxy_async();
