@@ -20,6 +20,7 @@
 #include <atomic>
 #include <cstdlib>
 #include <string>
+#include <type_traits>
 
 #include "common.cuh"
 #include "llama_kernels.h"
@@ -447,7 +448,11 @@ __global__ void __launch_bounds__(FwdCfg<HD, NG>::kThreads, FwdCfg<HD, NG>::kMin
       const int nvalid = min(FK, q - kbase + 1);  // keys <= q are visible (causal)
       const uint32_t prow = C::kPTmem || C::kPAlias ? 0u : smem_u32(sm.p[g][pb]) + r * 128;
       // P = 2^(S scale - mc) -> bf16 -> swizzled smem (32 keys at a time); returns the row sum
-      auto write_p = [&](float mc) -> float {
+      // the causal mask only on the last two key tiles (j >= 2 qb: keys above some query of the
+      // tile), a warp-uniform branch between two copies of the loop, not selects on every tile
+      const bool diag = j >= nkb - 2;
+      auto write_p_t = [&](auto mask_tag, float mc) -> float {
+        constexpr bool kMask = decltype(mask_tag)::value;
         const f32x2 sc2 = f2(scale_log2, scale_log2), nm2 = f2(-mc, -mc);
         float lt = 0.f;
 #pragma unroll
@@ -467,7 +472,7 @@ __global__ void __launch_bounds__(FwdCfg<HD, NG>::kThreads, FwdCfg<HD, NG>::kMin
               p0 = ex2(x0);
               p1 = ex2(x1);
             }
-            if (nvalid < FK) {
+            if (kMask) {
               p0 = tt < nvalid ? p0 : 0.f;
               p1 = tt + 1 < nvalid ? p1 : 0.f;
             }
@@ -489,6 +494,9 @@ __global__ void __launch_bounds__(FwdCfg<HD, NG>::kThreads, FwdCfg<HD, NG>::kMin
           }
         }
         return lt;
+      };
+      auto write_p = [&](float mc) -> float {
+        return diag ? write_p_t(std::true_type{}, mc) : write_p_t(std::false_type{}, mc);
       };
       const long long t2 = (kDbg && dbg) ? clock64() : 0;
       mbar_wait(&sm.p_free[g][pb], ((jt >> 1) & 1) ^ 1);  // P V_{j-2} has read this P buffer
