@@ -485,6 +485,17 @@ def run_ours(args, w: dict):
     e2e_value = tok / (e2e_ms / 1e3)
     # dominant kernel class (by device time inside the timed region)
     dom = max(kstats, key=lambda c: kstats[c][0])
+
+    def class_rate(c, v):
+        # every class against its own roofline: the tensor classes in TFLOP/s against the sustained
+        # bf16 peak, the others in GB/s of algorithmic bytes against the measured copy bandwidth
+        cms, cn, cfl, cby = v
+        r = {"ms": cms, "launches": cn}
+        if cms > 0 and c in ("gemm", "attention") and cfl > 0:
+            r.update(tflops=cfl / (cms / 1e3) / 1e12, frac=cfl / (cms / 1e3) / 1e12 / peaks["bf16_tflops_sustained"])
+        elif cms > 0 and cby > 0:
+            r.update(gbs=cby / (cms / 1e3) / 1e9, frac=cby / (cms / 1e3) / 1e9 / peaks["hbm_gbs"])
+        return r
     kms, kn, kfl, kby = kstats[dom]
     if dom in ("gemm", "attention") and w["precision"] == "bf16":
         achieved = kfl / (kms / 1e3) / 1e12
@@ -514,7 +525,7 @@ def run_ours(args, w: dict):
                 peak_source=peak_src, launches=kn, share_of_step=kms / ms_prof,
                 timing="CUDA events around each launch on the engine stream, separate pass of the same steps",
                 per_launch={"ms": kms / max(kn, 1), "flops": kfl / max(kn, 1), "bytes": kby / max(kn, 1)},
-                classes={c: {"ms": v[0], "launches": v[1]} for c, v in kstats.items() if v[1]})
+                classes={c: class_rate(c, v) for c, v in kstats.items() if v[1]})
     step_tflops = flops_per_token(w) * tok / (ms / 1e3) / 1e12
 
     if rec is not None:
